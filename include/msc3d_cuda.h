@@ -1,0 +1,152 @@
+/*
+ * msc3d_cuda.h -- the C ABI of the B200 Morse-Smale-complex pipeline.
+ *
+ * This is the drop-in boundary under the reference library's public C++ API
+ * (/root/reference/proj/include/msc3d/*.hpp).  The reference has no FFI of its
+ * own; its "operator API" is those headers.  Our C++ layer
+ * (paper_2009_03707_b200/csrc/msc3d_api.cpp, header include/msc3d/msc3d_b200.hpp)
+ * keeps the reference's signatures and calls the functions below; Python (ctypes)
+ * calls them directly.  No C++ or torch types cross this boundary: plain
+ * pointers, sizes, int status codes.  No exceptions cross it either: the C++
+ * wrappers turn the status codes back into the reference's exception types
+ * (see msc3d_status_string).
+ *
+ * Conventions
+ *   - Lattice / cell ids / pair codes exactly as grid.hpp:8-23, gradient.hpp:29-41.
+ *   - Cell-id arrays are uint32 when the lattice has < 2^32 cells (the reference's
+ *     CellIndex, grid.hpp:33) and uint64 above that (configs 4-5; the reference
+ *     rejects those grids, grid.cpp:17-20).  msc3d_id_width() says which.
+ *   - Dense vertex / cube indices (parents, labels) are uint32 (requires
+ *     nx*ny*nz < 2^32).
+ *   - Every stage runs on the context's CUDA stream; results stay in device
+ *     memory owned by the context until downloaded.
+ *   - Results are identical for every run and every device count (the reference's
+ *     "any thread count" determinism, primitives.hpp:3-8).
+ */
+#ifndef MSC3D_CUDA_H
+#define MSC3D_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (the reference's exception types, msc3d_cli.cpp:157-166) ---- */
+#define MSC3D_OK 0
+#define MSC3D_ERR_INVALID 1  /* std::invalid_argument (bad dims, non-finite value, bad source) */
+#define MSC3D_ERR_OVERFLOW 2 /* std::overflow_error   (path count leaves 64 bits, path_matrix.cpp:44-48) */
+#define MSC3D_ERR_RUNTIME 3  /* std::runtime_error    (cycle guards saddle_graph.cpp:173, path_matrix.cpp:202) */
+#define MSC3D_ERR_CUDA 4     /* CUDA runtime failure / no device */
+#define MSC3D_ERR_NOMEM 5    /* device allocation failed */
+#define MSC3D_ERR_IO 6       /* IoError (volume.hpp:22-25) */
+#define MSC3D_ERR_STATE 7    /* a stage was called before its inputs exist */
+
+#define MSC3D_VALUE_F32 0
+#define MSC3D_VALUE_F64 1
+
+typedef struct msc3d_dims {
+    int64_t nx, ny, nz; /* vertices per axis, each >= 2 (grid.cpp:13-16) */
+} msc3d_dims;
+
+typedef struct msc3d_ctx msc3d_ctx;
+
+const char* msc3d_status_string(int status);
+/* 0 ok / MSC3D_ERR_INVALID for dims < 2; allow_wide = 0 also rejects > 2^32-1 cells
+ * exactly like GridDims::GridDims (grid.cpp:11-21). */
+int msc3d_check_dims(msc3d_dims d, int allow_wide);
+int msc3d_id_width(msc3d_dims d); /* 4 or 8 */
+uint64_t msc3d_total_cells(msc3d_dims d);
+
+/* ---- context ------------------------------------------------------------------------ */
+int msc3d_ctx_create(msc3d_ctx** out, int device);
+void msc3d_ctx_destroy(msc3d_ctx* ctx);
+/* cudaStream_t passed as void*; NULL = the context's own non-blocking stream. */
+int msc3d_ctx_set_stream(msc3d_ctx* ctx, void* stream);
+void* msc3d_ctx_stream(msc3d_ctx* ctx);
+int msc3d_ctx_sync(msc3d_ctx* ctx);
+/* Number of kernels this context launched since creation (bench evidence). */
+uint64_t msc3d_ctx_launches(msc3d_ctx* ctx);
+
+/* Named device arrays owned by the context ("codes", "crit1", "labels_min", ...).
+ * *elem_bytes is the element width; *count the number of elements. */
+int msc3d_ctx_array(msc3d_ctx* ctx, const char* name, void** device_ptr, uint64_t* count,
+                    int* elem_bytes);
+/* Copy a named array to host memory (capacity in bytes); synchronises the stream. */
+int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t capacity_bytes);
+/* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...). */
+int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, int64_t* value);
+
+/* ---- scalar-grid load: ScalarField / read_volume (grid.hpp:117-125, volume.hpp:42) -- */
+/* Upload samples (host pointer; f32 or f64 x-fastest) and validate them on device:
+ * non-finite -> MSC3D_ERR_INVALID (grid.cpp:86-88). */
+int msc3d_ctx_load_values(msc3d_ctx* ctx, msc3d_dims dims, int value_type, const void* host_values);
+/* Same from a device pointer (not copied; must outlive the context's use of it). */
+int msc3d_ctx_bind_values(msc3d_ctx* ctx, msc3d_dims dims, int value_type, const void* device_values);
+/* Raw volume file -> device f32/f64 (u8/u16 widen exactly to f32), volume.cpp:67-96.
+ * dtype "u8"|"u16"|"f32"|"f64". */
+int msc3d_ctx_read_volume(msc3d_ctx* ctx, const char* path, msc3d_dims dims, const char* dtype,
+                          int big_endian);
+
+/* ---- gradient: assign_gradient (gradient.hpp:66) -> array "codes" (u8, N) ------------ */
+int msc3d_ctx_gradient(msc3d_ctx* ctx);
+/* Install an existing GradientField (host codes) for the stage entry points below. */
+int msc3d_ctx_load_codes(msc3d_ctx* ctx, msc3d_dims dims, const uint8_t* host_codes);
+
+/* ---- critical cells: extract_critical_cells (gradient.hpp:80) -> "crit0".."crit3" --- */
+int msc3d_ctx_critical(msc3d_ctx* ctx);
+
+/* ---- manifold traversal (extrema.hpp:43-78) ------------------------------------------ */
+/* build_forest -> "parent0" (u32, V) or "parent3" (u32, Cu). */
+int msc3d_ctx_forest(msc3d_ctx* ctx, int dim);
+/* find_roots: synchronous pointer doubling, bit-exact labels and round count
+ * (extrema.cpp:79-101) -> "label0"/"label3", scalar "rounds0"/"rounds3". */
+int msc3d_ctx_roots(msc3d_ctx* ctx, int dim);
+/* Install a parent array (host) for find_roots on arbitrary forests. */
+int msc3d_ctx_load_parent(msc3d_ctx* ctx, int dim, const uint32_t* host_parent, uint64_t n);
+/* saddle_extremum_arcs (extrema.cpp:103-148) from "label0"/"label3"
+ * -> "se_saddle" (id), "se_extremum" (id), "se_mult" (u32), reference order. */
+int msc3d_ctx_se_arcs(msc3d_ctx* ctx);
+int msc3d_ctx_load_labels(msc3d_ctx* ctx, const uint32_t* host_label0, const uint32_t* host_label3);
+
+/* ---- saddle graph (saddle_graph.hpp:39-74) ------------------------------------------- */
+/* mark_reachable from the given 1-saddles (host ids, width msc3d_id_width); NULL/0 =
+ * all critical 1-cells.  -> "marked" (u8, N), "one_saddles", "two_saddles". */
+int msc3d_ctx_mark(msc3d_ctx* ctx, const void* host_sources, uint64_t n_sources);
+/* build_minor -> "junctions" + 4 typed edge lists "<kind>.src/.dst" (u32) ".mult" (u64),
+ * kind in s1_to_j, j_to_j, j_to_s2, s1_to_s2 (saddle_graph.cpp:121-217). */
+int msc3d_ctx_minor(msc3d_ctx* ctx);
+
+/* ---- path counting (path_matrix.hpp:40-64) ------------------------------------------- */
+/* count_paths on the device DAG (after msc3d_ctx_mark): 2-saddle-rooted backward
+ * wavefronts over the contracted V-path graph -> "ss_one", "ss_two" (ids), "ss_paths"
+ * (u64), sorted by (one, two).  MSC3D_ERR_OVERFLOW with the reference's semantics. */
+int msc3d_ctx_count(msc3d_ctx* ctx);
+/* count_paths on an explicit DagMinor (host arrays; edge lists in the order
+ * s1_to_j, j_to_j, j_to_s2, s1_to_s2) -> "ss_one", "ss_two", "ss_paths". */
+int msc3d_ctx_count_minor(msc3d_ctx* ctx, const void* one_saddles, uint64_t n1,
+                          const void* junctions, uint64_t nj, const void* two_saddles,
+                          uint64_t n2, const uint32_t* const* src, const uint32_t* const* dst,
+                          const uint64_t* const* mult, const uint64_t* count, int id_width);
+
+/* ---- MS graph: compute (msc.hpp:87) ----------------------------------------------------- */
+#define MSC3D_OPT_SEGMENTATION 1 /* ComputeOptions::with_segmentation */
+#define MSC3D_OPT_VALIDATE 2     /* ComputeOptions::validate (device audit) */
+/* Whole pipeline on the loaded values.  Device results:
+ *   "cp_cell" (id) "cp_index" (u8)      critical points sorted by (index, cell)
+ *   "arc_src" "arc_dst" (u32) "arc_mult" (u64)   sorted by (src, dst)
+ *   "labels_min" (u32, V) "labels_max" (u32, Cu)  when MSC3D_OPT_SEGMENTATION
+ * stage_ms[5] (nullable) receives device milliseconds of the reference's five
+ * StageTimings (gradient, critical, extrema, reachability, counting). */
+int msc3d_ctx_compute(msc3d_ctx* ctx, int options, double* stage_ms);
+
+/* FNV-1a 64 over the widened f64 samples (msc.cpp:31-42), host-side, of the values
+ * last loaded from host memory. */
+uint64_t msc3d_field_hash_f64(const double* values, uint64_t n);
+uint64_t msc3d_field_hash_f32(const float* values, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSC3D_CUDA_H */

@@ -1,0 +1,106 @@
+// Shared device-side vocabulary for the msc3d B200 pipeline.
+//
+// Lattice conventions follow proj/include/msc3d/grid.hpp:8-23 (doubled
+// coordinates, x-fastest ids, dimension = number of odd coordinates) and the
+// pair-code byte of proj/include/msc3d/gradient.hpp:29-41.  Cell ids are 64-bit
+// on the device; list outputs use IdT = uint32_t when the lattice has < 2^32
+// cells (the reference's CellIndex, grid.hpp:33) and uint64_t beyond that.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/msc3d_cuda.h"
+
+namespace msc3d_dev {
+
+constexpr std::uint8_t kUnset = 0;
+constexpr std::uint8_t kCritical = 1;
+constexpr std::uint8_t kFacetBase = 2;
+constexpr std::uint8_t kCofacetBase = 8;
+constexpr std::uint32_t kNoLabel = 0xffffffffu;
+
+struct Dims {
+    std::int64_t nx, ny, nz;   // vertices
+    std::int64_t ex, ey, ez;   // lattice extents 2n-1
+    std::int64_t exy;          // ex*ey
+    std::uint64_t n_cells, n_verts, n_cubes;
+
+    __host__ __device__ static Dims make(std::int64_t x, std::int64_t y, std::int64_t z) {
+        Dims d;
+        d.nx = x; d.ny = y; d.nz = z;
+        d.ex = 2 * x - 1; d.ey = 2 * y - 1; d.ez = 2 * z - 1;
+        d.exy = d.ex * d.ey;
+        d.n_cells = static_cast<std::uint64_t>(d.ex) * d.ey * d.ez;
+        d.n_verts = static_cast<std::uint64_t>(x) * y * z;
+        d.n_cubes = static_cast<std::uint64_t>(x - 1) * (y - 1) * (z - 1);
+        return d;
+    }
+};
+
+// Partner of a paired cell: one stride step along the encoded axis
+// (gradient.hpp:51-60).
+__host__ __device__ inline std::int64_t partner_of(const Dims& d, std::int64_t c, std::uint8_t k) {
+    const int dir = k - (k < kCofacetBase ? kFacetBase : kCofacetBase);
+    const int axis = dir >> 1;
+    const std::int64_t step = axis == 0 ? 1 : (axis == 1 ? d.ex : d.exy);
+    return (dir & 1) ? c + step : c - step;
+}
+
+__host__ __device__ inline bool paired_with_facet(std::uint8_t k) {
+    return k >= kFacetBase && k < kCofacetBase;
+}
+__host__ __device__ inline bool paired_with_cofacet(std::uint8_t k) { return k >= kCofacetBase; }
+
+struct Coord {
+    std::int64_t x, y, z;
+};
+
+__host__ __device__ inline Coord unpack(const Dims& d, std::uint64_t id) {
+    Coord c;
+    const std::uint64_t q = id / static_cast<std::uint64_t>(d.ex);
+    c.x = static_cast<std::int64_t>(id - q * d.ex);
+    c.z = static_cast<std::int64_t>(q / static_cast<std::uint64_t>(d.ey));
+    c.y = static_cast<std::int64_t>(q - static_cast<std::uint64_t>(c.z) * d.ey);
+    return c;
+}
+
+__host__ __device__ inline std::uint64_t pack(const Dims& d, std::int64_t x, std::int64_t y,
+                                              std::int64_t z) {
+    return static_cast<std::uint64_t>(x + d.ex * (y + d.ey * z));
+}
+
+__host__ __device__ inline int cell_dim(const Coord& c) {
+    return static_cast<int>((c.x & 1) + (c.y & 1) + (c.z & 1));
+}
+
+// Dense vertex / cube indices (proj/src/extrema.cpp:11-35).
+__host__ __device__ inline std::uint32_t vertex_dense(const Dims& d, const Coord& c) {
+    return static_cast<std::uint32_t>(c.x / 2 + d.nx * (c.y / 2 + d.ny * (c.z / 2)));
+}
+__host__ __device__ inline std::uint32_t cube_dense(const Dims& d, const Coord& c) {
+    return static_cast<std::uint32_t>(c.x / 2 + (d.nx - 1) * (c.y / 2 + (d.ny - 1) * (c.z / 2)));
+}
+__host__ __device__ inline std::uint64_t vertex_cell(const Dims& d, std::uint64_t i) {
+    const std::uint64_t x = i % d.nx, r = i / d.nx, y = r % d.ny, z = r / d.ny;
+    return pack(d, 2 * x, 2 * y, 2 * z);
+}
+__host__ __device__ inline std::uint64_t cube_cell(const Dims& d, std::uint64_t i) {
+    const std::uint64_t mx = d.nx - 1, my = d.ny - 1;
+    const std::uint64_t x = i % mx, r = i / mx, y = r % my, z = r / my;
+    return pack(d, 2 * x + 1, 2 * y + 1, 2 * z + 1);
+}
+
+}  // namespace msc3d_dev
+
+namespace msc3d_dev {
+// Kernel launches issued by this library (process-wide); bench.py reports it.
+std::uint64_t& launch_counter();
+inline void count_launch(std::uint64_t n = 1) { launch_counter() += n; }
+}  // namespace msc3d_dev
+
+#define MSC3D_CUDA_TRY(expr)                                              \
+    do {                                                                  \
+        cudaError_t _e = (expr);                                          \
+        if (_e != cudaSuccess) return MSC3D_ERR_CUDA;                     \
+    } while (0)

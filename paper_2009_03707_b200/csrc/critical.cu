@@ -1,0 +1,235 @@
+// Critical-cell extraction (extract_critical_cells, proj/src/gradient.cpp:285-297):
+// one pass over the N pair codes, four ascending id lists (one per dimension).
+//
+// Each thread reads 16 consecutive codes with one 16-byte load (vectorised,
+// coalesced), derives each cell's dimension from its lattice coordinates (one
+// 64-bit division per 16 cells, then incremental), and counts critical cells per
+// dimension.  Counts are packed 16 bits per dimension, block-scanned with warp
+// shuffles, and chained across tiles by decoupled look-back (scan.cuh); the ids
+// are then written in ascending order.  The same kernel family also serves every
+// other "cells of dimension d satisfying P, ascending" compaction of the
+// reference (stream_compact_indices, primitives.hpp:147-182) through the Pred
+// functor.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "scan.cuh"
+
+namespace msc3d_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = 16;
+constexpr int kTile = kThreads * kPerThread;
+
+// A predicate maps (cell id, code, dimension) to an output list (0..3) or -1.
+struct CritPred {
+    __device__ __forceinline__ int operator()(std::uint64_t, std::uint8_t code, int dm) const {
+        return code == kCritical ? dm : -1;
+    }
+};
+
+// Marked critical cells (mark_reachable's one_saddles / two_saddles compaction,
+// saddle_graph.cpp:71-85).
+struct MarkedCritPred {
+    const std::uint8_t* marked;
+    __device__ __forceinline__ int operator()(std::uint64_t i, std::uint8_t code, int dm) const {
+        return (code == kCritical && marked[i]) ? dm : -1;
+    }
+};
+
+// All critical saddles (dims 1 and 2) into ONE ascending list: the merged saddle
+// order of saddle_extremum_arcs (extrema.cpp:109-117).
+struct SaddlePred {
+    __device__ __forceinline__ int operator()(std::uint64_t, std::uint8_t code, int dm) const {
+        return (code == kCritical && (dm == 1 || dm == 2)) ? 0 : -1;
+    }
+};
+
+template <typename Pred, typename IdT>
+__global__ void __launch_bounds__(kThreads)
+k_compact_by_dim(const std::uint8_t* __restrict__ codes, Dims d, Pred pred, TileStatus st,
+                 IdT* out0, IdT* out1, IdT* out2, IdT* out3, std::uint64_t* totals) {
+    __shared__ std::uint64_t sm[40];
+    __shared__ std::uint32_t s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const std::uint32_t tile = s_tile;
+    const std::uint64_t first = static_cast<std::uint64_t>(tile) * kTile +
+                                static_cast<std::uint64_t>(threadIdx.x) * kPerThread;
+
+    std::uint8_t c[kPerThread];
+    if (first + kPerThread <= d.n_cells && (first & 15) == 0) {
+        const uint4 w = *reinterpret_cast<const uint4*>(codes + first);
+        const std::uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < kPerThread; ++k) c[k] = static_cast<std::uint8_t>(ws[k >> 2] >> (8 * (k & 3)));
+    } else {
+#pragma unroll
+        for (int k = 0; k < kPerThread; ++k)
+            c[k] = first + k < d.n_cells ? codes[first + k] : kUnset;
+    }
+
+    // Lattice coordinates of the first cell; dims of the following ones by
+    // incrementing x with carries.
+    Coord p = unpack(d, first < d.n_cells ? first : 0);
+    std::uint32_t dimbits = 0;  // 2 bits per cell: output list
+    std::uint32_t hit = 0;      // 1 bit per cell: predicate
+    std::uint64_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+        const int dm0 = static_cast<int>((p.x & 1) + (p.y & 1) + (p.z & 1));
+        const int dm = first + k < d.n_cells ? pred(first + k, c[k], dm0) : -1;
+        if (dm >= 0) {
+            dimbits |= static_cast<std::uint32_t>(dm) << (2 * k);
+            hit |= 1u << k;
+            packed += 1ull << (16 * dm);
+        }
+        if (++p.x == d.ex) {
+            p.x = 0;
+            if (++p.y == d.ey) {
+                p.y = 0;
+                ++p.z;
+            }
+        }
+    }
+
+    std::uint64_t block_total;
+    const std::uint64_t excl = block_excl_scan(packed, &block_total, sm);
+    std::uint64_t tot[4];
+    for (int k = 0; k < 4; ++k) tot[k] = unpack16(block_total, k);
+    tile_lookback4(st, tile, tot, sm + 34);
+
+    std::uint64_t at[4];
+    for (int k = 0; k < 4; ++k) at[k] = sm[34 + k] + unpack16(excl, k);
+    IdT* outs[4] = {out0, out1, out2, out3};
+    for (std::uint32_t m = hit; m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        const int dm = (dimbits >> (2 * k)) & 3;
+        if (outs[dm]) outs[dm][at[dm]] = static_cast<IdT>(first + k);
+        ++at[dm];
+    }
+    const std::uint32_t ntiles = static_cast<std::uint32_t>((d.n_cells + kTile - 1) / kTile);
+    if (tile == ntiles - 1 && threadIdx.x == 0 && totals) {
+        for (int k = 0; k < 4; ++k) totals[k] = sm[34 + k] + tot[k];
+    }
+}
+
+// Count-only pass: totals per dimension with block reduction + one atomic per block.
+template <typename Pred>
+__global__ void __launch_bounds__(kThreads)
+k_count_by_dim(const std::uint8_t* __restrict__ codes, Dims d, Pred pred,
+               unsigned long long* totals) {
+    __shared__ unsigned long long s[4];
+    if (threadIdx.x < 4) s[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long local[4] = {0, 0, 0, 0};
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kTile;
+    for (std::uint64_t tbase = static_cast<std::uint64_t>(blockIdx.x) * kTile; tbase < d.n_cells;
+         tbase += stride) {
+        const std::uint64_t first = tbase + static_cast<std::uint64_t>(threadIdx.x) * kPerThread;
+        if (first >= d.n_cells) continue;
+        Coord p = unpack(d, first);
+        for (int k = 0; k < kPerThread && first + k < d.n_cells; ++k) {
+            const std::uint8_t c = codes[first + k];
+            const int cat = pred(first + k, c, static_cast<int>((p.x & 1) + (p.y & 1) + (p.z & 1)));
+            if (cat >= 0) ++local[cat];
+            if (++p.x == d.ex) {
+                p.x = 0;
+                if (++p.y == d.ey) {
+                    p.y = 0;
+                    ++p.z;
+                }
+            }
+        }
+    }
+    for (int k = 0; k < 4; ++k) {
+        unsigned long long v = local[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s[k], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && s[threadIdx.x]) atomicAdd(&totals[threadIdx.x], s[threadIdx.x]);
+}
+
+template <typename Pred>
+int compact_impl(const std::uint8_t* codes, const Dims& d, Pred pred, Workspace& ws,
+                 void* const outs[4], int id_width, std::uint64_t* d_totals, cudaStream_t s) {
+    const std::uint64_t ntiles = (d.n_cells + kTile - 1) / kTile;
+    if (ntiles == 0) return MSC3D_OK;
+    if (ntiles > 0xffffffffull) return MSC3D_ERR_INVALID;
+    TileStatus st;
+    const std::size_t bytes = ntiles * (4 + 64) + 16;
+    char* buf = static_cast<char*>(ws.get(bytes));
+    if (!buf) return MSC3D_ERR_NOMEM;
+    st.agg = reinterpret_cast<std::uint64_t*>(buf);
+    st.incl = st.agg + 4 * ntiles;
+    st.flag = reinterpret_cast<std::uint32_t*>(st.incl + 4 * ntiles);
+    st.ticket = st.flag + ntiles;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(st.flag, 0, (ntiles + 1) * 4, s));
+    const dim3 grid(static_cast<unsigned>(ntiles));
+    if (id_width == 4)
+        k_compact_by_dim<Pred, std::uint32_t><<<grid, kThreads, 0, s>>>(
+            codes, d, pred, st, static_cast<std::uint32_t*>(outs[0]),
+            static_cast<std::uint32_t*>(outs[1]), static_cast<std::uint32_t*>(outs[2]),
+            static_cast<std::uint32_t*>(outs[3]), d_totals);
+    else
+        k_compact_by_dim<Pred, std::uint64_t><<<grid, kThreads, 0, s>>>(
+            codes, d, pred, st, static_cast<std::uint64_t*>(outs[0]),
+            static_cast<std::uint64_t*>(outs[1]), static_cast<std::uint64_t*>(outs[2]),
+            static_cast<std::uint64_t*>(outs[3]), d_totals);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+template <typename Pred>
+int count_impl(const std::uint8_t* codes, const Dims& d, Pred pred, std::uint64_t* d_totals,
+               cudaStream_t s, int num_sms) {
+    MSC3D_CUDA_TRY(cudaMemsetAsync(d_totals, 0, 32, s));
+    const std::uint64_t ntiles = (d.n_cells + kTile - 1) / kTile;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, 8ull * num_sms));
+    k_count_by_dim<Pred><<<grid, kThreads, 0, s>>>(codes, d, pred,
+                                                   reinterpret_cast<unsigned long long*>(d_totals));
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+}  // namespace
+
+int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
+                          cudaStream_t s, int num_sms) {
+    return count_impl(codes, d, CritPred{}, d_totals, s, num_sms);
+}
+
+int launch_critical_compact(const std::uint8_t* codes, const Dims& d, Workspace& ws,
+                            void* const outs[4], int id_width, std::uint64_t* d_totals,
+                            cudaStream_t s) {
+    return compact_impl(codes, d, CritPred{}, ws, outs, id_width, d_totals, s);
+}
+
+int launch_saddle_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
+                        cudaStream_t s, int num_sms) {
+    return count_impl(codes, d, SaddlePred{}, d_totals, s, num_sms);
+}
+
+int launch_saddle_compact(const std::uint8_t* codes, const Dims& d, Workspace& ws, void* out,
+                          int id_width, std::uint64_t* d_totals, cudaStream_t s) {
+    void* const outs[4] = {out, nullptr, nullptr, nullptr};
+    return compact_impl(codes, d, SaddlePred{}, ws, outs, id_width, d_totals, s);
+}
+
+int launch_marked_critical_count(const std::uint8_t* codes, const std::uint8_t* marked,
+                                 const Dims& d, std::uint64_t* d_totals, cudaStream_t s,
+                                 int num_sms) {
+    return count_impl(codes, d, MarkedCritPred{marked}, d_totals, s, num_sms);
+}
+
+int launch_marked_critical_compact(const std::uint8_t* codes, const std::uint8_t* marked,
+                                   const Dims& d, Workspace& ws, void* const outs[4],
+                                   int id_width, std::uint64_t* d_totals, cudaStream_t s) {
+    return compact_impl(codes, d, MarkedCritPred{marked}, ws, outs, id_width, d_totals, s);
+}
+
+}  // namespace msc3d_dev

@@ -1,0 +1,90 @@
+// The context behind msc3d_ctx: device, stream, named device arrays, scalars and
+// scratch.  Arrays keep their capacity across calls so a repeated pipeline run on
+// the same grid allocates nothing.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct DevArray {
+    void* ptr = nullptr;
+    std::uint64_t count = 0;
+    int elem = 1;
+    std::size_t cap = 0;
+};
+
+struct msc3d_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    msc3d_dev::Dims dims{};
+    bool have_dims = false;
+    int value_type = MSC3D_VALUE_F32;
+    const void* values = nullptr;  // device pointer (owned "values" array or bound)
+    std::map<std::string, DevArray> arrays;
+    std::map<std::string, std::int64_t> scalars;
+    msc3d_dev::Workspace ws, ws2;
+    std::uint64_t* d_small = nullptr;  // 64 u64 of device scratch for totals / flags
+    std::uint64_t* h_small = nullptr;  // pinned mirror
+    std::uint64_t launches_at_create = 0;
+
+    ~msc3d_ctx() {
+        for (auto& kv : arrays)
+            if (kv.second.ptr) cudaFree(kv.second.ptr);
+        if (d_small) cudaFree(d_small);
+        if (h_small) cudaFreeHost(h_small);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+
+    // Ensure array `name` holds `count` elements of `elem` bytes; contents undefined.
+    void* ensure(const std::string& name, std::uint64_t count, int elem) {
+        DevArray& a = arrays[name];
+        const std::size_t bytes = static_cast<std::size_t>(count) * elem;
+        if (a.cap < bytes || !a.ptr) {
+            if (a.ptr) cudaFree(a.ptr);
+            a.ptr = nullptr;
+            a.cap = 0;
+            const std::size_t want = bytes ? bytes : 16;
+            if (cudaMalloc(&a.ptr, want) != cudaSuccess) {
+                cudaGetLastError();
+                a.ptr = nullptr;
+                return nullptr;
+            }
+            a.cap = want;
+        }
+        a.count = count;
+        a.elem = elem;
+        return a.ptr;
+    }
+    DevArray* find(const std::string& name) {
+        auto it = arrays.find(name);
+        return it == arrays.end() ? nullptr : &it->second;
+    }
+    template <typename T>
+    T* ptr(const std::string& name) {
+        DevArray* a = find(name);
+        return a ? static_cast<T*>(a->ptr) : nullptr;
+    }
+    std::uint64_t count(const std::string& name) {
+        DevArray* a = find(name);
+        return a ? a->count : 0;
+    }
+    void drop(const std::string& name) {
+        auto it = arrays.find(name);
+        if (it != arrays.end()) it->second.count = 0;
+    }
+    int id_width() const { return dims.n_cells <= 0xffffffffull ? 4 : 8; }
+    // Copy the first n u64 of d_small to h_small and wait.
+    int fetch_small(int n) {
+        if (cudaMemcpyAsync(h_small, d_small, n * 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+            return MSC3D_ERR_CUDA;
+        if (cudaStreamSynchronize(stream) != cudaSuccess) return MSC3D_ERR_CUDA;
+        return MSC3D_OK;
+    }
+};

@@ -1,0 +1,282 @@
+// Extremum forests, root finding and saddle-extremum arcs
+// (proj/src/extrema.cpp:43-155), plus the id remaps the assembly needs
+// (proj/src/msc.cpp:110-145).
+//
+//  * k_forest0 / k_forest3: build_forest from pair codes (the compute() pipeline
+//    gets the same parents for free from the gradient kernel).
+//  * k_double: one synchronous pointer-doubling round next[i] = label[label[i]]
+//    (extrema.cpp:79-101) -- bit-exact labels AND round count for find_roots.
+//  * k_jump: asynchronous in-place pointer jumping (same fixpoint, fewer passes)
+//    for the compute() pipeline where the round count is not observable.
+//  * se kernels: per saddle, the roots of its two descending (1-saddle) or
+//    ascending (2-saddle) walks, merged into multiplicity-2 arcs when equal.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace msc3d_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
+    const std::uint64_t need = (n + kThreads - 1) / kThreads;
+    return static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(need, static_cast<std::uint64_t>(num_sms) * per_sm)));
+}
+
+#define GRID_STRIDE(i, n)                                                                       \
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; \
+         i < (n); i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+
+__global__ void k_forest0(const std::uint8_t* __restrict__ codes, Dims d,
+                          std::uint32_t* __restrict__ parent) {
+    GRID_STRIDE(i, d.n_verts) {
+        const std::uint64_t c = vertex_cell(d, i);
+        const std::uint8_t k = codes[c];
+        if (k == kCritical) {
+            parent[i] = static_cast<std::uint32_t>(i);
+            continue;
+        }
+        const std::int64_t e = partner_of(d, static_cast<std::int64_t>(c), k);
+        const std::int64_t other = 2 * e - static_cast<std::int64_t>(c);
+        parent[i] = vertex_dense(d, unpack(d, static_cast<std::uint64_t>(other)));
+    }
+}
+
+__global__ void k_forest3(const std::uint8_t* __restrict__ codes, Dims d,
+                          std::uint32_t* __restrict__ parent) {
+    GRID_STRIDE(i, d.n_cubes) {
+        const std::uint64_t c = cube_cell(d, i);
+        const std::uint8_t k = codes[c];
+        if (k == kCritical) {
+            parent[i] = static_cast<std::uint32_t>(i);
+            continue;
+        }
+        // The paired quad q = c -/+ step along the encoded axis; the cube across
+        // q is q -/+ step again, if inside the lattice (extrema.cpp:68-75).
+        const int dir = k - kFacetBase;
+        const int axis = dir >> 1;
+        const Coord cc = unpack(d, c);
+        const std::int64_t coord = axis == 0 ? cc.x : (axis == 1 ? cc.y : cc.z);
+        const std::int64_t ext = axis == 0 ? d.ex : (axis == 1 ? d.ey : d.ez);
+        const std::int64_t across = (dir & 1) ? coord + 2 : coord - 2;
+        if (across < 0 || across >= ext) {
+            parent[i] = static_cast<std::uint32_t>(i);
+            continue;
+        }
+        Coord o = cc;
+        if (axis == 0) o.x = across;
+        else if (axis == 1) o.y = across;
+        else o.z = across;
+        parent[i] = cube_dense(d, o);
+    }
+}
+
+__global__ void k_double(const std::uint32_t* __restrict__ in, std::uint32_t* __restrict__ out,
+                         std::uint64_t n, unsigned int* changed) {
+    bool any = false;
+    GRID_STRIDE(i, n) {
+        const std::uint32_t l = in[i];
+        const std::uint32_t nl = in[l];
+        out[i] = nl;
+        any |= nl != l;
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *changed = 1u;
+}
+
+__global__ void k_jump(std::uint32_t* __restrict__ p, std::uint64_t n, unsigned int* changed) {
+    bool any = false;
+    GRID_STRIDE(i, n) {
+        std::uint32_t l = p[i];
+        std::uint32_t nl = p[l];
+        if (nl != l) {
+            // Chase a few steps at once: every intermediate is an ancestor, so
+            // writing any of them keeps the forest valid.
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const std::uint32_t nn = p[nl];
+                if (nn == nl) break;
+                nl = nn;
+            }
+            p[i] = nl;
+            any = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *changed = 1u;
+}
+
+// remap[dense(crit[k])] = base + k
+template <typename IdT>
+__global__ void k_scatter_remap(const IdT* __restrict__ crit, std::uint64_t n, Dims d, int dim,
+                                std::uint32_t base, std::uint32_t* __restrict__ remap) {
+    GRID_STRIDE(k, n) {
+        const Coord c = unpack(d, crit[k]);
+        const std::uint32_t di = dim == 0 ? vertex_dense(d, c) : cube_dense(d, c);
+        remap[di] = base + static_cast<std::uint32_t>(k);
+    }
+}
+
+__global__ void k_gather(const std::uint32_t* __restrict__ label, const std::uint32_t* __restrict__ remap,
+                         std::uint64_t n, std::uint32_t* __restrict__ out) {
+    GRID_STRIDE(i, n) out[i] = remap[label[i]];
+}
+
+// API saddle_extremum_arcs: per merged saddle, the two endpoint slots as cells.
+template <typename IdT>
+__global__ void k_se_slots(const std::uint8_t* __restrict__ codes, Dims d,
+                           const IdT* __restrict__ saddles, std::uint64_t ns,
+                           const std::uint32_t* __restrict__ l0, const std::uint32_t* __restrict__ l3,
+                           std::uint64_t* __restrict__ slot, std::uint32_t* __restrict__ cnt) {
+    GRID_STRIDE(i, ns) {
+        const std::uint64_t s = saddles[i];
+        const Coord c = unpack(d, s);
+        std::uint64_t a = ~0ull, b = ~0ull;
+        if (cell_dim(c) == 1) {
+            // endpoints in cell_vertices order: lower coordinate first (grid.cpp:61-73)
+            const int axis = (c.x & 1) ? 0 : ((c.y & 1) ? 1 : 2);
+            Coord lo = c, hi = c;
+            if (axis == 0) { lo.x -= 1; hi.x += 1; }
+            else if (axis == 1) { lo.y -= 1; hi.y += 1; }
+            else { lo.z -= 1; hi.z += 1; }
+            a = vertex_cell(d, l0[vertex_dense(d, lo)]);
+            b = vertex_cell(d, l0[vertex_dense(d, hi)]);
+        } else {
+            // cofacets of the quad in cofacet order (-axis first), clipped
+            const int axis = !(c.x & 1) ? 0 : (!(c.y & 1) ? 1 : 2);
+            const std::int64_t coord = axis == 0 ? c.x : (axis == 1 ? c.y : c.z);
+            const std::int64_t ext = axis == 0 ? d.ex : (axis == 1 ? d.ey : d.ez);
+            std::uint64_t got[2];
+            int ng = 0;
+            for (int sgn = -1; sgn <= 1; sgn += 2) {
+                const std::int64_t nc = coord + sgn;
+                if (nc < 0 || nc >= ext) continue;
+                Coord o = c;
+                if (axis == 0) o.x = nc;
+                else if (axis == 1) o.y = nc;
+                else o.z = nc;
+                const std::uint64_t root = cube_cell(d, l3[cube_dense(d, o)]);
+                got[ng++] = codes[root] == kCritical ? root : ~0ull;
+            }
+            a = ng > 0 ? got[0] : ~0ull;
+            b = ng > 1 ? got[1] : ~0ull;
+        }
+        // extrema.cpp:138-146: equal -> one arc of multiplicity 2; else min, max.
+        std::uint64_t x = a < b ? a : b, y = a < b ? b : a;
+        std::uint32_t n = 0;
+        if (a != ~0ull && a == b) {
+            slot[2 * i] = a | (1ull << 63);
+            slot[2 * i + 1] = ~0ull;
+            n = 1;
+        } else {
+            slot[2 * i] = x;
+            slot[2 * i + 1] = y;
+            n = (x != ~0ull) + (y != ~0ull);
+        }
+        cnt[i] = n;
+    }
+}
+
+template <typename IdT>
+__global__ void k_se_write(const IdT* __restrict__ saddles, std::uint64_t ns,
+                           const std::uint64_t* __restrict__ slot, const std::uint64_t* __restrict__ off,
+                           IdT* __restrict__ out_s, IdT* __restrict__ out_e,
+                           std::uint32_t* __restrict__ out_m) {
+    GRID_STRIDE(i, ns) {
+        std::uint64_t at = off[i];
+        for (int k = 0; k < 2; ++k) {
+            const std::uint64_t v = slot[2 * i + k];
+            if (v == ~0ull) continue;
+            out_s[at] = saddles[i];
+            out_e[at] = static_cast<IdT>(v & ~(1ull << 63));
+            out_m[at] = (v >> 63) ? 2u : 1u;
+            ++at;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_forest(const std::uint8_t* codes, const Dims& d, int dim, std::uint32_t* parent,
+                  cudaStream_t s, int num_sms) {
+    if (dim == 0)
+        k_forest0<<<grid_for(d.n_verts, num_sms), kThreads, 0, s>>>(codes, d, parent);
+    else if (d.n_cubes)
+        k_forest3<<<grid_for(d.n_cubes, num_sms), kThreads, 0, s>>>(codes, d, parent);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64_t n,
+                        unsigned int* changed, cudaStream_t s, int num_sms) {
+    k_double<<<grid_for(n, num_sms), kThreads, 0, s>>>(in, out, n, changed);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, cudaStream_t s,
+                      int num_sms) {
+    k_jump<<<grid_for(n, num_sms), kThreads, 0, s>>>(p, n, changed);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
+                         std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_scatter_remap<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(crit), n, d, dim, base, remap);
+    else
+        k_scatter_remap<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(crit), n, d, dim, base, remap);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_gather(const std::uint32_t* label, const std::uint32_t* remap, std::uint64_t n,
+                  std::uint32_t* out, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    k_gather<<<grid_for(n, num_sms), kThreads, 0, s>>>(label, remap, n, out);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_se_slots(const std::uint8_t* codes, const Dims& d, const void* saddles,
+                    std::uint64_t ns, int id_width, const std::uint32_t* l0,
+                    const std::uint32_t* l3, std::uint64_t* slot, std::uint32_t* cnt,
+                    cudaStream_t s, int num_sms) {
+    if (ns == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_se_slots<std::uint32_t><<<grid_for(ns, num_sms), kThreads, 0, s>>>(
+            codes, d, static_cast<const std::uint32_t*>(saddles), ns, l0, l3, slot, cnt);
+    else
+        k_se_slots<std::uint64_t><<<grid_for(ns, num_sms), kThreads, 0, s>>>(
+            codes, d, static_cast<const std::uint64_t*>(saddles), ns, l0, l3, slot, cnt);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_se_write(const void* saddles, std::uint64_t ns, int id_width,
+                    const std::uint64_t* slot, const std::uint64_t* off, void* out_s, void* out_e,
+                    std::uint32_t* out_m, cudaStream_t s, int num_sms) {
+    if (ns == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_se_write<std::uint32_t><<<grid_for(ns, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(saddles), ns, slot, off,
+            static_cast<std::uint32_t*>(out_s), static_cast<std::uint32_t*>(out_e), out_m);
+    else
+        k_se_write<std::uint64_t><<<grid_for(ns, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(saddles), ns, slot, off,
+            static_cast<std::uint64_t*>(out_s), static_cast<std::uint64_t*>(out_e), out_m);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+}  // namespace msc3d_dev

@@ -1,0 +1,25 @@
+// Stage orchestration (host code driving the device kernels for one context).
+#pragma once
+
+#include <cstdint>
+
+#include "ctx.cuh"
+
+namespace msc3d_stage {
+
+int gradient(msc3d_ctx* ctx, bool with_forests);
+int critical(msc3d_ctx* ctx);
+int forest(msc3d_ctx* ctx, int dim);
+int roots_sync(msc3d_ctx* ctx, int dim);
+int roots_fast(msc3d_ctx* ctx, int dim);
+int se_arcs(msc3d_ctx* ctx);
+int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources);
+int minor(msc3d_ctx* ctx);
+int count(msc3d_ctx* ctx);
+int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* juncs,
+                std::uint64_t nj, const void* twos, std::uint64_t n2,
+                const std::uint32_t* const* src, const std::uint32_t* const* dst,
+                const std::uint64_t* const* mult, const std::uint64_t* count, int id_width);
+int compute(msc3d_ctx* ctx, int options, double* stage_ms);
+
+}  // namespace msc3d_stage
