@@ -1,2 +1,380 @@
-// assembly kernels
+// Device-side assembly of the MSComplex (proj/src/msc.cpp:89-145):
+//   * critical points = concatenation of the four ascending lists (id = position);
+//   * arcs min->1s, 1s->2s, 2s->max in critical-point ids, globally sorted by
+//     (src, dst).  The 1s->2s block comes out of counting already sorted; the
+//     2s->max block is generated per 2-saddle in order; only the min->1s block must
+//     be transposed (grouped by minimum): counting scatter by minimum, then a
+//     per-minimum sort of the (small) buckets.
+//   * id translation helpers (rank -> cell, rank -> cp id).
 #include "common.cuh"
+#include "kernels.cuh"
+
+namespace msc3d_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
+    const std::uint64_t need = (n + kThreads - 1) / kThreads;
+    return static_cast<unsigned>(std::max<std::uint64_t>(
+        1, std::min<std::uint64_t>(need, static_cast<std::uint64_t>(num_sms) * per_sm)));
+}
+
+#define GRID_STRIDE(i, n)                                                                       \
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; \
+         i < (n); i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+
+template <typename IdT>
+__global__ void k_gather_ids(const IdT* __restrict__ list, const std::uint32_t* __restrict__ idx,
+                             std::uint64_t n, IdT* __restrict__ out) {
+    GRID_STRIDE(i, n) out[i] = list[idx[i]];
+}
+
+__global__ void k_add_base(std::uint32_t* __restrict__ v, std::uint64_t n, std::uint32_t base) {
+    GRID_STRIDE(i, n) v[i] += base;
+}
+
+template <typename IdT>
+__global__ void k_cp_concat(const IdT* __restrict__ src, std::uint64_t n, std::uint64_t at,
+                            std::uint8_t index, IdT* __restrict__ cp_cell,
+                            std::uint8_t* __restrict__ cp_index) {
+    GRID_STRIDE(i, n) {
+        cp_cell[at + i] = src[i];
+        cp_index[at + i] = index;
+    }
+}
+
+// Per 1-saddle k (cp id base1 + k): its minima via the vertex labels.
+// Emits (min id, saddle id, mult) into two slots; counts per minimum.
+template <typename IdT>
+__global__ void k_arcs_min(const IdT* __restrict__ crit1, std::uint64_t n1, Dims d,
+                           const std::uint32_t* __restrict__ label0, const std::uint32_t* __restrict__ remap0,
+                           std::uint32_t base1, std::uint32_t* __restrict__ slot_min,
+                           std::uint32_t* __restrict__ per_min) {
+    GRID_STRIDE(k, n1) {
+        const Coord c = unpack(d, crit1[k]);
+        const int axis = (c.x & 1) ? 0 : ((c.y & 1) ? 1 : 2);
+        Coord lo = c, hi = c;
+        if (axis == 0) { lo.x -= 1; hi.x += 1; }
+        else if (axis == 1) { lo.y -= 1; hi.y += 1; }
+        else { lo.z -= 1; hi.z += 1; }
+        const std::uint32_t a = remap0[label0[vertex_dense(d, lo)]];
+        const std::uint32_t b = remap0[label0[vertex_dense(d, hi)]];
+        if (a == b) {
+            slot_min[2 * k] = a;
+            slot_min[2 * k + 1] = kNoLabel;
+            atomicAdd(&per_min[a], 1u);
+        } else {
+            slot_min[2 * k] = a < b ? a : b;
+            slot_min[2 * k + 1] = a < b ? b : a;
+            atomicAdd(&per_min[a], 1u);
+            atomicAdd(&per_min[b], 1u);
+        }
+        (void)base1;
+    }
+}
+
+// Scatter into minimum buckets: key = saddle id << 1 | (mult == 2).
+__global__ void k_arcs_min_scatter(const std::uint32_t* __restrict__ slot_min, std::uint64_t n1,
+                                   std::uint32_t base1, const std::uint64_t* __restrict__ off,
+                                   std::uint32_t* __restrict__ cursor, std::uint64_t* __restrict__ key) {
+    GRID_STRIDE(k, n1) {
+        const std::uint32_t a = slot_min[2 * k], b = slot_min[2 * k + 1];
+        const std::uint64_t sid = base1 + k;
+        if (b == kNoLabel) {
+            const std::uint32_t at = atomicAdd(&cursor[a], 1u);
+            key[off[a] + at] = (sid << 1) | 1ull;
+        } else {
+            std::uint32_t at = atomicAdd(&cursor[a], 1u);
+            key[off[a] + at] = sid << 1;
+            at = atomicAdd(&cursor[b], 1u);
+            key[off[b] + at] = sid << 1;
+        }
+    }
+}
+
+// Sort every bucket [off[m], off[m+1]) ascending.  Thread per bucket (insertion
+// sort) for small buckets; large buckets are left for k_sort_large_buckets.
+__global__ void k_sort_small_buckets(const std::uint64_t* __restrict__ off, std::uint64_t nb,
+                                     std::uint64_t total, std::uint64_t* __restrict__ key,
+                                     std::uint32_t* __restrict__ large, unsigned long long* n_large) {
+    GRID_STRIDE(m, nb) {
+        const std::uint64_t b = off[m], e = m + 1 < nb ? off[m + 1] : total;
+        const std::uint64_t n = e - b;
+        if (n <= 1) continue;
+        if (n > 64) {
+            large[atomicAdd(n_large, 1ull)] = static_cast<std::uint32_t>(m);
+            continue;
+        }
+        for (std::uint64_t i = b + 1; i < e; ++i) {
+            const std::uint64_t v = key[i];
+            std::uint64_t j = i;
+            while (j > b && key[j - 1] > v) {
+                key[j] = key[j - 1];
+                --j;
+            }
+            key[j] = v;
+        }
+    }
+}
+
+// One block per large bucket: bitonic sort in shared memory in chunks of 4096,
+// then (if the bucket is larger) repeated block-level merges through global
+// memory scratch.
+constexpr int kChunk = 4096;
+
+__device__ void block_bitonic(std::uint64_t* s, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const std::uint64_t a = s[i], b = s[ixj];
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void k_sort_large_buckets(const std::uint64_t* __restrict__ off, std::uint64_t nb,
+                                     std::uint64_t total, const std::uint32_t* __restrict__ large,
+                                     std::uint64_t* __restrict__ key, std::uint64_t* __restrict__ scratch) {
+    __shared__ std::uint64_t s[kChunk];
+    const std::uint32_t m = large[blockIdx.x];
+    const std::uint64_t b = off[m], e = m + 1 < nb ? off[m + 1] : total;
+    const std::uint64_t n = e - b;
+    // 1) sort chunks
+    for (std::uint64_t c0 = 0; c0 < n; c0 += kChunk) {
+        const int cn = static_cast<int>(n - c0 < static_cast<std::uint64_t>(kChunk) ? n - c0 : static_cast<std::uint64_t>(kChunk));
+        int p2 = 1;
+        while (p2 < cn) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < cn ? key[b + c0 + i] : ~0ull;
+        __syncthreads();
+        block_bitonic(s, p2);
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) key[b + c0 + i] = s[i];
+        __syncthreads();
+    }
+    // 2) merge runs pairwise (runs of width w), ping-pong through scratch[b..e)
+    std::uint64_t* src = key + b;
+    std::uint64_t* dst = scratch + b;
+    for (std::uint64_t w = kChunk; w < n; w <<= 1) {
+        for (std::uint64_t r = 0; r < n; r += 2 * w) {
+            const std::uint64_t lo = r, mid = min(r + w, n), hi = min(r + 2 * w, n);
+            // each thread computes output positions of a subset of elements by
+            // binary search in the other run (merge by rank; keys are unique)
+            for (std::uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const std::uint64_t v = src[i];
+                std::uint64_t rank;
+                if (i < mid) {
+                    std::uint64_t a = mid, z = hi;  // count of elements in right run < v
+                    while (a < z) {
+                        const std::uint64_t h = (a + z) >> 1;
+                        if (src[h] < v) a = h + 1;
+                        else z = h;
+                    }
+                    rank = (i - lo) + (a - mid);
+                } else {
+                    std::uint64_t a = lo, z = mid;  // elements in left run <= v
+                    while (a < z) {
+                        const std::uint64_t h = (a + z) >> 1;
+                        if (src[h] <= v) a = h + 1;
+                        else z = h;
+                    }
+                    rank = (i - mid) + (a - lo);
+                }
+                dst[lo + rank] = v;
+            }
+        }
+        __syncthreads();
+        std::uint64_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != key + b)
+        for (std::uint64_t i = threadIdx.x; i < n; i += blockDim.x) key[b + i] = src[i];
+}
+
+// Block A arcs out of sorted buckets: src = minimum id, dst = saddle id.
+__global__ void k_arcs_min_emit(const std::uint64_t* __restrict__ off, std::uint64_t nb,
+                                std::uint64_t total, const std::uint64_t* __restrict__ key,
+                                std::uint32_t* __restrict__ asrc, std::uint32_t* __restrict__ adst,
+                                std::uint64_t* __restrict__ amult) {
+    GRID_STRIDE(m, nb) {
+        const std::uint64_t b = off[m], e = m + 1 < nb ? off[m + 1] : total;
+        for (std::uint64_t i = b; i < e; ++i) {
+            asrc[i] = static_cast<std::uint32_t>(m);
+            adst[i] = static_cast<std::uint32_t>(key[i] >> 1);
+            amult[i] = (key[i] & 1) ? 2ull : 1ull;
+        }
+    }
+}
+
+// Block C: per 2-saddle k (cp id base2 + k), its maxima via the cube labels.
+template <typename IdT>
+__global__ void k_arcs_max(const IdT* __restrict__ crit2, std::uint64_t n2, Dims d,
+                           const std::uint32_t* __restrict__ label3, const std::uint32_t* __restrict__ remap3,
+                           std::uint32_t* __restrict__ slot, std::uint32_t* __restrict__ cnt) {
+    GRID_STRIDE(k, n2) {
+        const Coord c = unpack(d, crit2[k]);
+        const int axis = !(c.x & 1) ? 0 : (!(c.y & 1) ? 1 : 2);
+        const std::int64_t coord = axis == 0 ? c.x : (axis == 1 ? c.y : c.z);
+        const std::int64_t ext = axis == 0 ? d.ex : (axis == 1 ? d.ey : d.ez);
+        std::uint32_t got[2] = {kNoLabel, kNoLabel};
+        int ng = 0;
+        for (int sgn = -1; sgn <= 1; sgn += 2) {
+            const std::int64_t nc = coord + sgn;
+            if (nc < 0 || nc >= ext) continue;
+            Coord o = c;
+            if (axis == 0) o.x = nc;
+            else if (axis == 1) o.y = nc;
+            else o.z = nc;
+            got[ng++] = remap3[label3[cube_dense(d, o)]];
+        }
+        const std::uint32_t a = got[0], b = got[1];
+        std::uint32_t n = 0;
+        if (a != kNoLabel && a == b) {
+            slot[2 * k] = a | 0x80000000u;
+            slot[2 * k + 1] = kNoLabel;
+            n = 1;
+        } else {
+            const std::uint32_t x = a < b ? a : b, y = a < b ? b : a;
+            slot[2 * k] = x;
+            slot[2 * k + 1] = y;
+            n = (x != kNoLabel) + (y != kNoLabel);
+        }
+        cnt[k] = n;
+    }
+}
+
+__global__ void k_arcs_max_emit(const std::uint32_t* __restrict__ slot, std::uint64_t n2,
+                                std::uint32_t base2, const std::uint64_t* __restrict__ off,
+                                std::uint32_t* __restrict__ asrc, std::uint32_t* __restrict__ adst,
+                                std::uint64_t* __restrict__ amult) {
+    GRID_STRIDE(k, n2) {
+        std::uint64_t at = off[k];
+        for (int s = 0; s < 2; ++s) {
+            const std::uint32_t v = slot[2 * k + s];
+            if (v == kNoLabel) continue;
+            asrc[at] = base2 + static_cast<std::uint32_t>(k);
+            adst[at] = v & 0x7fffffffu;
+            amult[at] = (v & 0x80000000u) ? 2ull : 1ull;
+            ++at;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t n, int id_width,
+                      void* out, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_gather_ids<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(list), idx, n, static_cast<std::uint32_t*>(out));
+    else
+        k_gather_ids<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(list), idx, n, static_cast<std::uint64_t*>(out));
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaStream_t s,
+                    int num_sms) {
+    if (n == 0 || base == 0) return MSC3D_OK;
+    k_add_base<<<grid_for(n, num_sms), kThreads, 0, s>>>(v, n, base);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int index, int id_width,
+                     void* cp_cell, std::uint8_t* cp_index, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_cp_concat<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(src), n, at, static_cast<std::uint8_t>(index),
+            static_cast<std::uint32_t*>(cp_cell), cp_index);
+    else
+        k_cp_concat<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(src), n, at, static_cast<std::uint8_t>(index),
+            static_cast<std::uint64_t*>(cp_cell), cp_index);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_arcs_min(const void* crit1, std::uint64_t n1, int id_width, const Dims& d,
+                    const std::uint32_t* label0, const std::uint32_t* remap0, std::uint32_t base1,
+                    std::uint32_t* slot_min, std::uint32_t* per_min, cudaStream_t s, int num_sms) {
+    if (n1 == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_arcs_min<std::uint32_t><<<grid_for(n1, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(crit1), n1, d, label0, remap0, base1, slot_min, per_min);
+    else
+        k_arcs_min<std::uint64_t><<<grid_for(n1, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(crit1), n1, d, label0, remap0, base1, slot_min, per_min);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::uint32_t base1,
+                         const std::uint64_t* off, std::uint64_t n0, std::uint64_t total,
+                         std::uint32_t* cursor, std::uint64_t* key, std::uint64_t* scratch,
+                         std::uint32_t* large, unsigned long long* n_large,
+                         std::uint64_t* h_small, std::uint32_t* asrc, std::uint32_t* adst,
+                         std::uint64_t* amult, cudaStream_t s, int num_sms) {
+    if (n1 == 0) return MSC3D_OK;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, n0 * 4, s));
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_large, 0, 8, s));
+    k_arcs_min_scatter<<<grid_for(n1, num_sms), kThreads, 0, s>>>(slot_min, n1, base1, off, cursor, key);
+    k_sort_small_buckets<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, large, n_large);
+    count_launch(2);
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(h_small, n_large, 8, cudaMemcpyDeviceToHost, s));
+    MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
+    const std::uint64_t nl = h_small[0];
+    if (nl) {
+        k_sort_large_buckets<<<static_cast<unsigned>(nl), 512, 0, s>>>(off, n0, total, large, key, scratch);
+        count_launch();
+    }
+    k_arcs_min_emit<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, asrc, adst, amult);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
+                    const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
+                    std::uint32_t* cnt, cudaStream_t s, int num_sms) {
+    if (n2 == 0) return MSC3D_OK;
+    if (id_width == 4)
+        k_arcs_max<std::uint32_t><<<grid_for(n2, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint32_t*>(crit2), n2, d, label3, remap3, slot, cnt);
+    else
+        k_arcs_max<std::uint64_t><<<grid_for(n2, num_sms), kThreads, 0, s>>>(
+            static_cast<const std::uint64_t*>(crit2), n2, d, label3, remap3, slot, cnt);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint32_t base2,
+                         const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,
+                         std::uint64_t* amult, cudaStream_t s, int num_sms) {
+    if (n2 == 0) return MSC3D_OK;
+    k_arcs_max_emit<<<grid_for(n2, num_sms), kThreads, 0, s>>>(slot, n2, base2, off, asrc, adst, amult);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+}  // namespace msc3d_dev

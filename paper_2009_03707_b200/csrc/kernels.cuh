@@ -74,3 +74,71 @@ int launch_se_write(const void* saddles, std::uint64_t ns, int id_width,
                     const std::uint64_t* slot, const std::uint64_t* off, void* out_s, void* out_e,
                     std::uint32_t* out_m, cudaStream_t s, int num_sms);
 }  // namespace msc3d_dev
+
+namespace msc3d_dev {
+// saddle.cu
+int launch_mark_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
+                        int id_width, std::uint8_t* marked, std::uint32_t* nodes,
+                        std::uint32_t* nid, unsigned int* bad, cudaStream_t s, int num_sms);
+int launch_bfs_level(const std::uint8_t* codes, const Dims& d, std::uint8_t* marked,
+                     std::uint32_t* nodes, std::uint64_t begin, std::uint64_t end,
+                     unsigned long long* tail, std::uint32_t* nid, cudaStream_t s, int num_sms);
+int launch_scatter_quad_rank(const void* list, std::uint64_t n, int id_width, const Dims& d,
+                             std::uint32_t* tmap, cudaStream_t s, int num_sms);
+int launch_node_succ(const std::uint8_t* codes, const Dims& d, const std::uint32_t* nodes,
+                     std::uint64_t m, const std::uint32_t* nid, const std::uint32_t* tmap,
+                     std::uint32_t* succ, std::uint8_t* outdeg, cudaStream_t s, int num_sms);
+int launch_chain_ptr(const std::uint32_t* succ, const std::uint8_t* outdeg, std::uint64_t m,
+                     std::uint64_t n_src, std::uint32_t* ptr, cudaStream_t s, int num_sms);
+int launch_junction_flags(const std::uint8_t* outdeg, std::uint64_t m, std::uint64_t n_src,
+                          std::uint32_t* flag, cudaStream_t s, int num_sms);
+int launch_junction_write(const std::uint32_t* flag, const std::uint64_t* off, std::uint64_t m,
+                          std::uint32_t* jlist, std::uint32_t* jidx, cudaStream_t s, int num_sms);
+int launch_origin_dests(const std::uint32_t* jlist, std::uint64_t n, const std::uint32_t* succ,
+                        const std::uint8_t* outdeg, const std::uint32_t* stop,
+                        const std::uint32_t* jidx, std::uint32_t* dest, std::uint32_t* pending,
+                        std::uint32_t* indeg, cudaStream_t s, int num_sms);
+int launch_fill_rev(const std::uint32_t* dest, std::uint64_t nj, const std::uint64_t* roff,
+                    std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
+int launch_initial_frontier(const std::uint32_t* pending, std::uint64_t nj, std::uint32_t* frontier,
+                            unsigned long long* count, cudaStream_t s, int num_sms);
+int launch_kahn_level(const std::uint32_t* frontier, std::uint64_t nf, const std::uint32_t* dest,
+                      std::uint64_t* poff, std::uint32_t* plen, std::uint32_t* pkey,
+                      std::uint64_t* pcnt, unsigned long long* ptop, std::uint64_t pcap,
+                      const std::uint64_t* roff, const std::uint32_t* rcnt, const std::uint32_t* rsrc,
+                      std::uint32_t* pending, std::uint32_t* next, unsigned long long* next_count,
+                      unsigned int* flags, cudaStream_t s, int num_sms);
+int launch_source_len(const std::uint32_t* dest, std::uint64_t n1, const std::uint64_t* poff,
+                      const std::uint32_t* plen, const std::uint32_t* pkey, const std::uint64_t* pcnt,
+                      std::uint32_t* len, unsigned int* flags, cudaStream_t s, int num_sms);
+int launch_source_write(const std::uint32_t* dest, std::uint64_t n1, const std::uint64_t* poff,
+                        const std::uint32_t* plen, const std::uint32_t* pkey,
+                        const std::uint64_t* pcnt, const std::uint64_t* off, std::uint32_t* o_one,
+                        std::uint32_t* o_two, std::uint64_t* o_cnt, unsigned int* flags,
+                        cudaStream_t s, int num_sms);
+}  // namespace msc3d_dev
+
+namespace msc3d_dev {
+// assemble.cu
+int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t n, int id_width,
+                      void* out, cudaStream_t s, int num_sms);
+int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaStream_t s,
+                    int num_sms);
+int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int index, int id_width,
+                     void* cp_cell, std::uint8_t* cp_index, cudaStream_t s, int num_sms);
+int launch_arcs_min(const void* crit1, std::uint64_t n1, int id_width, const Dims& d,
+                    const std::uint32_t* label0, const std::uint32_t* remap0, std::uint32_t base1,
+                    std::uint32_t* slot_min, std::uint32_t* per_min, cudaStream_t s, int num_sms);
+int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::uint32_t base1,
+                         const std::uint64_t* off, std::uint64_t n0, std::uint64_t total,
+                         std::uint32_t* cursor, std::uint64_t* key, std::uint64_t* scratch,
+                         std::uint32_t* large, unsigned long long* n_large,
+                         std::uint64_t* h_small, std::uint32_t* asrc, std::uint32_t* adst,
+                         std::uint64_t* amult, cudaStream_t s, int num_sms);
+int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
+                    const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
+                    std::uint32_t* cnt, cudaStream_t s, int num_sms);
+int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint32_t base2,
+                         const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,
+                         std::uint64_t* amult, cudaStream_t s, int num_sms);
+}  // namespace msc3d_dev

@@ -140,14 +140,397 @@ int se_arcs(msc3d_ctx* ctx) {
     return msc3d_dev::launch_se_write(sad, ns, w, slot, off, os, oe, om, ctx->stream, ctx->num_sms);
 }
 
-int mark(msc3d_ctx*, const void*, std::uint64_t) { return MSC3D_ERR_STATE; }
+// ---------------------------------------------------------------------------------
+// mark_reachable (saddle_graph.cpp:26-86)
+// ---------------------------------------------------------------------------------
+namespace {
+
+template <typename T>
+std::vector<T> sorted_unique(const T* p, std::uint64_t n) {
+    std::vector<T> v(p, p + n);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    return v;
+}
+
+int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
+    const Dims& d = ctx->dims;
+    const auto* codes = ctx->ptr<std::uint8_t>("codes");
+    const int w = ctx->id_width();
+    auto* marked = static_cast<std::uint8_t*>(ctx->ensure("marked", d.n_cells, 1));
+    const std::uint64_t cap = 3 * d.n_verts;
+    auto* nodes = static_cast<std::uint32_t*>(ctx->ensure("nodes", cap, 4));
+    auto* nid = static_cast<std::uint32_t*>(ctx->ensure("nid", cap, 4));
+    if (!marked || !nodes || !nid) return MSC3D_ERR_NOMEM;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(marked, 0, d.n_cells, ctx->stream));
+    auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 20);
+    auto* tail = reinterpret_cast<unsigned long long*>(ctx->d_small + 21);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, ctx->stream));
+    ctx->h_small[21] = n_src;
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(tail, &ctx->h_small[21], 8, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(msc3d_dev::launch_mark_sources(codes, d, d_sources, n_src, w, marked, nodes, nid, bad,
+                                       ctx->stream, ctx->num_sms));
+    TRY(ctx->fetch_small(21));
+    if (ctx->h_small[20] & 0xffffffffu) return MSC3D_ERR_INVALID;
+    std::uint64_t begin = 0, end = n_src;
+    int levels = 0;
+    while (begin < end) {
+        TRY(msc3d_dev::launch_bfs_level(codes, d, marked, nodes, begin, end, tail, nid, ctx->stream,
+                                        ctx->num_sms));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(&ctx->h_small[21], tail, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        begin = end;
+        end = ctx->h_small[21];
+        ++levels;
+    }
+    ctx->arrays["nodes"].count = end;
+    ctx->scalars["bfs_levels"] = levels;
+    ctx->scalars["dag_nodes"] = static_cast<std::int64_t>(end);
+    ctx->scalars["dag_sources"] = static_cast<std::int64_t>(n_src);
+    return MSC3D_OK;
+}
+
+int marked_lists(msc3d_ctx* ctx) {
+    const Dims& d = ctx->dims;
+    const auto* codes = ctx->ptr<std::uint8_t>("codes");
+    const auto* marked = ctx->ptr<std::uint8_t>("marked");
+    const int w = ctx->id_width();
+    TRY(msc3d_dev::launch_marked_critical_count(codes, marked, d, ctx->d_small, ctx->stream, ctx->num_sms));
+    TRY(ctx->fetch_small(4));
+    const std::uint64_t n1 = ctx->h_small[1], n2 = ctx->h_small[2];
+    void* outs[4] = {nullptr, ctx->ensure("one_saddles", n1, w), ctx->ensure("two_saddles", n2, w),
+                     nullptr};
+    if (!outs[1] || !outs[2]) return MSC3D_ERR_NOMEM;
+    return msc3d_dev::launch_marked_critical_compact(codes, marked, d, ctx->ws, outs, w,
+                                                     ctx->d_small + 8, ctx->stream);
+}
+
+}  // namespace
+
+int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources) {
+    const int w = ctx->id_width();
+    const void* dsrc = nullptr;
+    std::uint64_t n = 0;
+    if (!host_sources) {
+        TRY(critical(ctx));  // the codes may have changed since the last extraction
+        dsrc = ctx->ptr<void>("crit1");
+        n = ctx->count("crit1");
+    } else {
+        // The reference skips duplicate sources (saddle_graph.cpp:37-41); node ids
+        // are assigned in ascending source order.
+        if (w == 4) {
+            auto v = sorted_unique(static_cast<const std::uint32_t*>(host_sources), n_sources);
+            n = v.size();
+            void* p = ctx->ensure("sources", n, 4);
+            if (!p) return MSC3D_ERR_NOMEM;
+            if (n) MSC3D_CUDA_TRY(cudaMemcpyAsync(p, v.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+            MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        } else {
+            auto v = sorted_unique(static_cast<const std::uint64_t*>(host_sources), n_sources);
+            n = v.size();
+            void* p = ctx->ensure("sources", n, 8);
+            if (!p) return MSC3D_ERR_NOMEM;
+            if (n) MSC3D_CUDA_TRY(cudaMemcpyAsync(p, v.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+            MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        }
+        dsrc = ctx->ptr<void>("sources");
+    }
+    TRY(bfs(ctx, dsrc, n));
+    return marked_lists(ctx);
+}
+
+// ---------------------------------------------------------------------------------
+// path counting over the device DAG
+// ---------------------------------------------------------------------------------
+namespace {
+
+// term_list: ascending 2-saddle cells whose positions key the count vectors.
+int dag_count(msc3d_ctx* ctx, const std::string& term_list) {
+    const Dims& d = ctx->dims;
+    const auto* codes = ctx->ptr<std::uint8_t>("codes");
+    const int w = ctx->id_width();
+    const cudaStream_t s = ctx->stream;
+    const int sms = ctx->num_sms;
+    const std::uint64_t m = ctx->count("nodes");
+    const std::uint64_t n1 = static_cast<std::uint64_t>(ctx->scalars["dag_sources"]);
+    const auto* nodes = ctx->ptr<std::uint32_t>("nodes");
+    const auto* nid = ctx->ptr<std::uint32_t>("nid");
+
+    auto* tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", 3 * d.n_verts, 4));
+    auto* succ = static_cast<std::uint32_t*>(ctx->ensure("succ", 4 * m, 4));
+    auto* outdeg = static_cast<std::uint8_t*>(ctx->ensure("outdeg", m, 1));
+    auto* stop = static_cast<std::uint32_t*>(ctx->ensure("stop", m, 4));
+    auto* jflag = static_cast<std::uint32_t*>(ctx->ensure("jflag", m, 4));
+    auto* joff = static_cast<std::uint64_t*>(ctx->ensure("joff", m, 8));
+    auto* jidx = static_cast<std::uint32_t*>(ctx->ensure("jidx", m, 4));
+    if (!tmap || !succ || !outdeg || !stop || !jflag || !joff || !jidx) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d,
+                                            tmap, s, sms));
+    TRY(msc3d_dev::launch_node_succ(codes, d, nodes, m, nid, tmap, succ, outdeg, s, sms));
+    TRY(msc3d_dev::launch_chain_ptr(succ, outdeg, m, n1, stop, s, sms));
+    // chain contraction: pointer jumping to the chain stop
+    auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 24);
+    int rounds = 0;
+    while (m) {
+        MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, s));
+        TRY(msc3d_dev::launch_jump_round(stop, m, changed, s, sms));
+        TRY(ctx->fetch_small(25));
+        ++rounds;
+        if (!(ctx->h_small[24] & 0xffffffffu)) break;
+        if (rounds > 64) return MSC3D_ERR_RUNTIME;
+    }
+    ctx->scalars["chain_rounds"] = rounds;
+    // junctions (node order)
+    TRY(msc3d_dev::launch_junction_flags(outdeg, m, n1, jflag, s, sms));
+    TRY(msc3d_dev::scan_u32(jflag, m, joff, ctx->d_small, ctx->ws, s));
+    TRY(ctx->fetch_small(1));
+    const std::uint64_t nj = m ? ctx->h_small[0] : 0;
+    ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
+    auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
+    auto* jdest = static_cast<std::uint32_t*>(ctx->ensure("jdest", 4 * nj, 4));
+    auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nj, 4));
+    auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nj, 4));
+    auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
+    auto* roff = static_cast<std::uint64_t*>(ctx->ensure("roff", nj, 8));
+    auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("cursor", nj, 4));
+    auto* sdest = static_cast<std::uint32_t*>(ctx->ensure("sdest", 4 * n1, 4));
+    auto* poff = static_cast<std::uint64_t*>(ctx->ensure("poff", nj, 8));
+    auto* plen = static_cast<std::uint32_t*>(ctx->ensure("plen", nj, 4));
+    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nj, 4));
+    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nj, 4));
+    if (!jlist || !jdest || !pending || !pending0 || !indeg || !roff || !cursor || !sdest || !poff ||
+        !plen || !fa || !fb)
+        return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_junction_write(jflag, joff, m, jlist, jidx, s, sms));
+    if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
+    TRY(msc3d_dev::launch_origin_dests(jlist, nj, succ, outdeg, stop, jidx, jdest, pending, indeg, s, sms));
+    TRY(msc3d_dev::launch_origin_dests(nullptr, n1, succ, outdeg, stop, jidx, sdest, nullptr, nullptr, s, sms));
+    TRY(msc3d_dev::scan_u32(indeg, nj, roff, ctx->d_small, ctx->ws, s));
+    TRY(ctx->fetch_small(1));
+    const std::uint64_t nrev = nj ? ctx->h_small[0] : 0;
+    auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", nrev, 4));
+    if (!rsrc) return MSC3D_ERR_NOMEM;
+    if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, nj * 4, s));
+    TRY(msc3d_dev::launch_fill_rev(jdest, nj, roff, cursor, rsrc, s, sms));
+    if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nj * 4, cudaMemcpyDeviceToDevice, s));
+
+    // Kahn over the junction graph, sinks first; grow the pool and rerun on overflow.
+    std::uint64_t pcap = std::max<std::uint64_t>(1u << 20, 2 * m);
+    auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 26);  // [0] overflow [1] pool
+    auto* ptop = reinterpret_cast<unsigned long long*>(ctx->d_small + 27);
+    auto* fcount = reinterpret_cast<unsigned long long*>(ctx->d_small + 28);
+    std::uint32_t* pkey = nullptr;
+    std::uint64_t* pcnt = nullptr;
+    int levels = 0;
+    for (int attempt = 0;; ++attempt) {
+        pkey = static_cast<std::uint32_t*>(ctx->ensure("pool_key", pcap, 4));
+        pcnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
+        if (!pkey || !pcnt) return MSC3D_ERR_NOMEM;
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 26, 0, 3 * 8, s));
+        if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nj * 4, cudaMemcpyDeviceToDevice, s));
+        TRY(msc3d_dev::launch_initial_frontier(pending, nj, fa, fcount, s, sms));
+        TRY(ctx->fetch_small(29));
+        std::uint64_t nf = ctx->h_small[28], done = 0;
+        std::uint32_t* cur = fa;
+        std::uint32_t* nxt = fb;
+        levels = 0;
+        while (nf) {
+            MSC3D_CUDA_TRY(cudaMemsetAsync(fcount, 0, 8, s));
+            TRY(msc3d_dev::launch_kahn_level(cur, nf, jdest, poff, plen, pkey, pcnt, ptop, pcap, roff,
+                                             indeg, rsrc, pending, nxt, fcount, flags, s, sms));
+            TRY(ctx->fetch_small(29));
+            done += nf;
+            nf = ctx->h_small[28];
+            std::swap(cur, nxt);
+            ++levels;
+        }
+        const unsigned int pool_full = static_cast<unsigned int>(ctx->h_small[26] >> 32);
+        if (pool_full) {
+            if (attempt > 8) return MSC3D_ERR_NOMEM;
+            pcap = std::max<std::uint64_t>(2 * pcap, ctx->h_small[27] + ctx->h_small[27] / 4);
+            continue;
+        }
+        if (done != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
+        break;
+    }
+    ctx->scalars["count_levels"] = levels;
+    ctx->scalars["pool_entries"] = static_cast<std::int64_t>(ctx->h_small[27]);
+
+    // 1-saddles: lengths, offsets, write
+    auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
+    auto* soff = static_cast<std::uint64_t*>(ctx->ensure("soff", n1, 8));
+    if (!slen || !soff) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_source_len(sdest, n1, poff, plen, pkey, pcnt, slen, flags, s, sms));
+    TRY(msc3d_dev::scan_u32(slen, n1, soff, ctx->d_small, ctx->ws, s));
+    TRY(ctx->fetch_small(27));
+    if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
+    const std::uint64_t nout = n1 ? ctx->h_small[0] : 0;
+    auto* o1 = static_cast<std::uint32_t*>(ctx->ensure("ss_one_rank", nout, 4));
+    auto* o2 = static_cast<std::uint32_t*>(ctx->ensure("ss_two_rank", nout, 4));
+    auto* oc = static_cast<std::uint64_t*>(ctx->ensure("ss_paths", nout, 8));
+    if (!o1 || !o2 || !oc) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_source_write(sdest, n1, poff, plen, pkey, pcnt, soff, o1, o2, oc, flags, s, sms));
+    return MSC3D_OK;
+}
+
+}  // namespace
+
+int count(msc3d_ctx* ctx) {
+    TRY(dag_count(ctx, "two_saddles"));
+    const int w = ctx->id_width();
+    const std::uint64_t n = ctx->count("ss_paths");
+    void* a = ctx->ensure("ss_one", n, w);
+    void* b = ctx->ensure("ss_two", n, w);
+    if (!a || !b) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_gather_ids(ctx->ptr<void>("one_saddles"), ctx->ptr<std::uint32_t>("ss_one_rank"),
+                                     n, w, a, ctx->stream, ctx->num_sms));
+    return msc3d_dev::launch_gather_ids(ctx->ptr<void>("two_saddles"), ctx->ptr<std::uint32_t>("ss_two_rank"),
+                                        n, w, b, ctx->stream, ctx->num_sms);
+}
+
 int minor(msc3d_ctx*) { return MSC3D_ERR_STATE; }
-int count(msc3d_ctx*) { return MSC3D_ERR_STATE; }
 int count_minor(msc3d_ctx*, const void*, std::uint64_t, const void*, std::uint64_t, const void*,
                 std::uint64_t, const std::uint32_t* const*, const std::uint32_t* const*,
                 const std::uint64_t* const*, const std::uint64_t*, int) {
     return MSC3D_ERR_STATE;
 }
-int compute(msc3d_ctx*, int, double*) { return MSC3D_ERR_STATE; }
+
+// ---------------------------------------------------------------------------------
+// compute() (msc.cpp:57-147)
+// ---------------------------------------------------------------------------------
+namespace {
+
+struct StageClock {
+    cudaEvent_t ev[6] = {};
+    bool ok = false;
+    explicit StageClock(bool on) {
+        if (!on) return;
+        ok = true;
+        for (auto& e : ev)
+            if (cudaEventCreate(&e) != cudaSuccess) ok = false;
+    }
+    ~StageClock() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    void mark(int i, cudaStream_t s) {
+        if (ok) cudaEventRecord(ev[i], s);
+    }
+};
+
+}  // namespace
+
+int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
+    const Dims& d = ctx->dims;
+    const int w = ctx->id_width();
+    const cudaStream_t s = ctx->stream;
+    const int sms = ctx->num_sms;
+    StageClock clk(stage_ms != nullptr);
+    clk.mark(0, s);
+
+    // [gradient] codes + both extremum forests in one kernel
+    TRY(gradient(ctx, /*with_forests=*/true));
+    clk.mark(1, s);
+
+    // [critical]
+    TRY(critical(ctx));
+    clk.mark(2, s);
+    const std::uint64_t c0 = ctx->scalars["c0"], c1 = ctx->scalars["c1"], c2 = ctx->scalars["c2"],
+                        c3 = ctx->scalars["c3"];
+    const std::uint64_t ncp = c0 + c1 + c2 + c3;
+    if (ncp >= 0xffffffffull) return MSC3D_ERR_INVALID;  // cp ids are u32 (msc.hpp:25)
+    const std::uint32_t base1 = static_cast<std::uint32_t>(c0), base2 = static_cast<std::uint32_t>(c0 + c1),
+                        base3 = static_cast<std::uint32_t>(c0 + c1 + c2);
+
+    // [extrema] roots by pointer jumping, saddle-extremum arcs, label remaps
+    TRY(roots_fast(ctx, 0));
+    TRY(roots_fast(ctx, 3));
+    auto* label0 = ctx->ptr<std::uint32_t>("parent0");
+    auto* label3 = ctx->ptr<std::uint32_t>("parent3");
+    auto* remap0 = static_cast<std::uint32_t*>(ctx->ensure("remap0", d.n_verts, 4));
+    auto* remap3 = static_cast<std::uint32_t*>(ctx->ensure("remap3", std::max<std::uint64_t>(1, d.n_cubes), 4));
+    if (!remap0 || !remap3) return MSC3D_ERR_NOMEM;
+    if (d.n_cubes) MSC3D_CUDA_TRY(cudaMemsetAsync(remap3, 0xff, d.n_cubes * 4, s));
+    TRY(msc3d_dev::launch_scatter_remap(ctx->ptr<void>("crit0"), c0, w, d, 0, 0, remap0, s, sms));
+    TRY(msc3d_dev::launch_scatter_remap(ctx->ptr<void>("crit3"), c3, w, d, 3, base3, remap3, s, sms));
+    // block A (min -> 1s) slots + per-minimum counts; block C (2s -> max) slots
+    auto* slot_min = static_cast<std::uint32_t*>(ctx->ensure("slot_min", 2 * c1, 4));
+    auto* per_min = static_cast<std::uint32_t*>(ctx->ensure("per_min", c0, 4));
+    auto* min_off = static_cast<std::uint64_t*>(ctx->ensure("min_off", c0, 8));
+    auto* slot_max = static_cast<std::uint32_t*>(ctx->ensure("slot_max", 2 * c2, 4));
+    auto* cnt_max = static_cast<std::uint32_t*>(ctx->ensure("cnt_max", c2, 4));
+    auto* off_max = static_cast<std::uint64_t*>(ctx->ensure("off_max", c2, 8));
+    if (!slot_min || !per_min || !min_off || !slot_max || !cnt_max || !off_max) return MSC3D_ERR_NOMEM;
+    if (c0) MSC3D_CUDA_TRY(cudaMemsetAsync(per_min, 0, c0 * 4, s));
+    TRY(msc3d_dev::launch_arcs_min(ctx->ptr<void>("crit1"), c1, w, d, label0, remap0, base1, slot_min,
+                                   per_min, s, sms));
+    TRY(msc3d_dev::launch_arcs_max(ctx->ptr<void>("crit2"), c2, w, d, label3, remap3, slot_max, cnt_max, s, sms));
+    TRY(msc3d_dev::scan_u32(per_min, c0, min_off, ctx->d_small + 32, ctx->ws, s));
+    TRY(msc3d_dev::scan_u32(cnt_max, c2, off_max, ctx->d_small + 33, ctx->ws2, s));
+    clk.mark(3, s);
+
+    // [reachability]
+    TRY(bfs(ctx, ctx->ptr<void>("crit1"), c1));
+    clk.mark(4, s);
+
+    // [counting]
+    TRY(dag_count(ctx, "crit2"));
+    clk.mark(5, s);
+
+    // ---- assembly (untimed in the reference's StageTimings) ----
+    TRY(ctx->fetch_small(34));
+    const std::uint64_t na = c0 ? ctx->h_small[32] : 0;  // min->1s arcs
+    const std::uint64_t nc = c2 ? ctx->h_small[33] : 0;  // 2s->max arcs
+    const std::uint64_t nb = ctx->count("ss_paths");       // 1s->2s arcs
+    void* cp_cell = ctx->ensure("cp_cell", ncp, w);
+    auto* cp_index = static_cast<std::uint8_t*>(ctx->ensure("cp_index", ncp, 1));
+    auto* asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", na + nb + nc, 4));
+    auto* adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", na + nb + nc, 4));
+    auto* amul = static_cast<std::uint64_t*>(ctx->ensure("arc_mult", na + nb + nc, 8));
+    auto* key = static_cast<std::uint64_t*>(ctx->ensure("sort_key", na, 8));
+    auto* scratch = static_cast<std::uint64_t*>(ctx->ensure("sort_scratch", na, 8));
+    auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("sort_cursor", c0, 4));
+    auto* large = static_cast<std::uint32_t*>(ctx->ensure("sort_large", c0, 4));
+    if (!cp_cell || !cp_index || !asrc || !adst || !amul || !key || !scratch || !cursor || !large)
+        return MSC3D_ERR_NOMEM;
+    std::uint64_t at = 0;
+    for (int k = 0; k < 4; ++k) {
+        const std::string nm = "crit" + std::to_string(k);
+        const std::uint64_t n = ctx->count(nm);
+        TRY(msc3d_dev::launch_cp_concat(ctx->ptr<void>(nm), n, at, k, w, cp_cell, cp_index, s, sms));
+        at += n;
+    }
+    TRY(msc3d_dev::launch_arcs_min_sort(slot_min, c1, base1, min_off, c0, na, cursor, key, scratch, large,
+                                        reinterpret_cast<unsigned long long*>(ctx->d_small + 35),
+                                        ctx->h_small + 35, asrc, adst, amul, s, sms));
+    if (nb) {
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc + na, ctx->ptr<void>("ss_one_rank"), nb * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(adst + na, ctx->ptr<void>("ss_two_rank"), nb * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(amul + na, ctx->ptr<void>("ss_paths"), nb * 8, cudaMemcpyDeviceToDevice, s));
+        TRY(msc3d_dev::launch_add_base(asrc + na, nb, base1, s, sms));
+        TRY(msc3d_dev::launch_add_base(adst + na, nb, base2, s, sms));
+    }
+    TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, asrc + na + nb, adst + na + nb,
+                                        amul + na + nb, s, sms));
+    if (options & MSC3D_OPT_SEGMENTATION) {
+        auto* lmin = static_cast<std::uint32_t*>(ctx->ensure("labels_min", d.n_verts, 4));
+        auto* lmax = static_cast<std::uint32_t*>(ctx->ensure("labels_max", d.n_cubes, 4));
+        if (!lmin || (!lmax && d.n_cubes)) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_gather(label0, remap0, d.n_verts, lmin, s, sms));
+        TRY(msc3d_dev::launch_gather(label3, remap3, d.n_cubes, lmax, s, sms));
+    } else {
+        ctx->drop("labels_min");
+        ctx->drop("labels_max");
+    }
+    if (stage_ms) {
+        MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int i = 0; i < 5; ++i) {
+            float ms = 0;
+            if (clk.ok) cudaEventElapsedTime(&ms, clk.ev[i], clk.ev[i + 1]);
+            stage_ms[i] = ms;
+        }
+    }
+    return MSC3D_OK;
+}
 
 }  // namespace msc3d_stage

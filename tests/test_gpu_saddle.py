@@ -1,0 +1,175 @@
+"""GPU parity: saddle-graph reachability, path counting and the whole compute().
+
+Fixtures follow proj/tests/test_saddle_graph.cpp, test_path_matrix.cpp and
+test_msc.cpp; the checker is the unmodified reference library (oracle/_ref).
+"""
+import numpy as np
+import pytest
+
+import paper_2009_03707_b200 as m
+from tests.fields import quantized, ramp, random_field
+
+pytestmark = pytest.mark.gpu
+
+
+def _codes(ctx, ref, values, dims):
+    ctx.load_values(values, dims).gradient()
+    return ctx.get("codes")
+
+
+def _one_saddles(ref, codes, dims):
+    return ref.critical(codes, dims)[1]
+
+
+@pytest.mark.parametrize("dims,seed", [((8, 8, 8), 71), ((8, 8, 8), 72), ((8, 8, 8), 73),
+                                       ((6, 7, 5), 71), ((6, 7, 5), 72), ((6, 7, 5), 73)])
+def test_mark_reachable_equals_reference(ctx, ref, dims, seed):
+    codes = _codes(ctx, ref, random_field(ref, dims, seed), dims)
+    src = _one_saddles(ref, codes, dims)
+    ctx.mark(src)
+    want = ref.mark(codes, dims, src)
+    np.testing.assert_array_equal(ctx.get("marked"), want[0])
+    np.testing.assert_array_equal(ctx.get("one_saddles"), want[1])
+    np.testing.assert_array_equal(ctx.get("two_saddles"), want[2])
+
+
+@pytest.mark.parametrize("kind", ["gauss", "gnoise", "noise"])
+def test_mark_synth(ctx, ref, kind):
+    dims = (64, 64, 64)
+    codes = _codes(ctx, ref, m.synth(kind, dims), dims)
+    src = _one_saddles(ref, codes, dims)
+    ctx.mark(None)
+    want = ref.mark(codes, dims, src)
+    np.testing.assert_array_equal(ctx.get("marked"), want[0])
+    np.testing.assert_array_equal(ctx.get("two_saddles"), want[2])
+
+
+def test_mark_no_saddles(ctx, ref):
+    dims = (6, 4, 3)
+    _codes(ctx, ref, ramp(dims), dims)
+    ctx.mark(np.zeros(0, np.uint32))
+    assert ctx.get("marked").sum() == 0
+    assert ctx.get("one_saddles").size == 0 and ctx.get("two_saddles").size == 0
+
+
+def test_mark_rejects_non_saddles(ctx, ref):
+    dims = (2, 2, 2)
+    _codes(ctx, ref, ramp(dims), dims)
+    with pytest.raises(ValueError):
+        ctx.mark(np.array([0], np.uint32))  # a vertex
+    with pytest.raises(ValueError):
+        ctx.mark(np.array([1], np.uint32))  # a paired edge
+
+
+def _set_pair(codes, dims, lo, hi):
+    ex, ey = 2 * dims[0] - 1, 2 * dims[1] - 1
+    pack = lambda c: c[0] + ex * (c[1] + ey * c[2])
+    axis = 0 if lo[0] != hi[0] else (1 if lo[1] != hi[1] else 2)
+    sign = hi[axis] - lo[axis]
+    codes[pack(lo)] = m.COFACET_BASE + axis * 2 + (1 if sign > 0 else 0)
+    codes[pack(hi)] = m.FACET_BASE + axis * 2 + (1 if -sign > 0 else 0)
+    return pack
+
+
+def test_straight_vpath_fixture(ctx, ref):
+    """test_saddle_graph.cpp:35-52,145-171."""
+    dims = (2, 2, 2)
+    codes = np.full(27, m.CRITICAL, np.uint8)
+    pack = _set_pair(codes, dims, (1, 2, 0), (1, 1, 0))
+    _set_pair(codes, dims, (1, 0, 1), (1, 1, 1))
+    ctx.load_codes(codes, dims)
+    e0 = pack((1, 0, 0))
+    ctx.mark(np.array([e0], np.uint32))
+    want = {e0, pack((1, 1, 0)), pack((1, 2, 0)), pack((1, 2, 1))}
+    marked = ctx.get("marked")
+    assert set(np.flatnonzero(marked).tolist()) == want
+    ctx.count()
+    assert ctx.get("ss_one").tolist() == [e0]
+    assert ctx.get("ss_two").tolist() == [pack((1, 2, 1))]
+    assert ctx.get("ss_paths").tolist() == [1]
+
+
+def _count_vs_ref(ctx, ref, codes, dims):
+    src = _one_saddles(ref, codes, dims)
+    marked, ones, twos = ref.mark(codes, dims, src)
+    mn = ref.minor(codes, dims, marked, ones, twos)
+    want = ref.count_paths(mn)
+    ctx.load_codes(codes, dims).mark(src).count()
+    got = (ctx.get("ss_one"), ctx.get("ss_two"), ctx.get("ss_paths"))
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
+    return got
+
+
+@pytest.mark.parametrize("dims,seed", [((8, 8, 8), 91), ((8, 8, 8), 92), ((10, 9, 8), 93),
+                                       ((8, 8, 8), 81), ((10, 9, 8), 83), ((9, 8, 7), 94)])
+def test_count_paths_random(ctx, ref, dims, seed):
+    codes = _codes(ctx, ref, random_field(ref, dims, seed), dims)
+    got = _count_vs_ref(ctx, ref, codes, dims)
+    assert got[2].size > 0
+
+
+@pytest.mark.parametrize("kind", ["gauss", "gnoise", "noise"])
+def test_count_paths_synth(ctx, ref, kind):
+    dims = (48, 48, 48)
+    codes = _codes(ctx, ref, m.synth(kind, dims), dims)
+    _count_vs_ref(ctx, ref, codes, dims)
+
+
+def _compute_vs_ref(ctx, ref, values, dims, seg=True):
+    got = m.compute(values, dims, with_segmentation=seg, ctx=ctx)
+    want = ref.compute(np.asarray(values, dtype=np.float64), dims, with_segmentation=seg)
+    np.testing.assert_array_equal(got.cp_cell, want["cp_cell"])
+    np.testing.assert_array_equal(got.cp_index.astype(np.int32), want["cp_index"])
+    np.testing.assert_array_equal(got.arc_src, want["arc_src"])
+    np.testing.assert_array_equal(got.arc_dst, want["arc_dst"])
+    np.testing.assert_array_equal(got.arc_mult, want["arc_mult"])
+    assert got.input_hash == want["input_hash"]
+    if seg:
+        np.testing.assert_array_equal(got.labels_min, want["labels_min"])
+        np.testing.assert_array_equal(got.labels_max, want["labels_max"])
+    assert got.euler() == 1
+    return got
+
+
+@pytest.mark.parametrize("dims,seed", [((8, 8, 8), 101), ((8, 8, 8), 102), ((10, 9, 8), 103),
+                                       ((8, 8, 8), 105), ((8, 8, 8), 106), ((9, 8, 7), 107),
+                                       ((6, 6, 6), 108)])
+def test_compute_random(ctx, ref, dims, seed):
+    _compute_vs_ref(ctx, ref, random_field(ref, dims, seed), dims)
+
+
+def test_compute_ramp(ctx, ref):
+    dims = (4, 3, 3)
+    got = _compute_vs_ref(ctx, ref, ramp(dims), dims)
+    assert got.cp_cell.tolist() == [0] and got.arc_src.size == 0
+    assert (got.labels_max == m.NO_LABEL).all()
+
+
+def test_compute_tie_heavy(ctx, ref):
+    for seed in range(3):
+        _compute_vs_ref(ctx, ref, quantized((11, 9, 7), 3, seed), (11, 9, 7))
+
+
+@pytest.mark.parametrize("kind", ["gauss", "gnoise", "noise"])
+def test_compute_synth_64(ctx, ref, kind):
+    dims = (64, 64, 64)
+    got = _compute_vs_ref(ctx, ref, m.synth(kind, dims), dims)
+    if kind == "gauss":
+        assert [got.count_by_index(k) for k in range(4)] == [134, 461, 356, 28]
+        assert got.arc_src.size == 2768 and int(got.arc_mult.max()) == 4
+
+
+def test_compute_without_segmentation(ctx, ref):
+    dims = (8, 8, 8)
+    _compute_vs_ref(ctx, ref, random_field(ref, dims, 7), dims, seg=False)
+
+
+def test_compute_repeatable(ctx, ref):
+    dims = (40, 30, 20)
+    v = m.synth("gnoise", dims)
+    a = m.compute(v, dims, ctx=ctx)
+    b = m.compute(v, dims, ctx=ctx)
+    for x, y in ((a.arc_src, b.arc_src), (a.arc_dst, b.arc_dst), (a.arc_mult, b.arc_mult),
+                 (a.labels_min, b.labels_min)):
+        np.testing.assert_array_equal(x, y)
