@@ -1,0 +1,311 @@
+"""bench.py -- MS complex throughput on B200 (BASELINE.json metric).
+
+metric : end-to-end MS complex Mcells/s (N = (2nx-1)(2ny-1)(2nz-1) lattice cells per
+         second) with per-stage ms vs the HBM roofline.
+workload (N=1): BASELINE config 3 -- 512^3 float32 Gaussians + white noise, the
+         north-star grid (dense critical points; saddle-saddle wavefront bottleneck).
+step   : one full compute() (gradient, critical cells, extrema, reachability, path
+         counting, device assembly incl. label volumes) over the resident grid.
+value  : device-resident input, CUDA events on the pipeline stream, max over ranks.
+e2e    : the same step through the public C ABI with HOST buffers: pinned input ->
+         msc3d_ctx_load_values (H2D + validation) -> compute -> D2H of critical points,
+         arcs and both label volumes.
+--impl reference : the unmodified reference library (oracle/_ref, compiled from
+         /root/reference) on the host cores, bounded sample of the same workload.
+Multi-GPU: one process per GPU, each computing its own replica (weak scaling, no
+data-path collective).
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "end-to-end MS complex Mcells/s and per-stage ms vs HBM roofline, 1/2/4/8 B200"
+WORKLOAD = {"name": "config3_512cube_gnoise_f32", "dims": (512, 512, 512), "kind": "gnoise", "seed": 1}
+CPU_SAMPLE = {"dims": (128, 128, 128), "kind": "gnoise", "seed": 1}
+STAGES = ("gradient", "critical", "extrema", "reachability", "counting")
+
+
+def cells(d):
+    return (2 * d[0] - 1) * (2 * d[1] - 1) * (2 * d[2] - 1)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl != "reference" else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device=None):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_run(sample, threads):
+    """The unmodified reference compute() on the host; returns (seconds, timings, kind)."""
+    import paper_2009_03707_b200 as m
+    from oracle.pyoracle import REF_SO, Oracle64, Ref
+    v = m.synth(sample["kind"], sample["dims"], sample["seed"]).astype(np.float64)
+    if os.path.exists(REF_SO):
+        r = Ref()
+        out = r.compute(v, sample["dims"], threads=threads, with_segmentation=True)
+        return out["wall"] - 0.0, list(out["timings"]), "reference", threads
+    o = Oracle64()
+    out = o.compute(v, sample["dims"])
+    return out["wall"], None, "port", 1
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    d = CPU_SAMPLE["dims"]
+    times = []
+    kind = "reference"
+    used = threads
+    for i in range(args.warmup + args.steps):
+        secs, _, kind, used = cpu_reference_run(CPU_SAMPLE, threads)
+        if i >= args.warmup:
+            times.append(secs)
+    t = sum(times) / len(times)
+    val = cells(d) / t / 1e6
+    sample = f"{d[0]}x{d[1]}x{d[2]} {CPU_SAMPLE['kind']} f32 (bounded sample of {WORKLOAD['name']}), full compute() with segmentation"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Mcells/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64-compare (f32 samples widened)",
+        "data": "synthetic", "config": {"workload": WORKLOAD["name"], "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "Mcells/s", "cores": used, "kind": kind, "sample": sample},
+        "e2e": {"value": val, "unit": "Mcells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--size", type=int, default=0, help="dev only: cube size override")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import torch
+
+    import paper_2009_03707_b200 as m
+
+    torch.cuda.set_device(local)
+    dims = WORKLOAD["dims"] if not args.size else (args.size,) * 3
+    ncells = cells(dims)
+    v = m.synth(WORKLOAD["kind"], dims, WORKLOAD["seed"])
+    dev_in = torch.from_numpy(v).to(f"cuda:{local}")
+    ctx = m.Context(local)
+    stream = torch.cuda.Stream(device=local)
+    ctx._L.msc3d_ctx_set_stream(ctx.h, C.c_void_p(stream.cuda_stream))
+    torch.cuda.synchronize()
+    ctx.bind_values(dev_in.data_ptr(), dims, m.VALUE_F32)
+
+    for _ in range(args.warmup):
+        ctx.compute(m.OPT_SEGMENTATION)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident input (inputs > L2: 512 MiB f32 + 1 GiB codes)
+    stage_acc = np.zeros(5)
+    l0 = ctx.launches()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ms = ctx.compute(m.OPT_SEGMENTATION)
+            stage_acc += np.array(ms)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = (ctx.launches() - l0) // args.steps
+    ms_step = ev0.elapsed_time(ev1) / args.steps
+    ms_step = max_over_ranks(ms_step, world, f"cuda:{local}")
+    value = world * ncells / (ms_step / 1e3) / 1e6
+    stage_ms = (stage_acc / args.steps).tolist()
+
+    # counts for the algorithmic-byte model
+    c = [ctx.scalar(f"c{k}") for k in range(4)]
+    a_min, a_ss, a_max = ctx.scalar("arcs_min"), ctx.scalar("arcs_ss"), ctx.scalar("arcs_max")
+    V = dims[0] * dims[1] * dims[2]
+    Cu = (dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1)
+    idb = 4 if ncells <= 0xFFFFFFFF else 8
+    alg = {
+        "gradient": 4 * V + ncells,
+        "critical": ncells + idb * sum(c),
+        "extrema": 5 * (V + Cu) + (12 if idb == 4 else 20) * (a_min + a_max),
+        "reachability": ncells + ncells // 8,
+        "counting": ncells + (16 if idb == 4 else 24) * a_ss,
+    }
+    peak, peak_kind = peaks()
+    stages = {}
+    for name, t in zip(STAGES, stage_ms):
+        gbs = alg[name] / (t / 1e3) / 1e9 if t > 0 else 0.0
+        stages[name] = {"ms": t, "alg_bytes": alg[name], "achieved_gbs": gbs, "frac": gbs / peak}
+    dom = max(STAGES, key=lambda s: stages[s]["ms"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "stage": dom, "achieved": stages[dom]["achieved_gbs"], "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
+                "traffic": traffic, "alg_bytes_per_launch": alg[dom]}
+
+    # ---- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.from_numpy(v).pin_memory()
+        outs = {}
+        e2e_times = []
+        h2d = V * 4
+        d2h = 0
+        for i in range(2 + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx._L.msc3d_ctx_load_values(ctx.h, m.Dims(*dims), m.VALUE_F32, C.c_void_p(host_in.data_ptr()))
+            ctx.compute(m.OPT_SEGMENTATION)
+            d2h = 0
+            for name in ("cp_cell", "cp_index", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+                _, n, e = ctx.array_info(name)
+                buf = outs.get(name)
+                if buf is None or buf.numel() < n * e:
+                    buf = torch.empty(max(1, int(n * e * 1.1)), dtype=torch.uint8).pin_memory()
+                    outs[name] = buf
+                ctx._L.msc3d_ctx_download(ctx.h, name.encode(), C.c_void_p(buf.data_ptr()), C.c_uint64(buf.numel()))
+                d2h += n * e
+            t1 = time.perf_counter()
+            if i >= 2:
+                e2e_times.append(t1 - t0)
+        te = max_over_ranks(sum(e2e_times) / len(e2e_times), world, f"cuda:{local}")
+        e2e = {"value": world * ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        secs, tim, kind, used = cpu_reference_run(CPU_SAMPLE, threads)
+        d = CPU_SAMPLE["dims"]
+        cpu = {"value": cells(d) / secs / 1e6, "unit": "Mcells/s", "cores": used, "kind": kind,
+               "sample": f"{d[0]}^3 {CPU_SAMPLE['kind']} f32, one full compute() with segmentation, "
+                         f"threads={used}", "seconds": secs, "stage_s": tim}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mcells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD["name"], "dims": list(dims), "field": WORKLOAD["kind"],
+                       "seed": WORKLOAD["seed"], "lattice_cells": ncells,
+                       "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (512 MiB f32 in, 1 GiB codes)"},
+            "stages_ms": dict(zip(STAGES, stage_ms)), "stages": stages, "roofline": roofline,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "counts": {"critical": c, "arcs_min": a_min, "arcs_ss": a_ss, "arcs_max": a_max},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

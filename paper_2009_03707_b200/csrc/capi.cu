@@ -267,6 +267,7 @@ int msc3d_ctx_load_codes(msc3d_ctx* ctx, msc3d_dims dims, const std::uint8_t* ho
     if (!p) return MSC3D_ERR_NOMEM;
     MSC3D_CUDA_TRY(cudaMemcpyAsync(p, host_codes, ctx->dims.n_cells, cudaMemcpyHostToDevice,
                                    ctx->stream));
+    ctx->crit_counts_valid = false;
     return MSC3D_OK;
 }
 

@@ -20,11 +20,33 @@ constexpr std::uint8_t kFacetBase = 2;
 constexpr std::uint8_t kCofacetBase = 8;
 constexpr std::uint32_t kNoLabel = 0xffffffffu;
 
+// Division by a grid-invariant divisor with one 64x64->128 high multiply:
+// q = umulhi(n, ceil(2^64 / d)), exact whenever n * d < 2^64 (ids < 2^36, d < 2^26
+// here).  Replaces the 64-bit integer divisions of every id <-> coordinate map.
+struct FastDiv {
+    std::uint64_t d = 1, m = 0;
+    __host__ __device__ static FastDiv make(std::uint64_t dv) {
+        FastDiv f;
+        f.d = dv;
+        f.m = dv <= 1 ? 0 : (~0ull) / dv + 1;
+        return f;
+    }
+    __host__ __device__ __forceinline__ std::uint64_t div(std::uint64_t n) const {
+        if (d == 1) return n;
+#ifdef __CUDA_ARCH__
+        return __umul64hi(n, m);
+#else
+        return static_cast<std::uint64_t>((static_cast<unsigned __int128>(n) * m) >> 64);
+#endif
+    }
+};
+
 struct Dims {
     std::int64_t nx, ny, nz;   // vertices
     std::int64_t ex, ey, ez;   // lattice extents 2n-1
     std::int64_t exy;          // ex*ey
     std::uint64_t n_cells, n_verts, n_cubes;
+    FastDiv fex, fey, fnx, fny, fmx, fmy;  // by ex, ey, nx, ny, nx-1, ny-1
 
     __host__ __device__ static Dims make(std::int64_t x, std::int64_t y, std::int64_t z) {
         Dims d;
@@ -34,6 +56,12 @@ struct Dims {
         d.n_cells = static_cast<std::uint64_t>(d.ex) * d.ey * d.ez;
         d.n_verts = static_cast<std::uint64_t>(x) * y * z;
         d.n_cubes = static_cast<std::uint64_t>(x - 1) * (y - 1) * (z - 1);
+        d.fex = FastDiv::make(d.ex);
+        d.fey = FastDiv::make(d.ey);
+        d.fnx = FastDiv::make(x);
+        d.fny = FastDiv::make(y);
+        d.fmx = FastDiv::make(x - 1);
+        d.fmy = FastDiv::make(y - 1);
         return d;
     }
 };
@@ -58,9 +86,9 @@ struct Coord {
 
 __host__ __device__ inline Coord unpack(const Dims& d, std::uint64_t id) {
     Coord c;
-    const std::uint64_t q = id / static_cast<std::uint64_t>(d.ex);
+    const std::uint64_t q = d.fex.div(id);
     c.x = static_cast<std::int64_t>(id - q * d.ex);
-    c.z = static_cast<std::int64_t>(q / static_cast<std::uint64_t>(d.ey));
+    c.z = static_cast<std::int64_t>(d.fey.div(q));
     c.y = static_cast<std::int64_t>(q - static_cast<std::uint64_t>(c.z) * d.ey);
     return c;
 }
@@ -82,12 +110,12 @@ __host__ __device__ inline std::uint32_t cube_dense(const Dims& d, const Coord& 
     return static_cast<std::uint32_t>(c.x / 2 + (d.nx - 1) * (c.y / 2 + (d.ny - 1) * (c.z / 2)));
 }
 __host__ __device__ inline std::uint64_t vertex_cell(const Dims& d, std::uint64_t i) {
-    const std::uint64_t x = i % d.nx, r = i / d.nx, y = r % d.ny, z = r / d.ny;
+    const std::uint64_t r = d.fnx.div(i), x = i - r * d.nx, z = d.fny.div(r), y = r - z * d.ny;
     return pack(d, 2 * x, 2 * y, 2 * z);
 }
 __host__ __device__ inline std::uint64_t cube_cell(const Dims& d, std::uint64_t i) {
     const std::uint64_t mx = d.nx - 1, my = d.ny - 1;
-    const std::uint64_t x = i % mx, r = i / mx, y = r % my, z = r / my;
+    const std::uint64_t r = d.fmx.div(i), x = i - r * mx, z = d.fmy.div(r), y = r - z * my;
     return pack(d, 2 * x + 1, 2 * y + 1, 2 * z + 1);
 }
 

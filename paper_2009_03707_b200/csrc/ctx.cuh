@@ -25,6 +25,7 @@ struct msc3d_ctx {
     bool own_stream = false;
     msc3d_dev::Dims dims{};
     bool have_dims = false;
+    bool crit_counts_valid = false;  // d_small[40..43] hold the codes' critical counts
     int value_type = MSC3D_VALUE_F32;
     const void* values = nullptr;  // device pointer (owned "values" array or bound)
     std::map<std::string, DevArray> arrays;

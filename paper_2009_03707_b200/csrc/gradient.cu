@@ -1,25 +1,33 @@
 // Lower-star discrete gradient on the B200 (assign_gradient, proj/src/gradient.cpp:79-283).
 //
-// One thread per vertex; the 3x3x3 vertex block around it is staged in shared
-// memory once per CTA tile.  The reference's per-star work (27-slot arrays,
-// per-cell sorted keys, two lazily-pruned queues) is restated as 27-bit slot
-// masks:
-//   * lower-star membership: the subset rule (gradient.cpp:104-120) evaluated as
-//     two rounds of shifted mask ANDs;
-//   * cell order key: the reference compares cells by their vertex values sorted
-//     descending, then by vertex ids sorted descending, *independently*
-//     (grid.cpp:91-122, gradient.cpp:53-63).  Inside one star this equals an
-//     unsigned compare of ((value-thermometer mask) << 27 | vertex-slot mask):
-//     the value part sets, for each vertex, the highest free bit at or below the
-//     top rank of its equal-value group (so equal values compare as multisets),
-//     the id part uses that ids of in-range neighbours increase with slot index;
-//   * queues q0/q1 as masks; pop_min = argmin of the key over the mask; "number
-//     of unassigned facets" = popcount(facet mask & ~assigned).
-// Every cell is written exactly once, by the owner of its maximal vertex, so the
-// scattered byte stores need no synchronisation.  Optionally the same kernel emits
-// the two extremum forests (build_forest, extrema.cpp:43-77): a vertex's parent is
-// the far end of the edge it pairs with, a cube's parent the cube across the quad
-// it pairs with (itself at the boundary or when critical).
+// One CTA stages a 32x4x2 vertex tile (+1 halo) in shared memory; each vertex's
+// lower star is processed as 27-bit slot masks (slot t = (dx+1) + 3(dy+1) + 9(dz+1)):
+//   * membership: the subset rule (gradient.cpp:104-120) as two rounds of shifted
+//     mask ANDs;
+//   * cell order (grid.cpp:91-122, gradient.cpp:53-63): cells are compared by their
+//     vertex values sorted descending, then by vertex ids sorted descending,
+//     *independently*.  With the star's vertices ranked by value (distinct values),
+//     that is exactly an unsigned compare of the cells' rank bitmasks M(t)
+//     (the larger maximum of the symmetric difference wins; a prefix loses);
+//   * queues q0/q1 and "unassigned facets" as masks (popcount of facets & ~assigned),
+//     pop_min = the cell of least rank mask.
+//
+// Fast path (registers only, no per-step memory chains): the star's vertices are
+// compacted with __fns into K registers (K = 8/16/32, chosen per warp), sorted by a
+// bitonic network, ranked; every cell's rank mask is built from its facets' masks
+// (unrolled over the 26 slots, constant indices); the cells are sorted by mask with
+// a second network of u32 keys (mask << 5 | slot); the expansion then pops minima
+// by position.  Vertices are bucketed by star size inside the CTA first, so the
+// warps running the sort networks are size-homogeneous.
+//
+// Stars containing two equal values go to the slow path (k_gradient_deferred),
+// which keeps the reference's general multiset-then-ids key (value thermometer
+// << 27 | vertex-slot mask): equal values compare as multisets, the id part uses
+// that ids of in-range neighbours increase with slot index.
+//
+// Every cell is written exactly once, by the owner of its maximal vertex (plain
+// byte stores).  The same kernel emits both extremum forests (build_forest,
+// extrema.cpp:43-77) and the per-dimension critical counts.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -49,8 +57,7 @@ SlotTables host_tables() {
         std::uint32_t sub = 0;
         for (int u = 0; u < 27; ++u) {
             bool ok = true;
-            for (int a = 0; a < 3; ++a)
-                ok = ok && (s.off[u][a] == 0 || s.off[u][a] == s.off[t][a]);
+            for (int a = 0; a < 3; ++a) ok = ok && (s.off[u][a] == 0 || s.off[u][a] == s.off[t][a]);
             if (ok) sub |= 1u << u;
         }
         s.sub[t] = sub;
@@ -69,6 +76,7 @@ SlotTables host_tables() {
 }
 
 constexpr int TX = 32, TY = 4, TZ = 2;
+constexpr int NT = TX * TY * TZ;
 constexpr int SX = TX + 2, SY = TY + 2, SZ = TZ + 2;
 constexpr std::uint32_t kCentre = 1u << 13;
 constexpr std::uint32_t kAll = (1u << 27) - 1;
@@ -85,6 +93,14 @@ constexpr std::uint32_t kXP = axis_mask(0, 1), kXM = axis_mask(0, -1);
 constexpr std::uint32_t kYP = axis_mask(1, 1), kYM = axis_mask(1, -1);
 constexpr std::uint32_t kZP = axis_mask(2, 1), kZM = axis_mask(2, -1);
 constexpr std::uint32_t kDim1 = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 14) | (1u << 16) | (1u << 22);
+constexpr std::uint32_t kDim3 = (1u << 0) | (1u << 2) | (1u << 6) | (1u << 8) | (1u << 18) | (1u << 20) |
+                                (1u << 24) | (1u << 26);
+
+constexpr int slot_off(int t, int a) { return a == 0 ? t % 3 - 1 : (a == 1 ? (t / 3) % 3 - 1 : t / 9 - 1); }
+constexpr int slot_dim(int t) {
+    return (slot_off(t, 0) != 0) + (slot_off(t, 1) != 0) + (slot_off(t, 2) != 0);
+}
+constexpr int slot_tile(int t) { return slot_off(t, 2) * (SX * SY) + slot_off(t, 1) * SX + slot_off(t, 0); }
 
 __device__ __forceinline__ std::uint32_t facets_present(std::uint32_t s) {
     const std::uint32_t okx = (~(kXP | kXM) | ((s << 1) & kXP) | ((s >> 1) & kXM));
@@ -93,167 +109,138 @@ __device__ __forceinline__ std::uint32_t facets_present(std::uint32_t s) {
     return okx & oky & okz & kAll;
 }
 
-__device__ __forceinline__ int argmin_key(std::uint32_t m, const std::uint64_t* key) {
-    int best = __ffs(m) - 1;
-    std::uint64_t bk = key[best];
-    m &= m - 1;
-    while (m) {
-        const int t = __ffs(m) - 1;
-        m &= m - 1;
-        if (key[t] < bk) {
-            bk = key[t];
-            best = t;
-        }
-    }
-    return best;
+// slot -> offset in the shared tile (dynamic slot)
+__device__ __forceinline__ int tile_off(int t) {
+    const int z = (t * 57) >> 9;  // t / 9 for t < 27
+    const int r = t - 9 * z;
+    const int y = (r * 11) >> 5;  // r / 3 for r < 9
+    const int x = r - 3 * y;
+    return (z - 1) * (SX * SY) + (y - 1) * SX + (x - 1);
 }
 
+// Order-preserving unsigned key of a sample value (+0 and -0 compare equal).
+__device__ __forceinline__ std::uint32_t ord_key(float v) {
+    const std::uint32_t u = __float_as_uint(v + 0.0f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ std::uint64_t ord_key(double v) {
+    const std::uint64_t u = static_cast<std::uint64_t>(__double_as_longlong(v + 0.0));
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
 template <typename T>
-__global__ void __launch_bounds__(TX * TY * TZ)
-k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
-           std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3) {
-    __shared__ T tile[SZ][SY][SX];
-    const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * TX - 1;
-    const std::int64_t y0 = static_cast<std::int64_t>(blockIdx.y) * TY - 1;
-    const std::int64_t z0 = static_cast<std::int64_t>(blockIdx.z) * TZ - 1;
-    const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
-    for (int i = tid; i < SX * SY * SZ; i += TX * TY * TZ) {
-        const int lx = i % SX, ly = (i / SX) % SY, lz = i / (SX * SY);
-        const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        T v = T(0);
-        if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz)
-            v = f[gx + d.nx * (gy + d.ny * gz)];
-        tile[lz][ly][lx] = v;
+struct KeyOf;
+template <>
+struct KeyOf<float> {
+    using type = std::uint32_t;
+};
+template <>
+struct KeyOf<double> {
+    using type = std::uint64_t;
+};
+
+// 5-bit fields indexed by slot (0..26) in three 64-bit words.
+struct Pack5 {
+    std::uint64_t w[3] = {0, 0, 0};
+    __device__ __forceinline__ void set(int slot, std::uint32_t v) {
+        const int wi = slot >= 24 ? 2 : (slot >= 12 ? 1 : 0);
+        const std::uint64_t x = static_cast<std::uint64_t>(v) << (5 * (slot - 12 * wi));
+        if (wi == 0) w[0] |= x;
+        else if (wi == 1) w[1] |= x;
+        else w[2] |= x;
     }
-    __syncthreads();
-
-    const std::int64_t vx = x0 + 1 + threadIdx.x, vy = y0 + 1 + threadIdx.y,
-                       vz = z0 + 1 + threadIdx.z;
-    if (vx >= d.nx || vy >= d.ny || vz >= d.nz) return;
-    const T* base = &tile[threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + 1];
-    auto val = [&](int t) {
-        return base[(t / 9 - 1) * (SX * SY) + ((t / 3) % 3 - 1) * SX + (t % 3 - 1)];
-    };
-
-    // In-range neighbours and "below the centre" in (value, id) order
-    // (gradient.cpp:86-102); ids grow with slot index, so id < vi <=> slot < 13.
-    std::uint32_t inr = kAll;
-    if (vx == 0) inr &= ~kXM;
-    if (vx == d.nx - 1) inr &= ~kXP;
-    if (vy == 0) inr &= ~kYM;
-    if (vy == d.ny - 1) inr &= ~kYP;
-    if (vz == 0) inr &= ~kZM;
-    if (vz == d.nz - 1) inr &= ~kZP;
-    const T fv = val(13);
-    std::uint32_t below = kCentre;
-#pragma unroll
-    for (int t = 0; t < 27; ++t) {
-        if (t == 13) continue;
-        const T u = val(t);
-        if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+    __device__ __forceinline__ std::uint32_t get(int slot) const {
+        const int wi = slot >= 24 ? 2 : (slot >= 12 ? 1 : 0);
+        const std::uint64_t ww = wi == 0 ? w[0] : (wi == 1 ? w[1] : w[2]);
+        return static_cast<std::uint32_t>(ww >> (5 * (slot - 12 * wi))) & 31u;
     }
-    std::uint32_t S = below & inr;
-    S &= facets_present(S);
-    S &= facets_present(S);
+};
 
-    const std::int64_t vi = vx + d.nx * (vy + d.ny * vz);
-    const std::int64_t vcell = 2 * vx + d.ex * (2 * vy + d.ey * 2 * vz);
-    const std::int64_t sstep[3] = {1, d.ex, d.exy};
-    auto cell_of = [&](int t) {
-        return vcell + c_slot.off[t][0] + c_slot.off[t][1] * d.ex + c_slot.off[t][2] * d.exy;
-    };
+// Output side of one star: codes, forests, critical counts.
+struct StarWriter {
+    std::uint8_t* cbase;           // codes + vertex cell id
+    const std::int32_t* cell_off;  // lattice offset per slot
+    std::uint32_t* parent0;
+    std::uint32_t* parent3;
+    Dims d;
+    std::int64_t vx, vy, vz;
+    std::uint32_t inr;
+    std::uint64_t ncrit;           // 16 bits per dimension
 
-    if (S == kCentre) {  // |star| == 1: critical minimum (gradient.cpp:128-131)
-        codes[vcell] = kCritical;
+    __device__ __forceinline__ std::uint32_t cube_dense_of(int t) const {
+        const int z = (t * 57) >> 9, r = t - 9 * z, y = (r * 11) >> 5, x = r - 3 * y;
+        return static_cast<std::uint32_t>((vx + (x == 0 ? -1 : 0)) +
+                                          (d.nx - 1) * ((vy + (y == 0 ? -1 : 0)) +
+                                                        (d.ny - 1) * (vz + (z == 0 ? -1 : 0))));
+    }
+    __device__ __forceinline__ void pair(int lo, int hi) {  // gradient.cpp:162-174
+        const int diff = hi - lo;  // +-1, +-3 or +-9
+        const int ad = diff < 0 ? -diff : diff;
+        const int ax = ad == 1 ? 0 : (ad == 3 ? 1 : 2);
+        const int pos = diff > 0;
+        cbase[cell_off[lo]] = static_cast<std::uint8_t>(kCofacetBase + ax * 2 + pos);
+        cbase[cell_off[hi]] = static_cast<std::uint8_t>(kFacetBase + ax * 2 + (1 - pos));
+        if (lo == 13 && parent0) {
+            const std::int64_t vi = vx + d.nx * (vy + d.ny * vz);
+            const std::int64_t step = ax == 0 ? 1 : (ax == 1 ? d.nx : d.nx * d.ny);
+            parent0[vi] = static_cast<std::uint32_t>(pos ? vi + step : vi - step);
+        }
+        if (parent3 && ((kDim3 >> hi) & 1u)) {
+            // cube hi pairs with quad lo: continue into the cube across lo
+            const int across = lo - diff;
+            const std::uint32_t self = cube_dense_of(hi);
+            parent3[self] = ((inr >> across) & 1u) ? cube_dense_of(across) : self;
+        }
+    }
+    __device__ __forceinline__ void critical(int t, int dm) {
+        cbase[cell_off[t]] = kCritical;
+        ncrit += 1ull << (16 * dm);
+        if (parent3 && dm == 3) {
+            const std::uint32_t self = cube_dense_of(t);
+            parent3[self] = self;
+        }
+    }
+    __device__ __forceinline__ void minimum() {
+        cbase[0] = kCritical;
+        ncrit += 1ull;
+        const std::int64_t vi = vx + d.nx * (vy + d.ny * vz);
         if (parent0) parent0[vi] = static_cast<std::uint32_t>(vi);
-        return;
     }
+};
 
-    // Top rank of each star vertex's equal-value group.
-    std::uint8_t top[27];
-    for (std::uint32_t m = S; m; m &= m - 1) {
-        const int s = __ffs(m) - 1;
-        const T vs = val(s);
-        int c = -1;
-        for (std::uint32_t n = S; n; n &= n - 1) c += val(__ffs(n) - 1) <= vs;
-        top[s] = static_cast<std::uint8_t>(c);
-    }
-    std::uint64_t key[27];
-    for (std::uint32_t m = S & ~kCentre; m; m &= m - 1) {
-        const int t = __ffs(m) - 1;
-        std::uint32_t vm = 0;
-        for (std::uint32_t n = c_slot.sub[t]; n; n &= n - 1) {
-            int b = top[__ffs(n) - 1];
-            while ((vm >> b) & 1u) --b;
-            vm |= 1u << b;
-        }
-        key[t] = (static_cast<std::uint64_t>(vm) << 27) | c_slot.sub[t];
-    }
-
-    auto write_pair = [&](int lo, int hi) {  // gradient.cpp:162-174
-        int ax = 0;
-        while (c_slot.off[lo][ax] == c_slot.off[hi][ax]) ++ax;
-        const int sign = c_slot.off[hi][ax] - c_slot.off[lo][ax];
-        codes[cell_of(lo)] = static_cast<std::uint8_t>(kCofacetBase + ax * 2 + (sign > 0));
-        codes[cell_of(hi)] = static_cast<std::uint8_t>(kFacetBase + ax * 2 + (sign < 0));
-        if (parent3 && c_slot.dim[hi] == 3) {
-            // Cube hi pairs with quad lo; continue into the cube across lo
-            // (extrema.cpp:63-75), or stop at a boundary quad.
-            const int across = lo - (hi - lo);
-            const std::int64_t cx = 2 * vx + c_slot.off[hi][0], cy = 2 * vy + c_slot.off[hi][1],
-                               cz = 2 * vz + c_slot.off[hi][2];
-            const std::uint32_t self =
-                static_cast<std::uint32_t>(cx / 2 + (d.nx - 1) * (cy / 2 + (d.ny - 1) * (cz / 2)));
-            std::uint32_t par = self;
-            if ((inr >> across) & 1u) {
-                const std::int64_t ax2 = 2 * vx + c_slot.off[across][0],
-                                   ay2 = 2 * vy + c_slot.off[across][1],
-                                   az2 = 2 * vz + c_slot.off[across][2];
-                par = static_cast<std::uint32_t>(ax2 / 2 + (d.nx - 1) * (ay2 / 2 + (d.ny - 1) * (az2 / 2)));
-            }
-            parent3[self] = par;
-        }
-        (void)sstep;
-    };
-
+// The lower-star expansion (gradient.cpp:196-264) over slot masks; `argmin`
+// returns the least cell of a non-empty slot mask.
+template <typename ArgMin>
+__device__ __forceinline__ void robins(std::uint32_t S, const std::uint32_t* fac, const std::uint32_t* cof,
+                                       ArgMin argmin, StarWriter& w) {
     std::uint32_t assigned = 0, q0 = 0, q1 = 0;
-    auto settle = [&](int t) {  // gradient.cpp:178-193
+    auto settle = [&](int t) {
         assigned |= 1u << t;
-        for (std::uint32_t m = c_slot.cofacet[t] & S & ~assigned; m; m &= m - 1) {
+        for (std::uint32_t m = cof[t] & S & ~assigned; m; m &= m - 1) {
             const int c = __ffs(m) - 1;
-            if (__popc(c_slot.facet[c] & ~assigned) == 1) q1 |= 1u << c;
+            if (__popc(fac[c] & ~assigned) == 1) q1 |= 1u << c;
         }
     };
-
-    // The vertex pairs with its lowest edge; other edges become candidates
-    // (gradient.cpp:196-207).
     const std::uint32_t edges = S & kDim1;
-    const int delta = argmin_key(edges, key);
+    const int delta = argmin(edges);
     q0 = edges & ~(1u << delta);
-    write_pair(13, delta);
-    if (parent0) {
-        parent0[vi] = static_cast<std::uint32_t>(vi + c_slot.off[delta][0] +
-                                                 c_slot.off[delta][1] * d.nx +
-                                                 c_slot.off[delta][2] * d.nx * d.ny);
-    }
+    w.pair(13, delta);
     settle(13);
     settle(delta);
-
     int remaining = __popc(S) - 2;
-    while (remaining > 0) {  // gradient.cpp:226-264
+    while (remaining > 0) {
         bool worked = false;
         for (;;) {
             const std::uint32_t cand = q1 & ~assigned;
             if (!cand) break;
-            const int t = argmin_key(cand, key);
+            const int t = argmin(cand);
             q1 &= ~(1u << t);
-            const std::uint32_t free_facets = c_slot.facet[t] & ~assigned;
-            if (__popc(free_facets) != 1) {
+            const std::uint32_t free_f = fac[t] & ~assigned;
+            if (__popc(free_f) != 1) {
                 q0 |= 1u << t;
                 continue;
             }
-            const int fs = __ffs(free_facets) - 1;
-            write_pair(fs, t);
+            const int fs = __ffs(free_f) - 1;
+            w.pair(fs, t);
             settle(fs);
             settle(t);
             remaining -= 2;
@@ -262,21 +249,369 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         if (remaining == 0) break;
         const std::uint32_t cand = q0 & ~assigned;
         if (cand) {
-            const int t = argmin_key(cand, key);
+            const int t = argmin(cand);
             q0 &= ~(1u << t);
-            codes[cell_of(t)] = kCritical;
-            if (parent3 && c_slot.dim[t] == 3) {
-                const std::int64_t cx = 2 * vx + c_slot.off[t][0], cy = 2 * vy + c_slot.off[t][1],
-                                   cz = 2 * vz + c_slot.off[t][2];
-                const std::uint32_t self = static_cast<std::uint32_t>(
-                    cx / 2 + (d.nx - 1) * (cy / 2 + (d.ny - 1) * (cz / 2)));
-                parent3[self] = self;
-            }
+            const int nf = __popc(fac[t]);  // dimension = number of v-containing facets
+            w.critical(t, nf);
             settle(t);
             --remaining;
             worked = true;
         }
         if (!worked) break;  // cannot happen on a valid star (gradient.cpp:259-262)
+    }
+}
+
+template <typename KT>
+__device__ __forceinline__ void ce_pair(KT& ka, std::uint32_t& sa, KT& kb, std::uint32_t& sb, bool up) {
+    const bool sw = up ? (kb < ka) : (ka < kb);
+    const KT k0 = sw ? kb : ka, k1 = sw ? ka : kb;
+    const std::uint32_t s0 = sw ? sb : sa, s1 = sw ? sa : sb;
+    ka = k0;
+    kb = k1;
+    sa = s0;
+    sb = s1;
+}
+
+__device__ __forceinline__ void ce_u32(std::uint32_t& a, std::uint32_t& b, bool up) {
+    const std::uint32_t lo = min(a, b), hi = max(a, b);
+    a = up ? lo : hi;
+    b = up ? hi : lo;
+}
+
+// Fast path for one star with n <= K vertices and distinct values.  Returns false
+// (nothing written) when two star values tie.
+template <int K, typename T>
+__device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
+                                          const std::uint32_t* fac, const std::uint32_t* cof,
+                                          std::uint32_t* mscratch, StarWriter& w) {
+    using KT = typename KeyOf<T>::type;
+    KT key[K];
+    std::uint32_t slot[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+        if (p < n) {
+            const int s = static_cast<int>(__fns(S, 0, p + 1));
+            slot[p] = static_cast<std::uint32_t>(s);
+            key[p] = ord_key(base[tile_off(s)]);
+        } else {
+            slot[p] = 31u;
+            key[p] = static_cast<KT>(~static_cast<KT>(0));
+        }
+    }
+    // (1) vertices by value: bitonic network
+#pragma unroll
+    for (int k = 2; k <= K; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const int l = i ^ j;
+                if (l > i) ce_pair(key[i], slot[i], key[l], slot[l], (i & k) == 0);
+            }
+    bool tie = false;
+#pragma unroll
+    for (int p = 0; p + 1 < K; ++p)
+        if (p + 1 < n) tie |= key[p] == key[p + 1];
+    if (tie) return false;
+    // (2) rank of every star vertex (the centre is the largest: rank n-1)
+    Pack5 rank;
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+        if (p < n) rank.set(static_cast<int>(slot[p]), static_cast<std::uint32_t>(p));
+    // (3) rank mask of every star cell, from its facets' masks (constant slots)
+    std::uint32_t M[27];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) M[t] = 0;
+    M[13] = 1u << (n - 1);
+    mscratch[13 * NT] = M[13];
+#pragma unroll
+    for (int dim = 1; dim <= 3; ++dim)
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            if (slot_dim(t) != dim) continue;
+            std::uint32_t m = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int o = slot_off(t, a);
+                if (o != 0) m |= M[t - o * (a == 0 ? 1 : (a == 1 ? 3 : 9))];
+            }
+            if ((S >> t) & 1u) {
+                m |= 1u << rank.get(t);
+                mscratch[t * NT] = m;
+            }
+            M[t] = m;
+        }
+    // (4) cells by mask: u32 keys (mask << 5 | slot), second network
+    std::uint32_t ck[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+        ck[p] = p < n ? ((mscratch[slot[p] * NT] << 5) | slot[p]) : 0xffffffffu;
+#pragma unroll
+    for (int k = 2; k <= K; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const int l = i ^ j;
+                if (l > i) ce_u32(ck[i], ck[l], (i & k) == 0);
+            }
+    Pack5 cpos, slotp;  // slot -> position, position -> slot
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+        if (p < n) {
+            const int s = static_cast<int>(ck[p] & 31u);
+            cpos.set(s, static_cast<std::uint32_t>(p));
+            if (p < 27) slotp.set(p, static_cast<std::uint32_t>(s));
+        }
+    // (5) expansion, pop-min by position
+    robins(S, fac, cof,
+           [&](std::uint32_t m) {
+               std::uint32_t pm = 0;
+               for (; m; m &= m - 1) pm |= 1u << cpos.get(__ffs(m) - 1);
+               return static_cast<int>(slotp.get(__ffs(pm) - 1));
+           },
+           w);
+    return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT)
+k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
+           std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
+           unsigned long long* __restrict__ crit_totals, std::uint32_t* __restrict__ deferred,
+           unsigned long long* __restrict__ n_deferred) {
+    __shared__ T tile[SZ][SY][SX];
+    __shared__ std::uint32_t s_fac[27], s_cof[27];
+    __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_S[NT];
+    __shared__ std::uint16_t s_order[NT];
+    __shared__ std::uint32_t s_hist[32];
+    __shared__ std::uint32_t s_total;
+    __shared__ unsigned long long s_crit[4];
+    __shared__ std::uint32_t s_M[27 * NT];
+    const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
+    if (tid < 27) {
+        s_fac[tid] = c_slot.facet[tid];
+        s_cof[tid] = c_slot.cofacet[tid];
+        s_cell[tid] = static_cast<std::int32_t>(c_slot.off[tid][0] + c_slot.off[tid][1] * d.ex +
+                                                c_slot.off[tid][2] * d.exy);
+    }
+    if (tid < 32) s_hist[tid] = 0;
+    if (tid < 4) s_crit[tid] = 0;
+    const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * TX - 1;
+    const std::int64_t y0 = static_cast<std::int64_t>(blockIdx.y) * TY - 1;
+    const std::int64_t z0 = static_cast<std::int64_t>(blockIdx.z) * TZ - 1;
+    for (int i = tid; i < SX * SY * SZ; i += NT) {
+        const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
+        const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+        T v = T(0);
+        if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz)
+            v = f[gx + d.nx * (gy + d.ny * gz)];
+        tile[lz][ly][lx] = v;
+    }
+    __syncthreads();
+
+    auto writer_for = [&](int lid) {
+        const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
+        StarWriter w;
+        w.vx = x0 + 1 + lx;
+        w.vy = y0 + 1 + ly;
+        w.vz = z0 + 1 + lz;
+        std::uint32_t inr = kAll;
+        if (w.vx == 0) inr &= ~kXM;
+        if (w.vx == d.nx - 1) inr &= ~kXP;
+        if (w.vy == 0) inr &= ~kYM;
+        if (w.vy == d.ny - 1) inr &= ~kYP;
+        if (w.vz == 0) inr &= ~kZM;
+        if (w.vz == d.nz - 1) inr &= ~kZP;
+        w.inr = inr;
+        w.d = d;
+        w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
+        w.cell_off = s_cell;
+        w.parent0 = parent0;
+        w.parent3 = parent3;
+        w.ncrit = 0;
+        return w;
+    };
+
+    // ---- phase 1: own vertex: star mask; trivial stars finished here -------------------
+    std::uint64_t ncrit = 0;
+    std::uint32_t S = 0;
+    {
+        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
+        const std::int64_t vx = x0 + 1 + lx, vy = y0 + 1 + ly, vz = z0 + 1 + lz;
+        if (vx < d.nx && vy < d.ny && vz < d.nz) {
+            StarWriter w = writer_for(tid);
+            const T* base = &tile[lz + 1][ly + 1][lx + 1];
+            const T fv = base[0];
+            std::uint32_t below = kCentre;
+#pragma unroll
+            for (int t = 0; t < 27; ++t) {
+                if (t == 13) continue;
+                const T u = base[slot_tile(t)];
+                if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+            }
+            S = below & w.inr;
+            S &= facets_present(S);
+            S &= facets_present(S);
+            const int n = __popc(S);
+            if (n == 1) {  // critical minimum (gradient.cpp:128-131)
+                w.minimum();
+                S = 0;
+            } else if (n == 2) {  // the vertex and its only edge pair up
+                w.pair(13, __ffs(S & ~kCentre) - 1);
+                S = 0;
+            }
+            ncrit = w.ncrit;
+        }
+    }
+    // ---- bucket the remaining stars by size (counting sort in shared memory) ---------
+    const int n_own = S ? __popc(S) : 0;
+    s_S[tid] = S;
+    if (n_own) atomicAdd(&s_hist[n_own], 1u);
+    __syncthreads();
+    if (tid < 32) {
+        const std::uint32_t v = s_hist[tid];
+        std::uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        s_hist[tid] = incl - v;
+        if (tid == 31) s_total = incl;
+    }
+    __syncthreads();
+    if (n_own) s_order[atomicAdd(&s_hist[n_own], 1u)] = static_cast<std::uint16_t>(tid);
+    __syncthreads();
+    const int nwork = static_cast<int>(s_total);
+
+    // ---- phase 2: size-homogeneous warps run the fast path ----------------------------
+    if (tid < nwork) {
+        const int lid = s_order[tid];
+        const std::uint32_t Sv = s_S[lid];
+        const int n = __popc(Sv);
+        StarWriter w = writer_for(lid);
+        const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
+        const T* base = &tile[lz + 1][ly + 1][lx + 1];
+        const unsigned active = __activemask();
+        const int kmax = static_cast<int>(__reduce_max_sync(active, static_cast<unsigned>(n)));
+        bool ok;
+        if (kmax <= 8) ok = star_fast<8>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
+        else if (kmax <= 16) ok = star_fast<16>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
+        else ok = star_fast<32>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
+        if (!ok) {
+            const unsigned long long at = atomicAdd(n_deferred, 1ull);
+            deferred[at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+        }
+        ncrit += w.ncrit;
+    }
+    if (crit_totals) {
+        std::uint64_t v = ncrit;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0 && v)
+            for (int k = 0; k < 4; ++k) {
+                const unsigned long long c = (v >> (16 * k)) & 0xffffu;
+                if (c) atomicAdd(&s_crit[k], c);
+            }
+        __syncthreads();
+        if (tid < 4 && s_crit[tid]) atomicAdd(&crit_totals[tid], s_crit[tid]);
+    }
+}
+
+// Slow path: stars with equal values.  The general key of the reference
+// (value multiset, then vertex ids), one thread per deferred vertex, values read
+// straight from global memory.
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
+                    std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
+                    const std::uint32_t* __restrict__ list, const unsigned long long* __restrict__ n_list,
+                    unsigned long long* __restrict__ crit_totals) {
+    __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_fac[27], s_cof[27];
+    if (threadIdx.x < 27) {
+        s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
+        s_cof[threadIdx.x] = c_slot.cofacet[threadIdx.x];
+        s_cell[threadIdx.x] = static_cast<std::int32_t>(
+            c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
+    }
+    __syncthreads();
+    const std::uint64_t nl = *n_list;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < nl;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t vi = list[i];
+        const std::uint64_t r = d.fnx.div(vi), vx = vi - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
+        StarWriter w;
+        w.vx = static_cast<std::int64_t>(vx);
+        w.vy = static_cast<std::int64_t>(vy);
+        w.vz = static_cast<std::int64_t>(vz);
+        std::uint32_t inr = kAll;
+        if (w.vx == 0) inr &= ~kXM;
+        if (w.vx == d.nx - 1) inr &= ~kXP;
+        if (w.vy == 0) inr &= ~kYM;
+        if (w.vy == d.ny - 1) inr &= ~kYP;
+        if (w.vz == 0) inr &= ~kZM;
+        if (w.vz == d.nz - 1) inr &= ~kZP;
+        w.inr = inr;
+        w.d = d;
+        w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
+        w.cell_off = s_cell;
+        w.parent0 = parent0;
+        w.parent3 = parent3;
+        w.ncrit = 0;
+        auto val = [&](int t) {
+            const std::int64_t ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
+            return f[(w.vx + ox) + d.nx * ((w.vy + oy) + d.ny * (w.vz + oz))];
+        };
+        const T fv = val(13);
+        std::uint32_t below = kCentre;
+        for (int t = 0; t < 27; ++t) {
+            if (t == 13 || !((inr >> t) & 1u)) continue;
+            const T u = val(t);
+            if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+        }
+        std::uint32_t S = below & inr;
+        S &= facets_present(S);
+        S &= facets_present(S);
+        // top rank of each star vertex's equal-value group, then the general key
+        std::uint8_t top[27];
+        for (std::uint32_t m = S; m; m &= m - 1) {
+            const int s = __ffs(m) - 1;
+            const T vs = val(s);
+            int c = -1;
+            for (std::uint32_t q = S; q; q &= q - 1) c += val(__ffs(q) - 1) <= vs;
+            top[s] = static_cast<std::uint8_t>(c);
+        }
+        std::uint64_t key[27];
+        for (std::uint32_t m = S & ~kCentre; m; m &= m - 1) {
+            const int t = __ffs(m) - 1;
+            std::uint32_t vm = 0;
+            for (std::uint32_t q = c_slot.sub[t]; q; q &= q - 1) {
+                int b = top[__ffs(q) - 1];
+                while ((vm >> b) & 1u) --b;
+                vm |= 1u << b;
+            }
+            key[t] = (static_cast<std::uint64_t>(vm) << 27) | c_slot.sub[t];
+        }
+        robins(S, s_fac, s_cof,
+               [&](std::uint32_t m) {
+                   int best = __ffs(m) - 1;
+                   std::uint64_t bk = key[best];
+                   for (m &= m - 1; m; m &= m - 1) {
+                       const int t = __ffs(m) - 1;
+                       if (key[t] < bk) {
+                           bk = key[t];
+                           best = t;
+                       }
+                   }
+                   return best;
+               },
+               w);
+        if (crit_totals)
+            for (int k = 0; k < 4; ++k) {
+                const unsigned long long c = (w.ncrit >> (16 * k)) & 0xffffu;
+                if (c) atomicAdd(&crit_totals[k], c);
+            }
     }
 }
 
@@ -293,22 +628,34 @@ int upload_gradient_tables(int device) {
 }
 
 int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
-                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream) {
+                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
+                    unsigned long long* crit_totals, std::uint32_t* deferred,
+                    unsigned long long* n_deferred, int num_sms) {
     int dev = 0;
     MSC3D_CUDA_TRY(cudaGetDevice(&dev));
     const int rc = upload_gradient_tables(dev);
     if (rc != MSC3D_OK) return rc;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(crit_totals, 0, 32, stream));
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_deferred, 0, 8, stream));
     const dim3 block(TX, TY, TZ);
     const dim3 grid(static_cast<unsigned>((d.nx + TX - 1) / TX),
                     static_cast<unsigned>((d.ny + TY - 1) / TY),
                     static_cast<unsigned>((d.nz + TZ - 1) / TZ));
-    if (value_type == MSC3D_VALUE_F64)
-        k_gradient<double><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d,
-                                                        codes, parent0, parent3);
-    else
-        k_gradient<float><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d,
-                                                      codes, parent0, parent3);
-    count_launch();
+    const unsigned dgrid = static_cast<unsigned>(4 * num_sms);
+    if (value_type == MSC3D_VALUE_F64) {
+        k_gradient<double><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d, codes,
+                                                        parent0, parent3, crit_totals, deferred, n_deferred);
+        k_gradient_deferred<double><<<dgrid, 128, 0, stream>>>(static_cast<const double*>(values), d, codes,
+                                                              parent0, parent3, deferred, n_deferred,
+                                                              crit_totals);
+    } else {
+        k_gradient<float><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes,
+                                                      parent0, parent3, crit_totals, deferred, n_deferred);
+        k_gradient_deferred<float><<<dgrid, 128, 0, stream>>>(static_cast<const float*>(values), d, codes,
+                                                            parent0, parent3, deferred, n_deferred,
+                                                            crit_totals);
+    }
+    count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }

@@ -29,7 +29,9 @@ struct Workspace {
 
 // gradient.cu
 int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
-                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream);
+                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
+                    unsigned long long* crit_totals, std::uint32_t* deferred,
+                    unsigned long long* n_deferred, int num_sms);
 
 // critical.cu
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
@@ -77,37 +79,35 @@ int launch_se_write(const void* saddles, std::uint64_t ns, int id_width,
 
 namespace msc3d_dev {
 // saddle.cu
-int launch_mark_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
-                        int id_width, std::uint8_t* marked, std::uint32_t* nodes,
-                        std::uint32_t* nid, unsigned int* bad, cudaStream_t s, int num_sms);
-int launch_bfs_level(const std::uint8_t* codes, const Dims& d, std::uint8_t* marked,
-                     std::uint32_t* nodes, std::uint64_t begin, std::uint64_t end,
-                     unsigned long long* tail, std::uint32_t* nid, cudaStream_t s, int num_sms);
+int launch_bfs_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
+                       int id_width, unsigned int* bitmap, std::uint32_t* frontier, unsigned int* bad,
+                       cudaStream_t s, int num_sms);
+int launch_bfs_persistent(const std::uint8_t* codes, const Dims& d, unsigned int* bitmap,
+                          std::uint32_t* fa, std::uint32_t* fb, unsigned long long* cnt,
+                          unsigned long long* stats, cudaStream_t s, int num_sms);
+int launch_marked_bytes(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                        std::uint64_t nwords, std::uint8_t* marked, cudaStream_t s, int num_sms);
 int launch_scatter_quad_rank(const void* list, std::uint64_t n, int id_width, const Dims& d,
                              std::uint32_t* tmap, cudaStream_t s, int num_sms);
-int launch_node_succ(const std::uint8_t* codes, const Dims& d, const std::uint32_t* nodes,
-                     std::uint64_t m, const std::uint32_t* nid, const std::uint32_t* tmap,
-                     std::uint32_t* succ, std::uint8_t* outdeg, cudaStream_t s, int num_sms);
-int launch_chain_ptr(const std::uint32_t* succ, const std::uint8_t* outdeg, std::uint64_t m,
-                     std::uint64_t n_src, std::uint32_t* ptr, cudaStream_t s, int num_sms);
-int launch_junction_flags(const std::uint8_t* outdeg, std::uint64_t m, std::uint64_t n_src,
-                          std::uint32_t* flag, cudaStream_t s, int num_sms);
-int launch_junction_write(const std::uint32_t* flag, const std::uint64_t* off, std::uint64_t m,
-                          std::uint32_t* jlist, std::uint32_t* jidx, cudaStream_t s, int num_sms);
-int launch_origin_dests(const std::uint32_t* jlist, std::uint64_t n, const std::uint32_t* succ,
-                        const std::uint8_t* outdeg, const std::uint32_t* stop,
-                        const std::uint32_t* jidx, std::uint32_t* dest, std::uint32_t* pending,
-                        std::uint32_t* indeg, cudaStream_t s, int num_sms);
+int launch_junction_count(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                          std::uint64_t nwords, std::uint32_t* per_word, cudaStream_t s, int num_sms);
+int launch_junction_write(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                          std::uint64_t nwords, const std::uint64_t* off, std::uint32_t* jlist,
+                          std::uint32_t* jidx, cudaStream_t s, int num_sms);
+int launch_origin_dests(const std::uint8_t* codes, const Dims& d, const std::uint32_t* jlist,
+                        const void* srcs, int id_width, std::uint64_t n, const std::uint32_t* jidx,
+                        const std::uint32_t* tmap, std::uint32_t* dest, std::uint32_t* pending,
+                        std::uint32_t* indeg, unsigned int* flags, cudaStream_t s, int num_sms);
 int launch_fill_rev(const std::uint32_t* dest, std::uint64_t nj, const std::uint64_t* roff,
                     std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
 int launch_initial_frontier(const std::uint32_t* pending, std::uint64_t nj, std::uint32_t* frontier,
                             unsigned long long* count, cudaStream_t s, int num_sms);
-int launch_kahn_level(const std::uint32_t* frontier, std::uint64_t nf, const std::uint32_t* dest,
-                      std::uint64_t* poff, std::uint32_t* plen, std::uint32_t* pkey,
-                      std::uint64_t* pcnt, unsigned long long* ptop, std::uint64_t pcap,
-                      const std::uint64_t* roff, const std::uint32_t* rcnt, const std::uint32_t* rsrc,
-                      std::uint32_t* pending, std::uint32_t* next, unsigned long long* next_count,
-                      unsigned int* flags, cudaStream_t s, int num_sms);
+int launch_kahn_persistent(const std::uint32_t* dest, std::uint64_t* poff, std::uint32_t* plen,
+                           std::uint32_t* pkey, std::uint64_t* pcnt, unsigned long long* ptop,
+                           std::uint64_t pcap, const std::uint64_t* roff, const std::uint32_t* rcnt,
+                           const std::uint32_t* rsrc, std::uint32_t* pending, std::uint32_t* fa,
+                           std::uint32_t* fb, unsigned long long* cnt, unsigned int* flags,
+                           unsigned long long* stats, cudaStream_t s, int num_sms);
 int launch_source_len(const std::uint32_t* dest, std::uint64_t n1, const std::uint64_t* poff,
                       const std::uint32_t* plen, const std::uint32_t* pkey, const std::uint64_t* pcnt,
                       std::uint32_t* len, unsigned int* flags, cudaStream_t s, int num_sms);

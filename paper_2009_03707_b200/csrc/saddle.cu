@@ -1,34 +1,37 @@
-// Saddle-saddle stages: DAG successors, reachability, chain contraction, minor
-// edges, and 2-saddle-keyed path counting (proj/src/saddle_graph.cpp,
-// proj/src/path_matrix.cpp), re-designed for the device.
+// Saddle-saddle stages: DAG successors, reachability, branch contraction and
+// 2-saddle-keyed path counting (proj/src/saddle_graph.cpp, proj/src/path_matrix.cpp),
+// re-designed for the device.
 //
-// Node store.  Every 1-cell reached from a 1-saddle becomes a node, numbered in
-// discovery order (sources first).  Nodes are kept as u32 "dense edge" indices
-// (3 * lower-vertex + axis), and nid[dense edge] maps back to the node number; it
-// is written only when a node is claimed and read only for claimed nodes, so it
-// is never initialised.
+// Node space.  DAG nodes are 1-cells; every per-node array is indexed by the "dense
+// edge" index de = 3 * (lower vertex) + axis, so a warp walking consecutive nodes
+// touches neighbouring lattice cells (no node renumbering, no id map).  Visited
+// nodes are one bit each (3V bits: 50 MB at 512^3, L2-resident).
 //
 // Successors (saddle_graph.cpp:10-24): for each cofacet quad q of e in cofacet
-// order, q critical -> terminal 2-saddle q; q paired with a facet edge e' != e ->
-// edge e'; q paired with a cube -> nothing.
+// order: q critical -> terminal 2-saddle q; q paired with a facet edge e' != e ->
+// edge e'; q paired with a cube -> nothing.  Recomputed from the pair codes
+// whenever needed (4 byte loads, spatially local) instead of stored.
 //
-// Reachability (saddle_graph.cpp:26-86): level-synchronous frontier expansion;
-// a node is claimed with an atomic OR on its marked byte (so the marked SET is the
-// reference's, whatever the schedule), and the quad it was entered through is
-// marked with it.
+// Reachability (saddle_graph.cpp:26-86): one persistent cooperative kernel runs all
+// BFS levels, with a grid barrier per level, warp-aggregated frontier appends and
+// an atomic test-and-set per claimed node bit.  The claimed SET equals the
+// reference's serial claim-order result.
 //
-// Counting.  The reference contracts junction-free paths into a minor and runs
-// sparse matrix products A* = A(I + B + B^2 ...), A*B* + D.  Here: (1) chain
-// contraction by pointer jumping over out-degree-1 nodes (the same forest trick as
-// the extrema), (2) per junction, the sparse vector P(j) of path counts to
-// 2-saddles, computed in reverse topological order (Kahn's algorithm on the
-// junction graph, one frontier per level) by merging the successors' vectors, and
-// (3) per 1-saddle the same merge written straight to the output.  Total work is
-// the sum of backward cone sizes of the 2-saddles (measured 1.3-1.9x the node count
-// on the BASELINE fields, SURVEY/BASELINE config data).  Counts are exact u64 with
-// sticky overflow detection.
+// Counting.  The reference contracts junction-free traces into a minor and then
+// multiplies sparse matrices, A* = A(I + B + B^2 ...), A*B* + D.  Here every
+// junction / 1-saddle branch is walked to its end (2-saddle, junction or dead end;
+// total walk length ~ the node count: 240.6 M trace steps for 243 M
+// nodes at config 3), and each junction's sparse vector P(j) of path counts to
+// 2-saddles is built in reverse topological order (Kahn's algorithm on the junction
+// graph: one persistent kernel, one grid barrier per level) by merging the
+// vectors of its branch destinations.  1-saddles merge the same way straight into
+// the sorted output.  Counts are exact u64; any overflow is sticky and reported.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace msc3d_dev {
 
@@ -48,31 +51,32 @@ inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; \
          i < (n); i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
 
-__device__ __forceinline__ std::uint32_t edge_dense(const Dims& d, const Coord& c) {
+struct C3 {
+    std::int32_t x, y, z;
+};
+
+__device__ __forceinline__ std::int64_t cell_id(const Dims& d, const C3& c) {
+    return c.x + d.ex * (c.y + d.ey * static_cast<std::int64_t>(c.z));
+}
+__device__ __forceinline__ std::uint32_t edge_dense(const Dims& d, const C3& c) {
     const int axis = (c.x & 1) ? 0 : ((c.y & 1) ? 1 : 2);
     return 3u * static_cast<std::uint32_t>((c.x >> 1) + d.nx * ((c.y >> 1) + d.ny * (c.z >> 1))) + axis;
 }
-__device__ __forceinline__ std::uint32_t quad_dense(const Dims& d, const Coord& c) {
+__device__ __forceinline__ std::uint32_t quad_dense(const Dims& d, const C3& c) {
     const int axis = !(c.x & 1) ? 0 : (!(c.y & 1) ? 1 : 2);
     return 3u * static_cast<std::uint32_t>((c.x >> 1) + d.nx * ((c.y >> 1) + d.ny * (c.z >> 1))) + axis;
 }
-__device__ __forceinline__ Coord edge_coord(const Dims& d, std::uint32_t de) {
-    const std::uint32_t v = de / 3, a = de - 3 * v;
-    const std::uint64_t vx = v % d.nx, r = v / d.nx, vy = r % d.ny, vz = r / d.ny;
-    Coord c;
-    c.x = 2 * vx + (a == 0);
-    c.y = 2 * vy + (a == 1);
-    c.z = 2 * vz + (a == 2);
+__device__ __forceinline__ C3 edge_coord(const Dims& d, std::uint32_t de) {
+    const std::uint32_t v = __umulhi(de, 0xAAAAAAABu) >> 1, a = de - 3 * v;
+    const std::uint64_t r = d.fnx.div(v), vx = v - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
+    C3 c;
+    c.x = static_cast<std::int32_t>(2 * vx + (a == 0));
+    c.y = static_cast<std::int32_t>(2 * vy + (a == 1));
+    c.z = static_cast<std::int32_t>(2 * vz + (a == 2));
     return c;
 }
-
-// Byte-granular atomic OR on a u8 array; returns the previous byte.
-__device__ __forceinline__ std::uint8_t atomic_or_byte(std::uint8_t* base, std::uint64_t i,
-                                                       std::uint8_t v) {
-    auto* w = reinterpret_cast<unsigned int*>(base + (i & ~3ull));
-    const int sh = 8 * static_cast<int>(i & 3);
-    const unsigned int old = atomicOr(w, static_cast<unsigned int>(v) << sh);
-    return static_cast<std::uint8_t>(old >> sh);
+__device__ __forceinline__ C3 to_c3(const Coord& c) {
+    return C3{static_cast<std::int32_t>(c.x), static_cast<std::int32_t>(c.y), static_cast<std::int32_t>(c.z)};
 }
 
 // Warp-aggregated reservation of n slots on a global counter.  Must be called by
@@ -92,13 +96,21 @@ __device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* c
     return base + incl - n;
 }
 
-// Successor enumeration of edge cell e (coords c): calls f(is_terminal, cell id).
-template <typename F>
-__device__ __forceinline__ void for_successors(const std::uint8_t* __restrict__ codes, const Dims& d,
-                                               const Coord& c, F&& f) {
-    const std::int64_t e = static_cast<std::int64_t>(pack(d, c.x, c.y, c.z));
-    const std::int64_t co[3] = {c.x, c.y, c.z};
+struct Succ {
+    C3 c[4];
+    std::uint32_t term;  // bit k: successor k is a terminal 2-saddle (quad)
+    int n;
+};
+
+// saddle_graph.cpp:10-24 on coordinates (no id <-> coordinate divisions).
+__device__ __forceinline__ Succ successors(const std::uint8_t* __restrict__ codes, const Dims& d,
+                                           const C3& e) {
+    Succ s;
+    s.n = 0;
+    s.term = 0;
+    const std::int32_t co[3] = {e.x, e.y, e.z};
     const std::int64_t ext[3] = {d.ex, d.ey, d.ez};
+    const std::int64_t eid = cell_id(d, e);
     const std::int64_t step[3] = {1, d.ex, d.exy};
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
@@ -106,23 +118,32 @@ __device__ __forceinline__ void for_successors(const std::uint8_t* __restrict__ 
 #pragma unroll
         for (int sgn = -1; sgn <= 1; sgn += 2) {
             if (sgn < 0 ? co[b] == 0 : co[b] == ext[b] - 1) continue;
-            const std::int64_t q = e + sgn * step[b];
-            const std::uint8_t k = codes[q];
+            const std::uint8_t k = codes[eid + sgn * step[b]];
+            C3 q = e;
+            if (b == 0) q.x += sgn;
+            else if (b == 1) q.y += sgn;
+            else q.z += sgn;
             if (k == kCritical) {
-                f(true, q);
+                s.term |= 1u << s.n;
+                s.c[s.n++] = q;
             } else if (paired_with_facet(k)) {
-                const std::int64_t o = partner_of(d, q, k);
-                if (o != e) f(false, o);
+                const int dir = k - kFacetBase, ax = dir >> 1, ps = (dir & 1) ? 1 : -1;
+                C3 o = q;
+                if (ax == 0) o.x += ps;
+                else if (ax == 1) o.y += ps;
+                else o.z += ps;
+                if (o.x != e.x || o.y != e.y || o.z != e.z) s.c[s.n++] = o;
             }
         }
     }
+    return s;
 }
 
 template <typename IdT>
-__global__ void k_mark_sources(const std::uint8_t* __restrict__ codes, Dims d,
-                               const IdT* __restrict__ src, std::uint64_t n,
-                               std::uint8_t* __restrict__ marked, std::uint32_t* __restrict__ nodes,
-                               std::uint32_t* __restrict__ nid, unsigned int* bad) {
+__global__ void k_bfs_sources(const std::uint8_t* __restrict__ codes, Dims d,
+                              const IdT* __restrict__ src, std::uint64_t n,
+                              unsigned int* __restrict__ bitmap, std::uint32_t* __restrict__ frontier,
+                              unsigned int* bad) {
     GRID_STRIDE(i, n) {
         const std::uint64_t e = src[i];
         if (e >= d.n_cells) {
@@ -134,38 +155,80 @@ __global__ void k_mark_sources(const std::uint8_t* __restrict__ codes, Dims d,
             *bad = 1u;
             continue;
         }
-        atomic_or_byte(marked, e, 1);
-        const std::uint32_t de = edge_dense(d, c);
-        nodes[i] = de;
-        nid[de] = static_cast<std::uint32_t>(i);
+        const std::uint32_t de = edge_dense(d, to_c3(c));
+        atomicOr(&bitmap[de >> 5], 1u << (de & 31));
+        frontier[i] = de;
     }
 }
 
-__global__ void k_bfs_level(const std::uint8_t* __restrict__ codes, Dims d,
-                            std::uint8_t* __restrict__ marked, std::uint32_t* __restrict__ nodes,
-                            std::uint64_t begin, std::uint64_t end,
-                            unsigned long long* __restrict__ tail, std::uint32_t* __restrict__ nid) {
-    const std::uint64_t n = end - begin;
+// All BFS levels in one cooperative launch.  cnt[0] holds the source count, cnt[1]
+// must be 0.  stats[0] = levels, stats[1] = nodes visited.
+__global__ void __launch_bounds__(kThreads)
+k_bfs_persistent(const std::uint8_t* __restrict__ codes, Dims d, unsigned int* __restrict__ bitmap,
+                 std::uint32_t* __restrict__ fa, std::uint32_t* __restrict__ fb,
+                 unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ stats) {
+    cg::grid_group g = cg::this_grid();
+    std::uint32_t* cur = fa;
+    std::uint32_t* nxt = fb;
+    unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&cnt[0]);
+    unsigned long long total = ncur;
+    int level = 0;
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
-         base < n; base += stride) {
-        const std::uint64_t j = base + (threadIdx.x & 31);
-        std::uint32_t won[4];
-        unsigned nwon = 0;
-        if (j < n) {
-            const Coord c = edge_coord(d, nodes[begin + j]);
-            for_successors(codes, d, c, [&](bool term, std::int64_t x) {
-                if (atomic_or_byte(marked, static_cast<std::uint64_t>(x), 1) || term) return;
-                // claimed: mark the quad we came through (its pair partner)
-                const std::uint8_t kx = codes[x];
-                atomic_or_byte(marked, static_cast<std::uint64_t>(partner_of(d, x, kx)), 1);
-                won[nwon++] = edge_dense(d, unpack(d, static_cast<std::uint64_t>(x)));
-            });
+    while (ncur) {
+        unsigned long long* next_cnt = &cnt[(level + 1) % 3];
+        if (g.thread_rank() == 0) cnt[(level + 2) % 3] = 0;
+        for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+             base < ncur; base += stride) {
+            const std::uint64_t j = base + (threadIdx.x & 31);
+            std::uint32_t won[4];
+            unsigned nwon = 0;
+            if (j < ncur) {
+                const Succ s = successors(codes, d, edge_coord(d, cur[j]));
+                for (int k = 0; k < s.n; ++k) {
+                    if ((s.term >> k) & 1u) continue;
+                    const std::uint32_t de = edge_dense(d, s.c[k]);
+                    const unsigned bit = 1u << (de & 31);
+                    if (bitmap[de >> 5] & bit) continue;  // cheap pre-check
+                    if (atomicOr(&bitmap[de >> 5], bit) & bit) continue;
+                    won[nwon++] = de;
+                }
+            }
+            const unsigned long long at = warp_reserve(next_cnt, nwon);
+            for (unsigned k = 0; k < nwon; ++k) nxt[at + k] = won[k];
         }
-        const unsigned long long at = warp_reserve(tail, nwon);
-        for (unsigned k = 0; k < nwon; ++k) {
-            nodes[at + k] = won[k];
-            nid[won[k]] = static_cast<std::uint32_t>(at + k);
+        g.sync();
+        ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
+        total += ncur;
+        ++level;
+        std::uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    if (g.thread_rank() == 0) {
+        stats[0] = static_cast<unsigned long long>(level);
+        stats[1] = total;
+    }
+}
+
+// The API's marked bytes (saddle_graph.hpp:45-50): visited edges, the quads they
+// were entered through (their pair partners), and the discovered 2-saddles.
+__global__ void k_marked_bytes(const std::uint8_t* __restrict__ codes, Dims d,
+                               const unsigned int* __restrict__ bitmap, std::uint64_t nwords,
+                               std::uint8_t* __restrict__ marked) {
+    GRID_STRIDE(w, nwords) {
+        unsigned int bits = bitmap[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const std::uint32_t de = static_cast<std::uint32_t>(w * 32 + b);
+            const C3 c = edge_coord(d, de);
+            const std::int64_t id = cell_id(d, c);
+            marked[id] = 1;
+            const std::uint8_t k = codes[id];
+            if (k != kCritical) marked[partner_of(d, id, k)] = 1;
+            const Succ s = successors(codes, d, c);
+            for (int q = 0; q < s.n; ++q)
+                if ((s.term >> q) & 1u) marked[cell_id(d, s.c[q])] = 1;
         }
     }
 }
@@ -174,93 +237,97 @@ __global__ void k_bfs_level(const std::uint8_t* __restrict__ codes, Dims d,
 template <typename IdT>
 __global__ void k_scatter_quad_rank(const IdT* __restrict__ list, std::uint64_t n, Dims d,
                                     std::uint32_t* __restrict__ tmap) {
-    GRID_STRIDE(k, n) tmap[quad_dense(d, unpack(d, list[k]))] = static_cast<std::uint32_t>(k);
+    GRID_STRIDE(k, n) tmap[quad_dense(d, to_c3(unpack(d, list[k])))] = static_cast<std::uint32_t>(k);
 }
 
-// Successor table of every node: 4 slots (kNone-padded), terminals as kTerm|rank.
-__global__ void k_node_succ(const std::uint8_t* __restrict__ codes, Dims d,
-                            const std::uint32_t* __restrict__ nodes, std::uint64_t m,
-                            const std::uint32_t* __restrict__ nid,
-                            const std::uint32_t* __restrict__ tmap,
-                            std::uint32_t* __restrict__ succ, std::uint8_t* __restrict__ outdeg) {
-    GRID_STRIDE(k, m) {
-        const Coord c = edge_coord(d, nodes[k]);
-        std::uint32_t s[4] = {kNone, kNone, kNone, kNone};
-        int n = 0;
-        for_successors(codes, d, c, [&](bool term, std::int64_t x) {
-            const Coord cx = unpack(d, static_cast<std::uint64_t>(x));
-            s[n++] = term ? (kTerm | tmap[quad_dense(d, cx)]) : nid[edge_dense(d, cx)];
-        });
-        reinterpret_cast<uint4*>(succ)[k] = make_uint4(s[0], s[1], s[2], s[3]);
-        outdeg[k] = static_cast<std::uint8_t>(n);
-    }
-}
-
-// Chain pointer: a non-source, non-junction node whose single successor is a
-// non-junction edge node continues into it; everything else is a stop.
-__global__ void k_chain_ptr(const std::uint32_t* __restrict__ succ, const std::uint8_t* __restrict__ outdeg,
-                            std::uint64_t m, std::uint64_t n_src, std::uint32_t* __restrict__ ptr) {
-    GRID_STRIDE(k, m) {
-        std::uint32_t p = static_cast<std::uint32_t>(k);
-        if (k >= n_src && outdeg[k] == 1) {
-            const std::uint32_t s = succ[4 * k];
-            if (!(s & kTerm) && outdeg[s] <= 1) p = s;
+// Junctions (saddle_graph.cpp:126-133): visited non-critical edges with > 1
+// successor.  Counting pass over the visited bitmap, 32 nodes per thread.
+__global__ void k_junction_count(const std::uint8_t* __restrict__ codes, Dims d,
+                                 const unsigned int* __restrict__ bitmap, std::uint64_t nwords,
+                                 std::uint32_t* __restrict__ per_word) {
+    GRID_STRIDE(w, nwords) {
+        unsigned int bits = bitmap[w];
+        std::uint32_t n = 0;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const C3 c = edge_coord(d, static_cast<std::uint32_t>(w * 32 + b));
+            if (codes[cell_id(d, c)] == kCritical) continue;
+            n += successors(codes, d, c).n > 1;
         }
-        ptr[k] = p;
+        per_word[w] = n;
     }
 }
 
-// Junction flags -> counts for compaction (node order).
-__global__ void k_junction_flags(const std::uint8_t* __restrict__ outdeg, std::uint64_t m,
-                                 std::uint64_t n_src, std::uint32_t* __restrict__ flag) {
-    GRID_STRIDE(k, m) flag[k] = (k >= n_src && outdeg[k] > 1) ? 1u : 0u;
-}
-
-__global__ void k_junction_write(const std::uint32_t* __restrict__ flag, const std::uint64_t* __restrict__ off,
-                                 std::uint64_t m, std::uint32_t* __restrict__ jlist,
+__global__ void k_junction_write(const std::uint8_t* __restrict__ codes, Dims d,
+                                 const unsigned int* __restrict__ bitmap, std::uint64_t nwords,
+                                 const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ jlist,
                                  std::uint32_t* __restrict__ jidx) {
-    GRID_STRIDE(k, m) {
-        if (flag[k]) {
-            jlist[off[k]] = static_cast<std::uint32_t>(k);
-            jidx[k] = static_cast<std::uint32_t>(off[k]);
+    GRID_STRIDE(w, nwords) {
+        unsigned int bits = bitmap[w];
+        std::uint64_t at = off[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const std::uint32_t de = static_cast<std::uint32_t>(w * 32 + b);
+            const C3 c = edge_coord(d, de);
+            if (codes[cell_id(d, c)] == kCritical) continue;
+            if (successors(codes, d, c).n > 1) {
+                jlist[at] = de;
+                jidx[de] = static_cast<std::uint32_t>(at);
+                ++at;
+            }
         }
     }
 }
 
-// Destination of one successor slot: terminal rank, junction index, or none.
-__device__ __forceinline__ std::uint32_t branch_dest(std::uint32_t s, const std::uint32_t* __restrict__ succ,
-                                                     const std::uint8_t* __restrict__ outdeg,
-                                                     const std::uint32_t* __restrict__ stop,
-                                                     const std::uint32_t* __restrict__ jidx) {
-    if (s == kNone) return kNone;
-    if (s & kTerm) return s;
-    if (outdeg[s] > 1) return jidx[s];
-    const std::uint32_t y = stop[s];
-    if (outdeg[y] == 0) return kNone;
-    const std::uint32_t s2 = succ[4ull * y];
-    if (s2 & kTerm) return s2;
-    return jidx[s2];
-}
-
-// Per origin (junction list entries, or sources when jlist == nullptr) the 4
-// branch destinations.
-__global__ void k_origin_dests(const std::uint32_t* __restrict__ jlist, std::uint64_t n,
-                               const std::uint32_t* __restrict__ succ, const std::uint8_t* __restrict__ outdeg,
-                               const std::uint32_t* __restrict__ stop, const std::uint32_t* __restrict__ jidx,
-                               std::uint32_t* __restrict__ dest, std::uint32_t* __restrict__ pending,
-                               std::uint32_t* __restrict__ indeg) {
+// Per origin (junctions: list of dense edges; sources: id list), the <= 4 branch
+// destinations: every branch is walked to its end (saddle_graph.cpp:139-202):
+// terminal 2-saddle -> kTerm|rank, junction -> junction index, dead end -> kNone.
+// Junction origins also count pending junction branches and predecessor
+// in-degrees for Kahn.
+template <typename IdT>
+__global__ void k_origin_dests(const std::uint8_t* __restrict__ codes, Dims d,
+                               const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs,
+                               std::uint64_t n, const std::uint32_t* __restrict__ jidx,
+                               const std::uint32_t* __restrict__ tmap, std::uint32_t* __restrict__ dest,
+                               std::uint32_t* __restrict__ pending, std::uint32_t* __restrict__ indeg,
+                               unsigned int* __restrict__ flags) {
     GRID_STRIDE(i, n) {
-        const std::uint64_t k = jlist ? jlist[i] : i;
-        const uint4 s4 = reinterpret_cast<const uint4*>(succ)[k];
-        const std::uint32_t s[4] = {s4.x, s4.y, s4.z, s4.w};
-        std::uint32_t dd[4];
+        const C3 o = jlist ? edge_coord(d, jlist[i]) : to_c3(unpack(d, srcs[i]));
+        const Succ s = successors(codes, d, o);
+        std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
         std::uint32_t pend = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            dd[b] = branch_dest(s[b], succ, outdeg, stop, jidx);
-            if (!(dd[b] & kTerm)) {
+        for (int b = 0; b < s.n; ++b) {
+            std::uint32_t t;
+            if ((s.term >> b) & 1u) {
+                t = kTerm | tmap[quad_dense(d, s.c[b])];
+            } else {
+                // the walk stops AT a junction, else follows the junction-free chain
+                C3 cur = s.c[b];
+                t = kNone;
+                for (std::uint64_t steps = 0;; ++steps) {
+                    const Succ nx = successors(codes, d, cur);
+                    if (nx.n > 1) {
+                        t = jidx[edge_dense(d, cur)];
+                        break;
+                    }
+                    if (nx.n == 0) break;
+                    if (nx.term & 1u) {
+                        t = kTerm | tmap[quad_dense(d, nx.c[0])];
+                        break;
+                    }
+                    cur = nx.c[0];
+                    if (steps > d.n_cells) {
+                        flags[2] = 1u;  // cycle: invalid gradient (saddle_graph.cpp:173-174)
+                        break;
+                    }
+                }
+            }
+            dd[b] = t;
+            if (!(t & kTerm)) {
                 ++pend;
-                if (indeg) atomicAdd(&indeg[dd[b]], 1u);
+                if (indeg) atomicAdd(&indeg[t], 1u);
             }
         }
         reinterpret_cast<uint4*>(dest)[i] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
@@ -285,8 +352,13 @@ __global__ void k_fill_rev(const std::uint32_t* __restrict__ dest, std::uint64_t
 __global__ void k_initial_frontier(const std::uint32_t* __restrict__ pending, std::uint64_t nj,
                                    std::uint32_t* __restrict__ frontier,
                                    unsigned long long* __restrict__ count) {
-    GRID_STRIDE(i, nj) {
-        if (pending[i] == 0) frontier[atomicAdd(count, 1ull)] = static_cast<std::uint32_t>(i);
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+         base < nj; base += stride) {
+        const std::uint64_t i = base + (threadIdx.x & 31);
+        const bool ready = i < nj && pending[i] == 0;
+        const unsigned long long at = warp_reserve(count, ready ? 1u : 0u);
+        if (ready) frontier[at] = static_cast<std::uint32_t>(i);
     }
 }
 
@@ -307,7 +379,7 @@ __device__ __forceinline__ bool mul_ovf(std::uint64_t a, std::uint64_t b, std::u
 }
 
 // K-way merge of up to 4 sorted (key, count) lists scaled by mult.  A terminal
-// branch is a one-element list.  With out == nullptr only the length is counted.
+// branch is a one-element list.  With okey == nullptr only the length is counted.
 struct MergeIn {
     const std::uint32_t* key[4];
     const std::uint64_t* cnt[4];
@@ -360,9 +432,11 @@ __device__ __forceinline__ void gather_inputs(const std::uint32_t* __restrict__ 
                                               const std::uint32_t* __restrict__ plen, const Pool& pool,
                                               MergeIn& in) {
     in.n = 0;
+    const uint4 d4 = reinterpret_cast<const uint4*>(dest)[i];
+    const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-        const std::uint32_t t = dest[4 * i + b];
+        const std::uint32_t t = dd[b];
         if (t == kNone) continue;
         const int k = in.n++;
         in.mult[k] = 1;
@@ -380,58 +454,80 @@ __device__ __forceinline__ void gather_inputs(const std::uint32_t* __restrict__ 
     }
 }
 
-__global__ void k_kahn_level(const std::uint32_t* __restrict__ frontier, std::uint64_t nf,
-                             const std::uint32_t* __restrict__ dest, std::uint64_t* __restrict__ poff,
-                             std::uint32_t* __restrict__ plen, Pool pool,
-                             const std::uint64_t* __restrict__ roff, const std::uint32_t* __restrict__ rcnt,
-                             const std::uint32_t* __restrict__ rsrc, std::uint32_t* __restrict__ pending,
-                             std::uint32_t* __restrict__ next, unsigned long long* __restrict__ next_count,
-                             unsigned int* __restrict__ flags) {
+// All Kahn levels in one cooperative launch.  cnt[0] = initial frontier size,
+// cnt[1] = 0.  stats[0] = levels, stats[1] = junctions processed.  flags[0]:
+// overflow, flags[1]: pool exhausted (the host grows the pool and reruns).
+__global__ void __launch_bounds__(kThreads)
+k_kahn_persistent(const std::uint32_t* __restrict__ dest, std::uint64_t* __restrict__ poff,
+                  std::uint32_t* __restrict__ plen, Pool pool, const std::uint64_t* __restrict__ roff,
+                  const std::uint32_t* __restrict__ rcnt, const std::uint32_t* __restrict__ rsrc,
+                  std::uint32_t* __restrict__ pending, std::uint32_t* __restrict__ fa,
+                  std::uint32_t* __restrict__ fb, unsigned long long* __restrict__ cnt,
+                  unsigned int* __restrict__ flags, unsigned long long* __restrict__ stats) {
+    cg::grid_group g = cg::this_grid();
+    std::uint32_t* cur = fa;
+    std::uint32_t* nxt = fb;
+    unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&cnt[0]);
+    unsigned long long done = 0;
+    int level = 0;
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
-         base < nf; base += stride) {
-        const std::uint64_t f = base + (threadIdx.x & 31);
-        const bool valid = f < nf;
-        std::uint32_t j = 0, len = 0;
-        MergeIn in;
-        in.n = 0;
-        if (valid) {
-            j = frontier[f];
-            gather_inputs(dest, j, poff, plen, pool, in);
-            len = kway_merge(in, nullptr, nullptr, &flags[0]);
-        }
-        const unsigned long long at = warp_reserve(pool.top, len);
-        if (valid) {
-            if (at + len > pool.cap) {
-                flags[1] = 1u;  // pool exhausted: host grows it and reruns
-                poff[j] = 0;
-                plen[j] = 0;
-            } else {
-                kway_merge(in, pool.key + at, pool.cnt + at, &flags[0]);
-                poff[j] = at;
-                plen[j] = len;
+    while (ncur) {
+        unsigned long long* next_cnt = &cnt[(level + 1) % 3];
+        if (g.thread_rank() == 0) cnt[(level + 2) % 3] = 0;
+        for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+             base < ncur; base += stride) {
+            const std::uint64_t f = base + (threadIdx.x & 31);
+            const bool valid = f < ncur;
+            std::uint32_t j = 0, len = 0;
+            MergeIn in;
+            in.n = 0;
+            if (valid) {
+                j = cur[f];
+                gather_inputs(dest, j, poff, plen, pool, in);
+                len = kway_merge(in, nullptr, nullptr, &flags[0]);
+            }
+            const unsigned long long at = warp_reserve(pool.top, len);
+            if (valid) {
+                if (at + len > pool.cap) {
+                    flags[1] = 1u;
+                    poff[j] = 0;
+                    plen[j] = 0;
+                } else {
+                    kway_merge(in, pool.key + at, pool.cnt + at, &flags[0]);
+                    poff[j] = at;
+                    plen[j] = len;
+                }
+            }
+            std::uint64_t r0 = 0;
+            std::uint32_t rn = 0;
+            if (valid) {
+                r0 = roff[j];
+                rn = rcnt[j];
+            }
+            for (;;) {
+                std::uint32_t rel[4];
+                unsigned nrel = 0;
+                while (rn && nrel < 4) {
+                    const std::uint32_t p = rsrc[r0++];
+                    --rn;
+                    if (atomicSub(&pending[p], 1u) == 1u) rel[nrel++] = p;
+                }
+                const unsigned long long q = warp_reserve(next_cnt, nrel);
+                for (unsigned k = 0; k < nrel; ++k) nxt[q + k] = rel[k];
+                if (!__any_sync(0xffffffffu, rn != 0)) break;
             }
         }
-        // Kahn: release predecessors; aggregate the pushes per warp
-        std::uint64_t r0 = 0;
-        std::uint32_t rn = 0;
-        if (valid) {
-            r0 = roff[j];
-            rn = rcnt[j];
-        }
-        for (;;) {
-            // process releases in rounds of at most 4 per lane
-            std::uint32_t rel[4];
-            unsigned nrel = 0;
-            while (rn && nrel < 4) {
-                const std::uint32_t p = rsrc[r0++];
-                --rn;
-                if (atomicSub(&pending[p], 1u) == 1u) rel[nrel++] = p;
-            }
-            const unsigned long long q = warp_reserve(next_count, nrel);
-            for (unsigned k = 0; k < nrel; ++k) next[q + k] = rel[k];
-            if (!__any_sync(0xffffffffu, rn != 0)) break;
-        }
+        g.sync();
+        done += ncur;
+        ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
+        ++level;
+        std::uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    if (g.thread_rank() == 0) {
+        stats[0] = static_cast<unsigned long long>(level);
+        stats[1] = done;
     }
 }
 
@@ -460,33 +556,54 @@ __global__ void k_source_write(const std::uint32_t* __restrict__ dest, std::uint
     }
 }
 
+int coop_grid(const void* fn, int num_sms, int* grid) {
+    int per_sm = 0;
+    MSC3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+    if (per_sm <= 0) return MSC3D_ERR_CUDA;
+    *grid = per_sm * num_sms;
+    return MSC3D_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------
 // host wrappers
 // ---------------------------------------------------------------------------------
 
-int launch_mark_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
-                        int id_width, std::uint8_t* marked, std::uint32_t* nodes,
-                        std::uint32_t* nid, unsigned int* bad, cudaStream_t s, int num_sms) {
+int launch_bfs_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
+                       int id_width, unsigned int* bitmap, std::uint32_t* frontier, unsigned int* bad,
+                       cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
     if (id_width == 4)
-        k_mark_sources<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
-            codes, d, static_cast<const std::uint32_t*>(src), n, marked, nodes, nid, bad);
+        k_bfs_sources<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            codes, d, static_cast<const std::uint32_t*>(src), n, bitmap, frontier, bad);
     else
-        k_mark_sources<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
-            codes, d, static_cast<const std::uint64_t*>(src), n, marked, nodes, nid, bad);
+        k_bfs_sources<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+            codes, d, static_cast<const std::uint64_t*>(src), n, bitmap, frontier, bad);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_bfs_level(const std::uint8_t* codes, const Dims& d, std::uint8_t* marked,
-                     std::uint32_t* nodes, std::uint64_t begin, std::uint64_t end,
-                     unsigned long long* tail, std::uint32_t* nid, cudaStream_t s, int num_sms) {
-    if (end <= begin) return MSC3D_OK;
-    k_bfs_level<<<grid_for(end - begin, num_sms, 32), kThreads, 0, s>>>(codes, d, marked, nodes,
-                                                                        begin, end, tail, nid);
+int launch_bfs_persistent(const std::uint8_t* codes, const Dims& d, unsigned int* bitmap,
+                          std::uint32_t* fa, std::uint32_t* fb, unsigned long long* cnt,
+                          unsigned long long* stats, cudaStream_t s, int num_sms) {
+    int grid = 0;
+    const int rc = coop_grid(reinterpret_cast<const void*>(k_bfs_persistent), num_sms, &grid);
+    if (rc != MSC3D_OK) return rc;
+    Dims dd = d;
+    const std::uint8_t* c = codes;
+    void* args[] = {&c, &dd, &bitmap, &fa, &fb, &cnt, &stats};
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs_persistent),
+                                               dim3(grid), dim3(kThreads), args, 0, s));
+    count_launch();
+    return MSC3D_OK;
+}
+
+int launch_marked_bytes(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                        std::uint64_t nwords, std::uint8_t* marked, cudaStream_t s, int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    k_marked_bytes<<<grid_for(nwords, num_sms), kThreads, 0, s>>>(codes, d, bitmap, nwords, marked);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -506,50 +623,39 @@ int launch_scatter_quad_rank(const void* list, std::uint64_t n, int id_width, co
     return MSC3D_OK;
 }
 
-int launch_node_succ(const std::uint8_t* codes, const Dims& d, const std::uint32_t* nodes,
-                     std::uint64_t m, const std::uint32_t* nid, const std::uint32_t* tmap,
-                     std::uint32_t* succ, std::uint8_t* outdeg, cudaStream_t s, int num_sms) {
-    if (m == 0) return MSC3D_OK;
-    k_node_succ<<<grid_for(m, num_sms), kThreads, 0, s>>>(codes, d, nodes, m, nid, tmap, succ, outdeg);
+int launch_junction_count(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                          std::uint64_t nwords, std::uint32_t* per_word, cudaStream_t s, int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    k_junction_count<<<grid_for(nwords, num_sms, 32), kThreads, 0, s>>>(codes, d, bitmap, nwords, per_word);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_chain_ptr(const std::uint32_t* succ, const std::uint8_t* outdeg, std::uint64_t m,
-                     std::uint64_t n_src, std::uint32_t* ptr, cudaStream_t s, int num_sms) {
-    if (m == 0) return MSC3D_OK;
-    k_chain_ptr<<<grid_for(m, num_sms), kThreads, 0, s>>>(succ, outdeg, m, n_src, ptr);
+int launch_junction_write(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
+                          std::uint64_t nwords, const std::uint64_t* off, std::uint32_t* jlist,
+                          std::uint32_t* jidx, cudaStream_t s, int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    k_junction_write<<<grid_for(nwords, num_sms, 32), kThreads, 0, s>>>(codes, d, bitmap, nwords, off,
+                                                                        jlist, jidx);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_junction_flags(const std::uint8_t* outdeg, std::uint64_t m, std::uint64_t n_src,
-                          std::uint32_t* flag, cudaStream_t s, int num_sms) {
-    if (m == 0) return MSC3D_OK;
-    k_junction_flags<<<grid_for(m, num_sms), kThreads, 0, s>>>(outdeg, m, n_src, flag);
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
-
-int launch_junction_write(const std::uint32_t* flag, const std::uint64_t* off, std::uint64_t m,
-                          std::uint32_t* jlist, std::uint32_t* jidx, cudaStream_t s, int num_sms) {
-    if (m == 0) return MSC3D_OK;
-    k_junction_write<<<grid_for(m, num_sms), kThreads, 0, s>>>(flag, off, m, jlist, jidx);
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
-
-int launch_origin_dests(const std::uint32_t* jlist, std::uint64_t n, const std::uint32_t* succ,
-                        const std::uint8_t* outdeg, const std::uint32_t* stop,
-                        const std::uint32_t* jidx, std::uint32_t* dest, std::uint32_t* pending,
-                        std::uint32_t* indeg, cudaStream_t s, int num_sms) {
+int launch_origin_dests(const std::uint8_t* codes, const Dims& d, const std::uint32_t* jlist,
+                        const void* srcs, int id_width, std::uint64_t n, const std::uint32_t* jidx,
+                        const std::uint32_t* tmap, std::uint32_t* dest, std::uint32_t* pending,
+                        std::uint32_t* indeg, unsigned int* flags, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
-    k_origin_dests<<<grid_for(n, num_sms), kThreads, 0, s>>>(jlist, n, succ, outdeg, stop, jidx,
-                                                            dest, pending, indeg);
+    if (id_width == 4)
+        k_origin_dests<std::uint32_t><<<grid_for(n, num_sms, 32), kThreads, 0, s>>>(
+            codes, d, jlist, static_cast<const std::uint32_t*>(srcs), n, jidx, tmap, dest, pending,
+            indeg, flags);
+    else
+        k_origin_dests<std::uint64_t><<<grid_for(n, num_sms, 32), kThreads, 0, s>>>(
+            codes, d, jlist, static_cast<const std::uint64_t*>(srcs), n, jidx, tmap, dest, pending,
+            indeg, flags);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -573,19 +679,20 @@ int launch_initial_frontier(const std::uint32_t* pending, std::uint64_t nj, std:
     return MSC3D_OK;
 }
 
-int launch_kahn_level(const std::uint32_t* frontier, std::uint64_t nf, const std::uint32_t* dest,
-                      std::uint64_t* poff, std::uint32_t* plen, std::uint32_t* pkey,
-                      std::uint64_t* pcnt, unsigned long long* ptop, std::uint64_t pcap,
-                      const std::uint64_t* roff, const std::uint32_t* rcnt, const std::uint32_t* rsrc,
-                      std::uint32_t* pending, std::uint32_t* next, unsigned long long* next_count,
-                      unsigned int* flags, cudaStream_t s, int num_sms) {
-    if (nf == 0) return MSC3D_OK;
+int launch_kahn_persistent(const std::uint32_t* dest, std::uint64_t* poff, std::uint32_t* plen,
+                           std::uint32_t* pkey, std::uint64_t* pcnt, unsigned long long* ptop,
+                           std::uint64_t pcap, const std::uint64_t* roff, const std::uint32_t* rcnt,
+                           const std::uint32_t* rsrc, std::uint32_t* pending, std::uint32_t* fa,
+                           std::uint32_t* fb, unsigned long long* cnt, unsigned int* flags,
+                           unsigned long long* stats, cudaStream_t s, int num_sms) {
+    int grid = 0;
+    const int rc = coop_grid(reinterpret_cast<const void*>(k_kahn_persistent), num_sms, &grid);
+    if (rc != MSC3D_OK) return rc;
     Pool pool{pkey, pcnt, ptop, pcap};
-    k_kahn_level<<<grid_for(nf, num_sms, 32), kThreads, 0, s>>>(frontier, nf, dest, poff, plen, pool,
-                                                              roff, rcnt, rsrc, pending, next,
-                                                              next_count, flags);
+    void* args[] = {&dest, &poff, &plen, &pool, &roff, &rcnt, &rsrc, &pending, &fa, &fb, &cnt, &flags, &stats};
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn_persistent),
+                                               dim3(grid), dim3(kThreads), args, 0, s));
     count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 

@@ -31,16 +31,29 @@ int gradient(msc3d_ctx* ctx, bool with_forests) {
         p3 = static_cast<std::uint32_t*>(ctx->ensure("parent3", d.n_cubes, 4));
         if (!p0 || !p3) return MSC3D_ERR_NOMEM;
     }
-    return msc3d_dev::launch_gradient(ctx->values, ctx->value_type, d, codes, p0, p3, ctx->stream);
+    // per-dimension critical counts come for free from the gradient kernel; stars
+    // with tied values are finished by the deferred slow-path kernel
+    auto* deferred = static_cast<std::uint32_t*>(ctx->ensure("deferred", d.n_verts, 4));
+    if (!deferred) return MSC3D_ERR_NOMEM;
+    ctx->crit_counts_valid = true;
+    return msc3d_dev::launch_gradient(ctx->values, ctx->value_type, d, codes, p0, p3, ctx->stream,
+                                      reinterpret_cast<unsigned long long*>(ctx->d_small + 40),
+                                      deferred, reinterpret_cast<unsigned long long*>(ctx->d_small + 44),
+                                      ctx->num_sms);
 }
 
 int critical(msc3d_ctx* ctx) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");
-    TRY(msc3d_dev::launch_critical_count(codes, d, ctx->d_small, ctx->stream, ctx->num_sms));
-    TRY(ctx->fetch_small(4));
     std::uint64_t n[4];
-    std::memcpy(n, ctx->h_small, sizeof n);
+    if (ctx->crit_counts_valid) {
+        TRY(ctx->fetch_small(44));
+        std::memcpy(n, ctx->h_small + 40, sizeof n);
+    } else {
+        TRY(msc3d_dev::launch_critical_count(codes, d, ctx->d_small, ctx->stream, ctx->num_sms));
+        TRY(ctx->fetch_small(4));
+        std::memcpy(n, ctx->h_small, sizeof n);
+    }
     const int w = ctx->id_width();
     void* outs[4];
     for (int k = 0; k < 4; ++k) {
@@ -157,35 +170,28 @@ int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");
     const int w = ctx->id_width();
-    auto* marked = static_cast<std::uint8_t*>(ctx->ensure("marked", d.n_cells, 1));
-    const std::uint64_t cap = 3 * d.n_verts;
-    auto* nodes = static_cast<std::uint32_t*>(ctx->ensure("nodes", cap, 4));
-    auto* nid = static_cast<std::uint32_t*>(ctx->ensure("nid", cap, 4));
-    if (!marked || !nodes || !nid) return MSC3D_ERR_NOMEM;
-    MSC3D_CUDA_TRY(cudaMemsetAsync(marked, 0, d.n_cells, ctx->stream));
-    auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 20);
-    auto* tail = reinterpret_cast<unsigned long long*>(ctx->d_small + 21);
-    MSC3D_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, ctx->stream));
-    ctx->h_small[21] = n_src;
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(tail, &ctx->h_small[21], 8, cudaMemcpyHostToDevice, ctx->stream));
-    TRY(msc3d_dev::launch_mark_sources(codes, d, d_sources, n_src, w, marked, nodes, nid, bad,
-                                       ctx->stream, ctx->num_sms));
-    TRY(ctx->fetch_small(21));
-    if (ctx->h_small[20] & 0xffffffffu) return MSC3D_ERR_INVALID;
-    std::uint64_t begin = 0, end = n_src;
-    int levels = 0;
-    while (begin < end) {
-        TRY(msc3d_dev::launch_bfs_level(codes, d, marked, nodes, begin, end, tail, nid, ctx->stream,
-                                        ctx->num_sms));
-        MSC3D_CUDA_TRY(cudaMemcpyAsync(&ctx->h_small[21], tail, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        begin = end;
-        end = ctx->h_small[21];
-        ++levels;
-    }
-    ctx->arrays["nodes"].count = end;
-    ctx->scalars["bfs_levels"] = levels;
-    ctx->scalars["dag_nodes"] = static_cast<std::int64_t>(end);
+    const std::uint64_t nde = 3 * d.n_verts;
+    const std::uint64_t nwords = (nde + 31) / 32;
+    auto* bitmap = static_cast<unsigned int*>(ctx->ensure("visited", nwords, 4));
+    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
+    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
+    if (!bitmap || !fa || !fb) return MSC3D_ERR_NOMEM;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(bitmap, 0, nwords * 4, ctx->stream));
+    auto* cnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 48);
+    auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 51);
+    auto* stats = reinterpret_cast<unsigned long long*>(ctx->d_small + 52);
+    ctx->h_small[48] = n_src;
+    ctx->h_small[49] = 0;
+    ctx->h_small[50] = 0;
+    ctx->h_small[51] = 0;
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(cnt, &ctx->h_small[48], 4 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(msc3d_dev::launch_bfs_sources(codes, d, d_sources, n_src, w, bitmap, fa, bad, ctx->stream,
+                                      ctx->num_sms));
+    TRY(msc3d_dev::launch_bfs_persistent(codes, d, bitmap, fa, fb, cnt, stats, ctx->stream, ctx->num_sms));
+    TRY(ctx->fetch_small(54));
+    if (ctx->h_small[51] & 0xffffffffu) return MSC3D_ERR_INVALID;  // saddle_graph.cpp:29-31
+    ctx->scalars["bfs_levels"] = static_cast<std::int64_t>(ctx->h_small[52]);
+    ctx->scalars["dag_nodes"] = static_cast<std::int64_t>(ctx->h_small[53]);
     ctx->scalars["dag_sources"] = static_cast<std::int64_t>(n_src);
     return MSC3D_OK;
 }
@@ -193,8 +199,13 @@ int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
 int marked_lists(msc3d_ctx* ctx) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");
-    const auto* marked = ctx->ptr<std::uint8_t>("marked");
     const int w = ctx->id_width();
+    auto* marked = static_cast<std::uint8_t*>(ctx->ensure("marked", d.n_cells, 1));
+    if (!marked) return MSC3D_ERR_NOMEM;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(marked, 0, d.n_cells, ctx->stream));
+    const std::uint64_t nwords = ctx->count("visited");
+    TRY(msc3d_dev::launch_marked_bytes(codes, d, ctx->ptr<unsigned int>("visited"), nwords, marked,
+                                       ctx->stream, ctx->num_sms));
     TRY(msc3d_dev::launch_marked_critical_count(codes, marked, d, ctx->d_small, ctx->stream, ctx->num_sms));
     TRY(ctx->fetch_small(4));
     const std::uint64_t n1 = ctx->h_small[1], n2 = ctx->h_small[2];
@@ -209,15 +220,16 @@ int marked_lists(msc3d_ctx* ctx) {
 
 int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources) {
     const int w = ctx->id_width();
-    const void* dsrc = nullptr;
     std::uint64_t n = 0;
     if (!host_sources) {
         TRY(critical(ctx));  // the codes may have changed since the last extraction
-        dsrc = ctx->ptr<void>("crit1");
         n = ctx->count("crit1");
+        void* p = ctx->ensure("sources", n, w);
+        if (!p) return MSC3D_ERR_NOMEM;
+        if (n) MSC3D_CUDA_TRY(cudaMemcpyAsync(p, ctx->ptr<void>("crit1"), n * w, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
-        // The reference skips duplicate sources (saddle_graph.cpp:37-41); node ids
-        // are assigned in ascending source order.
+        // The reference skips duplicate sources (saddle_graph.cpp:37-41); sources are
+        // kept in ascending order, which is also the order of one_saddles.
         if (w == 4) {
             auto v = sorted_unique(static_cast<const std::uint32_t*>(host_sources), n_sources);
             n = v.size();
@@ -233,9 +245,8 @@ int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources) {
             if (n) MSC3D_CUDA_TRY(cudaMemcpyAsync(p, v.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
             MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         }
-        dsrc = ctx->ptr<void>("sources");
     }
-    TRY(bfs(ctx, dsrc, n));
+    TRY(bfs(ctx, ctx->ptr<void>("sources"), n));
     return marked_lists(ctx);
 }
 
@@ -244,47 +255,32 @@ int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources) {
 // ---------------------------------------------------------------------------------
 namespace {
 
-// term_list: ascending 2-saddle cells whose positions key the count vectors.
-int dag_count(msc3d_ctx* ctx, const std::string& term_list) {
+// src_list: the BFS sources (ascending 1-saddle ids); term_list: ascending 2-saddle
+// ids whose positions key the count vectors.  Output ranks into those lists.
+int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& term_list) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");
     const int w = ctx->id_width();
     const cudaStream_t s = ctx->stream;
     const int sms = ctx->num_sms;
-    const std::uint64_t m = ctx->count("nodes");
-    const std::uint64_t n1 = static_cast<std::uint64_t>(ctx->scalars["dag_sources"]);
-    const auto* nodes = ctx->ptr<std::uint32_t>("nodes");
-    const auto* nid = ctx->ptr<std::uint32_t>("nid");
+    const std::uint64_t nde = 3 * d.n_verts;
+    const std::uint64_t nwords = (nde + 31) / 32;
+    const std::uint64_t n1 = ctx->count(src_list);
+    const auto* bitmap = ctx->ptr<unsigned int>("visited");
+    auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 26);  // [0] overflow [1] pool [2] cycle
+    MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 16, s));
 
-    auto* tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", 3 * d.n_verts, 4));
-    auto* succ = static_cast<std::uint32_t*>(ctx->ensure("succ", 4 * m, 4));
-    auto* outdeg = static_cast<std::uint8_t*>(ctx->ensure("outdeg", m, 1));
-    auto* stop = static_cast<std::uint32_t*>(ctx->ensure("stop", m, 4));
-    auto* jflag = static_cast<std::uint32_t*>(ctx->ensure("jflag", m, 4));
-    auto* joff = static_cast<std::uint64_t*>(ctx->ensure("joff", m, 8));
-    auto* jidx = static_cast<std::uint32_t*>(ctx->ensure("jidx", m, 4));
-    if (!tmap || !succ || !outdeg || !stop || !jflag || !joff || !jidx) return MSC3D_ERR_NOMEM;
+    auto* tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", nde, 4));
+    auto* jidx = static_cast<std::uint32_t*>(ctx->ensure("jidx", nde, 4));
+    auto* jcnt = static_cast<std::uint32_t*>(ctx->ensure("jcount", nwords, 4));
+    auto* joff = static_cast<std::uint64_t*>(ctx->ensure("joff", nwords, 8));
+    if (!tmap || !jidx || !jcnt || !joff) return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d,
                                             tmap, s, sms));
-    TRY(msc3d_dev::launch_node_succ(codes, d, nodes, m, nid, tmap, succ, outdeg, s, sms));
-    TRY(msc3d_dev::launch_chain_ptr(succ, outdeg, m, n1, stop, s, sms));
-    // chain contraction: pointer jumping to the chain stop
-    auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 24);
-    int rounds = 0;
-    while (m) {
-        MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, s));
-        TRY(msc3d_dev::launch_jump_round(stop, m, changed, s, sms));
-        TRY(ctx->fetch_small(25));
-        ++rounds;
-        if (!(ctx->h_small[24] & 0xffffffffu)) break;
-        if (rounds > 64) return MSC3D_ERR_RUNTIME;
-    }
-    ctx->scalars["chain_rounds"] = rounds;
-    // junctions (node order)
-    TRY(msc3d_dev::launch_junction_flags(outdeg, m, n1, jflag, s, sms));
-    TRY(msc3d_dev::scan_u32(jflag, m, joff, ctx->d_small, ctx->ws, s));
+    TRY(msc3d_dev::launch_junction_count(codes, d, bitmap, nwords, jcnt, s, sms));
+    TRY(msc3d_dev::scan_u32(jcnt, nwords, joff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(1));
-    const std::uint64_t nj = m ? ctx->h_small[0] : 0;
+    const std::uint64_t nj = ctx->h_small[0];
     ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
     auto* jdest = static_cast<std::uint32_t*>(ctx->ensure("jdest", 4 * nj, 4));
@@ -296,17 +292,20 @@ int dag_count(msc3d_ctx* ctx, const std::string& term_list) {
     auto* sdest = static_cast<std::uint32_t*>(ctx->ensure("sdest", 4 * n1, 4));
     auto* poff = static_cast<std::uint64_t*>(ctx->ensure("poff", nj, 8));
     auto* plen = static_cast<std::uint32_t*>(ctx->ensure("plen", nj, 4));
-    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nj, 4));
-    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nj, 4));
+    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
+    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
     if (!jlist || !jdest || !pending || !pending0 || !indeg || !roff || !cursor || !sdest || !poff ||
         !plen || !fa || !fb)
         return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_junction_write(jflag, joff, m, jlist, jidx, s, sms));
+    TRY(msc3d_dev::launch_junction_write(codes, d, bitmap, nwords, joff, jlist, jidx, s, sms));
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_origin_dests(jlist, nj, succ, outdeg, stop, jidx, jdest, pending, indeg, s, sms));
-    TRY(msc3d_dev::launch_origin_dests(nullptr, n1, succ, outdeg, stop, jidx, sdest, nullptr, nullptr, s, sms));
+    TRY(msc3d_dev::launch_origin_dests(codes, d, jlist, nullptr, w, nj, jidx, tmap, jdest, pending,
+                                       indeg, flags, s, sms));
+    TRY(msc3d_dev::launch_origin_dests(codes, d, nullptr, ctx->ptr<void>(src_list), w, n1, jidx, tmap,
+                                       sdest, nullptr, nullptr, flags, s, sms));
     TRY(msc3d_dev::scan_u32(indeg, nj, roff, ctx->d_small, ctx->ws, s));
-    TRY(ctx->fetch_small(1));
+    TRY(ctx->fetch_small(28));
+    if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle
     const std::uint64_t nrev = nj ? ctx->h_small[0] : 0;
     auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", nrev, 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
@@ -315,46 +314,36 @@ int dag_count(msc3d_ctx* ctx, const std::string& term_list) {
     if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nj * 4, cudaMemcpyDeviceToDevice, s));
 
     // Kahn over the junction graph, sinks first; grow the pool and rerun on overflow.
-    std::uint64_t pcap = std::max<std::uint64_t>(1u << 20, 2 * m);
-    auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 26);  // [0] overflow [1] pool
-    auto* ptop = reinterpret_cast<unsigned long long*>(ctx->d_small + 27);
-    auto* fcount = reinterpret_cast<unsigned long long*>(ctx->d_small + 28);
+    const std::uint64_t m = static_cast<std::uint64_t>(ctx->scalars["dag_nodes"]);
+    std::uint64_t pcap = std::max<std::uint64_t>(1u << 20, m + m / 2);
+    auto* ptop = reinterpret_cast<unsigned long long*>(ctx->d_small + 55);
+    auto* kcnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 56);   // 3 counters
+    auto* kstats = reinterpret_cast<unsigned long long*>(ctx->d_small + 59); // 2
     std::uint32_t* pkey = nullptr;
     std::uint64_t* pcnt = nullptr;
-    int levels = 0;
     for (int attempt = 0;; ++attempt) {
         pkey = static_cast<std::uint32_t*>(ctx->ensure("pool_key", pcap, 4));
         pcnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
         if (!pkey || !pcnt) return MSC3D_ERR_NOMEM;
-        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 26, 0, 3 * 8, s));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 55, 0, 6 * 8, s));
         if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nj * 4, cudaMemcpyDeviceToDevice, s));
-        TRY(msc3d_dev::launch_initial_frontier(pending, nj, fa, fcount, s, sms));
-        TRY(ctx->fetch_small(29));
-        std::uint64_t nf = ctx->h_small[28], done = 0;
-        std::uint32_t* cur = fa;
-        std::uint32_t* nxt = fb;
-        levels = 0;
-        while (nf) {
-            MSC3D_CUDA_TRY(cudaMemsetAsync(fcount, 0, 8, s));
-            TRY(msc3d_dev::launch_kahn_level(cur, nf, jdest, poff, plen, pkey, pcnt, ptop, pcap, roff,
-                                             indeg, rsrc, pending, nxt, fcount, flags, s, sms));
-            TRY(ctx->fetch_small(29));
-            done += nf;
-            nf = ctx->h_small[28];
-            std::swap(cur, nxt);
-            ++levels;
-        }
+        TRY(msc3d_dev::launch_initial_frontier(pending, nj, fa, kcnt, s, sms));
+        if (nj)
+            TRY(msc3d_dev::launch_kahn_persistent(jdest, poff, plen, pkey, pcnt, ptop, pcap, roff, indeg,
+                                                  rsrc, pending, fa, fb, kcnt, flags, kstats, s, sms));
+        TRY(ctx->fetch_small(61));
         const unsigned int pool_full = static_cast<unsigned int>(ctx->h_small[26] >> 32);
         if (pool_full) {
             if (attempt > 8) return MSC3D_ERR_NOMEM;
-            pcap = std::max<std::uint64_t>(2 * pcap, ctx->h_small[27] + ctx->h_small[27] / 4);
+            pcap = std::max<std::uint64_t>(2 * pcap, ctx->h_small[55] + ctx->h_small[55] / 4);
             continue;
         }
-        if (done != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
+        if (nj && ctx->h_small[60] != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
         break;
     }
-    ctx->scalars["count_levels"] = levels;
-    ctx->scalars["pool_entries"] = static_cast<std::int64_t>(ctx->h_small[27]);
+    ctx->scalars["count_levels"] = nj ? static_cast<std::int64_t>(ctx->h_small[59]) : 0;
+    ctx->scalars["pool_entries"] = static_cast<std::int64_t>(ctx->h_small[55]);
 
     // 1-saddles: lengths, offsets, write
     auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
@@ -369,20 +358,19 @@ int dag_count(msc3d_ctx* ctx, const std::string& term_list) {
     auto* o2 = static_cast<std::uint32_t*>(ctx->ensure("ss_two_rank", nout, 4));
     auto* oc = static_cast<std::uint64_t*>(ctx->ensure("ss_paths", nout, 8));
     if (!o1 || !o2 || !oc) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_source_write(sdest, n1, poff, plen, pkey, pcnt, soff, o1, o2, oc, flags, s, sms));
-    return MSC3D_OK;
+    return msc3d_dev::launch_source_write(sdest, n1, poff, plen, pkey, pcnt, soff, o1, o2, oc, flags, s, sms);
 }
 
 }  // namespace
 
 int count(msc3d_ctx* ctx) {
-    TRY(dag_count(ctx, "two_saddles"));
+    TRY(dag_count(ctx, "sources", "two_saddles"));
     const int w = ctx->id_width();
     const std::uint64_t n = ctx->count("ss_paths");
     void* a = ctx->ensure("ss_one", n, w);
     void* b = ctx->ensure("ss_two", n, w);
     if (!a || !b) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_gather_ids(ctx->ptr<void>("one_saddles"), ctx->ptr<std::uint32_t>("ss_one_rank"),
+    TRY(msc3d_dev::launch_gather_ids(ctx->ptr<void>("sources"), ctx->ptr<std::uint32_t>("ss_one_rank"),
                                      n, w, a, ctx->stream, ctx->num_sms));
     return msc3d_dev::launch_gather_ids(ctx->ptr<void>("two_saddles"), ctx->ptr<std::uint32_t>("ss_two_rank"),
                                         n, w, b, ctx->stream, ctx->num_sms);
@@ -474,7 +462,7 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
     clk.mark(4, s);
 
     // [counting]
-    TRY(dag_count(ctx, "crit2"));
+    TRY(dag_count(ctx, "crit1", "crit2"));
     clk.mark(5, s);
 
     // ---- assembly (untimed in the reference's StageTimings) ----
@@ -482,6 +470,9 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
     const std::uint64_t na = c0 ? ctx->h_small[32] : 0;  // min->1s arcs
     const std::uint64_t nc = c2 ? ctx->h_small[33] : 0;  // 2s->max arcs
     const std::uint64_t nb = ctx->count("ss_paths");       // 1s->2s arcs
+    ctx->scalars["arcs_min"] = static_cast<std::int64_t>(na);
+    ctx->scalars["arcs_ss"] = static_cast<std::int64_t>(nb);
+    ctx->scalars["arcs_max"] = static_cast<std::int64_t>(nc);
     void* cp_cell = ctx->ensure("cp_cell", ncp, w);
     auto* cp_index = static_cast<std::uint8_t*>(ctx->ensure("cp_index", ncp, 1));
     auto* asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", na + nb + nc, 4));

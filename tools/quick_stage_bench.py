@@ -38,4 +38,4 @@ t = timeit(lambda: ctx.roots(0), stream, iters=2, warm=1)
 print(f"roots0 sync-doubling: {t:.3f} ms rounds {ctx.scalar('rounds0')}", flush=True)
 t = timeit(lambda: ctx.compute(m.OPT_SEGMENTATION), stream, iters=3, warm=1)
 ms = ctx.compute(m.OPT_SEGMENTATION)
-print(f"compute: {t:.3f} ms  stages {['%.3f' % x for x in ms]}  levels bfs={ctx.scalar('bfs_levels')} count={ctx.scalar('count_levels')} chain={ctx.scalar('chain_rounds')} nodes={ctx.scalar('dag_nodes')} junc={ctx.scalar('junctions')} pool={ctx.scalar('pool_entries')} arcs={ctx.array_info('arc_src')[1]}", flush=True)
+print(f"compute: {t:.3f} ms  stages {['%.3f' % x for x in ms]}  levels bfs={ctx.scalar('bfs_levels')} count={ctx.scalar('count_levels')} nodes={ctx.scalar('dag_nodes')} junc={ctx.scalar('junctions')} pool={ctx.scalar('pool_entries')} arcs={ctx.array_info('arc_src')[1]}", flush=True)
