@@ -1,0 +1,3 @@
+// Forwards to the B200 drop-in API (same declarations as the reference's msc3d/serialize.hpp).
+#pragma once
+#include "msc3d/api.hpp"

@@ -13,12 +13,13 @@
 //     pop_min = the cell of least rank mask.
 //
 // Fast path (registers only, no per-step memory chains): the star's vertices are
-// compacted with __fns into K registers (K = 8/16/32, chosen per warp), sorted by a
-// bitonic network, ranked; every cell's rank mask is built from its facets' masks
-// (unrolled over the 26 slots, constant indices); the cells are sorted by mask with
-// a second network of u32 keys (mask << 5 | slot); the expansion then pops minima
-// by position.  Vertices are bucketed by star size inside the CTA first, so the
-// warps running the sort networks are size-homogeneous.
+// compacted into K registers, sorted by a bitonic network, ranked; every cell's rank
+// mask is built from its facets' masks (unrolled over the 26 slots, constant
+// indices); the cells are sorted by mask with a second network of u32 keys
+// (mask << 5 | slot); the expansion then pops minima by position.  The tile kernel
+// runs stars of <= 8 cells (K = 8); larger stars are appended to two work lists
+// processed by K = 16 / K = 32 kernels, whose register budgets do not cap the tile
+// kernel's occupancy and whose warps are size-homogeneous.
 //
 // Stars containing two equal values go to the slow path (k_gradient_deferred),
 // which keeps the reference's general multiset-then-ids key (value thermometer
@@ -280,19 +281,21 @@ __device__ __forceinline__ void ce_u32(std::uint32_t& a, std::uint32_t& b, bool 
 
 // Fast path for one star with n <= K vertices and distinct values.  Returns false
 // (nothing written) when two star values tie.
-template <int K, typename T>
-__device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
+template <int K, typename T, typename Val>
+__device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
                                           const std::uint32_t* fac, const std::uint32_t* cof,
-                                          std::uint32_t* mscratch, StarWriter& w) {
+                                          std::uint32_t* mscratch, int mstride, StarWriter& w) {
     using KT = typename KeyOf<T>::type;
     KT key[K];
     std::uint32_t slot[K];
+    std::uint32_t rest = S;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
         if (p < n) {
-            const int s = static_cast<int>(__fns(S, 0, p + 1));
+            const int s = __ffs(rest) - 1;
+            rest &= rest - 1;
             slot[p] = static_cast<std::uint32_t>(s);
-            key[p] = ord_key(base[tile_off(s)]);
+            key[p] = ord_key(val(s));
         } else {
             slot[p] = 31u;
             key[p] = static_cast<KT>(~static_cast<KT>(0));
@@ -323,7 +326,7 @@ __device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
 #pragma unroll
     for (int t = 0; t < 27; ++t) M[t] = 0;
     M[13] = 1u << (n - 1);
-    mscratch[13 * NT] = M[13];
+    mscratch[13 * mstride] = M[13];
 #pragma unroll
     for (int dim = 1; dim <= 3; ++dim)
 #pragma unroll
@@ -337,7 +340,7 @@ __device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
             }
             if ((S >> t) & 1u) {
                 m |= 1u << rank.get(t);
-                mscratch[t * NT] = m;
+                mscratch[t * mstride] = m;
             }
             M[t] = m;
         }
@@ -345,7 +348,7 @@ __device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
     std::uint32_t ck[K];
 #pragma unroll
     for (int p = 0; p < K; ++p)
-        ck[p] = p < n ? ((mscratch[slot[p] * NT] << 5) | slot[p]) : 0xffffffffu;
+        ck[p] = p < n ? ((mscratch[slot[p] * mstride] << 5) | slot[p]) : 0xffffffffu;
 #pragma unroll
     for (int k = 2; k <= K; k <<= 1)
 #pragma unroll
@@ -374,19 +377,21 @@ __device__ __forceinline__ bool star_fast(const T* base, std::uint32_t S, int n,
     return true;
 }
 
+// Work lists handed from the tile kernel to the size-specialised kernels:
+// [0] stars of 9..16 cells, [1] 17..27 cells, [2] stars with tied values.
+struct StarLists {
+    std::uint32_t* list[3];
+    unsigned long long* count;  // 3 counters
+};
+
 template <typename T>
 __global__ void __launch_bounds__(NT)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
-           unsigned long long* __restrict__ crit_totals, std::uint32_t* __restrict__ deferred,
-           unsigned long long* __restrict__ n_deferred) {
+           unsigned long long* __restrict__ crit_totals, StarLists lists) {
     __shared__ T tile[SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
-    __shared__ std::uint32_t s_S[NT];
-    __shared__ std::uint16_t s_order[NT];
-    __shared__ std::uint32_t s_hist[32];
-    __shared__ std::uint32_t s_total;
     __shared__ unsigned long long s_crit[4];
     __shared__ std::uint32_t s_M[27 * NT];
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
@@ -396,7 +401,6 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         s_cell[tid] = static_cast<std::int32_t>(c_slot.off[tid][0] + c_slot.off[tid][1] * d.ex +
                                                 c_slot.off[tid][2] * d.exy);
     }
-    if (tid < 32) s_hist[tid] = 0;
     if (tid < 4) s_crit[tid] = 0;
     const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * TX - 1;
     const std::int64_t y0 = static_cast<std::int64_t>(blockIdx.y) * TY - 1;
@@ -465,45 +469,25 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             ncrit = w.ncrit;
         }
     }
-    // ---- bucket the remaining stars by size (counting sort in shared memory) ---------
-    const int n_own = S ? __popc(S) : 0;
-    s_S[tid] = S;
-    if (n_own) atomicAdd(&s_hist[n_own], 1u);
-    __syncthreads();
-    if (tid < 32) {
-        const std::uint32_t v = s_hist[tid];
-        std::uint32_t incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (tid >= o) incl += y;
-        }
-        s_hist[tid] = incl - v;
-        if (tid == 31) s_total = incl;
-    }
-    __syncthreads();
-    if (n_own) s_order[atomicAdd(&s_hist[n_own], 1u)] = static_cast<std::uint16_t>(tid);
-    __syncthreads();
-    const int nwork = static_cast<int>(s_total);
-
-    // ---- phase 2: size-homogeneous warps run the fast path ----------------------------
-    if (tid < nwork) {
-        const int lid = s_order[tid];
-        const std::uint32_t Sv = s_S[lid];
-        const int n = __popc(Sv);
-        StarWriter w = writer_for(lid);
-        const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
+    // ---- stars of 3..8 cells: register fast path here; larger stars go to the
+    //      size-specialised list kernels (their registers do not limit this one) ----
+    if (S) {
+        const int n = __popc(S);
+        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
+        StarWriter w = writer_for(tid);
         const T* base = &tile[lz + 1][ly + 1][lx + 1];
-        const unsigned active = __activemask();
-        const int kmax = static_cast<int>(__reduce_max_sync(active, static_cast<unsigned>(n)));
-        bool ok;
-        if (kmax <= 8) ok = star_fast<8>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
-        else if (kmax <= 16) ok = star_fast<16>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
-        else ok = star_fast<32>(base, Sv, n, s_fac, s_cof, &s_M[tid], w);
-        if (!ok) {
-            const unsigned long long at = atomicAdd(n_deferred, 1ull);
-            deferred[at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+        const unsigned long long vi = static_cast<unsigned long long>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+        if (n <= 8) {
+            if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, S, n, s_fac, s_cof, &s_M[tid], NT, w)) {
+                const unsigned long long at = atomicAdd(&lists.count[2], 1ull);
+                lists.list[2][at] = static_cast<std::uint32_t>(vi);
+            }
+            ncrit += w.ncrit;
+        } else {
+            const int which = n <= 16 ? 0 : 1;
+            const unsigned long long at = atomicAdd(&lists.count[which], 1ull);
+            lists.list[which][at] = static_cast<std::uint32_t>(vi);
         }
-        ncrit += w.ncrit;
     }
     if (crit_totals) {
         std::uint64_t v = ncrit;
@@ -518,6 +502,85 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     }
 }
 
+// Stars of 9..27 cells, one thread per listed vertex (values from global memory,
+// L1/L2-resident neighbourhoods).  Same register fast path with a wider network;
+// tied stars are forwarded to the slow path list.
+template <int K, typename T>
+__global__ void __launch_bounds__(128)
+k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
+                std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
+                unsigned long long* __restrict__ crit_totals, StarLists lists, int which) {
+    __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_fac[27], s_cof[27];
+    __shared__ std::uint32_t s_M[27 * 128];
+    __shared__ unsigned long long s_crit[4];
+    if (threadIdx.x < 27) {
+        s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
+        s_cof[threadIdx.x] = c_slot.cofacet[threadIdx.x];
+        s_cell[threadIdx.x] = static_cast<std::int32_t>(
+            c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
+    }
+    if (threadIdx.x < 4) s_crit[threadIdx.x] = 0;
+    __syncthreads();
+    const std::uint64_t nl = *reinterpret_cast<volatile unsigned long long*>(&lists.count[which]);
+    std::uint64_t ncrit = 0;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < nl;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t vi = lists.list[which][i];
+        const std::uint64_t r = d.fnx.div(vi), vx = vi - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
+        StarWriter w;
+        w.vx = static_cast<std::int64_t>(vx);
+        w.vy = static_cast<std::int64_t>(vy);
+        w.vz = static_cast<std::int64_t>(vz);
+        std::uint32_t inr = kAll;
+        if (w.vx == 0) inr &= ~kXM;
+        if (w.vx == d.nx - 1) inr &= ~kXP;
+        if (w.vy == 0) inr &= ~kYM;
+        if (w.vy == d.ny - 1) inr &= ~kYP;
+        if (w.vz == 0) inr &= ~kZM;
+        if (w.vz == d.nz - 1) inr &= ~kZP;
+        w.inr = inr;
+        w.d = d;
+        w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
+        w.cell_off = s_cell;
+        w.parent0 = parent0;
+        w.parent3 = parent3;
+        w.ncrit = 0;
+        const T* centre = f + vi;
+        const std::int64_t sy = d.nx, sz = d.nx * d.ny;
+        auto val = [&](int t) {
+            const int z = (t * 57) >> 9, rr = t - 9 * z, y = (rr * 11) >> 5, x = rr - 3 * y;
+            return centre[(x - 1) + (y - 1) * sy + (z - 1) * sz];
+        };
+        const T fv = centre[0];
+        std::uint32_t below = kCentre;
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            if (t == 13) continue;
+            if (!((inr >> t) & 1u)) continue;
+            const T u = centre[slot_off(t, 0) + slot_off(t, 1) * sy + slot_off(t, 2) * sz];
+            if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+        }
+        std::uint32_t S = below & inr;
+        S &= facets_present(S);
+        S &= facets_present(S);
+        if (!star_fast<K, T>(val, S, __popc(S), s_fac, s_cof, &s_M[threadIdx.x], 128, w)) {
+            const unsigned long long at = atomicAdd(&lists.count[2], 1ull);
+            lists.list[2][at] = vi;
+        }
+        ncrit += w.ncrit;
+    }
+    std::uint64_t v = ncrit;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v)
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long c = (v >> (16 * k)) & 0xffffu;
+            if (c) atomicAdd(&s_crit[k], c);
+        }
+    __syncthreads();
+    if (threadIdx.x < 4 && s_crit[threadIdx.x]) atomicAdd(&crit_totals[threadIdx.x], s_crit[threadIdx.x]);
+}
+
 // Slow path: stars with equal values.  The general key of the reference
 // (value multiset, then vertex ids), one thread per deferred vertex, values read
 // straight from global memory.
@@ -525,8 +588,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                     std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
-                    const std::uint32_t* __restrict__ list, const unsigned long long* __restrict__ n_list,
-                    unsigned long long* __restrict__ crit_totals) {
+                    StarLists lists, unsigned long long* __restrict__ crit_totals) {
     __shared__ std::int32_t s_cell[27];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     if (threadIdx.x < 27) {
@@ -536,10 +598,10 @@ k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ 
             c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
     }
     __syncthreads();
-    const std::uint64_t nl = *n_list;
+    const std::uint64_t nl = *reinterpret_cast<volatile unsigned long long*>(&lists.count[2]);
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < nl;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const std::uint32_t vi = list[i];
+        const std::uint32_t vi = lists.list[2][i];
         const std::uint64_t r = d.fnx.div(vi), vx = vi - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
         StarWriter w;
         w.vx = static_cast<std::int64_t>(vx);
@@ -629,33 +691,35 @@ int upload_gradient_tables(int device) {
 
 int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
                     std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
-                    unsigned long long* crit_totals, std::uint32_t* deferred,
-                    unsigned long long* n_deferred, int num_sms) {
+                    unsigned long long* crit_totals, std::uint32_t* const lists3[3],
+                    unsigned long long* list_counts, int num_sms) {
     int dev = 0;
     MSC3D_CUDA_TRY(cudaGetDevice(&dev));
     const int rc = upload_gradient_tables(dev);
     if (rc != MSC3D_OK) return rc;
     MSC3D_CUDA_TRY(cudaMemsetAsync(crit_totals, 0, 32, stream));
-    MSC3D_CUDA_TRY(cudaMemsetAsync(n_deferred, 0, 8, stream));
+    MSC3D_CUDA_TRY(cudaMemsetAsync(list_counts, 0, 24, stream));
+    StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
     const dim3 block(TX, TY, TZ);
     const dim3 grid(static_cast<unsigned>((d.nx + TX - 1) / TX),
                     static_cast<unsigned>((d.ny + TY - 1) / TY),
                     static_cast<unsigned>((d.nz + TZ - 1) / TZ));
+    const unsigned lgrid = static_cast<unsigned>(16 * num_sms);
     const unsigned dgrid = static_cast<unsigned>(4 * num_sms);
     if (value_type == MSC3D_VALUE_F64) {
-        k_gradient<double><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d, codes,
-                                                        parent0, parent3, crit_totals, deferred, n_deferred);
-        k_gradient_deferred<double><<<dgrid, 128, 0, stream>>>(static_cast<const double*>(values), d, codes,
-                                                              parent0, parent3, deferred, n_deferred,
-                                                              crit_totals);
+        const double* v = static_cast<const double*>(values);
+        k_gradient<double><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists);
+        k_gradient_list<16, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
+        k_gradient_list<32, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
+        k_gradient_deferred<double><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
     } else {
-        k_gradient<float><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes,
-                                                      parent0, parent3, crit_totals, deferred, n_deferred);
-        k_gradient_deferred<float><<<dgrid, 128, 0, stream>>>(static_cast<const float*>(values), d, codes,
-                                                            parent0, parent3, deferred, n_deferred,
-                                                            crit_totals);
+        const float* v = static_cast<const float*>(values);
+        k_gradient<float><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists);
+        k_gradient_list<16, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
+        k_gradient_list<32, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
+        k_gradient_deferred<float><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
     }
-    count_launch(2);
+    count_launch(4);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }

@@ -30,8 +30,8 @@ struct Workspace {
 // gradient.cu
 int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
                     std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
-                    unsigned long long* crit_totals, std::uint32_t* deferred,
-                    unsigned long long* n_deferred, int num_sms);
+                    unsigned long long* crit_totals, std::uint32_t* const lists3[3],
+                    unsigned long long* list_counts, int num_sms);
 
 // critical.cu
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,

@@ -96,17 +96,31 @@ __device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* c
     return base + incl - n;
 }
 
+// Successors at fixed positions 2*b + (sign > 0) over the three axes b (the odd axis
+// of the edge never contributes): ascending position == cofacet order, and all
+// accesses use compile-time indices (no local-memory arrays).
 struct Succ {
-    C3 c[4];
-    std::uint32_t term;  // bit k: successor k is a terminal 2-saddle (quad)
-    int n;
+    C3 c[6];
+    std::uint32_t valid;  // bit k: position k holds a successor
+    std::uint32_t term;   // bit k: that successor is a terminal 2-saddle (quad)
+    __device__ __forceinline__ int n() const { return __popc(valid); }
+    // the successor at the lowest valid position (valid != 0)
+    __device__ __forceinline__ C3 first() const {
+        const int k = __ffs(valid) - 1;
+        C3 r = c[0];
+#pragma unroll
+        for (int j = 1; j < 6; ++j)
+            if (k == j) r = c[j];
+        return r;
+    }
+    __device__ __forceinline__ bool first_is_term() const { return (term >> (__ffs(valid) - 1)) & 1u; }
 };
 
 // saddle_graph.cpp:10-24 on coordinates (no id <-> coordinate divisions).
 __device__ __forceinline__ Succ successors(const std::uint8_t* __restrict__ codes, const Dims& d,
                                            const C3& e) {
     Succ s;
-    s.n = 0;
+    s.valid = 0;
     s.term = 0;
     const std::int32_t co[3] = {e.x, e.y, e.z};
     const std::int64_t ext[3] = {d.ex, d.ey, d.ez};
@@ -114,25 +128,31 @@ __device__ __forceinline__ Succ successors(const std::uint8_t* __restrict__ code
     const std::int64_t step[3] = {1, d.ex, d.exy};
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-        if (co[b] & 1) continue;
 #pragma unroll
-        for (int sgn = -1; sgn <= 1; sgn += 2) {
-            if (sgn < 0 ? co[b] == 0 : co[b] == ext[b] - 1) continue;
-            const std::uint8_t k = codes[eid + sgn * step[b]];
+        for (int h = 0; h < 2; ++h) {
+            const int k = 2 * b + h, sgn = h ? 1 : -1;
+            s.c[k] = e;
+            if (co[b] & 1) continue;
+            if (h == 0 ? co[b] == 0 : co[b] == ext[b] - 1) continue;
+            const std::uint8_t code = codes[eid + sgn * step[b]];
             C3 q = e;
             if (b == 0) q.x += sgn;
             else if (b == 1) q.y += sgn;
             else q.z += sgn;
-            if (k == kCritical) {
-                s.term |= 1u << s.n;
-                s.c[s.n++] = q;
-            } else if (paired_with_facet(k)) {
-                const int dir = k - kFacetBase, ax = dir >> 1, ps = (dir & 1) ? 1 : -1;
+            if (code == kCritical) {
+                s.valid |= 1u << k;
+                s.term |= 1u << k;
+                s.c[k] = q;
+            } else if (paired_with_facet(code)) {
+                const int dir = code - kFacetBase, ax = dir >> 1, ps = (dir & 1) ? 1 : -1;
                 C3 o = q;
                 if (ax == 0) o.x += ps;
                 else if (ax == 1) o.y += ps;
                 else o.z += ps;
-                if (o.x != e.x || o.y != e.y || o.z != e.z) s.c[s.n++] = o;
+                if (o.x != e.x || o.y != e.y || o.z != e.z) {
+                    s.valid |= 1u << k;
+                    s.c[k] = o;
+                }
             }
         }
     }
@@ -180,21 +200,25 @@ k_bfs_persistent(const std::uint8_t* __restrict__ codes, Dims d, unsigned int* _
         for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
              base < ncur; base += stride) {
             const std::uint64_t j = base + (threadIdx.x & 31);
-            std::uint32_t won[4];
-            unsigned nwon = 0;
+            std::uint32_t de[6];
+            std::uint32_t won = 0;
             if (j < ncur) {
                 const Succ s = successors(codes, d, edge_coord(d, cur[j]));
-                for (int k = 0; k < s.n; ++k) {
-                    if ((s.term >> k) & 1u) continue;
-                    const std::uint32_t de = edge_dense(d, s.c[k]);
-                    const unsigned bit = 1u << (de & 31);
-                    if (bitmap[de >> 5] & bit) continue;  // cheap pre-check
-                    if (atomicOr(&bitmap[de >> 5], bit) & bit) continue;
-                    won[nwon++] = de;
+                const std::uint32_t edges = s.valid & ~s.term;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    de[k] = edge_dense(d, s.c[k]);
+                    if (!((edges >> k) & 1u)) continue;
+                    const unsigned bit = 1u << (de[k] & 31);
+                    if (bitmap[de[k] >> 5] & bit) continue;  // cheap pre-check
+                    if (atomicOr(&bitmap[de[k] >> 5], bit) & bit) continue;
+                    won |= 1u << k;
                 }
             }
-            const unsigned long long at = warp_reserve(next_cnt, nwon);
-            for (unsigned k = 0; k < nwon; ++k) nxt[at + k] = won[k];
+            const unsigned long long at = warp_reserve(next_cnt, __popc(won));
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if ((won >> k) & 1u) nxt[at + __popc(won & ((1u << k) - 1))] = de[k];
         }
         g.sync();
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
@@ -227,7 +251,8 @@ __global__ void k_marked_bytes(const std::uint8_t* __restrict__ codes, Dims d,
             const std::uint8_t k = codes[id];
             if (k != kCritical) marked[partner_of(d, id, k)] = 1;
             const Succ s = successors(codes, d, c);
-            for (int q = 0; q < s.n; ++q)
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
                 if ((s.term >> q) & 1u) marked[cell_id(d, s.c[q])] = 1;
         }
     }
@@ -253,7 +278,7 @@ __global__ void k_junction_count(const std::uint8_t* __restrict__ codes, Dims d,
             bits &= bits - 1;
             const C3 c = edge_coord(d, static_cast<std::uint32_t>(w * 32 + b));
             if (codes[cell_id(d, c)] == kCritical) continue;
-            n += successors(codes, d, c).n > 1;
+            n += successors(codes, d, c).n() > 1;
         }
         per_word[w] = n;
     }
@@ -272,7 +297,7 @@ __global__ void k_junction_write(const std::uint8_t* __restrict__ codes, Dims d,
             const std::uint32_t de = static_cast<std::uint32_t>(w * 32 + b);
             const C3 c = edge_coord(d, de);
             if (codes[cell_id(d, c)] == kCritical) continue;
-            if (successors(codes, d, c).n > 1) {
+            if (successors(codes, d, c).n() > 1) {
                 jlist[at] = de;
                 jidx[de] = static_cast<std::uint32_t>(at);
                 ++at;
@@ -298,7 +323,10 @@ __global__ void k_origin_dests(const std::uint8_t* __restrict__ codes, Dims d,
         const Succ s = successors(codes, d, o);
         std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
         std::uint32_t pend = 0;
-        for (int b = 0; b < s.n; ++b) {
+        int nd = 0;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+            if (!((s.valid >> b) & 1u)) continue;
             std::uint32_t t;
             if ((s.term >> b) & 1u) {
                 t = kTerm | tmap[quad_dense(d, s.c[b])];
@@ -308,23 +336,29 @@ __global__ void k_origin_dests(const std::uint8_t* __restrict__ codes, Dims d,
                 t = kNone;
                 for (std::uint64_t steps = 0;; ++steps) {
                     const Succ nx = successors(codes, d, cur);
-                    if (nx.n > 1) {
+                    const int nn = nx.n();
+                    if (nn > 1) {
                         t = jidx[edge_dense(d, cur)];
                         break;
                     }
-                    if (nx.n == 0) break;
-                    if (nx.term & 1u) {
-                        t = kTerm | tmap[quad_dense(d, nx.c[0])];
+                    if (nn == 0) break;
+                    if (nx.first_is_term()) {
+                        t = kTerm | tmap[quad_dense(d, nx.first())];
                         break;
                     }
-                    cur = nx.c[0];
+                    cur = nx.first();
                     if (steps > d.n_cells) {
                         flags[2] = 1u;  // cycle: invalid gradient (saddle_graph.cpp:173-174)
                         break;
                     }
                 }
             }
-            dd[b] = t;
+            // append in branch order (constant-index selects, no local memory)
+            dd[0] = nd == 0 ? t : dd[0];
+            dd[1] = nd == 1 ? t : dd[1];
+            dd[2] = nd == 2 ? t : dd[2];
+            dd[3] = nd == 3 ? t : dd[3];
+            ++nd;
             if (!(t & kTerm)) {
                 ++pend;
                 if (indeg) atomicAdd(&indeg[t], 1u);
@@ -380,13 +414,12 @@ __device__ __forceinline__ bool mul_ovf(std::uint64_t a, std::uint64_t b, std::u
 
 // K-way merge of up to 4 sorted (key, count) lists scaled by mult.  A terminal
 // branch is a one-element list.  With okey == nullptr only the length is counted.
-struct MergeIn {
+struct MergeIn {  // slot b = branch b of the origin (empty when len[b] == 0)
     const std::uint32_t* key[4];
     const std::uint64_t* cnt[4];
     std::uint32_t len[4];
     std::uint32_t one_key[4];
     std::uint64_t mult[4];
-    int n;
 };
 
 __device__ __forceinline__ std::uint32_t kway_merge(const MergeIn& in, std::uint32_t* okey,
@@ -398,7 +431,7 @@ __device__ __forceinline__ std::uint32_t kway_merge(const MergeIn& in, std::uint
         bool any = false;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            if (b >= in.n || pos[b] >= in.len[b]) continue;
+            if (pos[b] >= in.len[b]) continue;
             const std::uint32_t kk = in.key[b] ? in.key[b][pos[b]] : in.one_key[b];
             if (!any || kk < best) best = kk;
             any = true;
@@ -408,7 +441,7 @@ __device__ __forceinline__ std::uint32_t kway_merge(const MergeIn& in, std::uint
         bool o = false;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            if (b >= in.n || pos[b] >= in.len[b]) continue;
+            if (pos[b] >= in.len[b]) continue;
             const std::uint32_t kk = in.key[b] ? in.key[b][pos[b]] : in.one_key[b];
             if (kk != best) continue;
             const std::uint64_t c = in.cnt[b] ? in.cnt[b][pos[b]] : 1ull;
@@ -431,25 +464,23 @@ __device__ __forceinline__ void gather_inputs(const std::uint32_t* __restrict__ 
                                               const std::uint64_t* __restrict__ poff,
                                               const std::uint32_t* __restrict__ plen, const Pool& pool,
                                               MergeIn& in) {
-    in.n = 0;
     const uint4 d4 = reinterpret_cast<const uint4*>(dest)[i];
     const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
         const std::uint32_t t = dd[b];
+        in.mult[b] = 1;
+        in.one_key[b] = t & ~kTerm;
+        in.key[b] = nullptr;
+        in.cnt[b] = nullptr;
+        in.len[b] = 0;
         if (t == kNone) continue;
-        const int k = in.n++;
-        in.mult[k] = 1;
         if (t & kTerm) {
-            in.key[k] = nullptr;
-            in.cnt[k] = nullptr;
-            in.len[k] = 1;
-            in.one_key[k] = t & ~kTerm;
+            in.len[b] = 1;
         } else {
-            in.key[k] = pool.key + poff[t];
-            in.cnt[k] = pool.cnt + poff[t];
-            in.len[k] = plen[t];
-            in.one_key[k] = 0;
+            in.key[b] = pool.key + poff[t];
+            in.cnt[b] = pool.cnt + poff[t];
+            in.len[b] = plen[t];
         }
     }
 }
@@ -480,7 +511,8 @@ k_kahn_persistent(const std::uint32_t* __restrict__ dest, std::uint64_t* __restr
             const bool valid = f < ncur;
             std::uint32_t j = 0, len = 0;
             MergeIn in;
-            in.n = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) in.len[b] = 0;
             if (valid) {
                 j = cur[f];
                 gather_inputs(dest, j, poff, plen, pool, in);

@@ -33,12 +33,14 @@ int gradient(msc3d_ctx* ctx, bool with_forests) {
     }
     // per-dimension critical counts come for free from the gradient kernel; stars
     // with tied values are finished by the deferred slow-path kernel
-    auto* deferred = static_cast<std::uint32_t*>(ctx->ensure("deferred", d.n_verts, 4));
-    if (!deferred) return MSC3D_ERR_NOMEM;
+    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list_ties", d.n_verts, 4))};
+    if (!lists[0] || !lists[1] || !lists[2]) return MSC3D_ERR_NOMEM;
     ctx->crit_counts_valid = true;
     return msc3d_dev::launch_gradient(ctx->values, ctx->value_type, d, codes, p0, p3, ctx->stream,
-                                      reinterpret_cast<unsigned long long*>(ctx->d_small + 40),
-                                      deferred, reinterpret_cast<unsigned long long*>(ctx->d_small + 44),
+                                      reinterpret_cast<unsigned long long*>(ctx->d_small + 40), lists,
+                                      reinterpret_cast<unsigned long long*>(ctx->d_small + 44),
                                       ctx->num_sms);
 }
 
