@@ -114,6 +114,10 @@ int msc3d_ctx_load_labels(msc3d_ctx* ctx, const uint32_t* host_label0, const uin
 /* mark_reachable from the given 1-saddles (host ids, width msc3d_id_width); NULL/0 =
  * all critical 1-cells.  -> "marked" (u8, N), "one_saddles", "two_saddles". */
 int msc3d_ctx_mark(msc3d_ctx* ctx, const void* host_sources, uint64_t n_sources);
+/* Install a MarkedSubgraph (host marked bytes + ascending 1-/2-saddle ids) for
+ * build_minor (saddle_graph.hpp:45-50). */
+int msc3d_ctx_load_marked(msc3d_ctx* ctx, const uint8_t* host_marked, const void* one_saddles,
+                          uint64_t n1, const void* two_saddles, uint64_t n2);
 /* build_minor -> "junctions" + 4 typed edge lists "<kind>.src/.dst" (u32) ".mult" (u64),
  * kind in s1_to_j, j_to_j, j_to_s2, s1_to_s2 (saddle_graph.cpp:121-217). */
 int msc3d_ctx_minor(msc3d_ctx* ctx);
@@ -129,6 +133,13 @@ int msc3d_ctx_count_minor(msc3d_ctx* ctx, const void* one_saddles, uint64_t n1,
                           const void* junctions, uint64_t nj, const void* two_saddles,
                           uint64_t n2, const uint32_t* const* src, const uint32_t* const* dst,
                           const uint64_t* const* mult, const uint64_t* count, int id_width);
+
+/* sp_multiply (op 0) / sp_add (op 1) of two canonical CSR count matrices
+ * (path_matrix.hpp:40-52, path_matrix.cpp:115-186) -> "sp_row_ptr" (u64, rows+1),
+ * "sp_col_idx" (u32), "sp_count" (u64).  MSC3D_ERR_OVERFLOW as the reference. */
+int msc3d_sp_op(msc3d_ctx* ctx, int op, uint32_t x_rows, uint32_t x_cols, const uint64_t* x_row_ptr,
+                const uint32_t* x_col_idx, const uint64_t* x_count, uint32_t y_rows, uint32_t y_cols,
+                const uint64_t* y_row_ptr, const uint32_t* y_col_idx, const uint64_t* y_count);
 
 /* ---- MS graph: compute (msc.hpp:87) ----------------------------------------------------- */
 #define MSC3D_OPT_SEGMENTATION 1 /* ComputeOptions::with_segmentation */

@@ -352,6 +352,26 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
     return MSC3D_OK;
 }
 
+// Sort every bucket [off[m], off[m+1]) (last bucket ends at `total`) of u64 keys
+// ascending: thread-per-bucket insertion sort, block bitonic/merge for large ones.
+int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t total,
+                       std::uint64_t* key, std::uint64_t* scratch, std::uint32_t* large,
+                       unsigned long long* n_large, std::uint64_t* h_small, cudaStream_t s, int num_sms) {
+    if (nb == 0 || total == 0) return MSC3D_OK;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_large, 0, 8, s));
+    k_sort_small_buckets<<<grid_for(nb, num_sms), kThreads, 0, s>>>(off, nb, total, key, large, n_large);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(h_small, n_large, 8, cudaMemcpyDeviceToHost, s));
+    MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_small[0]) {
+        k_sort_large_buckets<<<static_cast<unsigned>(h_small[0]), 512, 0, s>>>(off, nb, total, large, key, scratch);
+        count_launch();
+        MSC3D_CUDA_TRY(cudaGetLastError());
+    }
+    return MSC3D_OK;
+}
+
 int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
                     const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
                     std::uint32_t* cnt, cudaStream_t s, int num_sms) {

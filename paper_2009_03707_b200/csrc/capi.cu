@@ -319,6 +319,18 @@ int msc3d_ctx_mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sou
     return msc3d_stage::mark(ctx, host_sources, n_sources);
 }
 
+int msc3d_ctx_load_marked(msc3d_ctx* ctx, const std::uint8_t* host_marked, const void* ones,
+                          std::uint64_t n1, const void* twos, std::uint64_t n2) {
+    return msc3d_stage::load_marked(ctx, host_marked, ones, n1, twos, n2);
+}
+
+int msc3d_sp_op(msc3d_ctx* ctx, int op, std::uint32_t xr, std::uint32_t xc, const std::uint64_t* xp,
+                const std::uint32_t* xcol, const std::uint64_t* xcnt, std::uint32_t yr, std::uint32_t yc,
+                const std::uint64_t* yp, const std::uint32_t* ycol, const std::uint64_t* ycnt) {
+    if (op != 0 && op != 1) return MSC3D_ERR_INVALID;
+    return msc3d_stage::sp_op(ctx, op, xr, xc, xp, xcol, xcnt, yr, yc, yp, ycol, ycnt);
+}
+
 int msc3d_ctx_minor(msc3d_ctx* ctx) {
     if (!ctx->find("marked")) return MSC3D_ERR_STATE;
     return msc3d_stage::minor(ctx);

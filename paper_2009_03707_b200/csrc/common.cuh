@@ -132,3 +132,30 @@ inline void count_launch(std::uint64_t n = 1) { launch_counter() += n; }
         cudaError_t _e = (expr);                                          \
         if (_e != cudaSuccess) return MSC3D_ERR_CUDA;                     \
     } while (0)
+
+namespace msc3d_dev {
+// Number of DAG successors of the edge at lattice coords (x, y, z)
+// (saddle_graph.cpp:10-24): cofacet quads that are critical, or paired with a
+// facet edge other than this one.
+__device__ __forceinline__ int edge_successor_count(const std::uint8_t* __restrict__ codes, const Dims& d,
+                                                    std::int64_t x, std::int64_t y, std::int64_t z) {
+    const std::int64_t co[3] = {x, y, z};
+    const std::int64_t ext[3] = {d.ex, d.ey, d.ez};
+    const std::int64_t step[3] = {1, d.ex, d.exy};
+    const std::int64_t e = x + d.ex * (y + d.ey * z);
+    int n = 0;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        if (co[b] & 1) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 0 ? co[b] == 0 : co[b] == ext[b] - 1) continue;
+            const std::int64_t q = e + (h ? step[b] : -step[b]);
+            const std::uint8_t k = codes[q];
+            if (k == kCritical) ++n;
+            else if (paired_with_facet(k) && partner_of(d, q, k) != e) ++n;
+        }
+    }
+    return n;
+}
+}  // namespace msc3d_dev

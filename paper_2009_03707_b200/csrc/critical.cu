@@ -46,6 +46,18 @@ struct SaddlePred {
     }
 };
 
+// Junctions of a marked subgraph (saddle_graph.cpp:126-133), ascending.
+struct JunctionPred {
+    const std::uint8_t* codes;
+    const std::uint8_t* marked;
+    Dims d;
+    __device__ __forceinline__ int operator()(std::uint64_t i, std::uint8_t code, int dm) const {
+        if (dm != 1 || code == kCritical || !marked[i]) return -1;
+        const Coord c = unpack(d, i);
+        return edge_successor_count(codes, d, c.x, c.y, c.z) > 1 ? 0 : -1;
+    }
+};
+
 template <typename Pred, typename IdT>
 __global__ void __launch_bounds__(kThreads)
 k_compact_by_dim(const std::uint8_t* __restrict__ codes, Dims d, Pred pred, TileStatus st,
@@ -218,6 +230,15 @@ int launch_saddle_compact(const std::uint8_t* codes, const Dims& d, Workspace& w
                           int id_width, std::uint64_t* d_totals, cudaStream_t s) {
     void* const outs[4] = {out, nullptr, nullptr, nullptr};
     return compact_impl(codes, d, SaddlePred{}, ws, outs, id_width, d_totals, s);
+}
+
+int launch_junction_cells(const std::uint8_t* codes, const std::uint8_t* marked, const Dims& d,
+                          Workspace& ws, void* out, int id_width, std::uint64_t* d_totals,
+                          cudaStream_t s, int num_sms, bool count_only) {
+    const JunctionPred pred{codes, marked, d};
+    if (count_only) return count_impl(codes, d, pred, d_totals, s, num_sms);
+    void* const outs[4] = {out, nullptr, nullptr, nullptr};
+    return compact_impl(codes, d, pred, ws, outs, id_width, d_totals, s);
 }
 
 int launch_marked_critical_count(const std::uint8_t* codes, const std::uint8_t* marked,

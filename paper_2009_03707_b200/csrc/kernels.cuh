@@ -43,6 +43,9 @@ int launch_saddle_count(const std::uint8_t* codes, const Dims& d, std::uint64_t*
                         cudaStream_t s, int num_sms);
 int launch_saddle_compact(const std::uint8_t* codes, const Dims& d, Workspace& ws, void* out,
                           int id_width, std::uint64_t* d_totals, cudaStream_t s);
+int launch_junction_cells(const std::uint8_t* codes, const std::uint8_t* marked, const Dims& d,
+                          Workspace& ws, void* out, int id_width, std::uint64_t* d_totals,
+                          cudaStream_t s, int num_sms, bool count_only);
 int launch_marked_critical_count(const std::uint8_t* codes, const std::uint8_t* marked,
                                  const Dims& d, std::uint64_t* d_totals, cudaStream_t s,
                                  int num_sms);
@@ -135,6 +138,9 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
                          std::uint32_t* large, unsigned long long* n_large,
                          std::uint64_t* h_small, std::uint32_t* asrc, std::uint32_t* adst,
                          std::uint64_t* amult, cudaStream_t s, int num_sms);
+int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t total,
+                       std::uint64_t* key, std::uint64_t* scratch, std::uint32_t* large,
+                       unsigned long long* n_large, std::uint64_t* h_small, cudaStream_t s, int num_sms);
 int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
                     const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
                     std::uint32_t* cnt, cudaStream_t s, int num_sms);

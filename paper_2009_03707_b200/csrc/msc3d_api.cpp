@@ -1,2 +1,664 @@
-// C++ drop-in API
+// The C++ drop-in API (include/msc3d/api.hpp): the reference's public functions
+// with the reference's signatures and exception types, implemented over the C ABI
+// of include/msc3d_cuda.h.  Pipeline stages run on the device; this file only
+// marshals host containers, translates status codes into exceptions, and holds
+// the O(1) lattice queries and host audits the reference exposes.
+#include <algorithm>
+#include <array>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msc3d/api.hpp"
 #include "msc3d_cuda.h"
+
+namespace msc3d {
+
+namespace {
+
+[[noreturn]] void raise_status(int st, const std::string& what) {
+    const std::string msg = what + ": " + msc3d_status_string(st);
+    switch (st) {
+        case MSC3D_ERR_INVALID: throw std::invalid_argument(msg);
+        case MSC3D_ERR_OVERFLOW: throw std::overflow_error(msg);
+        case MSC3D_ERR_RUNTIME: throw std::runtime_error(msg);
+        case MSC3D_ERR_IO: throw IoError(msg);
+        default: throw std::runtime_error("msc3d CUDA failure: " + msg);
+    }
+}
+
+void check(int st, const char* what) {
+    if (st != MSC3D_OK) raise_status(st, what);
+}
+
+// One device context per process (device 0), created on first use.  Calls are
+// serialised: the context's named arrays are shared state.
+struct Device {
+    msc3d_ctx* ctx = nullptr;
+    std::mutex mu;
+    ~Device() {
+        if (ctx) msc3d_ctx_destroy(ctx);
+    }
+};
+
+Device& device() {
+    static Device dev;
+    if (!dev.ctx) check(msc3d_ctx_create(&dev.ctx, 0), "msc3d_ctx_create");
+    return dev;
+}
+
+msc3d_dims to_c(const GridDims& d) { return msc3d_dims{d.nx, d.ny, d.nz}; }
+
+template <typename T>
+std::vector<T> fetch(msc3d_ctx* ctx, const char* name) {
+    void* p = nullptr;
+    std::uint64_t n = 0;
+    int elem = 0;
+    check(msc3d_ctx_array(ctx, name, &p, &n, &elem), name);
+    std::vector<T> out(static_cast<std::size_t>(n * elem / sizeof(T)));
+    check(msc3d_ctx_download(ctx, name, out.data(), out.size() * sizeof(T)), name);
+    return out;
+}
+
+std::int64_t scalar(msc3d_ctx* ctx, const char* name) {
+    std::int64_t v = 0;
+    check(msc3d_ctx_scalar(ctx, name, &v), name);
+    return v;
+}
+
+void upload_field(msc3d_ctx* ctx, const ScalarField& f) {
+    // Samples that are exact in f32 (u8/u16/f32 sources) run the f32 kernels; the
+    // order of the widened doubles is then identical.  Anything else stays f64.
+    bool exact32 = true;
+    for (const double v : f.values)
+        if (static_cast<double>(static_cast<float>(v)) != v) {
+            exact32 = false;
+            break;
+        }
+    if (exact32) {
+        std::vector<float> v32(f.values.begin(), f.values.end());
+        check(msc3d_ctx_load_values(ctx, to_c(f.dims), MSC3D_VALUE_F32, v32.data()), "ScalarField");
+    } else {
+        check(msc3d_ctx_load_values(ctx, to_c(f.dims), MSC3D_VALUE_F64, f.values.data()), "ScalarField");
+    }
+}
+
+void upload_codes(msc3d_ctx* ctx, const GradientField& g) {
+    if (g.code.size() != g.dims.total_cells()) throw std::invalid_argument("gradient code array size mismatch");
+    check(msc3d_ctx_load_codes(ctx, to_c(g.dims), g.code.data()), "GradientField");
+}
+
+}  // namespace
+
+// ================================================================== grid (grid.cpp)
+GridDims::GridDims(std::int64_t nx_, std::int64_t ny_, std::int64_t nz_) : nx(nx_), ny(ny_), nz(nz_) {
+    if (nx < 2 || ny < 2 || nz < 2)
+        throw std::invalid_argument("grid dims must be at least 2 per axis, got " + std::to_string(nx) + "x" +
+                                    std::to_string(ny) + "x" + std::to_string(nz));
+    if (total_cells() > 0xffffffffull)
+        throw std::invalid_argument("grid too large: " + std::to_string(total_cells()) +
+                                    " cells exceed 32-bit cell indexing");
+}
+
+CellIndex pack_cell(const GridDims& d, CellCoord c) {
+    return static_cast<CellIndex>(c.x + d.ex() * (c.y + d.ey() * static_cast<std::int64_t>(c.z)));
+}
+
+CellCoord unpack_cell(const GridDims& d, CellIndex id) {
+    const std::int64_t i = id, ex = d.ex(), ey = d.ey();
+    return CellCoord{static_cast<std::int32_t>(i % ex), static_cast<std::int32_t>((i / ex) % ey),
+                     static_cast<std::int32_t>(i / (ex * ey))};
+}
+
+int cell_dimension(const GridDims& d, CellIndex id) { return cell_dimension(unpack_cell(d, id)); }
+
+CellList facets(const GridDims& d, CellIndex id) {
+    const CellCoord c = unpack_cell(d, id);
+    const std::int32_t v[3] = {c.x, c.y, c.z};
+    const std::int64_t step[3] = {1, d.ex(), d.ex() * d.ey()};
+    CellList out;
+    for (int a = 0; a < 3; ++a)
+        if (v[a] & 1) {
+            out.push(static_cast<CellIndex>(id - step[a]));
+            out.push(static_cast<CellIndex>(id + step[a]));
+        }
+    return out;
+}
+
+CellList cofacets(const GridDims& d, CellIndex id) {
+    const CellCoord c = unpack_cell(d, id);
+    const std::int32_t v[3] = {c.x, c.y, c.z};
+    const std::int64_t ext[3] = {d.ex(), d.ey(), d.ez()};
+    const std::int64_t step[3] = {1, d.ex(), d.ex() * d.ey()};
+    CellList out;
+    for (int a = 0; a < 3; ++a) {
+        if (v[a] & 1) continue;
+        if (v[a] > 0) out.push(static_cast<CellIndex>(id - step[a]));
+        if (v[a] < ext[a] - 1) out.push(static_cast<CellIndex>(id + step[a]));
+    }
+    return out;
+}
+
+VertexList cell_vertices(const GridDims& d, CellIndex id) {
+    const CellCoord c = unpack_cell(d, id);
+    VertexList out;
+    const int nz = (c.z & 1) ? 2 : 1, ny = (c.y & 1) ? 2 : 1, nx = (c.x & 1) ? 2 : 1;
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i)
+                out.push(static_cast<VertexIndex>((c.x / 2 + i) + d.nx * ((c.y / 2 + j) + d.ny * (c.z / 2 + k))));
+    return out;
+}
+
+bool cell_on_boundary(const GridDims& d, CellIndex id) {
+    const CellCoord c = unpack_cell(d, id);
+    return c.x == 0 || c.y == 0 || c.z == 0 || c.x == d.ex() - 1 || c.y == d.ey() - 1 || c.z == d.ez() - 1;
+}
+
+ScalarField::ScalarField(GridDims d, std::vector<double> v) : dims(d), values(std::move(v)) {
+    if (values.size() != dims.vertex_count())
+        throw std::invalid_argument("scalar field size " + std::to_string(values.size()) +
+                                    " does not match vertex count " + std::to_string(dims.vertex_count()));
+    for (const double x : values)
+        if (!std::isfinite(x)) throw std::invalid_argument("scalar field contains a non-finite value");
+}
+
+CellOrderKey cell_order_key(const ScalarField& f, CellIndex id) {
+    const VertexList vs = cell_vertices(f.dims, id);
+    CellOrderKey k;
+    k.count = vs.count;
+    for (int i = 0; i < vs.count; ++i) {
+        k.value[static_cast<std::size_t>(i)] = f[vs[i]];
+        k.vertex[static_cast<std::size_t>(i)] = vs[i];
+    }
+    std::sort(k.value.begin(), k.value.begin() + k.count, [](double a, double b) { return a > b; });
+    std::sort(k.vertex.begin(), k.vertex.begin() + k.count, [](VertexIndex a, VertexIndex b) { return a > b; });
+    return k;
+}
+
+std::strong_ordering compare_keys(const CellOrderKey& a, const CellOrderKey& b) {
+    const int m = std::min(a.count, b.count);
+    for (int i = 0; i < m; ++i) {
+        const double x = a.value[static_cast<std::size_t>(i)], y = b.value[static_cast<std::size_t>(i)];
+        if (x != y) return x < y ? std::strong_ordering::less : std::strong_ordering::greater;
+    }
+    if (a.count != b.count) return a.count <=> b.count;
+    for (int i = 0; i < m; ++i) {
+        const VertexIndex x = a.vertex[static_cast<std::size_t>(i)], y = b.vertex[static_cast<std::size_t>(i)];
+        if (x != y) return x <=> y;
+    }
+    return std::strong_ordering::equal;
+}
+
+std::strong_ordering compare_cells(const ScalarField& f, CellIndex a, CellIndex b) {
+    if (a == b) return std::strong_ordering::equal;
+    return compare_keys(cell_order_key(f, a), cell_order_key(f, b));
+}
+
+VertexIndex max_vertex_of(const ScalarField& f, CellIndex id) {
+    const VertexList vs = cell_vertices(f.dims, id);
+    VertexIndex best = vs[0];
+    for (int i = 1; i < vs.count; ++i)
+        if (f[vs[i]] > f[best] || (f[vs[i]] == f[best] && vs[i] > best)) best = vs[i];
+    return best;
+}
+
+// ================================================================== gradient (device)
+GradientField assign_gradient(const ScalarField& f, int) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_field(dev.ctx, f);
+    check(msc3d_ctx_gradient(dev.ctx), "assign_gradient");
+    return GradientField{f.dims, fetch<std::uint8_t>(dev.ctx, "codes")};
+}
+
+CriticalCells extract_critical_cells(const GradientField& g, int) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    check(msc3d_ctx_critical(dev.ctx), "extract_critical_cells");
+    CriticalCells c;
+    const char* names[4] = {"crit0", "crit1", "crit2", "crit3"};
+    for (int k = 0; k < 4; ++k) c.by_dim[k] = fetch<CellIndex>(dev.ctx, names[k]);
+    return c;
+}
+
+// Host audit (gradient.cpp:299-377): matching everywhere, closed V-paths on small grids.
+GradientReport validate_gradient(const GradientField& g, std::uint64_t max_cells_for_cycles) {
+    GradientReport rep;
+    const GridDims& d = g.dims;
+    const std::uint64_t n = d.total_cells();
+    if (g.code.size() != n) throw std::invalid_argument("gradient code array size mismatch");
+    std::uint64_t pairs = 0;
+    auto flag = [&](CellIndex c) {
+        ++rep.matching_violations;
+        if (rep.samples.size() < 32) rep.samples.push_back(c);
+    };
+    const std::int64_t ext[3] = {d.ex(), d.ey(), d.ez()};
+    for (CellIndex c = 0; c < n; ++c) {
+        const std::uint8_t k = g.code[c];
+        if (k == pair_code::kCritical) continue;
+        if (k == pair_code::kUnset || k >= pair_code::kCofacetBase + 6) {
+            flag(c);
+            continue;
+        }
+        ++pairs;
+        const bool up = k >= pair_code::kCofacetBase;
+        const int dir = k - (up ? pair_code::kCofacetBase : pair_code::kFacetBase);
+        const int axis = dir >> 1, sign = (dir & 1) ? 1 : -1;
+        const CellCoord cc = unpack_cell(d, c);
+        const std::int32_t v[3] = {cc.x, cc.y, cc.z};
+        if (((v[axis] & 1) != 0) == up || v[axis] + sign < 0 || v[axis] + sign >= ext[axis]) {
+            flag(c);
+            continue;
+        }
+        const std::uint8_t want = up ? pair_code::with_facet(axis, -sign) : pair_code::with_cofacet(axis, -sign);
+        if (g.code[g.partner(c)] != want) flag(c);
+    }
+    rep.degenerate = pairs == 0;
+    if (n <= max_cells_for_cycles) {
+        rep.acyclicity_checked = true;
+        std::vector<std::uint32_t> indeg(n, 0);
+        auto each_next = [&](CellIndex a, auto&& fn) {
+            for (CellIndex x : facets(d, g.partner(a)))
+                if (x != a && g.is_paired_with_cofacet(x)) fn(x);
+        };
+        std::uint64_t up_total = 0;
+        for (CellIndex c = 0; c < n; ++c)
+            if (g.is_paired_with_cofacet(c)) {
+                ++up_total;
+                each_next(c, [&](CellIndex x) { ++indeg[x]; });
+            }
+        std::vector<CellIndex> stack;
+        for (CellIndex c = 0; c < n; ++c)
+            if (g.is_paired_with_cofacet(c) && indeg[c] == 0) stack.push_back(c);
+        std::uint64_t peeled = 0;
+        while (!stack.empty()) {
+            const CellIndex c = stack.back();
+            stack.pop_back();
+            ++peeled;
+            each_next(c, [&](CellIndex x) {
+                if (--indeg[x] == 0) stack.push_back(x);
+            });
+        }
+        rep.cells_in_closed_vpath = up_total - peeled;
+        for (CellIndex c = 0; c < n && rep.cells_in_closed_vpath && rep.samples.size() < 32; ++c)
+            if (g.is_paired_with_cofacet(c) && indeg[c] > 0) rep.samples.push_back(c);
+    }
+    return rep;
+}
+
+// ================================================================== extrema (device)
+std::uint64_t dense_cell_count(const GridDims& d, int dim) {
+    if (dim == 0) return d.vertex_count();
+    if (dim == 3) return d.cube_count();
+    throw std::invalid_argument("dense_cell_count: dim must be 0 or 3");
+}
+
+CellIndex dense_to_cell(const GridDims& d, int dim, std::uint32_t i) {
+    const std::int64_t mx = dim == 0 ? d.nx : d.nx - 1, my = dim == 0 ? d.ny : d.ny - 1;
+    const std::int32_t o = dim == 0 ? 0 : 1;
+    const std::int64_t x = i % mx, y = (i / mx) % my, z = i / (mx * my);
+    return pack_cell(d, {static_cast<std::int32_t>(2 * x + o), static_cast<std::int32_t>(2 * y + o),
+                         static_cast<std::int32_t>(2 * z + o)});
+}
+
+std::uint32_t cell_to_dense(const GridDims& d, int dim, CellIndex c) {
+    const CellCoord cc = unpack_cell(d, c);
+    const std::int64_t mx = dim == 0 ? d.nx : d.nx - 1, my = dim == 0 ? d.ny : d.ny - 1;
+    return static_cast<std::uint32_t>(cc.x / 2 + mx * (cc.y / 2 + my * (cc.z / 2)));
+}
+
+ParentForest build_forest(const GradientField& g, int dim, int) {
+    if (dim != 0 && dim != 3) throw std::invalid_argument("build_forest: dim must be 0 or 3");
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    check(msc3d_ctx_forest(dev.ctx, dim), "build_forest");
+    ParentForest f;
+    f.dims = g.dims;
+    f.dim = dim;
+    f.parent = fetch<std::uint32_t>(dev.ctx, dim == 0 ? "parent0" : "parent3");
+    return f;
+}
+
+RootLabels find_roots(const ParentForest& forest, int) {
+    RootLabels r;
+    if (forest.parent.empty()) return r;
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    check(msc3d_ctx_load_parent(dev.ctx, 0, forest.parent.data(), forest.parent.size()), "find_roots");
+    check(msc3d_ctx_roots(dev.ctx, 0), "find_roots");
+    r.label = fetch<std::uint32_t>(dev.ctx, "label0");
+    r.rounds = static_cast<int>(scalar(dev.ctx, "rounds0"));
+    return r;
+}
+
+std::vector<SaddleExtremumArc> saddle_extremum_arcs(const GradientField& g, const RootLabels& labels0,
+                                                    const RootLabels& labels3, int) {
+    if (labels0.label.size() != g.dims.vertex_count() || labels3.label.size() != g.dims.cube_count())
+        throw std::invalid_argument("saddle_extremum_arcs: label sizes do not match dims");
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    check(msc3d_ctx_load_labels(dev.ctx, labels0.label.data(), labels3.label.data()), "saddle_extremum_arcs");
+    check(msc3d_ctx_se_arcs(dev.ctx), "saddle_extremum_arcs");
+    const auto s = fetch<CellIndex>(dev.ctx, "se_saddle");
+    const auto e = fetch<CellIndex>(dev.ctx, "se_extremum");
+    const auto m = fetch<std::uint32_t>(dev.ctx, "se_mult");
+    std::vector<SaddleExtremumArc> out(s.size());
+    for (std::size_t i = 0; i < s.size(); ++i) out[i] = {s[i], e[i], m[i]};
+    return out;
+}
+
+Segmentation extremum_segmentation(const GridDims& dims, const RootLabels& labels0, const RootLabels& labels3) {
+    if (labels0.label.size() != dims.vertex_count() || labels3.label.size() != dims.cube_count())
+        throw std::invalid_argument("extremum_segmentation: label sizes do not match dims");
+    return Segmentation{dims, labels0.label, labels3.label};
+}
+
+// ================================================================== saddle graph
+SuccessorList successors(const GradientField& g, CellIndex e) {
+    SuccessorList out;
+    for (const CellIndex q : cofacets(g.dims, e)) {
+        if (g.is_critical(q)) {
+            out.push(DagSuccessor{DagSuccessor::kTerminal2Saddle, q});
+        } else if (g.is_paired_with_facet(q)) {
+            const CellIndex o = g.partner(q);
+            if (o != e) out.push(DagSuccessor{DagSuccessor::kEdge, o});
+        }
+    }
+    return out;
+}
+
+MarkedSubgraph mark_reachable(const GradientField& g, const std::vector<CellIndex>& one_saddles, int) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    const CellIndex dummy = 0;
+    check(msc3d_ctx_mark(dev.ctx, one_saddles.empty() ? &dummy : one_saddles.data(), one_saddles.size()),
+          "mark_reachable");
+    MarkedSubgraph m;
+    m.dims = g.dims;
+    m.marked = fetch<std::uint8_t>(dev.ctx, "marked");
+    m.one_saddles = fetch<CellIndex>(dev.ctx, "one_saddles");
+    m.two_saddles = fetch<CellIndex>(dev.ctx, "two_saddles");
+    return m;
+}
+
+DagMinor build_minor(const MarkedSubgraph& m, const GradientField& g, int) {
+    if (m.marked.size() != g.dims.total_cells()) throw std::invalid_argument("build_minor: marked size mismatch");
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    const CellIndex dummy = 0;
+    check(msc3d_ctx_load_marked(dev.ctx, m.marked.data(), m.one_saddles.empty() ? &dummy : m.one_saddles.data(),
+                                m.one_saddles.size(), m.two_saddles.empty() ? &dummy : m.two_saddles.data(),
+                                m.two_saddles.size()),
+          "build_minor");
+    check(msc3d_ctx_minor(dev.ctx), "build_minor");
+    DagMinor mn;
+    mn.one_saddles = m.one_saddles;
+    mn.two_saddles = m.two_saddles;
+    mn.junctions = fetch<CellIndex>(dev.ctx, "junctions");
+    const char* kinds[4] = {"s1_to_j", "j_to_j", "j_to_s2", "s1_to_s2"};
+    std::vector<MinorEdge>* lists[4] = {&mn.s1_to_j, &mn.j_to_j, &mn.j_to_s2, &mn.s1_to_s2};
+    for (int k = 0; k < 4; ++k) {
+        const auto s = fetch<std::uint32_t>(dev.ctx, (std::string(kinds[k]) + ".src").c_str());
+        const auto t = fetch<std::uint32_t>(dev.ctx, (std::string(kinds[k]) + ".dst").c_str());
+        const auto u = fetch<std::uint64_t>(dev.ctx, (std::string(kinds[k]) + ".mult").c_str());
+        lists[k]->resize(s.size());
+        for (std::size_t i = 0; i < s.size(); ++i) (*lists[k])[i] = MinorEdge{s[i], t[i], u[i]};
+    }
+    return mn;
+}
+
+// ================================================================== path matrix
+SparseCountMatrix from_edges(const std::vector<MinorEdge>& edges, std::uint32_t rows, std::uint32_t cols) {
+    for (const MinorEdge& e : edges)
+        if (e.src >= rows || e.dst >= cols) throw std::invalid_argument("from_edges: edge endpoint out of range");
+    std::vector<MinorEdge> sorted = edges;
+    std::sort(sorted.begin(), sorted.end(), [](const MinorEdge& a, const MinorEdge& b) {
+        return a.src != b.src ? a.src < b.src : a.dst < b.dst;
+    });
+    SparseCountMatrix m;
+    m.rows = rows;
+    m.cols = cols;
+    m.row_ptr.assign(static_cast<std::size_t>(rows) + 1, 0);
+    for (std::size_t i = 0; i < sorted.size();) {
+        std::uint64_t sum = 0;
+        std::size_t j = i;
+        for (; j < sorted.size() && sorted[j].src == sorted[i].src && sorted[j].dst == sorted[i].dst; ++j)
+            if (__builtin_add_overflow(sum, sorted[j].multiplicity, &sum))
+                throw std::overflow_error("from_edges: multiplicity sum exceeds 64 bits");
+        if (sum) {
+            m.col_idx.push_back(sorted[i].dst);
+            m.count.push_back(sum);
+            ++m.row_ptr[sorted[i].src + 1];
+        }
+        i = j;
+    }
+    for (std::uint32_t r = 0; r < rows; ++r) m.row_ptr[r + 1] += m.row_ptr[r];
+    return m;
+}
+
+namespace {
+SparseCountMatrix device_spgemm(const SparseCountMatrix& x, const SparseCountMatrix& y, int op,
+                                const char* what) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    const std::uint64_t one = 0;
+    check(msc3d_sp_op(dev.ctx, op, x.rows, x.cols, x.row_ptr.data(), x.col_idx.empty() ? nullptr : x.col_idx.data(),
+                      x.count.empty() ? &one : x.count.data(), y.rows, y.cols, y.row_ptr.data(),
+                      y.col_idx.empty() ? nullptr : y.col_idx.data(), y.count.empty() ? &one : y.count.data()),
+          what);
+    SparseCountMatrix z;
+    z.rows = x.rows;
+    z.cols = op == 0 ? y.cols : x.cols;
+    z.row_ptr = fetch<std::uint64_t>(dev.ctx, "sp_row_ptr");
+    z.col_idx = fetch<std::uint32_t>(dev.ctx, "sp_col_idx");
+    z.count = fetch<std::uint64_t>(dev.ctx, "sp_count");
+    return z;
+}
+}  // namespace
+
+SparseCountMatrix sp_multiply(const SparseCountMatrix& x, const SparseCountMatrix& y, int) {
+    if (x.cols != y.rows) throw std::invalid_argument("sp_multiply: inner dimensions differ");
+    return device_spgemm(x, y, 0, "sp_multiply");
+}
+
+SparseCountMatrix sp_add(const SparseCountMatrix& x, const SparseCountMatrix& y, int) {
+    if (x.rows != y.rows || x.cols != y.cols) throw std::invalid_argument("sp_add: dimensions differ");
+    return device_spgemm(x, y, 1, "sp_add");
+}
+
+std::vector<SaddleConnection> count_paths(const DagMinor& minor, int) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    const std::vector<MinorEdge>* lists[4] = {&minor.s1_to_j, &minor.j_to_j, &minor.j_to_s2, &minor.s1_to_s2};
+    std::vector<std::uint32_t> src[4], dst[4];
+    std::vector<std::uint64_t> mul[4];
+    const std::uint32_t* ps[4];
+    const std::uint32_t* pd[4];
+    const std::uint64_t* pm[4];
+    std::uint64_t cnt[4];
+    for (int k = 0; k < 4; ++k) {
+        for (const MinorEdge& e : *lists[k]) {
+            src[k].push_back(e.src);
+            dst[k].push_back(e.dst);
+            mul[k].push_back(e.multiplicity);
+        }
+        src[k].push_back(0);  // keep the pointers valid when empty
+        dst[k].push_back(0);
+        mul[k].push_back(0);
+        ps[k] = src[k].data();
+        pd[k] = dst[k].data();
+        pm[k] = mul[k].data();
+        cnt[k] = lists[k]->size();
+    }
+    const CellIndex dummy = 0;
+    check(msc3d_ctx_count_minor(dev.ctx, minor.one_saddles.empty() ? &dummy : minor.one_saddles.data(),
+                                minor.one_saddles.size(), minor.junctions.empty() ? &dummy : minor.junctions.data(),
+                                minor.junctions.size(), minor.two_saddles.empty() ? &dummy : minor.two_saddles.data(),
+                                minor.two_saddles.size(), ps, pd, pm, cnt, 4),
+          "count_paths");
+    const auto a = fetch<std::uint32_t>(dev.ctx, "ss_one_rank");
+    const auto b = fetch<std::uint32_t>(dev.ctx, "ss_two_rank");
+    const auto p = fetch<std::uint64_t>(dev.ctx, "ss_paths");
+    std::vector<SaddleConnection> out(a.size());
+    for (std::size_t i = 0; i < a.size(); ++i) out[i] = {minor.one_saddles[a[i]], minor.two_saddles[b[i]], p[i]};
+    return out;
+}
+
+// ================================================================== msc
+std::uint64_t MSComplex::count_by_index(int index) const {
+    std::uint64_t n = 0;
+    for (const CriticalPoint& cp : critical_points) n += cp.index == index;
+    return n;
+}
+
+std::int64_t MSComplex::euler() const {
+    std::int64_t e = 0;
+    for (const CriticalPoint& cp : critical_points) e += (cp.index & 1) ? -1 : 1;
+    return e;
+}
+
+std::uint64_t field_hash(const ScalarField& f) { return msc3d_field_hash_f64(f.values.data(), f.values.size()); }
+
+MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_field(dev.ctx, f);
+    double ms[5] = {0, 0, 0, 0, 0};
+    check(msc3d_ctx_compute(dev.ctx, opt.with_segmentation ? MSC3D_OPT_SEGMENTATION : 0, ms), "compute");
+    if (opt.validate) {
+        const GradientField g{f.dims, fetch<std::uint8_t>(dev.ctx, "codes")};
+        if (!validate_gradient(g).ok()) throw std::runtime_error("compute: gradient failed validation");
+    }
+    if (opt.timings) {
+        opt.timings->gradient = ms[0] / 1e3;
+        opt.timings->critical = ms[1] / 1e3;
+        opt.timings->extrema = ms[2] / 1e3;
+        opt.timings->reachability = ms[3] / 1e3;
+        opt.timings->counting = ms[4] / 1e3;
+    }
+    MSComplex m;
+    m.dims = f.dims;
+    m.dtype = opt.source_dtype;
+    m.input_hash = field_hash(f);
+    const auto cells = fetch<CellIndex>(dev.ctx, "cp_cell");
+    const auto index = fetch<std::uint8_t>(dev.ctx, "cp_index");
+    m.critical_points.resize(cells.size());
+    for (std::size_t i = 0; i < cells.size(); ++i) {
+        CriticalPoint& cp = m.critical_points[i];
+        cp.id = static_cast<std::uint32_t>(i);
+        cp.cell = cells[i];
+        cp.index = index[i];
+        cp.doubled = unpack_cell(f.dims, cells[i]);
+        cp.midpoint = {cp.doubled.x / 2.0, cp.doubled.y / 2.0, cp.doubled.z / 2.0};
+        cp.value = f[max_vertex_of(f, cells[i])];
+    }
+    const auto s = fetch<std::uint32_t>(dev.ctx, "arc_src");
+    const auto d = fetch<std::uint32_t>(dev.ctx, "arc_dst");
+    const auto u = fetch<std::uint64_t>(dev.ctx, "arc_mult");
+    m.arcs.resize(s.size());
+    for (std::size_t i = 0; i < s.size(); ++i) m.arcs[i] = Arc{s[i], d[i], u[i]};
+    if (opt.with_segmentation) {
+        LabelVolumes lv;
+        lv.vertex_to_min = fetch<std::uint32_t>(dev.ctx, "labels_min");
+        lv.cube_to_max = fetch<std::uint32_t>(dev.ctx, "labels_max");
+        m.labels = std::move(lv);
+    }
+    return m;
+}
+
+BoundaryReport boundary_check(const MSComplex& m) {
+    std::vector<std::vector<std::pair<std::uint32_t, std::uint64_t>>> below(m.critical_points.size());
+    for (const Arc& a : m.arcs) below[a.dst].push_back({a.src, a.multiplicity});
+    BoundaryReport r;
+    for (const CriticalPoint& top : m.critical_points) {
+        if (top.index < 2) continue;
+        std::map<std::uint32_t, unsigned> odd;
+        for (const auto& [mid, m1] : below[top.id])
+            for (const auto& [low, m2] : below[mid]) odd[low] ^= static_cast<unsigned>(m1 & m2 & 1);
+        for (const auto& [low, o] : odd)
+            if (o) r.odd_pairs.push_back({top.id, low});
+    }
+    return r;
+}
+
+std::vector<Arc> query_arcs(const MSComplex& m, std::uint32_t cp_id) {
+    if (cp_id >= m.critical_points.size()) throw std::out_of_range("query_arcs: unknown critical point id");
+    std::vector<Arc> out;
+    for (const Arc& a : m.arcs)
+        if (a.src == cp_id || a.dst == cp_id) out.push_back(a);
+    return out;
+}
+
+// ================================================================== volume
+SampleType parse_sample_type(const std::string& name) {
+    if (name == "u8") return SampleType::u8;
+    if (name == "u16") return SampleType::u16;
+    if (name == "f32") return SampleType::f32;
+    if (name == "f64") return SampleType::f64;
+    throw std::invalid_argument("unknown sample type '" + name + "' (want u8|u16|f32|f64)");
+}
+
+const char* sample_type_name(SampleType t) {
+    return t == SampleType::u8 ? "u8" : (t == SampleType::u16 ? "u16" : (t == SampleType::f32 ? "f32" : "f64"));
+}
+
+std::size_t sample_size(SampleType t) {
+    return t == SampleType::u8 ? 1 : (t == SampleType::u16 ? 2 : (t == SampleType::f32 ? 4 : 8));
+}
+
+ScalarField read_volume(const VolumeSpec& spec) {
+    std::FILE* fp = std::fopen(spec.path.c_str(), "rb");
+    if (!fp) throw IoError("cannot read '" + spec.path + "'");
+    std::fseek(fp, 0, SEEK_END);
+    const long long size = std::ftell(fp);
+    std::fseek(fp, 0, SEEK_SET);
+    const std::size_t width = sample_size(spec.dtype);
+    const std::uint64_t want = spec.dims.vertex_count() * width;
+    if (size < 0 || static_cast<std::uint64_t>(size) != want) {
+        std::fclose(fp);
+        throw std::invalid_argument("volume size mismatch for '" + spec.path + "': file has " +
+                                    std::to_string(size) + " bytes, need " + std::to_string(want));
+    }
+    std::vector<unsigned char> raw(want);
+    const std::size_t got = want ? std::fread(raw.data(), 1, want, fp) : 0;
+    std::fclose(fp);
+    if (got != want) throw IoError("short read on '" + spec.path + "'");
+    std::vector<double> v(spec.dims.vertex_count());
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        std::uint64_t b = 0;
+        for (std::size_t k = 0; k < width; ++k)
+            b |= static_cast<std::uint64_t>(raw[i * width + (spec.big_endian ? width - 1 - k : k)]) << (8 * k);
+        double x;
+        if (spec.dtype == SampleType::u8 || spec.dtype == SampleType::u16) {
+            x = static_cast<double>(b);
+        } else if (spec.dtype == SampleType::f32) {
+            float fl;
+            const std::uint32_t b32 = static_cast<std::uint32_t>(b);
+            std::memcpy(&fl, &b32, 4);
+            x = fl;
+        } else {
+            std::memcpy(&x, &b, 8);
+        }
+        if (!std::isfinite(x))
+            throw std::invalid_argument("volume '" + spec.path + "' holds a non-finite sample at index " +
+                                        std::to_string(i));
+        v[i] = x;
+    }
+    return ScalarField(spec.dims, std::move(v));
+}
+
+}  // namespace msc3d

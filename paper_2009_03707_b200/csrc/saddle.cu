@@ -114,6 +114,14 @@ struct Succ {
         return r;
     }
     __device__ __forceinline__ bool first_is_term() const { return (term >> (__ffs(valid) - 1)) & 1u; }
+    // the successor at position k (runtime k, select chain: no local memory)
+    __device__ __forceinline__ C3 at(int k) const {
+        C3 r = c[0];
+#pragma unroll
+        for (int j = 1; j < 6; ++j)
+            if (k == j) r = c[j];
+        return r;
+    }
 };
 
 // saddle_graph.cpp:10-24 on coordinates (no id <-> coordinate divisions).
@@ -324,15 +332,16 @@ __global__ void k_origin_dests(const std::uint8_t* __restrict__ codes, Dims d,
         std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
         std::uint32_t pend = 0;
         int nd = 0;
-#pragma unroll
-        for (int b = 0; b < 6; ++b) {
-            if (!((s.valid >> b) & 1u)) continue;
+#pragma unroll 1
+        for (std::uint32_t todo = s.valid; todo; todo &= todo - 1) {
+            const int b = __ffs(todo) - 1;
+            const C3 sb = s.at(b);
             std::uint32_t t;
             if ((s.term >> b) & 1u) {
-                t = kTerm | tmap[quad_dense(d, s.c[b])];
+                t = kTerm | tmap[quad_dense(d, sb)];
             } else {
                 // the walk stops AT a junction, else follows the junction-free chain
-                C3 cur = s.c[b];
+                C3 cur = sb;
                 t = kNone;
                 for (std::uint64_t steps = 0;; ++steps) {
                     const Succ nx = successors(codes, d, cur);

@@ -378,13 +378,6 @@ int count(msc3d_ctx* ctx) {
                                         n, w, b, ctx->stream, ctx->num_sms);
 }
 
-int minor(msc3d_ctx*) { return MSC3D_ERR_STATE; }
-int count_minor(msc3d_ctx*, const void*, std::uint64_t, const void*, std::uint64_t, const void*,
-                std::uint64_t, const std::uint32_t* const*, const std::uint32_t* const*,
-                const std::uint64_t* const*, const std::uint64_t*, int) {
-    return MSC3D_ERR_STATE;
-}
-
 // ---------------------------------------------------------------------------------
 // compute() (msc.cpp:57-147)
 // ---------------------------------------------------------------------------------

@@ -21,5 +21,10 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
                 const std::uint32_t* const* src, const std::uint32_t* const* dst,
                 const std::uint64_t* const* mult, const std::uint64_t* count, int id_width);
 int compute(msc3d_ctx* ctx, int options, double* stage_ms);
+int load_marked(msc3d_ctx* ctx, const std::uint8_t* host_marked, const void* ones, std::uint64_t n1,
+                const void* twos, std::uint64_t n2);
+int sp_op(msc3d_ctx* ctx, int op, std::uint32_t xr, std::uint32_t xc, const std::uint64_t* xp,
+          const std::uint32_t* xcol, const std::uint64_t* xcnt, std::uint32_t yr, std::uint32_t yc,
+          const std::uint64_t* yp, const std::uint32_t* ycol, const std::uint64_t* ycnt);
 
 }  // namespace msc3d_stage
