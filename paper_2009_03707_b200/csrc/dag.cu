@@ -1,0 +1,988 @@
+// The saddle-saddle DAG on the device, built around a per-edge successor table.
+//
+// Successor table.  The DAG of the reference (saddle_graph.cpp:10-24) has the 1-cells
+// as nodes; a 1-cell e has at most four cofacet quads q (two even axes b, two signs
+// s, in cofacet order), and q contributes: a terminal 2-saddle (q critical), nothing
+// (q paired with a cube, or with e itself, or outside the box), or the edge q is
+// paired with -- which is one of three edges: the one parallel to e across q
+// ("straight") or one of the two edges of q along b ("turn" towards -a / +a, a the
+// odd axis of e).  That is 5 states = 3 bits per cofacet position, 12 bits per edge,
+// plus one bit "e is critical".  k_succ_table derives the 16-bit word of every edge
+// from the pair codes in one pass; afterwards every DAG step is ONE 2-byte load and
+// integer arithmetic on the dense edge index de = 3 * (lower vertex) + axis -- no
+// lattice-coordinate divisions, no per-step byte gathers from the 1 GB code array.
+//
+// Reachability (mark_reachable, saddle_graph.cpp:26-86): level-synchronous BFS in
+// one cooperative kernel (a grid barrier per level), 32 frontier nodes per warp
+// iteration, claims by atomic test-and-set in the visited bitmap (1 bit per dense
+// edge, L2-resident), one warp-aggregated reservation per iteration for the next
+// frontier.  (Depth-first / chain-following variants were measured and lose: a
+// long V-path walked by one thread costs more than the BFS levels that reach the
+// same nodes in parallel.)
+//
+// Junctions (saddle_graph.cpp:126-133) = visited, non-critical edges with > 1
+// successor: a bitmap, ranked by per-word popcount prefix sums (rank(de) =
+// woff[de/32] + popc(jbits[de/32] & below)), so no 1.6 GB id-map is scattered.
+//
+// Counting (path_matrix.cpp:188-219).  Every junction / 1-saddle branch is walked
+// to its end (k_walk).  Each junction j then needs P(j), the sorted sparse vector
+// of path counts to 2-saddles, P(j) = sum over branches of P(dest): Kahn's
+// algorithm over the junction graph in one cooperative kernel -- round 0 scans
+// every node without pending children in index order (coalesced, no frontier),
+// later rounds take the frontier of nodes whose last child finished in the
+// previous round.  P(j) with <= 2 entries is stored inline in a 32-byte record,
+// longer ones in a pool (64 arenas, one reservation per warp).  1-saddles are the
+// roots: they only record their merged length; a final pass writes the sorted
+// (1-saddle, 2-saddle, count) output.  Counts are exact u64 with sticky overflow.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace msc3d_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr std::uint32_t kTerm = 0x80000000u;
+constexpr std::uint32_t kNone = 0xffffffffu;
+constexpr std::uint32_t kSuccCrit = 1u << 12;
+constexpr std::uint32_t kFieldLow = 0x249u;  // lowest bit of each 3-bit field
+constexpr int kArenas = 64;
+constexpr std::uint64_t kBadOff = ~0ull;
+
+inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
+    const std::uint64_t need = (n + kThreads - 1) / kThreads;
+    return static_cast<unsigned>(std::max<std::uint64_t>(
+        1, std::min<std::uint64_t>(need, static_cast<std::uint64_t>(num_sms) * per_sm)));
+}
+
+// Vertex strides as u32 (dense edge ids are < 2^32 for every grid this path takes).
+struct EGrid {
+    std::uint32_t sy, sz;  // nx, nx*ny
+    __device__ __forceinline__ std::uint32_t st(int axis) const {
+        return axis == 0 ? 1u : (axis == 1 ? sy : sz);
+    }
+};
+
+// Device clock in ns, for per-round timelines (stats arrays).
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr int kTimeline = 256;
+
+__device__ __forceinline__ int other_axis(int a, int k) { return a == 0 ? 1 + k : (a == 1 ? 2 * k : k); }
+
+__device__ __forceinline__ std::uint32_t n_succ(std::uint32_t s) {
+    return __popc((s | (s >> 1) | (s >> 2)) & kFieldLow);
+}
+
+struct EdgeRef {
+    std::uint32_t v;  // lower vertex
+    int a;            // odd axis
+    __device__ __forceinline__ explicit EdgeRef(std::uint32_t de) {
+        v = __umulhi(de, 0xAAAAAAABu) >> 1;
+        a = static_cast<int>(de - 3u * v);
+    }
+};
+
+// Successor edge at cofacet position p (0..3) with field f in {2, 3, 4}.
+__device__ __forceinline__ std::uint32_t succ_edge(const EdgeRef& e, std::uint32_t de, int p,
+                                                   std::uint32_t f, const EGrid& g) {
+    const int b = other_axis(e.a, p >> 1);
+    const std::uint32_t sb = g.st(b);
+    const bool neg = !(p & 1);
+    if (f == 2) return neg ? de - 3u * sb : de + 3u * sb;
+    std::uint32_t lv = neg ? e.v - sb : e.v;
+    if (f == 4) lv += g.st(e.a);
+    return 3u * lv + static_cast<std::uint32_t>(b);
+}
+// Dense index 3 * (lower vertex) + normal axis of the terminal quad at position p.
+__device__ __forceinline__ std::uint32_t term_quad(const EdgeRef& e, int p, const EGrid& g) {
+    const int b = other_axis(e.a, p >> 1);
+    const std::uint32_t lv = (p & 1) ? e.v : e.v - g.st(b);
+    return 3u * lv + static_cast<std::uint32_t>(3 - e.a - b);
+}
+
+// ---------------------------------------------------------------------------------
+// successor table
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+k_succ_table(const std::uint8_t* __restrict__ codes, Dims d, std::uint16_t* __restrict__ succ) {
+    const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
+    const std::int64_t step[3] = {1, d.ex, d.exy};
+    const std::int64_t nn[3] = {d.nx, d.ny, d.nz};
+    for (std::uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const std::int64_t vz = static_cast<std::int64_t>(d.fny.div(r));
+        const std::int64_t vy = static_cast<std::int64_t>(r) - vz * d.ny;
+        for (std::int64_t vx = threadIdx.x; vx < d.nx; vx += blockDim.x) {
+            const std::int64_t vc[3] = {vx, vy, vz};
+            const std::int64_t cv = 2 * vx + d.ex * (2 * vy + d.ey * 2 * vz);
+            const std::uint64_t v = static_cast<std::uint64_t>(vx) + static_cast<std::uint64_t>(d.nx) * r;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                std::uint32_t out = 0;
+                if (vc[a] < nn[a] - 1) {
+                    const std::int64_t eid = cv + step[a];
+                    if (codes[eid] == kCritical) out |= kSuccCrit;
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int b = a == 0 ? 1 + k : (a == 1 ? 2 * k : k);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (h ? vc[b] >= nn[b] - 1 : vc[b] <= 0) continue;
+                            const std::uint8_t qc = codes[eid + (h ? step[b] : -step[b])];
+                            std::uint32_t f = 0;
+                            if (qc == kCritical) {
+                                f = 1;
+                            } else if (paired_with_facet(qc)) {
+                                const int dir = qc - kFacetBase, ax = dir >> 1, ps = dir & 1;
+                                if (ax == b) f = ps == h ? 2u : 0u;  // the other way is e itself
+                                else f = ps ? 4u : 3u;                // ax == a
+                            }
+                            out |= f << (3 * (2 * k + h));
+                        }
+                    }
+                }
+                succ[3 * v + a] = static_cast<std::uint16_t>(out);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// reachability: rounds of chain-following traversal, one cooperative launch
+// ---------------------------------------------------------------------------------
+// Warp-aggregated reservation of n slots on a global counter.  Must be called by
+// all 32 lanes of the warp (n may be 0); returns this lane's first slot.
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* ctr, unsigned n) {
+    const int lane = threadIdx.x & 31;
+    unsigned incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(ctr, static_cast<unsigned long long>(total));
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return base + incl - n;
+}
+
+// cnt[0] = number of (already claimed) seeds in fa; cnt[1], cnt[2] scratch.
+// stats[0] = rounds, stats[1] = nodes claimed here.  Level-synchronous: one
+// round per BFS level, 32 nodes per warp iteration, one reservation per iteration.
+__global__ void __launch_bounds__(kThreads)
+k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restrict__ bitmap,
+        std::uint32_t* __restrict__ fa, std::uint32_t* __restrict__ fb, unsigned long long* __restrict__ cnt,
+        unsigned long long* __restrict__ stats) {
+    cg::grid_group grid = cg::this_grid();
+    std::uint32_t* cur = fa;
+    std::uint32_t* nxt = fb;
+    unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&cnt[0]);
+    unsigned long long mine = 0;
+    int round = 0;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    const std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+    const int lane = threadIdx.x & 31;
+    while (ncur) {
+        unsigned long long* next_cnt = &cnt[(round + 1) % 3];
+        if (grid.thread_rank() == 0) {
+            cnt[(round + 2) % 3] = 0;
+            if (round < kTimeline) stats[2 + round] = gtimer();
+        }
+        for (std::uint64_t base = wbase; base < ncur; base += stride) {
+            const std::uint64_t j = base + lane;
+            std::uint32_t de[4] = {0, 0, 0, 0};
+            std::uint32_t won = 0;
+            if (j < ncur) {
+                const std::uint32_t node = __ldcg(cur + j);
+                const std::uint32_t s = succ[node];
+                const EdgeRef e(node);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const std::uint32_t f = (s >> (3 * p)) & 7u;
+                    if (f < 2) continue;
+                    de[p] = succ_edge(e, node, p, f, g);
+                    const unsigned bit = 1u << (de[p] & 31);
+                    unsigned int* w = &bitmap[de[p] >> 5];
+                    if (*w & bit) continue;  // bits only ever go 0 -> 1
+                    if (atomicOr(w, bit) & bit) continue;
+                    won |= 1u << p;
+                }
+            }
+            mine += __popc(won);
+            const unsigned long long at = warp_reserve(next_cnt, __popc(won));
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+                if ((won >> p) & 1u) nxt[at + __popc(won & ((1u << p) - 1u))] = de[p];
+        }
+        grid.sync();
+        ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
+        ++round;
+        std::uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&stats[1], mine);
+    if (grid.thread_rank() == 0) {
+        stats[0] = static_cast<unsigned long long>(round);
+        if (round < kTimeline) stats[2 + round] = gtimer();
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// junction bitmap, ranks and list
+// ---------------------------------------------------------------------------------
+__global__ void k_junction_bits(const std::uint16_t* __restrict__ succ, const unsigned int* __restrict__ bitmap,
+                                std::uint64_t nwords, unsigned int* __restrict__ jbits,
+                                std::uint32_t* __restrict__ jcnt, unsigned long long* __restrict__ nodes) {
+    unsigned long long mine = 0;
+    for (std::uint64_t w = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
+         w += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        unsigned int bits = bitmap[w], jb = 0;
+        mine += __popc(bits);
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const std::uint32_t s = succ[32 * w + b];
+            if (!(s & kSuccCrit) && n_succ(s) > 1) jb |= 1u << b;
+        }
+        jbits[w] = jb;
+        jcnt[w] = __popc(jb);
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(nodes, mine);
+}
+
+__global__ void k_junction_list(const unsigned int* __restrict__ jbits, std::uint64_t nwords,
+                                const std::uint64_t* __restrict__ woff, std::uint32_t* __restrict__ jlist) {
+    for (std::uint64_t w = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
+         w += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        unsigned int jb = jbits[w];
+        std::uint64_t at = woff[w];
+        while (jb) {
+            const int b = __ffs(jb) - 1;
+            jb &= jb - 1;
+            jlist[at++] = static_cast<std::uint32_t>(32 * w + b);
+        }
+    }
+}
+
+__device__ __forceinline__ std::uint32_t junction_rank(const std::uint64_t* __restrict__ woff,
+                                                       const unsigned int* __restrict__ jbits, std::uint32_t de) {
+    const std::uint32_t w = de >> 5;
+    return static_cast<std::uint32_t>(woff[w]) + __popc(jbits[w] & ((1u << (de & 31)) - 1u));
+}
+
+// ---------------------------------------------------------------------------------
+// branch walks: origin -> up to 4 destinations (junction rank | kTerm|2-saddle rank | kNone)
+// ---------------------------------------------------------------------------------
+struct WalkCtx {
+    const std::uint16_t* succ;
+    EGrid g;
+    const std::uint64_t* woff;
+    const unsigned int* jbits;
+    const std::uint32_t* tmap;
+    std::uint64_t limit;
+};
+
+__device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, std::uint32_t cur, unsigned int* cycle) {
+    for (std::uint64_t steps = 0;; ++steps) {
+        const std::uint32_t s = __ldg(&c.succ[cur]);
+        const std::uint32_t present = (s | (s >> 1) | (s >> 2)) & kFieldLow;
+        if (present == 0) return kNone;                       // dead end
+        if (present & (present - 1)) return junction_rank(c.woff, c.jbits, cur);
+        const int p = (__ffs(present) - 1) / 3;
+        const std::uint32_t f = (s >> (3 * p)) & 7u;
+        const EdgeRef e(cur);
+        if (f == 1) return kTerm | c.tmap[term_quad(e, p, c.g)];
+        cur = succ_edge(e, cur, p, f, c.g);
+        if (steps > c.limit) {
+            *cycle = 1u;  // invalid gradient (saddle_graph.cpp:173-174)
+            return kNone;
+        }
+    }
+}
+
+template <typename IdT>
+__global__ void __launch_bounds__(kThreads)
+k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
+       uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, std::uint32_t* __restrict__ indeg,
+       unsigned int* __restrict__ flags) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        std::uint32_t de0;
+        if (jlist) {
+            de0 = jlist[i];
+        } else {
+            const Coord o = unpack(d, srcs[i]);
+            const int a = (o.x & 1) ? 0 : ((o.y & 1) ? 1 : 2);
+            de0 = 3u * static_cast<std::uint32_t>((o.x >> 1) + d.nx * ((o.y >> 1) + d.ny * (o.z >> 1))) + a;
+        }
+        const std::uint32_t s0 = c.succ[de0];
+        const EdgeRef e(de0);
+        std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
+        std::uint32_t pend = 0;
+        int nd = 0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const std::uint32_t f = (s0 >> (3 * p)) & 7u;
+            if (f == 0) continue;
+            const std::uint32_t t = f == 1 ? (kTerm | c.tmap[term_quad(e, p, c.g)])
+                                           : walk_branch(c, succ_edge(e, de0, p, f, c.g), &flags[2]);
+            dd[0] = nd == 0 ? t : dd[0];
+            dd[1] = nd == 1 ? t : dd[1];
+            dd[2] = nd == 2 ? t : dd[2];
+            dd[3] = nd == 3 ? t : dd[3];
+            ++nd;
+            if (!(t & kTerm)) {
+                ++pend;
+                atomicAdd(&indeg[t], 1u);
+            }
+        }
+        dest[i] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+        pending[i] = pend;
+    }
+}
+
+__global__ void k_fill_parents(const uint4* __restrict__ dest, std::uint64_t n_nodes,
+                               const std::uint64_t* __restrict__ roff, std::uint32_t* __restrict__ cursor,
+                               std::uint32_t* __restrict__ rsrc) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 d4 = dest[i];
+        const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const std::uint32_t t = dd[b];
+            if (t & kTerm) continue;
+            const std::uint32_t at = atomicAdd(&cursor[t], 1u);
+            rsrc[roff[t] + at] = static_cast<std::uint32_t>(i);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// counting: sparse count vectors, "last child continues"
+// ---------------------------------------------------------------------------------
+// P(j) record, 32 bytes: kind 0 = inline (len <= 2: k0/c0, k1/c1), kind 1 = pool
+// (c0 = offset of len sorted entries; offsets and capacities are multiples of 4 so
+// keys load as aligned uint4 chunks and counts as uint4 pairs).
+struct alignas(16) JRec {
+    std::uint32_t len, k0, k1, kind;
+    std::uint64_t c0, c1;
+};
+
+struct PoolRef {
+    std::uint32_t* key;
+    std::uint64_t* cnt;
+    unsigned long long* top;  // kArenas counters
+    std::uint64_t arena_cap;  // multiple of 4
+};
+
+template <bool kL2, typename T>
+__device__ __forceinline__ T ld(const T* p) {
+    return kL2 ? __ldcg(p) : __ldg(p);
+}
+
+template <bool kL2>
+__device__ __forceinline__ JRec load_rec(const JRec* r) {
+    const uint4 a = ld<kL2>(reinterpret_cast<const uint4*>(r));
+    const uint4 b = ld<kL2>(reinterpret_cast<const uint4*>(r) + 1);
+    JRec o;
+    o.len = a.x;
+    o.k0 = a.y;
+    o.k1 = a.z;
+    o.kind = a.w;
+    o.c0 = static_cast<std::uint64_t>(b.x) | (static_cast<std::uint64_t>(b.y) << 32);
+    o.c1 = static_cast<std::uint64_t>(b.z) | (static_cast<std::uint64_t>(b.w) << 32);
+    return o;
+}
+
+// Store P(u): inline (kind 0) or a pool reference (kind 1).
+__device__ __forceinline__ void store_rec(JRec* rec, std::uint32_t u, std::uint32_t len, std::uint32_t kind,
+                                          std::uint32_t k0, std::uint32_t k1, std::uint64_t c0, std::uint64_t c1) {
+    uint4* dst = reinterpret_cast<uint4*>(rec + u);
+    dst[0] = make_uint4(len, k0, k1, kind);
+    dst[1] = make_uint4(static_cast<std::uint32_t>(c0), static_cast<std::uint32_t>(c0 >> 32),
+                        static_cast<std::uint32_t>(c1), static_cast<std::uint32_t>(c1 >> 32));
+}
+
+// Up to four sorted input lists of one node.  Inside k_count they were written by
+// other SMs during the same launch, so they are read through the L2 (kL2).
+struct Inputs {
+    std::uint32_t len[4];
+    std::uint32_t k0[4], k1[4];
+    std::uint64_t c0[4], c1[4];
+    std::uint64_t off[4];  // kBadOff: inline
+};
+
+template <bool kL2>
+__device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ rec, Inputs& in) {
+    const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const std::uint32_t t = dd[b];
+        in.len[b] = 0;
+        in.k0[b] = in.k1[b] = 0;
+        in.c0[b] = in.c1[b] = 0;
+        in.off[b] = kBadOff;
+        if (t == kNone) continue;
+        if (t & kTerm) {
+            in.len[b] = 1;
+            in.k0[b] = t & ~kTerm;
+            in.c0[b] = 1;
+        } else {
+            const JRec r = load_rec<kL2>(rec + t);
+            in.len[b] = r.len;
+            if (r.kind == 0) {
+                in.k0[b] = r.k0;
+                in.k1[b] = r.k1;
+                in.c0[b] = r.c0;
+                in.c1[b] = r.c1;
+            } else {
+                in.off[b] = r.c0;
+                if (r.c0 == kBadOff) in.len[b] = 0;  // pool exhausted: the host reruns
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool add_ovf(std::uint64_t a, std::uint64_t b, std::uint64_t* r) {
+    *r = a + b;
+    return *r < a;
+}
+
+// Merge the inputs straight from memory; emit(out_index, key, count) per output
+// entry; returns the output length.  Used where staging does not apply (k_count_write,
+// inputs larger than a warp buffer).  Keys are 2-saddle ranks (< 2^31), so
+// 0xffffffff marks an exhausted list.
+template <bool kL2, typename Emit>
+__device__ __forceinline__ std::uint32_t merge(const Inputs& in, const PoolRef& pool, bool* ovf, Emit emit) {
+    std::uint32_t pos[4] = {0, 0, 0, 0};
+    std::uint32_t kk[4];
+    auto key_at = [&](int b, std::uint32_t q) -> std::uint32_t {
+        if (q >= in.len[b]) return 0xffffffffu;
+        return in.off[b] != kBadOff ? ld<kL2>(pool.key + in.off[b] + q) : (q == 0 ? in.k0[b] : in.k1[b]);
+    };
+#pragma unroll
+    for (int b = 0; b < 4; ++b) kk[b] = key_at(b, 0);
+    std::uint32_t out = 0;
+    for (;;) {
+        const std::uint32_t best = min(min(kk[0], kk[1]), min(kk[2], kk[3]));
+        if (best == 0xffffffffu) break;
+        std::uint64_t sum = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (kk[b] != best) continue;
+            const std::uint64_t c = in.off[b] != kBadOff ? ld<kL2>(pool.cnt + in.off[b] + pos[b])
+                                                         : (pos[b] == 0 ? in.c0[b] : in.c1[b]);
+            *ovf |= add_ovf(sum, c, &sum);
+            ++pos[b];
+            kk[b] = key_at(b, pos[b]);
+        }
+        emit(out, best, sum);
+        ++out;
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------------
+// staged merges: every lane's inputs copied to a per-warp shared buffer first
+// ---------------------------------------------------------------------------------
+// A merge read straight from memory is a chain of dependent L2 loads (~0.5 us per
+// entry); in the later rounds of Kahn's algorithm (long vectors in the smooth parts
+// of the field) such chains decide the length of every round.  Instead each lane
+// copies its <= 4 inputs into its slice of a per-warp shared buffer with
+// independent 16-byte loads (all in flight at once), then merges from shared memory.
+constexpr int kWarpCap = 1024;  // entries per warp buffer (larger inputs: direct merge)
+
+struct alignas(16) WarpBuf {
+    std::uint64_t cnt[kWarpCap];
+    std::uint32_t key[kWarpCap];
+};
+
+// Slot of list b in the lane's staging area: lists start at multiples of 4 entries
+// (16-byte aligned for the asynchronous copies).
+__device__ __forceinline__ std::uint32_t staged_size(const Inputs& in) {
+    return ((in.len[0] + 3u) & ~3u) + ((in.len[1] + 3u) & ~3u) + ((in.len[2] + 3u) & ~3u) + ((in.len[3] + 3u) & ~3u);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Copy this lane's inputs to wb[base ...) (base a multiple of 4): pool lists by
+// asynchronous 16-byte copies (no registers, all in flight at once), inline ones
+// by plain stores.  The caller waits with cp_async_wait_all + __syncwarp.
+template <bool kCounts>
+__device__ __forceinline__ void stage(const Inputs& in, const PoolRef& pool, WarpBuf& wb, std::uint32_t base) {
+    std::uint32_t at = base;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const std::uint32_t n = in.len[b];
+        if (in.off[b] == kBadOff) {
+            if (n > 0) {
+                wb.key[at] = in.k0[b];
+                if (kCounts) wb.cnt[at] = in.c0[b];
+            }
+            if (n > 1) {
+                wb.key[at + 1] = in.k1[b];
+                if (kCounts) wb.cnt[at + 1] = in.c1[b];
+            }
+        } else {
+            for (std::uint32_t q = 0; q < n; q += 4) cp_async16(&wb.key[at + q], pool.key + in.off[b] + q);
+            if (kCounts)
+                for (std::uint32_t q = 0; q < n; q += 2) cp_async16(&wb.cnt[at + q], pool.cnt + in.off[b] + q);
+        }
+        at += (n + 3u) & ~3u;
+    }
+}
+
+// Merge the staged lists of this lane; emit(out_index, key, count).
+template <bool kCounts, typename Emit>
+__device__ __forceinline__ std::uint32_t merge_staged(const Inputs& in, const WarpBuf& wb, std::uint32_t base,
+                                                      bool* ovf, Emit emit) {
+    std::uint32_t pos[4], end[4], kk[4];
+    std::uint32_t at = base;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        pos[b] = at;
+        end[b] = at + in.len[b];
+        kk[b] = pos[b] < end[b] ? wb.key[pos[b]] : 0xffffffffu;
+        at += (in.len[b] + 3u) & ~3u;
+    }
+    std::uint32_t out = 0;
+    for (;;) {
+        const std::uint32_t best = min(min(kk[0], kk[1]), min(kk[2], kk[3]));
+        if (best == 0xffffffffu) break;
+        std::uint64_t sum = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (kk[b] != best) continue;
+            if (kCounts) *ovf |= add_ovf(sum, wb.cnt[pos[b]], &sum);
+            ++pos[b];
+            kk[b] = pos[b] < end[b] ? wb.key[pos[b]] : 0xffffffffu;
+        }
+        emit(out, best, sum);
+        ++out;
+    }
+    return out;
+}
+
+// Pool allocation: all 32 lanes call (len 0 for lanes that need nothing); one
+// atomic per warp on the warp's arena; len rounded up to a multiple of 4.
+__device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, std::uint32_t len, unsigned int* full) {
+    const int arena = static_cast<int>(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % kArenas);
+    const std::uint32_t want = (len + 3u) & ~3u;
+    const unsigned long long at = warp_reserve(&pool.top[arena], want);
+    if (len == 0) return kBadOff;
+    if (at + want > pool.arena_cap) {
+        *full = 1u;
+        return kBadOff;
+    }
+    return static_cast<std::uint64_t>(arena) * pool.arena_cap + at;
+}
+
+struct CountArgs {
+    const uint4* dest;           // nj junctions, then n1 sources
+    std::uint32_t* pending;      // live counters (nj + n1)
+    const std::uint32_t* pending0;
+    const std::uint64_t* roff;   // junction parent lists
+    const std::uint32_t* rcnt;
+    const std::uint32_t* rsrc;
+    JRec* rec;
+    PoolRef pool;
+    std::uint32_t* slen;
+    std::uint64_t nj, n1;
+    std::uint32_t* fa;
+    std::uint32_t* fb;
+    unsigned long long* cnt;   // 3 frontier counters
+    unsigned long long* stats; // [0] rounds
+    unsigned long long* done;  // junctions evaluated
+    unsigned int* flags;       // [0] overflow, [1] pool exhausted
+    unsigned long long* diag;  // optional per-round maxima (development diagnostics)
+};
+
+__device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::uint32_t* total) {
+    const int lane = threadIdx.x & 31;
+    std::uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    *total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
+}
+
+// One warp iteration: lane `valid` holds node u.  Merge its branch vectors (staged
+// in shared memory); junctions store P(u) -- inline when it has <= 2 input entries,
+// else in pool space sized by the input length (single pass) -- and release their
+// parents; parents that reach zero pending children are appended to the next
+// frontier.  1-saddles record their merged length.  All lanes call.
+template <bool kChain>
+__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, bool valid, std::uint32_t u,
+                                                    std::uint32_t* nxt, unsigned long long* next_cnt,
+                                                    unsigned long long& done, bool prof) {
+    const int lane = threadIdx.x & 31;
+    prof = prof && a.diag != nullptr;
+    long long t_0 = prof ? clock64() : 0;
+    auto lap = [&](int k) {
+        if (prof) {
+            __syncwarp();
+            const long long t1 = clock64();
+            if (lane == 0) atomicAdd(&a.diag[900 + k], static_cast<unsigned long long>(t1 - t_0));
+            t_0 = t1;
+        }
+    };
+    Inputs in;
+    bool ovf = false;
+    const bool junction = valid && u < a.nj;
+    std::uint32_t T = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) in.len[b] = 0;
+    std::uint32_t S = 0;  // staged size (lists padded to multiples of 4)
+    if (valid) {
+        gather<true>(a.dest[u], a.rec, in);
+        T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+        S = staged_size(in);
+    }
+    lap(0);
+    const bool pooled = junction && T > 2;
+    const std::uint64_t off = pool_alloc(a.pool, pooled ? T : 0u, &a.flags[1]);
+    std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
+    std::uint64_t* oc = a.pool.cnt + (off == kBadOff ? 0 : off);
+    JRec r;
+    r.k0 = r.k1 = 0;
+    r.c0 = r.c1 = 0;
+    auto emit = [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
+        if (pooled) {
+            if (off != kBadOff) {
+                ok[o] = k;
+                oc[o] = c;
+            }
+        } else if (o == 0) {
+            r.k0 = k;
+            r.c0 = c;
+        } else {
+            r.k1 = k;
+            r.c1 = c;
+        }
+    };
+    auto finish = [&](std::uint32_t len) {
+        if (!junction) a.slen[u - a.nj] = len;
+        else if (pooled) store_rec(a.rec, u, len, 1u, 0u, 0u, off, 0ull);
+        else store_rec(a.rec, u, len, 0u, r.k0, r.k1, r.c0, r.c1);
+    };
+    lap(1);
+    // inputs larger than the warp buffer: direct merge
+    if (valid && S > kWarpCap) {
+        const std::uint32_t len = junction ? merge<true>(in, a.pool, &ovf, emit)
+                                           : merge<true>(in, a.pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
+        finish(len);
+    }
+    // staged merges, in batches that fit the buffer
+    unsigned todo = __ballot_sync(0xffffffffu, valid && S <= kWarpCap);
+    while (todo) {
+        const bool mine = (todo >> lane) & 1u;
+        std::uint32_t total = 0;
+        const std::uint32_t base = warp_excl_scan(mine ? S : 0u, &total);
+        const bool go = mine && base + S <= kWarpCap;
+        if (go) {
+            if (junction) stage<true>(in, a.pool, wb, base);
+            else stage<false>(in, a.pool, wb, base);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        lap(2);
+        if (go) {
+            const std::uint32_t len =
+                junction ? merge_staged<true>(in, wb, base, &ovf, emit)
+                         : merge_staged<false>(in, wb, base, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
+            finish(len);
+        }
+        __syncwarp();
+        lap(3);
+        todo &= ~__ballot_sync(0xffffffffu, go);
+    }
+    if (junction) ++done;
+    if (ovf) a.flags[0] = 1u;
+    // release parents (visible to the next round through the grid barrier)
+    std::uint64_t r0 = 0;
+    std::uint32_t rn = 0;
+    if (junction) {
+        r0 = a.roff[u];
+        rn = a.rcnt[u];
+    }
+    if (a.diag) {
+        if (T) atomicMax(&a.diag[0], static_cast<unsigned long long>(T));
+        if (rn) atomicMax(&a.diag[1], static_cast<unsigned long long>(rn));
+        if (T > kWarpCap) atomicAdd(&a.diag[2], 1ull);
+    }
+    // kChain: the lane continues with the first parent it releases (no barrier in
+    // between), so its writes must be released before the decrements and the other
+    // children's writes acquired after them.
+    if (kChain) __threadfence();
+    std::uint32_t next = kNone;
+    // four parents per step, their decrements issued back to back
+    for (;;) {
+        std::uint32_t p[4], old[4];
+        const std::uint32_t m = rn < 4 ? rn : 4u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = k < static_cast<int>(m) ? a.rsrc[r0 + k] : kNone;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
+        r0 += m;
+        rn -= m;
+        unsigned rel = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rel |= (old[k] == 1u ? 1u : 0u) << k;
+        if (kChain && rel && next == kNone) {
+            const int k0 = __ffs(rel) - 1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k == k0) next = p[k];
+            rel &= rel - 1;
+        }
+        const unsigned long long q = warp_reserve(next_cnt, __popc(rel));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((rel >> k) & 1u) nxt[q + __popc(rel & ((1u << k) - 1u))] = p[k];
+        if (!__any_sync(0xffffffffu, rn != 0)) break;
+    }
+    if (kChain && next != kNone) __threadfence();
+    lap(4);
+    if (prof && lane == 0) atomicAdd(&a.diag[910], 1ull);
+    return next;
+}
+
+// Round 0: every node without pending children, in index order; then the frontiers.
+__global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
+    extern __shared__ WarpBuf s_wb[];
+    WarpBuf& wb = s_wb[threadIdx.x >> 5];
+    cg::grid_group grid = cg::this_grid();
+    unsigned long long done = 0;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    const std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+    const int lane = threadIdx.x & 31;
+    std::uint32_t* cur = a.fa;
+    std::uint32_t* nxt = a.fb;
+    const std::uint64_t total = a.nj + a.n1;
+    if (grid.thread_rank() == 0) a.stats[1] = gtimer();
+    for (std::uint64_t base = wbase; base < total; base += stride) {
+        const std::uint64_t i = base + lane;
+        const bool valid = i < total && a.pending0[i] == 0;
+        count_iter<false>(a, wb, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false);
+    }
+    grid.sync();
+    int round = 1;
+    unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
+    {
+        std::uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    while (ncur) {
+        unsigned long long* next_cnt = &a.cnt[(round + 1) % 3];
+        if (grid.thread_rank() == 0) {
+            a.cnt[(round + 2) % 3] = 0;
+            if (round < kTimeline) a.stats[1 + round] = gtimer();
+        }
+        for (std::uint64_t base = wbase; base < ncur; base += stride) {
+            const std::uint64_t f = base + lane;
+            const bool valid = f < ncur;
+            count_iter<false>(a, wb, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12);
+        }
+        grid.sync();
+        if (a.diag && grid.thread_rank() == 0 && round < kTimeline) {
+            a.diag[4 + 3 * round] = a.diag[0];
+            a.diag[5 + 3 * round] = a.diag[1];
+            a.diag[6 + 3 * round] = ncur;
+            a.diag[0] = a.diag[1] = a.diag[2] = 0;
+        }
+        grid.sync();
+        ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
+        ++round;
+        std::uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
+    if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.done, done);
+    if (grid.thread_rank() == 0) {
+        a.stats[0] = static_cast<unsigned long long>(round);
+        if (round < kTimeline) a.stats[1 + round] = gtimer();
+    }
+}
+
+__global__ void k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __restrict__ rec,
+                              PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
+                              std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
+                              std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Inputs in;
+        gather<false>(sdest[i], rec, in);
+        const std::uint64_t at = off[i];
+        bool ovf = false;
+        const std::uint32_t one = base_one + static_cast<std::uint32_t>(i);
+        merge<false>(in, pool, &ovf, [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
+            o_one[at + o] = one;
+            o_two[at + o] = base_two + k;
+            o_cnt[at + o] = c;
+        });
+        if (ovf) flags[0] = 1u;
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+// host wrappers
+// ---------------------------------------------------------------------------------
+namespace {
+EGrid egrid(const Dims& d) {
+    return EGrid{static_cast<std::uint32_t>(d.nx), static_cast<std::uint32_t>(d.nx * d.ny)};
+}
+}  // namespace
+
+int launch_succ_table(const std::uint8_t* codes, const Dims& d, std::uint16_t* succ, cudaStream_t s, int num_sms) {
+    const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
+    if (rows == 0) return MSC3D_OK;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(rows, static_cast<std::uint64_t>(num_sms) * 32));
+    k_succ_table<<<grid, 128, 0, s>>>(codes, d, succ);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int coop_blocks(const void* fn, int num_sms, int* grid, std::size_t smem = 0) {
+    int per_sm = 0;
+    MSC3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    if (per_sm <= 0) return MSC3D_ERR_CUDA;
+    *grid = per_sm * num_sms;
+    return MSC3D_OK;
+}
+
+int launch_reach(const std::uint16_t* succ, const Dims& d, unsigned int* bitmap, std::uint32_t* fa,
+                 std::uint32_t* fb, unsigned long long* cnt, unsigned long long* stats, cudaStream_t s,
+                 int num_sms) {
+    int grid = 0;
+    const int rc = coop_blocks(reinterpret_cast<const void*>(k_reach), num_sms, &grid);
+    if (rc != MSC3D_OK) return rc;
+    EGrid g = egrid(d);
+    void* args[] = {&succ, &g, &bitmap, &fa, &fb, &cnt, &stats};
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_reach), dim3(grid), dim3(kThreads),
+                                               args, 0, s));
+    count_launch();
+    return MSC3D_OK;
+}
+
+int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, std::uint64_t nwords,
+                         unsigned int* jbits, std::uint32_t* jcnt, unsigned long long* nodes, cudaStream_t s,
+                         int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    k_junction_bits<<<grid_for(nwords, num_sms, 16), kThreads, 0, s>>>(succ, bitmap, nwords, jbits, jcnt, nodes);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff,
+                         std::uint32_t* jlist, cudaStream_t s, int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    k_junction_list<<<grid_for(nwords, num_sms, 16), kThreads, 0, s>>>(jbits, nwords, woff, jlist);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
+                const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
+                std::uint64_t n, std::uint32_t* dest, std::uint32_t* pending, std::uint32_t* indeg,
+                unsigned int* flags, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
+    uint4* d4 = reinterpret_cast<uint4*>(dest);
+    if (id_width == 4)
+        k_walk<std::uint32_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
+            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, d4, pending, indeg, flags);
+    else
+        k_walk<std::uint64_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
+            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, d4, pending, indeg, flags);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_fill_parents(const std::uint32_t* dest, std::uint64_t n_nodes, const std::uint64_t* roff,
+                        std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms) {
+    if (n_nodes == 0) return MSC3D_OK;
+    k_fill_parents<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(reinterpret_cast<const uint4*>(dest), n_nodes,
+                                                                  roff, cursor, rsrc);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int count_rec_bytes() { return static_cast<int>(sizeof(JRec)); }
+int count_arenas() { return kArenas; }
+
+int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
+    CountArgs a;
+    a.dest = reinterpret_cast<const uint4*>(L.dest);
+    a.pending = L.pending;
+    a.pending0 = L.pending0;
+    a.roff = L.roff;
+    a.rcnt = L.rcnt;
+    a.rsrc = L.rsrc;
+    a.rec = static_cast<JRec*>(L.rec);
+    a.pool = PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
+    a.slen = L.slen;
+    a.nj = L.nj;
+    a.n1 = L.n1;
+    a.fa = L.fa;
+    a.fb = L.fb;
+    a.cnt = L.cnt;
+    a.stats = L.stats;
+    a.done = L.done;
+    a.flags = L.flags;
+    a.diag = L.diag;
+    if (L.nj + L.n1 == 0) return MSC3D_OK;
+    const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int grid = 0;
+    const int rc = coop_blocks(reinterpret_cast<const void*>(k_count), num_sms, &grid, smem);
+    if (rc != MSC3D_OK) return rc;
+    void* args[] = {&a};
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_count), dim3(grid), dim3(kThreads),
+                                               args, smem, s));
+    count_launch();
+    return MSC3D_OK;
+}
+
+int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
+                       std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
+                       int num_sms) {
+    if (L.n1 == 0) return MSC3D_OK;
+    const uint4* sdest = reinterpret_cast<const uint4*>(L.dest) + L.nj;
+    k_count_write<<<grid_for(L.n1, num_sms, 8), kThreads, 0, s>>>(
+        sdest, L.n1, static_cast<const JRec*>(L.rec), PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap}, off,
+        o_one, o_two, o_cnt, base_one, base_two, L.flags);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+}  // namespace msc3d_dev

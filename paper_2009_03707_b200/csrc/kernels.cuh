@@ -148,3 +148,50 @@ int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint3
                          const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,
                          std::uint64_t* amult, cudaStream_t s, int num_sms);
 }  // namespace msc3d_dev
+
+namespace msc3d_dev {
+// dag.cu -- successor table, reachability, junction ranks, branch walks, counting
+struct CountLaunch {
+    const std::uint32_t* dest;      // uint4 per node: nj junctions, then n1 1-saddles
+    std::uint32_t* pending;
+    const std::uint32_t* pending0;
+    const std::uint64_t* roff;
+    const std::uint32_t* rcnt;
+    const std::uint32_t* rsrc;
+    void* rec;                      // count_rec_bytes() per junction
+    std::uint32_t* pool_key;
+    std::uint64_t* pool_cnt;
+    unsigned long long* pool_top;   // count_arenas() counters
+    std::uint64_t arena_cap;
+    std::uint32_t* slen;
+    std::uint64_t nj, n1;
+    std::uint32_t* fa;              // frontier buffers (nj + n1 each)
+    std::uint32_t* fb;
+    unsigned long long* cnt;        // 3 counters
+    unsigned long long* stats;      // [0] rounds
+    unsigned long long* done;
+    unsigned int* flags;            // [0] overflow [1] pool exhausted
+    unsigned long long* diag;       // optional development diagnostics (nullptr: off)
+};
+int count_rec_bytes();
+int count_arenas();
+int launch_succ_table(const std::uint8_t* codes, const Dims& d, std::uint16_t* succ, cudaStream_t s, int num_sms);
+int launch_reach(const std::uint16_t* succ, const Dims& d, unsigned int* bitmap, std::uint32_t* fa,
+                 std::uint32_t* fb, unsigned long long* cnt, unsigned long long* stats, cudaStream_t s,
+                 int num_sms);
+int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, std::uint64_t nwords,
+                         unsigned int* jbits, std::uint32_t* jcnt, unsigned long long* nodes, cudaStream_t s,
+                         int num_sms);
+int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff,
+                         std::uint32_t* jlist, cudaStream_t s, int num_sms);
+int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
+                const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
+                std::uint64_t n, std::uint32_t* dest, std::uint32_t* pending, std::uint32_t* indeg,
+                unsigned int* flags, cudaStream_t s, int num_sms);
+int launch_fill_parents(const std::uint32_t* dest, std::uint64_t n_nodes, const std::uint64_t* roff,
+                        std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
+int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms);
+int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
+                       std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
+                       int num_sms);
+}  // namespace msc3d_dev

@@ -1,6 +1,7 @@
 // Stage orchestration: allocation of named device arrays, launch order, and the
 // few host<->device handshakes (output sizes) each stage needs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -168,32 +169,48 @@ std::vector<T> sorted_unique(const T* p, std::uint64_t n) {
     return v;
 }
 
+// Successor table of the current codes (dag.cu): 2 bytes per dense edge.
+int succ_table(msc3d_ctx* ctx) {
+    const Dims& d = ctx->dims;
+    auto* succ = static_cast<std::uint16_t*>(ctx->ensure("succ", 3 * d.n_verts, 2));
+    if (!succ) return MSC3D_ERR_NOMEM;
+    return msc3d_dev::launch_succ_table(ctx->ptr<std::uint8_t>("codes"), d, succ, ctx->stream, ctx->num_sms);
+}
+
 int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");
     const int w = ctx->id_width();
     const std::uint64_t nde = 3 * d.n_verts;
     const std::uint64_t nwords = (nde + 31) / 32;
+    TRY(succ_table(ctx));
     auto* bitmap = static_cast<unsigned int*>(ctx->ensure("visited", nwords, 4));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
     if (!bitmap || !fa || !fb) return MSC3D_ERR_NOMEM;
     MSC3D_CUDA_TRY(cudaMemsetAsync(bitmap, 0, nwords * 4, ctx->stream));
-    auto* cnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 48);
+    auto* cnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 48);     // 3 counters
     auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 51);
-    auto* stats = reinterpret_cast<unsigned long long*>(ctx->d_small + 52);
+    // [0] rounds [1] claims [2 + r] device time at the start of round r (ns)
+    auto* stats = static_cast<unsigned long long*>(ctx->ensure("reach_stats", 2 + 256, 8));
+    if (!stats) return MSC3D_ERR_NOMEM;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(stats, 0, 2 * 8, ctx->stream));
     ctx->h_small[48] = n_src;
-    ctx->h_small[49] = 0;
-    ctx->h_small[50] = 0;
-    ctx->h_small[51] = 0;
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(cnt, &ctx->h_small[48], 4 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (int k = 49; k < 54; ++k) ctx->h_small[k] = 0;
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(cnt, &ctx->h_small[48], 6 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    // seeds: validated 1-saddles, their bits set (saddle_graph.cpp:29-41)
     TRY(msc3d_dev::launch_bfs_sources(codes, d, d_sources, n_src, w, bitmap, fa, bad, ctx->stream,
                                       ctx->num_sms));
-    TRY(msc3d_dev::launch_bfs_persistent(codes, d, bitmap, fa, fb, cnt, stats, ctx->stream, ctx->num_sms));
+    if (n_src)
+        TRY(msc3d_dev::launch_reach(ctx->ptr<std::uint16_t>("succ"), d, bitmap, fa, fb, cnt, stats, ctx->stream,
+                                    ctx->num_sms));
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 52, stats, 2 * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     TRY(ctx->fetch_small(54));
     if (ctx->h_small[51] & 0xffffffffu) return MSC3D_ERR_INVALID;  // saddle_graph.cpp:29-31
-    ctx->scalars["bfs_levels"] = static_cast<std::int64_t>(ctx->h_small[52]);
-    ctx->scalars["dag_nodes"] = static_cast<std::int64_t>(ctx->h_small[53]);
+    const std::int64_t rounds = static_cast<std::int64_t>(ctx->h_small[52]);
+    ctx->h_small[49] = ctx->h_small[53];
+    ctx->scalars["bfs_levels"] = rounds;  // BFS levels
+    ctx->scalars["dag_nodes"] = static_cast<std::int64_t>(n_src + ctx->h_small[49]);
     ctx->scalars["dag_sources"] = static_cast<std::int64_t>(n_src);
     return MSC3D_OK;
 }
@@ -261,7 +278,6 @@ namespace {
 // ids whose positions key the count vectors.  Output ranks into those lists.
 int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& term_list) {
     const Dims& d = ctx->dims;
-    const auto* codes = ctx->ptr<std::uint8_t>("codes");
     const int w = ctx->id_width();
     const cudaStream_t s = ctx->stream;
     const int sms = ctx->num_sms;
@@ -269,42 +285,49 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     const std::uint64_t nwords = (nde + 31) / 32;
     const std::uint64_t n1 = ctx->count(src_list);
     const auto* bitmap = ctx->ptr<unsigned int>("visited");
+    const auto* succ = ctx->ptr<std::uint16_t>("succ");
     auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 26);  // [0] overflow [1] pool [2] cycle
     MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 16, s));
 
+    // junctions: bitmap + per-word ranks + list in dense-edge order
     auto* tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", nde, 4));
-    auto* jidx = static_cast<std::uint32_t*>(ctx->ensure("jidx", nde, 4));
+    auto* jbits = static_cast<unsigned int*>(ctx->ensure("jbits", nwords, 4));
     auto* jcnt = static_cast<std::uint32_t*>(ctx->ensure("jcount", nwords, 4));
-    auto* joff = static_cast<std::uint64_t*>(ctx->ensure("joff", nwords, 8));
-    if (!tmap || !jidx || !jcnt || !joff) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d,
-                                            tmap, s, sms));
-    TRY(msc3d_dev::launch_junction_count(codes, d, bitmap, nwords, jcnt, s, sms));
-    TRY(msc3d_dev::scan_u32(jcnt, nwords, joff, ctx->d_small, ctx->ws, s));
+    auto* woff = static_cast<std::uint64_t*>(ctx->ensure("joff", nwords, 8));
+    if (!tmap || !jbits || !jcnt || !woff) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d, tmap, s, sms));
+    MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 50, 0, 8, s));
+    TRY(msc3d_dev::launch_junction_bits(succ, bitmap, nwords, jbits, jcnt,
+                                        reinterpret_cast<unsigned long long*>(ctx->d_small + 50), s, sms));
+    TRY(msc3d_dev::scan_u32(jcnt, nwords, woff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(1));
     const std::uint64_t nj = ctx->h_small[0];
+    const std::uint64_t nn = nj + n1;
     ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
-    auto* jdest = static_cast<std::uint32_t*>(ctx->ensure("jdest", 4 * nj, 4));
-    auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nj, 4));
-    auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nj, 4));
+    auto* dest = static_cast<std::uint32_t*>(ctx->ensure("jdest", 4 * nn, 4));
+    auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nn, 4));
+    auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nn, 4));
     auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
     auto* roff = static_cast<std::uint64_t*>(ctx->ensure("roff", nj, 8));
     auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("cursor", nj, 4));
-    auto* sdest = static_cast<std::uint32_t*>(ctx->ensure("sdest", 4 * n1, 4));
-    auto* poff = static_cast<std::uint64_t*>(ctx->ensure("poff", nj, 8));
-    auto* plen = static_cast<std::uint32_t*>(ctx->ensure("plen", nj, 4));
+    void* rec = ctx->ensure("jrec", nj, msc3d_dev::count_rec_bytes());
+    auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
+    auto* soff = static_cast<std::uint64_t*>(ctx->ensure("soff", n1, 8));
+    auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!jlist || !jdest || !pending || !pending0 || !indeg || !roff || !cursor || !sdest || !poff ||
-        !plen || !fa || !fb)
+    if (!jlist || !dest || !pending || !pending0 || !indeg || !roff || !cursor || !rec || !slen || !soff ||
+        !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_junction_write(codes, d, bitmap, nwords, joff, jlist, jidx, s, sms));
+    TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
+
+    // branch walks (saddle_graph.cpp:139-202): destinations, pending children, in-degrees
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_origin_dests(codes, d, jlist, nullptr, w, nj, jidx, tmap, jdest, pending,
-                                       indeg, flags, s, sms));
-    TRY(msc3d_dev::launch_origin_dests(codes, d, nullptr, ctx->ptr<void>(src_list), w, n1, jidx, tmap,
-                                       sdest, nullptr, nullptr, flags, s, sms));
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, dest, pending, indeg, flags, s,
+                               sms));
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, ctx->ptr<void>(src_list), w, n1, dest + 4 * nj,
+                               pending + nj, indeg, flags, s, sms));
     TRY(msc3d_dev::scan_u32(indeg, nj, roff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(28));
     if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle
@@ -312,46 +335,73 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", nrev, 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_fill_rev(jdest, nj, roff, cursor, rsrc, s, sms));
-    if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nj * 4, cudaMemcpyDeviceToDevice, s));
+    TRY(msc3d_dev::launch_fill_parents(dest, nn, roff, cursor, rsrc, s, sms));
+    if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nn * 4, cudaMemcpyDeviceToDevice, s));
 
-    // Kahn over the junction graph, sinks first; grow the pool and rerun on overflow.
+    // count vectors, "last child continues"; grow the pool and rerun if it ran out
     const std::uint64_t m = static_cast<std::uint64_t>(ctx->scalars["dag_nodes"]);
-    std::uint64_t pcap = std::max<std::uint64_t>(1u << 20, m + m / 2);
-    auto* ptop = reinterpret_cast<unsigned long long*>(ctx->d_small + 55);
-    auto* kcnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 56);   // 3 counters
-    auto* kstats = reinterpret_cast<unsigned long long*>(ctx->d_small + 59); // 2
-    std::uint32_t* pkey = nullptr;
-    std::uint64_t* pcnt = nullptr;
+    const std::uint64_t arenas = static_cast<std::uint64_t>(msc3d_dev::count_arenas());
+    // pool space is reserved per junction by its input length (rounded up to 4)
+    std::uint64_t pcap = std::max<std::uint64_t>(arenas << 16, m + m / 2);
+    auto* kcnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 55);  // 3 counters
+    // [0] rounds [1 + r] device time at the start of round r (ns)
+    auto* kstats = static_cast<unsigned long long*>(ctx->ensure("count_stats", 1 + 256, 8));
+    if (!kstats) return MSC3D_ERR_NOMEM;
+    auto* done = reinterpret_cast<unsigned long long*>(ctx->d_small + 59);
+    msc3d_dev::CountLaunch L{};
     for (int attempt = 0;; ++attempt) {
-        pkey = static_cast<std::uint32_t*>(ctx->ensure("pool_key", pcap, 4));
-        pcnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
-        if (!pkey || !pcnt) return MSC3D_ERR_NOMEM;
+        L.pool_key = static_cast<std::uint32_t*>(ctx->ensure("pool_key", pcap, 4));
+        L.pool_cnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
+        if (!L.pool_key || !L.pool_cnt) return MSC3D_ERR_NOMEM;
+        L.dest = dest;
+        L.pending = pending;
+        L.pending0 = pending0;
+        L.roff = roff;
+        L.rcnt = indeg;
+        L.rsrc = rsrc;
+        L.rec = rec;
+        L.pool_top = ptop;
+        L.arena_cap = (pcap / arenas) & ~3ull;
+        L.slen = slen;
+        L.nj = nj;
+        L.n1 = n1;
+        L.fa = fa;
+        L.fb = fb;
+        L.cnt = kcnt;
+        L.stats = kstats;
+        L.done = done;
+        L.flags = flags;
+        L.diag = nullptr;
+        if (std::getenv("MSC3D_DIAG")) {
+            L.diag = static_cast<unsigned long long*>(ctx->ensure("count_diag", 1024, 8));
+            if (L.diag) MSC3D_CUDA_TRY(cudaMemsetAsync(L.diag, 0, 1024 * 8, s));
+        }
         MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
-        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 55, 0, 6 * 8, s));
-        if (nj) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nj * 4, cudaMemcpyDeviceToDevice, s));
-        TRY(msc3d_dev::launch_initial_frontier(pending, nj, fa, kcnt, s, sms));
-        if (nj)
-            TRY(msc3d_dev::launch_kahn_persistent(jdest, poff, plen, pkey, pcnt, ptop, pcap, roff, indeg,
-                                                  rsrc, pending, fa, fb, kcnt, flags, kstats, s, sms));
-        TRY(ctx->fetch_small(61));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ptop, 0, arenas * 8, s));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 55, 0, 5 * 8, s));
+        if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nn * 4, cudaMemcpyDeviceToDevice, s));
+        TRY(msc3d_dev::launch_count(L, s, sms));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 58, kstats, 8, cudaMemcpyDeviceToDevice, s));
+        TRY(ctx->fetch_small(60));
+        ctx->scalars["count_levels"] = static_cast<std::int64_t>(ctx->h_small[58]);
         const unsigned int pool_full = static_cast<unsigned int>(ctx->h_small[26] >> 32);
         if (pool_full) {
             if (attempt > 8) return MSC3D_ERR_NOMEM;
-            pcap = std::max<std::uint64_t>(2 * pcap, ctx->h_small[55] + ctx->h_small[55] / 4);
+            pcap *= 2;
             continue;
         }
-        if (nj && ctx->h_small[60] != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
+        if (ctx->h_small[59] != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
         break;
     }
-    ctx->scalars["count_levels"] = nj ? static_cast<std::int64_t>(ctx->h_small[59]) : 0;
-    ctx->scalars["pool_entries"] = static_cast<std::int64_t>(ctx->h_small[55]);
+    {
+        std::vector<unsigned long long> tops(arenas);
+        MSC3D_CUDA_TRY(cudaMemcpy(tops.data(), ptop, arenas * 8, cudaMemcpyDeviceToHost));
+        std::uint64_t used = 0;
+        for (auto t : tops) used += t;
+        ctx->scalars["pool_entries"] = static_cast<std::int64_t>(used);
+    }
 
-    // 1-saddles: lengths, offsets, write
-    auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
-    auto* soff = static_cast<std::uint64_t*>(ctx->ensure("soff", n1, 8));
-    if (!slen || !soff) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_source_len(sdest, n1, poff, plen, pkey, pcnt, slen, flags, s, sms));
+    // 1-saddles: offsets, sorted output
     TRY(msc3d_dev::scan_u32(slen, n1, soff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(27));
     if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
@@ -360,7 +410,10 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     auto* o2 = static_cast<std::uint32_t*>(ctx->ensure("ss_two_rank", nout, 4));
     auto* oc = static_cast<std::uint64_t*>(ctx->ensure("ss_paths", nout, 8));
     if (!o1 || !o2 || !oc) return MSC3D_ERR_NOMEM;
-    return msc3d_dev::launch_source_write(sdest, n1, poff, plen, pkey, pcnt, soff, o1, o2, oc, flags, s, sms);
+    TRY(msc3d_dev::launch_count_write(L, soff, o1, o2, oc, 0, 0, s, sms));
+    TRY(ctx->fetch_small(27));
+    if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
+    return MSC3D_OK;
 }
 
 }  // namespace
