@@ -174,6 +174,76 @@ __device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* c
     return base + incl - n;
 }
 
+// Frontier appends through a per-warp shared-memory queue: one global reservation
+// per block per round (flush_block) instead of one per warp iteration -- a single
+// frontier counter hit by every warp of the grid serialises in the L2.  A warp
+// queue that fills up mid-round is flushed on its own.
+constexpr int kQCap = 256;
+
+struct WarpQ {
+    std::uint32_t item[kQCap];
+    std::uint32_t n;
+};
+
+__device__ __forceinline__ void flush_warp(WarpQ& q, std::uint32_t* out, unsigned long long* ctr) {
+    const int lane = threadIdx.x & 31;
+    const std::uint32_t n = q.n;
+    unsigned long long base = 0;
+    if (lane == 0 && n) base = atomicAdd(ctr, static_cast<unsigned long long>(n));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (std::uint32_t k = lane; k < n; k += 32) out[base + k] = q.item[k];
+    __syncwarp();
+    if (lane == 0) q.n = 0;
+    __syncwarp();
+}
+
+// All lanes call; lane pushes the items[k] with bit k of `mask` set (k < 4).
+__device__ __forceinline__ void warp_push(WarpQ& q, const std::uint32_t* items, unsigned mask, std::uint32_t* out,
+                                          unsigned long long* ctr) {
+    const int lane = threadIdx.x & 31;
+    const unsigned mine = __popc(mask);
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    if (q.n + total > kQCap) flush_warp(q, out, ctr);
+    std::uint32_t at = q.n + incl - mine;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if ((mask >> k) & 1u) q.item[at++] = items[k];
+    __syncwarp();
+    if (lane == 0) q.n += total;
+    __syncwarp();
+}
+
+// All threads of the block call (before the grid barrier): one reservation for
+// every warp queue of the block.
+__device__ __forceinline__ void flush_block(WarpQ* qs, std::uint32_t* out, unsigned long long* ctr) {
+    __shared__ unsigned long long s_base[kThreads / 32 + 1];
+    __syncthreads();
+    const int nw = blockDim.x / 32;
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            s_base[w] = tot;
+            tot += qs[w].n;
+        }
+        const unsigned long long b = tot ? atomicAdd(ctr, tot) : 0ull;
+        for (int w = 0; w < nw; ++w) s_base[w] += b;
+    }
+    __syncthreads();
+    WarpQ& q = qs[threadIdx.x >> 5];
+    const unsigned long long base = s_base[threadIdx.x >> 5];
+    for (std::uint32_t k = threadIdx.x & 31; k < q.n; k += 32) out[base + k] = q.item[k];
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) q.n = 0;
+    __syncthreads();
+}
+
 // cnt[0] = number of (already claimed) seeds in fa; cnt[1], cnt[2] scratch.
 // stats[0] = rounds, stats[1] = nodes claimed here.  Level-synchronous: one
 // round per BFS level, 32 nodes per warp iteration, one reservation per iteration.
@@ -181,6 +251,10 @@ __global__ void __launch_bounds__(kThreads)
 k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restrict__ bitmap,
         std::uint32_t* __restrict__ fa, std::uint32_t* __restrict__ fb, unsigned long long* __restrict__ cnt,
         unsigned long long* __restrict__ stats) {
+    __shared__ WarpQ s_q[kThreads / 32];
+    WarpQ& wq = s_q[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) == 0) wq.n = 0;
+    __syncwarp();
     cg::grid_group grid = cg::this_grid();
     std::uint32_t* cur = fa;
     std::uint32_t* nxt = fb;
@@ -217,11 +291,9 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
                 }
             }
             mine += __popc(won);
-            const unsigned long long at = warp_reserve(next_cnt, __popc(won));
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-                if ((won >> p) & 1u) nxt[at + __popc(won & ((1u << p) - 1u))] = de[p];
+            warp_push(wq, de, won, nxt, next_cnt);
         }
+        flush_block(s_q, nxt, next_cnt);
         grid.sync();
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
         ++round;
@@ -631,7 +703,7 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
 // parents; parents that reach zero pending children are appended to the next
 // frontier.  1-saddles record their merged length.  All lanes call.
 template <bool kChain>
-__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, bool valid, std::uint32_t u,
+__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, bool valid, std::uint32_t u,
                                                     std::uint32_t* nxt, unsigned long long* next_cnt,
                                                     unsigned long long& done, bool prof) {
     const int lane = threadIdx.x & 31;
@@ -754,10 +826,7 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
                 if (k == k0) next = p[k];
             rel &= rel - 1;
         }
-        const unsigned long long q = warp_reserve(next_cnt, __popc(rel));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if ((rel >> k) & 1u) nxt[q + __popc(rel & ((1u << k) - 1u))] = p[k];
+        warp_push(wq, p, rel, nxt, next_cnt);
         if (!__any_sync(0xffffffffu, rn != 0)) break;
     }
     if (kChain && next != kNone) __threadfence();
@@ -770,6 +839,10 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
 __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     extern __shared__ WarpBuf s_wb[];
     WarpBuf& wb = s_wb[threadIdx.x >> 5];
+    __shared__ WarpQ s_q[kThreads / 32];
+    WarpQ& wq = s_q[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) == 0) wq.n = 0;
+    __syncwarp();
     cg::grid_group grid = cg::this_grid();
     unsigned long long done = 0;
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
@@ -782,8 +855,9 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     for (std::uint64_t base = wbase; base < total; base += stride) {
         const std::uint64_t i = base + lane;
         const bool valid = i < total && a.pending0[i] == 0;
-        count_iter<false>(a, wb, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false);
+        count_iter<false>(a, wb, wq, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false);
     }
+    flush_block(s_q, nxt, &a.cnt[1]);
     grid.sync();
     int round = 1;
     unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
@@ -801,8 +875,9 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
         for (std::uint64_t base = wbase; base < ncur; base += stride) {
             const std::uint64_t f = base + lane;
             const bool valid = f < ncur;
-            count_iter<false>(a, wb, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12);
+            count_iter<false>(a, wb, wq, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12);
         }
+        flush_block(s_q, nxt, next_cnt);
         grid.sync();
         if (a.diag && grid.thread_rank() == 0 && round < kTimeline) {
             a.diag[4 + 3 * round] = a.diag[0];
