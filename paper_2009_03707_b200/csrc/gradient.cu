@@ -29,6 +29,8 @@
 // Every cell is written exactly once, by the owner of its maximal vertex (plain
 // byte stores).  The same kernel emits both extremum forests (build_forest,
 // extrema.cpp:43-77) and the per-dimension critical counts.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -384,16 +386,24 @@ struct StarLists {
     unsigned long long* count;  // 3 counters
 };
 
+// Block-level buffers for the large-star work lists: appends are shared-memory
+// atomics; the global list counters are touched once per flush (a counter hit by
+// every thread of the grid serialises in the L2).
+constexpr int kListBuf = 1024;
+
 template <typename T>
 __global__ void __launch_bounds__(NT)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
-           unsigned long long* __restrict__ crit_totals, StarLists lists) {
+           unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles) {
     __shared__ T tile[SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
     __shared__ unsigned long long s_crit[4];
     __shared__ std::uint32_t s_M[27 * NT];
+    __shared__ std::uint32_t s_lb[2][kListBuf];
+    __shared__ std::uint32_t s_ln[2];
+    __shared__ unsigned long long s_base[2];
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
     if (tid < 27) {
         s_fac[tid] = c_slot.facet[tid];
@@ -402,25 +412,43 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                                                 c_slot.off[tid][2] * d.exy);
     }
     if (tid < 4) s_crit[tid] = 0;
-    const std::int64_t x0 = static_cast<std::int64_t>(blockIdx.x) * TX - 1;
-    const std::int64_t y0 = static_cast<std::int64_t>(blockIdx.y) * TY - 1;
-    const std::int64_t z0 = static_cast<std::int64_t>(blockIdx.z) * TZ - 1;
-    for (int i = tid; i < SX * SY * SZ; i += NT) {
-        const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
-        const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        T v = T(0);
-        if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz)
-            v = f[gx + d.nx * (gy + d.ny * gz)];
-        tile[lz][ly][lx] = v;
-    }
-    __syncthreads();
+    if (tid < 2) s_ln[tid] = 0;
+    auto flush_lists = [&]() {  // all threads
+        __syncthreads();
+        if (tid < 2) s_base[tid] = s_ln[tid] ? atomicAdd(&lists.count[tid], static_cast<unsigned long long>(s_ln[tid])) : 0ull;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+            for (std::uint32_t k = tid; k < s_ln[w]; k += NT) lists.list[w][s_base[w] + k] = s_lb[w][k];
+        __syncthreads();
+        if (tid < 2) s_ln[tid] = 0;
+        __syncthreads();
+    };
+    std::uint32_t crit[4] = {0, 0, 0, 0};
+    const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
+    for (std::uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const std::uint64_t tyz = ti / tiles.x;
+        const std::int64_t x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
+        const std::int64_t y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
+        const std::int64_t z0 = static_cast<std::int64_t>(tyz / tiles.y) * TZ - 1;
+        __syncthreads();  // previous tile done with the shared tile / list counts stable
+        if (s_ln[0] + NT > kListBuf || s_ln[1] + NT > kListBuf) flush_lists();
+        for (int i = tid; i < SX * SY * SZ; i += NT) {
+            const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
+            const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+            T v = T(0);
+            if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz)
+                v = f[gx + d.nx * (gy + d.ny * gz)];
+            tile[lz][ly][lx] = v;
+        }
+        __syncthreads();
 
-    auto writer_for = [&](int lid) {
-        const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
+        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
         StarWriter w;
         w.vx = x0 + 1 + lx;
         w.vy = y0 + 1 + ly;
         w.vz = z0 + 1 + lz;
+        if (w.vx >= d.nx || w.vy >= d.ny || w.vz >= d.nz) continue;
         std::uint32_t inr = kAll;
         if (w.vx == 0) inr &= ~kXM;
         if (w.vx == d.nx - 1) inr &= ~kXP;
@@ -435,68 +463,47 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         w.parent0 = parent0;
         w.parent3 = parent3;
         w.ncrit = 0;
-        return w;
-    };
-
-    // ---- phase 1: own vertex: star mask; trivial stars finished here -------------------
-    std::uint64_t ncrit = 0;
-    std::uint32_t S = 0;
-    {
-        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
-        const std::int64_t vx = x0 + 1 + lx, vy = y0 + 1 + ly, vz = z0 + 1 + lz;
-        if (vx < d.nx && vy < d.ny && vz < d.nz) {
-            StarWriter w = writer_for(tid);
-            const T* base = &tile[lz + 1][ly + 1][lx + 1];
-            const T fv = base[0];
-            std::uint32_t below = kCentre;
-#pragma unroll
-            for (int t = 0; t < 27; ++t) {
-                if (t == 13) continue;
-                const T u = base[slot_tile(t)];
-                if (u < fv || (u == fv && t < 13)) below |= 1u << t;
-            }
-            S = below & w.inr;
-            S &= facets_present(S);
-            S &= facets_present(S);
-            const int n = __popc(S);
-            if (n == 1) {  // critical minimum (gradient.cpp:128-131)
-                w.minimum();
-                S = 0;
-            } else if (n == 2) {  // the vertex and its only edge pair up
-                w.pair(13, __ffs(S & ~kCentre) - 1);
-                S = 0;
-            }
-            ncrit = w.ncrit;
-        }
-    }
-    // ---- stars of 3..8 cells: register fast path here; larger stars go to the
-    //      size-specialised list kernels (their registers do not limit this one) ----
-    if (S) {
-        const int n = __popc(S);
-        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
-        StarWriter w = writer_for(tid);
+        // ---- own vertex: star mask; trivial stars finished here
         const T* base = &tile[lz + 1][ly + 1][lx + 1];
-        const unsigned long long vi = static_cast<unsigned long long>(w.vx + d.nx * (w.vy + d.ny * w.vz));
-        if (n <= 8) {
+        const T fv = base[0];
+        std::uint32_t below = kCentre;
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            if (t == 13) continue;
+            const T u = base[slot_tile(t)];
+            if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+        }
+        std::uint32_t S = below & w.inr;
+        S &= facets_present(S);
+        S &= facets_present(S);
+        const int n = __popc(S);
+        const std::uint32_t vi = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+        if (n == 1) {  // critical minimum (gradient.cpp:128-131)
+            w.minimum();
+        } else if (n == 2) {  // the vertex and its only edge pair up
+            w.pair(13, __ffs(S & ~kCentre) - 1);
+        } else if (n <= 8) {
+            // ---- stars of 3..8 cells: register fast path here; larger stars go to the
+            //      size-specialised list kernels (their registers do not limit this one)
             if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, S, n, s_fac, s_cof, &s_M[tid], NT, w)) {
-                const unsigned long long at = atomicAdd(&lists.count[2], 1ull);
-                lists.list[2][at] = static_cast<std::uint32_t>(vi);
+                const unsigned long long at = atomicAdd(&lists.count[2], 1ull);  // ties: rare
+                lists.list[2][at] = vi;
             }
-            ncrit += w.ncrit;
         } else {
             const int which = n <= 16 ? 0 : 1;
-            const unsigned long long at = atomicAdd(&lists.count[which], 1ull);
-            lists.list[which][at] = static_cast<std::uint32_t>(vi);
+            s_lb[which][atomicAdd(&s_ln[which], 1u)] = vi;
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
     }
+    flush_lists();
     if (crit_totals) {
-        std::uint64_t v = ncrit;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((tid & 31) == 0 && v)
-            for (int k = 0; k < 4; ++k) {
-                const unsigned long long c = (v >> (16 * k)) & 0xffffu;
-                if (c) atomicAdd(&s_crit[k], c);
-            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            std::uint32_t v = crit[k];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((tid & 31) == 0 && v) atomicAdd(&s_crit[k], static_cast<unsigned long long>(v));
+        }
         __syncthreads();
         if (tid < 4 && s_crit[tid]) atomicAdd(&crit_totals[tid], s_crit[tid]);
     }
@@ -701,20 +708,23 @@ int launch_gradient(const void* values, int value_type, const Dims& d, std::uint
     MSC3D_CUDA_TRY(cudaMemsetAsync(list_counts, 0, 24, stream));
     StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
     const dim3 block(TX, TY, TZ);
-    const dim3 grid(static_cast<unsigned>((d.nx + TX - 1) / TX),
-                    static_cast<unsigned>((d.ny + TY - 1) / TY),
-                    static_cast<unsigned>((d.nz + TZ - 1) / TZ));
+    const uint3 tiles = make_uint3(static_cast<unsigned>((d.nx + TX - 1) / TX),
+                                   static_cast<unsigned>((d.ny + TY - 1) / TY),
+                                   static_cast<unsigned>((d.nz + TZ - 1) / TZ));
+    const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
+    // persistent tile loop: a few blocks per SM, each walking tiles with stride grid
+    const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(num_sms) * 8)));
     const unsigned lgrid = static_cast<unsigned>(16 * num_sms);
     const unsigned dgrid = static_cast<unsigned>(4 * num_sms);
     if (value_type == MSC3D_VALUE_F64) {
         const double* v = static_cast<const double*>(values);
-        k_gradient<double><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists);
+        k_gradient<double><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, tiles);
         k_gradient_list<16, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
         k_gradient_list<32, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
         k_gradient_deferred<double><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
     } else {
         const float* v = static_cast<const float*>(values);
-        k_gradient<float><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists);
+        k_gradient<float><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, tiles);
         k_gradient_list<16, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
         k_gradient_list<32, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
         k_gradient_deferred<float><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
