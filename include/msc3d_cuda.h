@@ -152,6 +152,29 @@ int msc3d_sp_op(msc3d_ctx* ctx, int op, uint32_t x_rows, uint32_t x_cols, const 
  * StageTimings (gradient, critical, extrema, reachability, counting). */
 int msc3d_ctx_compute(msc3d_ctx* ctx, int options, double* stage_ms);
 
+/* The same pipeline with the results delivered to HOST memory (pinned buffers give
+ * full PCIe/C2C bandwidth): every output is copied on a second stream as soon as it
+ * is final, overlapping the later stages.  Capacities: cp_cell_cap / cp_index_cap in
+ * bytes, arc_cap in arcs; labels_min (n_verts u32) / labels_max (n_cubes u32) only
+ * with MSC3D_OPT_SEGMENTATION (NULL: not copied).  Too small a buffer ->
+ * MSC3D_ERR_INVALID.  On return n_cp / n_arcs hold the sizes; the device arrays of
+ * msc3d_ctx_compute stay valid as well. */
+typedef struct msc3d_host_outputs {
+    void* cp_cell;
+    uint64_t cp_cell_cap;
+    uint8_t* cp_index;
+    uint64_t cp_index_cap;
+    uint32_t* arc_src;
+    uint32_t* arc_dst;
+    uint64_t* arc_mult;
+    uint64_t arc_cap;
+    uint32_t* labels_min;
+    uint32_t* labels_max;
+    uint64_t n_cp;   /* out */
+    uint64_t n_arcs; /* out */
+} msc3d_host_outputs;
+int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out);
+
 /* FNV-1a 64 over the widened f64 samples (msc.cpp:31-42), host-side, of the values
  * last loaded from host memory. */
 uint64_t msc3d_field_hash_f64(const double* values, uint64_t n);

@@ -37,6 +37,14 @@ class Dims(C.Structure):
     _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64)]
 
 
+class HostOutputs(C.Structure):
+    """msc3d_host_outputs (include/msc3d_cuda.h): host buffers for msc3d_ctx_compute_host."""
+    _fields_ = [("cp_cell", C.c_void_p), ("cp_cell_cap", C.c_uint64), ("cp_index", C.c_void_p),
+                ("cp_index_cap", C.c_uint64), ("arc_src", C.c_void_p), ("arc_dst", C.c_void_p),
+                ("arc_mult", C.c_void_p), ("arc_cap", C.c_uint64), ("labels_min", C.c_void_p),
+                ("labels_max", C.c_void_p), ("n_cp", C.c_uint64), ("n_arcs", C.c_uint64)]
+
+
 class IoError(RuntimeError):
     pass
 
@@ -83,6 +91,7 @@ def lib():
         "msc3d_ctx_count": (i32, [vp]),
         "msc3d_ctx_count_minor": (i32, [vp, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp, i32]),
         "msc3d_ctx_compute": (i32, [vp, i32, C.POINTER(C.c_double)]),
+        "msc3d_ctx_compute_host": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_field_hash_f64": (u64, [vp, u64]),
         "msc3d_field_hash_f32": (u64, [vp, u64]),
     }

@@ -339,7 +339,12 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
     k_sort_small_buckets<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, large, n_large);
     count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(h_small, n_large, 8, cudaMemcpyDeviceToHost, s));
+    {  // kernel copy into the mapped host mirror (a DMA would queue behind bulk copies)
+        std::uint64_t* hd = nullptr;
+        MSC3D_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd), h_small, 0));
+        const int rc = launch_small_copy(reinterpret_cast<const std::uint64_t*>(n_large), hd, 1, s);
+        if (rc != MSC3D_OK) return rc;
+    }
     MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
     const std::uint64_t nl = h_small[0];
     if (nl) {
@@ -362,7 +367,12 @@ int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t
     k_sort_small_buckets<<<grid_for(nb, num_sms), kThreads, 0, s>>>(off, nb, total, key, large, n_large);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(h_small, n_large, 8, cudaMemcpyDeviceToHost, s));
+    {  // kernel copy into the mapped host mirror (a DMA would queue behind bulk copies)
+        std::uint64_t* hd = nullptr;
+        MSC3D_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd), h_small, 0));
+        const int rc = launch_small_copy(reinterpret_cast<const std::uint64_t*>(n_large), hd, 1, s);
+        if (rc != MSC3D_OK) return rc;
+    }
     MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
     if (h_small[0]) {
         k_sort_large_buckets<<<static_cast<unsigned>(h_small[0]), 512, 0, s>>>(off, nb, total, large, key, scratch);

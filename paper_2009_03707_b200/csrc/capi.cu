@@ -109,8 +109,9 @@ int msc3d_ctx_create(msc3d_ctx** out, int device) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMalloc(&ctx->d_small, 64 * 8) != cudaSuccess ||
-        cudaMallocHost(&ctx->h_small, 64 * 8) != cudaSuccess) {
+        cudaMalloc(&ctx->d_small, msc3d_ctx::kSmall * 8) != cudaSuccess ||
+        cudaHostAlloc(&ctx->h_small, msc3d_ctx::kSmall * 8, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_small_dev), ctx->h_small, 0) != cudaSuccess) {
         delete ctx;
         return MSC3D_ERR_CUDA;
     }
@@ -348,6 +349,12 @@ int msc3d_ctx_count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, co
                           int id_width) {
     return msc3d_stage::count_minor(ctx, ones, n1, juncs, nj, twos, n2, src, dst, mult, count,
                                     id_width);
+}
+
+int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out) {
+    if (!ctx || !out) return MSC3D_ERR_INVALID;
+    if (!ctx->values) return MSC3D_ERR_STATE;
+    return msc3d_stage::compute(ctx, options, stage_ms, out);
 }
 
 int msc3d_ctx_compute(msc3d_ctx* ctx, int options, double* stage_ms) {

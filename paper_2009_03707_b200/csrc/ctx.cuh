@@ -31,9 +31,17 @@ struct msc3d_ctx {
     std::map<std::string, DevArray> arrays;
     std::map<std::string, std::int64_t> scalars;
     msc3d_dev::Workspace ws, ws2;
-    std::uint64_t* d_small = nullptr;  // 64 u64 of device scratch for totals / flags
-    std::uint64_t* h_small = nullptr;  // pinned mirror
+    static constexpr int kSmall = 256;
+    std::uint64_t* d_small = nullptr;      // kSmall u64 of device scratch for totals / flags
+    std::uint64_t* h_small = nullptr;      // mapped pinned mirror
+    std::uint64_t* h_small_dev = nullptr;  // its device address
     std::uint64_t launches_at_create = 0;
+    cudaStream_t copy = nullptr;  // device-to-host copies overlapping the pipeline
+
+    cudaStream_t copy_stream() {
+        if (!copy && cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking) != cudaSuccess) copy = nullptr;
+        return copy;
+    }
 
     ~msc3d_ctx() {
         for (auto& kv : arrays)
@@ -41,6 +49,7 @@ struct msc3d_ctx {
         if (d_small) cudaFree(d_small);
         if (h_small) cudaFreeHost(h_small);
         if (own_stream && stream) cudaStreamDestroy(stream);
+        if (copy) cudaStreamDestroy(copy);
     }
 
     // Ensure array `name` holds `count` elements of `elem` bytes; contents undefined.
@@ -81,9 +90,12 @@ struct msc3d_ctx {
         if (it != arrays.end()) it->second.count = 0;
     }
     int id_width() const { return dims.n_cells <= 0xffffffffull ? 4 : 8; }
-    // Copy the first n u64 of d_small to h_small and wait.
-    int fetch_small(int n) {
-        if (cudaMemcpyAsync(h_small, d_small, n * 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    // Copy the first n u64 of d_small to h_small and wait.  The copy is a tiny
+    // kernel writing the mapped host mirror over the bus, not a DMA: a DMA would
+    // queue behind bulk device-to-host output copies on the copy engine.
+    int fetch_small(int n) { return fetch_range(0, n); }
+    int fetch_range(int first, int n) {
+        if (msc3d_dev::launch_small_copy(d_small + first, h_small_dev + first, n, stream) != MSC3D_OK)
             return MSC3D_ERR_CUDA;
         if (cudaStreamSynchronize(stream) != cudaSuccess) return MSC3D_ERR_CUDA;
         return MSC3D_OK;

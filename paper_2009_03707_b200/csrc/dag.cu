@@ -383,11 +383,25 @@ __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, std::uint
     }
 }
 
+// Per-node record of the junction graph (64 bytes, one load of four uint4): the
+// <= 4 branch destinations, the parent count, and the first kInlineParents parents
+// inline (the rest in an overflow list), so processing a node costs one dependent
+// load for all of its structure.
+constexpr int kInlineParents = 9;
+constexpr std::uint32_t kSkip = 0xffffffffu;  // pending0 of a contracted pass-through junction
+
+struct alignas(16) NodeRec {
+    std::uint32_t dest[4];
+    std::uint32_t npar;
+    std::uint32_t ov_lo, ov_hi;  // overflow list offset
+    std::uint32_t par[kInlineParents];
+};
+static_assert(sizeof(NodeRec) == 64, "NodeRec is one 64-byte line");
+
 template <typename IdT>
 __global__ void __launch_bounds__(kThreads)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
-       uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, std::uint32_t* __restrict__ indeg,
-       unsigned int* __restrict__ flags) {
+       NodeRec* __restrict__ node, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         std::uint32_t de0;
@@ -414,29 +428,96 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
             dd[2] = nd == 2 ? t : dd[2];
             dd[3] = nd == 3 ? t : dd[3];
             ++nd;
-            if (!(t & kTerm)) {
-                ++pend;
-                atomicAdd(&indeg[t], 1u);
-            }
+            if (!(t & kTerm)) ++pend;
         }
-        dest[i] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+        *reinterpret_cast<uint4*>(node[i].dest) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
         pending[i] = pend;
     }
 }
 
-__global__ void k_fill_parents(const uint4* __restrict__ dest, std::uint64_t n_nodes,
-                               const std::uint64_t* __restrict__ roff, std::uint32_t* __restrict__ cursor,
+// Pass-through junctions: exactly one live branch, and it ends at a junction, so
+// P(j) = P(child).  fwd[j] = child (resolved to the end of such chains by pointer
+// jumping), or j itself.
+__global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj, std::uint32_t* __restrict__ fwd) {
+    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
+         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 d4 = *reinterpret_cast<const uint4*>(node[j].dest);
+        const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+        int live = 0;
+        std::uint32_t child = kNone;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (dd[b] == kNone) continue;
+            ++live;
+            if (!(dd[b] & kTerm)) child = dd[b];
+        }
+        fwd[j] = live == 1 && child != kNone ? child : static_cast<std::uint32_t>(j);
+    }
+}
+
+// Redirect every branch through fwd; contracted junctions leave the graph
+// (no branches, pending kSkip); count parent references per junction.
+__global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
+                          const std::uint32_t* __restrict__ fwd, std::uint32_t* __restrict__ pending,
+                          std::uint32_t* __restrict__ indeg, unsigned long long* __restrict__ n_skip) {
+    unsigned long long mine = 0;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        uint4* dp = reinterpret_cast<uint4*>(node[i].dest);
+        if (i < nj && fwd[i] != i) {
+            *dp = make_uint4(kNone, kNone, kNone, kNone);
+            pending[i] = kSkip;
+            ++mine;
+            continue;
+        }
+        uint4 d4 = *dp;
+        std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (dd[b] & kTerm) continue;
+            dd[b] = fwd[dd[b]];
+            atomicAdd(&indeg[dd[b]], 1u);
+        }
+        *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_skip, mine);
+}
+
+__global__ void k_parent_overflow(const std::uint32_t* __restrict__ indeg, std::uint64_t nj,
+                                  std::uint32_t* __restrict__ ovcnt) {
+    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
+         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint32_t k = indeg[j];
+        ovcnt[j] = k > static_cast<std::uint32_t>(kInlineParents) ? k - kInlineParents : 0u;
+    }
+}
+
+__global__ void k_node_meta(NodeRec* __restrict__ node, std::uint64_t nj, const std::uint32_t* __restrict__ indeg,
+                            const std::uint64_t* __restrict__ ovoff) {
+    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
+         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t o = ovoff[j];
+        node[j].npar = indeg[j];
+        node[j].ov_lo = static_cast<std::uint32_t>(o);
+        node[j].ov_hi = static_cast<std::uint32_t>(o >> 32);
+    }
+}
+
+__global__ void k_fill_parents(NodeRec* __restrict__ node, std::uint64_t n_nodes,
+                               const std::uint64_t* __restrict__ ovoff, std::uint32_t* __restrict__ cursor,
                                std::uint32_t* __restrict__ rsrc) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const uint4 d4 = dest[i];
+        const uint4 d4 = *reinterpret_cast<const uint4*>(node[i].dest);
         const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const std::uint32_t t = dd[b];
             if (t & kTerm) continue;
             const std::uint32_t at = atomicAdd(&cursor[t], 1u);
-            rsrc[roff[t] + at] = static_cast<std::uint32_t>(i);
+            if (at < static_cast<std::uint32_t>(kInlineParents)) node[t].par[at] = static_cast<std::uint32_t>(i);
+            else rsrc[ovoff[t] + at - kInlineParents] = static_cast<std::uint32_t>(i);
         }
     }
 }
@@ -651,27 +732,62 @@ __device__ __forceinline__ std::uint32_t merge_staged(const Inputs& in, const Wa
     return out;
 }
 
-// Pool allocation: all 32 lanes call (len 0 for lanes that need nothing); one
-// atomic per warp on the warp's arena; len rounded up to a multiple of 4.
-__device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, std::uint32_t len, unsigned int* full) {
-    const int arena = static_cast<int>(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % kArenas);
+// Pool allocation: all 32 lanes call (len 0 for lanes that need nothing); lengths
+// rounded up to multiples of 4.  Each warp carves its requests out of a private
+// chunk and reserves a new chunk (one atomic) only when the current one is used up.
+constexpr std::uint32_t kPoolChunk = 4096;
+
+struct PoolChunk {
+    unsigned long long base;
+    std::uint32_t left;
+};
+
+__device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, PoolChunk& ch, std::uint32_t len,
+                                                    unsigned int* full) {
+    const int lane = threadIdx.x & 31;
     const std::uint32_t want = (len + 3u) & ~3u;
-    const unsigned long long at = warp_reserve(&pool.top[arena], want);
-    if (len == 0) return kBadOff;
-    if (at + want > pool.arena_cap) {
-        *full = 1u;
-        return kBadOff;
+    std::uint32_t incl = want;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    return static_cast<std::uint64_t>(arena) * pool.arena_cap + at;
+    const std::uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return kBadOff;
+    __syncwarp();
+    if (total > ch.left) {  // warp-uniform
+        if (lane == 0) {
+            const std::uint32_t take = total > kPoolChunk ? total : kPoolChunk;
+            const int arena = static_cast<int>(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % kArenas);
+            const unsigned long long at = atomicAdd(&pool.top[arena], static_cast<unsigned long long>(take));
+            if (at + take > pool.arena_cap) {
+                *full = 1u;
+                ch.base = kBadOff;
+                ch.left = 0;
+            } else {
+                ch.base = static_cast<unsigned long long>(arena) * pool.arena_cap + at;
+                ch.left = take;
+            }
+        }
+        __syncwarp();
+    }
+    const unsigned long long base = ch.base;
+    const bool ok = base != kBadOff && total <= ch.left;
+    __syncwarp();
+    if (lane == 0 && ok) {
+        ch.base += total;
+        ch.left -= total;
+    }
+    __syncwarp();
+    if (!ok || len == 0) return kBadOff;
+    return base + incl - want;
 }
 
 struct CountArgs {
-    const uint4* dest;           // nj junctions, then n1 sources
+    const NodeRec* node;         // nj junctions, then n1 sources
     std::uint32_t* pending;      // live counters (nj + n1)
     const std::uint32_t* pending0;
-    const std::uint64_t* roff;   // junction parent lists
-    const std::uint32_t* rcnt;
-    const std::uint32_t* rsrc;
+    const std::uint32_t* rsrc;   // parents beyond the inline ones
     JRec* rec;
     PoolRef pool;
     std::uint32_t* slen;
@@ -703,9 +819,10 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
 // parents; parents that reach zero pending children are appended to the next
 // frontier.  1-saddles record their merged length.  All lanes call.
 template <bool kChain>
-__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, bool valid, std::uint32_t u,
+__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch,
+                                                    bool valid, std::uint32_t u,
                                                     std::uint32_t* nxt, unsigned long long* next_cnt,
-                                                    unsigned long long& done, bool prof) {
+                                                    unsigned long long& done, bool prof, unsigned long long* phase) {
     const int lane = threadIdx.x & 31;
     prof = prof && a.diag != nullptr;
     long long t_0 = prof ? clock64() : 0;
@@ -713,7 +830,7 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         if (prof) {
             __syncwarp();
             const long long t1 = clock64();
-            if (lane == 0) atomicAdd(&a.diag[900 + k], static_cast<unsigned long long>(t1 - t_0));
+            phase[k] += static_cast<unsigned long long>(t1 - t_0);
             t_0 = t1;
         }
     };
@@ -724,14 +841,20 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
 #pragma unroll
     for (int b = 0; b < 4; ++b) in.len[b] = 0;
     std::uint32_t S = 0;  // staged size (lists padded to multiples of 4)
+    uint4 meta = make_uint4(0u, 0u, 0u, 0u), par0 = meta, par1 = meta;
     if (valid) {
-        gather<true>(a.dest[u], a.rec, in);
+        const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
+        const uint4 d4 = nr[0];
+        meta = nr[1];
+        par0 = nr[2];
+        par1 = nr[3];
+        gather<true>(d4, a.rec, in);
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
     }
     lap(0);
     const bool pooled = junction && T > 2;
-    const std::uint64_t off = pool_alloc(a.pool, pooled ? T : 0u, &a.flags[1]);
+    const std::uint64_t off = pool_alloc(a.pool, ch, pooled ? T : 0u, &a.flags[1]);
     std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
     std::uint64_t* oc = a.pool.cnt + (off == kBadOff ? 0 : off);
     JRec r;
@@ -789,49 +912,53 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
     }
     if (junction) ++done;
     if (ovf) a.flags[0] = 1u;
-    // release parents (visible to the next round through the grid barrier)
-    std::uint64_t r0 = 0;
-    std::uint32_t rn = 0;
-    if (junction) {
-        r0 = a.roff[u];
-        rn = a.rcnt[u];
-    }
-    if (a.diag) {
-        if (T) atomicMax(&a.diag[0], static_cast<unsigned long long>(T));
-        if (rn) atomicMax(&a.diag[1], static_cast<unsigned long long>(rn));
-        if (T > kWarpCap) atomicAdd(&a.diag[2], 1ull);
-    }
+    // release parents (visible to the next round through the grid barrier): the
+    // first kInlineParents come with the node record, the rest from the overflow list
+    std::uint32_t rn = junction ? meta.x : 0u;
+    const std::uint64_t ov = static_cast<std::uint64_t>(meta.y) | (static_cast<std::uint64_t>(meta.z) << 32);
     // kChain: the lane continues with the first parent it releases (no barrier in
     // between), so its writes must be released before the decrements and the other
     // children's writes acquired after them.
     if (kChain) __threadfence();
     std::uint32_t next = kNone;
-    // four parents per step, their decrements issued back to back
+    const std::uint32_t inl[kInlineParents] = {meta.w, par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
+    std::uint32_t k0 = 0;  // parents handled so far
     for (;;) {
         std::uint32_t p[4], old[4];
-        const std::uint32_t m = rn < 4 ? rn : 4u;
+        const std::uint32_t m = rn - k0 < 4 ? rn - k0 : 4u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) p[k] = k < static_cast<int>(m) ? a.rsrc[r0 + k] : kNone;
+        for (int k = 0; k < 4; ++k) {
+            p[k] = kNone;
+            if (k < static_cast<int>(m)) {
+                const std::uint32_t q = k0 + k;
+                if (q < static_cast<std::uint32_t>(kInlineParents)) {
+#pragma unroll
+                    for (int z = 0; z < kInlineParents; ++z)
+                        if (static_cast<std::uint32_t>(z) == q) p[k] = inl[z];
+                } else {
+                    p[k] = a.rsrc[ov + q - kInlineParents];
+                }
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
-        r0 += m;
-        rn -= m;
+        k0 += m;
         unsigned rel = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) rel |= (old[k] == 1u ? 1u : 0u) << k;
         if (kChain && rel && next == kNone) {
-            const int k0 = __ffs(rel) - 1;
+            const int kk = __ffs(rel) - 1;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (k == k0) next = p[k];
+                if (k == kk) next = p[k];
             rel &= rel - 1;
         }
         warp_push(wq, p, rel, nxt, next_cnt);
-        if (!__any_sync(0xffffffffu, rn != 0)) break;
+        if (!__any_sync(0xffffffffu, k0 < rn)) break;
     }
     if (kChain && next != kNone) __threadfence();
     lap(4);
-    if (prof && lane == 0) atomicAdd(&a.diag[910], 1ull);
+    if (prof) phase[5] += 1;
     return next;
 }
 
@@ -840,11 +967,18 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     extern __shared__ WarpBuf s_wb[];
     WarpBuf& wb = s_wb[threadIdx.x >> 5];
     __shared__ WarpQ s_q[kThreads / 32];
+    __shared__ PoolChunk s_ch[kThreads / 32];
     WarpQ& wq = s_q[threadIdx.x >> 5];
-    if ((threadIdx.x & 31) == 0) wq.n = 0;
+    PoolChunk& ch = s_ch[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) == 0) {
+        wq.n = 0;
+        ch.base = 0;
+        ch.left = 0;
+    }
     __syncwarp();
     cg::grid_group grid = cg::this_grid();
     unsigned long long done = 0;
+    unsigned long long phase[6] = {0, 0, 0, 0, 0, 0};  // development diagnostics (a.diag)
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     const std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
     const int lane = threadIdx.x & 31;
@@ -854,8 +988,8 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     if (grid.thread_rank() == 0) a.stats[1] = gtimer();
     for (std::uint64_t base = wbase; base < total; base += stride) {
         const std::uint64_t i = base + lane;
-        const bool valid = i < total && a.pending0[i] == 0;
-        count_iter<false>(a, wb, wq, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false);
+        const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted
+        count_iter<false>(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false, phase);
     }
     flush_block(s_q, nxt, &a.cnt[1]);
     grid.sync();
@@ -875,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
         for (std::uint64_t base = wbase; base < ncur; base += stride) {
             const std::uint64_t f = base + lane;
             const bool valid = f < ncur;
-            count_iter<false>(a, wb, wq, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12);
+            count_iter<false>(a, wb, wq, ch, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12, phase);
         }
         flush_block(s_q, nxt, next_cnt);
         grid.sync();
@@ -894,20 +1028,23 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     }
     for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.done, done);
+    if (a.diag && (threadIdx.x & 31) == 0)
+        for (int k = 0; k < 6; ++k)
+            if (phase[k]) atomicAdd(&a.diag[900 + k], phase[k]);
     if (grid.thread_rank() == 0) {
         a.stats[0] = static_cast<unsigned long long>(round);
         if (round < kTimeline) a.stats[1 + round] = gtimer();
     }
 }
 
-__global__ void k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __restrict__ rec,
+__global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
                               PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
                               std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
                               std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         Inputs in;
-        gather<false>(sdest[i], rec, in);
+        gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
         const std::uint64_t at = off[i];
         bool ovf = false;
         const std::uint32_t one = base_one + static_cast<std::uint32_t>(i);
@@ -984,27 +1121,62 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, std::uint32_t* dest, std::uint32_t* pending, std::uint32_t* indeg,
-                unsigned int* flags, cudaStream_t s, int num_sms) {
+                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, cudaStream_t s,
+                int num_sms) {
     if (n == 0) return MSC3D_OK;
     WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
-    uint4* d4 = reinterpret_cast<uint4*>(dest);
+    auto* nr = static_cast<NodeRec*>(node);
     if (id_width == 4)
         k_walk<std::uint32_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, d4, pending, indeg, flags);
+            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags);
     else
         k_walk<std::uint64_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, d4, pending, indeg, flags);
+            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_fill_parents(const std::uint32_t* dest, std::uint64_t n_nodes, const std::uint64_t* roff,
-                        std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms) {
+int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
+
+int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, cudaStream_t s, int num_sms) {
+    if (nj == 0) return MSC3D_OK;
+    k_passthrough<<<grid_for(nj, num_sms), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
+                   std::uint32_t* pending, std::uint32_t* indeg, unsigned long long* n_skip, cudaStream_t s,
+                   int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_fill_parents<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(reinterpret_cast<const uint4*>(dest), n_nodes,
-                                                                  roff, cursor, rsrc);
+    k_rewrite<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, pending,
+                                                             indeg, n_skip);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
+                           int num_sms) {
+    if (nj == 0) return MSC3D_OK;
+    k_parent_overflow<<<grid_for(nj, num_sms), kThreads, 0, s>>>(indeg, nj, ovcnt);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_fill_parents(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* indeg,
+                        const std::uint64_t* ovoff, std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s,
+                        int num_sms) {
+    if (n_nodes == 0) return MSC3D_OK;
+    auto* nr = static_cast<NodeRec*>(node);
+    if (nj) {
+        k_node_meta<<<grid_for(nj, num_sms), kThreads, 0, s>>>(nr, nj, indeg, ovoff);
+        count_launch();
+    }
+    k_fill_parents<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(nr, n_nodes, ovoff, cursor, rsrc);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -1015,11 +1187,9 @@ int count_arenas() { return kArenas; }
 
 int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     CountArgs a;
-    a.dest = reinterpret_cast<const uint4*>(L.dest);
+    a.node = static_cast<const NodeRec*>(L.node);
     a.pending = L.pending;
     a.pending0 = L.pending0;
-    a.roff = L.roff;
-    a.rcnt = L.rcnt;
     a.rsrc = L.rsrc;
     a.rec = static_cast<JRec*>(L.rec);
     a.pool = PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
@@ -1051,9 +1221,9 @@ int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint
                        std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
                        int num_sms) {
     if (L.n1 == 0) return MSC3D_OK;
-    const uint4* sdest = reinterpret_cast<const uint4*>(L.dest) + L.nj;
+    const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
     k_count_write<<<grid_for(L.n1, num_sms, 8), kThreads, 0, s>>>(
-        sdest, L.n1, static_cast<const JRec*>(L.rec), PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap}, off,
+        snode, L.n1, static_cast<const JRec*>(L.rec), PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap}, off,
         o_one, o_two, o_cnt, base_one, base_two, L.flags);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());

@@ -57,6 +57,8 @@ int launch_marked_critical_compact(const std::uint8_t* codes, const std::uint8_t
 
 namespace msc3d_dev {
 // primitives.cu
+// Copy n u64 device -> mapped host memory with a kernel (no copy engine).
+int launch_small_copy(const std::uint64_t* src, std::uint64_t* dst_mapped, int n, cudaStream_t s);
 int scan_u32(const std::uint32_t* in, std::uint64_t n, std::uint64_t* out, std::uint64_t* d_total,
              Workspace& ws, cudaStream_t s);
 
@@ -152,12 +154,10 @@ int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint3
 namespace msc3d_dev {
 // dag.cu -- successor table, reachability, junction ranks, branch walks, counting
 struct CountLaunch {
-    const std::uint32_t* dest;      // uint4 per node: nj junctions, then n1 1-saddles
+    const void* node;               // node_rec_bytes() per node: nj junctions, then n1 1-saddles
     std::uint32_t* pending;
     const std::uint32_t* pending0;
-    const std::uint64_t* roff;
-    const std::uint32_t* rcnt;
-    const std::uint32_t* rsrc;
+    const std::uint32_t* rsrc;      // parents beyond the inline ones
     void* rec;                      // count_rec_bytes() per junction
     std::uint32_t* pool_key;
     std::uint64_t* pool_cnt;
@@ -186,10 +186,18 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
                          std::uint32_t* jlist, cudaStream_t s, int num_sms);
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, std::uint32_t* dest, std::uint32_t* pending, std::uint32_t* indeg,
-                unsigned int* flags, cudaStream_t s, int num_sms);
-int launch_fill_parents(const std::uint32_t* dest, std::uint64_t n_nodes, const std::uint64_t* roff,
-                        std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
+                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, cudaStream_t s,
+                int num_sms);
+int node_rec_bytes();
+int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, cudaStream_t s, int num_sms);
+int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
+                   std::uint32_t* pending, std::uint32_t* indeg, unsigned long long* n_skip, cudaStream_t s,
+                   int num_sms);
+int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
+                           int num_sms);
+int launch_fill_parents(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* indeg,
+                        const std::uint64_t* ovoff, std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s,
+                        int num_sms);
 int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms);
 int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
                        std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,

@@ -46,7 +46,19 @@ k_scan_u32(const std::uint32_t* __restrict__ in, std::uint64_t n, std::uint64_t*
     if (tile == ntiles - 1 && threadIdx.x == 0 && total) *total = sm[34] + block_total;
 }
 
+__global__ void k_small_copy(const std::uint64_t* __restrict__ src, volatile std::uint64_t* dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace
+
+int launch_small_copy(const std::uint64_t* src, std::uint64_t* dst_mapped, int n, cudaStream_t s) {
+    if (n <= 0) return MSC3D_OK;
+    k_small_copy<<<1, 128, 0, s>>>(src, dst_mapped, n);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
 
 int scan_u32(const std::uint32_t* in, std::uint64_t n, std::uint64_t* out, std::uint64_t* d_total,
              Workspace& ws, cudaStream_t s) {

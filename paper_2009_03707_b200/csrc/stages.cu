@@ -1,8 +1,10 @@
 // Stage orchestration: allocation of named device arrays, launch order, and the
 // few host<->device handshakes (output sizes) each stage needs.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -118,10 +120,8 @@ int roots_fast(msc3d_ctx* ctx, int dim) {
     while (n) {
         MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, ctx->stream));
         TRY(msc3d_dev::launch_jump_round(p, n, changed, ctx->stream, ctx->num_sms));
-        unsigned int h = 0;
-        MSC3D_CUDA_TRY(cudaMemcpyAsync(&ctx->h_small[16 + dim], changed, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        MSC3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        h = static_cast<unsigned int>(ctx->h_small[16 + dim] & 0xffffffffu);
+        TRY(ctx->fetch_range(16 + dim, 1));
+        const unsigned int h = static_cast<unsigned int>(ctx->h_small[16 + dim] & 0xffffffffu);
         ++rounds;
         if (!h) break;
         if (rounds > 64) return MSC3D_ERR_RUNTIME;
@@ -276,7 +276,17 @@ namespace {
 
 // src_list: the BFS sources (ascending 1-saddle ids); term_list: ascending 2-saddle
 // ids whose positions key the count vectors.  Output ranks into those lists.
-int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& term_list) {
+// `place` (optional) receives the output length and returns where to write the
+// (one, two, paths) triples and the bases added to the ranks; default: the arrays
+// "ss_one_rank", "ss_two_rank", "ss_paths" with ranks as they are.
+struct CountOut {
+    std::uint32_t* one = nullptr;
+    std::uint32_t* two = nullptr;
+    std::uint64_t* paths = nullptr;
+    std::uint32_t base_one = 0, base_two = 0;
+};
+int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& term_list,
+              const std::function<int(std::uint64_t, CountOut*)>& place = nullptr) {
     const Dims& d = ctx->dims;
     const int w = ctx->id_width();
     const cudaStream_t s = ctx->stream;
@@ -305,11 +315,13 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     const std::uint64_t nn = nj + n1;
     ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
-    auto* dest = static_cast<std::uint32_t*>(ctx->ensure("jdest", 4 * nn, 4));
+    void* node = ctx->ensure("jnode", nn, msc3d_dev::node_rec_bytes());
     auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nn, 4));
     auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nn, 4));
     auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
-    auto* roff = static_cast<std::uint64_t*>(ctx->ensure("roff", nj, 8));
+    auto* fwd = static_cast<std::uint32_t*>(ctx->ensure("jfwd", nj, 4));
+    auto* ovcnt = static_cast<std::uint32_t*>(ctx->ensure("ovcnt", nj, 4));
+    auto* ovoff = static_cast<std::uint64_t*>(ctx->ensure("ovoff", nj, 8));
     auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("cursor", nj, 4));
     void* rec = ctx->ensure("jrec", nj, msc3d_dev::count_rec_bytes());
     auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
@@ -317,25 +329,44 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!jlist || !dest || !pending || !pending0 || !indeg || !roff || !cursor || !rec || !slen || !soff ||
-        !ptop || !fa || !fb)
+    if (!jlist || !node || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !cursor || !rec ||
+        !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
 
-    // branch walks (saddle_graph.cpp:139-202): destinations, pending children, in-degrees
-    if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, dest, pending, indeg, flags, s,
+    // branch walks (saddle_graph.cpp:139-202): destinations and pending children
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, node, pending, flags, s, sms));
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, ctx->ptr<void>(src_list), w, n1,
+                               static_cast<char*>(node) + nj * msc3d_dev::node_rec_bytes(), pending + nj, flags, s,
                                sms));
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, ctx->ptr<void>(src_list), w, n1, dest + 4 * nj,
-                               pending + nj, indeg, flags, s, sms));
-    TRY(msc3d_dev::scan_u32(indeg, nj, roff, ctx->d_small, ctx->ws, s));
+    // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
+    // contracted away by pointer jumping
+    TRY(msc3d_dev::launch_passthrough(node, nj, fwd, s, sms));
+    auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 18);
+    for (int r = 0; nj; ++r) {
+        MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, s));
+        TRY(msc3d_dev::launch_jump_round(fwd, nj, changed, s, sms));
+        TRY(ctx->fetch_small(28));
+        if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle in a walk
+        if (!(ctx->h_small[18] & 0xffffffffu)) break;
+        if (r > 64) return MSC3D_ERR_RUNTIME;  // cycle of pass-through junctions
+    }
+    if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
+    auto* n_skip = reinterpret_cast<unsigned long long*>(ctx->d_small + 19);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_skip, 0, 8, s));
+    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, pending, indeg, n_skip, s, sms));
+    // parents: the first few inline in the node records, the rest in an overflow list
+    TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
+    TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(28));
     if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle
-    const std::uint64_t nrev = nj ? ctx->h_small[0] : 0;
-    auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", nrev, 4));
+    const std::uint64_t nov = nj ? ctx->h_small[0] : 0;
+    const std::uint64_t nskip = ctx->h_small[19];
+    ctx->scalars["junctions_contracted"] = static_cast<std::int64_t>(nskip);
+    auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", std::max<std::uint64_t>(nov, 1), 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_fill_parents(dest, nn, roff, cursor, rsrc, s, sms));
+    TRY(msc3d_dev::launch_fill_parents(node, nj, nn, indeg, ovoff, cursor, rsrc, s, sms));
     if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nn * 4, cudaMemcpyDeviceToDevice, s));
 
     // count vectors, "last child continues"; grow the pool and rerun if it ran out
@@ -353,11 +384,9 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
         L.pool_key = static_cast<std::uint32_t*>(ctx->ensure("pool_key", pcap, 4));
         L.pool_cnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
         if (!L.pool_key || !L.pool_cnt) return MSC3D_ERR_NOMEM;
-        L.dest = dest;
+        L.node = node;
         L.pending = pending;
         L.pending0 = pending0;
-        L.roff = roff;
-        L.rcnt = indeg;
         L.rsrc = rsrc;
         L.rec = rec;
         L.pool_top = ptop;
@@ -390,14 +419,14 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
             pcap *= 2;
             continue;
         }
-        if (ctx->h_small[59] != nj) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
+        if (ctx->h_small[59] != nj - nskip) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
         break;
     }
     {
-        std::vector<unsigned long long> tops(arenas);
-        MSC3D_CUDA_TRY(cudaMemcpy(tops.data(), ptop, arenas * 8, cudaMemcpyDeviceToHost));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 128, ptop, arenas * 8, cudaMemcpyDeviceToDevice, s));
+        TRY(ctx->fetch_range(128, static_cast<int>(arenas)));
         std::uint64_t used = 0;
-        for (auto t : tops) used += t;
+        for (std::uint64_t k = 0; k < arenas; ++k) used += ctx->h_small[128 + k];
         ctx->scalars["pool_entries"] = static_cast<std::int64_t>(used);
     }
 
@@ -406,11 +435,17 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     TRY(ctx->fetch_small(27));
     if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
     const std::uint64_t nout = n1 ? ctx->h_small[0] : 0;
-    auto* o1 = static_cast<std::uint32_t*>(ctx->ensure("ss_one_rank", nout, 4));
-    auto* o2 = static_cast<std::uint32_t*>(ctx->ensure("ss_two_rank", nout, 4));
-    auto* oc = static_cast<std::uint64_t*>(ctx->ensure("ss_paths", nout, 8));
-    if (!o1 || !o2 || !oc) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_count_write(L, soff, o1, o2, oc, 0, 0, s, sms));
+    ctx->scalars["arcs_ss"] = static_cast<std::int64_t>(nout);
+    CountOut o;
+    if (place) {
+        TRY(place(nout, &o));
+    } else {
+        o.one = static_cast<std::uint32_t*>(ctx->ensure("ss_one_rank", nout, 4));
+        o.two = static_cast<std::uint32_t*>(ctx->ensure("ss_two_rank", nout, 4));
+        o.paths = static_cast<std::uint64_t*>(ctx->ensure("ss_paths", nout, 8));
+    }
+    if (!o.one || !o.two || !o.paths) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_count_write(L, soff, o.one, o.two, o.paths, o.base_one, o.base_two, s, sms));
     TRY(ctx->fetch_small(27));
     if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
     return MSC3D_OK;
@@ -421,7 +456,7 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
 int count(msc3d_ctx* ctx) {
     TRY(dag_count(ctx, "sources", "two_saddles"));
     const int w = ctx->id_width();
-    const std::uint64_t n = ctx->count("ss_paths");
+    const std::uint64_t n = static_cast<std::uint64_t>(ctx->scalars["arcs_ss"]);
     void* a = ctx->ensure("ss_one", n, w);
     void* b = ctx->ensure("ss_two", n, w);
     if (!a || !b) return MSC3D_ERR_NOMEM;
@@ -456,13 +491,82 @@ struct StageClock {
 
 }  // namespace
 
-int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
+// Device-to-host copies of final outputs on a second stream, each enqueued as soon
+// as its array is final, so they overlap the later stages.
+struct Sink {
+    msc3d_ctx* ctx;
+    const msc3d_host_outputs* out;
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> evs;
+    bool ok() const { return out != nullptr; }
+    // development timeline (MSC3D_DIAG): [t0 on the compute stream, per copy: ready, start, end]
+    bool diag = std::getenv("MSC3D_DIAG") != nullptr;
+    std::vector<cudaEvent_t> tl;
+    int copy(void* host, const void* dev, std::uint64_t bytes) {
+        if (!out || !host || bytes == 0) return MSC3D_OK;
+        if (!cs) {
+            cs = ctx->copy_stream();
+            if (!cs) return MSC3D_ERR_CUDA;
+        }
+        cudaEvent_t ev;
+        MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&ev, diag ? cudaEventDefault : cudaEventDisableTiming));
+        evs.push_back(ev);
+        MSC3D_CUDA_TRY(cudaEventRecord(ev, ctx->stream));
+        MSC3D_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (diag) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, cs);
+            tl.push_back(ev);
+            tl.push_back(a);
+        }
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, cs));
+        if (diag) {
+            cudaEventRecord(b, cs);
+            tl.push_back(b);
+        }
+        return MSC3D_OK;
+    }
+    int finish() {
+        int rc = MSC3D_OK;
+        if (cs && cudaStreamSynchronize(cs) != cudaSuccess) rc = MSC3D_ERR_CUDA;
+        if (diag && tl.size() >= 3) {
+            cudaDeviceSynchronize();
+            for (std::size_t k = 0; k + 2 < tl.size(); k += 3) {
+                float r = 0, a = 0, b = 0;
+                cudaEventElapsedTime(&r, tl[0], tl[k]);
+                cudaEventElapsedTime(&a, tl[0], tl[k + 1]);
+                cudaEventElapsedTime(&b, tl[0], tl[k + 2]);
+                std::fprintf(stderr, "sink copy %zu: ready %.2f start %.2f end %.2f ms\n", k / 3, r, a, b);
+            }
+            for (std::size_t k = 0; k < tl.size(); k += 3) {
+                cudaEventDestroy(tl[k + 1]);
+                cudaEventDestroy(tl[k + 2]);
+            }
+            tl.clear();
+        }
+        for (auto e : evs) cudaEventDestroy(e);
+        evs.clear();
+        return rc;
+    }
+    ~Sink() { finish(); }
+};
+
+int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {
     const Dims& d = ctx->dims;
     const int w = ctx->id_width();
     const cudaStream_t s = ctx->stream;
     const int sms = ctx->num_sms;
+    const bool seg = (options & MSC3D_OPT_SEGMENTATION) != 0;
     StageClock clk(stage_ms != nullptr);
+    Sink sink{ctx, host};
     clk.mark(0, s);
+    cudaEvent_t t_start = nullptr;
+    if (host && sink.diag) {
+        cudaEventCreate(&t_start);
+        cudaEventRecord(t_start, s);
+    }
 
     // [gradient] codes + both extremum forests in one kernel
     TRY(gradient(ctx, /*with_forests=*/true));
@@ -505,32 +609,28 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
     TRY(msc3d_dev::scan_u32(cnt_max, c2, off_max, ctx->d_small + 33, ctx->ws2, s));
     clk.mark(3, s);
 
-    // [reachability]
-    TRY(bfs(ctx, ctx->ptr<void>("crit1"), c1));
-    clk.mark(4, s);
-
-    // [counting]
-    TRY(dag_count(ctx, "crit1", "crit2"));
-    clk.mark(5, s);
-
-    // ---- assembly (untimed in the reference's StageTimings) ----
+    // ---- outputs that are final now (untimed in the reference's StageTimings) ----
+    // critical points, label volumes, min->1s and 2s->max arcs; their host copies
+    // overlap the saddle stages
     TRY(ctx->fetch_small(34));
     const std::uint64_t na = c0 ? ctx->h_small[32] : 0;  // min->1s arcs
     const std::uint64_t nc = c2 ? ctx->h_small[33] : 0;  // 2s->max arcs
-    const std::uint64_t nb = ctx->count("ss_paths");       // 1s->2s arcs
     ctx->scalars["arcs_min"] = static_cast<std::int64_t>(na);
-    ctx->scalars["arcs_ss"] = static_cast<std::int64_t>(nb);
     ctx->scalars["arcs_max"] = static_cast<std::int64_t>(nc);
     void* cp_cell = ctx->ensure("cp_cell", ncp, w);
     auto* cp_index = static_cast<std::uint8_t*>(ctx->ensure("cp_index", ncp, 1));
-    auto* asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", na + nb + nc, 4));
-    auto* adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", na + nb + nc, 4));
-    auto* amul = static_cast<std::uint64_t*>(ctx->ensure("arc_mult", na + nb + nc, 8));
+    auto* amin_src = static_cast<std::uint32_t*>(ctx->ensure("arcA_src", na, 4));
+    auto* amin_dst = static_cast<std::uint32_t*>(ctx->ensure("arcA_dst", na, 4));
+    auto* amin_mul = static_cast<std::uint64_t*>(ctx->ensure("arcA_mult", na, 8));
+    auto* amax_src = static_cast<std::uint32_t*>(ctx->ensure("arcC_src", nc, 4));
+    auto* amax_dst = static_cast<std::uint32_t*>(ctx->ensure("arcC_dst", nc, 4));
+    auto* amax_mul = static_cast<std::uint64_t*>(ctx->ensure("arcC_mult", nc, 8));
     auto* key = static_cast<std::uint64_t*>(ctx->ensure("sort_key", na, 8));
     auto* scratch = static_cast<std::uint64_t*>(ctx->ensure("sort_scratch", na, 8));
     auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("sort_cursor", c0, 4));
     auto* large = static_cast<std::uint32_t*>(ctx->ensure("sort_large", c0, 4));
-    if (!cp_cell || !cp_index || !asrc || !adst || !amul || !key || !scratch || !cursor || !large)
+    if (!cp_cell || !cp_index || !amin_src || !amin_dst || !amin_mul || !amax_src || !amax_dst || !amax_mul || !key ||
+        !scratch || !cursor || !large)
         return MSC3D_ERR_NOMEM;
     std::uint64_t at = 0;
     for (int k = 0; k < 4; ++k) {
@@ -539,34 +639,111 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms) {
         TRY(msc3d_dev::launch_cp_concat(ctx->ptr<void>(nm), n, at, k, w, cp_cell, cp_index, s, sms));
         at += n;
     }
-    TRY(msc3d_dev::launch_arcs_min_sort(slot_min, c1, base1, min_off, c0, na, cursor, key, scratch, large,
-                                        reinterpret_cast<unsigned long long*>(ctx->d_small + 35),
-                                        ctx->h_small + 35, asrc, adst, amul, s, sms));
-    if (nb) {
-        MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc + na, ctx->ptr<void>("ss_one_rank"), nb * 4, cudaMemcpyDeviceToDevice, s));
-        MSC3D_CUDA_TRY(cudaMemcpyAsync(adst + na, ctx->ptr<void>("ss_two_rank"), nb * 4, cudaMemcpyDeviceToDevice, s));
-        MSC3D_CUDA_TRY(cudaMemcpyAsync(amul + na, ctx->ptr<void>("ss_paths"), nb * 8, cudaMemcpyDeviceToDevice, s));
-        TRY(msc3d_dev::launch_add_base(asrc + na, nb, base1, s, sms));
-        TRY(msc3d_dev::launch_add_base(adst + na, nb, base2, s, sms));
+    if (host) {
+        if (host->cp_cell_cap < ncp * w || host->cp_index_cap < ncp) return MSC3D_ERR_INVALID;
+        TRY(sink.copy(host->cp_cell, cp_cell, ncp * w));
+        TRY(sink.copy(host->cp_index, cp_index, ncp));
     }
-    TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, asrc + na + nb, adst + na + nb,
-                                        amul + na + nb, s, sms));
-    if (options & MSC3D_OPT_SEGMENTATION) {
+    if (seg) {
         auto* lmin = static_cast<std::uint32_t*>(ctx->ensure("labels_min", d.n_verts, 4));
         auto* lmax = static_cast<std::uint32_t*>(ctx->ensure("labels_max", d.n_cubes, 4));
         if (!lmin || (!lmax && d.n_cubes)) return MSC3D_ERR_NOMEM;
         TRY(msc3d_dev::launch_gather(label0, remap0, d.n_verts, lmin, s, sms));
         TRY(msc3d_dev::launch_gather(label3, remap3, d.n_cubes, lmax, s, sms));
+        if (host) {
+            TRY(sink.copy(host->labels_min, lmin, d.n_verts * 4));
+            TRY(sink.copy(host->labels_max, lmax, d.n_cubes * 4));
+        }
     } else {
         ctx->drop("labels_min");
         ctx->drop("labels_max");
     }
+    TRY(msc3d_dev::launch_arcs_min_sort(slot_min, c1, base1, min_off, c0, na, cursor, key, scratch, large,
+                                        reinterpret_cast<unsigned long long*>(ctx->d_small + 35),
+                                        ctx->h_small + 35, amin_src, amin_dst, amin_mul, s, sms));
+    TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, amax_src, amax_dst, amax_mul, s, sms));
+    if (host) {
+        if (host->arc_cap < na) return MSC3D_ERR_INVALID;
+        TRY(sink.copy(host->arc_src, amin_src, na * 4));
+        TRY(sink.copy(host->arc_dst, amin_dst, na * 4));
+        TRY(sink.copy(host->arc_mult, amin_mul, na * 8));
+    }
+    clk.mark(4, s);  // (end of the untimed block: re-based below)
+
+    // [reachability]
+    StageClock clk2(stage_ms != nullptr);
+    clk2.mark(0, s);
+    TRY(bfs(ctx, ctx->ptr<void>("crit1"), c1));
+    clk2.mark(1, s);
+
+    // [counting] -- 1s->2s arcs written straight into the final arc arrays (as cp ids)
+    std::uint32_t *asrc = nullptr, *adst = nullptr;
+    std::uint64_t* amul = nullptr;
+    auto place = [&](std::uint64_t nb, CountOut* o) -> int {
+        const std::uint64_t total = na + nb + nc;
+        asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", total, 4));
+        adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", total, 4));
+        amul = static_cast<std::uint64_t*>(ctx->ensure("arc_mult", total, 8));
+        if (!asrc || !adst || !amul) return MSC3D_ERR_NOMEM;
+        o->one = asrc + na;
+        o->two = adst + na;
+        o->paths = amul + na;
+        o->base_one = base1;
+        o->base_two = base2;
+        return MSC3D_OK;
+    };
+    TRY(dag_count(ctx, "crit1", "crit2", place));
+    clk2.mark(2, s);
+    const std::uint64_t nb = static_cast<std::uint64_t>(ctx->scalars["arcs_ss"]);
+    if (host) {
+        if (host->arc_cap < na + nb + nc) return MSC3D_ERR_INVALID;
+        TRY(sink.copy(host->arc_src + na, asrc + na, nb * 4));
+        TRY(sink.copy(host->arc_dst + na, adst + na, nb * 4));
+        TRY(sink.copy(host->arc_mult + na, amul + na, nb * 8));
+        TRY(sink.copy(host->arc_src + na + nb, amax_src, nc * 4));
+        TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
+        TRY(sink.copy(host->arc_mult + na + nb, amax_mul, nc * 8));
+    }
+    // device-side arc arrays complete: the min and max blocks around the 1s->2s block
+    if (na) {
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc, amin_src, na * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(adst, amin_dst, na * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(amul, amin_mul, na * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (nc) {
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc + na + nb, amax_src, nc * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(adst + na + nb, amax_dst, nc * 4, cudaMemcpyDeviceToDevice, s));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(amul + na + nb, amax_mul, nc * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (host && sink.diag && t_start) {
+        cudaEvent_t t_end;
+        cudaEventCreate(&t_end);
+        cudaEventRecord(t_end, s);
+        cudaEventSynchronize(t_end);
+        float a = 0, b = 0;
+        if (!sink.tl.empty()) cudaEventElapsedTime(&a, t_start, sink.tl[0]);
+        cudaEventElapsedTime(&b, t_start, t_end);
+        std::fprintf(stderr, "pipeline: first copy ready at %.2f ms, compute stream done at %.2f ms\n", a, b);
+        cudaEventDestroy(t_end);
+        cudaEventDestroy(t_start);
+    }
+    if (host) {
+        auto* h = const_cast<msc3d_host_outputs*>(host);
+        h->n_cp = ncp;
+        h->n_arcs = na + nb + nc;
+        TRY(sink.finish());
+    }
     if (stage_ms) {
         MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
-        for (int i = 0; i < 5; ++i) {
+        for (int i = 0; i < 3; ++i) {
             float ms = 0;
             if (clk.ok) cudaEventElapsedTime(&ms, clk.ev[i], clk.ev[i + 1]);
             stage_ms[i] = ms;
+        }
+        for (int i = 0; i < 2; ++i) {
+            float ms = 0;
+            if (clk2.ok) cudaEventElapsedTime(&ms, clk2.ev[i], clk2.ev[i + 1]);
+            stage_ms[3 + i] = ms;
         }
     }
     return MSC3D_OK;

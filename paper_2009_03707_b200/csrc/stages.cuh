@@ -20,7 +20,7 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
                 std::uint64_t nj, const void* twos, std::uint64_t n2,
                 const std::uint32_t* const* src, const std::uint32_t* const* dst,
                 const std::uint64_t* const* mult, const std::uint64_t* count, int id_width);
-int compute(msc3d_ctx* ctx, int options, double* stage_ms);
+int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host = nullptr);
 int load_marked(msc3d_ctx* ctx, const std::uint8_t* host_marked, const void* ones, std::uint64_t n1,
                 const void* twos, std::uint64_t n2);
 int sp_op(msc3d_ctx* ctx, int op, std::uint32_t xr, std::uint32_t xc, const std::uint64_t* xp,

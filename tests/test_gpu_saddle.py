@@ -173,3 +173,30 @@ def test_compute_repeatable(ctx, ref):
     for x, y in ((a.arc_src, b.arc_src), (a.arc_dst, b.arc_dst), (a.arc_mult, b.arc_mult),
                  (a.labels_min, b.labels_min)):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("kind", ["gnoise", "noise"])
+def test_compute_host_outputs(ctx, ref, kind):
+    """msc3d_ctx_compute_host: the overlapped host copies equal the reference."""
+    import ctypes as C
+    dims = (40, 36, 32)
+    v = m.synth(kind, dims)
+    want = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
+    ncp, na = len(want["cp_cell"]), len(want["arc_src"])
+    V, Cu = dims[0] * dims[1] * dims[2], (dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1)
+    buf = {"cp_cell": np.zeros(ncp, np.uint32), "cp_index": np.zeros(ncp, np.uint8),
+           "arc_src": np.zeros(na, np.uint32), "arc_dst": np.zeros(na, np.uint32),
+           "arc_mult": np.zeros(na, np.uint64), "labels_min": np.zeros(V, np.uint32),
+           "labels_max": np.zeros(Cu, np.uint32)}
+    ptr = {k: a.ctypes.data for k, a in buf.items()}
+    ho = m.HostOutputs(ptr["cp_cell"], ncp * 4, ptr["cp_index"], ncp, ptr["arc_src"], ptr["arc_dst"],
+                       ptr["arc_mult"], na, ptr["labels_min"], ptr["labels_max"], 0, 0)
+    ctx.load_values(v, dims)
+    assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == 0
+    assert ho.n_cp == ncp and ho.n_arcs == na
+    for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+        np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype))
+    np.testing.assert_array_equal(buf["cp_index"].astype(np.int32), want["cp_index"])
+    # too small an arc buffer is rejected (invalid_argument)
+    ho.arc_cap = max(0, na - 1)
+    assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == m.ERR_INVALID

@@ -1,28 +1,30 @@
-"""Aggregate ncu warp-stall samples per CUDA source line from
-`ncu -i rep --page source --csv --print-source cuda,sass` output (stdin or file)."""
+"""Aggregate ncu warp-stall samples per CUDA source line, per kernel, from
+`ncu -i rep --page source --csv --print-source cuda,sass` output."""
 import collections, csv, sys
 rows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-hdr = None
-agg = collections.Counter()
-src = {}
-cur = None
+filt = sys.argv[3] if len(sys.argv) > 3 else ""
+kern, si, agg, src = None, None, {}, {}
 for r in rows:
+    if len(r) >= 2 and r[0] == "Function Name":
+        kern = r[1]
+        agg.setdefault(kern, collections.Counter())
+        continue
     if len(r) > 2 and r[0] == "Line No":
-        hdr = r
         si = r.index("Warp Stall Sampling (All Samples)")
         continue
-    if hdr is None or not r:
+    if si is None or kern is None or not r or not r[0].strip().isdigit():
         continue
-    if r[0].strip().isdigit():
-        cur = int(r[0]); src[cur] = r[1][:110]
+    ln = int(r[0])
+    src[(kern, ln)] = r[1][:110]
     try:
-        v = int(r[si])
+        agg[kern][ln] += int(r[si])
     except (ValueError, IndexError):
+        pass
+for kern, c in agg.items():
+    if filt and filt not in kern:
         continue
-    if cur is not None:
-        agg[cur] += v
-tot = sum(agg.values()) or 1
-print("total samples", tot)
-for ln, v in agg.most_common(top):
-    print(f"{v:8d} {100*v/tot:5.1f}%  L{ln:<5d} {src.get(ln,'').strip()}")
+    tot = sum(c.values()) or 1
+    print(f"== {kern[:120]}  samples {tot}")
+    for ln, v in c.most_common(top):
+        print(f"{v:8d} {100*v/tot:5.1f}%  L{ln:<5d} {src.get((kern, ln), '').strip()}")

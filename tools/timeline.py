@@ -32,7 +32,7 @@ except Exception as e:
     print("no diag", e)
 try:
     dg = ctx.get("count_diag", np.uint64)
-    ph = dg[900:905].astype(np.float64); it = float(dg[910])
+    ph = dg[900:905].astype(np.float64); it = float(dg[905])
     if it:
         print("tail rounds: warp iterations", int(it), "mean cycles per iteration by phase [gather, alloc, stage, merge, release]",
               np.round(ph / it).tolist())
