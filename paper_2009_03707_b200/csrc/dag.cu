@@ -456,10 +456,15 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
 }
 
 // Redirect every branch through fwd; contracted junctions leave the graph
-// (no branches, pending kSkip); count parent references per junction.
+// (no branches, pending kSkip).  Each branch reference takes the next parent slot of
+// its destination (the atomic's old value): slots < kInlineParents are written
+// into the destination's node record right here; later ones (in-degree > 9, rare)
+// are queued as (destination, slot, parent) for the overflow list.
 __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
                           const std::uint32_t* __restrict__ fwd, std::uint32_t* __restrict__ pending,
-                          std::uint32_t* __restrict__ indeg, unsigned long long* __restrict__ n_skip) {
+                          std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
+                          unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
+                          unsigned long long* __restrict__ n_skip) {
     unsigned long long mine = 0;
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -475,8 +480,15 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             if (dd[b] & kTerm) continue;
-            dd[b] = fwd[dd[b]];
-            atomicAdd(&indeg[dd[b]], 1u);
+            const std::uint32_t t = fwd[dd[b]];
+            dd[b] = t;
+            const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
+            if (slot < static_cast<std::uint32_t>(kInlineParents)) {
+                node[t].par[slot] = static_cast<std::uint32_t>(i);
+            } else {
+                const unsigned long long q = atomicAdd(ovq_n, 1ull);
+                if (q < ovq_cap) ovq[q] = make_uint4(t, slot, static_cast<std::uint32_t>(i), 0u);
+            }
         }
         *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
     }
@@ -493,32 +505,43 @@ __global__ void k_parent_overflow(const std::uint32_t* __restrict__ indeg, std::
     }
 }
 
+// Parent counts and overflow offsets into the node records; the inline parents are
+// sorted ascending (the atomics that placed them ran in arbitrary order), so each
+// round's frontier, appended in release order, keeps some spatial order -- the
+// later, latency-bound rounds are measurably faster with it.
 __global__ void k_node_meta(NodeRec* __restrict__ node, std::uint64_t nj, const std::uint32_t* __restrict__ indeg,
                             const std::uint64_t* __restrict__ ovoff) {
     for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
          j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         const std::uint64_t o = ovoff[j];
-        node[j].npar = indeg[j];
-        node[j].ov_lo = static_cast<std::uint32_t>(o);
-        node[j].ov_hi = static_cast<std::uint32_t>(o >> 32);
+        const std::uint32_t k = indeg[j];
+        uint4* r = reinterpret_cast<uint4*>(node + j);
+        uint4 m = r[1], p0 = r[2], p1 = r[3];
+        std::uint32_t q[kInlineParents] = {m.w, p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        const std::uint32_t n = k < static_cast<std::uint32_t>(kInlineParents) ? k : kInlineParents;
+        if (n > 1) {
+#pragma unroll
+            for (int a = 0; a < kInlineParents; ++a)
+#pragma unroll
+                for (int b = 0; b + 1 < kInlineParents - a; ++b) {
+                    const bool in = static_cast<std::uint32_t>(b + 1) < n;
+                    const std::uint32_t lo = min(q[b], q[b + 1]), hi = max(q[b], q[b + 1]);
+                    q[b] = in ? lo : q[b];
+                    q[b + 1] = in ? hi : q[b + 1];
+                }
+        }
+        r[1] = make_uint4(k, static_cast<std::uint32_t>(o), static_cast<std::uint32_t>(o >> 32), q[0]);
+        r[2] = make_uint4(q[1], q[2], q[3], q[4]);
+        r[3] = make_uint4(q[5], q[6], q[7], q[8]);
     }
 }
 
-__global__ void k_fill_parents(NodeRec* __restrict__ node, std::uint64_t n_nodes,
-                               const std::uint64_t* __restrict__ ovoff, std::uint32_t* __restrict__ cursor,
-                               std::uint32_t* __restrict__ rsrc) {
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const uint4 d4 = *reinterpret_cast<const uint4*>(node[i].dest);
-        const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const std::uint32_t t = dd[b];
-            if (t & kTerm) continue;
-            const std::uint32_t at = atomicAdd(&cursor[t], 1u);
-            if (at < static_cast<std::uint32_t>(kInlineParents)) node[t].par[at] = static_cast<std::uint32_t>(i);
-            else rsrc[ovoff[t] + at - kInlineParents] = static_cast<std::uint32_t>(i);
-        }
+__global__ void k_fill_overflow(const uint4* __restrict__ ovq, std::uint64_t n, const std::uint64_t* __restrict__ ovoff,
+                                std::uint32_t* __restrict__ rsrc) {
+    for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 e = ovq[k];
+        rsrc[ovoff[e.x] + e.y - kInlineParents] = e.z;
     }
 }
 
@@ -1148,11 +1171,11 @@ int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, c
 }
 
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   std::uint32_t* pending, std::uint32_t* indeg, unsigned long long* n_skip, cudaStream_t s,
-                   int num_sms) {
+                   std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
     k_rewrite<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, pending,
-                                                             indeg, n_skip);
+                                                             indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -1167,17 +1190,18 @@ int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::ui
     return MSC3D_OK;
 }
 
-int launch_fill_parents(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* indeg,
-                        const std::uint64_t* ovoff, std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s,
-                        int num_sms) {
-    if (n_nodes == 0) return MSC3D_OK;
+int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg, const std::uint64_t* ovoff,
+                        const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms) {
     auto* nr = static_cast<NodeRec*>(node);
     if (nj) {
         k_node_meta<<<grid_for(nj, num_sms), kThreads, 0, s>>>(nr, nj, indeg, ovoff);
         count_launch();
     }
-    k_fill_parents<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(nr, n_nodes, ovoff, cursor, rsrc);
-    count_launch();
+    if (n_ovq) {
+        k_fill_overflow<<<grid_for(n_ovq, num_sms), kThreads, 0, s>>>(static_cast<const uint4*>(ovq), n_ovq, ovoff,
+                                                                       rsrc);
+        count_launch();
+    }
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }

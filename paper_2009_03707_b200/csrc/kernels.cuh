@@ -191,13 +191,13 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
 int node_rec_bytes();
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, cudaStream_t s, int num_sms);
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   std::uint32_t* pending, std::uint32_t* indeg, unsigned long long* n_skip, cudaStream_t s,
-                   int num_sms);
+                   std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms);
 int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
                            int num_sms);
-int launch_fill_parents(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* indeg,
-                        const std::uint64_t* ovoff, std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s,
-                        int num_sms);
+// node records' parent counts / overflow offsets, and the queued overflow parents
+int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg, const std::uint64_t* ovoff,
+                        const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
 int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms);
 int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
                        std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,

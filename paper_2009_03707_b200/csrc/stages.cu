@@ -322,14 +322,13 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     auto* fwd = static_cast<std::uint32_t*>(ctx->ensure("jfwd", nj, 4));
     auto* ovcnt = static_cast<std::uint32_t*>(ctx->ensure("ovcnt", nj, 4));
     auto* ovoff = static_cast<std::uint64_t*>(ctx->ensure("ovoff", nj, 8));
-    auto* cursor = static_cast<std::uint32_t*>(ctx->ensure("cursor", nj, 4));
     void* rec = ctx->ensure("jrec", nj, msc3d_dev::count_rec_bytes());
     auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
     auto* soff = static_cast<std::uint64_t*>(ctx->ensure("soff", n1, 8));
     auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!jlist || !node || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !cursor || !rec ||
+    if (!jlist || !node || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !rec ||
         !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
@@ -353,20 +352,26 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     }
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
     auto* n_skip = reinterpret_cast<unsigned long long*>(ctx->d_small + 19);
-    MSC3D_CUDA_TRY(cudaMemsetAsync(n_skip, 0, 8, s));
-    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, pending, indeg, n_skip, s, sms));
-    // parents: the first few inline in the node records, the rest in an overflow list
+    auto* ovq_n = reinterpret_cast<unsigned long long*>(ctx->d_small + 20);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 19, 0, 16, s));
+    // overflow queue (parents beyond the inline ones): reuse a frontier buffer
+    // (nde u32 = 3V*4 bytes, room for 3V/4 entries >> the measured ~0.1% of nodes)
+    void* ovq = fa;
+    const std::uint64_t ovq_cap = nde / 4;
+    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s, sms));
+    // parents beyond the inline ones: an overflow list
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
     TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(28));
     if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle
     const std::uint64_t nov = nj ? ctx->h_small[0] : 0;
     const std::uint64_t nskip = ctx->h_small[19];
+    const std::uint64_t nq = ctx->h_small[20];
+    if (nq != nov || nq > ovq_cap) return MSC3D_ERR_RUNTIME;
     ctx->scalars["junctions_contracted"] = static_cast<std::int64_t>(nskip);
     auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", std::max<std::uint64_t>(nov, 1), 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
-    if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, nj * 4, s));
-    TRY(msc3d_dev::launch_fill_parents(node, nj, nn, indeg, ovoff, cursor, rsrc, s, sms));
+    TRY(msc3d_dev::launch_fill_parents(node, nj, indeg, ovoff, ovq, nq, rsrc, s, sms));
     if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nn * 4, cudaMemcpyDeviceToDevice, s));
 
     // count vectors, "last child continues"; grow the pool and rerun if it ran out
