@@ -679,6 +679,7 @@ __device__ __forceinline__ std::uint32_t merge(const Inputs& in, const PoolRef& 
 // copies its <= 4 inputs into its slice of a per-warp shared buffer with
 // independent 16-byte loads (all in flight at once), then merges from shared memory.
 constexpr int kWarpCap = 1024;  // entries per warp buffer (larger inputs: direct merge)
+constexpr std::uint32_t kHeavy = 48;  // total input length above which the whole warp merges the node
 
 struct alignas(16) WarpBuf {
     std::uint64_t cnt[kWarpCap];
@@ -752,6 +753,88 @@ __device__ __forceinline__ std::uint32_t merge_staged(const Inputs& in, const Wa
         emit(out, best, sum);
         ++out;
     }
+    return out;
+}
+
+// Number of entries < x (upper == false) or <= x (upper == true) in sorted k[0, n).
+__device__ __forceinline__ std::uint32_t count_below(const std::uint32_t* k, std::uint32_t n, std::uint32_t x,
+                                                     bool upper) {
+    std::uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::uint32_t mid = (lo + hi) >> 1;
+        if (upper ? k[mid] <= x : k[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Warp-cooperative merge of ONE heavy node whose inputs are staged at wb[0, S)
+// (list b at st[b], lengths in.len).  Every entry goes to its stable rank in the
+// union (own position + binary-search counts in the other lists, ties ordered by
+// list) in the shared scratch wb[S, S + T); then runs of equal keys (<= 4 long) are
+// summed and the run heads written, compacted, to the output [ok, oc).  Returns the
+// output length (uniform).  All 32 lanes call; requires S + T <= kWarpCap.
+__device__ __forceinline__ std::uint32_t merge_heavy(const Inputs& in, WarpBuf& wb, std::uint32_t* ok,
+                                                     std::uint64_t* oc, bool* ovf) {
+    const int lane = threadIdx.x & 31;
+    std::uint32_t st[4], S = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        st[b] = S;
+        S += (in.len[b] + 3u) & ~3u;
+    }
+    const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+    std::uint32_t* sk = wb.key + S;
+    std::uint64_t* sc = wb.cnt + S;
+    for (std::uint32_t t = lane; t < T; t += 32) {
+        // list and position of the t-th entry (lists concatenated without padding)
+        int b = 0;
+        std::uint32_t q = t;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb)
+            if (b == bb && q >= in.len[bb]) {
+                q -= in.len[bb];
+                b = bb + 1;
+            }
+        std::uint32_t k = 0;
+        std::uint64_t c = 0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+            if (bb == b) {
+                k = wb.key[st[bb] + q];
+                c = wb.cnt[st[bb] + q];
+            }
+        std::uint32_t r = q;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+            if (bb != b) r += count_below(wb.key + st[bb], in.len[bb], k, bb < b);
+        sk[r] = k;
+        sc[r] = c;
+    }
+    __syncwarp();
+    std::uint32_t out = 0;
+    for (std::uint32_t base = 0; base < T; base += 32) {
+        const std::uint32_t t = base + lane;
+        bool head = false;
+        std::uint32_t k = 0;
+        std::uint64_t sum = 0;
+        if (t < T) {
+            k = sk[t];
+            head = t == 0 || sk[t - 1] != k;
+            if (head) {
+                sum = sc[t];
+                for (std::uint32_t v = t + 1; v < T && sk[v] == k; ++v) *ovf |= add_ovf(sum, sc[v], &sum);
+            }
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, head);
+        if (head && ok) {
+            const std::uint32_t o = out + __popc(hm & ((1u << lane) - 1u));
+            ok[o] = k;
+            oc[o] = sum;
+        }
+        out += __popc(hm);
+    }
+    __syncwarp();
     return out;
 }
 
@@ -849,11 +932,14 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
     const int lane = threadIdx.x & 31;
     prof = prof && a.diag != nullptr;
     long long t_0 = prof ? clock64() : 0;
+    const long long t_begin = t_0;
+    unsigned long long mine_ph[5] = {0, 0, 0, 0, 0};
     auto lap = [&](int k) {
         if (prof) {
             __syncwarp();
             const long long t1 = clock64();
             phase[k] += static_cast<unsigned long long>(t1 - t_0);
+            mine_ph[k] = static_cast<unsigned long long>(t1 - t_0);
             t_0 = t1;
         }
     };
@@ -876,6 +962,9 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         S = staged_size(in);
     }
     lap(0);
+    // heavy nodes (long inputs) are merged by the whole warp; 1-saddles get scratch
+    // pool space for that too
+    const bool heavy = valid && T > kHeavy && S + T <= kWarpCap;
     const bool pooled = junction && T > 2;
     const std::uint64_t off = pool_alloc(a.pool, ch, pooled ? T : 0u, &a.flags[1]);
     std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
@@ -909,8 +998,53 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
                                            : merge<true>(in, a.pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
         finish(len);
     }
-    // staged merges, in batches that fit the buffer
-    unsigned todo = __ballot_sync(0xffffffffu, valid && S <= kWarpCap);
+    // heavy nodes, one at a time: stage (all lanes' asynchronous copies), merge by rank
+    for (unsigned hm = __ballot_sync(0xffffffffu, heavy); hm; hm &= hm - 1) {
+        const int src = __ffs(hm) - 1;
+        Inputs h;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            h.len[b] = __shfl_sync(0xffffffffu, in.len[b], src);
+            h.k0[b] = __shfl_sync(0xffffffffu, in.k0[b], src);
+            h.k1[b] = __shfl_sync(0xffffffffu, in.k1[b], src);
+            h.c0[b] = __shfl_sync(0xffffffffu, in.c0[b], src);
+            h.c1[b] = __shfl_sync(0xffffffffu, in.c1[b], src);
+            h.off[b] = __shfl_sync(0xffffffffu, in.off[b], src);
+        }
+        const std::uint64_t hoff = __shfl_sync(0xffffffffu, off, src);
+        std::uint32_t at = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const std::uint32_t n = h.len[b];
+            if (h.off[b] == kBadOff) {
+                if (lane == 0 && n > 0) {
+                    wb.key[at] = h.k0[b];
+                    wb.cnt[at] = h.c0[b];
+                }
+                if (lane == 1 && n > 1) {
+                    wb.key[at + 1] = h.k1[b];
+                    wb.cnt[at + 1] = h.c1[b];
+                }
+            } else {
+                for (std::uint32_t q = 4 * lane; q < n; q += 128) cp_async16(&wb.key[at + q], a.pool.key + h.off[b] + q);
+                for (std::uint32_t q = 2 * lane; q < n; q += 64) cp_async16(&wb.cnt[at + q], a.pool.cnt + h.off[b] + q);
+            }
+            at += (n + 3u) & ~3u;
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        const bool hjunction = __shfl_sync(0xffffffffu, junction ? 1 : 0, src) != 0;
+        std::uint32_t L = 0;
+        bool hovf = false;
+        if (!hjunction) L = merge_heavy(h, wb, nullptr, nullptr, &hovf);  // 1-saddle: length only
+        else if (hoff != kBadOff) L = merge_heavy(h, wb, a.pool.key + hoff, a.pool.cnt + hoff, &hovf);
+        if (__any_sync(0xffffffffu, hovf)) ovf = true;
+        if (lane == src) finish(L);
+        __syncwarp();
+    }
+    lap(2);
+    // light nodes: staged merges, in batches that fit the buffer
+    unsigned todo = __ballot_sync(0xffffffffu, valid && !heavy && S <= kWarpCap);
     while (todo) {
         const bool mine = (todo >> lane) & 1u;
         std::uint32_t total = 0;
@@ -922,7 +1056,6 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         }
         cp_async_wait_all();
         __syncwarp();
-        lap(2);
         if (go) {
             const std::uint32_t len =
                 junction ? merge_staged<true>(in, wb, base, &ovf, emit)
@@ -930,9 +1063,9 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
             finish(len);
         }
         __syncwarp();
-        lap(3);
         todo &= ~__ballot_sync(0xffffffffu, go);
     }
+    lap(3);
     if (junction) ++done;
     if (ovf) a.flags[0] = 1u;
     // release parents (visible to the next round through the grid barrier): the
@@ -981,7 +1114,21 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
     }
     if (kChain && next != kNone) __threadfence();
     lap(4);
-    if (prof) phase[5] += 1;
+    if (prof) {
+        phase[5] += 1;
+        // diagnostics: slowest warp iteration of the run and its largest input
+        const long long tot = clock64() - t_begin;
+        std::uint32_t tmax = T;
+        for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        if (lane == 0) {
+            atomicMax(&a.diag[920], static_cast<unsigned long long>(tot));
+            atomicMax(&a.diag[921], static_cast<unsigned long long>(tmax));
+            if (tot > 100000) {
+                atomicAdd(&a.diag[922], 1ull);
+                for (int k = 0; k < 5; ++k) atomicAdd(&a.diag[930 + k], mine_ph[k]);
+            }
+        }
+    }
     return next;
 }
 

@@ -12,11 +12,10 @@
 //   * queues q0/q1 and "unassigned facets" as masks (popcount of facets & ~assigned),
 //     pop_min = the cell of least rank mask.
 //
-// Fast path (registers only, no per-step memory chains): the star's vertices are
-// compacted into K registers, sorted by a bitonic network, ranked; every cell's rank
-// mask is built from its facets' masks (unrolled over the 26 slots, constant
-// indices); the cells are sorted by mask with a second network of u32 keys
-// (mask << 5 | slot); the expansion then pops minima by position.  The tile kernel
+// Fast path: the star's vertices are compacted into K registers, sorted by a
+// bitonic network, ranked; every cell's rank mask is built from its facets' masks
+// (unrolled over the 26 slots, constant indices) into a per-thread shared-memory
+// column; the expansion pops the candidate of least mask (candidate sets are small).  The tile kernel
 // runs stars of <= 8 cells (K = 8); larger stars are appended to two work lists
 // processed by K = 16 / K = 32 kernels, whose register budgets do not cap the tile
 // kernel's occupancy and whose warps are size-homogeneous.
@@ -275,11 +274,6 @@ __device__ __forceinline__ void ce_pair(KT& ka, std::uint32_t& sa, KT& kb, std::
     sb = s1;
 }
 
-__device__ __forceinline__ void ce_u32(std::uint32_t& a, std::uint32_t& b, bool up) {
-    const std::uint32_t lo = min(a, b), hi = max(a, b);
-    a = up ? lo : hi;
-    b = up ? hi : lo;
-}
 
 // Fast path for one star with n <= K vertices and distinct values.  Returns false
 // (nothing written) when two star values tie.
@@ -346,34 +340,21 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
             }
             M[t] = m;
         }
-    // (4) cells by mask: u32 keys (mask << 5 | slot), second network
-    std::uint32_t ck[K];
-#pragma unroll
-    for (int p = 0; p < K; ++p)
-        ck[p] = p < n ? ((mscratch[slot[p] * mstride] << 5) | slot[p]) : 0xffffffffu;
-#pragma unroll
-    for (int k = 2; k <= K; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                const int l = i ^ j;
-                if (l > i) ce_u32(ck[i], ck[l], (i & k) == 0);
-            }
-    Pack5 cpos, slotp;  // slot -> position, position -> slot
-#pragma unroll
-    for (int p = 0; p < K; ++p)
-        if (p < n) {
-            const int s = static_cast<int>(ck[p] & 31u);
-            cpos.set(s, static_cast<std::uint32_t>(p));
-            if (p < 27) slotp.set(p, static_cast<std::uint32_t>(s));
-        }
-    // (5) expansion, pop-min by position
+    // (4) expansion: pop-min = the candidate cell of least rank mask (candidate
+    //     sets are small, so a scan over them beats sorting all cells)
     robins(S, fac, cof,
            [&](std::uint32_t m) {
-               std::uint32_t pm = 0;
-               for (; m; m &= m - 1) pm |= 1u << cpos.get(__ffs(m) - 1);
-               return static_cast<int>(slotp.get(__ffs(pm) - 1));
+               int best = __ffs(m) - 1;
+               std::uint32_t bv = mscratch[best * mstride];
+               for (m &= m - 1; m; m &= m - 1) {
+                   const int t = __ffs(m) - 1;
+                   const std::uint32_t v = mscratch[t * mstride];
+                   if (v < bv) {
+                       bv = v;
+                       best = t;
+                   }
+               }
+               return best;
            },
            w);
     return true;

@@ -34,7 +34,18 @@ try:
     dg = ctx.get("count_diag", np.uint64)
     ph = dg[900:905].astype(np.float64); it = float(dg[905])
     if it:
-        print("tail rounds: warp iterations", int(it), "mean cycles per iteration by phase [gather, alloc, stage, merge, release]",
+        print("tail rounds: warp iterations", int(it), "mean cycles per iteration by phase [gather, alloc, heavy, light, release]",
               np.round(ph / it).tolist())
 except Exception as e:
+    pass
+try:
+    dg = ctx.get("count_diag", np.uint64)
+    print("slowest tail warp iteration cycles", int(dg[920]), "max T", int(dg[921]), "iterations > 100k cycles", int(dg[922]))
+except Exception:
+    pass
+try:
+    dg = ctx.get("count_diag", np.uint64)
+    if int(dg[922]):
+        print("slow iterations (>100k cycles): mean phase cycles", np.round(dg[930:935].astype(np.float64) / float(dg[922])).tolist())
+except Exception:
     pass
