@@ -237,16 +237,24 @@ def main():
         gbs = alg[name] / (t / 1e3) / 1e9 if t > 0 else 0.0
         stages[name] = {"ms": t, "alg_bytes": alg[name], "achieved_gbs": gbs, "frac": gbs / peak}
     dom = max(STAGES, key=lambda s: stages[s]["ms"])
-    traffic = None
+    # DRAM traffic per stage from the committed ncu capture of the same workload
+    # (tools/ncu_traffic.sh: dram__bytes_read.sum + dram__bytes_write.sum summed over
+    # the stage's kernels of one compute()); None when absent
+    traffic = {}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dom)
+            traffic = {k: v.get("dram_bytes") for k, v in json.load(open(tp)).items()}
         except Exception:
-            traffic = None
+            traffic = {}
+    for name in STAGES:
+        stages[name]["dram_bytes_ncu"] = traffic.get(name)
     roofline = {"bound": "hbm", "stage": dom, "achieved": stages[dom]["achieved_gbs"], "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
-                "traffic": traffic, "alg_bytes_per_launch": alg[dom]}
+                "traffic": traffic.get(dom), "alg_bytes_per_launch": alg[dom],
+                "note": "per stage (the reference's StageTimings unit): algorithmic bytes (SURVEY.md 8(d)) / "
+                        "stage time from CUDA events on the pipeline stream; traffic = ncu DRAM bytes of the "
+                        "stage's kernels for one compute() (profiles/traffic.json)"}
 
     # ---- e2e through the C ABI with host buffers: pinned f32 samples in,
     # msc3d_ctx_load_values (H2D + device validation), msc3d_ctx_compute_host
