@@ -102,7 +102,17 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl != "reference" else "gloo")
+        if args.impl != "reference":
+            import torch
+            # MSC3D_BENCH_BACKEND=gloo: development runs of several ranks on one GPU
+            backend = os.environ.get("MSC3D_BENCH_BACKEND", "nccl")
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            else:
+                dist.init_process_group(backend)
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -163,6 +173,101 @@ def run_reference_arm(args, world, rank):
     return 0
 
 
+def run_sharded(args, world, rank, local):
+    """N > 1: ONE grid across the ranks (strong scaling), paper_2009_03707_b200/multigpu.py:
+    z-slab gradient with 2-plane halos, allgather of the owned code planes (NCCL),
+    replicated critical/extrema, reachability + counting sharded by 1-saddle slices,
+    allgather-v of the 1s->2s arc blocks (NCCL).  Every rank ends with the whole complex."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_03707_b200 as m
+    from paper_2009_03707_b200 import multigpu as mg
+
+    dims = WORKLOAD["dims"] if not args.size else (args.size,) * 3
+    ncells = cells(dims)
+    local = local % torch.cuda.device_count()
+    plan = mg.slab_plan(dims[2], world, rank)
+    v = m.synth(WORKLOAD["kind"], dims, WORKLOAD["seed"])  # every rank builds the same field
+    sv = mg.slab_values(v, dims, plan)
+    dev_in = torch.from_numpy(sv).cuda()
+    sc = mg.ShardedCompute(m, dims, plan, local)
+    for _ in range(args.warmup):
+        sc.step(dev_in, m.OPT_SEGMENTATION)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    stage_acc = np.zeros(5)
+    l0 = sc.slab.launches() + sc.full.launches()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            out = sc.step(dev_in, m.OPT_SEGMENTATION)
+            stage_acc += np.array(sc.stage_ms)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+    # every step ends with host synchronisation (the library's size handshakes), so the
+    # wall clock between the synchronised ends equals the device time of the steps
+    ms_step = max_over_ranks((t1 - t0) * 1e3 / args.steps, world, f"cuda:{local}")
+    value = ncells / (ms_step / 1e3) / 1e6
+    n_arcs = int(out["arc_src"].numel())
+    launches = (sc.slab.launches() + sc.full.launches() - l0) // args.steps
+    if os.environ.get("MSC3D_BENCH_VERIFY") and rank == 0:
+        # development check: the assembled complex equals the single-GPU compute()
+        want = m.compute(v, dims, with_segmentation=True)
+        for k, w in (("cp_cell", want.cp_cell), ("arc_src", want.arc_src), ("arc_dst", want.arc_dst),
+                     ("arc_mult", want.arc_mult), ("labels_min", want.labels_min), ("labels_max", want.labels_max)):
+            got = out[k].cpu().numpy()
+            if not np.array_equal(got.view(np.asarray(w).dtype) if got.dtype != np.asarray(w).dtype else got, w):
+                raise AssertionError(f"sharded {k} differs from the single-GPU compute")
+        print("verify ok: sharded complex == single-GPU compute", file=sys.stderr, flush=True)
+
+    # e2e: host slab in (pinned), step, rank 0 copies the assembled complex to host
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.from_numpy(sv).pin_memory()
+        hbuf = {k: torch.empty(t.numel(), dtype=t.dtype).pin_memory() for k, t in out.items()} if rank == 0 else {}
+        times = []
+        d2h = 0
+        for i in range(2 + args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            ta = time.perf_counter()
+            dev_in.copy_(host_in, non_blocking=True)
+            o = sc.step(dev_in, m.OPT_SEGMENTATION)
+            if rank == 0:
+                d2h = 0
+                for k, t in o.items():
+                    hbuf[k][: t.numel()].copy_(t, non_blocking=True)
+                    d2h += t.numel() * t.element_size()
+            torch.cuda.synchronize()
+            tb = time.perf_counter()
+            if i >= 2:
+                times.append(tb - ta)
+        te = max_over_ranks(sum(times) / len(times), world, f"cuda:{local}")
+        e2e = {"value": ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
+               "h2d_bytes_per_step": int(sv.nbytes), "d2h_bytes_per_step": int(d2h),
+               "path": "per rank: pinned slab -> device, sharded step (C ABI + NCCL); rank 0: complex -> pinned host"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mcells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD["name"], "dims": list(dims), "field": WORKLOAD["kind"],
+                       "seed": WORKLOAD["seed"], "lattice_cells": ncells,
+                       "parallelism": f"z-slabs x{world} (gradient, 2-plane halos) + allgather codes; "
+                                      f"1-saddle shards x{world} (reachability, counting) + allgather-v arcs",
+                       "l2": "inputs larger than L2"},
+            "stages_ms_rank0": dict(zip(STAGES, (stage_acc / args.steps).tolist())),
+            "e2e": e2e, "gpu_launches": int(launches), "counts": {"arcs": n_arcs},
+            "clocks": clk.summary(), "cpu_baseline": None, "roofline": None,
+        }
+        print(json.dumps(line), flush=True)
+    sc.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -177,6 +282,8 @@ def main():
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
+    if world > 1:
+        return run_sharded(args, world, rank, local)
 
     import torch
 

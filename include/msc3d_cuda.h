@@ -94,6 +94,10 @@ int msc3d_ctx_gradient(msc3d_ctx* ctx);
 /* Install an existing GradientField (host codes) for the stage entry points below. */
 int msc3d_ctx_load_codes(msc3d_ctx* ctx, msc3d_dims dims, const uint8_t* host_codes);
 
+/* Install a GradientField already in device memory (copied; e.g. assembled from
+ * z-slabs computed on several GPUs). */
+int msc3d_ctx_bind_codes(msc3d_ctx* ctx, msc3d_dims dims, const uint8_t* device_codes);
+
 /* ---- critical cells: extract_critical_cells (gradient.hpp:80) -> "crit0".."crit3" --- */
 int msc3d_ctx_critical(msc3d_ctx* ctx);
 
@@ -174,6 +178,18 @@ typedef struct msc3d_host_outputs {
     uint64_t n_arcs; /* out */
 } msc3d_host_outputs;
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out);
+
+/* The pipeline after the gradient, on the installed codes (msc3d_ctx_load_codes /
+ * msc3d_ctx_bind_codes): extremum forests are built from the codes; the saddle
+ * stages use shard `shard` of `n_shards` balanced contiguous slices of the critical
+ * 1-cells as sources (crit1[c1*shard/n_shards, c1*(shard+1)/n_shards)).  With one
+ * shard the results equal msc3d_ctx_compute's.  With several (a rank of a multi-GPU
+ * run) the 1s->2s arcs of the shard's 1-saddles -- a contiguous block of the global
+ * sorted arc list -- are left in "arcB_src", "arcB_dst" (cp ids), "arcB_mult"; the
+ * min->1s and 2s->max blocks are always in "arcA_*" / "arcC_*", the critical points
+ * and labels as for msc3d_ctx_compute. */
+int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, uint32_t shard, uint32_t n_shards,
+                            double* stage_ms);
 
 /* FNV-1a 64 over the widened f64 samples (msc.cpp:31-42), host-side, of the values
  * last loaded from host memory. */

@@ -351,6 +351,25 @@ int msc3d_ctx_count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, co
                                     id_width);
 }
 
+int msc3d_ctx_bind_codes(msc3d_ctx* ctx, msc3d_dims dims, const std::uint8_t* device_codes) {
+    int rc = set_dims(ctx, dims);
+    if (rc != MSC3D_OK) return rc;
+    void* p = ctx->ensure("codes", ctx->dims.n_cells, 1);
+    if (!p) return MSC3D_ERR_NOMEM;
+    MSC3D_CUDA_TRY(cudaMemcpyAsync(p, device_codes, ctx->dims.n_cells, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->crit_counts_valid = false;
+    return MSC3D_OK;
+}
+
+int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, std::uint32_t shard, std::uint32_t n_shards,
+                            double* stage_ms) {
+    if (!ctx || n_shards == 0 || shard >= n_shards) return MSC3D_ERR_INVALID;
+    if (!ctx->have_dims || !ctx->find("codes")) return MSC3D_ERR_STATE;
+    ctx->crit_counts_valid = false;
+    return msc3d_stage::compute_from_codes(ctx, options, stage_ms, nullptr, false, shard, n_shards, nullptr,
+                                           /*sharded=*/true);
+}
+
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out) {
     if (!ctx || !out) return MSC3D_ERR_INVALID;
     if (!ctx->values) return MSC3D_ERR_STATE;

@@ -274,8 +274,9 @@ int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources) {
 // ---------------------------------------------------------------------------------
 namespace {
 
-// src_list: the BFS sources (ascending 1-saddle ids); term_list: ascending 2-saddle
-// ids whose positions key the count vectors.  Output ranks into those lists.
+// src_ids[0, n1): the BFS sources (ascending 1-saddle ids, already traversed by bfs());
+// term_list: ascending 2-saddle ids whose positions key the count vectors.  Output
+// ranks into those lists.
 // `place` (optional) receives the output length and returns where to write the
 // (one, two, paths) triples and the bases added to the ranks; default: the arrays
 // "ss_one_rank", "ss_two_rank", "ss_paths" with ranks as they are.
@@ -285,7 +286,7 @@ struct CountOut {
     std::uint64_t* paths = nullptr;
     std::uint32_t base_one = 0, base_two = 0;
 };
-int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& term_list,
+int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::string& term_list,
               const std::function<int(std::uint64_t, CountOut*)>& place = nullptr) {
     const Dims& d = ctx->dims;
     const int w = ctx->id_width();
@@ -293,7 +294,6 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
     const int sms = ctx->num_sms;
     const std::uint64_t nde = 3 * d.n_verts;
     const std::uint64_t nwords = (nde + 31) / 32;
-    const std::uint64_t n1 = ctx->count(src_list);
     const auto* bitmap = ctx->ptr<unsigned int>("visited");
     const auto* succ = ctx->ptr<std::uint16_t>("succ");
     auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 26);  // [0] overflow [1] pool [2] cycle
@@ -335,7 +335,7 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
 
     // branch walks (saddle_graph.cpp:139-202): destinations and pending children
     TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, node, pending, flags, s, sms));
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, ctx->ptr<void>(src_list), w, n1,
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, src_ids, w, n1,
                                static_cast<char*>(node) + nj * msc3d_dev::node_rec_bytes(), pending + nj, flags, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
@@ -459,7 +459,7 @@ int dag_count(msc3d_ctx* ctx, const std::string& src_list, const std::string& te
 }  // namespace
 
 int count(msc3d_ctx* ctx) {
-    TRY(dag_count(ctx, "sources", "two_saddles"));
+    TRY(dag_count(ctx, ctx->ptr<void>("sources"), ctx->count("sources"), "two_saddles"));
     const int w = ctx->id_width();
     const std::uint64_t n = static_cast<std::uint64_t>(ctx->scalars["arcs_ss"]);
     void* a = ctx->ensure("ss_one", n, w);
@@ -558,7 +558,15 @@ struct Sink {
     ~Sink() { finish(); }
 };
 
-int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {
+// The pipeline after the gradient.  forests_ready: parent0/parent3 already hold the
+// extremum forests (the gradient kernel emits them); else they are built from the
+// codes.  Sources: the critical 1-cells crit1[src_first, src_first + src_count) --
+// all of them for a whole compute(); a slice when the saddle stages are sharded
+// across GPUs (their 1s->2s arcs are then a contiguous block of the global list:
+// "arcB_src/dst/mult").  grad_ms: the gradient's device time (already measured).
+int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host,
+                       bool forests_ready, std::uint64_t src_first, std::uint64_t src_count, cudaEvent_t grad_t0,
+                       bool sharded) {
     const Dims& d = ctx->dims;
     const int w = ctx->id_width();
     const cudaStream_t s = ctx->stream;
@@ -573,8 +581,6 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
         cudaEventRecord(t_start, s);
     }
 
-    // [gradient] codes + both extremum forests in one kernel
-    TRY(gradient(ctx, /*with_forests=*/true));
     clk.mark(1, s);
 
     // [critical]
@@ -588,6 +594,10 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
                         base3 = static_cast<std::uint32_t>(c0 + c1 + c2);
 
     // [extrema] roots by pointer jumping, saddle-extremum arcs, label remaps
+    if (!forests_ready) {
+        TRY(forest(ctx, 0));
+        TRY(forest(ctx, 3));
+    }
     TRY(roots_fast(ctx, 0));
     TRY(roots_fast(ctx, 3));
     auto* label0 = ctx->ptr<std::uint32_t>("parent0");
@@ -678,13 +688,32 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
     // [reachability]
     StageClock clk2(stage_ms != nullptr);
     clk2.mark(0, s);
-    TRY(bfs(ctx, ctx->ptr<void>("crit1"), c1));
+    if (sharded) {  // shard src_first of src_count balanced slices
+        const std::uint64_t k = src_first, n = src_count;
+        src_first = c1 * k / n;
+        src_count = c1 * (k + 1) / n - src_first;
+        ctx->scalars["shard_first"] = static_cast<std::int64_t>(src_first);
+        ctx->scalars["shard_count"] = static_cast<std::int64_t>(src_count);
+    }
+    if (src_first > c1) return MSC3D_ERR_INVALID;
+    src_count = std::min(src_count, c1 - src_first);
+    const bool sliced = src_first != 0 || src_count != c1;
+    const void* srcs = static_cast<const char*>(ctx->ptr<void>("crit1")) + src_first * w;
+    TRY(bfs(ctx, srcs, src_count));
     clk2.mark(1, s);
 
     // [counting] -- 1s->2s arcs written straight into the final arc arrays (as cp ids)
     std::uint32_t *asrc = nullptr, *adst = nullptr;
     std::uint64_t* amul = nullptr;
     auto place = [&](std::uint64_t nb, CountOut* o) -> int {
+        if (sliced) {  // this shard's block only
+            o->one = static_cast<std::uint32_t*>(ctx->ensure("arcB_src", nb, 4));
+            o->two = static_cast<std::uint32_t*>(ctx->ensure("arcB_dst", nb, 4));
+            o->paths = static_cast<std::uint64_t*>(ctx->ensure("arcB_mult", nb, 8));
+            o->base_one = base1 + static_cast<std::uint32_t>(src_first);
+            o->base_two = base2;
+            return MSC3D_OK;
+        }
         const std::uint64_t total = na + nb + nc;
         asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", total, 4));
         adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", total, 4));
@@ -697,9 +726,29 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
         o->base_two = base2;
         return MSC3D_OK;
     };
-    TRY(dag_count(ctx, "crit1", "crit2", place));
+    TRY(dag_count(ctx, srcs, src_count, "crit2", place));
     clk2.mark(2, s);
     const std::uint64_t nb = static_cast<std::uint64_t>(ctx->scalars["arcs_ss"]);
+    if (sliced) {
+        if (host) return MSC3D_ERR_INVALID;  // host delivery is for whole computes
+        ctx->drop("arc_src");
+        ctx->drop("arc_dst");
+        ctx->drop("arc_mult");
+        if (stage_ms) {
+            MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
+            for (int i = 0; i < 3; ++i) {
+                float ms = 0;
+                if (clk.ok) cudaEventElapsedTime(&ms, i == 0 && grad_t0 ? grad_t0 : clk.ev[i], clk.ev[i + 1]);
+                stage_ms[i] = ms;
+            }
+            for (int i = 0; i < 2; ++i) {
+                float ms = 0;
+                if (clk2.ok) cudaEventElapsedTime(&ms, clk2.ev[i], clk2.ev[i + 1]);
+                stage_ms[3 + i] = ms;
+            }
+        }
+        return MSC3D_OK;
+    }
     if (host) {
         if (host->arc_cap < na + nb + nc) return MSC3D_ERR_INVALID;
         TRY(sink.copy(host->arc_src + na, asrc + na, nb * 4));
@@ -742,7 +791,7 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
         MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
         for (int i = 0; i < 3; ++i) {
             float ms = 0;
-            if (clk.ok) cudaEventElapsedTime(&ms, clk.ev[i], clk.ev[i + 1]);
+            if (clk.ok) cudaEventElapsedTime(&ms, i == 0 && grad_t0 ? grad_t0 : clk.ev[i], clk.ev[i + 1]);
             stage_ms[i] = ms;
         }
         for (int i = 0; i < 2; ++i) {
@@ -752,6 +801,20 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
         }
     }
     return MSC3D_OK;
+}
+
+int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {
+    // [gradient] codes + both extremum forests in one kernel
+    cudaEvent_t t0 = nullptr;
+    if (stage_ms) {
+        MSC3D_CUDA_TRY(cudaEventCreate(&t0));
+        MSC3D_CUDA_TRY(cudaEventRecord(t0, ctx->stream));
+    }
+    int rc = gradient(ctx, /*with_forests=*/true);
+    if (rc == MSC3D_OK)
+        rc = compute_from_codes(ctx, options, stage_ms, host, true, 0, ~0ull, t0);
+    if (t0) cudaEventDestroy(t0);
+    return rc;
 }
 
 }  // namespace msc3d_stage

@@ -21,6 +21,10 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
                 const std::uint32_t* const* src, const std::uint32_t* const* dst,
                 const std::uint64_t* const* mult, const std::uint64_t* count, int id_width);
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host = nullptr);
+// sharded == false: sources crit1[a, a + b); true: shard a of b balanced slices
+int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host,
+                       bool forests_ready, std::uint64_t a, std::uint64_t b, cudaEvent_t grad_t0,
+                       bool sharded = false);
 int load_marked(msc3d_ctx* ctx, const std::uint8_t* host_marked, const void* ones, std::uint64_t n1,
                 const void* twos, std::uint64_t n2);
 int sp_op(msc3d_ctx* ctx, int op, std::uint32_t xr, std::uint32_t xc, const std::uint64_t* xp,
