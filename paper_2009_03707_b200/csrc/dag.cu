@@ -904,7 +904,10 @@ struct CountArgs {
     unsigned long long* stats; // [0] rounds
     unsigned long long* done;  // junctions evaluated
     unsigned int* flags;       // [0] overflow, [1] pool exhausted
-    unsigned long long* diag;  // optional per-round maxima (development diagnostics)
+    unsigned long long* diag;  // optional development diagnostics
+    std::uint32_t* heavy_q;    // the round's heavy nodes
+    unsigned long long* heavy_n;
+    unsigned long long* heavy_head;
 };
 
 __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::uint32_t* total) {
@@ -919,33 +922,57 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
     return incl - v;
 }
 
-// One warp iteration: lane `valid` holds node u.  Merge its branch vectors (staged
-// in shared memory); junctions store P(u) -- inline when it has <= 2 input entries,
-// else in pool space sized by the input length (single pass) -- and release their
-// parents; parents that reach zero pending children are appended to the next
-// frontier.  1-saddles record their merged length.  All lanes call.
-template <bool kChain>
-__device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch,
-                                                    bool valid, std::uint32_t u,
-                                                    std::uint32_t* nxt, unsigned long long* next_cnt,
-                                                    unsigned long long& done, bool prof, unsigned long long* phase) {
-    const int lane = threadIdx.x & 31;
-    prof = prof && a.diag != nullptr;
-    long long t_0 = prof ? clock64() : 0;
-    const long long t_begin = t_0;
-    unsigned long long mine_ph[5] = {0, 0, 0, 0, 0};
-    auto lap = [&](int k) {
-        if (prof) {
-            __syncwarp();
-            const long long t1 = clock64();
-            phase[k] += static_cast<unsigned long long>(t1 - t_0);
-            mine_ph[k] = static_cast<unsigned long long>(t1 - t_0);
-            t_0 = t1;
+// Release the parents of a finished junction (visible to the next round through
+// the grid barrier): the first kInlineParents come with the node record, the rest
+// from the overflow list; parents reaching zero pending children are appended to
+// the next frontier.  All lanes call (rn = 0 for lanes without a junction).
+__device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, std::uint32_t rn, const uint4 meta,
+                                                const uint4 par0, const uint4 par1, std::uint32_t* nxt,
+                                                unsigned long long* next_cnt) {
+    const std::uint64_t ov = static_cast<std::uint64_t>(meta.y) | (static_cast<std::uint64_t>(meta.z) << 32);
+    const std::uint32_t inl[kInlineParents] = {meta.w, par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
+    std::uint32_t k0 = 0;  // parents handled so far
+    for (;;) {
+        std::uint32_t p[4], old[4];
+        const std::uint32_t m = rn - k0 < 4 ? rn - k0 : 4u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            p[k] = kNone;
+            if (k < static_cast<int>(m)) {
+                const std::uint32_t q = k0 + k;
+                if (q < static_cast<std::uint32_t>(kInlineParents)) {
+#pragma unroll
+                    for (int z = 0; z < kInlineParents; ++z)
+                        if (static_cast<std::uint32_t>(z) == q) p[k] = inl[z];
+                } else {
+                    p[k] = a.rsrc[ov + q - kInlineParents];
+                }
+            }
         }
-    };
+#pragma unroll
+        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
+        k0 += m;
+        unsigned rel = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rel |= (old[k] == 1u ? 1u : 0u) << k;
+        warp_push(wq, p, rel, nxt, next_cnt);
+        if (!__any_sync(0xffffffffu, k0 < rn)) break;
+    }
+}
+
+// One warp iteration over light nodes: lane `valid` holds node u.  Nodes with long
+// inputs (> kHeavy entries) are only queued here -- the whole grid merges them,
+// one warp per node, after the light pass of the round, so a few heavy nodes never
+// serialise inside one warp.  Light nodes: inputs staged in the warp's shared
+// buffer, merged per lane; junctions store P(u) -- inline when it has <= 2 input
+// entries, else in pool space sized by the input length (single pass) -- and
+// release their parents.  1-saddles record their merged length.  All lanes call.
+__device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch, bool valid,
+                                           std::uint32_t u, std::uint32_t* nxt, unsigned long long* next_cnt,
+                                           unsigned long long& done) {
+    const int lane = threadIdx.x & 31;
     Inputs in;
     bool ovf = false;
-    const bool junction = valid && u < a.nj;
     std::uint32_t T = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) in.len[b] = 0;
@@ -961,10 +988,19 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
     }
-    lap(0);
-    // heavy nodes (long inputs) are merged by the whole warp; 1-saddles get scratch
-    // pool space for that too
+    // heavy nodes -> the round's heavy queue
     const bool heavy = valid && T > kHeavy && S + T <= kWarpCap;
+    {
+        const unsigned hm = __ballot_sync(0xffffffffu, heavy);
+        if (hm) {
+            unsigned long long hb = 0;
+            if (lane == 0) hb = atomicAdd(a.heavy_n, static_cast<unsigned long long>(__popc(hm)));
+            hb = __shfl_sync(0xffffffffu, hb, 0);
+            if (heavy) a.heavy_q[hb + __popc(hm & ((1u << lane) - 1u))] = u;
+        }
+    }
+    valid = valid && !heavy;
+    const bool junction = valid && u < a.nj;
     const bool pooled = junction && T > 2;
     const std::uint64_t off = pool_alloc(a.pool, ch, pooled ? T : 0u, &a.flags[1]);
     std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
@@ -991,60 +1027,14 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         else if (pooled) store_rec(a.rec, u, len, 1u, 0u, 0u, off, 0ull);
         else store_rec(a.rec, u, len, 0u, r.k0, r.k1, r.c0, r.c1);
     };
-    lap(1);
     // inputs larger than the warp buffer: direct merge
     if (valid && S > kWarpCap) {
         const std::uint32_t len = junction ? merge<true>(in, a.pool, &ovf, emit)
                                            : merge<true>(in, a.pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
         finish(len);
     }
-    // heavy nodes, one at a time: stage (all lanes' asynchronous copies), merge by rank
-    for (unsigned hm = __ballot_sync(0xffffffffu, heavy); hm; hm &= hm - 1) {
-        const int src = __ffs(hm) - 1;
-        Inputs h;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            h.len[b] = __shfl_sync(0xffffffffu, in.len[b], src);
-            h.k0[b] = __shfl_sync(0xffffffffu, in.k0[b], src);
-            h.k1[b] = __shfl_sync(0xffffffffu, in.k1[b], src);
-            h.c0[b] = __shfl_sync(0xffffffffu, in.c0[b], src);
-            h.c1[b] = __shfl_sync(0xffffffffu, in.c1[b], src);
-            h.off[b] = __shfl_sync(0xffffffffu, in.off[b], src);
-        }
-        const std::uint64_t hoff = __shfl_sync(0xffffffffu, off, src);
-        std::uint32_t at = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const std::uint32_t n = h.len[b];
-            if (h.off[b] == kBadOff) {
-                if (lane == 0 && n > 0) {
-                    wb.key[at] = h.k0[b];
-                    wb.cnt[at] = h.c0[b];
-                }
-                if (lane == 1 && n > 1) {
-                    wb.key[at + 1] = h.k1[b];
-                    wb.cnt[at + 1] = h.c1[b];
-                }
-            } else {
-                for (std::uint32_t q = 4 * lane; q < n; q += 128) cp_async16(&wb.key[at + q], a.pool.key + h.off[b] + q);
-                for (std::uint32_t q = 2 * lane; q < n; q += 64) cp_async16(&wb.cnt[at + q], a.pool.cnt + h.off[b] + q);
-            }
-            at += (n + 3u) & ~3u;
-        }
-        cp_async_wait_all();
-        __syncwarp();
-        const bool hjunction = __shfl_sync(0xffffffffu, junction ? 1 : 0, src) != 0;
-        std::uint32_t L = 0;
-        bool hovf = false;
-        if (!hjunction) L = merge_heavy(h, wb, nullptr, nullptr, &hovf);  // 1-saddle: length only
-        else if (hoff != kBadOff) L = merge_heavy(h, wb, a.pool.key + hoff, a.pool.cnt + hoff, &hovf);
-        if (__any_sync(0xffffffffu, hovf)) ovf = true;
-        if (lane == src) finish(L);
-        __syncwarp();
-    }
-    lap(2);
-    // light nodes: staged merges, in batches that fit the buffer
-    unsigned todo = __ballot_sync(0xffffffffu, valid && !heavy && S <= kWarpCap);
+    // staged merges, in batches that fit the buffer
+    unsigned todo = __ballot_sync(0xffffffffu, valid && S <= kWarpCap);
     while (todo) {
         const bool mine = (todo >> lane) & 1u;
         std::uint32_t total = 0;
@@ -1065,71 +1055,72 @@ __device__ __forceinline__ std::uint32_t count_iter(const CountArgs& a, WarpBuf&
         __syncwarp();
         todo &= ~__ballot_sync(0xffffffffu, go);
     }
-    lap(3);
     if (junction) ++done;
     if (ovf) a.flags[0] = 1u;
-    // release parents (visible to the next round through the grid barrier): the
-    // first kInlineParents come with the node record, the rest from the overflow list
-    std::uint32_t rn = junction ? meta.x : 0u;
-    const std::uint64_t ov = static_cast<std::uint64_t>(meta.y) | (static_cast<std::uint64_t>(meta.z) << 32);
-    // kChain: the lane continues with the first parent it releases (no barrier in
-    // between), so its writes must be released before the decrements and the other
-    // children's writes acquired after them.
-    if (kChain) __threadfence();
-    std::uint32_t next = kNone;
-    const std::uint32_t inl[kInlineParents] = {meta.w, par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
-    std::uint32_t k0 = 0;  // parents handled so far
+    release_parents(a, wq, junction ? meta.x : 0u, meta, par0, par1, nxt, next_cnt);
+}
+
+// One heavy node, merged by the whole warp (all lanes call with the same u).
+__device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch, std::uint32_t u,
+                                            std::uint32_t* nxt, unsigned long long* next_cnt,
+                                            unsigned long long& done) {
+    const int lane = threadIdx.x & 31;
+    const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
+    const uint4 d4 = nr[0], meta = nr[1], par0 = nr[2], par1 = nr[3];
+    Inputs h;
+    gather<true>(d4, a.rec, h);
+    const std::uint32_t T = h.len[0] + h.len[1] + h.len[2] + h.len[3];
+    const bool junction = u < a.nj;
+    const std::uint64_t off = pool_alloc(a.pool, ch, lane == 0 && junction ? T : 0u, &a.flags[1]);
+    const std::uint64_t hoff = __shfl_sync(0xffffffffu, off, 0);
+    std::uint32_t at = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const std::uint32_t n = h.len[b];
+        if (h.off[b] == kBadOff) {
+            if (lane == 0 && n > 0) {
+                wb.key[at] = h.k0[b];
+                wb.cnt[at] = h.c0[b];
+            }
+            if (lane == 1 && n > 1) {
+                wb.key[at + 1] = h.k1[b];
+                wb.cnt[at + 1] = h.c1[b];
+            }
+        } else {
+            for (std::uint32_t q = 4 * lane; q < n; q += 128) cp_async16(&wb.key[at + q], a.pool.key + h.off[b] + q);
+            for (std::uint32_t q = 2 * lane; q < n; q += 64) cp_async16(&wb.cnt[at + q], a.pool.cnt + h.off[b] + q);
+        }
+        at += (n + 3u) & ~3u;
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    std::uint32_t L = 0;
+    bool ovf = false;
+    if (!junction) L = merge_heavy(h, wb, nullptr, nullptr, &ovf);  // 1-saddle: length only
+    else if (hoff != kBadOff) L = merge_heavy(h, wb, a.pool.key + hoff, a.pool.cnt + hoff, &ovf);
+    if (__any_sync(0xffffffffu, ovf) && lane == 0) a.flags[0] = 1u;
+    if (lane == 0) {
+        if (!junction) a.slen[u - a.nj] = L;
+        else store_rec(a.rec, u, L, 1u, 0u, 0u, hoff, 0ull);
+        if (junction) ++done;
+    }
+    __syncwarp();
+    release_parents(a, wq, lane == 0 && junction ? meta.x : 0u, meta, par0, par1, nxt, next_cnt);
+}
+
+// The round's heavy queue, one warp per node (dynamic: warps take the next node).
+__device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch,
+                                           std::uint32_t* nxt, unsigned long long* next_cnt,
+                                           unsigned long long& done) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long n = *reinterpret_cast<volatile unsigned long long*>(a.heavy_n);
     for (;;) {
-        std::uint32_t p[4], old[4];
-        const std::uint32_t m = rn - k0 < 4 ? rn - k0 : 4u;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            p[k] = kNone;
-            if (k < static_cast<int>(m)) {
-                const std::uint32_t q = k0 + k;
-                if (q < static_cast<std::uint32_t>(kInlineParents)) {
-#pragma unroll
-                    for (int z = 0; z < kInlineParents; ++z)
-                        if (static_cast<std::uint32_t>(z) == q) p[k] = inl[z];
-                } else {
-                    p[k] = a.rsrc[ov + q - kInlineParents];
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
-        k0 += m;
-        unsigned rel = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rel |= (old[k] == 1u ? 1u : 0u) << k;
-        if (kChain && rel && next == kNone) {
-            const int kk = __ffs(rel) - 1;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (k == kk) next = p[k];
-            rel &= rel - 1;
-        }
-        warp_push(wq, p, rel, nxt, next_cnt);
-        if (!__any_sync(0xffffffffu, k0 < rn)) break;
+        unsigned long long k = 0;
+        if (lane == 0) k = atomicAdd(a.heavy_head, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= n) break;
+        count_heavy(a, wb, wq, ch, __ldcg(a.heavy_q + k), nxt, next_cnt, done);
     }
-    if (kChain && next != kNone) __threadfence();
-    lap(4);
-    if (prof) {
-        phase[5] += 1;
-        // diagnostics: slowest warp iteration of the run and its largest input
-        const long long tot = clock64() - t_begin;
-        std::uint32_t tmax = T;
-        for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-        if (lane == 0) {
-            atomicMax(&a.diag[920], static_cast<unsigned long long>(tot));
-            atomicMax(&a.diag[921], static_cast<unsigned long long>(tmax));
-            if (tot > 100000) {
-                atomicAdd(&a.diag[922], 1ull);
-                for (int k = 0; k < 5; ++k) atomicAdd(&a.diag[930 + k], mine_ph[k]);
-            }
-        }
-    }
-    return next;
 }
 
 // Round 0: every node without pending children, in index order; then the frontiers.
@@ -1148,7 +1139,6 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     __syncwarp();
     cg::grid_group grid = cg::this_grid();
     unsigned long long done = 0;
-    unsigned long long phase[6] = {0, 0, 0, 0, 0, 0};  // development diagnostics (a.diag)
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     const std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
     const int lane = threadIdx.x & 31;
@@ -1159,10 +1149,13 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     for (std::uint64_t base = wbase; base < total; base += stride) {
         const std::uint64_t i = base + lane;
         const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted
-        count_iter<false>(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, false, phase);
+        count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done);
     }
+    grid.sync();
+    heavy_pass(a, wb, wq, ch, nxt, &a.cnt[1], done);
     flush_block(s_q, nxt, &a.cnt[1]);
     grid.sync();
+    if (grid.thread_rank() == 0) *a.heavy_n = *a.heavy_head = 0;
     int round = 1;
     unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
     {
@@ -1179,17 +1172,16 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
         for (std::uint64_t base = wbase; base < ncur; base += stride) {
             const std::uint64_t f = base + lane;
             const bool valid = f < ncur;
-            count_iter<false>(a, wb, wq, ch, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done, round >= 12, phase);
+            count_iter(a, wb, wq, ch, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done);
         }
+        grid.sync();
+        heavy_pass(a, wb, wq, ch, nxt, next_cnt, done);
         flush_block(s_q, nxt, next_cnt);
         grid.sync();
-        if (a.diag && grid.thread_rank() == 0 && round < kTimeline) {
-            a.diag[4 + 3 * round] = a.diag[0];
-            a.diag[5 + 3 * round] = a.diag[1];
-            a.diag[6 + 3 * round] = ncur;
-            a.diag[0] = a.diag[1] = a.diag[2] = 0;
+        if (grid.thread_rank() == 0) {
+            *a.heavy_n = *a.heavy_head = 0;
+            if (a.diag && round < kTimeline) a.diag[6 + 3 * round] = ncur;
         }
-        grid.sync();
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
         ++round;
         std::uint32_t* t = cur;
@@ -1198,9 +1190,6 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     }
     for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.done, done);
-    if (a.diag && (threadIdx.x & 31) == 0)
-        for (int k = 0; k < 6; ++k)
-            if (phase[k]) atomicAdd(&a.diag[900 + k], phase[k]);
     if (grid.thread_rank() == 0) {
         a.stats[0] = static_cast<unsigned long long>(round);
         if (round < kTimeline) a.stats[1 + round] = gtimer();
@@ -1374,6 +1363,9 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.done = L.done;
     a.flags = L.flags;
     a.diag = L.diag;
+    a.heavy_q = L.heavy_q;
+    a.heavy_n = L.heavy_n;
+    a.heavy_head = L.heavy_n + 1;
     if (L.nj + L.n1 == 0) return MSC3D_OK;
     const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);
     MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count),

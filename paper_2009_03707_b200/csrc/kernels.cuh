@@ -172,6 +172,8 @@ struct CountLaunch {
     unsigned long long* done;
     unsigned int* flags;            // [0] overflow [1] pool exhausted
     unsigned long long* diag;       // optional development diagnostics (nullptr: off)
+    std::uint32_t* heavy_q;         // capacity nj + n1
+    unsigned long long* heavy_n;    // 2 counters, zeroed
 };
 int count_rec_bytes();
 int count_arenas();
