@@ -19,8 +19,9 @@ namespace msc3d_dev {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPerThread = 16;
-constexpr int kTile = kThreads * kPerThread;
+constexpr int kChunks = 4;                  // 16-byte loads per thread
+constexpr int kPerThread = 16 * kChunks;    // codes per thread
+constexpr int kTile = kThreads * kPerThread;  // 16384 codes: per-category tile counts < 2^16
 
 // A predicate maps (cell id, code, dimension) to an output list (0..3) or -1.
 struct CritPred {
@@ -70,38 +71,57 @@ k_compact_by_dim(const std::uint8_t* __restrict__ codes, Dims d, Pred pred, Tile
     const std::uint64_t first = static_cast<std::uint64_t>(tile) * kTile +
                                 static_cast<std::uint64_t>(threadIdx.x) * kPerThread;
 
-    std::uint8_t c[kPerThread];
+    // kPerThread codes: kChunks 16-byte loads issued back to back
+    std::uint32_t ws[kPerThread / 4];
     if (first + kPerThread <= d.n_cells && (first & 15) == 0) {
-        const uint4 w = *reinterpret_cast<const uint4*>(codes + first);
-        const std::uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int k = 0; k < kPerThread; ++k) c[k] = static_cast<std::uint8_t>(ws[k >> 2] >> (8 * (k & 3)));
+        for (int q = 0; q < kChunks; ++q) {
+            const uint4 w = *reinterpret_cast<const uint4*>(codes + first + 16 * q);
+            ws[4 * q] = w.x;
+            ws[4 * q + 1] = w.y;
+            ws[4 * q + 2] = w.z;
+            ws[4 * q + 3] = w.w;
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < kPerThread; ++k)
-            c[k] = first + k < d.n_cells ? codes[first + k] : kUnset;
+        for (int q = 0; q < kPerThread / 4; ++q) {
+            std::uint32_t v = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const std::uint64_t i = first + 4 * q + b;
+                v |= static_cast<std::uint32_t>(i < d.n_cells ? codes[i] : kUnset) << (8 * b);
+            }
+            ws[q] = v;
+        }
     }
 
     // Lattice coordinates of the first cell; dims of the following ones by
     // incrementing x with carries.
     Coord p = unpack(d, first < d.n_cells ? first : 0);
-    std::uint32_t dimbits = 0;  // 2 bits per cell: output list
-    std::uint32_t hit = 0;      // 1 bit per cell: predicate
+    std::uint32_t dimbits[kChunks];  // 2 bits per cell: output list
+    std::uint32_t hit[kChunks];      // 1 bit per cell: predicate
     std::uint64_t packed = 0;
 #pragma unroll
-    for (int k = 0; k < kPerThread; ++k) {
-        const int dm0 = static_cast<int>((p.x & 1) + (p.y & 1) + (p.z & 1));
-        const int dm = first + k < d.n_cells ? pred(first + k, c[k], dm0) : -1;
-        if (dm >= 0) {
-            dimbits |= static_cast<std::uint32_t>(dm) << (2 * k);
-            hit |= 1u << k;
-            packed += 1ull << (16 * dm);
-        }
-        if (++p.x == d.ex) {
-            p.x = 0;
-            if (++p.y == d.ey) {
-                p.y = 0;
-                ++p.z;
+    for (int q = 0; q < kChunks; ++q) {
+        dimbits[q] = 0;
+        hit[q] = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const std::uint8_t c = static_cast<std::uint8_t>(ws[(16 * q + k) >> 2] >> (8 * (k & 3)));
+            const std::uint64_t i = first + 16 * q + k;
+            const int dm0 = static_cast<int>((p.x & 1) + (p.y & 1) + (p.z & 1));
+            const int dm = i < d.n_cells ? pred(i, c, dm0) : -1;
+            if (dm >= 0) {
+                dimbits[q] |= static_cast<std::uint32_t>(dm) << (2 * k);
+                hit[q] |= 1u << k;
+                packed += 1ull << (16 * dm);
+            }
+            if (++p.x == d.ex) {
+                p.x = 0;
+                if (++p.y == d.ey) {
+                    p.y = 0;
+                    ++p.z;
+                }
             }
         }
     }
@@ -115,12 +135,14 @@ k_compact_by_dim(const std::uint8_t* __restrict__ codes, Dims d, Pred pred, Tile
     std::uint64_t at[4];
     for (int k = 0; k < 4; ++k) at[k] = sm[34 + k] + unpack16(excl, k);
     IdT* outs[4] = {out0, out1, out2, out3};
-    for (std::uint32_t m = hit; m; m &= m - 1) {
-        const int k = __ffs(m) - 1;
-        const int dm = (dimbits >> (2 * k)) & 3;
-        if (outs[dm]) outs[dm][at[dm]] = static_cast<IdT>(first + k);
-        ++at[dm];
-    }
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q)
+        for (std::uint32_t m = hit[q]; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const int dm = (dimbits[q] >> (2 * k)) & 3;
+            if (outs[dm]) outs[dm][at[dm]] = static_cast<IdT>(first + 16 * q + k);
+            ++at[dm];
+        }
     const std::uint32_t ntiles = static_cast<std::uint32_t>((d.n_cells + kTile - 1) / kTile);
     if (tile == ntiles - 1 && threadIdx.x == 0 && totals) {
         for (int k = 0; k < 4; ++k) totals[k] = sm[34 + k] + tot[k];
