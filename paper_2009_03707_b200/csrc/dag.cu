@@ -438,20 +438,31 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
 // Pass-through junctions: exactly one live branch, and it ends at a junction, so
 // P(j) = P(child).  fwd[j] = child (resolved to the end of such chains by pointer
 // jumping), or j itself.
-__global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj, std::uint32_t* __restrict__ fwd) {
-    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
-         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const uint4 d4 = *reinterpret_cast<const uint4*>(node[j].dest);
-        const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
-        int live = 0;
-        std::uint32_t child = kNone;
+// ptbits: one bit per junction, set for pass-through ones (10 MB at 512^3,
+// L2-resident), so the rewrite reads fwd only where it can differ.
+__global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj, std::uint32_t* __restrict__ fwd,
+                              unsigned int* __restrict__ ptbits) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < nj;
+         base += stride) {
+        const std::uint64_t j = base + (threadIdx.x & 31);
+        bool pt = false;
+        if (j < nj) {
+            const uint4 d4 = *reinterpret_cast<const uint4*>(node[j].dest);
+            const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+            int live = 0;
+            std::uint32_t child = kNone;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            if (dd[b] == kNone) continue;
-            ++live;
-            if (!(dd[b] & kTerm)) child = dd[b];
+            for (int b = 0; b < 4; ++b) {
+                if (dd[b] == kNone) continue;
+                ++live;
+                if (!(dd[b] & kTerm)) child = dd[b];
+            }
+            pt = live == 1 && child != kNone;
+            fwd[j] = pt ? child : static_cast<std::uint32_t>(j);
         }
-        fwd[j] = live == 1 && child != kNone ? child : static_cast<std::uint32_t>(j);
+        const unsigned bits = __ballot_sync(0xffffffffu, pt);
+        if ((threadIdx.x & 31) == 0) ptbits[base >> 5] = bits;
     }
 }
 
@@ -461,7 +472,8 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
 // into the destination's node record right here; later ones (in-degree > 9, rare)
 // are queued as (destination, slot, parent) for the overflow list.
 __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
-                          const std::uint32_t* __restrict__ fwd, std::uint32_t* __restrict__ pending,
+                          const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
+                          std::uint32_t* __restrict__ pending,
                           std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
                           unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
                           unsigned long long* __restrict__ n_skip) {
@@ -469,7 +481,7 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         uint4* dp = reinterpret_cast<uint4*>(node[i].dest);
-        if (i < nj && fwd[i] != i) {
+        if (i < nj && ((ptbits[i >> 5] >> (i & 31)) & 1u)) {
             *dp = make_uint4(kNone, kNone, kNone, kNone);
             pending[i] = kSkip;
             ++mine;
@@ -480,7 +492,7 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             if (dd[b] & kTerm) continue;
-            const std::uint32_t t = fwd[dd[b]];
+            const std::uint32_t t = ((ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u) ? fwd[dd[b]] : dd[b];
             dd[b] = t;
             const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
             if (slot < static_cast<std::uint32_t>(kInlineParents)) {
@@ -1196,14 +1208,23 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     }
 }
 
+// The sorted (1-saddle, 2-saddle, count) output.  Light 1-saddles are merged per
+// thread; heavy ones (> kHeavy input entries) are queued for k_count_write_heavy,
+// one warp per 1-saddle, like the heavy junctions of k_count.
 __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
                               PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
                               std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
-                              std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags) {
+                              std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
+                              std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         Inputs in;
         gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
+        const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+        if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {
+            heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
+            continue;
+        }
         const std::uint64_t at = off[i];
         bool ovf = false;
         const std::uint32_t one = base_one + static_cast<std::uint32_t>(i);
@@ -1213,6 +1234,54 @@ __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n
             o_cnt[at + o] = c;
         });
         if (ovf) flags[0] = 1u;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ rec, PoolRef pool,
+                    const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
+                    std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt, std::uint32_t base_one,
+                    std::uint32_t base_two, unsigned int* __restrict__ flags,
+                    const std::uint32_t* __restrict__ heavy_q, const unsigned long long* __restrict__ heavy_n) {
+    extern __shared__ WarpBuf s_wb[];
+    WarpBuf& wb = s_wb[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned long long n = *heavy_n;
+    for (unsigned long long k = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5; k < n;
+         k += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
+        const std::uint32_t i = heavy_q[k];
+        Inputs h;
+        gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, h);
+        std::uint32_t at = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const std::uint32_t m = h.len[b];
+            if (h.off[b] == kBadOff) {
+                if (lane == 0 && m > 0) {
+                    wb.key[at] = h.k0[b];
+                    wb.cnt[at] = h.c0[b];
+                }
+                if (lane == 1 && m > 1) {
+                    wb.key[at + 1] = h.k1[b];
+                    wb.cnt[at + 1] = h.c1[b];
+                }
+            } else {
+                for (std::uint32_t q = 4 * lane; q < m; q += 128) cp_async16(&wb.key[at + q], pool.key + h.off[b] + q);
+                for (std::uint32_t q = 2 * lane; q < m; q += 64) cp_async16(&wb.cnt[at + q], pool.cnt + h.off[b] + q);
+            }
+            at += (m + 3u) & ~3u;
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        const std::uint64_t o = off[i];
+        bool ovf = false;
+        const std::uint32_t L = merge_heavy(h, wb, o_two + o, o_cnt + o, &ovf);
+        for (std::uint32_t t = lane; t < L; t += 32) {
+            o_one[o + t] = base_one + i;
+            o_two[o + t] += base_two;
+        }
+        if (__any_sync(0xffffffffu, ovf) && lane == 0) flags[0] = 1u;
+        __syncwarp();
     }
 }
 
@@ -1298,19 +1367,21 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
 
 int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
 
-int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, cudaStream_t s, int num_sms) {
+int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
+                       int num_sms) {
     if (nj == 0) return MSC3D_OK;
-    k_passthrough<<<grid_for(nj, num_sms), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd);
+    k_passthrough<<<grid_for(nj, num_sms), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd, ptbits);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_rewrite<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, pending,
+    k_rewrite<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits,
+                                                             pending,
                                                              indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
@@ -1385,10 +1456,18 @@ int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint
                        int num_sms) {
     if (L.n1 == 0) return MSC3D_OK;
     const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
-    k_count_write<<<grid_for(L.n1, num_sms, 8), kThreads, 0, s>>>(
-        snode, L.n1, static_cast<const JRec*>(L.rec), PoolRef{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap}, off,
-        o_one, o_two, o_cnt, base_one, base_two, L.flags);
-    count_launch();
+    const PoolRef pool{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
+    MSC3D_CUDA_TRY(cudaMemsetAsync(L.heavy_n, 0, 8, s));
+    k_count_write<<<grid_for(L.n1, num_sms, 8), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
+                                                                 o_one, o_two, o_cnt, base_one, base_two, L.flags,
+                                                                 L.heavy_q, L.heavy_n);
+    const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write_heavy),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_count_write_heavy<<<num_sms * 2, kThreads, smem, s>>>(snode, static_cast<const JRec*>(L.rec), pool, off, o_one,
+                                                            o_two, o_cnt, base_one, base_two, L.flags, L.heavy_q,
+                                                            L.heavy_n);
+    count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }

@@ -191,9 +191,10 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, cudaStream_t s,
                 int num_sms);
 int node_rec_bytes();
-int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, cudaStream_t s, int num_sms);
+int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
+                       int num_sms);
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms);
 int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
                            int num_sms);

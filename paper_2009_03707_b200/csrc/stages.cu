@@ -340,7 +340,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
     // contracted away by pointer jumping
-    TRY(msc3d_dev::launch_passthrough(node, nj, fwd, s, sms));
+    auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
+    if (!ptbits) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_passthrough(node, nj, fwd, ptbits, s, sms));
     auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 18);
     for (int r = 0; nj; ++r) {
         MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, s));
@@ -358,7 +360,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // (nde u32 = 3V*4 bytes, room for 3V/4 entries >> the measured ~0.1% of nodes)
     void* ovq = fa;
     const std::uint64_t ovq_cap = nde / 4;
-    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s, sms));
+    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s, sms));
     // parents beyond the inline ones: an overflow list
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
     TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
