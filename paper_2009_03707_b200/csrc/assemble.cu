@@ -15,10 +15,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
-inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
-    const std::uint64_t need = (n + kThreads - 1) / kThreads;
-    return static_cast<unsigned>(std::max<std::uint64_t>(
-        1, std::min<std::uint64_t>(need, static_cast<std::uint64_t>(num_sms) * per_sm)));
+// One item per thread (the grid-stride loops below then run once): blocks are
+// scheduled in id order, so the resident ones sweep the id space as a compact
+// wavefront and spatially neighbouring items share the L2.
+inline unsigned grid_for(std::uint64_t n, int /*num_sms*/, int /*per_sm*/ = 16) {
+    return static_cast<unsigned>(std::max<std::uint64_t>(1, (n + kThreads - 1) / kThreads));
 }
 
 #define GRID_STRIDE(i, n)                                                                       \

@@ -53,6 +53,14 @@ constexpr std::uint32_t kFieldLow = 0x249u;  // lowest bit of each 3-bit field
 constexpr int kArenas = 64;
 constexpr std::uint64_t kBadOff = ~0ull;
 
+// One item per thread, blocks in id order: the resident blocks then sweep the id
+// space as a compact wavefront, so the random accesses of neighbouring items (which
+// are spatial neighbours) share the L2.  (A capped grid with a grid-stride loop lets
+// blocks drift apart across the whole volume and defeats the L2.)
+inline unsigned grid_full(std::uint64_t n) {
+    return static_cast<unsigned>(std::max<std::uint64_t>(1, (n + kThreads - 1) / kThreads));
+}
+
 inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
     const std::uint64_t need = (n + kThreads - 1) / kThreads;
     return static_cast<unsigned>(std::max<std::uint64_t>(
@@ -1355,10 +1363,10 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
     WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
     auto* nr = static_cast<NodeRec*>(node);
     if (id_width == 4)
-        k_walk<std::uint32_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
+        k_walk<std::uint32_t><<<grid_full(n), kThreads, 0, s>>>(
             c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags);
     else
-        k_walk<std::uint64_t><<<grid_for(n, num_sms, 8), kThreads, 0, s>>>(
+        k_walk<std::uint64_t><<<grid_full(n), kThreads, 0, s>>>(
             c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
@@ -1370,7 +1378,7 @@ int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
                        int num_sms) {
     if (nj == 0) return MSC3D_OK;
-    k_passthrough<<<grid_for(nj, num_sms), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd, ptbits);
+    k_passthrough<<<grid_full(nj), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd, ptbits);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -1380,7 +1388,7 @@ int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const st
                    const unsigned int* ptbits, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_rewrite<<<grid_for(n_nodes, num_sms), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits,
+    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits,
                                                              pending,
                                                              indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip);
     count_launch();
@@ -1401,7 +1409,7 @@ int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg
                         const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms) {
     auto* nr = static_cast<NodeRec*>(node);
     if (nj) {
-        k_node_meta<<<grid_for(nj, num_sms), kThreads, 0, s>>>(nr, nj, indeg, ovoff);
+        k_node_meta<<<grid_full(nj), kThreads, 0, s>>>(nr, nj, indeg, ovoff);
         count_launch();
     }
     if (n_ovq) {
@@ -1458,7 +1466,7 @@ int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint
     const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
     const PoolRef pool{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
     MSC3D_CUDA_TRY(cudaMemsetAsync(L.heavy_n, 0, 8, s));
-    k_count_write<<<grid_for(L.n1, num_sms, 8), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
+    k_count_write<<<grid_full(L.n1), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
                                                                  o_one, o_two, o_cnt, base_one, base_two, L.flags,
                                                                  L.heavy_q, L.heavy_n);
     const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);

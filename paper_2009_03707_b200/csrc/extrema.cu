@@ -19,9 +19,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
-inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
-    const std::uint64_t need = (n + kThreads - 1) / kThreads;
-    return static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(need, static_cast<std::uint64_t>(num_sms) * per_sm)));
+// One item per thread (the grid-stride loops below then run once): blocks are
+// scheduled in id order, so the resident ones sweep the id space as a compact
+// wavefront and spatially neighbouring items share the L2.
+inline unsigned grid_for(std::uint64_t n, int /*num_sms*/, int /*per_sm*/ = 16) {
+    return static_cast<unsigned>(std::max<std::uint64_t>(1, (n + kThreads - 1) / kThreads));
 }
 
 #define GRID_STRIDE(i, n)                                                                       \
@@ -217,7 +219,11 @@ int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64
 
 int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, cudaStream_t s,
                       int num_sms) {
-    k_jump<<<grid_for(n, num_sms), kThreads, 0, s>>>(p, n, changed);
+    // capped grid: every block reports "changed" once, and in-place jumping gains
+    // from later items seeing earlier updates within a pass
+    const unsigned g = static_cast<unsigned>(std::max<std::uint64_t>(
+        1, std::min<std::uint64_t>((n + kThreads - 1) / kThreads, static_cast<std::uint64_t>(num_sms) * 16)));
+    k_jump<<<g, kThreads, 0, s>>>(p, n, changed);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

@@ -364,7 +364,7 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
 // [0] stars of 9..16 cells, [1] 17..27 cells, [2] stars with tied values.
 struct StarLists {
     std::uint32_t* list[3];
-    unsigned long long* count;  // 3 counters
+    unsigned long long* count;  // 3 counters, then 3 chunk heads for the list kernels
 };
 
 // Block-level buffers for the large-star work lists: appends are shared-memory
@@ -512,8 +512,16 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
     __syncthreads();
     const std::uint64_t nl = *reinterpret_cast<volatile unsigned long long*>(&lists.count[which]);
     std::uint64_t ncrit = 0;
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < nl;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    // chunks of blockDim.x list entries taken in list (= spatial) order by whichever
+    // block is free: the grid sweeps the volume as one wavefront
+    __shared__ unsigned long long s_chunk;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_chunk = atomicAdd(&lists.count[3 + which], 1ull);
+        __syncthreads();
+        const std::uint64_t i = s_chunk * blockDim.x + threadIdx.x;
+        if (s_chunk * blockDim.x >= nl) break;
+        if (i >= nl) continue;
         const std::uint32_t vi = lists.list[which][i];
         const std::uint64_t r = d.fnx.div(vi), vx = vi - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
         StarWriter w;
@@ -686,7 +694,7 @@ int launch_gradient(const void* values, int value_type, const Dims& d, std::uint
     const int rc = upload_gradient_tables(dev);
     if (rc != MSC3D_OK) return rc;
     MSC3D_CUDA_TRY(cudaMemsetAsync(crit_totals, 0, 32, stream));
-    MSC3D_CUDA_TRY(cudaMemsetAsync(list_counts, 0, 24, stream));
+    MSC3D_CUDA_TRY(cudaMemsetAsync(list_counts, 0, 48, stream));
     StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
     const dim3 block(TX, TY, TZ);
     const uint3 tiles = make_uint3(static_cast<unsigned>((d.nx + TX - 1) / TX),
