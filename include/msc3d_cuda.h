@@ -127,9 +127,11 @@ int msc3d_ctx_load_marked(msc3d_ctx* ctx, const uint8_t* host_marked, const void
 int msc3d_ctx_minor(msc3d_ctx* ctx);
 
 /* ---- path counting (path_matrix.hpp:40-64) ------------------------------------------- */
-/* count_paths on the device DAG (after msc3d_ctx_mark): 2-saddle-rooted backward
- * wavefronts over the contracted V-path graph -> "ss_one", "ss_two" (ids), "ss_paths"
- * (u64), sorted by (one, two).  MSC3D_ERR_OVERFLOW with the reference's semantics. */
+/* count_paths on the device DAG (after msc3d_ctx_mark): branch walks to the ends of
+ * junction-free chains, then sparse count vectors over the junction graph in reverse
+ * topological order (Kahn rounds in one cooperative kernel) -> "ss_one", "ss_two"
+ * (ids), "ss_paths" (u64), sorted by (one, two).  MSC3D_ERR_OVERFLOW with the
+ * reference's semantics. */
 int msc3d_ctx_count(msc3d_ctx* ctx);
 /* count_paths on an explicit DagMinor (host arrays; edge lists in the order
  * s1_to_j, j_to_j, j_to_s2, s1_to_s2) -> "ss_one", "ss_two", "ss_paths". */
