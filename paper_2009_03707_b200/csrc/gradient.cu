@@ -385,6 +385,9 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ std::uint32_t s_lb[2][kListBuf];
     __shared__ std::uint32_t s_ln[2];
     __shared__ unsigned long long s_base[2];
+    __shared__ std::uint32_t s_wn[6], s_wtotal;  // phase-2 work list: buckets of star size 3..8
+    __shared__ std::uint32_t s_wS[NT];
+    __shared__ std::uint8_t s_wid[NT];
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
     if (tid < 27) {
         s_fac[tid] = c_slot.facet[tid];
@@ -424,58 +427,99 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         }
         __syncthreads();
 
-        const int lx = threadIdx.x, ly = threadIdx.y, lz = threadIdx.z;
-        StarWriter w;
-        w.vx = x0 + 1 + lx;
-        w.vy = y0 + 1 + ly;
-        w.vz = z0 + 1 + lz;
-        if (w.vx >= d.nx || w.vy >= d.ny || w.vz >= d.nz) continue;
-        std::uint32_t inr = kAll;
-        if (w.vx == 0) inr &= ~kXM;
-        if (w.vx == d.nx - 1) inr &= ~kXP;
-        if (w.vy == 0) inr &= ~kYM;
-        if (w.vy == d.ny - 1) inr &= ~kYP;
-        if (w.vz == 0) inr &= ~kZM;
-        if (w.vz == d.nz - 1) inr &= ~kZP;
-        w.inr = inr;
-        w.d = d;
-        w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
-        w.cell_off = s_cell;
-        w.parent0 = parent0;
-        w.parent3 = parent3;
-        w.ncrit = 0;
-        // ---- own vertex: star mask; trivial stars finished here
-        const T* base = &tile[lz + 1][ly + 1][lx + 1];
-        const T fv = base[0];
-        std::uint32_t below = kCentre;
+        auto writer_for = [&](int lid, StarWriter& w) {  // false: vertex outside the grid
+            const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
+            w.vx = x0 + 1 + lx;
+            w.vy = y0 + 1 + ly;
+            w.vz = z0 + 1 + lz;
+            if (w.vx >= d.nx || w.vy >= d.ny || w.vz >= d.nz) return false;
+            std::uint32_t inr = kAll;
+            if (w.vx == 0) inr &= ~kXM;
+            if (w.vx == d.nx - 1) inr &= ~kXP;
+            if (w.vy == 0) inr &= ~kYM;
+            if (w.vy == d.ny - 1) inr &= ~kYP;
+            if (w.vz == 0) inr &= ~kZM;
+            if (w.vz == d.nz - 1) inr &= ~kZP;
+            w.inr = inr;
+            w.d = d;
+            w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
+            w.cell_off = s_cell;
+            w.parent0 = parent0;
+            w.parent3 = parent3;
+            w.ncrit = 0;
+            return true;
+        };
+        // ---- phase 1, own vertex: star mask; trivial stars finished here; stars of
+        //      3..8 cells bucketed by size into the block's work list (so that phase 2
+        //      runs them densely and size-homogeneously: no idle lanes, even loops);
+        //      larger stars go to the size-specialised list kernels
+        if (tid < 6) s_wn[tid] = 0;
+        __syncthreads();
+        int n = 0;
+        std::uint32_t S = 0;
+        {
+            StarWriter w;
+            if (writer_for(tid, w)) {
+                const T* base = &tile[threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + 1];
+                const T fv = base[0];
+                std::uint32_t below = kCentre;
 #pragma unroll
-        for (int t = 0; t < 27; ++t) {
-            if (t == 13) continue;
-            const T u = base[slot_tile(t)];
-            if (u < fv || (u == fv && t < 13)) below |= 1u << t;
-        }
-        std::uint32_t S = below & w.inr;
-        S &= facets_present(S);
-        S &= facets_present(S);
-        const int n = __popc(S);
-        const std::uint32_t vi = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
-        if (n == 1) {  // critical minimum (gradient.cpp:128-131)
-            w.minimum();
-        } else if (n == 2) {  // the vertex and its only edge pair up
-            w.pair(13, __ffs(S & ~kCentre) - 1);
-        } else if (n <= 8) {
-            // ---- stars of 3..8 cells: register fast path here; larger stars go to the
-            //      size-specialised list kernels (their registers do not limit this one)
-            if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, S, n, s_fac, s_cof, &s_M[tid], NT, w)) {
-                const unsigned long long at = atomicAdd(&lists.count[2], 1ull);  // ties: rare
-                lists.list[2][at] = vi;
+                for (int t = 0; t < 27; ++t) {
+                    if (t == 13) continue;
+                    const T u = base[slot_tile(t)];
+                    if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+                }
+                S = below & w.inr;
+                S &= facets_present(S);
+                S &= facets_present(S);
+                n = __popc(S);
+                if (n == 1) {  // critical minimum (gradient.cpp:128-131)
+                    w.minimum();
+                } else if (n == 2) {  // the vertex and its only edge pair up
+                    w.pair(13, __ffs(S & ~kCentre) - 1);
+                } else if (n > 8) {
+                    const int which = n <= 16 ? 0 : 1;
+                    s_lb[which][atomicAdd(&s_ln[which], 1u)] =
+                        static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+                } else {
+                    atomicAdd(&s_wn[n - 3], 1u);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
             }
-        } else {
-            const int which = n <= 16 ? 0 : 1;
-            s_lb[which][atomicAdd(&s_ln[which], 1u)] = vi;
         }
+        __syncthreads();
+        if (tid == 0) {
+            std::uint32_t acc = 0;
+            for (int k = 0; k < 6; ++k) {
+                const std::uint32_t c = s_wn[k];
+                s_wn[k] = acc;
+                acc += c;
+            }
+            s_wtotal = acc;
+        }
+        __syncthreads();
+        if (n >= 3 && n <= 8) {
+            const std::uint32_t at = atomicAdd(&s_wn[n - 3], 1u);
+            s_wS[at] = S;
+            s_wid[at] = static_cast<std::uint8_t>(tid);
+        }
+        __syncthreads();
+        // ---- phase 2: the bucketed stars, one per thread, register fast path
+        if (static_cast<std::uint32_t>(tid) < s_wtotal) {
+            const int lid = s_wid[tid];
+            const std::uint32_t Sw = s_wS[tid];
+            StarWriter w;
+            writer_for(lid, w);
+            const T* base = &tile[lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + 1];
+            if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, Sw, __popc(Sw), s_fac, s_cof, &s_M[tid], NT,
+                                 w)) {
+                const unsigned long long at = atomicAdd(&lists.count[2], 1ull);  // ties: rare
+                lists.list[2][at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+            }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
+            for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
+        }
     }
     flush_lists();
     if (crit_totals) {
