@@ -366,6 +366,10 @@ int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, std::uint32_t shard, st
     if (!ctx || n_shards == 0 || shard >= n_shards) return MSC3D_ERR_INVALID;
     if (!ctx->have_dims || !ctx->find("codes")) return MSC3D_ERR_STATE;
     ctx->crit_counts_valid = false;
+    if (options & MSC3D_OPT_VALIDATE) {
+        const int rc = msc3d_stage::validate(ctx);
+        if (rc != MSC3D_OK) return rc;
+    }
     return msc3d_stage::compute_from_codes(ctx, options, stage_ms, nullptr, false, shard, n_shards, nullptr,
                                            /*sharded=*/true);
 }

@@ -809,6 +809,18 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     return MSC3D_OK;
 }
 
+// ComputeOptions::validate (msc.cpp:67-70): the gradient's matching audit on the
+// device; a broken gradient -> runtime_error.
+int validate(msc3d_ctx* ctx) {
+    auto* bad = reinterpret_cast<unsigned long long*>(ctx->d_small + 21);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(bad, 0, 8, ctx->stream));
+    TRY(msc3d_dev::launch_validate_matching(ctx->ptr<std::uint8_t>("codes"), ctx->dims, bad, ctx->stream,
+                                            ctx->num_sms));
+    TRY(ctx->fetch_range(21, 1));
+    ctx->scalars["validate_violations"] = static_cast<std::int64_t>(ctx->h_small[21]);
+    return ctx->h_small[21] ? MSC3D_ERR_RUNTIME : MSC3D_OK;
+}
+
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {
     // [gradient] codes + both extremum forests in one kernel
     cudaEvent_t t0 = nullptr;
@@ -817,6 +829,7 @@ int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outp
         MSC3D_CUDA_TRY(cudaEventRecord(t0, ctx->stream));
     }
     int rc = gradient(ctx, /*with_forests=*/true);
+    if (rc == MSC3D_OK && (options & MSC3D_OPT_VALIDATE)) rc = validate(ctx);
     if (rc == MSC3D_OK)
         rc = compute_from_codes(ctx, options, stage_ms, host, true, 0, ~0ull, t0);
     if (t0) cudaEventDestroy(t0);

@@ -1,0 +1,60 @@
+"""The msc3d CLI driver (paper_2009_03707_b200/bin/msc3d) -- flags, outputs and exit
+codes of the reference CLI (proj/tools/msc3d_cli.cpp:99-166; proj/tests/test_cli.cpp)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2009_03707_b200 as m
+
+BIN = os.path.join(os.path.dirname(m.__file__), "bin", "msc3d")
+pytestmark = pytest.mark.skipif(not os.path.exists(BIN), reason="CLI not built")
+
+
+def run(*args):
+    return subprocess.run([BIN, *map(str, args)], capture_output=True, text=True)
+
+
+def test_usage_and_exit_codes(tmp_path):
+    assert run("--help").returncode == 0
+    assert run("--bogus").returncode == 1                       # usage error
+    assert run("--input", "x.raw").returncode == 1              # missing --dims/--out
+    assert run("--dims", "4", "4").returncode == 1              # --dims expects 3 values
+    assert run("--input", tmp_path / "missing.raw", "--dims", 4, 4, 4, "--out", tmp_path / "o.json").returncode == 2
+    bad = tmp_path / "short.raw"
+    bad.write_bytes(b"\0" * 10)                                 # size mismatch -> invalid input
+    assert run("--input", bad, "--dims", 4, 4, 4, "--dtype", "f32", "--out", tmp_path / "o.json").returncode == 3
+
+
+def test_generate_writes_the_baseline_field(tmp_path):
+    out = tmp_path / "g.raw"
+    r = run("generate", "--kind", "gnoise", "--dims", 12, 10, 8, "--out", out)
+    assert r.returncode == 0, r.stderr
+    v = np.fromfile(out, dtype="<f4")
+    np.testing.assert_array_equal(v, m.synth("gnoise", (12, 10, 8)))
+    assert run("generate", "--kind", "ramp", "--dims", 4, 4, 4, "--out", out).returncode == 1
+
+
+@pytest.mark.gpu
+def test_cli_compute_matches_reference(tmp_path, ref):
+    dims = (20, 18, 16)
+    v = m.synth("gnoise", dims)
+    raw = tmp_path / "v.raw"
+    v.astype("<f4").tofile(raw)
+    pre = tmp_path / "out"
+    r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--format", "csv", "--out", pre,
+            "--labels", tmp_path / "lab", "--check")
+    assert r.returncode == 0, r.stderr
+    want = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
+    cps = np.loadtxt(f"{pre}_critical_points.csv", delimiter=",", skiprows=1, ndmin=2)
+    np.testing.assert_array_equal(cps[:, 1].astype(np.uint64), np.asarray(want["cp_cell"], dtype=np.uint64))
+    arcs = np.loadtxt(f"{pre}_arcs.csv", delimiter=",", skiprows=1, ndmin=2, dtype=np.uint64)
+    np.testing.assert_array_equal(arcs[:, 0], np.asarray(want["arc_src"], dtype=np.uint64))
+    np.testing.assert_array_equal(arcs[:, 1], np.asarray(want["arc_dst"], dtype=np.uint64))
+    np.testing.assert_array_equal(arcs[:, 2], np.asarray(want["arc_mult"], dtype=np.uint64))
+    np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_min.raw", dtype="<u4"), want["labels_min"])
+    np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_max.raw", dtype="<u4"), want["labels_max"])
+    assert "check: gradient ok, euler ok, boundary ok" in r.stderr
+    r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--out", tmp_path / "c.json")
+    assert r.returncode == 0 and (tmp_path / "c.json").stat().st_size > 0

@@ -168,3 +168,26 @@ def test_se_arcs_synth(ctx, ref):
     want = ref.se_arcs(codes, dims, l0, l3)
     for g, w in zip((ctx.get("se_saddle"), ctx.get("se_extremum"), ctx.get("se_mult")), want):
         np.testing.assert_array_equal(g, w)
+
+
+def test_validate_option_device_audit(ctx):
+    """ComputeOptions::validate (msc.cpp:67-70): the device matching audit accepts real
+    gradients and rejects tampered ones with runtime_error."""
+    dims = (20, 18, 16)
+    v = m.synth("gnoise", dims)
+    ctx.load_values(v, dims)
+    ctx.compute(m.OPT_SEGMENTATION | m.OPT_VALIDATE)
+    assert ctx.scalar("validate_violations") == 0
+    codes = ctx.get("codes").copy()
+    ctx.load_codes(codes, dims)
+    assert ctx._L.msc3d_ctx_compute_codes(ctx.h, m.OPT_VALIDATE, 0, 1, None) == m.OK
+    paired = np.flatnonzero(codes >= m.FACET_BASE)
+    bad = codes.copy()
+    bad[paired[len(paired) // 2]] = m.UNSET          # an unassigned cell
+    ctx.load_codes(bad, dims)
+    assert ctx._L.msc3d_ctx_compute_codes(ctx.h, m.OPT_VALIDATE, 0, 1, None) == m.ERR_RUNTIME
+    bad = codes.copy()
+    i = paired[len(paired) // 3]
+    bad[i] = codes[i] ^ 1                              # pair direction flipped
+    ctx.load_codes(bad, dims)                         # a partner that does not pair back
+    assert ctx._L.msc3d_ctx_compute_codes(ctx.h, m.OPT_VALIDATE, 0, 1, None) == m.ERR_RUNTIME
