@@ -363,10 +363,10 @@ def main():
                         "stage time from CUDA events on the pipeline stream; traffic = ncu DRAM bytes of the "
                         "stage's kernels for one compute() (profiles/traffic.json)"}
 
-    # ---- e2e through the C ABI with host buffers: pinned f32 samples in,
-    # msc3d_ctx_load_values (H2D + device validation), msc3d_ctx_compute_host
-    # (pipeline + every output copied to pinned host buffers, overlapped with the
-    # later stages); the wall clock covers all of it, every step.
+    # ---- e2e through the C ABI with host buffers: pinned f32 samples in, one
+    # msc3d_ctx_compute_host_values call (upload in z-chunks overlapped with the
+    # gradient, device validation, pipeline, every output copied to pinned host
+    # buffers as soon as it is final); the wall clock covers all of it, every step.
     e2e = None
     if not args.no_e2e:
         host_in = torch.from_numpy(v).pin_memory()
@@ -393,8 +393,9 @@ def main():
         for i in range(2 + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rc = ctx._L.msc3d_ctx_load_values(ctx.h, m.Dims(*dims), m.VALUE_F32, C.c_void_p(host_in.data_ptr()))
-            rc = rc or ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho))
+            rc = ctx._L.msc3d_ctx_compute_host_values(ctx.h, m.Dims(*dims), m.VALUE_F32,
+                                                      C.c_void_p(host_in.data_ptr()), m.OPT_SEGMENTATION, None,
+                                                      C.byref(ho))
             t1 = time.perf_counter()
             if rc:
                 raise RuntimeError(f"compute_host failed: {rc}")
@@ -406,7 +407,8 @@ def main():
         te = max_over_ranks(sum(e2e_times) / len(e2e_times), world, f"cuda:{local}")
         e2e = {"value": world * ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
-               "path": "msc3d_ctx_load_values + msc3d_ctx_compute_host (C ABI), pinned host buffers"}
+               "path": "msc3d_ctx_compute_host_values (C ABI): pinned samples in (upload overlapped with the "
+                       "gradient), pinned host outputs (copies overlapped with the later stages)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -180,6 +180,12 @@ typedef struct msc3d_host_outputs {
     uint64_t n_arcs; /* out */
 } msc3d_host_outputs;
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out);
+/* Host samples in, host results out: msc3d_ctx_load_values + msc3d_ctx_compute_host in
+ * one call, with the upload overlapped too -- the samples go up in z-chunks and the
+ * gradient's tile layers start as soon as the planes they read have arrived.  Same
+ * results and errors (non-finite sample -> MSC3D_ERR_INVALID). */
+int msc3d_ctx_compute_host_values(msc3d_ctx* ctx, msc3d_dims dims, int value_type, const void* host_values,
+                                  int options, double* stage_ms, msc3d_host_outputs* out);
 
 /* The pipeline after the gradient, on the installed codes (msc3d_ctx_load_codes /
  * msc3d_ctx_bind_codes): extremum forests are built from the codes; the saddle

@@ -93,6 +93,7 @@ def lib():
         "msc3d_ctx_compute": (i32, [vp, i32, C.POINTER(C.c_double)]),
         "msc3d_ctx_compute_host": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_ctx_bind_codes": (i32, [vp, Dims, vp]),
+        "msc3d_ctx_compute_host_values": (i32, [vp, Dims, i32, vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_ctx_compute_codes": (i32, [vp, i32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
         "msc3d_field_hash_f64": (u64, [vp, u64]),
         "msc3d_field_hash_f32": (u64, [vp, u64]),

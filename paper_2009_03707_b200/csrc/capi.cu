@@ -374,6 +374,15 @@ int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, std::uint32_t shard, st
                                            /*sharded=*/true);
 }
 
+int msc3d_ctx_compute_host_values(msc3d_ctx* ctx, msc3d_dims dims, int value_type, const void* host_values,
+                                  int options, double* stage_ms, msc3d_host_outputs* out) {
+    if (!ctx || !out || !host_values) return MSC3D_ERR_INVALID;
+    if (value_type != MSC3D_VALUE_F32 && value_type != MSC3D_VALUE_F64) return MSC3D_ERR_INVALID;
+    const int rc = set_dims(ctx, dims);
+    if (rc != MSC3D_OK) return rc;
+    return msc3d_stage::compute_streamed(ctx, host_values, value_type, options, stage_ms, out);
+}
+
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out) {
     if (!ctx || !out) return MSC3D_ERR_INVALID;
     if (!ctx->values) return MSC3D_ERR_STATE;

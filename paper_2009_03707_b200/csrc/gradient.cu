@@ -376,7 +376,7 @@ template <typename T>
 __global__ void __launch_bounds__(NT)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
-           unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles) {
+           unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first) {
     __shared__ T tile[SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
@@ -414,7 +414,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         const std::uint64_t tyz = ti / tiles.x;
         const std::int64_t x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
         const std::int64_t y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
-        const std::int64_t z0 = static_cast<std::int64_t>(tyz / tiles.y) * TZ - 1;
+        const std::int64_t z0 = static_cast<std::int64_t>(tyz / tiles.y + tz_first) * TZ - 1;
         __syncthreads();  // previous tile done with the shared tile / list counts stable
         if (s_ln[0] + NT > kListBuf || s_ln[1] + NT > kListBuf) flush_lists();
         for (int i = tid; i < SX * SY * SZ; i += NT) {
@@ -729,42 +729,78 @@ int upload_gradient_tables(int device) {
     return MSC3D_OK;
 }
 
-int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
-                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
-                    unsigned long long* crit_totals, std::uint32_t* const lists3[3],
-                    unsigned long long* list_counts, int num_sms) {
+int gradient_begin(unsigned long long* crit_totals, unsigned long long* list_counts, cudaStream_t stream) {
     int dev = 0;
     MSC3D_CUDA_TRY(cudaGetDevice(&dev));
     const int rc = upload_gradient_tables(dev);
     if (rc != MSC3D_OK) return rc;
     MSC3D_CUDA_TRY(cudaMemsetAsync(crit_totals, 0, 32, stream));
     MSC3D_CUDA_TRY(cudaMemsetAsync(list_counts, 0, 48, stream));
+    return MSC3D_OK;
+}
+
+unsigned gradient_tile_layers(const Dims& d) { return static_cast<unsigned>((d.nz + TZ - 1) / TZ); }
+int gradient_layer_last_plane(const Dims& d, unsigned tz_end) {  // last vertex plane the layers read
+    return static_cast<int>(std::min<std::int64_t>(d.nz - 1, static_cast<std::int64_t>(tz_end) * TZ));
+}
+
+int gradient_tiles(const void* values, int value_type, const Dims& d, std::uint8_t* codes, std::uint32_t* parent0,
+                   std::uint32_t* parent3, cudaStream_t stream, unsigned long long* crit_totals,
+                   std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms, unsigned tz0,
+                   unsigned tz1) {
+    if (tz1 <= tz0) return MSC3D_OK;
     StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
     const dim3 block(TX, TY, TZ);
     const uint3 tiles = make_uint3(static_cast<unsigned>((d.nx + TX - 1) / TX),
-                                   static_cast<unsigned>((d.ny + TY - 1) / TY),
-                                   static_cast<unsigned>((d.nz + TZ - 1) / TZ));
+                                   static_cast<unsigned>((d.ny + TY - 1) / TY), tz1 - tz0);
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
     // persistent tile loop: a few blocks per SM, each walking tiles with stride grid
     const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(num_sms) * 8)));
+    if (value_type == MSC3D_VALUE_F64)
+        k_gradient<double><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d, codes, parent0, parent3,
+                                                       crit_totals, lists, tiles, tz0);
+    else
+        k_gradient<float><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes, parent0, parent3,
+                                                      crit_totals, lists, tiles, tz0);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int gradient_finish(const void* values, int value_type, const Dims& d, std::uint8_t* codes, std::uint32_t* parent0,
+                    std::uint32_t* parent3, cudaStream_t stream, unsigned long long* crit_totals,
+                    std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms) {
+    StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
     const unsigned lgrid = static_cast<unsigned>(16 * num_sms);
     const unsigned dgrid = static_cast<unsigned>(4 * num_sms);
     if (value_type == MSC3D_VALUE_F64) {
         const double* v = static_cast<const double*>(values);
-        k_gradient<double><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, tiles);
         k_gradient_list<16, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
         k_gradient_list<32, double><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
         k_gradient_deferred<double><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
     } else {
         const float* v = static_cast<const float*>(values);
-        k_gradient<float><<<grid, block, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, tiles);
         k_gradient_list<16, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 0);
         k_gradient_list<32, float><<<lgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, crit_totals, lists, 1);
         k_gradient_deferred<float><<<dgrid, 128, 0, stream>>>(v, d, codes, parent0, parent3, lists, crit_totals);
     }
-    count_launch(4);
+    count_launch(3);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
+}
+
+int launch_gradient(const void* values, int value_type, const Dims& d, std::uint8_t* codes,
+                    std::uint32_t* parent0, std::uint32_t* parent3, cudaStream_t stream,
+                    unsigned long long* crit_totals, std::uint32_t* const lists3[3],
+                    unsigned long long* list_counts, int num_sms) {
+    int rc = gradient_begin(crit_totals, list_counts, stream);
+    if (rc == MSC3D_OK)
+        rc = gradient_tiles(values, value_type, d, codes, parent0, parent3, stream, crit_totals, lists3, list_counts,
+                            num_sms, 0, gradient_tile_layers(d));
+    if (rc == MSC3D_OK)
+        rc = gradient_finish(values, value_type, d, codes, parent0, parent3, stream, crit_totals, lists3, list_counts,
+                             num_sms);
+    return rc;
 }
 
 }  // namespace msc3d_dev

@@ -33,6 +33,20 @@ int launch_gradient(const void* values, int value_type, const Dims& d, std::uint
                     unsigned long long* crit_totals, std::uint32_t* const lists3[3],
                     unsigned long long* list_counts, int num_sms);
 
+// The gradient in pieces (streamed input): tables + counters; tile layers
+// [tz0, tz1) (TZ = 2 vertex planes each; they read vertex planes up to
+// gradient_layer_last_plane(d, tz1)); the large-star list kernels.
+int gradient_begin(unsigned long long* crit_totals, unsigned long long* list_counts, cudaStream_t stream);
+unsigned gradient_tile_layers(const Dims& d);
+int gradient_layer_last_plane(const Dims& d, unsigned tz_end);
+int gradient_tiles(const void* values, int value_type, const Dims& d, std::uint8_t* codes, std::uint32_t* parent0,
+                   std::uint32_t* parent3, cudaStream_t stream, unsigned long long* crit_totals,
+                   std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms, unsigned tz0,
+                   unsigned tz1);
+int gradient_finish(const void* values, int value_type, const Dims& d, std::uint8_t* codes, std::uint32_t* parent0,
+                    std::uint32_t* parent3, cudaStream_t stream, unsigned long long* crit_totals,
+                    std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms);
+
 // critical.cu
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
                           cudaStream_t s, int num_sms);
@@ -62,6 +76,9 @@ namespace msc3d_dev {
 // primitives.cu
 // Copy n u64 device -> mapped host memory with a kernel (no copy engine).
 int launch_small_copy(const std::uint64_t* src, std::uint64_t* dst_mapped, int n, cudaStream_t s);
+// *first_bad = min(*first_bad, index of a non-finite sample) (grid.cpp:86-88)
+int launch_check_finite(const void* values, int value_type, std::uint64_t n, unsigned long long* first_bad,
+                        cudaStream_t s, int num_sms);
 int scan_u32(const std::uint32_t* in, std::uint64_t n, std::uint64_t* out, std::uint64_t* d_total,
              Workspace& ws, cudaStream_t s);
 

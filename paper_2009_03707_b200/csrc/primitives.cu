@@ -3,6 +3,8 @@
 //     look-back (prefix_sum, primitives.hpp:48-106);
 //   * gather / iota helpers used by the stage code.
 // Hand-written; no CUB/Thrust.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "scan.cuh"
@@ -46,11 +48,33 @@ k_scan_u32(const std::uint32_t* __restrict__ in, std::uint64_t n, std::uint64_t*
     if (tile == ntiles - 1 && threadIdx.x == 0 && total) *total = sm[34] + block_total;
 }
 
+__global__ void k_finite_f32(const float* v, std::uint64_t n, unsigned long long* bad) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+        if (!isfinite(v[i])) atomicMin(bad, static_cast<unsigned long long>(i));
+}
+__global__ void k_finite_f64(const double* v, std::uint64_t n, unsigned long long* bad) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+        if (!isfinite(v[i])) atomicMin(bad, static_cast<unsigned long long>(i));
+}
+
 __global__ void k_small_copy(const std::uint64_t* __restrict__ src, volatile std::uint64_t* dst, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 }  // namespace
+
+int launch_check_finite(const void* values, int value_type, std::uint64_t n, unsigned long long* first_bad,
+                        cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>((n + 255) / 256, 16ull * num_sms));
+    if (value_type == MSC3D_VALUE_F64) k_finite_f64<<<grid, 256, 0, s>>>(static_cast<const double*>(values), n, first_bad);
+    else k_finite_f32<<<grid, 256, 0, s>>>(static_cast<const float*>(values), n, first_bad);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
 
 int launch_small_copy(const std::uint64_t* src, std::uint64_t* dst_mapped, int n, cudaStream_t s) {
     if (n <= 0) return MSC3D_OK;

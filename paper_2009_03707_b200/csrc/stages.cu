@@ -725,6 +725,12 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", total, 4));
         amul = static_cast<std::uint64_t*>(ctx->ensure("arc_mult", total, 8));
         if (!asrc || !adst || !amul) return MSC3D_ERR_NOMEM;
+        if (host) {  // the 2s->max block's host position is known now: send it before the 1s->2s block
+            if (host->arc_cap < total) return MSC3D_ERR_INVALID;
+            TRY(sink.copy(host->arc_src + na + nb, amax_src, nc * 4));
+            TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
+            TRY(sink.copy(host->arc_mult + na + nb, amax_mul, nc * 8));
+        }
         o->one = asrc + na;
         o->two = adst + na;
         o->paths = amul + na;
@@ -760,9 +766,6 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         TRY(sink.copy(host->arc_src + na, asrc + na, nb * 4));
         TRY(sink.copy(host->arc_dst + na, adst + na, nb * 4));
         TRY(sink.copy(host->arc_mult + na, amul + na, nb * 8));
-        TRY(sink.copy(host->arc_src + na + nb, amax_src, nc * 4));
-        TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
-        TRY(sink.copy(host->arc_mult + na + nb, amax_mul, nc * 8));
     }
     // device-side arc arrays complete: the min and max blocks around the 1s->2s block
     if (na) {

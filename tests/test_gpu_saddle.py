@@ -200,3 +200,32 @@ def test_compute_host_outputs(ctx, ref, kind):
     # too small an arc buffer is rejected (invalid_argument)
     ho.arc_cap = max(0, na - 1)
     assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == m.ERR_INVALID
+
+
+@pytest.mark.parametrize("chunk_kb", ["8", "16", "100000"])
+def test_compute_host_values_streamed(ctx, ref, monkeypatch, chunk_kb):
+    """msc3d_ctx_compute_host_values: chunked upload overlapped with the gradient, host
+    outputs; identical results; non-finite samples rejected (invalid_argument)."""
+    import ctypes as C
+    monkeypatch.setenv("MSC3D_UPLOAD_CHUNK_KB", chunk_kb)  # 8 KB: 2-plane chunks here
+    dims = (33, 29, 70)
+    v = m.synth("gnoise", dims)
+    want = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
+    ncp, na = len(want["cp_cell"]), len(want["arc_src"])
+    V, Cu = dims[0] * dims[1] * dims[2], (dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1)
+    buf = {"cp_cell": np.zeros(ncp, np.uint32), "cp_index": np.zeros(ncp, np.uint8),
+           "arc_src": np.zeros(na, np.uint32), "arc_dst": np.zeros(na, np.uint32),
+           "arc_mult": np.zeros(na, np.uint64), "labels_min": np.zeros(V, np.uint32),
+           "labels_max": np.zeros(Cu, np.uint32)}
+    ptr = {k: a.ctypes.data for k, a in buf.items()}
+    ho = m.HostOutputs(ptr["cp_cell"], ncp * 4, ptr["cp_index"], ncp, ptr["arc_src"], ptr["arc_dst"],
+                       ptr["arc_mult"], na, ptr["labels_min"], ptr["labels_max"], 0, 0)
+    vv = np.ascontiguousarray(v)
+    assert ctx._L.msc3d_ctx_compute_host_values(ctx.h, m.Dims(*dims), m.VALUE_F32, vv.ctypes.data,
+                                                m.OPT_SEGMENTATION, None, C.byref(ho)) == 0
+    for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+        np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype))
+    bad = vv.copy()
+    bad[V // 2] = np.nan
+    assert ctx._L.msc3d_ctx_compute_host_values(ctx.h, m.Dims(*dims), m.VALUE_F32, bad.ctypes.data,
+                                                m.OPT_SEGMENTATION, None, C.byref(ho)) == m.ERR_INVALID
