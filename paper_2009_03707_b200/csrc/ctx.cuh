@@ -37,10 +37,15 @@ struct msc3d_ctx {
     std::uint64_t* h_small_dev = nullptr;  // its device address
     std::uint64_t launches_at_create = 0;
     cudaStream_t copy = nullptr;  // device-to-host copies overlapping the pipeline
+    cudaStream_t h2d = nullptr;   // host-to-device input chunks overlapping the gradient
 
     cudaStream_t copy_stream() {
         if (!copy && cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking) != cudaSuccess) copy = nullptr;
         return copy;
+    }
+    cudaStream_t h2d_stream() {
+        if (!h2d && cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess) h2d = nullptr;
+        return h2d;
     }
 
     ~msc3d_ctx() {
@@ -50,6 +55,7 @@ struct msc3d_ctx {
         if (h_small) cudaFreeHost(h_small);
         if (own_stream && stream) cudaStreamDestroy(stream);
         if (copy) cudaStreamDestroy(copy);
+        if (h2d) cudaStreamDestroy(h2d);
     }
 
     // Ensure array `name` holds `count` elements of `elem` bytes; contents undefined.

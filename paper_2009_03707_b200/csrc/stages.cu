@@ -812,6 +812,92 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     return MSC3D_OK;
 }
 
+int validate(msc3d_ctx* ctx);
+
+// The whole pipeline from HOST samples: the input goes up in z-chunks on a copy
+// stream and the gradient's tile layers start as soon as the planes they read have
+// arrived, so the upload overlaps the gradient; the outputs come back as in
+// compute_host.  Non-finite samples -> invalid_argument (grid.cpp:86-88), checked
+// on the device after the upload.
+int compute_streamed(msc3d_ctx* ctx, const void* host_values, int value_type, int options, double* stage_ms,
+                     const msc3d_host_outputs* host) {
+    const Dims& d = ctx->dims;
+    const int elem = value_type == MSC3D_VALUE_F64 ? 8 : 4;
+    void* vals = ctx->ensure("values", d.n_verts, elem);
+    if (!vals) return MSC3D_ERR_NOMEM;
+    ctx->values = vals;
+    ctx->value_type = value_type;
+    const cudaStream_t s = ctx->stream;
+    const cudaStream_t up = ctx->h2d_stream();
+    if (!up) return MSC3D_ERR_CUDA;
+    cudaEvent_t t0 = nullptr;
+    if (stage_ms) {
+        MSC3D_CUDA_TRY(cudaEventCreate(&t0));
+        MSC3D_CUDA_TRY(cudaEventRecord(t0, s));
+        MSC3D_CUDA_TRY(cudaStreamWaitEvent(up, t0, 0));
+    }
+    // chunks of vertex planes
+    const std::uint64_t plane = static_cast<std::uint64_t>(d.nx) * d.ny * elem;
+    std::int64_t chunk_bytes = 32ll << 20;  // ~32 MB per upload chunk (MSC3D_UPLOAD_CHUNK_KB overrides, for tests)
+    if (const char* e = std::getenv("MSC3D_UPLOAD_CHUNK_KB")) chunk_bytes = std::max(1ll, std::atoll(e)) << 10;
+    const std::int64_t zc = std::max<std::int64_t>(2, chunk_bytes / static_cast<std::int64_t>(plane));
+    const std::int64_t nchunks = (d.nz + zc - 1) / zc;
+    std::vector<cudaEvent_t> ev(static_cast<std::size_t>(nchunks), nullptr);
+    int rc = MSC3D_OK;
+    for (std::int64_t c = 0; c < nchunks && rc == MSC3D_OK; ++c) {
+        const std::int64_t z0 = c * zc, z1 = std::min<std::int64_t>(d.nz, z0 + zc);
+        if (cudaMemcpyAsync(static_cast<char*>(vals) + z0 * plane, static_cast<const char*>(host_values) + z0 * plane,
+                            (z1 - z0) * plane, cudaMemcpyHostToDevice, up) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventRecord(ev[c], up) != cudaSuccess)
+            rc = MSC3D_ERR_CUDA;
+    }
+    auto cleanup = [&]() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (t0) cudaEventDestroy(t0);
+    };
+    // gradient tile layers as their planes arrive
+    auto* codes = static_cast<std::uint8_t*>(ctx->ensure("codes", d.n_cells, 1));
+    auto* p0 = static_cast<std::uint32_t*>(ctx->ensure("parent0", d.n_verts, 4));
+    auto* p3 = static_cast<std::uint32_t*>(ctx->ensure("parent3", d.n_cubes, 4));
+    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list_ties", d.n_verts, 4))};
+    if (!codes || !p0 || !p3 || !lists[0] || !lists[1] || !lists[2]) rc = rc ? rc : MSC3D_ERR_NOMEM;
+    auto* crit_totals = reinterpret_cast<unsigned long long*>(ctx->d_small + 40);
+    auto* list_counts = reinterpret_cast<unsigned long long*>(ctx->d_small + 44);
+    if (rc == MSC3D_OK) rc = msc3d_dev::gradient_begin(crit_totals, list_counts, s);
+    const unsigned layers = msc3d_dev::gradient_tile_layers(d);
+    const unsigned step = static_cast<unsigned>(std::max<std::int64_t>(1, zc / 2));
+    std::int64_t waited = -1;
+    for (unsigned t0l = 0; t0l < layers && rc == MSC3D_OK; t0l += step) {
+        const unsigned t1l = std::min(layers, t0l + step);
+        const std::int64_t need = msc3d_dev::gradient_layer_last_plane(d, t1l) / zc;  // chunk of the last plane read
+        for (; waited < need && rc == MSC3D_OK; ++waited)
+            if (cudaStreamWaitEvent(s, ev[waited + 1], 0) != cudaSuccess) rc = MSC3D_ERR_CUDA;
+        if (rc == MSC3D_OK)
+            rc = msc3d_dev::gradient_tiles(vals, value_type, d, codes, p0, p3, s, crit_totals, lists, list_counts,
+                                           ctx->num_sms, t0l, t1l);
+    }
+    for (; waited + 1 < nchunks && rc == MSC3D_OK; ++waited)
+        if (cudaStreamWaitEvent(s, ev[waited + 1], 0) != cudaSuccess) rc = MSC3D_ERR_CUDA;
+    if (rc == MSC3D_OK)
+        rc = msc3d_dev::gradient_finish(vals, value_type, d, codes, p0, p3, s, crit_totals, lists, list_counts,
+                                        ctx->num_sms);
+    // samples must be finite (checked once all of them are up)
+    auto* bad = reinterpret_cast<unsigned long long*>(ctx->d_small + 22);
+    if (rc == MSC3D_OK && cudaMemsetAsync(bad, 0xff, 8, s) != cudaSuccess) rc = MSC3D_ERR_CUDA;
+    if (rc == MSC3D_OK) rc = msc3d_dev::launch_check_finite(vals, value_type, d.n_verts, bad, s, ctx->num_sms);
+    if (rc == MSC3D_OK) rc = ctx->fetch_range(22, 1);
+    if (rc == MSC3D_OK && ctx->h_small[22] != ~0ull) rc = MSC3D_ERR_INVALID;
+    ctx->crit_counts_valid = true;
+    if (rc == MSC3D_OK && (options & MSC3D_OPT_VALIDATE)) rc = validate(ctx);
+    if (rc == MSC3D_OK) rc = compute_from_codes(ctx, options, stage_ms, host, true, 0, ~0ull, t0);
+    cleanup();
+    return rc;
+}
+
 // ComputeOptions::validate (msc.cpp:67-70): the gradient's matching audit on the
 // device; a broken gradient -> runtime_error.
 int validate(msc3d_ctx* ctx) {
