@@ -373,7 +373,7 @@ struct StarLists {
 constexpr int kListBuf = 1024;
 
 template <typename T>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 5)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
            unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first) {
