@@ -356,9 +356,14 @@ def main():
             traffic = {}
     for name in STAGES:
         stages[name]["dram_bytes_ncu"] = traffic.get(name)
+        t = stages[name]["ms"]
+        if traffic.get(name) and t > 0:  # what the stage actually moves through HBM
+            stages[name]["dram_gbs_ncu"] = traffic[name] / (t / 1e3) / 1e9
+            stages[name]["dram_frac_ncu"] = stages[name]["dram_gbs_ncu"] / peak
     roofline = {"bound": "hbm", "stage": dom, "achieved": stages[dom]["achieved_gbs"], "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
                 "traffic": traffic.get(dom), "alg_bytes_per_launch": alg[dom],
+                "traffic_frac": stages[dom].get("dram_frac_ncu"),
                 "note": "per stage (the reference's StageTimings unit): algorithmic bytes (SURVEY.md 8(d)) / "
                         "stage time from CUDA events on the pipeline stream; traffic = ncu DRAM bytes of the "
                         "stage's kernels for one compute() (profiles/traffic.json)"}
