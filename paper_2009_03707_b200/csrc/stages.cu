@@ -604,8 +604,13 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         TRY(forest(ctx, 0));
         TRY(forest(ctx, 3));
     }
-    TRY(roots_fast(ctx, 0));
-    TRY(roots_fast(ctx, 3));
+    {  // roots of both forests in place (the parent arrays become the label arrays)
+        auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);  // 3 x u32 (slots 23-24)
+        auto* rounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 23, 0, 16, s));
+        TRY(msc3d_dev::launch_jump_all(ctx->ptr<std::uint32_t>("parent0"), ctx->count("parent0"),
+                                       ctx->ptr<std::uint32_t>("parent3"), ctx->count("parent3"), flags, rounds, s, sms));
+    }
     auto* label0 = ctx->ptr<std::uint32_t>("parent0");
     auto* label3 = ctx->ptr<std::uint32_t>("parent3");
     auto* remap0 = static_cast<std::uint32_t*>(ctx->ensure("remap0", d.n_verts, 4));
@@ -634,6 +639,8 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     // critical points, label volumes, min->1s and 2s->max arcs; their host copies
     // overlap the saddle stages
     TRY(ctx->fetch_small(34));
+    if (ctx->h_small[25] > 64) return MSC3D_ERR_RUNTIME;  // root finding did not converge: a cycle
+    ctx->scalars["jump_rounds"] = static_cast<std::int64_t>(ctx->h_small[25]);
     const std::uint64_t na = c0 ? ctx->h_small[32] : 0;  // min->1s arcs
     const std::uint64_t nc = c2 ? ctx->h_small[33] : 0;  // 2s->max arcs
     ctx->scalars["arcs_min"] = static_cast<std::int64_t>(na);
