@@ -343,14 +343,11 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
     if (!ptbits) return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_passthrough(node, nj, fwd, ptbits, s, sms));
-    auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 18);
-    for (int r = 0; nj; ++r) {
-        MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, s));
-        TRY(msc3d_dev::launch_jump_round(fwd, nj, changed, s, sms));
-        TRY(ctx->fetch_small(28));
-        if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle in a walk
-        if (!(ctx->h_small[18] & 0xffffffffu)) break;
-        if (r > 64) return MSC3D_ERR_RUNTIME;  // cycle of pass-through junctions
+    {  // pointer jumping to the end of pass-through chains, all rounds in one launch
+        auto* jflags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);
+        auto* jrounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 23, 0, 24, s));
+        TRY(msc3d_dev::launch_jump_all(fwd, nj, nullptr, 0, jflags, jrounds, s, sms));
     }
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
     auto* n_skip = reinterpret_cast<unsigned long long*>(ctx->d_small + 19);
@@ -365,7 +362,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
     TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(28));
-    if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle
+    if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle in a walk
+    if (nj && ctx->h_small[25] > 64) return MSC3D_ERR_RUNTIME;                  // cycle of pass-through junctions
     const std::uint64_t nov = nj ? ctx->h_small[0] : 0;
     const std::uint64_t nskip = ctx->h_small[19];
     const std::uint64_t nq = ctx->h_small[20];
