@@ -406,40 +406,100 @@ struct alignas(16) NodeRec {
 };
 static_assert(sizeof(NodeRec) == 64, "NodeRec is one 64-byte line");
 
+constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by the walk itself
+
+// Leaves finished during the walk: a node whose branches all end at 2-saddles (or
+// dead ends) has P = its sorted terminal keys with multiplicities.  A junction leaf
+// with <= 2 distinct keys stores its inline record right here (coalesced: junctions
+// are walked in index order) and sets its bit in `predone`; a 1-saddle leaf records
+// its merged length.  Both get pending kDone: Kahn's round 0 skips them, and the
+// rewrite drops predone children from their parents' pending counts and parent
+// lists -- no atomics for the ~40% of the junction graph that are leaves.
 template <typename IdT>
 __global__ void __launch_bounds__(kThreads)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
-       NodeRec* __restrict__ node, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags) {
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        std::uint32_t de0;
-        if (jlist) {
-            de0 = jlist[i];
-        } else {
-            const Coord o = unpack(d, srcs[i]);
-            const int a = (o.x & 1) ? 0 : ((o.y & 1) ? 1 : 2);
-            de0 = 3u * static_cast<std::uint32_t>((o.x >> 1) + d.nx * ((o.y >> 1) + d.ny * (o.z >> 1))) + a;
-        }
-        const std::uint32_t s0 = c.succ[de0];
-        const EdgeRef e(de0);
-        std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
-        std::uint32_t pend = 0;
-        int nd = 0;
+       NodeRec* __restrict__ node, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
+       uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
+       unsigned long long* __restrict__ n_predone) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < n;
+         base += stride) {
+        const std::uint64_t i = base + (threadIdx.x & 31);
+        bool pre = false;
+        if (i < n) {
+            std::uint32_t de0;
+            if (jlist) {
+                de0 = jlist[i];
+            } else {
+                const Coord o = unpack(d, srcs[i]);
+                const int a = (o.x & 1) ? 0 : ((o.y & 1) ? 1 : 2);
+                de0 = 3u * static_cast<std::uint32_t>((o.x >> 1) + d.nx * ((o.y >> 1) + d.ny * (o.z >> 1))) + a;
+            }
+            const std::uint32_t s0 = c.succ[de0];
+            const EdgeRef e(de0);
+            std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
+            std::uint32_t pend = 0;
+            int nd = 0;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const std::uint32_t f = (s0 >> (3 * p)) & 7u;
-            if (f == 0) continue;
-            const std::uint32_t t = f == 1 ? (kTerm | c.tmap[term_quad(e, p, c.g)])
-                                           : walk_branch(c, succ_edge(e, de0, p, f, c.g), &flags[2]);
-            dd[0] = nd == 0 ? t : dd[0];
-            dd[1] = nd == 1 ? t : dd[1];
-            dd[2] = nd == 2 ? t : dd[2];
-            dd[3] = nd == 3 ? t : dd[3];
-            ++nd;
-            if (!(t & kTerm)) ++pend;
+            for (int p = 0; p < 4; ++p) {
+                const std::uint32_t f = (s0 >> (3 * p)) & 7u;
+                if (f == 0) continue;
+                const std::uint32_t t = f == 1 ? (kTerm | c.tmap[term_quad(e, p, c.g)])
+                                               : walk_branch(c, succ_edge(e, de0, p, f, c.g), &flags[2]);
+                dd[0] = nd == 0 ? t : dd[0];
+                dd[1] = nd == 1 ? t : dd[1];
+                dd[2] = nd == 2 ? t : dd[2];
+                dd[3] = nd == 3 ? t : dd[3];
+                ++nd;
+                if (!(t & kTerm)) ++pend;
+            }
+            *reinterpret_cast<uint4*>(node[i].dest) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+            if (pend == 0) {
+                // terminal keys (kNone sorts last), sorted, runs counted
+                std::uint32_t k[4] = {dd[0] & ~kTerm, dd[1] & ~kTerm, dd[2] & ~kTerm, dd[3] & ~kTerm};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (dd[q] == kNone) k[q] = 0xffffffffu;
+                auto ce = [](std::uint32_t& x, std::uint32_t& y) {
+                    const std::uint32_t lo = min(x, y), hi = max(x, y);
+                    x = lo;
+                    y = hi;
+                };
+                ce(k[0], k[1]);
+                ce(k[2], k[3]);
+                ce(k[0], k[2]);
+                ce(k[1], k[3]);
+                ce(k[1], k[2]);
+                std::uint32_t uk[4] = {0, 0, 0, 0}, uc[4] = {0, 0, 0, 0};
+                std::uint32_t m = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (k[q] == 0xffffffffu) continue;
+                    const bool same = q > 0 && k[q] == k[q - 1];
+                    if (!same) ++m;
+#pragma unroll
+                    for (int z = 0; z < 4; ++z)
+                        if (static_cast<std::uint32_t>(z) == m - 1) {
+                            uk[z] = k[q];
+                            uc[z] += 1;
+                        }
+                }
+                if (!jlist) {
+                    slen[i] = m;
+                    pre = true;
+                } else if (m <= 2) {
+                    rec[2 * i] = make_uint4(m, uk[0], uk[1], 0u);
+                    rec[2 * i + 1] = make_uint4(uc[0], 0u, uc[1], 0u);
+                    pre = true;
+                }
+            }
+            pending[i] = pre ? kDone : pend;
         }
-        *reinterpret_cast<uint4*>(node[i].dest) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
-        pending[i] = pend;
+        const unsigned bits = __ballot_sync(0xffffffffu, pre);
+        if ((threadIdx.x & 31) == 0 && predone) {
+            predone[base >> 5] = bits;
+            if (bits) atomicAdd(n_predone, static_cast<unsigned long long>(__popc(bits)));
+        }
     }
 }
 
@@ -481,7 +541,7 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
 // are queued as (destination, slot, parent) for the overflow list.
 __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
                           const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
-                          std::uint32_t* __restrict__ pending,
+                          const unsigned int* __restrict__ predone, std::uint32_t* __restrict__ pending,
                           std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
                           unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
                           unsigned long long* __restrict__ n_skip) {
@@ -497,11 +557,14 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
         }
         uint4 d4 = *dp;
         std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+        std::uint32_t waiting = 0;  // junction children Kahn still has to finish
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             if (dd[b] & kTerm) continue;
             const std::uint32_t t = ((ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u) ? fwd[dd[b]] : dd[b];
             dd[b] = t;
+            if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
+            ++waiting;
             const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
             if (slot < static_cast<std::uint32_t>(kInlineParents)) {
                 node[t].par[slot] = static_cast<std::uint32_t>(i);
@@ -510,6 +573,7 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
                 if (q < ovq_cap) ovq[q] = make_uint4(t, slot, static_cast<std::uint32_t>(i), 0u);
             }
         }
+        if (pending[i] != kDone) pending[i] = waiting;
         *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
     }
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
@@ -1357,17 +1421,19 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, cudaStream_t s,
+                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
+                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, cudaStream_t s,
                 int num_sms) {
     if (n == 0) return MSC3D_OK;
     WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
     auto* nr = static_cast<NodeRec*>(node);
+    auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)
         k_walk<std::uint32_t><<<grid_full(n), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags);
+            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone);
     else
         k_walk<std::uint64_t><<<grid_full(n), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags);
+            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -1385,11 +1451,11 @@ int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, u
 }
 
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   const unsigned int* ptbits, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
     k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits,
-                                                             pending,
+                                                      predone, pending,
                                                              indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());

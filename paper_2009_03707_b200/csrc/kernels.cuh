@@ -209,15 +209,18 @@ int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, 
                          int num_sms);
 int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff,
                          std::uint32_t* jlist, cudaStream_t s, int num_sms);
+// junction launch: rec / predone (bit per junction) / n_predone set, slen null;
+// 1-saddle launch: slen set (their merged length when all branches are terminal), rec/predone null
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, cudaStream_t s,
+                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
+                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, cudaStream_t s,
                 int num_sms);
 int node_rec_bytes();
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
                        int num_sms);
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   const unsigned int* ptbits, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms);
 int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
                            int num_sms);

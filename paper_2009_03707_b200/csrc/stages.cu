@@ -334,9 +334,14 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
 
     // branch walks (saddle_graph.cpp:139-202): destinations and pending children
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, node, pending, flags, s, sms));
+    auto* predone = static_cast<unsigned int*>(ctx->ensure("predone", (nj + 31) / 32 + 1, 4));
+    if (!predone) return MSC3D_ERR_NOMEM;
+    auto* n_predone = reinterpret_cast<unsigned long long*>(ctx->d_small + 30);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_predone, 0, 8, s));
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, node, pending, flags, rec, nullptr,
+                               predone, n_predone, s, sms));
     TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, src_ids, w, n1,
-                               static_cast<char*>(node) + nj * msc3d_dev::node_rec_bytes(), pending + nj, flags, s,
+                               static_cast<char*>(node) + nj * msc3d_dev::node_rec_bytes(), pending + nj, flags, nullptr, slen, nullptr, nullptr, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
     // contracted away by pointer jumping
@@ -357,7 +362,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // (nde u32 = 3V*4 bytes, room for 3V/4 entries >> the measured ~0.1% of nodes)
     void* ovq = fa;
     const std::uint64_t ovq_cap = nde / 4;
-    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s, sms));
+    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s,
+                                  sms));
     // parents beyond the inline ones: an overflow list
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
     TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
@@ -428,7 +434,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
             pcap *= 2;
             continue;
         }
-        if (ctx->h_small[59] != nj - nskip) return MSC3D_ERR_RUNTIME;  // junction cycle (path_matrix.cpp:202-203)
+        // junctions finished by Kahn + by the walk (leaves) + contracted = all, else a cycle
+        if (ctx->h_small[59] + ctx->h_small[30] != nj - nskip) return MSC3D_ERR_RUNTIME;  // path_matrix.cpp:202-203
         break;
     }
     {
