@@ -364,13 +364,14 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
 // [0] stars of 9..16 cells, [1] 17..27 cells, [2] stars with tied values.
 struct StarLists {
     std::uint32_t* list[3];
+    std::uint32_t* mask[2];     // lists 0/1: the star's slot mask S, computed by the tile kernel
     unsigned long long* count;  // 3 counters, then 3 chunk heads for the list kernels
 };
 
 // Block-level buffers for the large-star work lists: appends are shared-memory
 // atomics; the global list counters are touched once per flush (a counter hit by
 // every thread of the grid serialises in the L2).
-constexpr int kListBuf = 1024;
+constexpr int kListBuf = 768;
 
 template <typename T>
 __global__ void __launch_bounds__(NT, 5)
@@ -383,6 +384,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ unsigned long long s_crit[4];
     __shared__ std::uint32_t s_M[27 * NT];
     __shared__ std::uint32_t s_lb[2][kListBuf];
+    __shared__ std::uint32_t s_lm[2][kListBuf];
     __shared__ std::uint32_t s_ln[2];
     __shared__ unsigned long long s_base[2];
     __shared__ std::uint32_t s_wn[6], s_wtotal;  // phase-2 work list: buckets of star size 3..8
@@ -403,7 +405,10 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         __syncthreads();
 #pragma unroll
         for (int w = 0; w < 2; ++w)
-            for (std::uint32_t k = tid; k < s_ln[w]; k += NT) lists.list[w][s_base[w] + k] = s_lb[w][k];
+            for (std::uint32_t k = tid; k < s_ln[w]; k += NT) {
+                lists.list[w][s_base[w] + k] = s_lb[w][k];
+                lists.mask[w][s_base[w] + k] = s_lm[w][k];
+            }
         __syncthreads();
         if (tid < 2) s_ln[tid] = 0;
         __syncthreads();
@@ -479,8 +484,9 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                     w.pair(13, __ffs(S & ~kCentre) - 1);
                 } else if (n > 8) {
                     const int which = n <= 16 ? 0 : 1;
-                    s_lb[which][atomicAdd(&s_ln[which], 1u)] =
-                        static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+                    const std::uint32_t at = atomicAdd(&s_ln[which], 1u);
+                    s_lb[which][at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
+                    s_lm[which][at] = S;
                 } else {
                     atomicAdd(&s_wn[n - 3], 1u);
                 }
@@ -592,18 +598,23 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
             const int z = (t * 57) >> 9, rr = t - 9 * z, y = (rr * 11) >> 5, x = rr - 3 * y;
             return centre[(x - 1) + (y - 1) * sy + (z - 1) * sz];
         };
-        const T fv = centre[0];
-        std::uint32_t below = kCentre;
+        std::uint32_t S;
+        if (K == 16) {
+            S = lists.mask[which][i];  // from the tile kernel
+        } else {  // (recomputing it measured faster here: fewer live registers across the loads)
+            const T fv = centre[0];
+            std::uint32_t below = kCentre;
 #pragma unroll
-        for (int t = 0; t < 27; ++t) {
-            if (t == 13) continue;
-            if (!((inr >> t) & 1u)) continue;
-            const T u = centre[slot_off(t, 0) + slot_off(t, 1) * sy + slot_off(t, 2) * sz];
-            if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+            for (int t = 0; t < 27; ++t) {
+                if (t == 13) continue;
+                if (!((inr >> t) & 1u)) continue;
+                const T u = centre[slot_off(t, 0) + slot_off(t, 1) * sy + slot_off(t, 2) * sz];
+                if (u < fv || (u == fv && t < 13)) below |= 1u << t;
+            }
+            S = below & inr;
+            S &= facets_present(S);
+            S &= facets_present(S);
         }
-        std::uint32_t S = below & inr;
-        S &= facets_present(S);
-        S &= facets_present(S);
         if (!star_fast<K, T>(val, S, __popc(S), s_fac, s_cof, &s_M[threadIdx.x], 128, w)) {
             const unsigned long long at = atomicAdd(&lists.count[2], 1ull);
             lists.list[2][at] = vi;
@@ -749,7 +760,8 @@ int gradient_tiles(const void* values, int value_type, const Dims& d, std::uint8
                    std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms, unsigned tz0,
                    unsigned tz1) {
     if (tz1 <= tz0) return MSC3D_OK;
-    StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
+    // lists 0/1 hold 2 * n_verts entries: ids, then the stars' slot masks
+    StarLists lists{{lists3[0], lists3[1], lists3[2]}, {lists3[0] + d.n_verts, lists3[1] + d.n_verts}, list_counts};
     const dim3 block(TX, TY, TZ);
     const uint3 tiles = make_uint3(static_cast<unsigned>((d.nx + TX - 1) / TX),
                                    static_cast<unsigned>((d.ny + TY - 1) / TY), tz1 - tz0);
@@ -770,7 +782,8 @@ int gradient_tiles(const void* values, int value_type, const Dims& d, std::uint8
 int gradient_finish(const void* values, int value_type, const Dims& d, std::uint8_t* codes, std::uint32_t* parent0,
                     std::uint32_t* parent3, cudaStream_t stream, unsigned long long* crit_totals,
                     std::uint32_t* const lists3[3], unsigned long long* list_counts, int num_sms) {
-    StarLists lists{{lists3[0], lists3[1], lists3[2]}, list_counts};
+    // lists 0/1 hold 2 * n_verts entries: ids, then the stars' slot masks
+    StarLists lists{{lists3[0], lists3[1], lists3[2]}, {lists3[0] + d.n_verts, lists3[1] + d.n_verts}, list_counts};
     const unsigned lgrid = static_cast<unsigned>(16 * num_sms);
     const unsigned dgrid = static_cast<unsigned>(4 * num_sms);
     if (value_type == MSC3D_VALUE_F64) {

@@ -36,8 +36,8 @@ int gradient(msc3d_ctx* ctx, bool with_forests) {
     }
     // per-dimension critical counts come for free from the gradient kernel; stars
     // with tied values are finished by the deferred slow-path kernel
-    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", d.n_verts, 4)),
-                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", d.n_verts, 4)),
+    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", 2 * d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", 2 * d.n_verts, 4)),
                                static_cast<std::uint32_t*>(ctx->ensure("star_list_ties", d.n_verts, 4))};
     if (!lists[0] || !lists[1] || !lists[2]) return MSC3D_ERR_NOMEM;
     ctx->crit_counts_valid = true;
@@ -873,8 +873,8 @@ int compute_streamed(msc3d_ctx* ctx, const void* host_values, int value_type, in
     auto* codes = static_cast<std::uint8_t*>(ctx->ensure("codes", d.n_cells, 1));
     auto* p0 = static_cast<std::uint32_t*>(ctx->ensure("parent0", d.n_verts, 4));
     auto* p3 = static_cast<std::uint32_t*>(ctx->ensure("parent3", d.n_cubes, 4));
-    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", d.n_verts, 4)),
-                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", d.n_verts, 4)),
+    std::uint32_t* lists[3] = {static_cast<std::uint32_t*>(ctx->ensure("star_list16", 2 * d.n_verts, 4)),
+                               static_cast<std::uint32_t*>(ctx->ensure("star_list32", 2 * d.n_verts, 4)),
                                static_cast<std::uint32_t*>(ctx->ensure("star_list_ties", d.n_verts, 4))};
     if (!codes || !p0 || !p3 || !lists[0] || !lists[1] || !lists[2]) rc = rc ? rc : MSC3D_ERR_NOMEM;
     auto* crit_totals = reinterpret_cast<unsigned long long*>(ctx->d_small + 40);
