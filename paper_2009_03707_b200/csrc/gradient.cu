@@ -371,14 +371,17 @@ struct StarLists {
 // Block-level buffers for the large-star work lists: appends are shared-memory
 // atomics; the global list counters are touched once per flush (a counter hit by
 // every thread of the grid serialises in the L2).
-constexpr int kListBuf = 768;
+constexpr int kListBuf = 512;
 
 template <typename T>
 __global__ void __launch_bounds__(NT, 5)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
            unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first) {
-    __shared__ T tile[SZ][SY][SX];
+    // f32: two tile buffers, the next tile streams in (cp.async) while this one is
+    // processed; f64: one (static shared memory budget)
+    constexpr int kBufs = sizeof(T) == 4 ? 2 : 1;
+    __shared__ T tiles_sm[kBufs][SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
     __shared__ unsigned long long s_crit[4];
@@ -415,22 +418,45 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     };
     std::uint32_t crit[4] = {0, 0, 0, 0};
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
-    for (std::uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    auto origin = [&](std::uint64_t ti, std::int64_t& x0, std::int64_t& y0, std::int64_t& z0) {
         const std::uint64_t tyz = ti / tiles.x;
-        const std::int64_t x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
-        const std::int64_t y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
-        const std::int64_t z0 = static_cast<std::int64_t>(tyz / tiles.y + tz_first) * TZ - 1;
-        __syncthreads();  // previous tile done with the shared tile / list counts stable
-        if (s_ln[0] + NT > kListBuf || s_ln[1] + NT > kListBuf) flush_lists();
+        x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
+        y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
+        z0 = static_cast<std::int64_t>(tyz / tiles.y + tz_first) * TZ - 1;
+    };
+    // tile ti (+1 halo) -> buffer b: in-range samples by asynchronous copies, the rest 0
+    auto load_tile = [&](std::uint64_t ti, int b) {
+        std::int64_t x0, y0, z0;
+        origin(ti, x0, y0, z0);
+        T* dst = &tiles_sm[b][0][0][0];
         for (int i = tid; i < SX * SY * SZ; i += NT) {
             const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
             const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-            T v = T(0);
-            if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz)
-                v = f[gx + d.nx * (gy + d.ny * gz)];
-            tile[lz][ly][lx] = v;
+            if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+                const T* src = f + gx + d.nx * (gy + d.ny * gz);
+                if (sizeof(T) == 4)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+            } else {
+                dst[i] = T(0);
+            }
         }
-        __syncthreads();
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (blockIdx.x < ntiles) load_tile(blockIdx.x, 0);
+    int cur = 0;
+    for (std::uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        std::int64_t x0, y0, z0;
+        origin(ti, x0, y0, z0);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();  // tile ti in shared memory; the previous tile's work done
+        if (s_ln[0] + NT > kListBuf || s_ln[1] + NT > kListBuf) flush_lists();
+        const std::uint64_t tn = ti + gridDim.x;
+        if (kBufs == 2 && tn < ntiles) load_tile(tn, cur ^ 1);  // overlaps this tile's work
+        auto& tile = tiles_sm[cur];
+        if (kBufs == 2) cur ^= 1;
 
         auto writer_for = [&](int lid, StarWriter& w) {  // false: vertex outside the grid
             const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
@@ -525,6 +551,10 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
+        }
+        if (kBufs == 1 && tn < ntiles) {
+            __syncthreads();  // everyone done with the single buffer
+            load_tile(tn, 0);
         }
     }
     flush_lists();
