@@ -763,12 +763,21 @@ __device__ __forceinline__ std::uint32_t merge(const Inputs& in, const PoolRef& 
 // copies its <= 4 inputs into its slice of a per-warp shared buffer with
 // independent 16-byte loads (all in flight at once), then merges from shared memory.
 constexpr int kWarpCap = 1024;  // entries per warp buffer (larger inputs: direct merge)
+constexpr int kWarpCapWide = 512;  // the high-occupancy configuration of the early rounds
+constexpr unsigned long long kSwitchBelow = 1ull << 20;  // frontier size below which the tail configuration takes over
 constexpr std::uint32_t kHeavy = 48;  // total input length above which the whole warp merges the node
 
-struct alignas(16) WarpBuf {
-    std::uint64_t cnt[kWarpCap];
-    std::uint32_t key[kWarpCap];
+// A warp's slice of the dynamic shared memory: cap (key, count) entries.
+struct WarpBuf {
+    std::uint64_t* cnt;
+    std::uint32_t* key;
+    std::uint32_t cap;
 };
+constexpr std::size_t warp_buf_bytes(int cap) { return static_cast<std::size_t>(cap) * 12; }
+__device__ __forceinline__ WarpBuf warp_buf(void* smem, std::uint32_t cap) {
+    char* base = static_cast<char*>(smem) + (threadIdx.x >> 5) * warp_buf_bytes(static_cast<int>(cap));
+    return WarpBuf{reinterpret_cast<std::uint64_t*>(base), reinterpret_cast<std::uint32_t*>(base + 8 * cap), cap};
+}
 
 // Slot of list b in the lane's staging area: lists start at multiples of 4 entries
 // (16-byte aligned for the asynchronous copies).
@@ -786,7 +795,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // asynchronous 16-byte copies (no registers, all in flight at once), inline ones
 // by plain stores.  The caller waits with cp_async_wait_all + __syncwarp.
 template <bool kCounts>
-__device__ __forceinline__ void stage(const Inputs& in, const PoolRef& pool, WarpBuf& wb, std::uint32_t base) {
+__device__ __forceinline__ void stage(const Inputs& in, const PoolRef& pool, WarpBuf wb, std::uint32_t base) {
     std::uint32_t at = base;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
@@ -811,7 +820,7 @@ __device__ __forceinline__ void stage(const Inputs& in, const PoolRef& pool, War
 
 // Merge the staged lists of this lane; emit(out_index, key, count).
 template <bool kCounts, typename Emit>
-__device__ __forceinline__ std::uint32_t merge_staged(const Inputs& in, const WarpBuf& wb, std::uint32_t base,
+__device__ __forceinline__ std::uint32_t merge_staged(const Inputs& in, WarpBuf wb, std::uint32_t base,
                                                       bool* ovf, Emit emit) {
     std::uint32_t pos[4], end[4], kk[4];
     std::uint32_t at = base;
@@ -858,7 +867,7 @@ __device__ __forceinline__ std::uint32_t count_below(const std::uint32_t* k, std
 // list) in the shared scratch wb[S, S + T); then runs of equal keys (<= 4 long) are
 // summed and the run heads written, compacted, to the output [ok, oc).  Returns the
 // output length (uniform).  All 32 lanes call; requires S + T <= kWarpCap.
-__device__ __forceinline__ std::uint32_t merge_heavy(const Inputs& in, WarpBuf& wb, std::uint32_t* ok,
+__device__ __forceinline__ std::uint32_t merge_heavy(const Inputs& in, WarpBuf wb, std::uint32_t* ok,
                                                      std::uint64_t* oc, bool* ovf) {
     const int lane = threadIdx.x & 31;
     std::uint32_t st[4], S = 0;
@@ -992,6 +1001,8 @@ struct CountArgs {
     std::uint32_t* heavy_q;    // the round's heavy nodes
     unsigned long long* heavy_n;
     unsigned long long* heavy_head;
+    unsigned long long switch_below;  // wide configuration: stop below this frontier size
+    unsigned long long* resume;       // [0] round [1] frontier size [2] frontier buffer (0: fa, 1: fb)
 };
 
 __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::uint32_t* total) {
@@ -1051,7 +1062,7 @@ __device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, s
 // buffer, merged per lane; junctions store P(u) -- inline when it has <= 2 input
 // entries, else in pool space sized by the input length (single pass) -- and
 // release their parents.  1-saddles record their merged length.  All lanes call.
-__device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch, bool valid,
+__device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch, bool valid,
                                            std::uint32_t u, std::uint32_t* nxt, unsigned long long* next_cnt,
                                            unsigned long long& done) {
     const int lane = threadIdx.x & 31;
@@ -1073,7 +1084,7 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf& wb, Warp
         S = staged_size(in);
     }
     // heavy nodes -> the round's heavy queue
-    const bool heavy = valid && T > kHeavy && S + T <= kWarpCap;
+    const bool heavy = valid && T > kHeavy && S + T <= wb.cap;
     {
         const unsigned hm = __ballot_sync(0xffffffffu, heavy);
         if (hm) {
@@ -1112,18 +1123,18 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf& wb, Warp
         else store_rec(a.rec, u, len, 0u, r.k0, r.k1, r.c0, r.c1);
     };
     // inputs larger than the warp buffer: direct merge
-    if (valid && S > kWarpCap) {
+    if (valid && S > wb.cap) {
         const std::uint32_t len = junction ? merge<true>(in, a.pool, &ovf, emit)
                                            : merge<true>(in, a.pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
         finish(len);
     }
     // staged merges, in batches that fit the buffer
-    unsigned todo = __ballot_sync(0xffffffffu, valid && S <= kWarpCap);
+    unsigned todo = __ballot_sync(0xffffffffu, valid && S <= wb.cap);
     while (todo) {
         const bool mine = (todo >> lane) & 1u;
         std::uint32_t total = 0;
         const std::uint32_t base = warp_excl_scan(mine ? S : 0u, &total);
-        const bool go = mine && base + S <= kWarpCap;
+        const bool go = mine && base + S <= wb.cap;
         if (go) {
             if (junction) stage<true>(in, a.pool, wb, base);
             else stage<false>(in, a.pool, wb, base);
@@ -1145,7 +1156,7 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf& wb, Warp
 }
 
 // One heavy node, merged by the whole warp (all lanes call with the same u).
-__device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch, std::uint32_t u,
+__device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch, std::uint32_t u,
                                             std::uint32_t* nxt, unsigned long long* next_cnt,
                                             unsigned long long& done) {
     const int lane = threadIdx.x & 31;
@@ -1193,7 +1204,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf& wb, War
 }
 
 // The round's heavy queue, one warp per node (dynamic: warps take the next node).
-__device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf& wb, WarpQ& wq, PoolChunk& ch,
+__device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch,
                                            std::uint32_t* nxt, unsigned long long* next_cnt,
                                            unsigned long long& done) {
     const int lane = threadIdx.x & 31;
@@ -1208,9 +1219,15 @@ __device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf& wb, Warp
 }
 
 // Round 0: every node without pending children, in index order; then the frontiers.
-__global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
-    extern __shared__ WarpBuf s_wb[];
-    WarpBuf& wb = s_wb[threadIdx.x >> 5];
+// Two configurations of one kernel: kWide (high occupancy: 3 blocks/SM, 512-entry
+// warp buffers) runs the big early rounds, which are latency-bound and have no long
+// inputs; it stops once the frontier falls below a.switch_below and leaves the state
+// (round, frontier buffer, size) in a.resume.  The default configuration (2 blocks/SM,
+// 1024-entry buffers for the long vectors of the tail) resumes from there.
+template <bool kWide>
+__global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const WarpBuf wb = warp_buf(s_dyn, kWide ? kWarpCapWide : kWarpCap);
     __shared__ WarpQ s_q[kThreads / 32];
     __shared__ PoolChunk s_ch[kThreads / 32];
     WarpQ& wq = s_q[threadIdx.x >> 5];
@@ -1228,26 +1245,35 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     const int lane = threadIdx.x & 31;
     std::uint32_t* cur = a.fa;
     std::uint32_t* nxt = a.fb;
-    const std::uint64_t total = a.nj + a.n1;
-    if (grid.thread_rank() == 0) a.stats[1] = gtimer();
-    for (std::uint64_t base = wbase; base < total; base += stride) {
-        const std::uint64_t i = base + lane;
-        const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted
-        count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done);
-    }
-    grid.sync();
-    heavy_pass(a, wb, wq, ch, nxt, &a.cnt[1], done);
-    flush_block(s_q, nxt, &a.cnt[1]);
-    grid.sync();
-    if (grid.thread_rank() == 0) *a.heavy_n = *a.heavy_head = 0;
     int round = 1;
-    unsigned long long ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
-    {
+    unsigned long long ncur = 0;
+    if (kWide) {
+        const std::uint64_t total = a.nj + a.n1;
+        if (grid.thread_rank() == 0) a.stats[1] = gtimer();
+        for (std::uint64_t base = wbase; base < total; base += stride) {
+            const std::uint64_t i = base + lane;
+            const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted, kDone: walked
+            count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done);
+        }
+        grid.sync();
+        heavy_pass(a, wb, wq, ch, nxt, &a.cnt[1], done);
+        flush_block(s_q, nxt, &a.cnt[1]);
+        grid.sync();
+        if (grid.thread_rank() == 0) *a.heavy_n = *a.heavy_head = 0;
+        ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
         std::uint32_t* t = cur;
         cur = nxt;
         nxt = t;
+    } else {  // resume
+        round = static_cast<int>(a.resume[0]);
+        ncur = a.resume[1];
+        if (a.resume[2]) {
+            cur = a.fb;
+            nxt = a.fa;
+        }
     }
     while (ncur) {
+        if (kWide && ncur < a.switch_below) break;
         unsigned long long* next_cnt = &a.cnt[(round + 1) % 3];
         if (grid.thread_rank() == 0) {
             a.cnt[(round + 2) % 3] = 0;
@@ -1275,6 +1301,9 @@ __global__ void __launch_bounds__(kThreads) k_count(CountArgs a) {
     for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.done, done);
     if (grid.thread_rank() == 0) {
+        a.resume[0] = static_cast<unsigned long long>(round);
+        a.resume[1] = ncur;
+        a.resume[2] = cur == a.fb ? 1ull : 0ull;
         a.stats[0] = static_cast<unsigned long long>(round);
         if (round < kTimeline) a.stats[1 + round] = gtimer();
     }
@@ -1293,7 +1322,7 @@ __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n
         Inputs in;
         gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
         const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
-        if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {
+        if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {  // (heavy kernel: kWarpCap)
             heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
             continue;
         }
@@ -1315,8 +1344,8 @@ k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ 
                     std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt, std::uint32_t base_one,
                     std::uint32_t base_two, unsigned int* __restrict__ flags,
                     const std::uint32_t* __restrict__ heavy_q, const unsigned long long* __restrict__ heavy_n) {
-    extern __shared__ WarpBuf s_wb[];
-    WarpBuf& wb = s_wb[threadIdx.x >> 5];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const WarpBuf wb = warp_buf(s_dyn, kWarpCap);
     const int lane = threadIdx.x & 31;
     const unsigned long long n = *heavy_n;
     for (unsigned long long k = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5; k < n;
@@ -1512,16 +1541,24 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.heavy_n = L.heavy_n;
     a.heavy_head = L.heavy_n + 1;
     if (L.nj + L.n1 == 0) return MSC3D_OK;
-    const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);
-    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    a.switch_below = kSwitchBelow;
+    a.resume = L.resume;
+    // early rounds: the wide configuration; then the default one resumes
+    const std::size_t smem_w = warp_buf_bytes(kWarpCapWide) * (kThreads / 32);
+    const std::size_t smem_d = warp_buf_bytes(kWarpCap) * (kThreads / 32);
+    const void* kw = reinterpret_cast<const void*>(k_count<true>);
+    const void* kd = reinterpret_cast<const void*>(k_count<false>);
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w)));
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_d)));
     int grid = 0;
-    const int rc = coop_blocks(reinterpret_cast<const void*>(k_count), num_sms, &grid, smem);
+    int rc = coop_blocks(kw, num_sms, &grid, smem_w);
     if (rc != MSC3D_OK) return rc;
     void* args[] = {&a};
-    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_count), dim3(grid), dim3(kThreads),
-                                               args, smem, s));
-    count_launch();
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(kw, dim3(grid), dim3(kThreads), args, smem_w, s));
+    rc = coop_blocks(kd, num_sms, &grid, smem_d);
+    if (rc != MSC3D_OK) return rc;
+    MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(kd, dim3(grid), dim3(kThreads), args, smem_d, s));
+    count_launch(2);
     return MSC3D_OK;
 }
 
@@ -1535,7 +1572,7 @@ int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint
     k_count_write<<<grid_full(L.n1), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
                                                                  o_one, o_two, o_cnt, base_one, base_two, L.flags,
                                                                  L.heavy_q, L.heavy_n);
-    const std::size_t smem = sizeof(WarpBuf) * (kThreads / 32);
+    const std::size_t smem = warp_buf_bytes(kWarpCap) * (kThreads / 32);
     MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write_heavy),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_count_write_heavy<<<num_sms * 2, kThreads, smem, s>>>(snode, static_cast<const JRec*>(L.rec), pool, off, o_one,

@@ -197,6 +197,7 @@ struct CountLaunch {
     unsigned long long* diag;       // optional development diagnostics (nullptr: off)
     std::uint32_t* heavy_q;         // capacity nj + n1
     unsigned long long* heavy_n;    // 2 counters, zeroed
+    unsigned long long* resume;     // 3 words of state between the two configurations
 };
 int count_rec_bytes();
 int count_arenas();
