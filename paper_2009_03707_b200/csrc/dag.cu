@@ -763,7 +763,7 @@ __device__ __forceinline__ std::uint32_t merge(const Inputs& in, const PoolRef& 
 // copies its <= 4 inputs into its slice of a per-warp shared buffer with
 // independent 16-byte loads (all in flight at once), then merges from shared memory.
 constexpr int kWarpCap = 1024;  // entries per warp buffer (larger inputs: direct merge)
-constexpr int kWarpCapWide = 512;  // the high-occupancy configuration of the early rounds
+constexpr int kWarpCapWide = 384;  // the high-occupancy configuration of the early rounds
 constexpr unsigned long long kSwitchBelow = 1ull << 20;  // frontier size below which the tail configuration takes over
 constexpr std::uint32_t kHeavy = 48;  // total input length above which the whole warp merges the node
 
@@ -1225,7 +1225,7 @@ __device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf wb, WarpQ
 // (round, frontier buffer, size) in a.resume.  The default configuration (2 blocks/SM,
 // 1024-entry buffers for the long vectors of the tail) resumes from there.
 template <bool kWide>
-__global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) {
+__global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const WarpBuf wb = warp_buf(s_dyn, kWide ? kWarpCapWide : kWarpCap);
     __shared__ WarpQ s_q[kThreads / 32];
