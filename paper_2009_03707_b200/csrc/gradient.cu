@@ -29,6 +29,7 @@
 // byte stores).  The same kernel emits both extremum forests (build_forest,
 // extrema.cpp:43-77) and the per-dimension critical counts.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -277,10 +278,16 @@ __device__ __forceinline__ void ce_pair(KT& ka, std::uint32_t& sa, KT& kb, std::
 
 // Fast path for one star with n <= K vertices and distinct values.  Returns false
 // (nothing written) when two star values tie.
+// Rank masks of a K-vertex star fit K bits: the per-thread scratch column uses the
+// narrowest type (a smaller shared-memory footprint -> more resident blocks).
+template <int K>
+using MaskT = typename std::conditional<(K <= 8), std::uint8_t,
+                                        typename std::conditional<(K <= 16), std::uint16_t, std::uint32_t>::type>::type;
+
 template <int K, typename T, typename Val>
 __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
                                           const std::uint32_t* fac, const std::uint32_t* cof,
-                                          std::uint32_t* mscratch, int mstride, StarWriter& w) {
+                                          MaskT<K>* mscratch, int mstride, StarWriter& w) {
     using KT = typename KeyOf<T>::type;
     KT key[K];
     std::uint32_t slot[K];
@@ -322,7 +329,7 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
 #pragma unroll
     for (int t = 0; t < 27; ++t) M[t] = 0;
     M[13] = 1u << (n - 1);
-    mscratch[13 * mstride] = M[13];
+    mscratch[13 * mstride] = static_cast<MaskT<K>>(M[13]);
 #pragma unroll
     for (int dim = 1; dim <= 3; ++dim)
 #pragma unroll
@@ -336,7 +343,7 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
             }
             if ((S >> t) & 1u) {
                 m |= 1u << rank.get(t);
-                mscratch[t * mstride] = m;
+                mscratch[t * mstride] = static_cast<MaskT<K>>(m);
             }
             M[t] = m;
         }
@@ -385,7 +392,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
     __shared__ unsigned long long s_crit[4];
-    __shared__ std::uint32_t s_M[27 * NT];
+    __shared__ MaskT<8> s_M[27 * NT];
     __shared__ std::uint32_t s_lb[2][kListBuf];
     __shared__ std::uint32_t s_lm[2][kListBuf];
     __shared__ std::uint32_t s_ln[2];
@@ -580,7 +587,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
                 unsigned long long* __restrict__ crit_totals, StarLists lists, int which) {
     __shared__ std::int32_t s_cell[27];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
-    __shared__ std::uint32_t s_M[27 * 128];
+    __shared__ MaskT<K> s_M[27 * 128];
     __shared__ unsigned long long s_crit[4];
     if (threadIdx.x < 27) {
         s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
