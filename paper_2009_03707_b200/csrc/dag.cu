@@ -400,8 +400,8 @@ constexpr std::uint32_t kSkip = 0xffffffffu;  // pending0 of a contracted pass-t
 
 struct alignas(16) NodeRec {
     std::uint32_t dest[4];
-    std::uint32_t npar;
-    std::uint32_t ov_lo, ov_hi;  // overflow list offset
+    std::uint32_t npar;          // (unused: the count comes from the rewrite's slot counters)
+    std::uint32_t ov_lo, ov_hi;  // (unused: overflow offsets are read from the scan's output)
     std::uint32_t par[kInlineParents];
 };
 static_assert(sizeof(NodeRec) == 64, "NodeRec is one 64-byte line");
@@ -586,37 +586,6 @@ __global__ void k_parent_overflow(const std::uint32_t* __restrict__ indeg, std::
          j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         const std::uint32_t k = indeg[j];
         ovcnt[j] = k > static_cast<std::uint32_t>(kInlineParents) ? k - kInlineParents : 0u;
-    }
-}
-
-// Parent counts and overflow offsets into the node records; the inline parents are
-// sorted ascending (the atomics that placed them ran in arbitrary order), so each
-// round's frontier, appended in release order, keeps some spatial order -- the
-// later, latency-bound rounds are measurably faster with it.
-__global__ void k_node_meta(NodeRec* __restrict__ node, std::uint64_t nj, const std::uint32_t* __restrict__ indeg,
-                            const std::uint64_t* __restrict__ ovoff) {
-    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
-         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const std::uint64_t o = ovoff[j];
-        const std::uint32_t k = indeg[j];
-        uint4* r = reinterpret_cast<uint4*>(node + j);
-        uint4 m = r[1], p0 = r[2], p1 = r[3];
-        std::uint32_t q[kInlineParents] = {m.w, p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-        const std::uint32_t n = k < static_cast<std::uint32_t>(kInlineParents) ? k : kInlineParents;
-        if (n > 1) {
-#pragma unroll
-            for (int a = 0; a < kInlineParents; ++a)
-#pragma unroll
-                for (int b = 0; b + 1 < kInlineParents - a; ++b) {
-                    const bool in = static_cast<std::uint32_t>(b + 1) < n;
-                    const std::uint32_t lo = min(q[b], q[b + 1]), hi = max(q[b], q[b + 1]);
-                    q[b] = in ? lo : q[b];
-                    q[b + 1] = in ? hi : q[b + 1];
-                }
-        }
-        r[1] = make_uint4(k, static_cast<std::uint32_t>(o), static_cast<std::uint32_t>(o >> 32), q[0]);
-        r[2] = make_uint4(q[1], q[2], q[3], q[4]);
-        r[3] = make_uint4(q[5], q[6], q[7], q[8]);
     }
 }
 
@@ -1001,6 +970,8 @@ struct CountArgs {
     std::uint32_t* heavy_q;    // the round's heavy nodes
     unsigned long long* heavy_n;
     unsigned long long* heavy_head;
+    const std::uint32_t* indeg;       // parents per junction (the rewrite's slot counters)
+    const std::uint64_t* ovoff;       // their overflow-list offsets (in-degree > kInlineParents)
     unsigned long long switch_below;  // wide configuration: stop below this frontier size
     unsigned long long* resume;       // [0] round [1] frontier size [2] frontier buffer (0: fa, 1: fb)
 };
@@ -1021,10 +992,9 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
 // the grid barrier): the first kInlineParents come with the node record, the rest
 // from the overflow list; parents reaching zero pending children are appended to
 // the next frontier.  All lanes call (rn = 0 for lanes without a junction).
-__device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, std::uint32_t rn, const uint4 meta,
-                                                const uint4 par0, const uint4 par1, std::uint32_t* nxt,
-                                                unsigned long long* next_cnt) {
-    const std::uint64_t ov = static_cast<std::uint64_t>(meta.y) | (static_cast<std::uint64_t>(meta.z) << 32);
+__device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, std::uint32_t rn, std::uint64_t ov,
+                                                const uint4 meta, const uint4 par0, const uint4 par1,
+                                                std::uint32_t* nxt, unsigned long long* next_cnt) {
     const std::uint32_t inl[kInlineParents] = {meta.w, par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
     std::uint32_t k0 = 0;  // parents handled so far
     for (;;) {
@@ -1073,9 +1043,11 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
     for (int b = 0; b < 4; ++b) in.len[b] = 0;
     std::uint32_t S = 0;  // staged size (lists padded to multiples of 4)
     uint4 meta = make_uint4(0u, 0u, 0u, 0u), par0 = meta, par1 = meta;
+    std::uint32_t npar = 0;  // parents: their count from the rewrite's slot counters
     if (valid) {
         const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
         const uint4 d4 = nr[0];
+        if (u < a.nj) npar = a.indeg[u];
         meta = nr[1];
         par0 = nr[2];
         par1 = nr[3];
@@ -1152,7 +1124,9 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
     }
     if (junction) ++done;
     if (ovf) a.flags[0] = 1u;
-    release_parents(a, wq, junction ? meta.x : 0u, meta, par0, par1, nxt, next_cnt);
+    const std::uint32_t rn = junction ? npar : 0u;
+    release_parents(a, wq, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, meta, par0, par1,
+                    nxt, next_cnt);
 }
 
 // One heavy node, merged by the whole warp (all lanes call with the same u).
@@ -1200,7 +1174,9 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
         if (junction) ++done;
     }
     __syncwarp();
-    release_parents(a, wq, lane == 0 && junction ? meta.x : 0u, meta, par0, par1, nxt, next_cnt);
+    const std::uint32_t rn = lane == 0 && junction ? a.indeg[u] : 0u;
+    release_parents(a, wq, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, meta, par0, par1,
+                    nxt, next_cnt);
 }
 
 // The round's heavy queue, one warp per node (dynamic: warps take the next node).
@@ -1503,10 +1479,9 @@ int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::ui
 int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg, const std::uint64_t* ovoff,
                         const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms) {
     auto* nr = static_cast<NodeRec*>(node);
-    if (nj) {
-        k_node_meta<<<grid_full(nj), kThreads, 0, s>>>(nr, nj, indeg, ovoff);
-        count_launch();
-    }
+    (void)nr;
+    (void)nj;
+    (void)indeg;  // parent counts are read from the rewrite's slot counters directly
     if (n_ovq) {
         k_fill_overflow<<<grid_for(n_ovq, num_sms), kThreads, 0, s>>>(static_cast<const uint4*>(ovq), n_ovq, ovoff,
                                                                        rsrc);
@@ -1542,6 +1517,8 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.heavy_head = L.heavy_n + 1;
     if (L.nj + L.n1 == 0) return MSC3D_OK;
     a.switch_below = kSwitchBelow;
+    a.indeg = L.indeg;
+    a.ovoff = L.ovoff;
     a.resume = L.resume;
     // early rounds: the wide configuration; then the default one resumes
     const std::size_t smem_w = warp_buf_bytes(kWarpCapWide) * (kThreads / 32);

@@ -198,6 +198,8 @@ struct CountLaunch {
     std::uint32_t* heavy_q;         // capacity nj + n1
     unsigned long long* heavy_n;    // 2 counters, zeroed
     unsigned long long* resume;     // 3 words of state between the two configurations
+    const std::uint32_t* indeg;     // parents per junction
+    const std::uint64_t* ovoff;     // overflow-list offsets
 };
 int count_rec_bytes();
 int count_arenas();
