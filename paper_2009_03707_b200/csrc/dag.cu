@@ -565,6 +565,7 @@ __global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uin
             dd[b] = t;
             if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
             ++waiting;
+            if (i >= nj) continue;  // 1-saddles wait for no release: their lengths come after the rounds
             const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
             if (slot < static_cast<std::uint32_t>(kInlineParents)) {
                 node[t].par[slot] = static_cast<std::uint32_t>(i);
@@ -1224,7 +1225,7 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
     int round = 1;
     unsigned long long ncur = 0;
     if (kWide) {
-        const std::uint64_t total = a.nj + a.n1;
+        const std::uint64_t total = a.nj;  // 1-saddles: after the rounds (launch_source_len)
         if (grid.thread_rank() == 0) a.stats[1] = gtimer();
         for (std::uint64_t base = wbase; base < total; base += stride) {
             const std::uint64_t i = base + lane;
@@ -1288,13 +1289,20 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
 // The sorted (1-saddle, 2-saddle, count) output.  Light 1-saddles are merged per
 // thread; heavy ones (> kHeavy input entries) are queued for k_count_write_heavy,
 // one warp per 1-saddle, like the heavy junctions of k_count.
+//
+// kLen: the same pass computing only the merged lengths (slen) of the 1-saddles the
+// walk did not finish (pending kDone) -- 1-saddles take no part in Kahn's rounds:
+// nothing waits for them, so their lengths are one coalesced pass after the junctions.
+template <bool kLen>
 __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
                               PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
                               std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
                               std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
-                              std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n) {
+                              std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n,
+                              const std::uint32_t* __restrict__ spending, std::uint32_t* __restrict__ slen) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        if (kLen && spending[i] == kDone) continue;
         Inputs in;
         gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
         const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
@@ -1302,8 +1310,12 @@ __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n
             heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
             continue;
         }
-        const std::uint64_t at = off[i];
         bool ovf = false;
+        if (kLen) {
+            slen[i] = merge<false>(in, pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
+            continue;
+        }
+        const std::uint64_t at = off[i];
         const std::uint32_t one = base_one + static_cast<std::uint32_t>(i);
         merge<false>(in, pool, &ovf, [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
             o_one[at + o] = one;
@@ -1314,12 +1326,14 @@ __global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n
     }
 }
 
+template <bool kLen>
 __global__ void __launch_bounds__(kThreads)
 k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ rec, PoolRef pool,
                     const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
                     std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt, std::uint32_t base_one,
                     std::uint32_t base_two, unsigned int* __restrict__ flags,
-                    const std::uint32_t* __restrict__ heavy_q, const unsigned long long* __restrict__ heavy_n) {
+                    const std::uint32_t* __restrict__ heavy_q, const unsigned long long* __restrict__ heavy_n,
+                    std::uint32_t* __restrict__ slen) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const WarpBuf wb = warp_buf(s_dyn, kWarpCap);
     const int lane = threadIdx.x & 31;
@@ -1350,8 +1364,14 @@ k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ 
         }
         cp_async_wait_all();
         __syncwarp();
-        const std::uint64_t o = off[i];
         bool ovf = false;
+        if (kLen) {
+            const std::uint32_t L = merge_heavy(h, wb, nullptr, nullptr, &ovf);
+            if (lane == 0) slen[i] = L;
+            __syncwarp();
+            continue;
+        }
+        const std::uint64_t o = off[i];
         const std::uint32_t L = merge_heavy(h, wb, o_two + o, o_cnt + o, &ovf);
         for (std::uint32_t t = lane; t < L; t += 32) {
             o_one[o + t] = base_one + i;
@@ -1539,25 +1559,38 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     return MSC3D_OK;
 }
 
-int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
-                       std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
-                       int num_sms) {
+namespace {
+template <bool kLen>
+int count_write_impl(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
+                     std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
+                     int num_sms) {
     if (L.n1 == 0) return MSC3D_OK;
     const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
     const PoolRef pool{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
     MSC3D_CUDA_TRY(cudaMemsetAsync(L.heavy_n, 0, 8, s));
-    k_count_write<<<grid_full(L.n1), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
-                                                                 o_one, o_two, o_cnt, base_one, base_two, L.flags,
-                                                                 L.heavy_q, L.heavy_n);
+    k_count_write<kLen><<<grid_full(L.n1), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
+                                                             o_one, o_two, o_cnt, base_one, base_two, L.flags,
+                                                             L.heavy_q, L.heavy_n, L.pending0 + L.nj, L.slen);
     const std::size_t smem = warp_buf_bytes(kWarpCap) * (kThreads / 32);
-    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write_heavy),
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write_heavy<kLen>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k_count_write_heavy<<<num_sms * 2, kThreads, smem, s>>>(snode, static_cast<const JRec*>(L.rec), pool, off, o_one,
-                                                            o_two, o_cnt, base_one, base_two, L.flags, L.heavy_q,
-                                                            L.heavy_n);
+    k_count_write_heavy<kLen><<<num_sms * 2, kThreads, smem, s>>>(snode, static_cast<const JRec*>(L.rec), pool, off,
+                                                                  o_one, o_two, o_cnt, base_one, base_two, L.flags,
+                                                                  L.heavy_q, L.heavy_n, L.slen);
     count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
+}
+}  // namespace
+
+int launch_source_len(const CountLaunch& L, cudaStream_t s, int num_sms) {
+    return count_write_impl<true>(L, nullptr, nullptr, nullptr, nullptr, 0, 0, s, num_sms);
+}
+
+int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
+                       std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
+                       int num_sms) {
+    return count_write_impl<false>(L, off, o_one, o_two, o_cnt, base_one, base_two, s, num_sms);
 }
 
 }  // namespace msc3d_dev

@@ -231,6 +231,8 @@ int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::ui
 int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg, const std::uint64_t* ovoff,
                         const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
 int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms);
+// merged lengths of the 1-saddles the walk did not finish (after k_count) -> L.slen
+int launch_source_len(const CountLaunch& L, cudaStream_t s, int num_sms);
 int launch_count_write(const CountLaunch& L, const std::uint64_t* off, std::uint32_t* o_one, std::uint32_t* o_two,
                        std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
                        int num_sms);

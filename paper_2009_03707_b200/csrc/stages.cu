@@ -449,7 +449,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         ctx->scalars["pool_entries"] = static_cast<std::int64_t>(used);
     }
 
-    // 1-saddles: offsets, sorted output
+    // 1-saddles: merged lengths (those the walk did not finish), offsets, sorted output
+    TRY(msc3d_dev::launch_source_len(L, s, sms));
     TRY(msc3d_dev::scan_u32(slen, n1, soff, ctx->d_small, ctx->ws, s));
     TRY(ctx->fetch_small(27));
     if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
