@@ -378,17 +378,20 @@ struct StarLists {
 // Block-level buffers for the large-star work lists: appends are shared-memory
 // atomics; the global list counters are touched once per flush (a counter hit by
 // every thread of the grid serialises in the L2).
-constexpr int kListBuf = 512;
+constexpr int kListBuf = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(NT, 5)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
            unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first) {
-    // f32: two tile buffers, the next tile streams in (cp.async) while this one is
-    // processed; f64: one (static shared memory budget)
-    constexpr int kBufs = sizeof(T) == 4 ? 2 : 1;
-    __shared__ T tiles_sm[kBufs][SZ][SY][SX];
+    // Tiles go in groups of kGroup (consecutive along x): phase 1 bins the group's
+    // 3..8-cell stars by size, phase 2 runs them all -- ~2x the work per barrier, so
+    // fewer idle lanes.  f32: two buffer sets, the next group streams in (cp.async)
+    // while this one is processed; f64: one set (static shared memory budget).
+    constexpr int kGroup = 2;
+    constexpr int kSets = sizeof(T) == 4 ? 2 : 1;
+    __shared__ T tiles_sm[kSets][kGroup][SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
     __shared__ unsigned long long s_crit[4];
@@ -398,8 +401,8 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ std::uint32_t s_ln[2];
     __shared__ unsigned long long s_base[2];
     __shared__ std::uint32_t s_wn[6], s_wtotal;  // phase-2 work list: buckets of star size 3..8
-    __shared__ std::uint32_t s_wS[NT];
-    __shared__ std::uint8_t s_wid[NT];
+    __shared__ std::uint32_t s_wS[kGroup * NT];
+    __shared__ std::uint16_t s_wid[kGroup * NT];  // tile-in-group << 8 | vertex in tile
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
     if (tid < 27) {
         s_fac[tid] = c_slot.facet[tid];
@@ -425,47 +428,54 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     };
     std::uint32_t crit[4] = {0, 0, 0, 0};
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
+    const std::uint64_t ngroups = (ntiles + kGroup - 1) / kGroup;
     auto origin = [&](std::uint64_t ti, std::int64_t& x0, std::int64_t& y0, std::int64_t& z0) {
         const std::uint64_t tyz = ti / tiles.x;
         x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
         y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
         z0 = static_cast<std::int64_t>(tyz / tiles.y + tz_first) * TZ - 1;
     };
-    // tile ti (+1 halo) -> buffer b: in-range samples by asynchronous copies, the rest 0
-    auto load_tile = [&](std::uint64_t ti, int b) {
-        std::int64_t x0, y0, z0;
-        origin(ti, x0, y0, z0);
-        T* dst = &tiles_sm[b][0][0][0];
-        for (int i = tid; i < SX * SY * SZ; i += NT) {
-            const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
-            const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-            if (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz) {
-                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
-                const T* src = f + gx + d.nx * (gy + d.ny * gz);
-                if (sizeof(T) == 4)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
-                else
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
-            } else {
-                dst[i] = T(0);
+    // group gi's tiles (+1 halo) -> buffer set b: in-range samples by asynchronous
+    // copies, the rest (and tiles past the end) 0
+    auto load_group = [&](std::uint64_t gi, int b) {
+        for (int g = 0; g < kGroup; ++g) {
+            const std::uint64_t ti = gi * kGroup + g;
+            std::int64_t x0, y0, z0;
+            origin(ti, x0, y0, z0);
+            T* dst = &tiles_sm[b][g][0][0][0];
+            for (int i = tid; i < SX * SY * SZ; i += NT) {
+                const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
+                const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+                if (ti < ntiles && gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 && gz < d.nz) {
+                    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+                    const T* src = f + gx + d.nx * (gy + d.ny * gz);
+                    if (sizeof(T) == 4)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+                } else {
+                    dst[i] = T(0);
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (blockIdx.x < ntiles) load_tile(blockIdx.x, 0);
+    if (blockIdx.x < ngroups) load_group(blockIdx.x, 0);
     int cur = 0;
-    for (std::uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        std::int64_t x0, y0, z0;
-        origin(ti, x0, y0, z0);
+    for (std::uint64_t gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
         asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();  // tile ti in shared memory; the previous tile's work done
-        if (s_ln[0] + NT > kListBuf || s_ln[1] + NT > kListBuf) flush_lists();
-        const std::uint64_t tn = ti + gridDim.x;
-        if (kBufs == 2 && tn < ntiles) load_tile(tn, cur ^ 1);  // overlaps this tile's work
-        auto& tile = tiles_sm[cur];
-        if (kBufs == 2) cur ^= 1;
+        __syncthreads();  // group gi in shared memory; the previous group's work done
+        if (s_ln[0] + kGroup * NT > kListBuf || s_ln[1] + kGroup * NT > kListBuf) flush_lists();
+        const std::uint64_t gn = gi + gridDim.x;
+        if (kSets == 2 && gn < ngroups) load_group(gn, cur ^ 1);  // overlaps this group's work
+        const int set = cur;
+        if (kSets == 2) cur ^= 1;
 
-        auto writer_for = [&](int lid, StarWriter& w) {  // false: vertex outside the grid
+        auto writer_for = [&](int g, int lid, StarWriter& w) {  // false: vertex outside the grid
+            const std::uint64_t ti = gi * kGroup + g;
+            if (ti >= ntiles) return false;
+            std::int64_t x0, y0, z0;
+            origin(ti, x0, y0, z0);
             const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
             w.vx = x0 + 1 + lx;
             w.vy = y0 + 1 + ly;
@@ -487,18 +497,19 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             w.ncrit = 0;
             return true;
         };
-        // ---- phase 1, own vertex: star mask; trivial stars finished here; stars of
-        //      3..8 cells bucketed by size into the block's work list (so that phase 2
-        //      runs them densely and size-homogeneously: no idle lanes, even loops);
-        //      larger stars go to the size-specialised list kernels
+        // ---- phase 1, own vertex of each tile: star mask; trivial stars finished here;
+        //      stars of 3..8 cells binned by size; larger stars to the list kernels
         if (tid < 6) s_wn[tid] = 0;
         __syncthreads();
-        int n = 0;
-        std::uint32_t S = 0;
-        {
+        int ng[kGroup];
+        std::uint32_t Sg[kGroup];
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+            ng[g] = 0;
+            Sg[g] = 0;
             StarWriter w;
-            if (writer_for(tid, w)) {
-                const T* base = &tile[threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + 1];
+            if (writer_for(g, tid, w)) {
+                const T* base = &tiles_sm[set][g][threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + 1];
                 const T fv = base[0];
                 std::uint32_t below = kCentre;
 #pragma unroll
@@ -507,10 +518,10 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                     const T u = base[slot_tile(t)];
                     if (u < fv || (u == fv && t < 13)) below |= 1u << t;
                 }
-                S = below & w.inr;
+                std::uint32_t S = below & w.inr;
                 S &= facets_present(S);
                 S &= facets_present(S);
-                n = __popc(S);
+                const int n = __popc(S);
                 if (n == 1) {  // critical minimum (gradient.cpp:128-131)
                     w.minimum();
                 } else if (n == 2) {  // the vertex and its only edge pair up
@@ -522,6 +533,8 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                     s_lm[which][at] = S;
                 } else {
                     atomicAdd(&s_wn[n - 3], 1u);
+                    ng[g] = n;
+                    Sg[g] = S;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
@@ -538,30 +551,32 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             s_wtotal = acc;
         }
         __syncthreads();
-        if (n >= 3 && n <= 8) {
-            const std::uint32_t at = atomicAdd(&s_wn[n - 3], 1u);
-            s_wS[at] = S;
-            s_wid[at] = static_cast<std::uint8_t>(tid);
-        }
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g)
+            if (ng[g] >= 3) {
+                const std::uint32_t at = atomicAdd(&s_wn[ng[g] - 3], 1u);
+                s_wS[at] = Sg[g];
+                s_wid[at] = static_cast<std::uint16_t>((g << 8) | tid);
+            }
         __syncthreads();
-        // ---- phase 2: the bucketed stars, one per thread, register fast path
-        if (static_cast<std::uint32_t>(tid) < s_wtotal) {
-            const int lid = s_wid[tid];
-            const std::uint32_t Sw = s_wS[tid];
+        // ---- phase 2: the binned stars, one per thread, register fast path
+        for (std::uint32_t k = tid; k < s_wtotal; k += NT) {
+            const int g = s_wid[k] >> 8, lid = s_wid[k] & 0xff;
+            const std::uint32_t Sw = s_wS[k];
             StarWriter w;
-            writer_for(lid, w);
-            const T* base = &tile[lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + 1];
+            writer_for(g, lid, w);
+            const T* base = &tiles_sm[set][g][lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + 1];
             if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, Sw, __popc(Sw), s_fac, s_cof, &s_M[tid], NT,
                                  w)) {
                 const unsigned long long at = atomicAdd(&lists.count[2], 1ull);  // ties: rare
                 lists.list[2][at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) crit[k] += static_cast<std::uint32_t>((w.ncrit >> (16 * k)) & 0xffffu);
+            for (int q = 0; q < 4; ++q) crit[q] += static_cast<std::uint32_t>((w.ncrit >> (16 * q)) & 0xffffu);
         }
-        if (kBufs == 1 && tn < ntiles) {
-            __syncthreads();  // everyone done with the single buffer
-            load_tile(tn, 0);
+        if (kSets == 1 && gn < ngroups) {
+            __syncthreads();  // everyone done with the single buffer set
+            load_group(gn, 0);
         }
     }
     flush_lists();
