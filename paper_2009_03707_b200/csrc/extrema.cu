@@ -90,35 +90,53 @@ __global__ void k_double(const std::uint32_t* __restrict__ in, std::uint32_t* __
 
 // Both forests' roots in one cooperative launch: rounds of in-place jumping over the
 // concatenated index space of parent0 and parent3, a grid barrier per round and a
-// rotating "changed" flag -- no host round trip per round.  flags[0..2] zeroed by the
+// rotating "changed" flag -- no host round trip per round.  conv: one bit per item,
+// set once the item points at a root (final: roots never move); rounds after the
+// first read the bitmap word of 32 items (L2-resident) and skip converged items
+// instead of re-reading their parents' random lines.  flags[0..2] zeroed by the
 // caller; rounds_out[0] = rounds run.
 __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std::uint32_t* __restrict__ p3,
-                           std::uint64_t n3, unsigned int* flags, unsigned long long* rounds_out) {
+                           std::uint64_t n3, unsigned int* __restrict__ conv, unsigned int* flags,
+                           unsigned long long* rounds_out) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     const std::uint64_t n = n0 + n3;
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    const std::uint64_t wstart = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+    const unsigned lane = threadIdx.x & 31u;
     int round = 0;
     for (;; ++round) {
         if (grid.thread_rank() == 0) flags[(round + 1) % 3] = 0u;
         bool any = false;
-        for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) {
-            std::uint32_t* p = k < n0 ? p0 : p3;
-            const std::uint64_t i = k < n0 ? k : k - n0;
-            std::uint32_t l = p[i];
-            std::uint32_t nl = p[l];
-            if (nl != l) {
+        for (std::uint64_t base = wstart; base < n; base += stride) {
+            const std::uint64_t k = base + lane;
+            const unsigned word = round ? conv[base >> 5] : 0u;
+            bool now = false;
+            if (k < n && !((word >> lane) & 1u)) {
+                std::uint32_t* p = k < n0 ? p0 : p3;
+                const std::uint64_t i = k < n0 ? k : k - n0;
+                const std::uint32_t l = p[i];
+                std::uint32_t nl = p[l];
+                if (nl != l) {
 #pragma unroll
-                for (int s = 0; s < 3; ++s) {
-                    const std::uint32_t nn = p[nl];
-                    if (nn == nl) break;
-                    nl = nn;
+                    for (int s = 0; s < 3; ++s) {
+                        const std::uint32_t nn = p[nl];
+                        if (nn == nl) {
+                            now = true;
+                            break;
+                        }
+                        nl = nn;
+                    }
+                    p[i] = nl;
+                    any = true;
+                } else {
+                    now = true;
                 }
-                p[i] = nl;
-                any = true;
             }
+            const unsigned bits = __ballot_sync(0xffffffffu, now);
+            if (lane == 0 && (bits || !round)) conv[base >> 5] = word | bits;
         }
-        if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(&flags[round % 3], 1u);
+        if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&flags[round % 3], 1u);
         grid.sync();
         if (*reinterpret_cast<volatile unsigned int*>(&flags[round % 3]) == 0u) break;
         if (round > 64) break;  // a cycle (invalid gradient): reported by the caller
@@ -257,15 +275,15 @@ int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64
     return MSC3D_OK;
 }
 
-int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* flags,
-                    unsigned long long* rounds, cudaStream_t s, int num_sms) {
+int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* conv,
+                    unsigned int* flags, unsigned long long* rounds, cudaStream_t s, int num_sms) {
     if (n0 + n3 == 0) return MSC3D_OK;
     int per_sm = 0;
     MSC3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_all, kThreads, 0));
     if (per_sm <= 0) return MSC3D_ERR_CUDA;
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
         static_cast<std::uint64_t>(per_sm) * num_sms, std::max<std::uint64_t>(1, (n0 + n3 + kThreads - 1) / kThreads)));
-    void* args[] = {&p0, &n0, &p3, &n3, &flags, &rounds};
+    void* args[] = {&p0, &n0, &p3, &n3, &conv, &flags, &rounds};
     MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_jump_all), dim3(grid), dim3(kThreads),
                                                args, 0, s));
     count_launch();

@@ -89,8 +89,10 @@ int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64
                         unsigned int* changed, cudaStream_t s, int num_sms);
 int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, cudaStream_t s,
                       int num_sms);
-// roots of both extremum forests in place, all rounds in one cooperative launch
-int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* flags,
+// roots of both extremum forests in place, all rounds in one cooperative launch;
+// conv: (n0 + n3 + 31) / 32 words of scratch
+int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* conv,
+                    unsigned int* flags,
                     unsigned long long* rounds, cudaStream_t s, int num_sms);
 int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
                          std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms);

@@ -352,7 +352,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         auto* jflags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);
         auto* jrounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 23, 0, 24, s));
-        TRY(msc3d_dev::launch_jump_all(fwd, nj, nullptr, 0, jflags, jrounds, s, sms));
+        auto* conv = static_cast<unsigned int*>(ctx->ensure("jump_conv_pt", nj / 32 + 1, 4));
+        if (!conv) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_jump_all(fwd, nj, nullptr, 0, conv, jflags, jrounds, s, sms));
     }
     if (nj) MSC3D_CUDA_TRY(cudaMemsetAsync(indeg, 0, nj * 4, s));
     auto* n_skip = reinterpret_cast<unsigned long long*>(ctx->d_small + 19);
@@ -617,8 +619,12 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         auto* flags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);  // 3 x u32 (slots 23-24)
         auto* rounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 23, 0, 16, s));
+        auto* conv = static_cast<unsigned int*>(
+            ctx->ensure("jump_conv", (ctx->count("parent0") + ctx->count("parent3")) / 32 + 1, 4));
+        if (!conv) return MSC3D_ERR_NOMEM;
         TRY(msc3d_dev::launch_jump_all(ctx->ptr<std::uint32_t>("parent0"), ctx->count("parent0"),
-                                       ctx->ptr<std::uint32_t>("parent3"), ctx->count("parent3"), flags, rounds, s, sms));
+                                       ctx->ptr<std::uint32_t>("parent3"), ctx->count("parent3"), conv, flags, rounds,
+                                       s, sms));
     }
     auto* label0 = ctx->ptr<std::uint32_t>("parent0");
     auto* label3 = ctx->ptr<std::uint32_t>("parent3");
