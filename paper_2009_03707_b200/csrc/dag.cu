@@ -1035,7 +1035,7 @@ __device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, s
 // release their parents.  1-saddles record their merged length.  All lanes call.
 __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch, bool valid,
                                            std::uint32_t u, std::uint32_t* nxt, unsigned long long* next_cnt,
-                                           unsigned long long& done) {
+                                           unsigned long long& done, unsigned long long* hn) {
     const int lane = threadIdx.x & 31;
     Inputs in;
     bool ovf = false;
@@ -1062,7 +1062,7 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
         const unsigned hm = __ballot_sync(0xffffffffu, heavy);
         if (hm) {
             unsigned long long hb = 0;
-            if (lane == 0) hb = atomicAdd(a.heavy_n, static_cast<unsigned long long>(__popc(hm)));
+            if (lane == 0) hb = atomicAdd(hn, static_cast<unsigned long long>(__popc(hm)));
             hb = __shfl_sync(0xffffffffu, hb, 0);
             if (heavy) a.heavy_q[hb + __popc(hm & ((1u << lane) - 1u))] = u;
         }
@@ -1183,12 +1183,11 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
 // The round's heavy queue, one warp per node (dynamic: warps take the next node).
 __device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch,
                                            std::uint32_t* nxt, unsigned long long* next_cnt,
-                                           unsigned long long& done) {
+                                           unsigned long long& done, unsigned long long n, unsigned long long* head) {
     const int lane = threadIdx.x & 31;
-    const unsigned long long n = *reinterpret_cast<volatile unsigned long long*>(a.heavy_n);
     for (;;) {
         unsigned long long k = 0;
-        if (lane == 0) k = atomicAdd(a.heavy_head, 1ull);
+        if (lane == 0) k = atomicAdd(head, 1ull);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= n) break;
         count_heavy(a, wb, wq, ch, __ldcg(a.heavy_q + k), nxt, next_cnt, done);
@@ -1224,19 +1223,28 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
     std::uint32_t* nxt = a.fb;
     int round = 1;
     unsigned long long ncur = 0;
+    // Round r's heavy queue counters are slot r % 3 (zeroed by the host, then by
+    // round r - 1 for round r + 1... i.e. each round zeroes the slot of the next one).
+    // A round without heavy nodes ends at its first grid barrier.
+    auto finish_round = [&](int r, unsigned long long* next_cnt) {
+        flush_block(s_q, nxt, next_cnt);
+        grid.sync();
+        const unsigned long long nh = *reinterpret_cast<volatile unsigned long long*>(&a.heavy_n[r % 3]);
+        if (nh) {
+            heavy_pass(a, wb, wq, ch, nxt, next_cnt, done, nh, &a.heavy_head[r % 3]);
+            flush_block(s_q, nxt, next_cnt);
+            grid.sync();
+        }
+    };
     if (kWide) {
         const std::uint64_t total = a.nj;  // 1-saddles: after the rounds (launch_source_len)
         if (grid.thread_rank() == 0) a.stats[1] = gtimer();
         for (std::uint64_t base = wbase; base < total; base += stride) {
             const std::uint64_t i = base + lane;
             const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted, kDone: walked
-            count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done);
+            count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, &a.heavy_n[0]);
         }
-        grid.sync();
-        heavy_pass(a, wb, wq, ch, nxt, &a.cnt[1], done);
-        flush_block(s_q, nxt, &a.cnt[1]);
-        grid.sync();
-        if (grid.thread_rank() == 0) *a.heavy_n = *a.heavy_head = 0;
+        finish_round(0, &a.cnt[1]);
         ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
         std::uint32_t* t = cur;
         cur = nxt;
@@ -1254,21 +1262,18 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
         unsigned long long* next_cnt = &a.cnt[(round + 1) % 3];
         if (grid.thread_rank() == 0) {
             a.cnt[(round + 2) % 3] = 0;
+            a.heavy_n[(round + 1) % 3] = 0;
+            a.heavy_head[(round + 1) % 3] = 0;
             if (round < kTimeline) a.stats[1 + round] = gtimer();
         }
         for (std::uint64_t base = wbase; base < ncur; base += stride) {
             const std::uint64_t f = base + lane;
             const bool valid = f < ncur;
-            count_iter(a, wb, wq, ch, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done);
+            count_iter(a, wb, wq, ch, valid, valid ? __ldcg(cur + f) : 0u, nxt, next_cnt, done,
+                       &a.heavy_n[round % 3]);
         }
-        grid.sync();
-        heavy_pass(a, wb, wq, ch, nxt, next_cnt, done);
-        flush_block(s_q, nxt, next_cnt);
-        grid.sync();
-        if (grid.thread_rank() == 0) {
-            *a.heavy_n = *a.heavy_head = 0;
-            if (a.diag && round < kTimeline) a.diag[6 + 3 * round] = ncur;
-        }
+        finish_round(round, next_cnt);
+        if (grid.thread_rank() == 0 && a.diag && round < kTimeline) a.diag[6 + 3 * round] = ncur;
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
         ++round;
         std::uint32_t* t = cur;
@@ -1533,8 +1538,8 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.flags = L.flags;
     a.diag = L.diag;
     a.heavy_q = L.heavy_q;
-    a.heavy_n = L.heavy_n;
-    a.heavy_head = L.heavy_n + 1;
+    a.heavy_n = L.heavy_rounds;
+    a.heavy_head = L.heavy_rounds + 3;
     if (L.nj + L.n1 == 0) return MSC3D_OK;
     a.switch_below = kSwitchBelow;
     a.indeg = L.indeg;

@@ -198,7 +198,8 @@ struct CountLaunch {
     unsigned int* flags;            // [0] overflow [1] pool exhausted
     unsigned long long* diag;       // optional development diagnostics (nullptr: off)
     std::uint32_t* heavy_q;         // capacity nj + n1
-    unsigned long long* heavy_n;    // 2 counters, zeroed
+    unsigned long long* heavy_n;    // 2 counters, zeroed (count_write's heavy queue)
+    unsigned long long* heavy_rounds;  // 6 counters, zeroed (Kahn rounds' heavy queues: size, head x 3)
     unsigned long long* resume;     // 3 words of state between the two configurations
     const std::uint32_t* indeg;     // parents per junction
     const std::uint64_t* ovoff;     // overflow-list offsets

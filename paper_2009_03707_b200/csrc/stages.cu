@@ -417,10 +417,12 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.heavy_q = static_cast<std::uint32_t*>(ctx->ensure("heavy_q", std::max<std::uint64_t>(nn, 1), 4));
         L.heavy_n = reinterpret_cast<unsigned long long*>(ctx->d_small + 61);
         L.resume = reinterpret_cast<unsigned long long*>(ctx->d_small + 64);  // 3 words
+        L.heavy_rounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 70);  // 6 words
         L.indeg = indeg;
         L.ovoff = ovoff;
         if (!L.heavy_q) return MSC3D_ERR_NOMEM;
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 61, 0, 16, s));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 70, 0, 48, s));
         if (std::getenv("MSC3D_DIAG")) {
             L.diag = static_cast<unsigned long long*>(ctx->ensure("count_diag", 1024, 8));
             if (L.diag) MSC3D_CUDA_TRY(cudaMemsetAsync(L.diag, 0, 1024 * 8, s));

@@ -49,3 +49,12 @@ try:
         print("slow iterations (>100k cycles): mean phase cycles", np.round(dg[930:935].astype(np.float64) / float(dg[922])).tolist())
 except Exception:
     pass
+if "--all" in sys.argv:
+    st = ctx.get("count_stats", np.uint64)
+    nr = int(st[0])
+    t = st[1:1 + min(nr, 255) + 1].astype(np.int64)
+    print("count round us:", np.round(np.diff(t) / 1e3, 1).tolist())
+    try:
+        print("frontier:", dg[4:4 + 3 * min(nr, 256)].reshape(-1, 3)[:, 2].tolist())
+    except Exception as e:
+        print(e)
