@@ -539,46 +539,73 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
 // its destination (the atomic's old value): slots < kInlineParents are written
 // into the destination's node record right here; later ones (in-degree > 9, rare)
 // are queued as (destination, slot, parent) for the overflow list.
-__global__ void k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
-                          const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
-                          const unsigned int* __restrict__ predone, std::uint32_t* __restrict__ pending,
-                          std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
-                          unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
-                          unsigned long long* __restrict__ n_skip) {
-    unsigned long long mine = 0;
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+// Junctions left with no pending child are Kahn's round 0: appended to `ready` in
+// index order within a block (one reservation per block; blocks run roughly in id
+// order), so round 0 runs over a dense list instead of scanning every junction.
+__global__ void __launch_bounds__(kThreads)
+k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
+          const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
+          const unsigned int* __restrict__ predone, std::uint32_t* __restrict__ pending,
+          std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
+          unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
+          unsigned long long* __restrict__ n_skip, std::uint32_t* __restrict__ ready,
+          unsigned long long* __restrict__ n_ready) {
+    __shared__ unsigned s_wc[kThreads / 32];
+    __shared__ unsigned long long s_base;
+    const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    bool skip = false, is_ready = false;
+    if (i < n_nodes) {
         uint4* dp = reinterpret_cast<uint4*>(node[i].dest);
         if (i < nj && ((ptbits[i >> 5] >> (i & 31)) & 1u)) {
             *dp = make_uint4(kNone, kNone, kNone, kNone);
             pending[i] = kSkip;
-            ++mine;
-            continue;
-        }
-        uint4 d4 = *dp;
-        std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
-        std::uint32_t waiting = 0;  // junction children Kahn still has to finish
+            skip = true;
+        } else {
+            uint4 d4 = *dp;
+            std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+            std::uint32_t waiting = 0;  // junction children Kahn still has to finish
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            if (dd[b] & kTerm) continue;
-            const std::uint32_t t = ((ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u) ? fwd[dd[b]] : dd[b];
-            dd[b] = t;
-            if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
-            ++waiting;
-            if (i >= nj) continue;  // 1-saddles wait for no release: their lengths come after the rounds
-            const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
-            if (slot < static_cast<std::uint32_t>(kInlineParents)) {
-                node[t].par[slot] = static_cast<std::uint32_t>(i);
-            } else {
-                const unsigned long long q = atomicAdd(ovq_n, 1ull);
-                if (q < ovq_cap) ovq[q] = make_uint4(t, slot, static_cast<std::uint32_t>(i), 0u);
+            for (int b = 0; b < 4; ++b) {
+                if (dd[b] & kTerm) continue;
+                const std::uint32_t t = ((ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u) ? fwd[dd[b]] : dd[b];
+                dd[b] = t;
+                if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
+                ++waiting;
+                if (i >= nj) continue;  // 1-saddles wait for no release: their lengths come after the rounds
+                const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
+                if (slot < static_cast<std::uint32_t>(kInlineParents)) {
+                    node[t].par[slot] = static_cast<std::uint32_t>(i);
+                } else {
+                    const unsigned long long q = atomicAdd(ovq_n, 1ull);
+                    if (q < ovq_cap) ovq[q] = make_uint4(t, slot, static_cast<std::uint32_t>(i), 0u);
+                }
             }
+            if (pending[i] != kDone) {
+                pending[i] = waiting;
+                is_ready = i < nj && waiting == 0;
+            }
+            *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
         }
-        if (pending[i] != kDone) pending[i] = waiting;
-        *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
     }
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_skip, mine);
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const unsigned rb = __ballot_sync(0xffffffffu, is_ready);
+    const unsigned sb = __ballot_sync(0xffffffffu, skip);
+    if (lane == 0) {
+        s_wc[w] = __popc(rb);
+        if (sb) atomicAdd(n_skip, static_cast<unsigned long long>(__popc(sb)));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int k = 0; k < kThreads / 32; ++k) {
+            const unsigned c = s_wc[k];
+            s_wc[k] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(n_ready, static_cast<unsigned long long>(tot)) : 0ull;
+    }
+    __syncthreads();
+    if (is_ready) ready[s_base + s_wc[w] + __popc(rb & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
 }
 
 __global__ void k_parent_overflow(const std::uint32_t* __restrict__ indeg, std::uint64_t nj,
@@ -953,6 +980,8 @@ __device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, PoolChu
 }
 
 struct CountArgs {
+    const std::uint32_t* ready;  // Kahn's round 0 (from the rewrite)
+    const unsigned long long* n_ready;
     const NodeRec* node;         // nj junctions, then n1 sources
     std::uint32_t* pending;      // live counters (nj + n1)
     const std::uint32_t* pending0;
@@ -1237,12 +1266,14 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
         }
     };
     if (kWide) {
-        const std::uint64_t total = a.nj;  // 1-saddles: after the rounds (launch_source_len)
+        // the junctions without pending children, listed by the rewrite (1-saddles:
+        // after the rounds, launch_source_len)
+        const std::uint64_t total = *reinterpret_cast<const volatile unsigned long long*>(a.n_ready);
         if (grid.thread_rank() == 0) a.stats[1] = gtimer();
         for (std::uint64_t base = wbase; base < total; base += stride) {
-            const std::uint64_t i = base + lane;
-            const bool valid = i < total && a.pending0[i] == 0;  // kSkip: contracted, kDone: walked
-            count_iter(a, wb, wq, ch, valid, static_cast<std::uint32_t>(i), nxt, &a.cnt[1], done, &a.heavy_n[0]);
+            const std::uint64_t f = base + lane;
+            const bool valid = f < total;
+            count_iter(a, wb, wq, ch, valid, valid ? __ldcg(a.ready + f) : 0u, nxt, &a.cnt[1], done, &a.heavy_n[0]);
         }
         finish_round(0, &a.cnt[1]);
         ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
@@ -1482,11 +1513,12 @@ int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, u
 
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
-                   std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms) {
+                   std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
+                   unsigned long long* n_ready, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits,
-                                                      predone, pending,
-                                                             indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip);
+    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits, predone,
+                                                      pending, indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip,
+                                                      ready, n_ready);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
@@ -1538,6 +1570,8 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.flags = L.flags;
     a.diag = L.diag;
     a.heavy_q = L.heavy_q;
+    a.ready = L.ready;
+    a.n_ready = L.n_ready;
     a.heavy_n = L.heavy_rounds;
     a.heavy_head = L.heavy_rounds + 3;
     if (L.nj + L.n1 == 0) return MSC3D_OK;

@@ -199,6 +199,8 @@ struct CountLaunch {
     unsigned long long* diag;       // optional development diagnostics (nullptr: off)
     std::uint32_t* heavy_q;         // capacity nj + n1
     unsigned long long* heavy_n;    // 2 counters, zeroed (count_write's heavy queue)
+    const std::uint32_t* ready;     // junctions without pending children (Kahn's round 0)
+    const unsigned long long* n_ready;
     unsigned long long* heavy_rounds;  // 6 counters, zeroed (Kahn rounds' heavy queues: size, head x 3)
     unsigned long long* resume;     // 3 words of state between the two configurations
     const std::uint32_t* indeg;     // parents per junction
@@ -227,7 +229,8 @@ int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, u
                        int num_sms);
 int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
-                   std::uint64_t ovq_cap, unsigned long long* n_skip, cudaStream_t s, int num_sms);
+                   std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
+                   unsigned long long* n_ready, cudaStream_t s, int num_sms);
 int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
                            int num_sms);
 // node records' parent counts / overflow offsets, and the queued overflow parents

@@ -364,8 +364,12 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // (nde u32 = 3V*4 bytes, room for 3V/4 entries >> the measured ~0.1% of nodes)
     void* ovq = fa;
     const std::uint64_t ovq_cap = nde / 4;
-    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip, s,
-                                  sms));
+    auto* ready = static_cast<std::uint32_t*>(ctx->ensure("ready0", std::max<std::uint64_t>(nj, 1), 4));
+    if (!ready) return MSC3D_ERR_NOMEM;
+    auto* n_ready = reinterpret_cast<unsigned long long*>(ctx->d_small + 77);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_ready, 0, 8, s));
+    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip,
+                                  ready, n_ready, s, sms));
     // parents beyond the inline ones: an overflow list
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
     TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
@@ -420,6 +424,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.heavy_rounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 70);  // 6 words
         L.indeg = indeg;
         L.ovoff = ovoff;
+        L.ready = ready;
+        L.n_ready = n_ready;
         if (!L.heavy_q) return MSC3D_ERR_NOMEM;
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 61, 0, 16, s));
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 70, 0, 48, s));
