@@ -1329,39 +1329,95 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
 // kLen: the same pass computing only the merged lengths (slen) of the 1-saddles the
 // walk did not finish (pending kDone) -- 1-saddles take no part in Kahn's rounds:
 // nothing waits for them, so their lengths are one coalesced pass after the junctions.
+constexpr int kWriteCap = 512;  // warp buffer entries of k_count_write
 template <bool kLen>
-__global__ void k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
-                              PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
-                              std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
-                              std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
-                              std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n,
-                              const std::uint32_t* __restrict__ spending, std::uint32_t* __restrict__ slen) {
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        if (kLen && spending[i] == kDone) continue;
-        Inputs in;
-        gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
-        const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
-        if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {  // (heavy kernel: kWarpCap)
-            heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
-            continue;
-        }
-        bool ovf = false;
-        if (kLen) {
+__global__ void __launch_bounds__(kThreads)
+k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
+              PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
+              std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
+              std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
+              std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n,
+              const std::uint32_t* __restrict__ spending, std::uint32_t* __restrict__ slen) {
+    // Light sources (<= kHeavy input entries): the warp stages its lanes' inputs in
+    // shared memory (asynchronous 16-byte copies, all in flight at once) and each lane
+    // merges its own from there -- instead of a chain of dependent global loads.
+    // (the length pass -- few live sources, mostly short -- merges per thread from
+    // global memory: measured faster than staging for it)
+    if constexpr (kLen) {
+        for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n1;
+             i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+            if (spending[i] == kDone) continue;
+            Inputs in;
+            gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
+            const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+            if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {
+                heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
+                continue;
+            }
+            bool ovf = false;
             slen[i] = merge<false>(in, pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
-            continue;
         }
-        const std::uint64_t at = off[i];
+        return;
+    }
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const WarpBuf wb = warp_buf(s_dyn, kWriteCap);
+    const int lane = threadIdx.x & 31;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+         wbase < n1; wbase += stride) {
+        const std::uint64_t i = wbase + lane;
+        bool valid = i < n1 && !(kLen && spending[i] == kDone);
+        Inputs in;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) in.len[b] = 0;
+        std::uint32_t T = 0, S = 0;
+        if (valid) {
+            gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
+            T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+            S = staged_size(in);
+        }
+        const bool heavy = valid && T > kHeavy && S + T <= static_cast<std::uint32_t>(kWarpCap);  // (heavy kernel)
+        {
+            const unsigned hm = __ballot_sync(0xffffffffu, heavy);
+            if (hm) {
+                unsigned long long hb = 0;
+                if (lane == 0) hb = atomicAdd(heavy_n, static_cast<unsigned long long>(__popc(hm)));
+                hb = __shfl_sync(0xffffffffu, hb, 0);
+                if (heavy) heavy_q[hb + __popc(hm & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
+            }
+        }
+        valid = valid && !heavy;
+        bool ovf = false;
+        const std::uint64_t at = (!kLen && valid) ? off[i] : 0ull;
         const std::uint32_t one = base_one + static_cast<std::uint32_t>(i);
-        merge<false>(in, pool, &ovf, [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
+        auto emit = [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
             o_one[at + o] = one;
             o_two[at + o] = base_two + k;
             o_cnt[at + o] = c;
-        });
+        };
+        if (valid && S > wb.cap) {  // larger than the buffer (not heavy: rare): direct merge
+            if (kLen) slen[i] = merge<false>(in, pool, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
+            else merge<false>(in, pool, &ovf, emit);
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, valid && S <= wb.cap);
+        while (todo) {
+            const bool mine = (todo >> lane) & 1u;
+            std::uint32_t total = 0;
+            const std::uint32_t base = warp_excl_scan(mine ? S : 0u, &total);
+            const bool go = mine && base + S <= wb.cap;
+            if (go) stage<!kLen>(in, pool, wb, base);
+            cp_async_wait_all();
+            __syncwarp();
+            if (go) {
+                if (kLen) slen[i] = merge_staged<false>(in, wb, base, &ovf, [](std::uint32_t, std::uint32_t, std::uint64_t) {});
+                else merge_staged<true>(in, wb, base, &ovf, emit);
+            }
+            __syncwarp();
+            todo &= ~__ballot_sync(0xffffffffu, go);
+        }
         if (ovf) flags[0] = 1u;
     }
 }
-
 template <bool kLen>
 __global__ void __launch_bounds__(kThreads)
 k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ rec, PoolRef pool,
@@ -1607,9 +1663,12 @@ int count_write_impl(const CountLaunch& L, const std::uint64_t* off, std::uint32
     const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
     const PoolRef pool{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
     MSC3D_CUDA_TRY(cudaMemsetAsync(L.heavy_n, 0, 8, s));
-    k_count_write<kLen><<<grid_full(L.n1), kThreads, 0, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool, off,
-                                                             o_one, o_two, o_cnt, base_one, base_two, L.flags,
-                                                             L.heavy_q, L.heavy_n, L.pending0 + L.nj, L.slen);
+    const std::size_t smem_l = kLen ? 0 : warp_buf_bytes(kWriteCap) * (kThreads / 32);
+    MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write<kLen>),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_l)));
+    k_count_write<kLen><<<grid_full(L.n1), kThreads, smem_l, s>>>(snode, L.n1, static_cast<const JRec*>(L.rec), pool,
+                                                                  off, o_one, o_two, o_cnt, base_one, base_two, L.flags,
+                                                                  L.heavy_q, L.heavy_n, L.pending0 + L.nj, L.slen);
     const std::size_t smem = warp_buf_bytes(kWarpCap) * (kThreads / 32);
     MSC3D_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_count_write_heavy<kLen>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
