@@ -1265,21 +1265,13 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
             grid.sync();
         }
     };
+    // Round 0 runs over the junctions without pending children, listed by the rewrite
+    // (1-saddles: after the rounds, launch_source_len); later rounds over the frontier
+    // (fb, fa, fb, ...).  One call site of the round body keeps the code compact.
     if (kWide) {
-        // the junctions without pending children, listed by the rewrite (1-saddles:
-        // after the rounds, launch_source_len)
-        const std::uint64_t total = *reinterpret_cast<const volatile unsigned long long*>(a.n_ready);
-        if (grid.thread_rank() == 0) a.stats[1] = gtimer();
-        for (std::uint64_t base = wbase; base < total; base += stride) {
-            const std::uint64_t f = base + lane;
-            const bool valid = f < total;
-            count_iter(a, wb, wq, ch, valid, valid ? __ldcg(a.ready + f) : 0u, nxt, &a.cnt[1], done, &a.heavy_n[0]);
-        }
-        finish_round(0, &a.cnt[1]);
-        ncur = *reinterpret_cast<volatile unsigned long long*>(&a.cnt[1]);
-        std::uint32_t* t = cur;
-        cur = nxt;
-        nxt = t;
+        round = 0;
+        cur = const_cast<std::uint32_t*>(a.ready);
+        ncur = *reinterpret_cast<const volatile unsigned long long*>(a.n_ready);
     } else {  // resume
         round = static_cast<int>(a.resume[0]);
         ncur = a.resume[1];
@@ -1289,7 +1281,7 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
         }
     }
     while (ncur) {
-        if (kWide && ncur < a.switch_below) break;
+        if (kWide && round > 0 && ncur < a.switch_below) break;
         unsigned long long* next_cnt = &a.cnt[(round + 1) % 3];
         if (grid.thread_rank() == 0) {
             a.cnt[(round + 2) % 3] = 0;
@@ -1309,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
         ++round;
         std::uint32_t* t = cur;
         cur = nxt;
-        nxt = t;
+        nxt = t == a.ready ? a.fa : t;
     }
     for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.done, done);
