@@ -277,6 +277,7 @@ def main():
     ap.add_argument("--size", type=int, default=0, help="dev only: cube size override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-api", action="store_true", help="skip the C++ drop-in msc3d::compute() timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -415,6 +416,31 @@ def main():
                "path": "msc3d_ctx_compute_host_values (C ABI): pinned samples in (upload overlapped with the "
                        "gradient), pinned host outputs (copies overlapped with the later stages)"}
 
+    # ---- the C++ drop-in msc3d::compute() (include/msc3d/api.hpp): host ScalarField of
+    # doubles in, host MSComplex out (critical points with coordinates and values,
+    # Arc vector, label volumes, input_hash) -- what a reference user's call costs.
+    # One warm-up call (pins the staging buffers), one timed; field_hash alone beside.
+    api = None
+    if rank == 0 and world == 1 and not args.no_api:
+        L = m.lib()
+        L.msc3d_api_timed_compute.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                              C.POINTER(C.c_double)]
+        out = (C.c_double * 8)()
+        v32 = np.ascontiguousarray(v, dtype=np.float32)
+        secs = []
+        for _ in range(2):
+            rc = L.msc3d_api_timed_compute(v32.ctypes.data, dims[0], dims[1], dims[2], 1, out)
+            if rc:
+                raise RuntimeError(f"msc3d::compute() failed: {rc}")
+            secs.append(out[0])
+        if int(out[2]) != a_min + a_ss + a_max or int(out[1]) != sum(c):
+            raise RuntimeError("msc3d::compute() output sizes differ from the device-resident run")
+        api = {"value": ncells / secs[-1] / 1e6, "unit": "Mcells/s", "seconds": secs[-1],
+               "first_call_seconds": secs[0], "field_hash_seconds": out[3],
+               "path": "msc3d::compute(ScalarField, {with_segmentation}) -> MSComplex (C++ drop-in API): "
+                       "parallel f32 conversion + pinned upload, device pipeline, pinned download, parallel "
+                       "host assembly; the byte-serial field_hash (FNV-1a, msc.cpp:31-42) runs concurrently"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -433,7 +459,7 @@ def main():
                        "seed": WORKLOAD["seed"], "lattice_cells": ncells,
                        "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (512 MiB f32 in, 1 GiB codes)"},
             "stages_ms": dict(zip(STAGES, stage_ms)), "stages": stages, "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_api": api, "gpu_launches": int(launches),
             "counts": {"critical": c, "arcs_min": a_min, "arcs_ss": a_ss, "arcs_max": a_max},
             "clocks": clk.summary(),
         }

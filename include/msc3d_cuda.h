@@ -73,6 +73,10 @@ uint64_t msc3d_ctx_launches(msc3d_ctx* ctx);
  * *elem_bytes is the element width; *count the number of elements. */
 int msc3d_ctx_array(msc3d_ctx* ctx, const char* name, void** device_ptr, uint64_t* count,
                     int* elem_bytes);
+/* Page-locked host memory for the host-buffer entry points (full-bandwidth copies). */
+int msc3d_host_alloc(void** out, uint64_t bytes);
+void msc3d_host_free(void* p);
+
 /* Copy a named array to host memory (capacity in bytes); synchronises the stream. */
 int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t capacity_bytes);
 /* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...). */

@@ -157,6 +157,21 @@ int msc3d_ctx_array(msc3d_ctx* ctx, const char* name, void** device_ptr, std::ui
     return MSC3D_OK;
 }
 
+int msc3d_host_alloc(void** out, std::uint64_t bytes) {
+    if (!out) return MSC3D_ERR_INVALID;
+    *out = nullptr;
+    if (cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return MSC3D_ERR_NOMEM;
+    }
+    return MSC3D_OK;
+}
+
+void msc3d_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, std::uint64_t capacity) {
     DevArray* a = ctx->find(name);
     if (!a) return MSC3D_ERR_STATE;
