@@ -73,6 +73,11 @@ uint64_t msc3d_ctx_launches(msc3d_ctx* ctx);
  * *elem_bytes is the element width; *count the number of elements. */
 int msc3d_ctx_array(msc3d_ctx* ctx, const char* name, void** device_ptr, uint64_t* count,
                     int* elem_bytes);
+/* After a compute: "cp_value" (f64 per critical point) = the sample at the cell's
+ * maximum vertex (larger value, then larger id; grid.cpp:129-137) -- CriticalPoint::value
+ * of msc.cpp:106 -- from "cp_cell" and the bound samples. */
+int msc3d_ctx_cp_values(msc3d_ctx* ctx);
+
 /* Page-locked host memory for the host-buffer entry points (full-bandwidth copies). */
 int msc3d_host_alloc(void** out, uint64_t bytes);
 void msc3d_host_free(void* p);

@@ -296,6 +296,56 @@ int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaS
     return MSC3D_OK;
 }
 
+// CriticalPoint::value (msc.cpp:106): the sample at the cell's maximum vertex, the
+// larger value and, on equal values, the larger id (max_vertex_of, grid.cpp:129-137),
+// widened to double exactly.
+template <typename IdT, typename T>
+__global__ void k_cp_values(const IdT* __restrict__ cells, std::uint64_t n, Dims d, const T* __restrict__ f,
+                            double* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        const Coord c = unpack(d, cells[i]);
+        const std::int64_t x0 = c.x >> 1, y0 = c.y >> 1, z0 = c.z >> 1;
+        const int dx = static_cast<int>(c.x & 1), dy = static_cast<int>(c.y & 1), dz = static_cast<int>(c.z & 1);
+        T bv = T(0);
+        std::int64_t bid = -1;
+        for (int oz = 0; oz <= dz; ++oz)
+            for (int oy = 0; oy <= dy; ++oy)
+                for (int ox = 0; ox <= dx; ++ox) {
+                    const std::int64_t vid = (x0 + ox) + d.nx * ((y0 + oy) + d.ny * (z0 + oz));
+                    const T v = f[vid];
+                    if (bid < 0 || v > bv || (v == bv && vid > bid)) {
+                        bv = v;
+                        bid = vid;
+                    }
+                }
+        out[i] = static_cast<double>(bv);
+    }
+}
+
+int launch_cp_values(const void* cells, int id_width, std::uint64_t n, const Dims& d, const void* values,
+                     int value_type, double* out, cudaStream_t s, int num_sms) {
+    if (n == 0) return MSC3D_OK;
+    const unsigned g = grid_for(n, num_sms);
+    if (value_type == MSC3D_VALUE_F64) {
+        if (id_width == 4)
+            k_cp_values<<<g, kThreads, 0, s>>>(static_cast<const std::uint32_t*>(cells), n, d,
+                                               static_cast<const double*>(values), out);
+        else
+            k_cp_values<<<g, kThreads, 0, s>>>(static_cast<const std::uint64_t*>(cells), n, d,
+                                               static_cast<const double*>(values), out);
+    } else {
+        if (id_width == 4)
+            k_cp_values<<<g, kThreads, 0, s>>>(static_cast<const std::uint32_t*>(cells), n, d,
+                                               static_cast<const float*>(values), out);
+        else
+            k_cp_values<<<g, kThreads, 0, s>>>(static_cast<const std::uint64_t*>(cells), n, d,
+                                               static_cast<const float*>(values), out);
+    }
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
 int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int index, int id_width,
                      void* cp_cell, std::uint8_t* cp_index, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;

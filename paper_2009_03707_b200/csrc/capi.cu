@@ -183,6 +183,17 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, std::uint64
     return MSC3D_OK;
 }
 
+int msc3d_ctx_cp_values(msc3d_ctx* ctx) {
+    if (!ctx) return MSC3D_ERR_INVALID;
+    DevArray* cells = ctx->find("cp_cell");
+    if (!cells || !ctx->values) return MSC3D_ERR_STATE;
+    auto* out = static_cast<double*>(ctx->ensure("cp_value", std::max<std::uint64_t>(1, cells->count), 8));
+    if (!out) return MSC3D_ERR_NOMEM;
+    ctx->find("cp_value")->count = cells->count;
+    return msc3d_dev::launch_cp_values(ctx->find("cp_cell")->ptr, ctx->find("cp_cell")->elem, cells->count, ctx->dims,
+                                       ctx->values, ctx->value_type, out, ctx->stream, ctx->num_sms);
+}
+
 int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, std::int64_t* value) {
     auto it = ctx->scalars.find(name);
     if (it == ctx->scalars.end()) return MSC3D_ERR_STATE;

@@ -154,6 +154,9 @@ int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t 
                       void* out, cudaStream_t s, int num_sms);
 int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaStream_t s,
                     int num_sms);
+// CriticalPoint::value of every critical cell (max vertex by value, then id), as f64
+int launch_cp_values(const void* cells, int id_width, std::uint64_t n, const Dims& d, const void* values,
+                     int value_type, double* out, cudaStream_t s, int num_sms);
 int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int index, int id_width,
                      void* cp_cell, std::uint8_t* cp_index, cudaStream_t s, int num_sms);
 int launch_arcs_min(const void* crit1, std::uint64_t n1, int id_width, const Dims& d,

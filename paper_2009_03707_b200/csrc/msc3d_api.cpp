@@ -10,8 +10,11 @@
 #include <chrono>
 #include <future>
 #include <thread>
+
+#include <sys/mman.h>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -68,7 +71,7 @@ struct Pinned {
 struct Device {
     msc3d_ctx* ctx = nullptr;
     std::mutex mu;
-    Pinned in, cp_cell, cp_index, arc_src, arc_dst, arc_mult;
+    Pinned in, cp_cell, cp_index, cp_value, arc_src, arc_dst, arc_mult;
     ~Device() {
         if (ctx) msc3d_ctx_destroy(ctx);
     }
@@ -81,6 +84,31 @@ int host_threads(int threads) {
 }
 
 // fn(begin, end) over [0, n) in `threads` contiguous slices (the calling thread takes one).
+template <typename F>
+void parallel_for(std::size_t n, int threads, F fn);
+
+// vec.resize(n) for a multi-GB result vector, without the serial first-touch page
+// faults: reserve the storage, ask for transparent huge pages on it, fault it in from
+// `threads` threads, then construct the elements (now a plain store stream).
+template <typename V>
+void resize_prefaulted(V& vec, std::size_t n, int threads) {
+    vec.reserve(n);
+    const std::size_t bytes = n * sizeof(typename V::value_type);
+    if (bytes >= (std::size_t{64} << 20)) {
+        auto* p = reinterpret_cast<unsigned char*>(vec.data());
+        const std::uintptr_t a = (reinterpret_cast<std::uintptr_t>(p) + 4095) & ~std::uintptr_t{4095};
+        const std::uintptr_t e = reinterpret_cast<std::uintptr_t>(p) + bytes;
+#ifdef MADV_HUGEPAGE
+        if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+#endif
+        const std::size_t pages = bytes / 4096;
+        parallel_for(pages, threads, [p](std::size_t b, std::size_t e2) {
+            for (std::size_t k = b; k < e2; ++k) reinterpret_cast<volatile unsigned char*>(p)[k * 4096] = 0;
+        });
+    }
+    vec.resize(n);
+}
+
 template <typename F>
 void parallel_for(std::size_t n, int threads, F fn) {
     const std::size_t t = std::max<std::size_t>(1, std::min<std::size_t>(static_cast<std::size_t>(threads), n / 65536 + 1));
@@ -585,6 +613,14 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     Device& dev = device();
     std::lock_guard<std::mutex> lock(dev.mu);
     const int T = host_threads(opt.threads);
+    // MSC3D_API_TRACE=1: phase times of this call on stderr
+    static const bool trace = std::getenv("MSC3D_API_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (trace)
+            std::fprintf(stderr, "compute() %-18s %8.1f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     auto hash = std::async(std::launch::async, [&f] { return field_hash(f); });
     const std::size_t nv = f.values.size();
     if (nv != f.dims.vertex_count()) throw std::invalid_argument("scalar field size mismatch");
@@ -605,8 +641,11 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
         else
             check(msc3d_ctx_load_values(dev.ctx, to_c(f.dims), MSC3D_VALUE_F64, f.values.data()), "ScalarField");
     }
+    mark("uploaded");
     double ms[5] = {0, 0, 0, 0, 0};
     check(msc3d_ctx_compute(dev.ctx, opt.with_segmentation ? MSC3D_OPT_SEGMENTATION : 0, ms), "compute");
+    check(msc3d_ctx_cp_values(dev.ctx), "critical point values");
+    mark("device done");
     if (opt.validate) {
         const GradientField g{f.dims, fetch<std::uint8_t>(dev.ctx, "codes")};
         if (!validate_gradient(g).ok()) throw std::runtime_error("compute: gradient failed validation");
@@ -642,11 +681,12 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
             if (t.joinable()) t.join();
         }
     };
-    Joiner alloc_cp{std::thread([&] { m.critical_points.resize(ncp); })};
-    Joiner alloc_arcs{std::thread([&] { m.arcs.resize(na); })};
+    const int Tq = std::max(1, T / 3);
+    Joiner alloc_cp{std::thread([&] { resize_prefaulted(m.critical_points, ncp, Tq); })};
+    Joiner alloc_arcs{std::thread([&] { resize_prefaulted(m.arcs, na, Tq); })};
     Joiner alloc_labels{std::thread([&] {
-        lv.vertex_to_min.resize(nlmin);
-        lv.cube_to_max.resize(nlmax);
+        resize_prefaulted(lv.vertex_to_min, nlmin, Tq);
+        resize_prefaulted(lv.cube_to_max, nlmax, Tq);
     })};
     auto download = [&](const char* name, Pinned& st, std::size_t bytes) {
         void* h = st.get(std::max<std::size_t>(1, bytes));
@@ -655,10 +695,13 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     };
     const auto* cells = static_cast<const CellIndex*>(download("cp_cell", dev.cp_cell, ncp * sizeof(CellIndex)));
     const auto* index = static_cast<const std::uint8_t*>(download("cp_index", dev.cp_index, ncp));
+    const auto* value = static_cast<const double*>(download("cp_value", dev.cp_value, ncp * 8));
     const auto* asrc = static_cast<const std::uint32_t*>(download("arc_src", dev.arc_src, na * 4));
     const auto* adst = static_cast<const std::uint32_t*>(download("arc_dst", dev.arc_dst, na * 4));
     const auto* amul = static_cast<const std::uint64_t*>(download("arc_mult", dev.arc_mult, na * 8));
+    mark("downloaded");
     alloc_cp.t.join();
+    mark("cp vector ready");
     parallel_for(ncp, T, [&](std::size_t b, std::size_t e) {
         for (std::size_t i = b; i < e; ++i) {
             CriticalPoint& cp = m.critical_points[i];
@@ -667,10 +710,12 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
             cp.index = index[i];
             cp.doubled = unpack_cell(f.dims, cells[i]);
             cp.midpoint = {cp.doubled.x / 2.0, cp.doubled.y / 2.0, cp.doubled.z / 2.0};
-            cp.value = f[max_vertex_of(f, cells[i])];
+            cp.value = value[i];  // f[max_vertex_of(f, cell)], from the device
         }
     });
+    mark("cps filled");
     alloc_arcs.t.join();
+    mark("arc vector ready");
     parallel_for(na, T, [&](std::size_t b, std::size_t e) {
         for (std::size_t i = b; i < e; ++i) m.arcs[i] = Arc{asrc[i], adst[i], amul[i]};
     });
@@ -682,7 +727,9 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
               "labels_max");
         m.labels = std::move(lv);
     }
+    mark("arcs+labels filled");
     m.input_hash = hash.get();
+    mark("hash done");
     return m;
 }
 
