@@ -684,6 +684,18 @@ struct Inputs {
 template <bool kL2>
 __device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ rec, Inputs& in) {
     const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
+    // all child records are loaded first (unconditionally: record 0 stands in for
+    // terminal / absent branches), so the up to eight loads are in flight together
+    // instead of one record round trip after another
+    uint4 ra[4], rb[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const std::uint32_t t = dd[b];
+        const bool need = t != kNone && !(t & kTerm);
+        const uint4* p = reinterpret_cast<const uint4*>(rec + (need ? t : 0u));
+        ra[b] = ld<kL2>(p);
+        rb[b] = ld<kL2>(p + 1);
+    }
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
         const std::uint32_t t = dd[b];
@@ -697,16 +709,16 @@ __device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ 
             in.k0[b] = t & ~kTerm;
             in.c0[b] = 1;
         } else {
-            const JRec r = load_rec<kL2>(rec + t);
-            in.len[b] = r.len;
-            if (r.kind == 0) {
-                in.k0[b] = r.k0;
-                in.k1[b] = r.k1;
-                in.c0[b] = r.c0;
-                in.c1[b] = r.c1;
+            const std::uint64_t c0 = static_cast<std::uint64_t>(rb[b].x) | (static_cast<std::uint64_t>(rb[b].y) << 32);
+            in.len[b] = ra[b].x;
+            if (ra[b].w == 0) {  // kind 0: inline
+                in.k0[b] = ra[b].y;
+                in.k1[b] = ra[b].z;
+                in.c0[b] = c0;
+                in.c1[b] = static_cast<std::uint64_t>(rb[b].z) | (static_cast<std::uint64_t>(rb[b].w) << 32);
             } else {
-                in.off[b] = r.c0;
-                if (r.c0 == kBadOff) in.len[b] = 0;  // pool exhausted: the host reruns
+                in.off[b] = c0;
+                if (c0 == kBadOff) in.len[b] = 0;  // pool exhausted: the host reruns
             }
         }
     }
@@ -1085,6 +1097,15 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
     }
+    // Parents are released first: they only run next round, after the grid barrier
+    // that also publishes P(u), so the release atomics overlap this node's gather and
+    // merge instead of following them.  (Heavy nodes too: the heavy pass finishes them
+    // within this round.)
+    {
+        const std::uint32_t rn = valid && u < a.nj ? npar : 0u;
+        release_parents(a, wq, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, meta, par0,
+                        par1, nxt, next_cnt);
+    }
     // heavy nodes -> the round's heavy queue
     const bool heavy = valid && T > kHeavy && S + T <= wb.cap;
     {
@@ -1154,9 +1175,6 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
     }
     if (junction) ++done;
     if (ovf) a.flags[0] = 1u;
-    const std::uint32_t rn = junction ? npar : 0u;
-    release_parents(a, wq, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, meta, par0, par1,
-                    nxt, next_cnt);
 }
 
 // One heavy node, merged by the whole warp (all lanes call with the same u).
@@ -1204,9 +1222,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
         if (junction) ++done;
     }
     __syncwarp();
-    const std::uint32_t rn = lane == 0 && junction ? a.indeg[u] : 0u;
-    release_parents(a, wq, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, meta, par0, par1,
-                    nxt, next_cnt);
+    // (its parents were released when the light pass queued it)
 }
 
 // The round's heavy queue, one warp per node (dynamic: warps take the next node).
