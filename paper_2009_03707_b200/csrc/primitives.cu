@@ -14,38 +14,104 @@ namespace msc3d_dev {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;
 
+// Single-value decoupled look-back over packed status words: bits 62-63 = 0 none,
+// 1 aggregate, 2 inclusive prefix; bits 0-61 = the value (one 8-byte load per
+// predecessor).  Called by all threads; returns the tile's exclusive prefix.
+__device__ __forceinline__ std::uint64_t tile_lookback1(unsigned long long* status, std::uint32_t tile,
+                                                        std::uint64_t tot, std::uint64_t* smem1) {
+    constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kVal = (1ull << 62) - 1;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (lane == 0)
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(status + tile),
+                         "l"((tile == 0 ? kIncl : kAgg) | tot) : "memory");
+        std::uint64_t excl = 0;
+        if (tile > 0) {
+            std::int64_t pred = static_cast<std::int64_t>(tile) - 1;
+            for (;;) {
+                const std::int64_t idx = pred - lane;
+                unsigned long long w = kIncl;  // (before tile 0: an empty inclusive prefix)
+                if (idx >= 0) {
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(status + idx) : "memory");
+                    } while ((w >> 62) == 0);
+                }
+                const std::uint32_t incl_mask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+                const int stop = incl_mask ? __ffs(incl_mask) - 1 : 31;
+                std::uint64_t x = lane <= stop ? (w & kVal) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                excl += x;
+                if (incl_mask) break;
+                pred -= 32;
+            }
+            if (lane == 0)
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(status + tile), "l"(kIncl | (excl + tot))
+                             : "memory");
+        }
+        if (lane == 0) *smem1 = excl;
+    }
+    __syncthreads();
+    return *smem1;
+}
+
+// Exclusive u32 -> u64 scan, one 4096-element tile per block with decoupled
+// look-back.  Inputs are read warp-striped (coalesced 128-byte rows) and transposed
+// through shared memory so each thread scans 16 consecutive items; the u64 results
+// go back through shared memory and leave warp-striped as well.
 __global__ void __launch_bounds__(kThreads)
 k_scan_u32(const std::uint32_t* __restrict__ in, std::uint64_t n, std::uint64_t* __restrict__ out,
-           TileStatus st, std::uint64_t* total) {
+           unsigned long long* status, std::uint32_t* ticket, std::uint64_t* total) {
     __shared__ std::uint64_t sm[40];
     __shared__ std::uint32_t s_tile;
-    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __shared__ std::uint64_t s_buf[kTile];  // 32 KB: u32 inputs (first half), then u64 outputs
+    auto* s_in = reinterpret_cast<std::uint32_t*>(s_buf);
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const std::uint32_t tile = s_tile;
-    const std::uint64_t first = static_cast<std::uint64_t>(tile) * kTile +
-                                static_cast<std::uint64_t>(threadIdx.x) * kItems;
+    const std::uint64_t base = static_cast<std::uint64_t>(tile) * kTile;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const std::uint64_t i = base + static_cast<std::uint64_t>(k) * kThreads + threadIdx.x;
+        s_in[k * kThreads + threadIdx.x] = i < n ? in[i] : 0u;
+    }
+    __syncthreads();
     std::uint32_t v[kItems];
     std::uint64_t sum = 0;
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        v[k] = first + k < n ? in[first + k] : 0u;
-        sum += v[k];
+        // rotated index: consecutive threads hit different banks
+        const int kk = (k + threadIdx.x) & (kItems - 1);
+        v[kk] = s_in[threadIdx.x * kItems + kk];
     }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) sum += v[k];
     std::uint64_t block_total;
-    const std::uint64_t excl = block_excl_scan(sum, &block_total, sm);
-    const std::uint64_t tot[4] = {block_total, 0, 0, 0};
-    tile_lookback4(st, tile, tot, sm + 34);
-    std::uint64_t at = sm[34] + excl;
+    const std::uint64_t excl = block_excl_scan(sum, &block_total, sm);  // (ends with a barrier)
+    const std::uint64_t prefix = tile_lookback1(status, tile, block_total, sm + 34);
+    std::uint64_t at = prefix + excl;
+    std::uint64_t r[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        if (first + k < n) out[first + k] = at;
+        r[k] = at;
         at += v[k];
     }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const int kk = (k + threadIdx.x) & (kItems - 1);
+        s_buf[threadIdx.x * kItems + kk] = r[kk];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const std::uint64_t i = base + static_cast<std::uint64_t>(k) * kThreads + threadIdx.x;
+        if (i < n) out[i] = s_buf[k * kThreads + threadIdx.x];
+    }
     const std::uint64_t ntiles = (n + kTile - 1) / kTile;
-    if (tile == ntiles - 1 && threadIdx.x == 0 && total) *total = sm[34] + block_total;
+    if (tile == ntiles - 1 && threadIdx.x == 0 && total) *total = prefix + block_total;
 }
 
 __global__ void k_finite_f32(const float* v, std::uint64_t n, unsigned long long* bad) {
@@ -91,15 +157,12 @@ int scan_u32(const std::uint32_t* in, std::uint64_t n, std::uint64_t* out, std::
         return MSC3D_OK;
     }
     const std::uint64_t ntiles = (n + kTile - 1) / kTile;
-    char* buf = static_cast<char*>(ws.get(ntiles * 68 + 16));
+    char* buf = static_cast<char*>(ws.get(ntiles * 8 + 16));
     if (!buf) return MSC3D_ERR_NOMEM;
-    TileStatus st;
-    st.agg = reinterpret_cast<std::uint64_t*>(buf);
-    st.incl = st.agg + 4 * ntiles;
-    st.flag = reinterpret_cast<std::uint32_t*>(st.incl + 4 * ntiles);
-    st.ticket = st.flag + ntiles;
-    MSC3D_CUDA_TRY(cudaMemsetAsync(st.flag, 0, (ntiles + 1) * 4, s));
-    k_scan_u32<<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(in, n, out, st, d_total);
+    auto* status = reinterpret_cast<unsigned long long*>(buf);
+    auto* ticket = reinterpret_cast<std::uint32_t*>(status + ntiles);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(buf, 0, ntiles * 8 + 4, s));
+    k_scan_u32<<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(in, n, out, status, ticket, d_total);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
