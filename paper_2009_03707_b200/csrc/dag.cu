@@ -1496,7 +1496,8 @@ EGrid egrid(const Dims& d) {
 int launch_succ_table(const std::uint8_t* codes, const Dims& d, std::uint16_t* succ, cudaStream_t s, int num_sms) {
     const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
     if (rows == 0) return MSC3D_OK;
-    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(rows, static_cast<std::uint64_t>(num_sms) * 32));
+    // one block per row, in row order: neighbouring rows share their code lines in L2
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(rows, 0x7fffffffull));
     k_succ_table<<<grid, 128, 0, s>>>(codes, d, succ);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
