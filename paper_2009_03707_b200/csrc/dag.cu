@@ -557,17 +557,19 @@ k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
     if (i < n_nodes) {
         uint4* dp = reinterpret_cast<uint4*>(node[i].dest);
         if (i < nj && ((ptbits[i >> 5] >> (i & 31)) & 1u)) {
-            *dp = make_uint4(kNone, kNone, kNone, kNone);
-            pending[i] = kSkip;
+            pending[i] = kSkip;  // (its record is never read again)
             skip = true;
         } else {
             uint4 d4 = *dp;
             std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
             std::uint32_t waiting = 0;  // junction children Kahn still has to finish
+            bool moved = false;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 if (dd[b] & kTerm) continue;
-                const std::uint32_t t = ((ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u) ? fwd[dd[b]] : dd[b];
+                const bool pt = (ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u;
+                const std::uint32_t t = pt ? fwd[dd[b]] : dd[b];
+                moved |= pt;
                 dd[b] = t;
                 if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
                 ++waiting;
@@ -584,7 +586,7 @@ k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
                 pending[i] = waiting;
                 is_ready = i < nj && waiting == 0;
             }
-            *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+            if (moved) *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);  // (most records are unchanged)
         }
     }
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
