@@ -418,7 +418,7 @@ constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by 
 template <typename IdT>
 __global__ void __launch_bounds__(kThreads)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
-       NodeRec* __restrict__ node, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
+       uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
        uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
        unsigned long long* __restrict__ n_predone) {
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
@@ -453,7 +453,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                 ++nd;
                 if (!(t & kTerm)) ++pend;
             }
-            *reinterpret_cast<uint4*>(node[i].dest) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+            dest[i] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
             if (pend == 0) {
                 // terminal keys (kNone sorts last), sorted, runs counted
                 std::uint32_t k[4] = {dd[0] & ~kTerm, dd[1] & ~kTerm, dd[2] & ~kTerm, dd[3] & ~kTerm};
@@ -508,7 +508,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
 // jumping), or j itself.
 // ptbits: one bit per junction, set for pass-through ones (10 MB at 512^3,
 // L2-resident), so the rewrite reads fwd only where it can differ.
-__global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj, std::uint32_t* __restrict__ fwd,
+__global__ void k_passthrough(const uint4* __restrict__ dest, std::uint64_t nj, std::uint32_t* __restrict__ fwd,
                               unsigned int* __restrict__ ptbits) {
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < nj;
@@ -516,7 +516,7 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
         const std::uint64_t j = base + (threadIdx.x & 31);
         bool pt = false;
         if (j < nj) {
-            const uint4 d4 = *reinterpret_cast<const uint4*>(node[j].dest);
+            const uint4 d4 = dest[j];
             const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
             int live = 0;
             std::uint32_t child = kNone;
@@ -543,7 +543,7 @@ __global__ void k_passthrough(const NodeRec* __restrict__ node, std::uint64_t nj
 // index order within a block (one reservation per block; blocks run roughly in id
 // order), so round 0 runs over a dense list instead of scanning every junction.
 __global__ void __launch_bounds__(kThreads)
-k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
+k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj, std::uint64_t n_nodes,
           const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
           const unsigned int* __restrict__ predone, std::uint32_t* __restrict__ pending,
           std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
@@ -555,7 +555,7 @@ k_rewrite(NodeRec* __restrict__ node, std::uint64_t nj, std::uint64_t n_nodes,
     const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     bool skip = false, is_ready = false;
     if (i < n_nodes) {
-        uint4* dp = reinterpret_cast<uint4*>(node[i].dest);
+        uint4* dp = dest + i;
         if (i < nj && ((ptbits[i >> 5] >> (i & 31)) & 1u)) {
             pending[i] = kSkip;  // (its record is never read again)
             skip = true;
@@ -994,6 +994,7 @@ __device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, PoolChu
 }
 
 struct CountArgs {
+    const uint4* dest;           // branch destinations per node
     const std::uint32_t* ready;  // Kahn's round 0 (from the rewrite)
     const unsigned long long* n_ready;
     const NodeRec* node;         // nj junctions, then n1 sources
@@ -1090,7 +1091,7 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
     std::uint32_t npar = 0;  // parents: their count from the rewrite's slot counters
     if (valid) {
         const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
-        const uint4 d4 = nr[0];
+        const uint4 d4 = a.dest[u];
         if (u < a.nj) npar = a.indeg[u];
         meta = nr[1];
         par0 = nr[2];
@@ -1185,7 +1186,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
                                             unsigned long long& done) {
     const int lane = threadIdx.x & 31;
     const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
-    const uint4 d4 = nr[0], meta = nr[1], par0 = nr[2], par1 = nr[3];
+    const uint4 d4 = a.dest[u], meta = nr[1], par0 = nr[2], par1 = nr[3];
     Inputs h;
     gather<true>(d4, a.rec, h);
     const std::uint32_t T = h.len[0] + h.len[1] + h.len[2] + h.len[3];
@@ -1342,7 +1343,7 @@ __global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) 
 constexpr int kWriteCap = 512;  // warp buffer entries of k_count_write
 template <bool kLen>
 __global__ void __launch_bounds__(kThreads)
-k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* __restrict__ rec,
+k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __restrict__ rec,
               PoolRef pool, const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
               std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
               std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
@@ -1358,7 +1359,7 @@ k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* _
              i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
             if (spending[i] == kDone) continue;
             Inputs in;
-            gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
+            gather<false>(sdest[i], rec, in);
             const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
             if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {
                 heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
@@ -1382,7 +1383,7 @@ k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* _
         for (int b = 0; b < 4; ++b) in.len[b] = 0;
         std::uint32_t T = 0, S = 0;
         if (valid) {
-            gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, in);
+            gather<false>(sdest[i], rec, in);
             T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
             S = staged_size(in);
         }
@@ -1430,7 +1431,7 @@ k_count_write(const NodeRec* __restrict__ snode, std::uint64_t n1, const JRec* _
 }
 template <bool kLen>
 __global__ void __launch_bounds__(kThreads)
-k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ rec, PoolRef pool,
+k_count_write_heavy(const uint4* __restrict__ sdest, const JRec* __restrict__ rec, PoolRef pool,
                     const std::uint64_t* __restrict__ off, std::uint32_t* __restrict__ o_one,
                     std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt, std::uint32_t base_one,
                     std::uint32_t base_two, unsigned int* __restrict__ flags,
@@ -1444,7 +1445,7 @@ k_count_write_heavy(const NodeRec* __restrict__ snode, const JRec* __restrict__ 
          k += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
         const std::uint32_t i = heavy_q[k];
         Inputs h;
-        gather<false>(*reinterpret_cast<const uint4*>(snode[i].dest), rec, h);
+        gather<false>(sdest[i], rec, h);
         std::uint32_t at = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -1554,7 +1555,7 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
                 int num_sms) {
     if (n == 0) return MSC3D_OK;
     WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
-    auto* nr = static_cast<NodeRec*>(node);
+    auto* nr = static_cast<uint4*>(node);  // the nodes' destination records
     auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)
         k_walk<std::uint32_t><<<grid_full(n), kThreads, 0, s>>>(
@@ -1572,18 +1573,18 @@ int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
                        int num_sms) {
     if (nj == 0) return MSC3D_OK;
-    k_passthrough<<<grid_full(nj), kThreads, 0, s>>>(static_cast<const NodeRec*>(node), nj, fwd, ptbits);
+    k_passthrough<<<grid_full(nj), kThreads, 0, s>>>(static_cast<const uint4*>(node), nj, fwd, ptbits);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
+int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), nj, n_nodes, fwd, ptbits, predone,
+    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), static_cast<uint4*>(dest), nj, n_nodes, fwd, ptbits, predone,
                                                       pending, indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip,
                                                       ready, n_ready);
     count_launch();
@@ -1637,6 +1638,7 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.flags = L.flags;
     a.diag = L.diag;
     a.heavy_q = L.heavy_q;
+    a.dest = static_cast<const uint4*>(L.dest);
     a.ready = L.ready;
     a.n_ready = L.n_ready;
     a.heavy_n = L.heavy_rounds;
@@ -1671,7 +1673,7 @@ int count_write_impl(const CountLaunch& L, const std::uint64_t* off, std::uint32
                      std::uint64_t* o_cnt, std::uint32_t base_one, std::uint32_t base_two, cudaStream_t s,
                      int num_sms) {
     if (L.n1 == 0) return MSC3D_OK;
-    const NodeRec* snode = static_cast<const NodeRec*>(L.node) + L.nj;
+    const uint4* snode = static_cast<const uint4*>(L.dest) + L.nj;
     const PoolRef pool{L.pool_key, L.pool_cnt, L.pool_top, L.arena_cap};
     MSC3D_CUDA_TRY(cudaMemsetAsync(L.heavy_n, 0, 8, s));
     const std::size_t smem_l = kLen ? 0 : warp_buf_bytes(kWriteCap) * (kThreads / 32);

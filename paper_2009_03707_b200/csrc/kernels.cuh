@@ -202,6 +202,7 @@ struct CountLaunch {
     unsigned long long* diag;       // optional development diagnostics (nullptr: off)
     std::uint32_t* heavy_q;         // capacity nj + n1
     unsigned long long* heavy_n;    // 2 counters, zeroed (count_write's heavy queue)
+    const void* dest;               // uint4 branch destinations per node (junctions, then 1-saddles)
     const std::uint32_t* ready;     // junctions without pending children (Kahn's round 0)
     const unsigned long long* n_ready;
     unsigned long long* heavy_rounds;  // 6 counters, zeroed (Kahn rounds' heavy queues: size, head x 3)
@@ -230,7 +231,7 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
 int node_rec_bytes();
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
                        int num_sms);
-int launch_rewrite(void* node, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
+int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms);

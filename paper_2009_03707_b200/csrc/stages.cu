@@ -316,6 +316,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
     void* node = ctx->ensure("jnode", nn, msc3d_dev::node_rec_bytes());
+    auto* jdest = static_cast<char*>(ctx->ensure("jdest", std::max<std::uint64_t>(nn, 1), 16));  // branch destinations
     auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nn, 4));
     auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nn, 4));
     auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
@@ -328,7 +329,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!jlist || !node || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !rec ||
+    if (!jlist || !node || !jdest || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !rec ||
         !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
@@ -338,16 +339,16 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     if (!predone) return MSC3D_ERR_NOMEM;
     auto* n_predone = reinterpret_cast<unsigned long long*>(ctx->d_small + 30);
     MSC3D_CUDA_TRY(cudaMemsetAsync(n_predone, 0, 8, s));
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, node, pending, flags, rec, nullptr,
+    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
                                predone, n_predone, s, sms));
     TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, src_ids, w, n1,
-                               static_cast<char*>(node) + nj * msc3d_dev::node_rec_bytes(), pending + nj, flags, nullptr, slen, nullptr, nullptr, s,
+                               jdest + nj * 16, pending + nj, flags, nullptr, slen, nullptr, nullptr, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
     // contracted away by pointer jumping
     auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
     if (!ptbits) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_passthrough(node, nj, fwd, ptbits, s, sms));
+    TRY(msc3d_dev::launch_passthrough(jdest, nj, fwd, ptbits, s, sms));
     {  // pointer jumping to the end of pass-through chains, all rounds in one launch
         auto* jflags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);
         auto* jrounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
@@ -368,7 +369,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     if (!ready) return MSC3D_ERR_NOMEM;
     auto* n_ready = reinterpret_cast<unsigned long long*>(ctx->d_small + 77);
     MSC3D_CUDA_TRY(cudaMemsetAsync(n_ready, 0, 8, s));
-    TRY(msc3d_dev::launch_rewrite(node, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip,
+    TRY(msc3d_dev::launch_rewrite(node, jdest, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip,
                                   ready, n_ready, s, sms));
     // parents beyond the inline ones: an overflow list
     TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
@@ -402,6 +403,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.pool_cnt = static_cast<std::uint64_t*>(ctx->ensure("pool_cnt", pcap, 8));
         if (!L.pool_key || !L.pool_cnt) return MSC3D_ERR_NOMEM;
         L.node = node;
+        L.dest = jdest;
         L.pending = pending;
         L.pending0 = pending0;
         L.rsrc = rsrc;
