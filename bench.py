@@ -192,6 +192,10 @@ def run_sharded(args, world, rank, local):
     sv = mg.slab_values(v, dims, plan)
     dev_in = torch.from_numpy(sv).cuda()
     sc = mg.ShardedCompute(m, dims, plan, local)
+    # both device contexts run on torch's current stream, which the collectives are
+    # ordered with: CUDA events on it bracket the whole step
+    stream = torch.cuda.current_stream()
+    sc.set_stream(stream.cuda_stream)
     for _ in range(args.warmup):
         sc.step(dev_in, m.OPT_SEGMENTATION)
     torch.cuda.synchronize()
@@ -199,16 +203,16 @@ def run_sharded(args, world, rank, local):
     torch.cuda.synchronize()
     stage_acc = np.zeros(5)
     l0 = sc.slab.launches() + sc.full.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
+        ev0.record(stream)
         for _ in range(args.steps):
             out = sc.step(dev_in, m.OPT_SEGMENTATION)
             stage_acc += np.array(sc.stage_ms)
+        ev1.record(stream)
         torch.cuda.synchronize()
-        t1 = time.perf_counter()
-    # every step ends with host synchronisation (the library's size handshakes), so the
-    # wall clock between the synchronised ends equals the device time of the steps
-    ms_step = max_over_ranks((t1 - t0) * 1e3 / args.steps, world, f"cuda:{local}")
+    dist.barrier()
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world, f"cuda:{local}")
     value = ncells / (ms_step / 1e3) / 1e6
     n_arcs = int(out["arc_src"].numel())
     launches = (sc.slab.launches() + sc.full.launches() - l0) // args.steps
