@@ -429,20 +429,41 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     std::uint32_t crit[4] = {0, 0, 0, 0};
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
     const std::uint64_t ngroups = (ntiles + kGroup - 1) / kGroup;
+    // tile origin (the -1 halo corner), 32-bit: tile ids and coordinates fit
     auto origin = [&](std::uint64_t ti, std::int64_t& x0, std::int64_t& y0, std::int64_t& z0) {
-        const std::uint64_t tyz = ti / tiles.x;
-        x0 = static_cast<std::int64_t>(ti - tyz * tiles.x) * TX - 1;
-        y0 = static_cast<std::int64_t>(tyz % tiles.y) * TY - 1;
-        z0 = static_cast<std::int64_t>(tyz / tiles.y + tz_first) * TZ - 1;
+        const std::uint32_t t32 = static_cast<std::uint32_t>(ti);
+        const std::uint32_t tyz = t32 / tiles.x;
+        x0 = static_cast<std::int64_t>(static_cast<int>((t32 - tyz * tiles.x) * TX) - 1);
+        y0 = static_cast<std::int64_t>(static_cast<int>((tyz % tiles.y) * TY) - 1);
+        z0 = static_cast<std::int64_t>(static_cast<int>((tyz / tiles.y + tz_first) * TZ) - 1);
     };
+    // element offsets inside a tile fit 32 bits when a 4-plane slab does
+    const bool off32 = static_cast<std::uint64_t>(d.nx) * d.ny * SZ < (1ull << 31);
+    const int nx32 = static_cast<int>(d.nx), nxy32 = static_cast<int>(d.nx * d.ny);
     // group gi's tiles (+1 halo) -> buffer set b: in-range samples by asynchronous
-    // copies, the rest (and tiles past the end) 0
+    // copies, the rest (and tiles past the end) 0.  Interior tiles (the common case)
+    // skip the per-sample range checks.
     auto load_group = [&](std::uint64_t gi, int b) {
         for (int g = 0; g < kGroup; ++g) {
             const std::uint64_t ti = gi * kGroup + g;
             std::int64_t x0, y0, z0;
             origin(ti, x0, y0, z0);
             T* dst = &tiles_sm[b][g][0][0][0];
+            const bool interior = off32 && ti < ntiles && x0 >= 0 && x0 + SX <= d.nx && y0 >= 0 && y0 + SY <= d.ny &&
+                                  z0 >= 0 && z0 + SZ <= d.nz;
+            if (interior) {
+                const T* fb = f + (x0 + d.nx * (y0 + d.ny * z0));
+                for (int i = tid; i < SX * SY * SZ; i += NT) {
+                    const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
+                    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+                    const T* src = fb + (lx + nx32 * ly + nxy32 * lz);
+                    if (sizeof(T) == 4)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+                }
+                continue;
+            }
             for (int i = tid; i < SX * SY * SZ; i += NT) {
                 const int lz = i / (SX * SY), r = i - lz * (SX * SY), ly = r / SX, lx = r - ly * SX;
                 const std::int64_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
@@ -471,11 +492,15 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         const int set = cur;
         if (kSets == 2) cur ^= 1;
 
+        // this group's tile origins, once (kGroup == 2: selects, not indexed arrays)
+        static_assert(kGroup == 2, "origins below are written out for pairs of tiles");
+        std::int64_t ox0, oy0, oz0, ox1, oy1, oz1;
+        origin(gi * kGroup, ox0, oy0, oz0);
+        origin(gi * kGroup + 1, ox1, oy1, oz1);
         auto writer_for = [&](int g, int lid, StarWriter& w) {  // false: vertex outside the grid
             const std::uint64_t ti = gi * kGroup + g;
             if (ti >= ntiles) return false;
-            std::int64_t x0, y0, z0;
-            origin(ti, x0, y0, z0);
+            const std::int64_t x0 = g ? ox1 : ox0, y0 = g ? oy1 : oy0, z0 = g ? oz1 : oz0;
             const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
             w.vx = x0 + 1 + lx;
             w.vy = y0 + 1 + ly;
