@@ -169,11 +169,18 @@ struct StarWriter {
     std::uint32_t inr;
     std::uint64_t ncrit;           // 16 bits per dimension
 
+    std::uint32_t cube0, csy, csz;  // dense id of the cube at slot 0 (mod 2^32), cube strides
+
+    __device__ __forceinline__ void init_cubes() {
+        csy = static_cast<std::uint32_t>(d.nx - 1);
+        csz = static_cast<std::uint32_t>((d.nx - 1) * (d.ny - 1));
+        cube0 = static_cast<std::uint32_t>(vx - 1) + csy * static_cast<std::uint32_t>(vy - 1) +
+                csz * static_cast<std::uint32_t>(vz - 1);
+    }
+    // dense id of the in-box cube at slot t (u32 wrap-around is exact: the result is)
     __device__ __forceinline__ std::uint32_t cube_dense_of(int t) const {
         const int z = (t * 57) >> 9, r = t - 9 * z, y = (r * 11) >> 5, x = r - 3 * y;
-        return static_cast<std::uint32_t>((vx + (x == 0 ? -1 : 0)) +
-                                          (d.nx - 1) * ((vy + (y == 0 ? -1 : 0)) +
-                                                        (d.ny - 1) * (vz + (z == 0 ? -1 : 0))));
+        return cube0 + (x != 0 ? 1u : 0u) + (y != 0 ? csy : 0u) + (z != 0 ? csz : 0u);
     }
     __device__ __forceinline__ void pair(int lo, int hi) {  // gradient.cpp:162-174
         const int diff = hi - lo;  // +-1, +-3 or +-9
@@ -520,6 +527,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             w.parent0 = parent0;
             w.parent3 = parent3;
             w.ncrit = 0;
+            w.init_cubes();
             return true;
         };
         // ---- phase 1, own vertex of each tile: star mask; trivial stars finished here;
@@ -669,6 +677,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
         w.parent0 = parent0;
         w.parent3 = parent3;
         w.ncrit = 0;
+        w.init_cubes();
         const T* centre = f + vi;
         const std::int64_t sy = d.nx, sz = d.nx * d.ny;
         auto val = [&](int t) {
@@ -749,6 +758,7 @@ k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ 
         w.parent0 = parent0;
         w.parent3 = parent3;
         w.ncrit = 0;
+        w.init_cubes();
         auto val = [&](int t) {
             const std::int64_t ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
             return f[(w.vx + ox) + d.nx * ((w.vy + oy) + d.ny * (w.vz + oz))];
