@@ -637,11 +637,14 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ MaskT<K> s_M[27 * 128];
     __shared__ unsigned long long s_crit[4];
+    __shared__ long long s_voff[27];  // sample offset of slot t from the star's vertex
     if (threadIdx.x < 27) {
         s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
         s_cof[threadIdx.x] = c_slot.cofacet[threadIdx.x];
         s_cell[threadIdx.x] = static_cast<std::int32_t>(
             c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
+        s_voff[threadIdx.x] = c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.nx +
+                              c_slot.off[threadIdx.x][2] * d.nx * d.ny;
     }
     if (threadIdx.x < 4) s_crit[threadIdx.x] = 0;
     __syncthreads();
@@ -680,10 +683,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
         w.init_cubes();
         const T* centre = f + vi;
         const std::int64_t sy = d.nx, sz = d.nx * d.ny;
-        auto val = [&](int t) {
-            const int z = (t * 57) >> 9, rr = t - 9 * z, y = (rr * 11) >> 5, x = rr - 3 * y;
-            return centre[(x - 1) + (y - 1) * sy + (z - 1) * sz];
-        };
+        auto val = [&](int t) { return centre[s_voff[t]]; };
         std::uint32_t S;
         if (K == 16) {
             S = lists.mask[which][i];  // from the tile kernel
