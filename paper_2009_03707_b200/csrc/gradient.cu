@@ -223,12 +223,24 @@ template <typename ArgMin>
 __device__ __forceinline__ void robins(std::uint32_t S, const std::uint32_t* fac, const std::uint32_t* cof,
                                        ArgMin argmin, StarWriter& w) {
     std::uint32_t assigned = 0, q0 = 0, q1 = 0;
+    // Bit-parallel unassigned-facet counts: a star cell's facets (those containing the
+    // vertex) are its neighbours towards the centre along its non-centre coordinates,
+    // so "facet along x unassigned" for all cells at once is a shift of the unassigned
+    // mask by one slot (3 for y, 9 for z) under the masks of slots with x = 0 / x = 2.
+    auto one_unassigned = [&](std::uint32_t U) {
+        constexpr std::uint32_t X0 = 0x1249249u, X2 = X0 << 2;      // slots with x = 0 / 2
+        constexpr std::uint32_t Y0 = 0x01c0e07u, Y2 = Y0 << 6;      // y = 0 / 2
+        constexpr std::uint32_t Z0 = 0x00001ffu, Z2 = Z0 << 18;     // z = 0 / 2
+        const std::uint32_t ux = ((U >> 1) & X0) | ((U << 1) & X2);
+        const std::uint32_t uy = ((U >> 3) & Y0) | ((U << 3) & Y2);
+        const std::uint32_t uz = ((U >> 9) & Z0) | ((U << 9) & Z2);
+        return (ux ^ uy ^ uz) & ~(ux & uy & uz);  // exactly one unassigned facet
+    };
+    // (gradient.cpp:208-218: the in-star cofacets of t whose unassigned-facet count
+    // drops to 1 join q1)
     auto settle = [&](int t) {
         assigned |= 1u << t;
-        for (std::uint32_t m = cof[t] & S & ~assigned; m; m &= m - 1) {
-            const int c = __ffs(m) - 1;
-            if (__popc(fac[c] & ~assigned) == 1) q1 |= 1u << c;
-        }
+        q1 |= cof[t] & S & ~assigned & one_unassigned(S & ~assigned);
     };
     const std::uint32_t edges = S & kDim1;
     const int delta = argmin(edges);
