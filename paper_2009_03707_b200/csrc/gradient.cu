@@ -33,6 +33,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sortnet.cuh"
 
 namespace msc3d_dev {
 
@@ -323,16 +324,11 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
             key[p] = static_cast<KT>(~static_cast<KT>(0));
         }
     }
-    // (1) vertices by value: bitonic network
-#pragma unroll
-    for (int k = 2; k <= K; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                const int l = i ^ j;
-                if (l > i) ce_pair(key[i], slot[i], key[l], slot[l], (i & k) == 0);
-            }
+    // (1) vertices by value: Batcher odd-even merge sort with explicit comparator lists
+    //     (sortnet.cuh; 19 / 63 / 156 comparators for 8 / 16 / <= 27 vertices, against
+    //     24 / 80 / 240 for bitonic networks of 8 / 16 / 32)
+    SortNet<(K > 27 ? 27 : K)>::run(
+        [&](int a, int b) { ce_pair(key[a], slot[a], key[b], slot[b], true); });
     bool tie = false;
 #pragma unroll
     for (int p = 0; p + 1 < K; ++p)
