@@ -420,12 +420,13 @@ __global__ void __launch_bounds__(kThreads)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
        uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
        uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
-       unsigned long long* __restrict__ n_predone) {
+       unsigned long long* __restrict__ n_predone,
+       std::uint32_t* __restrict__ fwd, unsigned int* __restrict__ ptbits) {
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < n;
          base += stride) {
         const std::uint64_t i = base + (threadIdx.x & 31);
-        bool pre = false;
+        bool pre = false, pt = false;
         if (i < n) {
             std::uint32_t de0;
             if (jlist) {
@@ -494,12 +495,26 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                 }
             }
             pending[i] = pre ? kDone : pend;
+            if (fwd) {  // pass-through: one live branch, ending at a junction (P(j) = P(child))
+                int live = 0;
+                std::uint32_t child = kNone;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if (dd[b] == kNone) continue;
+                    ++live;
+                    if (!(dd[b] & kTerm)) child = dd[b];
+                }
+                pt = live == 1 && child != kNone;
+                fwd[i] = pt ? child : static_cast<std::uint32_t>(i);
+            }
         }
         const unsigned bits = __ballot_sync(0xffffffffu, pre);
+        const unsigned ptb = __ballot_sync(0xffffffffu, pt);
         if ((threadIdx.x & 31) == 0 && predone) {
             predone[base >> 5] = bits;
             if (bits) atomicAdd(n_predone, static_cast<unsigned long long>(__popc(bits)));
         }
+        if ((threadIdx.x & 31) == 0 && ptbits) ptbits[base >> 5] = ptb;
     }
 }
 
@@ -1551,18 +1566,18 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
-                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, cudaStream_t s,
-                int num_sms) {
+                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
+                unsigned int* ptbits, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
     WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
     auto* nr = static_cast<uint4*>(node);  // the nodes' destination records
     auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)
         k_walk<std::uint32_t><<<grid_full(n), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone);
+            c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone, fwd, ptbits);
     else
         k_walk<std::uint64_t><<<grid_full(n), kThreads, 0, s>>>(
-            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone);
+            c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone, fwd, ptbits);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

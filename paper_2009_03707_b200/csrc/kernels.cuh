@@ -226,7 +226,8 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
-                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, cudaStream_t s,
+                std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
+                unsigned int* ptbits, cudaStream_t s,
                 int num_sms);
 int node_rec_bytes();
 int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,

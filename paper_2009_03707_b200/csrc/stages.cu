@@ -339,16 +339,17 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     if (!predone) return MSC3D_ERR_NOMEM;
     auto* n_predone = reinterpret_cast<unsigned long long*>(ctx->d_small + 30);
     MSC3D_CUDA_TRY(cudaMemsetAsync(n_predone, 0, 8, s));
+    // (the junction walks also flag the pass-through junctions: fwd, ptbits)
+    auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
+    if (!ptbits) return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
-                               predone, n_predone, s, sms));
+                               predone, n_predone, fwd, ptbits, s, sms));
     TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, src_ids, w, n1,
-                               jdest + nj * 16, pending + nj, flags, nullptr, slen, nullptr, nullptr, s,
+                               jdest + nj * 16, pending + nj, flags, nullptr, slen, nullptr, nullptr, nullptr, nullptr, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
     // contracted away by pointer jumping
-    auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
-    if (!ptbits) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_passthrough(jdest, nj, fwd, ptbits, s, sms));
+
     {  // pointer jumping to the end of pass-through chains, all rounds in one launch
         auto* jflags = reinterpret_cast<unsigned int*>(ctx->d_small + 23);
         auto* jrounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 25);
