@@ -286,17 +286,19 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
                 const std::uint32_t node = __ldcg(cur + j);
                 const std::uint32_t s = succ[node];
                 const EdgeRef e(node);
+                // claims by atomic test-and-set, the (<= 4) atomics issued back to back
+                unsigned old[4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const std::uint32_t f = (s >> (3 * p)) & 7u;
+                    old[p] = ~0u;
                     if (f < 2) continue;
                     de[p] = succ_edge(e, node, p, f, g);
-                    const unsigned bit = 1u << (de[p] & 31);
-                    unsigned int* w = &bitmap[de[p] >> 5];
-                    if (*w & bit) continue;  // bits only ever go 0 -> 1
-                    if (atomicOr(w, bit) & bit) continue;
-                    won |= 1u << p;
+                    old[p] = atomicOr(&bitmap[de[p] >> 5], 1u << (de[p] & 31));
                 }
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    if (!((old[p] >> (de[p] & 31)) & 1u)) won |= 1u << p;
             }
             mine += __popc(won);
             warp_push(wq, de, won, nxt, next_cnt);
