@@ -58,3 +58,52 @@ def test_cli_compute_matches_reference(tmp_path, ref):
     assert "check: gradient ok, euler ok, boundary ok" in r.stderr
     r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--out", tmp_path / "c.json")
     assert r.returncode == 0 and (tmp_path / "c.json").stat().st_size > 0
+
+
+@pytest.mark.gpu
+def test_cli_large_complex_matches_device(tmp_path):
+    """A complex large enough that the drop-in compute() takes its parallel host path
+    (result vectors >= 64 MB: reserved, huge-page advised, pre-faulted from several
+    threads; critical point values from the device): everything equals the device
+    pipeline's own outputs, and each value is the sample at the cell's max vertex."""
+    dims = (144, 144, 144)
+    v = m.synth("gnoise", dims)
+    raw = tmp_path / "v.raw"
+    v.astype("<f4").tofile(raw)
+    pre = tmp_path / "out"
+    r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--format", "csv", "--out", pre,
+            "--labels", tmp_path / "lab")
+    assert r.returncode == 0, r.stderr
+    want = m.compute(v, dims, with_segmentation=True)
+    cps = np.loadtxt(f"{pre}_critical_points.csv", delimiter=",", skiprows=1, ndmin=2)
+    assert len(cps) > 1_200_000  # >= 64 MB of CriticalPoint records
+    np.testing.assert_array_equal(cps[:, 0].astype(np.int64), np.arange(len(cps)))
+    np.testing.assert_array_equal(cps[:, 1].astype(np.uint64), np.asarray(want.cp_cell, dtype=np.uint64))
+    np.testing.assert_array_equal(cps[:, 2].astype(np.uint8), np.asarray(want.cp_index, dtype=np.uint8))
+    # doubled coordinates and values, from the cell ids
+    nx, ny, nz = dims
+    ex, ey = 2 * nx - 1, 2 * ny - 1
+    cell = np.asarray(want.cp_cell, dtype=np.int64)
+    x, y, z = cell % ex, (cell // ex) % ey, cell // (ex * ey)
+    np.testing.assert_array_equal(cps[:, 3:6].astype(np.int64), np.stack([x, y, z], axis=1))
+    vol = v.reshape(nz, ny, nx).astype(np.float64)
+    best = np.full(len(cell), -np.inf)
+    bid = np.full(len(cell), -1, dtype=np.int64)
+    for oz in (0, 1):
+        for oy in (0, 1):
+            for ox in (0, 1):
+                ok = ((ox == 0) | (x % 2 == 1)) & ((oy == 0) | (y % 2 == 1)) & ((oz == 0) | (z % 2 == 1))
+                vx, vy, vz = x // 2 + ox, y // 2 + oy, z // 2 + oz
+                vid = vx + nx * (vy + ny * vz)
+                val = np.where(ok, vol[np.minimum(vz, nz - 1), np.minimum(vy, ny - 1), np.minimum(vx, nx - 1)], -np.inf)
+                take = ok & ((val > best) | ((val == best) & (vid > bid)))
+                best = np.where(take, val, best)
+                bid = np.where(take, vid, bid)
+    np.testing.assert_array_equal(cps[:, 9], best)
+    arcs = np.loadtxt(f"{pre}_arcs.csv", delimiter=",", skiprows=1, ndmin=2, dtype=np.uint64)
+    assert arcs.shape[0] * 16 >= 64 << 20
+    np.testing.assert_array_equal(arcs[:, 0], np.asarray(want.arc_src, dtype=np.uint64))
+    np.testing.assert_array_equal(arcs[:, 1], np.asarray(want.arc_dst, dtype=np.uint64))
+    np.testing.assert_array_equal(arcs[:, 2], np.asarray(want.arc_mult, dtype=np.uint64))
+    np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_min.raw", dtype="<u4"), want.labels_min)
+    np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_max.raw", dtype="<u4"), want.labels_max)
