@@ -119,7 +119,7 @@ __device__ __forceinline__ std::uint32_t term_quad(const EdgeRef& e, int p, cons
 // ---------------------------------------------------------------------------------
 // successor table
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 16)
 k_succ_table(const std::uint8_t* __restrict__ codes, Dims d, std::uint16_t* __restrict__ succ) {
     const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
     const std::int64_t step[3] = {1, d.ex, d.exy};
