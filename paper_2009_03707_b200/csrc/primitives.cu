@@ -67,8 +67,11 @@ k_scan_u32(const std::uint32_t* __restrict__ in, std::uint64_t n, std::uint64_t*
            unsigned long long* status, std::uint32_t* ticket, std::uint64_t* total) {
     __shared__ std::uint64_t sm[40];
     __shared__ std::uint32_t s_tile;
-    __shared__ std::uint64_t s_buf[kTile];  // 32 KB: u32 inputs (first half), then u64 outputs
+    // shared staging with one pad word per 32 (conflict-free blocked and striped access)
+    constexpr int kPad = kTile + kTile / 32;
+    __shared__ std::uint64_t s_buf[kPad];  // u32 inputs (first half), then u64 outputs
     auto* s_in = reinterpret_cast<std::uint32_t*>(s_buf);
+    auto pad = [](int i) { return i + (i >> 5); };
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const std::uint32_t tile = s_tile;
@@ -76,39 +79,30 @@ k_scan_u32(const std::uint32_t* __restrict__ in, std::uint64_t n, std::uint64_t*
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         const std::uint64_t i = base + static_cast<std::uint64_t>(k) * kThreads + threadIdx.x;
-        s_in[k * kThreads + threadIdx.x] = i < n ? in[i] : 0u;
+        s_in[pad(k * kThreads + threadIdx.x)] = i < n ? in[i] : 0u;
     }
     __syncthreads();
     std::uint32_t v[kItems];
     std::uint64_t sum = 0;
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        // rotated index: consecutive threads hit different banks
-        const int kk = (k + threadIdx.x) & (kItems - 1);
-        v[kk] = s_in[threadIdx.x * kItems + kk];
+        v[k] = s_in[pad(threadIdx.x * kItems + k)];
+        sum += v[k];
     }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) sum += v[k];
     std::uint64_t block_total;
     const std::uint64_t excl = block_excl_scan(sum, &block_total, sm);  // (ends with a barrier)
     const std::uint64_t prefix = tile_lookback1(status, tile, block_total, sm + 34);
     std::uint64_t at = prefix + excl;
-    std::uint64_t r[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        r[k] = at;
+        s_buf[pad(threadIdx.x * kItems + k)] = at;
         at += v[k];
-    }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-        const int kk = (k + threadIdx.x) & (kItems - 1);
-        s_buf[threadIdx.x * kItems + kk] = r[kk];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         const std::uint64_t i = base + static_cast<std::uint64_t>(k) * kThreads + threadIdx.x;
-        if (i < n) out[i] = s_buf[k * kThreads + threadIdx.x];
+        if (i < n) out[i] = s_buf[pad(k * kThreads + threadIdx.x)];
     }
     const std::uint64_t ntiles = (n + kTile - 1) / kTile;
     if (tile == ntiles - 1 && threadIdx.x == 0 && total) *total = prefix + block_total;
