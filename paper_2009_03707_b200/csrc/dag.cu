@@ -1260,13 +1260,13 @@ __device__ __forceinline__ void heavy_pass(const CountArgs& a, WarpBuf wb, WarpQ
 }
 
 // Round 0: every node without pending children, in index order; then the frontiers.
-// Two configurations of one kernel: kWide (high occupancy: 3 blocks/SM, 512-entry
+// Two configurations of one kernel: kWide (3 blocks/SM, 384-entry
 // warp buffers) runs the big early rounds, which are latency-bound and have no long
 // inputs; it stops once the frontier falls below a.switch_below and leaves the state
 // (round, frontier buffer, size) in a.resume.  The default configuration (2 blocks/SM,
 // 1024-entry buffers for the long vectors of the tail) resumes from there.
 template <bool kWide>
-__global__ void __launch_bounds__(kThreads, kWide ? 4 : 2) k_count(CountArgs a) {
+__global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const WarpBuf wb = warp_buf(s_dyn, kWide ? kWarpCapWide : kWarpCap);
     __shared__ WarpQ s_q[kThreads / 32];
