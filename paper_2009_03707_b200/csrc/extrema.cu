@@ -119,7 +119,7 @@ __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std
                 std::uint32_t nl = p[l];
                 if (nl != l) {
 #pragma unroll
-                    for (int s = 0; s < 3; ++s) {
+                    for (int s = 0; s < 15; ++s) {
                         const std::uint32_t nn = p[nl];
                         if (nn == nl) {
                             now = true;
