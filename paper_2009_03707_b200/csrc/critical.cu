@@ -227,6 +227,118 @@ k_compact_crit(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, Id
     }
 }
 
+// Three 64-cell chunks per thread (49152-cell tiles: per-category tile counts still fit
+// 16 bits; a thread's chunks are consecutive, so thread order is cell order) amortise
+// the look-back; the tile's ids are staged in shared memory and
+// leave as contiguous runs per category (coalesced), unless the tile holds more than
+// kStage of them (then direct per-thread writes, as in k_compact_crit).
+constexpr int kSub = 3;
+constexpr int kStageBytes = 32768;
+template <typename IdT>
+__global__ void __launch_bounds__(kThreads)
+k_compact_crit3(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, IdT* out0, IdT* out1, IdT* out2,
+                IdT* out3, std::uint64_t* totals) {
+    static_assert(kPerThread == 64, "one 64-bit mask per thread and sub-tile");
+    __shared__ std::uint64_t sm[40];
+    __shared__ std::uint32_t s_tile;
+    constexpr int kStage = kStageBytes / static_cast<int>(sizeof(IdT));
+    __shared__ IdT s_ids[kStage];
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const std::uint32_t tile = s_tile;
+    std::uint64_t M[kSub][4];
+    std::uint64_t packed = 0;
+#pragma unroll
+    for (int sb = 0; sb < kSub; ++sb) {
+        const std::uint64_t first = static_cast<std::uint64_t>(tile) * kSub * kTile +
+                                    (static_cast<std::uint64_t>(threadIdx.x) * kSub + sb) * kPerThread;
+        std::uint64_t crit = 0;
+        if (first + kPerThread <= d.n_cells) {
+#pragma unroll
+            for (int q = 0; q < kChunks; ++q) {
+                const uint4 w = __ldcs(reinterpret_cast<const uint4*>(codes + first + 16 * q));
+                const std::uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const std::uint32_t m = __vcmpeq4(ws[e], 0x01010101u);  // kCritical bytes -> 0xff
+                    const std::uint64_t b4 = ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+                    crit |= b4 << (16 * q + 4 * e);
+                }
+            }
+        } else {
+            for (int k = 0; k < kPerThread; ++k)
+                if (first + k < d.n_cells && codes[first + k] == kCritical) crit |= 1ull << k;
+        }
+        const Coord p = unpack(d, first < d.n_cells ? first : 0);
+        const std::uint64_t lenA = min(static_cast<std::uint64_t>(kPerThread), static_cast<std::uint64_t>(d.ex - p.x));
+        const std::uint64_t segA = lenA >= 64 ? ~0ull : ((1ull << lenA) - 1);
+        constexpr std::uint64_t kAlt = 0xAAAAAAAAAAAAAAAAull;  // odd k
+        const std::uint64_t oddA = (p.x & 1) ? ~kAlt : kAlt;
+        const std::uint64_t oddB = (lenA & 1) ? ~kAlt : kAlt;
+        std::int64_t yB = p.y + 1, zB = p.z;
+        if (yB == d.ey) {
+            yB = 0;
+            ++zB;
+        }
+        const int rA = static_cast<int>((p.y & 1) + (p.z & 1));
+        const int rB = static_cast<int>((yB & 1) + (zB & 1));
+        const std::uint64_t cA = crit & segA, cB = crit & ~segA;
+#pragma unroll
+        for (int dm = 0; dm < 4; ++dm) {
+            M[sb][dm] = (rA == dm ? (cA & ~oddA) : 0ull) | (rA + 1 == dm ? (cA & oddA) : 0ull) |
+                        (rB == dm ? (cB & ~oddB) : 0ull) | (rB + 1 == dm ? (cB & oddB) : 0ull);
+            packed += static_cast<std::uint64_t>(__popcll(M[sb][dm])) << (16 * dm);
+        }
+    }
+    std::uint64_t block_total;
+    const std::uint64_t excl = block_excl_scan(packed, &block_total, sm);
+    std::uint64_t tot[4];
+    for (int k = 0; k < 4; ++k) tot[k] = unpack16(block_total, k);
+    tile_lookback4(st, tile, tot, sm + 34);
+    IdT* outs[4] = {out0, out1, out2, out3};
+    const std::uint64_t ttot = tot[0] + tot[1] + tot[2] + tot[3];
+    if (ttot <= static_cast<std::uint64_t>(kStage)) {
+        // tile-local positions: categories one after another
+        std::uint64_t cbase = 0;
+#pragma unroll
+        for (int dm = 0; dm < 4; ++dm) {
+            std::uint64_t at = cbase + unpack16(excl, dm);
+#pragma unroll
+            for (int sb = 0; sb < kSub; ++sb) {
+                const std::uint64_t first = static_cast<std::uint64_t>(tile) * kSub * kTile +
+                                            (static_cast<std::uint64_t>(threadIdx.x) * kSub + sb) * kPerThread;
+                for (std::uint64_t m = M[sb][dm]; m; m &= m - 1)
+                    s_ids[at++] = static_cast<IdT>(first + __ffsll(m) - 1);
+            }
+            cbase += tot[dm];
+        }
+        __syncthreads();
+        cbase = 0;
+#pragma unroll
+        for (int dm = 0; dm < 4; ++dm) {
+            IdT* dst = outs[dm] + sm[34 + dm];
+            for (std::uint64_t j = threadIdx.x; j < tot[dm]; j += kThreads) dst[j] = s_ids[cbase + j];
+            cbase += tot[dm];
+        }
+    } else {
+#pragma unroll
+        for (int dm = 0; dm < 4; ++dm) {
+            std::uint64_t at = sm[34 + dm] + unpack16(excl, dm);
+#pragma unroll
+            for (int sb = 0; sb < kSub; ++sb) {
+                const std::uint64_t first = static_cast<std::uint64_t>(tile) * kSub * kTile +
+                                            (static_cast<std::uint64_t>(threadIdx.x) * kSub + sb) * kPerThread;
+                for (std::uint64_t m = M[sb][dm]; m; m &= m - 1)
+                    outs[dm][at++] = static_cast<IdT>(first + __ffsll(m) - 1);
+            }
+        }
+    }
+    const std::uint32_t ntiles = static_cast<std::uint32_t>((d.n_cells + kSub * kTile - 1) / (kSub * kTile));
+    if (tile == ntiles - 1 && threadIdx.x == 0 && totals) {
+        for (int k = 0; k < 4; ++k) totals[k] = sm[34 + k] + tot[k];
+    }
+}
+
 // Count-only pass: totals per dimension with block reduction + one atomic per block.
 template <typename Pred>
 __global__ void __launch_bounds__(kThreads)
@@ -364,7 +476,7 @@ int launch_critical_compact(const std::uint8_t* codes, const Dims& d, Workspace&
                             cudaStream_t s) {
     if (d.ex < 64 || !outs[0] || !outs[1] || !outs[2] || !outs[3] || d.n_cells == 0)
         return compact_impl(codes, d, CritPred{}, ws, outs, id_width, d_totals, s);
-    const std::uint64_t ntiles = (d.n_cells + kTile - 1) / kTile;
+    const std::uint64_t ntiles = (d.n_cells + kSub * kTile - 1) / (kSub * kTile);
     char* buf = static_cast<char*>(ws.get(ntiles * 68 + 16));
     if (!buf) return MSC3D_ERR_NOMEM;
     TileStatus st;
@@ -374,11 +486,11 @@ int launch_critical_compact(const std::uint8_t* codes, const Dims& d, Workspace&
     st.ticket = st.flag + ntiles;
     MSC3D_CUDA_TRY(cudaMemsetAsync(st.flag, 0, (ntiles + 1) * 4, s));
     if (id_width == 4)
-        k_compact_crit<std::uint32_t><<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(
+        k_compact_crit3<std::uint32_t><<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(
             codes, d, st, static_cast<std::uint32_t*>(outs[0]), static_cast<std::uint32_t*>(outs[1]),
             static_cast<std::uint32_t*>(outs[2]), static_cast<std::uint32_t*>(outs[3]), d_totals);
     else
-        k_compact_crit<std::uint64_t><<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(
+        k_compact_crit3<std::uint64_t><<<static_cast<unsigned>(ntiles), kThreads, 0, s>>>(
             codes, d, st, static_cast<std::uint64_t*>(outs[0]), static_cast<std::uint64_t*>(outs[1]),
             static_cast<std::uint64_t*>(outs[2]), static_cast<std::uint64_t*>(outs[3]), d_totals);
     count_launch();
