@@ -50,7 +50,7 @@ __global__ void k_cp_concat(const IdT* __restrict__ src, std::uint64_t n, std::u
 // Emits (min id, saddle id, mult) into two slots; counts per minimum.
 template <typename IdT>
 __global__ void k_arcs_min(const IdT* __restrict__ crit1, std::uint64_t n1, Dims d,
-                           const std::uint32_t* __restrict__ label0, const std::uint32_t* __restrict__ remap0,
+                           const std::uint32_t* __restrict__ label0, RankRemap remap0,
                            std::uint32_t base1, std::uint32_t* __restrict__ slot_min,
                            std::uint32_t* __restrict__ per_min) {
     GRID_STRIDE(k, n1) {
@@ -60,8 +60,8 @@ __global__ void k_arcs_min(const IdT* __restrict__ crit1, std::uint64_t n1, Dims
         if (axis == 0) { lo.x -= 1; hi.x += 1; }
         else if (axis == 1) { lo.y -= 1; hi.y += 1; }
         else { lo.z -= 1; hi.z += 1; }
-        const std::uint32_t a = remap0[label0[vertex_dense(d, lo)]];
-        const std::uint32_t b = remap0[label0[vertex_dense(d, hi)]];
+        const std::uint32_t a = remap0(label0[vertex_dense(d, lo)]);
+        const std::uint32_t b = remap0(label0[vertex_dense(d, hi)]);
         if (a == b) {
             slot_min[2 * k] = a;
             slot_min[2 * k + 1] = kNoLabel;
@@ -220,7 +220,7 @@ __global__ void k_arcs_min_emit(const std::uint64_t* __restrict__ off, std::uint
 // Block C: per 2-saddle k (cp id base2 + k), its maxima via the cube labels.
 template <typename IdT>
 __global__ void k_arcs_max(const IdT* __restrict__ crit2, std::uint64_t n2, Dims d,
-                           const std::uint32_t* __restrict__ label3, const std::uint32_t* __restrict__ remap3,
+                           const std::uint32_t* __restrict__ label3, RankRemap remap3,
                            std::uint32_t* __restrict__ slot, std::uint32_t* __restrict__ cnt) {
     GRID_STRIDE(k, n2) {
         const Coord c = unpack(d, crit2[k]);
@@ -236,7 +236,7 @@ __global__ void k_arcs_max(const IdT* __restrict__ crit2, std::uint64_t n2, Dims
             if (axis == 0) o.x = nc;
             else if (axis == 1) o.y = nc;
             else o.z = nc;
-            got[ng++] = remap3[label3[cube_dense(d, o)]];
+            got[ng++] = remap3(label3[cube_dense(d, o)]);
         }
         const std::uint32_t a = got[0], b = got[1];
         std::uint32_t n = 0;
@@ -363,7 +363,7 @@ int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int ind
 }
 
 int launch_arcs_min(const void* crit1, std::uint64_t n1, int id_width, const Dims& d,
-                    const std::uint32_t* label0, const std::uint32_t* remap0, std::uint32_t base1,
+                    const std::uint32_t* label0, RankRemap remap0, std::uint32_t base1,
                     std::uint32_t* slot_min, std::uint32_t* per_min, cudaStream_t s, int num_sms) {
     if (n1 == 0) return MSC3D_OK;
     if (id_width == 4)
@@ -434,7 +434,7 @@ int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t
 }
 
 int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
-                    const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
+                    const std::uint32_t* label3, RankRemap remap3, std::uint32_t* slot,
                     std::uint32_t* cnt, cudaStream_t s, int num_sms) {
     if (n2 == 0) return MSC3D_OK;
     if (id_width == 4)

@@ -158,4 +158,18 @@ __device__ __forceinline__ int edge_successor_count(const std::uint8_t* __restri
     }
     return n;
 }
+// Dense vertex/cube index -> critical point id through a bitmap of the critical
+// extrema with one rank word per 32 entries (uint2 {rank of the word's first entry,
+// bits}: 8 bytes per 32 vertices, L2-resident) instead of a 4-byte-per-entry id map
+// gathered at random.  kNoLabel for entries whose bit is clear (non-critical roots).
+struct RankRemap {
+    const uint2* r;
+    std::uint32_t base;
+    __device__ __forceinline__ std::uint32_t operator()(std::uint32_t x) const {
+        const uint2 w = r[x >> 5];
+        const std::uint32_t b = 1u << (x & 31);
+        return (w.y & b) ? base + w.x + static_cast<std::uint32_t>(__popc(w.y & (b - 1u))) : kNoLabel;
+    }
+};
+
 }  // namespace msc3d_dev

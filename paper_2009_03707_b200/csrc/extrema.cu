@@ -176,9 +176,28 @@ __global__ void k_scatter_remap(const IdT* __restrict__ crit, std::uint64_t n, D
     }
 }
 
-__global__ void k_gather(const std::uint32_t* __restrict__ label, const std::uint32_t* __restrict__ remap,
-                         std::uint64_t n, std::uint32_t* __restrict__ out) {
-    GRID_STRIDE(i, n) out[i] = remap[label[i]];
+__global__ void k_gather(const std::uint32_t* __restrict__ label, RankRemap remap, std::uint64_t n,
+                         std::uint32_t* __restrict__ out) {
+    GRID_STRIDE(i, n) out[i] = remap(label[i]);
+}
+
+// bit of dense(crit[k]) in a zeroed bitmap
+template <typename IdT>
+__global__ void k_mark_bits(const IdT* __restrict__ crit, std::uint64_t n, Dims d, int dim,
+                            unsigned int* __restrict__ bits) {
+    GRID_STRIDE(k, n) {
+        const Coord c = unpack(d, crit[k]);
+        const std::uint32_t di = dim == 0 ? vertex_dense(d, c) : cube_dense(d, c);
+        atomicOr(&bits[di >> 5], 1u << (di & 31));
+    }
+}
+__global__ void k_word_popc(const unsigned int* __restrict__ bits, std::uint64_t nwords,
+                            std::uint32_t* __restrict__ cnt) {
+    GRID_STRIDE(w, nwords) cnt[w] = static_cast<std::uint32_t>(__popc(bits[w]));
+}
+__global__ void k_pack_rank(const unsigned int* __restrict__ bits, const std::uint64_t* __restrict__ pre,
+                            std::uint64_t nwords, uint2* __restrict__ rank) {
+    GRID_STRIDE(w, nwords) rank[w] = make_uint2(static_cast<std::uint32_t>(pre[w]), bits[w]);
 }
 
 // API saddle_extremum_arcs: per merged saddle, the two endpoint slots as cells.
@@ -302,6 +321,30 @@ int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, 
     return MSC3D_OK;
 }
 
+int launch_rank_map(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
+                    unsigned int* bits, std::uint32_t* cnt, std::uint64_t* pre, void* rank, std::uint64_t nwords,
+                    Workspace& ws, std::uint64_t* d_total, cudaStream_t s, int num_sms) {
+    if (nwords == 0) return MSC3D_OK;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(bits, 0, nwords * 4, s));
+    if (n) {
+        if (id_width == 4)
+            k_mark_bits<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+                static_cast<const std::uint32_t*>(crit), n, d, dim, bits);
+        else
+            k_mark_bits<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
+                static_cast<const std::uint64_t*>(crit), n, d, dim, bits);
+        count_launch();
+    }
+    k_word_popc<<<grid_for(nwords, num_sms), kThreads, 0, s>>>(bits, nwords, cnt);
+    count_launch();
+    int rc = scan_u32(cnt, nwords, pre, d_total, ws, s);
+    if (rc != MSC3D_OK) return rc;
+    k_pack_rank<<<grid_for(nwords, num_sms), kThreads, 0, s>>>(bits, pre, nwords, static_cast<uint2*>(rank));
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
 int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
                          std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
@@ -316,7 +359,7 @@ int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const 
     return MSC3D_OK;
 }
 
-int launch_gather(const std::uint32_t* label, const std::uint32_t* remap, std::uint64_t n,
+int launch_gather(const std::uint32_t* label, RankRemap remap, std::uint64_t n,
                   std::uint32_t* out, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
     k_gather<<<grid_for(n, num_sms), kThreads, 0, s>>>(label, remap, n, out);

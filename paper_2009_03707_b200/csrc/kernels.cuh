@@ -96,7 +96,12 @@ int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std:
                     unsigned long long* rounds, cudaStream_t s, int num_sms);
 int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
                          std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms);
-int launch_gather(const std::uint32_t* label, const std::uint32_t* remap, std::uint64_t n,
+// rank: nwords uint2 {rank of the word's first set bit, bits} over dense(crit[k]);
+// bits / cnt / pre: nwords scratch (u32, u32, u64)
+int launch_rank_map(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
+                    unsigned int* bits, std::uint32_t* cnt, std::uint64_t* pre, void* rank, std::uint64_t nwords,
+                    Workspace& ws, std::uint64_t* d_total, cudaStream_t s, int num_sms);
+int launch_gather(const std::uint32_t* label, RankRemap remap, std::uint64_t n,
                   std::uint32_t* out, cudaStream_t s, int num_sms);
 int launch_se_slots(const std::uint8_t* codes, const Dims& d, const void* saddles,
                     std::uint64_t ns, int id_width, const std::uint32_t* l0,
@@ -160,7 +165,7 @@ int launch_cp_values(const void* cells, int id_width, std::uint64_t n, const Dim
 int launch_cp_concat(const void* src, std::uint64_t n, std::uint64_t at, int index, int id_width,
                      void* cp_cell, std::uint8_t* cp_index, cudaStream_t s, int num_sms);
 int launch_arcs_min(const void* crit1, std::uint64_t n1, int id_width, const Dims& d,
-                    const std::uint32_t* label0, const std::uint32_t* remap0, std::uint32_t base1,
+                    const std::uint32_t* label0, RankRemap remap0, std::uint32_t base1,
                     std::uint32_t* slot_min, std::uint32_t* per_min, cudaStream_t s, int num_sms);
 int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::uint32_t base1,
                          const std::uint64_t* off, std::uint64_t n0, std::uint64_t total,
@@ -172,7 +177,7 @@ int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t
                        std::uint64_t* key, std::uint64_t* scratch, std::uint32_t* large,
                        unsigned long long* n_large, std::uint64_t* h_small, cudaStream_t s, int num_sms);
 int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
-                    const std::uint32_t* label3, const std::uint32_t* remap3, std::uint32_t* slot,
+                    const std::uint32_t* label3, RankRemap remap3, std::uint32_t* slot,
                     std::uint32_t* cnt, cudaStream_t s, int num_sms);
 int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint32_t base2,
                          const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,

@@ -639,12 +639,25 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     }
     auto* label0 = ctx->ptr<std::uint32_t>("parent0");
     auto* label3 = ctx->ptr<std::uint32_t>("parent3");
-    auto* remap0 = static_cast<std::uint32_t*>(ctx->ensure("remap0", d.n_verts, 4));
-    auto* remap3 = static_cast<std::uint32_t*>(ctx->ensure("remap3", std::max<std::uint64_t>(1, d.n_cubes), 4));
-    if (!remap0 || !remap3) return MSC3D_ERR_NOMEM;
-    if (d.n_cubes) MSC3D_CUDA_TRY(cudaMemsetAsync(remap3, 0xff, d.n_cubes * 4, s));
-    TRY(msc3d_dev::launch_scatter_remap(ctx->ptr<void>("crit0"), c0, w, d, 0, 0, remap0, s, sms));
-    TRY(msc3d_dev::launch_scatter_remap(ctx->ptr<void>("crit3"), c3, w, d, 3, base3, remap3, s, sms));
+    // cp ids of the minima / maxima: bitmaps of the critical vertices / cubes with a
+    // rank word per 32 entries (L2-resident) instead of full-size id maps
+    msc3d_dev::RankRemap remap0{}, remap3{};
+    {
+        const std::uint64_t nw0 = d.n_verts / 32 + 1, nw3 = d.n_cubes / 32 + 1;
+        const std::uint64_t nw = std::max(nw0, nw3);
+        auto* bits = static_cast<unsigned int*>(ctx->ensure("rank_bits", nw, 4));
+        auto* cnt = static_cast<std::uint32_t*>(ctx->ensure("rank_cnt", nw, 4));
+        auto* pre = static_cast<std::uint64_t*>(ctx->ensure("rank_pre", nw, 8));
+        auto* r0 = ctx->ensure("rank0", nw0, 8);
+        auto* r3 = ctx->ensure("rank3", nw3, 8);
+        if (!bits || !cnt || !pre || !r0 || !r3) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_rank_map(ctx->ptr<void>("crit0"), c0, w, d, 0, bits, cnt, pre, r0, nw0, ctx->ws,
+                                       ctx->d_small + 38, s, sms));
+        TRY(msc3d_dev::launch_rank_map(ctx->ptr<void>("crit3"), c3, w, d, 3, bits, cnt, pre, r3, nw3, ctx->ws,
+                                       ctx->d_small + 38, s, sms));
+        remap0 = msc3d_dev::RankRemap{static_cast<const uint2*>(r0), 0u};
+        remap3 = msc3d_dev::RankRemap{static_cast<const uint2*>(r3), static_cast<std::uint32_t>(base3)};
+    }
     // block A (min -> 1s) slots + per-minimum counts; block C (2s -> max) slots
     auto* slot_min = static_cast<std::uint32_t*>(ctx->ensure("slot_min", 2 * c1, 4));
     auto* per_min = static_cast<std::uint32_t*>(ctx->ensure("per_min", c0, 4));
