@@ -77,20 +77,26 @@ __global__ void k_arcs_min(const IdT* __restrict__ crit1, std::uint64_t n1, Dims
 }
 
 // Scatter into minimum buckets: key = saddle id << 1 | (mult == 2).
+// (The arc's source is its bucket's minimum whatever its place in the bucket, so it
+// is written here; the sorted keys then give destinations and multiplicities.)
 __global__ void k_arcs_min_scatter(const std::uint32_t* __restrict__ slot_min, std::uint64_t n1,
                                    std::uint32_t base1, const std::uint64_t* __restrict__ off,
-                                   std::uint32_t* __restrict__ cursor, std::uint64_t* __restrict__ key) {
+                                   std::uint32_t* __restrict__ cursor, std::uint64_t* __restrict__ key,
+                                   std::uint32_t* __restrict__ asrc) {
     GRID_STRIDE(k, n1) {
         const std::uint32_t a = slot_min[2 * k], b = slot_min[2 * k + 1];
         const std::uint64_t sid = base1 + k;
         if (b == kNoLabel) {
-            const std::uint32_t at = atomicAdd(&cursor[a], 1u);
-            key[off[a] + at] = (sid << 1) | 1ull;
+            const std::uint64_t at = off[a] + atomicAdd(&cursor[a], 1u);
+            key[at] = (sid << 1) | 1ull;
+            asrc[at] = a;
         } else {
-            std::uint32_t at = atomicAdd(&cursor[a], 1u);
-            key[off[a] + at] = sid << 1;
-            at = atomicAdd(&cursor[b], 1u);
-            key[off[b] + at] = sid << 1;
+            std::uint64_t at = off[a] + atomicAdd(&cursor[a], 1u);
+            key[at] = sid << 1;
+            asrc[at] = a;
+            at = off[b] + atomicAdd(&cursor[b], 1u);
+            key[at] = sid << 1;
+            asrc[at] = b;
         }
     }
 }
@@ -202,18 +208,13 @@ __global__ void k_sort_large_buckets(const std::uint64_t* __restrict__ off, std:
         for (std::uint64_t i = threadIdx.x; i < n; i += blockDim.x) key[b + i] = src[i];
 }
 
-// Block A arcs out of sorted buckets: src = minimum id, dst = saddle id.
-__global__ void k_arcs_min_emit(const std::uint64_t* __restrict__ off, std::uint64_t nb,
-                                std::uint64_t total, const std::uint64_t* __restrict__ key,
-                                std::uint32_t* __restrict__ asrc, std::uint32_t* __restrict__ adst,
-                                std::uint64_t* __restrict__ amult) {
-    GRID_STRIDE(m, nb) {
-        const std::uint64_t b = off[m], e = m + 1 < nb ? off[m + 1] : total;
-        for (std::uint64_t i = b; i < e; ++i) {
-            asrc[i] = static_cast<std::uint32_t>(m);
-            adst[i] = static_cast<std::uint32_t>(key[i] >> 1);
-            amult[i] = (key[i] & 1) ? 2ull : 1ull;
-        }
+// Block A arcs out of the sorted buckets, one arc per thread: dst = saddle id, mult.
+__global__ void k_arcs_min_emit(std::uint64_t total, const std::uint64_t* __restrict__ key,
+                                std::uint32_t* __restrict__ adst, std::uint64_t* __restrict__ amult) {
+    GRID_STRIDE(i, total) {
+        const std::uint64_t k = key[i];
+        adst[i] = static_cast<std::uint32_t>(k >> 1);
+        amult[i] = (k & 1) ? 2ull : 1ull;
     }
 }
 
@@ -386,7 +387,7 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
     if (n1 == 0) return MSC3D_OK;
     MSC3D_CUDA_TRY(cudaMemsetAsync(cursor, 0, n0 * 4, s));
     MSC3D_CUDA_TRY(cudaMemsetAsync(n_large, 0, 8, s));
-    k_arcs_min_scatter<<<grid_for(n1, num_sms), kThreads, 0, s>>>(slot_min, n1, base1, off, cursor, key);
+    k_arcs_min_scatter<<<grid_for(n1, num_sms), kThreads, 0, s>>>(slot_min, n1, base1, off, cursor, key, asrc);
     k_sort_small_buckets<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, large, n_large);
     count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
@@ -402,7 +403,7 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
         k_sort_large_buckets<<<static_cast<unsigned>(nl), 512, 0, s>>>(off, n0, total, large, key, scratch);
         count_launch();
     }
-    k_arcs_min_emit<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, asrc, adst, amult);
+    k_arcs_min_emit<<<grid_for(total, num_sms), kThreads, 0, s>>>(total, key, adst, amult);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
