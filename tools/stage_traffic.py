@@ -5,7 +5,7 @@ assembly) by launch order: each stage starts with a known first kernel.
 Usage: python tools/stage_traffic.py launches.csv [out.json]"""
 import collections, csv, json, sys
 
-FIRST = [("k_gradient", "gradient"), ("k_compact_crit", "critical"), ("k_compact_by_dim", "critical"),
+FIRST = [("k_gradient", "gradient"), ("k_compact_crit", "critical"), ("k_compact_crit3", "critical"), ("k_compact_by_dim", "critical"),
          ("k_jump_all", "extrema"), ("k_jump", "extrema"),
          ("k_cp_concat", "assembly"), ("k_succ_table", "reachability"), ("k_scatter_quad_rank", "counting")]
 rows = list(csv.reader(open(sys.argv[1])))
