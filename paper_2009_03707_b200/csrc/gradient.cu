@@ -367,6 +367,7 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
     robins(S, fac, cof,
            [&](std::uint32_t m) {
                int best = __ffs(m) - 1;
+               if (!(m & (m - 1))) return best;  // a single candidate (the common case)
                std::uint32_t bv = mscratch[best * mstride];
                for (m &= m - 1; m; m &= m - 1) {
                    const int t = __ffs(m) - 1;
