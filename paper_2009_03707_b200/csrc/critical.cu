@@ -227,6 +227,76 @@ k_compact_crit(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, Id
     }
 }
 
+// Per-dimension masks of the critical cells among the 64 cells [first, first + 64)
+// (bit k = cell first + k): byte compares to bits, then lattice parity masks.
+__device__ __forceinline__ void crit_chunk_masks(const std::uint8_t* __restrict__ codes, const Dims& d,
+                                                 std::uint64_t first, std::uint64_t M[4]) {
+    std::uint64_t crit = 0;
+    if (first + kPerThread <= d.n_cells) {
+#pragma unroll
+        for (int q = 0; q < kChunks; ++q) {
+            const uint4 w = __ldcs(reinterpret_cast<const uint4*>(codes + first + 16 * q));
+            const std::uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const std::uint32_t m = __vcmpeq4(ws[e], 0x01010101u);  // kCritical bytes -> 0xff
+                const std::uint64_t b4 = ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+                crit |= b4 << (16 * q + 4 * e);
+            }
+        }
+    } else {
+        for (int k = 0; k < kPerThread; ++k)
+            if (first + k < d.n_cells && codes[first + k] == kCritical) crit |= 1ull << k;
+    }
+    const Coord p = unpack(d, first < d.n_cells ? first : 0);
+    const std::uint64_t lenA = min(static_cast<std::uint64_t>(kPerThread), static_cast<std::uint64_t>(d.ex - p.x));
+    const std::uint64_t segA = lenA >= 64 ? ~0ull : ((1ull << lenA) - 1);
+    constexpr std::uint64_t kAlt = 0xAAAAAAAAAAAAAAAAull;  // odd k
+    const std::uint64_t oddA = (p.x & 1) ? ~kAlt : kAlt;
+    const std::uint64_t oddB = (lenA & 1) ? ~kAlt : kAlt;
+    std::int64_t yB = p.y + 1, zB = p.z;
+    if (yB == d.ey) {
+        yB = 0;
+        ++zB;
+    }
+    const int rA = static_cast<int>((p.y & 1) + (p.z & 1));
+    const int rB = static_cast<int>((yB & 1) + (zB & 1));
+    const std::uint64_t cA = crit & segA, cB = crit & ~segA;
+#pragma unroll
+    for (int dm = 0; dm < 4; ++dm)
+        M[dm] = (rA == dm ? (cA & ~oddA) : 0ull) | (rA + 1 == dm ? (cA & oddA) : 0ull) |
+                (rB == dm ? (cB & ~oddB) : 0ull) | (rB + 1 == dm ? (cB & oddB) : 0ull);
+}
+
+// Counts only (when the gradient kernel's totals are not available, e.g. codes
+// installed from outside): the same masks, block reduction, one atomic per block
+// and dimension.
+#define CRIT_GRID_STRIDE(i, n)                                                                  \
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < (n); \
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+__global__ void __launch_bounds__(kThreads)
+k_count_crit(const std::uint8_t* __restrict__ codes, Dims d, unsigned long long* __restrict__ totals) {
+    __shared__ unsigned long long s[4];
+    if (threadIdx.x < 4) s[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long local[4] = {0, 0, 0, 0};
+    const std::uint64_t nchunks = (d.n_cells + kPerThread - 1) / kPerThread;
+    CRIT_GRID_STRIDE(c, nchunks) {
+        std::uint64_t M[4];
+        crit_chunk_masks(codes, d, c * kPerThread, M);
+#pragma unroll
+        for (int dm = 0; dm < 4; ++dm) local[dm] += __popcll(M[dm]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        unsigned long long v = local[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s[k], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && s[threadIdx.x]) atomicAdd(&totals[threadIdx.x], s[threadIdx.x]);
+}
+
 // Three 64-cell chunks per thread (49152-cell tiles: per-category tile counts still fit
 // 16 bits; a thread's chunks are consecutive, so thread order is cell order) amortise
 // the look-back; the tile's ids are staged in shared memory and
@@ -252,43 +322,9 @@ k_compact_crit3(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, I
     for (int sb = 0; sb < kSub; ++sb) {
         const std::uint64_t first = static_cast<std::uint64_t>(tile) * kSub * kTile +
                                     (static_cast<std::uint64_t>(threadIdx.x) * kSub + sb) * kPerThread;
-        std::uint64_t crit = 0;
-        if (first + kPerThread <= d.n_cells) {
+        crit_chunk_masks(codes, d, first, M[sb]);
 #pragma unroll
-            for (int q = 0; q < kChunks; ++q) {
-                const uint4 w = __ldcs(reinterpret_cast<const uint4*>(codes + first + 16 * q));
-                const std::uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const std::uint32_t m = __vcmpeq4(ws[e], 0x01010101u);  // kCritical bytes -> 0xff
-                    const std::uint64_t b4 = ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
-                    crit |= b4 << (16 * q + 4 * e);
-                }
-            }
-        } else {
-            for (int k = 0; k < kPerThread; ++k)
-                if (first + k < d.n_cells && codes[first + k] == kCritical) crit |= 1ull << k;
-        }
-        const Coord p = unpack(d, first < d.n_cells ? first : 0);
-        const std::uint64_t lenA = min(static_cast<std::uint64_t>(kPerThread), static_cast<std::uint64_t>(d.ex - p.x));
-        const std::uint64_t segA = lenA >= 64 ? ~0ull : ((1ull << lenA) - 1);
-        constexpr std::uint64_t kAlt = 0xAAAAAAAAAAAAAAAAull;  // odd k
-        const std::uint64_t oddA = (p.x & 1) ? ~kAlt : kAlt;
-        const std::uint64_t oddB = (lenA & 1) ? ~kAlt : kAlt;
-        std::int64_t yB = p.y + 1, zB = p.z;
-        if (yB == d.ey) {
-            yB = 0;
-            ++zB;
-        }
-        const int rA = static_cast<int>((p.y & 1) + (p.z & 1));
-        const int rB = static_cast<int>((yB & 1) + (zB & 1));
-        const std::uint64_t cA = crit & segA, cB = crit & ~segA;
-#pragma unroll
-        for (int dm = 0; dm < 4; ++dm) {
-            M[sb][dm] = (rA == dm ? (cA & ~oddA) : 0ull) | (rA + 1 == dm ? (cA & oddA) : 0ull) |
-                        (rB == dm ? (cB & ~oddB) : 0ull) | (rB + 1 == dm ? (cB & oddB) : 0ull);
-            packed += static_cast<std::uint64_t>(__popcll(M[sb][dm])) << (16 * dm);
-        }
+        for (int dm = 0; dm < 4; ++dm) packed += static_cast<std::uint64_t>(__popcll(M[sb][dm])) << (16 * dm);
     }
     std::uint64_t block_total;
     const std::uint64_t excl = block_excl_scan(packed, &block_total, sm);
@@ -468,7 +504,15 @@ int launch_validate_matching(const std::uint8_t* codes, const Dims& d, unsigned 
 
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
                           cudaStream_t s, int num_sms) {
-    return count_impl(codes, d, CritPred{}, d_totals, s, num_sms);
+    if (d.ex < 64) return count_impl(codes, d, CritPred{}, d_totals, s, num_sms);
+    MSC3D_CUDA_TRY(cudaMemsetAsync(d_totals, 0, 32, s));
+    const std::uint64_t nchunks = (d.n_cells + kPerThread - 1) / kPerThread;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>((nchunks + kThreads - 1) / kThreads,
+                                                                        static_cast<std::uint64_t>(num_sms) * 16));
+    k_count_crit<<<grid, kThreads, 0, s>>>(codes, d, reinterpret_cast<unsigned long long*>(d_totals));
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
 }
 
 int launch_critical_compact(const std::uint8_t* codes, const Dims& d, Workspace& ws,

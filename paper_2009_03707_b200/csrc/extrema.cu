@@ -32,47 +32,40 @@ inline unsigned grid_for(std::uint64_t n, int /*num_sms*/, int /*per_sm*/ = 16) 
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; \
          i < (n); i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
 
+// The other endpoint of a vertex's paired edge is the vertex one stride away along the
+// code's axis (extrema.cpp:51-57); a cube's paired quad leads to the cube one stride
+// away along its axis, if that cube exists (extrema.cpp:68-75) -- index arithmetic on
+// the dense ids, no lattice coordinates beyond the vertex / cube position.
 __global__ void k_forest0(const std::uint8_t* __restrict__ codes, Dims d,
                           std::uint32_t* __restrict__ parent) {
+    const std::uint64_t vstep[3] = {1, static_cast<std::uint64_t>(d.nx), static_cast<std::uint64_t>(d.nx * d.ny)};
     GRID_STRIDE(i, d.n_verts) {
-        const std::uint64_t c = vertex_cell(d, i);
-        const std::uint8_t k = codes[c];
+        const std::uint8_t k = codes[vertex_cell(d, i)];
         if (k == kCritical) {
             parent[i] = static_cast<std::uint32_t>(i);
             continue;
         }
-        const std::int64_t e = partner_of(d, static_cast<std::int64_t>(c), k);
-        const std::int64_t other = 2 * e - static_cast<std::int64_t>(c);
-        parent[i] = vertex_dense(d, unpack(d, static_cast<std::uint64_t>(other)));
+        const int dir = k - kCofacetBase, axis = dir >> 1;  // a vertex pairs with a cofacet edge
+        parent[i] = static_cast<std::uint32_t>((dir & 1) ? i + vstep[axis] : i - vstep[axis]);
     }
 }
 
 __global__ void k_forest3(const std::uint8_t* __restrict__ codes, Dims d,
                           std::uint32_t* __restrict__ parent) {
+    const std::uint64_t mx = d.nx - 1, my = d.ny - 1, mz = d.nz - 1;
+    const std::uint64_t cstep[3] = {1, mx, mx * my};
     GRID_STRIDE(i, d.n_cubes) {
-        const std::uint64_t c = cube_cell(d, i);
-        const std::uint8_t k = codes[c];
+        const std::uint64_t r = d.fmx.div(i), x = i - r * mx, z = d.fmy.div(r), y = r - z * my;
+        const std::uint8_t k = codes[pack(d, 2 * x + 1, 2 * y + 1, 2 * z + 1)];
         if (k == kCritical) {
             parent[i] = static_cast<std::uint32_t>(i);
             continue;
         }
-        // The paired quad q = c -/+ step along the encoded axis; the cube across
-        // q is q -/+ step again, if inside the lattice (extrema.cpp:68-75).
-        const int dir = k - kFacetBase;
-        const int axis = dir >> 1;
-        const Coord cc = unpack(d, c);
-        const std::int64_t coord = axis == 0 ? cc.x : (axis == 1 ? cc.y : cc.z);
-        const std::int64_t ext = axis == 0 ? d.ex : (axis == 1 ? d.ey : d.ez);
-        const std::int64_t across = (dir & 1) ? coord + 2 : coord - 2;
-        if (across < 0 || across >= ext) {
-            parent[i] = static_cast<std::uint32_t>(i);
-            continue;
-        }
-        Coord o = cc;
-        if (axis == 0) o.x = across;
-        else if (axis == 1) o.y = across;
-        else o.z = across;
-        parent[i] = cube_dense(d, o);
+        const int dir = k - kFacetBase, axis = dir >> 1;  // a cube pairs with a facet quad
+        const std::uint64_t coord = axis == 0 ? x : (axis == 1 ? y : z);
+        const std::uint64_t ext = axis == 0 ? mx : (axis == 1 ? my : mz);
+        const bool inside = (dir & 1) ? coord + 1 < ext : coord > 0;
+        parent[i] = static_cast<std::uint32_t>(!inside ? i : ((dir & 1) ? i + cstep[axis] : i - cstep[axis]));
     }
 }
 
