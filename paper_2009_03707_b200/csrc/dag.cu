@@ -520,36 +520,6 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
     }
 }
 
-// Pass-through junctions: exactly one live branch, and it ends at a junction, so
-// P(j) = P(child).  fwd[j] = child (resolved to the end of such chains by pointer
-// jumping), or j itself.
-// ptbits: one bit per junction, set for pass-through ones (10 MB at 512^3,
-// L2-resident), so the rewrite reads fwd only where it can differ.
-__global__ void k_passthrough(const uint4* __restrict__ dest, std::uint64_t nj, std::uint32_t* __restrict__ fwd,
-                              unsigned int* __restrict__ ptbits) {
-    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < nj;
-         base += stride) {
-        const std::uint64_t j = base + (threadIdx.x & 31);
-        bool pt = false;
-        if (j < nj) {
-            const uint4 d4 = dest[j];
-            const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
-            int live = 0;
-            std::uint32_t child = kNone;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                if (dd[b] == kNone) continue;
-                ++live;
-                if (!(dd[b] & kTerm)) child = dd[b];
-            }
-            pt = live == 1 && child != kNone;
-            fwd[j] = pt ? child : static_cast<std::uint32_t>(j);
-        }
-        const unsigned bits = __ballot_sync(0xffffffffu, pt);
-        if ((threadIdx.x & 31) == 0) ptbits[base >> 5] = bits;
-    }
-}
 
 // Redirect every branch through fwd; contracted junctions leave the graph
 // (no branches, pending kSkip).  Each branch reference takes the next parent slot of
@@ -1587,14 +1557,6 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
 
 int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
 
-int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
-                       int num_sms) {
-    if (nj == 0) return MSC3D_OK;
-    k_passthrough<<<grid_full(nj), kThreads, 0, s>>>(static_cast<const uint4*>(node), nj, fwd, ptbits);
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
 
 int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,

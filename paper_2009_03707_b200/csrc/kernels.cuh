@@ -235,8 +235,7 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
                 unsigned int* ptbits, cudaStream_t s,
                 int num_sms);
 int node_rec_bytes();
-int launch_passthrough(const void* node, std::uint64_t nj, std::uint32_t* fwd, unsigned int* ptbits, cudaStream_t s,
-                       int num_sms);
+
 int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
