@@ -272,13 +272,9 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     const std::uint64_t wbase = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
     const int lane = threadIdx.x & 31;
-    while (ncur) {
-        unsigned long long* next_cnt = &cnt[(round + 1) % 3];
-        if (grid.thread_rank() == 0) {
-            cnt[(round + 2) % 3] = 0;
-            if (round < kTimeline) stats[2 + round] = gtimer();
-        }
-        for (std::uint64_t base = wbase; base < ncur; base += stride) {
+    // one BFS level over cur[0, ncur): warps start at `first` and step by `step`
+    auto level = [&](std::uint64_t first, std::uint64_t step, unsigned long long* next_cnt) {
+        for (std::uint64_t base = first; base < ncur; base += step) {
             const std::uint64_t j = base + lane;
             std::uint32_t de[4] = {0, 0, 0, 0};
             std::uint32_t won = 0;
@@ -304,12 +300,42 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
             warp_push(wq, de, won, nxt, next_cnt);
         }
         flush_block(s_q, nxt, next_cnt);
+    };
+    // Levels with big frontiers: the whole grid, a grid barrier per level.  Once the
+    // frontier is small, block 0 finishes alone with block barriers (a level then costs
+    // a few microseconds instead of a grid barrier's round trip); the other blocks exit
+    // (no grid barrier follows).
+    constexpr unsigned long long kSolo = 512;
+    while (ncur >= kSolo) {
+        unsigned long long* next_cnt = &cnt[(round + 1) % 3];
+        if (grid.thread_rank() == 0) {
+            cnt[(round + 2) % 3] = 0;
+            if (round < kTimeline) stats[2 + round] = gtimer();
+        }
+        level(wbase, stride, next_cnt);
         grid.sync();
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
         ++round;
         std::uint32_t* t = cur;
         cur = nxt;
         nxt = t;
+    }
+    if (blockIdx.x == 0) {
+        while (ncur) {
+            unsigned long long* next_cnt = &cnt[(round + 1) % 3];
+            if (threadIdx.x == 0) {
+                cnt[(round + 2) % 3] = 0;
+                if (round < kTimeline) stats[2 + round] = gtimer();
+            }
+            __syncthreads();
+            level(threadIdx.x & ~31u, blockDim.x, next_cnt);  // (ends with a block barrier)
+            ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
+            __syncthreads();
+            ++round;
+            std::uint32_t* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&stats[1], mine);
