@@ -444,7 +444,7 @@ constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by 
 // rewrite drops predone children from their parents' pending counts and parent
 // lists -- no atomics for the ~40% of the junction graph that are leaves.
 template <typename IdT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(128)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
        uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
        uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
@@ -1571,10 +1571,10 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* w
     auto* nr = static_cast<uint4*>(node);  // the nodes' destination records
     auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)
-        k_walk<std::uint32_t><<<grid_full(n), kThreads, 0, s>>>(
+        k_walk<std::uint32_t><<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(
             c, d, jlist, static_cast<const std::uint32_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone, fwd, ptbits);
     else
-        k_walk<std::uint64_t><<<grid_full(n), kThreads, 0, s>>>(
+        k_walk<std::uint64_t><<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(
             c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone, fwd, ptbits);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
