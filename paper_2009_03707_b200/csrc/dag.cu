@@ -401,7 +401,34 @@ struct WalkCtx {
     std::uint64_t limit;
 };
 
-__device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, std::uint32_t cur, unsigned int* cycle) {
+// Per-block step tables: every successor / terminal-quad index is the current dense
+// edge id plus an offset that depends only on the edge axis a, the cofacet position p
+// and the field value f (succ_edge / term_quad are linear in de), so a walk step is a
+// table lookup and an add (u32 wrap-around is exact) instead of the axis arithmetic.
+struct StepTables {
+    std::uint32_t step[36];  // [(a * 4 + p) * 3 + f - 2]: successor edge offset, f in {2, 3, 4}
+    std::uint32_t tq[12];    // [a * 4 + p]: terminal quad offset
+    std::uint8_t nax[12];    // [a * 4 + p]: axis of a turn's successor edge (f in {3, 4})
+};
+__device__ __forceinline__ void fill_step_tables(StepTables& t, const EGrid& g) {
+    // offsets read off a representative interior edge with the exact step functions
+    const std::uint32_t v = g.sz + g.sy + 1u;
+    for (int i = threadIdx.x; i < 36; i += blockDim.x) {
+        const int a = i / 12, p = (i / 3) % 4;
+        const std::uint32_t f = 2u + static_cast<std::uint32_t>(i % 3), de = 3u * v + static_cast<std::uint32_t>(a);
+        t.step[i] = succ_edge(EdgeRef(de), de, p, f, g) - de;
+    }
+    for (int i = threadIdx.x; i < 12; i += blockDim.x) {
+        const int a = i / 4, p = i % 4;
+        const std::uint32_t de = 3u * v + static_cast<std::uint32_t>(a);
+        t.tq[i] = term_quad(EdgeRef(de), p, g) - de;
+        t.nax[i] = static_cast<std::uint8_t>(other_axis(a, p >> 1));
+    }
+}
+
+// Walk from edge cur (axis a) to the branch's end.
+__device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, const StepTables& t, std::uint32_t cur,
+                                                     int a, unsigned int* cycle) {
     for (std::uint64_t steps = 0;; ++steps) {
         const std::uint32_t s = __ldg(&c.succ[cur]);
         const std::uint32_t present = (s | (s >> 1) | (s >> 2)) & kFieldLow;
@@ -409,9 +436,10 @@ __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, std::uint
         if (present & (present - 1)) return junction_rank(c.woff, c.jbits, cur);
         const int p = (__ffs(present) - 1) / 3;
         const std::uint32_t f = (s >> (3 * p)) & 7u;
-        const EdgeRef e(cur);
-        if (f == 1) return kTerm | c.tmap[term_quad(e, p, c.g)];
-        cur = succ_edge(e, cur, p, f, c.g);
+        const int ap = a * 4 + p;
+        if (f == 1) return kTerm | c.tmap[cur + t.tq[ap]];
+        cur += t.step[ap * 3 + static_cast<int>(f) - 2];
+        a = f == 2 ? a : t.nax[ap];
         if (steps > c.limit) {
             *cycle = 1u;  // invalid gradient (saddle_graph.cpp:173-174)
             return kNone;
@@ -450,6 +478,9 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
        uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
        unsigned long long* __restrict__ n_predone,
        std::uint32_t* __restrict__ fwd, unsigned int* __restrict__ ptbits) {
+    __shared__ StepTables s_tab;
+    fill_step_tables(s_tab, c.g);
+    __syncthreads();
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < n;
          base += stride) {
@@ -465,7 +496,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                 de0 = 3u * static_cast<std::uint32_t>((o.x >> 1) + d.nx * ((o.y >> 1) + d.ny * (o.z >> 1))) + a;
             }
             const std::uint32_t s0 = c.succ[de0];
-            const EdgeRef e(de0);
+            const int a0 = static_cast<int>(de0 - 3u * (__umulhi(de0, 0xAAAAAAABu) >> 1));
             std::uint32_t dd[4] = {kNone, kNone, kNone, kNone};
             std::uint32_t pend = 0;
             int nd = 0;
@@ -473,8 +504,10 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
             for (int p = 0; p < 4; ++p) {
                 const std::uint32_t f = (s0 >> (3 * p)) & 7u;
                 if (f == 0) continue;
-                const std::uint32_t t = f == 1 ? (kTerm | c.tmap[term_quad(e, p, c.g)])
-                                               : walk_branch(c, succ_edge(e, de0, p, f, c.g), &flags[2]);
+                const int ap = a0 * 4 + p;
+                const std::uint32_t t = f == 1 ? (kTerm | c.tmap[de0 + s_tab.tq[ap]])
+                                               : walk_branch(c, s_tab, de0 + s_tab.step[ap * 3 + static_cast<int>(f) - 2],
+                                                             f == 2 ? a0 : s_tab.nax[ap], &flags[2]);
                 dd[0] = nd == 0 ? t : dd[0];
                 dd[1] = nd == 1 ? t : dd[1];
                 dd[2] = nd == 2 ? t : dd[2];
