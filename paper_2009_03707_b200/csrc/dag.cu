@@ -116,6 +116,31 @@ __device__ __forceinline__ std::uint32_t term_quad(const EdgeRef& e, int p, cons
     return 3u * lv + static_cast<std::uint32_t>(3 - e.a - b);
 }
 
+// Per-block step tables: every successor / terminal-quad index is the current dense
+// edge id plus an offset that depends only on the edge axis a, the cofacet position p
+// and the field value f (succ_edge / term_quad are linear in de), so a walk step is a
+// table lookup and an add (u32 wrap-around is exact) instead of the axis arithmetic.
+struct StepTables {
+    std::uint32_t step[36];  // [(a * 4 + p) * 3 + f - 2]: successor edge offset, f in {2, 3, 4}
+    std::uint32_t tq[12];    // [a * 4 + p]: terminal quad offset
+    std::uint8_t nax[12];    // [a * 4 + p]: axis of a turn's successor edge (f in {3, 4})
+};
+__device__ __forceinline__ void fill_step_tables(StepTables& t, const EGrid& g) {
+    // offsets read off a representative interior edge with the exact step functions
+    const std::uint32_t v = g.sz + g.sy + 1u;
+    for (int i = threadIdx.x; i < 36; i += blockDim.x) {
+        const int a = i / 12, p = (i / 3) % 4;
+        const std::uint32_t f = 2u + static_cast<std::uint32_t>(i % 3), de = 3u * v + static_cast<std::uint32_t>(a);
+        t.step[i] = succ_edge(EdgeRef(de), de, p, f, g) - de;
+    }
+    for (int i = threadIdx.x; i < 12; i += blockDim.x) {
+        const int a = i / 4, p = i % 4;
+        const std::uint32_t de = 3u * v + static_cast<std::uint32_t>(a);
+        t.tq[i] = term_quad(EdgeRef(de), p, g) - de;
+        t.nax[i] = static_cast<std::uint8_t>(other_axis(a, p >> 1));
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // successor table
 // ---------------------------------------------------------------------------------
@@ -260,9 +285,11 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
         std::uint32_t* __restrict__ fa, std::uint32_t* __restrict__ fb, unsigned long long* __restrict__ cnt,
         unsigned long long* __restrict__ stats) {
     __shared__ WarpQ s_q[kThreads / 32];
+    __shared__ StepTables s_tab;
+    fill_step_tables(s_tab, g);
     WarpQ& wq = s_q[threadIdx.x >> 5];
     if ((threadIdx.x & 31) == 0) wq.n = 0;
-    __syncwarp();
+    __syncthreads();
     cg::grid_group grid = cg::this_grid();
     std::uint32_t* cur = fa;
     std::uint32_t* nxt = fb;
@@ -281,7 +308,7 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
             if (j < ncur) {
                 const std::uint32_t node = __ldcg(cur + j);
                 const std::uint32_t s = succ[node];
-                const EdgeRef e(node);
+                const int a4 = 4 * static_cast<int>(node - 3u * (__umulhi(node, 0xAAAAAAABu) >> 1));
                 // claims by atomic test-and-set, the (<= 4) atomics issued back to back
                 unsigned old[4];
 #pragma unroll
@@ -289,7 +316,7 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
                     const std::uint32_t f = (s >> (3 * p)) & 7u;
                     old[p] = ~0u;
                     if (f < 2) continue;
-                    de[p] = succ_edge(e, node, p, f, g);
+                    de[p] = node + s_tab.step[(a4 + p) * 3 + static_cast<int>(f) - 2];
                     old[p] = atomicOr(&bitmap[de[p] >> 5], 1u << (de[p] & 31));
                 }
 #pragma unroll
@@ -400,31 +427,6 @@ struct WalkCtx {
     const std::uint32_t* tmap;
     std::uint64_t limit;
 };
-
-// Per-block step tables: every successor / terminal-quad index is the current dense
-// edge id plus an offset that depends only on the edge axis a, the cofacet position p
-// and the field value f (succ_edge / term_quad are linear in de), so a walk step is a
-// table lookup and an add (u32 wrap-around is exact) instead of the axis arithmetic.
-struct StepTables {
-    std::uint32_t step[36];  // [(a * 4 + p) * 3 + f - 2]: successor edge offset, f in {2, 3, 4}
-    std::uint32_t tq[12];    // [a * 4 + p]: terminal quad offset
-    std::uint8_t nax[12];    // [a * 4 + p]: axis of a turn's successor edge (f in {3, 4})
-};
-__device__ __forceinline__ void fill_step_tables(StepTables& t, const EGrid& g) {
-    // offsets read off a representative interior edge with the exact step functions
-    const std::uint32_t v = g.sz + g.sy + 1u;
-    for (int i = threadIdx.x; i < 36; i += blockDim.x) {
-        const int a = i / 12, p = (i / 3) % 4;
-        const std::uint32_t f = 2u + static_cast<std::uint32_t>(i % 3), de = 3u * v + static_cast<std::uint32_t>(a);
-        t.step[i] = succ_edge(EdgeRef(de), de, p, f, g) - de;
-    }
-    for (int i = threadIdx.x; i < 12; i += blockDim.x) {
-        const int a = i / 4, p = i % 4;
-        const std::uint32_t de = 3u * v + static_cast<std::uint32_t>(a);
-        t.tq[i] = term_quad(EdgeRef(de), p, g) - de;
-        t.nax[i] = static_cast<std::uint8_t>(other_axis(a, p >> 1));
-    }
-}
 
 // Walk from edge cur (axis a) to the branch's end.
 __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, const StepTables& t, std::uint32_t cur,
