@@ -159,6 +159,13 @@ struct Pack5 {
     }
 };
 
+// Dense-id offset of the cube at slot t from the cube at slot 0 of a star.
+__device__ __forceinline__ std::uint32_t cube_slot_offset(int t, const Dims& d) {
+    const int z = t / 9, y = (t / 3) % 3, x = t % 3;
+    return (x != 0 ? 1u : 0u) + (y != 0 ? static_cast<std::uint32_t>(d.nx - 1) : 0u) +
+           (z != 0 ? static_cast<std::uint32_t>((d.nx - 1) * (d.ny - 1)) : 0u);
+}
+
 // Output side of one star: codes, forests, critical counts.
 struct StarWriter {
     std::uint8_t* cbase;           // codes + vertex cell id
@@ -179,10 +186,8 @@ struct StarWriter {
                 csz * static_cast<std::uint32_t>(vz - 1);
     }
     // dense id of the in-box cube at slot t (u32 wrap-around is exact: the result is)
-    __device__ __forceinline__ std::uint32_t cube_dense_of(int t) const {
-        const int z = (t * 57) >> 9, r = t - 9 * z, y = (r * 11) >> 5, x = r - 3 * y;
-        return cube0 + (x != 0 ? 1u : 0u) + (y != 0 ? csy : 0u) + (z != 0 ? csz : 0u);
-    }
+    const std::uint32_t* cube_off;  // per slot: (x != 0) + (y != 0) * csy + (z != 0) * csz (block table)
+    __device__ __forceinline__ std::uint32_t cube_dense_of(int t) const { return cube0 + cube_off[t]; }
     __device__ __forceinline__ void pair(int lo, int hi) {  // gradient.cpp:162-174
         const int diff = hi - lo;  // +-1, +-3 or +-9
         const int ad = diff < 0 ? -diff : diff;
@@ -410,6 +415,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ T tiles_sm[kSets][kGroup][SZ][SY][SX];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_coff[27];
     __shared__ unsigned long long s_crit[4];
     __shared__ MaskT<8> s_M[27 * NT];
     __shared__ std::uint32_t s_lb[2][kListBuf];
@@ -423,6 +429,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     if (tid < 27) {
         s_fac[tid] = c_slot.facet[tid];
         s_cof[tid] = c_slot.cofacet[tid];
+        s_coff[tid] = cube_slot_offset(tid, d);
         s_cell[tid] = static_cast<std::int32_t>(c_slot.off[tid][0] + c_slot.off[tid][1] * d.ex +
                                                 c_slot.off[tid][2] * d.exy);
     }
@@ -533,6 +540,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             w.d = d;
             w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
             w.cell_off = s_cell;
+            w.cube_off = s_coff;
             w.parent0 = parent0;
             w.parent3 = parent3;
             w.ncrit = 0;
@@ -643,6 +651,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
                 std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
                 unsigned long long* __restrict__ crit_totals, StarLists lists, int which) {
     __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_coff[27];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ MaskT<K> s_M[27 * 128];
     __shared__ unsigned long long s_crit[4];
@@ -650,6 +659,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
     if (threadIdx.x < 27) {
         s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
         s_cof[threadIdx.x] = c_slot.cofacet[threadIdx.x];
+        s_coff[threadIdx.x] = cube_slot_offset(static_cast<int>(threadIdx.x), d);
         s_cell[threadIdx.x] = static_cast<std::int32_t>(
             c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
         s_voff[threadIdx.x] = c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.nx +
@@ -686,6 +696,7 @@ k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ code
         w.d = d;
         w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
         w.cell_off = s_cell;
+        w.cube_off = s_coff;
         w.parent0 = parent0;
         w.parent3 = parent3;
         w.ncrit = 0;
@@ -736,10 +747,12 @@ k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ 
                     std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
                     StarLists lists, unsigned long long* __restrict__ crit_totals) {
     __shared__ std::int32_t s_cell[27];
+    __shared__ std::uint32_t s_coff[27];
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     if (threadIdx.x < 27) {
         s_fac[threadIdx.x] = c_slot.facet[threadIdx.x];
         s_cof[threadIdx.x] = c_slot.cofacet[threadIdx.x];
+        s_coff[threadIdx.x] = cube_slot_offset(static_cast<int>(threadIdx.x), d);
         s_cell[threadIdx.x] = static_cast<std::int32_t>(
             c_slot.off[threadIdx.x][0] + c_slot.off[threadIdx.x][1] * d.ex + c_slot.off[threadIdx.x][2] * d.exy);
     }
@@ -764,6 +777,7 @@ k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ 
         w.d = d;
         w.cbase = codes + (2 * w.vx + d.ex * (2 * w.vy + d.ey * 2 * w.vz));
         w.cell_off = s_cell;
+        w.cube_off = s_coff;
         w.parent0 = parent0;
         w.parent3 = parent3;
         w.ncrit = 0;
