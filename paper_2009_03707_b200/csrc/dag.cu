@@ -449,20 +449,17 @@ __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, const Ste
     }
 }
 
-// Per-node record of the junction graph (64 bytes, one load of four uint4): the
-// <= 4 branch destinations, the parent count, and the first kInlineParents parents
-// inline (the rest in an overflow list), so processing a node costs one dependent
-// load for all of its structure.
-constexpr int kInlineParents = 9;
+// Per-node parent record (32 bytes, one sector): the first kInlineParents parents,
+// in the slots the rewrite's per-child counters hand out; later ones (in-degree > 8,
+// rare) go to an overflow list.  (The branch destinations live in their own dense
+// array, the parent count in the counters.)
+constexpr int kInlineParents = 8;
 constexpr std::uint32_t kSkip = 0xffffffffu;  // pending0 of a contracted pass-through junction
 
 struct alignas(16) NodeRec {
-    std::uint32_t dest[4];
-    std::uint32_t npar;          // (unused: the count comes from the rewrite's slot counters)
-    std::uint32_t ov_lo, ov_hi;  // (unused: overflow offsets are read from the scan's output)
     std::uint32_t par[kInlineParents];
 };
-static_assert(sizeof(NodeRec) == 64, "NodeRec is one 64-byte line");
+static_assert(sizeof(NodeRec) == 32, "NodeRec is one 32-byte sector");
 
 constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by the walk itself
 
@@ -1088,7 +1085,8 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
 __device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, std::uint32_t rn, std::uint64_t ov,
                                                 const uint4 meta, const uint4 par0, const uint4 par1,
                                                 std::uint32_t* nxt, unsigned long long* next_cnt) {
-    const std::uint32_t inl[kInlineParents] = {meta.w, par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
+    const std::uint32_t inl[kInlineParents] = {par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
+    (void)meta;
     std::uint32_t k0 = 0;  // parents handled so far
     for (;;) {
         std::uint32_t p[4], old[4];
@@ -1141,9 +1139,8 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
         const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
         const uint4 d4 = a.dest[u];
         if (u < a.nj) npar = a.indeg[u];
-        meta = nr[1];
-        par0 = nr[2];
-        par1 = nr[3];
+        par0 = nr[0];
+        par1 = nr[1];
         gather<true>(d4, a.rec, in);
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
@@ -1234,7 +1231,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
                                             unsigned long long& done) {
     const int lane = threadIdx.x & 31;
     const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
-    const uint4 d4 = a.dest[u], meta = nr[1], par0 = nr[2], par1 = nr[3];
+    const uint4 d4 = a.dest[u], meta = make_uint4(0u, 0u, 0u, 0u), par0 = nr[0], par1 = nr[1];
     Inputs h;
     gather<true>(d4, a.rec, h);
     const std::uint32_t T = h.len[0] + h.len[1] + h.len[2] + h.len[3];
