@@ -646,7 +646,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
 // L1/L2-resident neighbourhoods).  Same register fast path with a wider network;
 // tied stars are forwarded to the slow path list.
 template <int K, typename T>
-__global__ void __launch_bounds__(128, 8)
+__global__ void __launch_bounds__(128, K == 32 ? 7 : 8)
 k_gradient_list(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                 std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
                 unsigned long long* __restrict__ crit_totals, StarLists lists, int which) {
