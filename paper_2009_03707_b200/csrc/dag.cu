@@ -396,12 +396,16 @@ __global__ void k_junction_bits(const std::uint16_t* __restrict__ succ, const un
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(nodes, mine);
 }
 
+// Also writes jrank[w] = (first rank of word w, junction bits of word w): a rank
+// lookup in the walks is then one 8-byte load.
 __global__ void k_junction_list(const unsigned int* __restrict__ jbits, std::uint64_t nwords,
-                                const std::uint64_t* __restrict__ woff, std::uint32_t* __restrict__ jlist) {
+                                const std::uint64_t* __restrict__ woff, std::uint32_t* __restrict__ jlist,
+                                uint2* __restrict__ jrank) {
     for (std::uint64_t w = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
          w += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         unsigned int jb = jbits[w];
         std::uint64_t at = woff[w];
+        jrank[w] = make_uint2(static_cast<std::uint32_t>(at), jb);
         while (jb) {
             const int b = __ffs(jb) - 1;
             jb &= jb - 1;
@@ -410,10 +414,9 @@ __global__ void k_junction_list(const unsigned int* __restrict__ jbits, std::uin
     }
 }
 
-__device__ __forceinline__ std::uint32_t junction_rank(const std::uint64_t* __restrict__ woff,
-                                                       const unsigned int* __restrict__ jbits, std::uint32_t de) {
-    const std::uint32_t w = de >> 5;
-    return static_cast<std::uint32_t>(woff[w]) + __popc(jbits[w] & ((1u << (de & 31)) - 1u));
+__device__ __forceinline__ std::uint32_t junction_rank(const uint2* __restrict__ jrank, std::uint32_t de) {
+    const uint2 r = jrank[de >> 5];
+    return r.x + __popc(r.y & ((1u << (de & 31)) - 1u));
 }
 
 // ---------------------------------------------------------------------------------
@@ -422,8 +425,7 @@ __device__ __forceinline__ std::uint32_t junction_rank(const std::uint64_t* __re
 struct WalkCtx {
     const std::uint16_t* succ;
     EGrid g;
-    const std::uint64_t* woff;
-    const unsigned int* jbits;
+    const uint2* jrank;
     const std::uint32_t* tmap;
     std::uint64_t limit;
 };
@@ -435,7 +437,7 @@ __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, const Ste
         const std::uint32_t s = __ldg(&c.succ[cur]);
         const std::uint32_t present = (s | (s >> 1) | (s >> 2)) & kFieldLow;
         if (present == 0) return kNone;                       // dead end
-        if (present & (present - 1)) return junction_rank(c.woff, c.jbits, cur);
+        if (present & (present - 1)) return junction_rank(c.jrank, cur);
         const int p = (__ffs(present) - 1) / 3;
         const std::uint32_t f = (s >> (3 * p)) & 7u;
         const int ap = a * 4 + p;
@@ -1584,22 +1586,22 @@ int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, 
     return MSC3D_OK;
 }
 
-int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff,
+int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff, void* jrank,
                          std::uint32_t* jlist, cudaStream_t s, int num_sms) {
     if (nwords == 0) return MSC3D_OK;
-    k_junction_list<<<grid_for(nwords, num_sms, 16), kThreads, 0, s>>>(jbits, nwords, woff, jlist);
+    k_junction_list<<<grid_for(nwords, num_sms, 16), kThreads, 0, s>>>(jbits, nwords, woff, jlist, static_cast<uint2*>(jrank));
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
 
-int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
+int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
                 unsigned int* ptbits, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
-    WalkCtx c{succ, egrid(d), woff, jbits, tmap, d.n_cells};
+    WalkCtx c{succ, egrid(d), static_cast<const uint2*>(jrank), tmap, d.n_cells};
     auto* nr = static_cast<uint4*>(node);  // the nodes' destination records
     auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)

@@ -224,11 +224,12 @@ int launch_reach(const std::uint16_t* succ, const Dims& d, unsigned int* bitmap,
 int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, std::uint64_t nwords,
                          unsigned int* jbits, std::uint32_t* jcnt, unsigned long long* nodes, cudaStream_t s,
                          int num_sms);
-int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff,
+// jrank: nwords uint2 (first rank of the word, its junction bits)
+int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const std::uint64_t* woff, void* jrank,
                          std::uint32_t* jlist, cudaStream_t s, int num_sms);
 // junction launch: rec / predone (bit per junction) / n_predone set, slen null;
 // 1-saddle launch: slen set (their merged length when all branches are terminal), rec/predone null
-int launch_walk(const std::uint16_t* succ, const Dims& d, const std::uint64_t* woff, const unsigned int* jbits,
+int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
                 const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,

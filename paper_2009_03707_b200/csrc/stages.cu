@@ -332,7 +332,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     if (!jlist || !node || !jdest || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !rec ||
         !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jlist, s, sms));
+    void* jrank = ctx->ensure("jrank", nwords, 8);
+    if (!jrank) return MSC3D_ERR_NOMEM;
+    TRY(msc3d_dev::launch_junction_list(jbits, nwords, woff, jrank, jlist, s, sms));
 
     // branch walks (saddle_graph.cpp:139-202): destinations and pending children
     auto* predone = static_cast<unsigned int*>(ctx->ensure("predone", (nj + 31) / 32 + 1, 4));
@@ -342,9 +344,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // (the junction walks also flag the pass-through junctions: fwd, ptbits)
     auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
     if (!ptbits) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
+    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
                                predone, n_predone, fwd, ptbits, s, sms));
-    TRY(msc3d_dev::launch_walk(succ, d, woff, jbits, tmap, nullptr, src_ids, w, n1,
+    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, nullptr, src_ids, w, n1,
                                jdest + nj * 16, pending + nj, flags, nullptr, slen, nullptr, nullptr, nullptr, nullptr, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
