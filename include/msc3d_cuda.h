@@ -84,6 +84,13 @@ void msc3d_host_free(void* p);
 
 /* Copy a named array to host memory (capacity in bytes); synchronises the stream. */
 int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t capacity_bytes);
+/* Context options (not in the reference; defaults reproduce it exactly):
+ *   "wide_ids" (0/1)          64-bit cell-id lists on any grid -- the layout grids with
+ *                             >= 2^32 cells use (configs 4-5), testable on small grids;
+ *   "kahn_switch_below" (>=1) frontier size at which path counting leaves its wide
+ *                             launch configuration for the tail one (default 2^18).
+ * Unknown names / bad values -> MSC3D_ERR_INVALID. */
+int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, int64_t value);
 /* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...). */
 int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, int64_t* value);
 

@@ -75,6 +75,7 @@ def lib():
         "msc3d_ctx_array": (i32, [vp, C.c_char_p, C.POINTER(vp), C.POINTER(u64), C.POINTER(i32)]),
         "msc3d_ctx_download": (i32, [vp, C.c_char_p, vp, u64]),
         "msc3d_ctx_scalar": (i32, [vp, C.c_char_p, C.POINTER(i64)]),
+        "msc3d_ctx_set_option": (i32, [vp, C.c_char_p, i64]),
         "msc3d_ctx_load_values": (i32, [vp, Dims, i32, vp]),
         "msc3d_ctx_bind_values": (i32, [vp, Dims, i32, vp]),
         "msc3d_ctx_read_volume": (i32, [vp, C.c_char_p, Dims, C.c_char_p, i32]),
@@ -95,6 +96,7 @@ def lib():
         "msc3d_ctx_bind_codes": (i32, [vp, Dims, vp]),
         "msc3d_ctx_compute_host_values": (i32, [vp, Dims, i32, vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_ctx_compute_codes": (i32, [vp, i32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+        "msc3d_ctx_cp_values": (i32, [vp]),
         "msc3d_field_hash_f64": (u64, [vp, u64]),
         "msc3d_field_hash_f32": (u64, [vp, u64]),
     }
@@ -152,6 +154,7 @@ class Context:
         _raise(self._L.msc3d_ctx_create(C.byref(h), int(device)), "msc3d_ctx_create")
         self.h = h
         self.dims = None
+        self.wide = False
 
     def close(self):
         if getattr(self, "h", None):
@@ -188,6 +191,22 @@ class Context:
         v = C.c_int64()
         _raise(self._L.msc3d_ctx_scalar(self.h, name.encode(), C.byref(v)), name)
         return v.value
+
+    def set_option(self, name, value):
+        """msc3d_ctx_set_option: "wide_ids" (64-bit id lists on any grid), "kahn_switch_below"."""
+        _raise(self._L.msc3d_ctx_set_option(self.h, name.encode(), C.c_int64(int(value))), name)
+        if name == "wide_ids":
+            self.wide = bool(value)
+        return self
+
+    def ids(self, dims):
+        """dtype of host cell-id arrays this context takes / returns for `dims`."""
+        return np.uint64 if self.wide else id_dtype(dims)
+
+    def cp_values(self):
+        """CriticalPoint::value (msc.cpp:106) of the last compute, f64 per critical point."""
+        _raise(self._L.msc3d_ctx_cp_values(self.h), "cp_values")
+        return self.get("cp_value", np.float64)
 
     def launches(self):
         return int(self._L.msc3d_ctx_launches(self.h))
@@ -261,7 +280,7 @@ class Context:
         if sources is None:
             _raise(self._L.msc3d_ctx_mark(self.h, None, C.c_uint64(0)), "mark_reachable")
         else:
-            s = np.ascontiguousarray(sources, dtype=id_dtype(self.dims))
+            s = np.ascontiguousarray(sources, dtype=self.ids(self.dims))
             _raise(self._L.msc3d_ctx_mark(self.h, s.ctypes.data_as(C.c_void_p) if s.size else C.c_void_p(1),
                                           C.c_uint64(s.size)), "mark_reachable")
         return self

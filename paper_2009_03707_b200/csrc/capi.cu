@@ -194,6 +194,20 @@ int msc3d_ctx_cp_values(msc3d_ctx* ctx) {
                                        ctx->values, ctx->value_type, out, ctx->stream, ctx->num_sms);
 }
 
+int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
+    if (!ctx || !name) return MSC3D_ERR_INVALID;
+    const std::string n(name);
+    if (n == "wide_ids") {
+        ctx->force_wide = value != 0;
+    } else if (n == "kahn_switch_below") {
+        if (value < 1) return MSC3D_ERR_INVALID;
+        ctx->kahn_switch_below = static_cast<std::uint64_t>(value);
+    } else {
+        return MSC3D_ERR_INVALID;
+    }
+    return MSC3D_OK;
+}
+
 int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, std::int64_t* value) {
     auto it = ctx->scalars.find(name);
     if (it == ctx->scalars.end()) return MSC3D_ERR_STATE;

@@ -27,6 +27,11 @@ struct msc3d_ctx {
     bool have_dims = false;
     bool crit_counts_valid = false;  // d_small[40..43] hold the codes' critical counts
     int value_type = MSC3D_VALUE_F32;
+    // msc3d_ctx_set_option: "wide_ids" forces 64-bit cell-id lists on any grid (the
+    // path configs 4-5 take, testable on small grids); "kahn_switch_below" is the
+    // frontier size at which the counting kernel hands over to its tail configuration.
+    bool force_wide = false;
+    std::uint64_t kahn_switch_below = 1ull << 18;
     const void* values = nullptr;  // device pointer (owned "values" array or bound)
     std::map<std::string, DevArray> arrays;
     std::map<std::string, std::int64_t> scalars;
@@ -95,7 +100,7 @@ struct msc3d_ctx {
         auto it = arrays.find(name);
         if (it != arrays.end()) it->second.count = 0;
     }
-    int id_width() const { return dims.n_cells <= 0xffffffffull ? 4 : 8; }
+    int id_width() const { return (!force_wide && dims.n_cells <= 0xffffffffull) ? 4 : 8; }
     // Copy the first n u64 of d_small to h_small and wait.  The copy is a tiny
     // kernel writing the mapped host mirror over the bus, not a DMA: a DMA would
     // queue behind bulk device-to-host output copies on the copy engine.

@@ -822,7 +822,6 @@ __device__ __forceinline__ std::uint32_t merge(const Inputs& in, const PoolRef& 
 // independent 16-byte loads (all in flight at once), then merges from shared memory.
 constexpr int kWarpCap = 1024;  // entries per warp buffer (larger inputs: direct merge)
 constexpr int kWarpCapWide = 384;  // the high-occupancy configuration of the early rounds
-constexpr unsigned long long kSwitchBelow = 1ull << 18;  // frontier size below which the tail configuration takes over
 constexpr std::uint32_t kHeavy = 48;  // total input length above which the whole warp merges the node
 
 // A warp's slice of the dynamic shared memory: cap (key, count) entries.
@@ -1683,7 +1682,7 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     a.heavy_n = L.heavy_rounds;
     a.heavy_head = L.heavy_rounds + 3;
     if (L.nj + L.n1 == 0) return MSC3D_OK;
-    a.switch_below = kSwitchBelow;
+    a.switch_below = L.switch_below;
     a.indeg = L.indeg;
     a.ovoff = L.ovoff;
     a.resume = L.resume;

@@ -214,6 +214,7 @@ struct CountLaunch {
     unsigned long long* resume;     // 3 words of state between the two configurations
     const std::uint32_t* indeg;     // parents per junction
     const std::uint64_t* ovoff;     // overflow-list offsets
+    unsigned long long switch_below;  // frontier size below which the tail configuration runs
 };
 int count_rec_bytes();
 int count_arenas();

@@ -183,6 +183,8 @@ int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
     const int w = ctx->id_width();
     const std::uint64_t nde = 3 * d.n_verts;
     const std::uint64_t nwords = (nde + 31) / 32;
+    // dense edge ids de = 3*vertex + axis and frontier entries are u32
+    if (nde >= 0xffffffffull) return MSC3D_ERR_INVALID;
     TRY(succ_table(ctx));
     auto* bitmap = static_cast<unsigned int*>(ctx->ensure("visited", nwords, 4));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
@@ -313,6 +315,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     TRY(ctx->fetch_small(1));
     const std::uint64_t nj = ctx->h_small[0];
     const std::uint64_t nn = nj + n1;
+    // branch destinations are u32 ranks with kTerm (bit 31) marking 2-saddles
+    if (nj >= 0x80000000ull || ctx->count(term_list) >= 0x80000000ull) return MSC3D_ERR_INVALID;
     ctx->scalars["junctions"] = static_cast<std::int64_t>(nj);
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
     void* node = ctx->ensure("jnode", nn, msc3d_dev::node_rec_bytes());
@@ -429,6 +433,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.heavy_rounds = reinterpret_cast<unsigned long long*>(ctx->d_small + 70);  // 6 words
         L.indeg = indeg;
         L.ovoff = ovoff;
+        L.switch_below = ctx->kahn_switch_below;
         L.ready = ready;
         L.n_ready = n_ready;
         if (!L.heavy_q) return MSC3D_ERR_NOMEM;
@@ -742,8 +747,10 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     // [reachability]
     StageClock clk2(stage_ms != nullptr);
     clk2.mark(0, s);
+    std::uint64_t n_shards = 1;
     if (sharded) {  // shard src_first of src_count balanced slices
         const std::uint64_t k = src_first, n = src_count;
+        n_shards = n;
         src_first = c1 * k / n;
         src_count = c1 * (k + 1) / n - src_first;
         ctx->scalars["shard_first"] = static_cast<std::int64_t>(src_first);
@@ -751,7 +758,9 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     }
     if (src_first > c1) return MSC3D_ERR_INVALID;
     src_count = std::min(src_count, c1 - src_first);
-    const bool sliced = src_first != 0 || src_count != c1;
+    // a rank of a multi-shard run always delivers its block in arcB_* (even when the
+    // balanced slice happens to be empty or the whole list)
+    const bool sliced = sharded ? n_shards > 1 : (src_first != 0 || src_count != c1);
     const void* srcs = static_cast<const char*>(ctx->ptr<void>("crit1")) + src_first * w;
     TRY(bfs(ctx, srcs, src_count));
     clk2.mark(1, s);

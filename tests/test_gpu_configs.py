@@ -1,0 +1,165 @@
+"""GPU parity at the BASELINE configs, on the 64-bit-id layout, and across the
+counting kernel's launch configurations.
+
+* Configs 1-2 (64^3 / 256^3 gauss) are compared LIVE against the unmodified
+  reference (oracle/_ref): codes, the four critical lists, critical points (cell,
+  index, value), sorted arcs with multiplicities, both label volumes, input_hash
+  (msc.cpp:57-147).
+* Config 3 (512^3 gnoise, ~40 min of reference CPU time) is compared against SHA-256
+  digests of the reference's outputs, committed in tests/golden/config3_digests.json
+  by tests/golden/make_config_digests.py (oracle/config_digest.cpp).
+* "wide_ids" forces the 64-bit cell-id lists grids with >= 2^32 cells use (configs
+  4-5; the reference rejects them, grid.cpp:17-20) on small grids, so that path is
+  compared with the reference too.
+* "kahn_switch_below" moves the hand-off between the counting kernel's two launch
+  configurations (dag.cu) so both, and the hand-off itself, run at test sizes.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2009_03707_b200 as m
+from tests.fields import quantized, random_field
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CONFIGS = {1: ("gauss", (64, 64, 64)), 2: ("gauss", (256, 256, 256)), 3: ("gnoise", (512, 512, 512))}
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _device_outputs(ctx, values, dims):
+    got = m.compute(values, dims, with_segmentation=True, ctx=ctx)
+    return {
+        "codes": ctx.get("codes"),
+        "crit": [ctx.get(f"crit{k}") for k in range(4)],
+        "cp_cell": got.cp_cell,
+        "cp_index": got.cp_index.astype(np.int32),
+        "cp_value": ctx.cp_values(),
+        "arc_src": got.arc_src,
+        "arc_dst": got.arc_dst,
+        "arc_mult": got.arc_mult,
+        "labels_min": got.labels_min,
+        "labels_max": got.labels_max,
+        "input_hash": got.input_hash,
+    }
+
+
+def _assert_same(got, ref, values, dims):
+    want = ref.compute(np.asarray(values, np.float64), dims, with_segmentation=True)
+    codes = ref.gradient(np.asarray(values, np.float64), dims)
+    np.testing.assert_array_equal(got["codes"], codes)
+    for k, c in enumerate(ref.critical(codes, dims)):
+        np.testing.assert_array_equal(got["crit"][k].astype(np.uint64), c.astype(np.uint64))
+    np.testing.assert_array_equal(got["cp_cell"].astype(np.uint64), want["cp_cell"].astype(np.uint64))
+    np.testing.assert_array_equal(got["cp_index"], want["cp_index"])
+    np.testing.assert_array_equal(got["cp_value"], want["cp_value"])
+    for k in ("arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    assert got["input_hash"] == want["input_hash"]
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_config_live_equals_reference(ctx, ref, config):
+    kind, dims = CONFIGS[config]
+    v = m.synth(kind, dims)
+    _assert_same(_device_outputs(ctx, v, dims), ref, v, dims)
+
+
+@pytest.mark.parametrize("config", [1, 2, 3])
+def test_config_digests_equal_reference(ctx, config):
+    path = os.path.join(GOLDEN, f"config{config}_digests.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    with open(path) as fh:
+        want = json.load(fh)
+    kind, dims = CONFIGS[config]
+    got = _device_outputs(ctx, m.synth(kind, dims), dims)
+    assert got["input_hash"] == want["input_hash"]
+    assert len(got["cp_cell"]) == want["n_cp"] and len(got["arc_src"]) == want["n_arcs"]
+    assert int(got["arc_mult"].max()) == want["max_mult"]
+    for k in range(4):
+        assert len(got["crit"][k]) == want[f"n_crit{k}"]
+        assert _sha(got["crit"][k]) == want[f"crit{k}"], f"crit{k}"
+    for k in ("codes", "cp_cell", "cp_index", "cp_value", "arc_src", "arc_dst", "arc_mult",
+              "labels_min", "labels_max"):
+        assert _sha(got[k]) == want[k], k
+
+
+WIDE_CASES = [
+    ("noise", (8, 8, 8), 1),
+    ("noise", (10, 9, 8), 93),
+    ("ties", (9, 8, 7), 5),
+    ("gnoise", (40, 36, 33), 1),
+    ("gauss", (48, 48, 48), 1),
+]
+
+
+def _field(ref, kind, dims, seed):
+    if kind == "noise":
+        return random_field(ref, dims, seed)
+    if kind == "ties":
+        return quantized(dims, 3, seed)
+    return m.synth(kind, dims, seed=seed)
+
+
+@pytest.fixture()
+def wide_ctx():
+    c = m.Context(0)
+    c.set_option("wide_ids", 1)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("kind,dims,seed", WIDE_CASES)
+def test_wide_ids_compute_equals_reference(wide_ctx, ref, kind, dims, seed):
+    v = _field(ref, kind, dims, seed)
+    got = _device_outputs(wide_ctx, v, dims)
+    assert got["cp_cell"].dtype == np.uint64 and got["crit"][1].dtype == np.uint64
+    _assert_same(got, ref, v, dims)
+
+
+@pytest.mark.parametrize("kind,dims,seed", WIDE_CASES[:3])
+def test_wide_ids_stages_equal_reference(wide_ctx, ref, kind, dims, seed):
+    v = np.asarray(_field(ref, kind, dims, seed), np.float64)
+    codes = ref.gradient(v, dims)
+    crit = ref.critical(codes, dims)
+    wide_ctx.load_codes(codes, dims).critical()
+    for k in range(4):
+        np.testing.assert_array_equal(wide_ctx.get(f"crit{k}"), crit[k].astype(np.uint64))
+    wide_ctx.mark(crit[1].astype(np.uint64))
+    marked, ones, twos = ref.mark(codes, dims, crit[1])
+    np.testing.assert_array_equal(wide_ctx.get("marked"), marked)
+    np.testing.assert_array_equal(wide_ctx.get("one_saddles"), ones.astype(np.uint64))
+    np.testing.assert_array_equal(wide_ctx.get("two_saddles"), twos.astype(np.uint64))
+    wide_ctx.count()
+    a, b, p = ref.count_paths(ref.minor(codes, dims, marked, ones, twos))
+    np.testing.assert_array_equal(wide_ctx.get("ss_one"), a.astype(np.uint64))
+    np.testing.assert_array_equal(wide_ctx.get("ss_two"), b.astype(np.uint64))
+    np.testing.assert_array_equal(wide_ctx.get("ss_paths"), p)
+
+
+@pytest.mark.parametrize("switch_below", [1, 64, 1 << 40])
+@pytest.mark.parametrize("kind,dims", [("gnoise", (48, 48, 48)), ("noise", (64, 64, 64)),
+                                       ("gauss", (64, 64, 64))])
+def test_kahn_switch_threshold(ref, switch_below, kind, dims):
+    v = m.synth(kind, dims)
+    with m.Context(0) as c:
+        c.set_option("kahn_switch_below", switch_below)
+        got = m.compute(v, dims, with_segmentation=False, ctx=c)
+    want = ref.compute(v.astype(np.float64), dims, with_segmentation=False)
+    for k in ("arc_src", "arc_dst", "arc_mult"):
+        np.testing.assert_array_equal(getattr(got, k), want[k], err_msg=k)
+
+
+def test_set_option_rejects_unknown(ctx):
+    with pytest.raises(ValueError):
+        ctx.set_option("no_such_option", 1)
+    with pytest.raises(ValueError):
+        ctx.set_option("kahn_switch_below", 0)
