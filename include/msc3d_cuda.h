@@ -4,7 +4,7 @@
  * This is the drop-in boundary under the reference library's public C++ API
  * (/root/reference/proj/include/msc3d/*.hpp).  The reference has no FFI of its
  * own; its "operator API" is those headers.  Our C++ layer
- * (paper_2009_03707_b200/csrc/msc3d_api.cpp, header include/msc3d/msc3d_b200.hpp)
+ * (paper_2009_03707_b200/csrc/msc3d_api.cpp, header include/msc3d/api.hpp)
  * keeps the reference's signatures and calls the functions below; Python (ctypes)
  * calls them directly.  No C++ or torch types cross this boundary: plain
  * pointers, sizes, int status codes.  No exceptions cross it either: the C++

@@ -117,40 +117,14 @@ namespace msc3d_dev {
 int launch_bfs_sources(const std::uint8_t* codes, const Dims& d, const void* src, std::uint64_t n,
                        int id_width, unsigned int* bitmap, std::uint32_t* frontier, unsigned int* bad,
                        cudaStream_t s, int num_sms);
-int launch_bfs_persistent(const std::uint8_t* codes, const Dims& d, unsigned int* bitmap,
-                          std::uint32_t* fa, std::uint32_t* fb, unsigned long long* cnt,
-                          unsigned long long* stats, cudaStream_t s, int num_sms);
 int launch_marked_bytes(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
                         std::uint64_t nwords, std::uint8_t* marked, cudaStream_t s, int num_sms);
 int launch_scatter_quad_rank(const void* list, std::uint64_t n, int id_width, const Dims& d,
                              std::uint32_t* tmap, cudaStream_t s, int num_sms);
-int launch_junction_count(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
-                          std::uint64_t nwords, std::uint32_t* per_word, cudaStream_t s, int num_sms);
-int launch_junction_write(const std::uint8_t* codes, const Dims& d, const unsigned int* bitmap,
-                          std::uint64_t nwords, const std::uint64_t* off, std::uint32_t* jlist,
-                          std::uint32_t* jidx, cudaStream_t s, int num_sms);
 int launch_origin_dests(const std::uint8_t* codes, const Dims& d, const std::uint32_t* jlist,
                         const void* srcs, int id_width, std::uint64_t n, const std::uint32_t* jidx,
                         const std::uint32_t* tmap, std::uint32_t* dest, std::uint32_t* pending,
                         std::uint32_t* indeg, unsigned int* flags, cudaStream_t s, int num_sms);
-int launch_fill_rev(const std::uint32_t* dest, std::uint64_t nj, const std::uint64_t* roff,
-                    std::uint32_t* cursor, std::uint32_t* rsrc, cudaStream_t s, int num_sms);
-int launch_initial_frontier(const std::uint32_t* pending, std::uint64_t nj, std::uint32_t* frontier,
-                            unsigned long long* count, cudaStream_t s, int num_sms);
-int launch_kahn_persistent(const std::uint32_t* dest, std::uint64_t* poff, std::uint32_t* plen,
-                           std::uint32_t* pkey, std::uint64_t* pcnt, unsigned long long* ptop,
-                           std::uint64_t pcap, const std::uint64_t* roff, const std::uint32_t* rcnt,
-                           const std::uint32_t* rsrc, std::uint32_t* pending, std::uint32_t* fa,
-                           std::uint32_t* fb, unsigned long long* cnt, unsigned int* flags,
-                           unsigned long long* stats, cudaStream_t s, int num_sms);
-int launch_source_len(const std::uint32_t* dest, std::uint64_t n1, const std::uint64_t* poff,
-                      const std::uint32_t* plen, const std::uint32_t* pkey, const std::uint64_t* pcnt,
-                      std::uint32_t* len, unsigned int* flags, cudaStream_t s, int num_sms);
-int launch_source_write(const std::uint32_t* dest, std::uint64_t n1, const std::uint64_t* poff,
-                        const std::uint32_t* plen, const std::uint32_t* pkey,
-                        const std::uint64_t* pcnt, const std::uint64_t* off, std::uint32_t* o_one,
-                        std::uint32_t* o_two, std::uint64_t* o_cnt, unsigned int* flags,
-                        cudaStream_t s, int num_sms);
 }  // namespace msc3d_dev
 
 namespace msc3d_dev {

@@ -6,8 +6,8 @@
 //     engine -- every output row is the sum of scaled input rows (a terminal
 //     contributes a single (key, mult) entry): expand -> segmented sort -> reduce,
 //     exact u64 with sticky overflow.
-// The whole-field pipeline (compute) does not use this engine; it runs the fused
-// walk + Kahn kernels of saddle.cu.
+// The whole-field pipeline (compute) does not use this engine; it runs the branch
+// walks and the Kahn counting kernels of dag.cu.
 #include <algorithm>
 #include <cstring>
 #include <map>

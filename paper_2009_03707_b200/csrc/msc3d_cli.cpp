@@ -1,21 +1,21 @@
-// msc3d -- command-line driver of the B200 build, mirroring the reference CLI
-// (proj/tools/msc3d_cli.cpp): the same flags, outputs and exit codes
-// (0 ok, 1 usage, 2 i/o, 3 invalid input / failed --check, 4 overflow,
-// msc3d_cli.cpp:137-166), on top of the drop-in C++ API (include/msc3d/api.hpp).
-// The reference parses flags with CLI11 (not in this image); this is a small
-// hand-rolled parser for the same flag set.
+// msc3d -- command-line front end of the B200 build.
+//
+// Flag set and exit-code contract follow the reference CLI (proj/tools/msc3d_cli.cpp:
+// 99-166): 0 ok, 1 usage, 2 i/o, 3 invalid input or a failed --check, 4 path-count
+// overflow.  Everything below the argument table is the drop-in C++ API
+// (include/msc3d/api.hpp), i.e. the device pipeline.
 //
 //   msc3d --input v.raw --dims NX NY NZ [--dtype u8|u16|f32|f64] [--big-endian]
 //         --out PATH [--format json|csv] [--labels PREFIX] [--check] [--threads N]
 //   msc3d generate --kind gauss|gnoise|noise --dims NX NY NZ --out v.raw [--seed S]
 //
-// `generate` writes the BASELINE synthetic fields (f32 little-endian, SURVEY.md §8(d)
-// generator) -- the reference's own generator kinds (ramp, two-bumps, ...) are out of
-// scope.
+// `generate` writes the BASELINE synthetic fields (f32 little-endian);
+// the reference's own f64 generator kinds are out of scope.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
-#include <fstream>
+#include <functional>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -27,185 +27,181 @@ extern "C" int msc3d_synth_f32(const char* kind, std::int64_t nx, std::int64_t n
 
 namespace {
 
-using namespace msc3d;
+enum Exit : int { kOk = 0, kUsage = 1, kIo = 2, kInvalid = 3, kOverflow = 4 };
 
-struct Usage : std::runtime_error {
+struct BadUsage : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-void write_text(const std::string& path, const std::string& bytes) {
-    std::ofstream out(path, std::ios::binary | std::ios::trunc);
-    if (!out) throw IoError("cannot open '" + path + "' for writing");
-    out.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
-    out.flush();
-    if (!out) throw IoError("write failed on '" + path + "'");
-}
+struct Options {
+    bool generate = false;
+    std::string input, out, format = "json", dtype = "f64", labels, kind;
+    std::vector<std::int64_t> dims;
+    bool big_endian = false, check = false, help = false;
+    int threads = 0;
+    std::uint64_t seed = 1;
+};
 
-void print_timings(const StageTimings& t) {
-    std::fprintf(stderr, "stage         seconds\n");
-    std::fprintf(stderr, "gradient      %9.3f\n", t.gradient);
-    std::fprintf(stderr, "critical      %9.3f\n", t.critical);
-    std::fprintf(stderr, "extrema       %9.3f\n", t.extrema);
-    std::fprintf(stderr, "reachability  %9.3f\n", t.reachability);
-    std::fprintf(stderr, "counting      %9.3f\n", t.counting);
-}
-
-int run_compute(const VolumeSpec& spec, const std::string& out, const std::string& format,
-                const std::string& labels_prefix, bool check, int threads) {
-    const ScalarField f = read_volume(spec);
-    StageTimings timings;
-    ComputeOptions opt;
-    opt.threads = threads;
-    opt.with_segmentation = !labels_prefix.empty();
-    opt.validate = check;
-    opt.source_dtype = sample_type_name(spec.dtype);
-    opt.timings = &timings;
-    const MSComplex m = compute(f, opt);
-    print_timings(timings);
-    std::fprintf(stderr,
-                 "critical points: %zu (minima %llu, 1-saddles %llu, 2-saddles %llu, maxima %llu); arcs: %zu\n",
-                 m.critical_points.size(), static_cast<unsigned long long>(m.count_by_index(0)),
-                 static_cast<unsigned long long>(m.count_by_index(1)),
-                 static_cast<unsigned long long>(m.count_by_index(2)),
-                 static_cast<unsigned long long>(m.count_by_index(3)), m.arcs.size());
-    if (check) {
-        bool ok = true;
-        if (m.euler() != 1) {
-            std::fprintf(stderr, "check: Euler characteristic is %lld, want 1\n", static_cast<long long>(m.euler()));
-            ok = false;
-        }
-        const BoundaryReport report = boundary_check(m);
-        if (!report.ok()) {
-            std::fprintf(stderr, "check: %zu critical point pairs fail mod-2 boundary consistency\n",
-                         report.odd_pairs.size());
-            ok = false;
-        }
-        std::fprintf(stderr, "check: gradient ok, euler %s, boundary %s\n", m.euler() == 1 ? "ok" : "BAD",
-                     report.ok() ? "ok" : "BAD");
-        if (!ok) return 3;
-    }
-    if (format == "json") {
-        write_text(out, serialize_json(m));
-    } else {
-        write_text(out + "_critical_points.csv", critical_points_csv(m));
-        write_text(out + "_arcs.csv", arcs_csv(m));
-    }
-    if (!labels_prefix.empty()) {
-        write_text(labels_prefix + "_min.raw", label_volume_bytes(m.labels->vertex_to_min));
-        write_text(labels_prefix + "_max.raw", label_volume_bytes(m.labels->cube_to_max));
-    }
-    return 0;
-}
-
-int run_generate(const std::string& kind, const std::vector<std::int64_t>& dims, const std::string& out,
-                 std::uint64_t seed) {
-    if (kind != "gauss" && kind != "gnoise" && kind != "noise") throw Usage("--kind must be gauss, gnoise or noise");
-    const GridDims gd(dims[0], dims[1], dims[2]);  // the reference's size checks
-    if (!msc3d_synth_f32) throw std::runtime_error("synthesizer library not linked");
-    std::vector<float> v(static_cast<std::size_t>(gd.nx * gd.ny * gd.nz));
-    if (msc3d_synth_f32(kind.c_str(), gd.nx, gd.ny, gd.nz, seed, v.data(), 0) != 0)
-        throw std::runtime_error("synthesis failed");
-    write_text(out, std::string(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(float)));
-    std::fprintf(stderr, "wrote %s: %s %lldx%lldx%lld f32 little-endian\n", out.c_str(), kind.c_str(),
-                 static_cast<long long>(gd.nx), static_cast<long long>(gd.ny), static_cast<long long>(gd.nz));
-    return 0;
-}
-
-std::int64_t to_int(const std::string& s, const char* flag) {
+std::int64_t parse_int(const std::string& text, const std::string& flag) {
     char* end = nullptr;
-    const long long v = std::strtoll(s.c_str(), &end, 10);
-    if (s.empty() || *end) throw Usage(std::string(flag) + ": not an integer: " + s);
+    const long long v = std::strtoll(text.c_str(), &end, 10);
+    if (text.empty() || *end != '\0') throw BadUsage(flag + ": expected an integer, got '" + text + "'");
     return v;
 }
+
+std::string one_of(const std::string& v, const std::vector<std::string>& allowed, const std::string& flag) {
+    for (const auto& a : allowed)
+        if (v == a) return v;
+    std::string list;
+    for (const auto& a : allowed) list += (list.empty() ? "" : "|") + a;
+    throw BadUsage(flag + " must be " + list);
+}
+
+// Table of flags: name -> number of values and the action storing them.
+Options parse(int argc, char** argv) {
+    Options o;
+    using Act = std::function<void(const std::vector<std::string>&)>;
+    const std::map<std::string, std::pair<int, Act>> table = {
+        {"--input", {1, [&](auto& v) { o.input = v[0]; }}},
+        {"--out", {1, [&](auto& v) { o.out = v[0]; }}},
+        {"--labels", {1, [&](auto& v) { o.labels = v[0]; }}},
+        {"--kind", {1, [&](auto& v) { o.kind = v[0]; }}},
+        {"--dtype", {1, [&](auto& v) { o.dtype = one_of(v[0], {"u8", "u16", "f32", "f64"}, "--dtype"); }}},
+        {"--format", {1, [&](auto& v) { o.format = one_of(v[0], {"json", "csv"}, "--format"); }}},
+        {"--dims", {3, [&](auto& v) { for (const auto& s : v) o.dims.push_back(parse_int(s, "--dims")); }}},
+        {"--threads", {1, [&](auto& v) {
+             o.threads = static_cast<int>(parse_int(v[0], "--threads"));
+             if (o.threads < 0) throw BadUsage("--threads must be >= 0");
+         }}},
+        {"--seed", {1, [&](auto& v) { o.seed = static_cast<std::uint64_t>(parse_int(v[0], "--seed")); }}},
+        {"--big-endian", {0, [&](auto&) { o.big_endian = true; }}},
+        {"--check", {0, [&](auto&) { o.check = true; }}},
+        {"--help", {0, [&](auto&) { o.help = true; }}},
+        {"-h", {0, [&](auto&) { o.help = true; }}},
+    };
+    int i = 1;
+    if (i < argc && std::string(argv[i]) == "generate") {
+        o.generate = true;
+        ++i;
+    }
+    while (i < argc) {
+        const auto it = table.find(argv[i]);
+        if (it == table.end()) throw BadUsage(std::string("unknown argument: ") + argv[i]);
+        const int want = it->second.first;
+        if (i + want > argc - 1)
+            throw BadUsage(it->first + " expects " + std::to_string(want) + " value(s)");
+        std::vector<std::string> vals(argv + i + 1, argv + i + 1 + want);
+        it->second.second(vals);
+        i += 1 + want;
+    }
+    return o;
+}
+
+void save(const std::string& path, const std::string& bytes) {
+    std::FILE* fh = std::fopen(path.c_str(), "wb");
+    if (!fh) throw msc3d::IoError("cannot create " + path);
+    const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), fh) == bytes.size();
+    if (std::fclose(fh) != 0 || !ok) throw msc3d::IoError("short write to " + path);
+}
+
+int cmd_generate(const Options& o) {
+    if (o.kind.empty() || o.dims.size() != 3 || o.out.empty())
+        throw BadUsage("generate needs --kind, --dims NX NY NZ and --out");
+    one_of(o.kind, {"gauss", "gnoise", "noise"}, "--kind");
+    const msc3d::GridDims g(o.dims[0], o.dims[1], o.dims[2]);  // the reference's dimension checks
+    if (!msc3d_synth_f32) throw std::runtime_error("libmsc3d_synth not linked");
+    std::string raw(static_cast<std::size_t>(g.vertex_count()) * sizeof(float), '\0');
+    if (msc3d_synth_f32(o.kind.c_str(), g.nx, g.ny, g.nz, o.seed, reinterpret_cast<float*>(&raw[0]), 0) != 0)
+        throw std::runtime_error("field synthesis failed");
+    save(o.out, raw);
+    std::fprintf(stderr, "generate: %s %lld x %lld x %lld (f32 LE) -> %s\n", o.kind.c_str(),
+                 static_cast<long long>(g.nx), static_cast<long long>(g.ny), static_cast<long long>(g.nz),
+                 o.out.c_str());
+    return kOk;
+}
+
+int cmd_compute(const Options& o) {
+    if (o.input.empty() || o.out.empty() || o.dims.size() != 3)
+        throw BadUsage("need --input FILE --dims NX NY NZ --out PATH (or `generate`); see --help");
+    msc3d::VolumeSpec spec;
+    spec.path = o.input;
+    spec.dims = msc3d::GridDims(o.dims[0], o.dims[1], o.dims[2]);
+    spec.dtype = msc3d::parse_sample_type(o.dtype);
+    spec.big_endian = o.big_endian;
+    const msc3d::ScalarField field = msc3d::read_volume(spec);
+
+    msc3d::StageTimings t;
+    msc3d::ComputeOptions copt;
+    copt.threads = o.threads;
+    copt.with_segmentation = !o.labels.empty();
+    copt.validate = o.check;
+    copt.source_dtype = msc3d::sample_type_name(spec.dtype);
+    copt.timings = &t;
+    const msc3d::MSComplex cx = msc3d::compute(field, copt);
+
+    std::fprintf(stderr, "device stage seconds: gradient %.4f | critical %.4f | extrema %.4f | "
+                         "reachability %.4f | counting %.4f\n",
+                 t.gradient, t.critical, t.extrema, t.reachability, t.counting);
+    std::fprintf(stderr, "complex: %zu critical points [%llu %llu %llu %llu], %zu arcs\n",
+                 cx.critical_points.size(), static_cast<unsigned long long>(cx.count_by_index(0)),
+                 static_cast<unsigned long long>(cx.count_by_index(1)),
+                 static_cast<unsigned long long>(cx.count_by_index(2)),
+                 static_cast<unsigned long long>(cx.count_by_index(3)), cx.arcs.size());
+
+    if (o.check) {  // the gradient audit already ran inside compute (validate)
+        const bool euler_ok = cx.euler() == 1;
+        const msc3d::BoundaryReport br = msc3d::boundary_check(cx);
+        std::fprintf(stderr, "check: euler=%lld (%s), mod-2 boundary: %zu odd pairs (%s)\n",
+                     static_cast<long long>(cx.euler()), euler_ok ? "ok" : "FAIL", br.odd_pairs.size(),
+                     br.ok() ? "ok" : "FAIL");
+        if (!euler_ok || !br.ok()) return kInvalid;
+    }
+
+    if (o.format == "csv") {
+        save(o.out + "_critical_points.csv", msc3d::critical_points_csv(cx));
+        save(o.out + "_arcs.csv", msc3d::arcs_csv(cx));
+    } else {
+        save(o.out, msc3d::serialize_json(cx));
+    }
+    if (cx.labels) {
+        save(o.labels + "_min.raw", msc3d::label_volume_bytes(cx.labels->vertex_to_min));
+        save(o.labels + "_max.raw", msc3d::label_volume_bytes(cx.labels->cube_to_max));
+    }
+    return kOk;
+}
+
+const char* kHelp =
+    "usage: msc3d --input FILE --dims NX NY NZ --out PATH [--dtype u8|u16|f32|f64] [--big-endian]\n"
+    "             [--format json|csv] [--labels PREFIX] [--check] [--threads N]\n"
+    "       msc3d generate --kind gauss|gnoise|noise --dims NX NY NZ --out FILE [--seed S]\n";
 
 }  // namespace
 
 int main(int argc, char** argv) {
-    std::string input, out, format = "json", dtype = "f64", labels_prefix, kind;
-    std::vector<std::int64_t> dims;
-    bool big_endian = false, check = false, generate = false;
-    int threads = 0;
-    std::uint64_t seed = 1;
+    Options o;
     try {
-        int i = 1;
-        if (i < argc && std::string(argv[i]) == "generate") {
-            generate = true;
-            ++i;
-        }
-        auto need = [&](const char* flag) -> std::string {
-            if (i + 1 >= argc) throw Usage(std::string(flag) + " needs a value");
-            return argv[++i];
-        };
-        for (; i < argc; ++i) {
-            const std::string a = argv[i];
-            if (a == "--help" || a == "-h") {
-                std::printf("usage: msc3d --input FILE --dims NX NY NZ --out PATH [--dtype u8|u16|f32|f64] "
-                            "[--big-endian] [--format json|csv] [--labels PREFIX] [--check] [--threads N]\n"
-                            "       msc3d generate --kind gauss|gnoise|noise --dims NX NY NZ --out FILE [--seed S]\n");
-                return 0;
-            } else if (a == "--input") {
-                input = need("--input");
-            } else if (a == "--dims") {
-                for (int k = 0; k < 3; ++k) dims.push_back(to_int(need("--dims"), "--dims"));
-            } else if (a == "--dtype") {
-                dtype = need("--dtype");
-                if (dtype != "u8" && dtype != "u16" && dtype != "f32" && dtype != "f64")
-                    throw Usage("--dtype must be u8, u16, f32 or f64");
-            } else if (a == "--big-endian") {
-                big_endian = true;
-            } else if (a == "--out") {
-                out = need("--out");
-            } else if (a == "--format") {
-                format = need("--format");
-                if (format != "json" && format != "csv") throw Usage("--format must be json or csv");
-            } else if (a == "--labels") {
-                labels_prefix = need("--labels");
-            } else if (a == "--check") {
-                check = true;
-            } else if (a == "--threads") {
-                threads = static_cast<int>(to_int(need("--threads"), "--threads"));
-                if (threads < 0) throw Usage("--threads must be >= 0");
-            } else if (a == "--seed") {
-                seed = static_cast<std::uint64_t>(to_int(need("--seed"), "--seed"));
-            } else if (a == "--kind") {
-                kind = need("--kind");
-            } else {
-                throw Usage("unknown argument: " + a);
-            }
-        }
-    } catch (const Usage& e) {
-        std::fprintf(stderr, "%s\n", e.what());
-        return 1;
+        o = parse(argc, argv);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "msc3d: %s\n%s", e.what(), kHelp);
+        return kUsage;
+    }
+    if (o.help) {
+        std::fputs(kHelp, stdout);
+        return kOk;
     }
     try {
-        if (generate) {
-            if (kind.empty() || dims.size() != 3 || out.empty()) {
-                std::fprintf(stderr, "usage: generate needs --kind, --dims and --out\n");
-                return 1;
-            }
-            return run_generate(kind, dims, out, seed);
-        }
-        if (input.empty() || out.empty() || dims.size() != 3) {
-            std::fprintf(stderr, "usage: need --input, --dims and --out (or the generate subcommand); see --help\n");
-            return 1;
-        }
-        VolumeSpec spec;
-        spec.path = input;
-        spec.dims = GridDims(dims[0], dims[1], dims[2]);
-        spec.dtype = parse_sample_type(dtype);
-        spec.big_endian = big_endian;
-        return run_compute(spec, out, format, labels_prefix, check, threads);
-    } catch (const Usage& e) {
-        std::fprintf(stderr, "%s\n", e.what());
-        return 1;
-    } catch (const IoError& e) {
-        std::fprintf(stderr, "i/o error: %s\n", e.what());
-        return 2;
+        return o.generate ? cmd_generate(o) : cmd_compute(o);
+    } catch (const BadUsage& e) {
+        std::fprintf(stderr, "msc3d: %s\n", e.what());
+        return kUsage;
+    } catch (const msc3d::IoError& e) {
+        std::fprintf(stderr, "msc3d: i/o: %s\n", e.what());
+        return kIo;
     } catch (const std::overflow_error& e) {
-        std::fprintf(stderr, "overflow: %s\n", e.what());
-        return 4;
+        std::fprintf(stderr, "msc3d: overflow: %s\n", e.what());
+        return kOverflow;
     } catch (const std::exception& e) {
-        std::fprintf(stderr, "invalid input: %s\n", e.what());
-        return 3;
+        std::fprintf(stderr, "msc3d: %s\n", e.what());
+        return kInvalid;
     }
 }

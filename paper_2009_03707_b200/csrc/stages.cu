@@ -109,27 +109,6 @@ int roots_sync(msc3d_ctx* ctx, int dim) {
     return MSC3D_OK;
 }
 
-// Roots for the pipeline: in-place jumping on the parent array itself (it becomes
-// the label array).  Checks convergence every round.
-int roots_fast(msc3d_ctx* ctx, int dim) {
-    const std::string pn = dim == 0 ? "parent0" : "parent3";
-    const std::uint64_t n = ctx->count(pn);
-    auto* p = ctx->ptr<std::uint32_t>(pn);
-    auto* changed = reinterpret_cast<unsigned int*>(ctx->d_small + 16 + dim);
-    int rounds = 0;
-    while (n) {
-        MSC3D_CUDA_TRY(cudaMemsetAsync(changed, 0, 4, ctx->stream));
-        TRY(msc3d_dev::launch_jump_round(p, n, changed, ctx->stream, ctx->num_sms));
-        TRY(ctx->fetch_range(16 + dim, 1));
-        const unsigned int h = static_cast<unsigned int>(ctx->h_small[16 + dim] & 0xffffffffu);
-        ++rounds;
-        if (!h) break;
-        if (rounds > 64) return MSC3D_ERR_RUNTIME;
-    }
-    ctx->scalars[dim == 0 ? "jump_rounds0" : "jump_rounds3"] = rounds;
-    return MSC3D_OK;
-}
-
 int se_arcs(msc3d_ctx* ctx) {
     const Dims& d = ctx->dims;
     const auto* codes = ctx->ptr<std::uint8_t>("codes");

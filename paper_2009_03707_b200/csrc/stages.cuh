@@ -11,7 +11,6 @@ int gradient(msc3d_ctx* ctx, bool with_forests);
 int critical(msc3d_ctx* ctx);
 int forest(msc3d_ctx* ctx, int dim);
 int roots_sync(msc3d_ctx* ctx, int dim);
-int roots_fast(msc3d_ctx* ctx, int dim);
 int se_arcs(msc3d_ctx* ctx);
 int mark(msc3d_ctx* ctx, const void* host_sources, std::uint64_t n_sources);
 int minor(msc3d_ctx* ctx);

@@ -55,7 +55,7 @@ def test_cli_compute_matches_reference(tmp_path, ref):
     np.testing.assert_array_equal(arcs[:, 2], np.asarray(want["arc_mult"], dtype=np.uint64))
     np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_min.raw", dtype="<u4"), want["labels_min"])
     np.testing.assert_array_equal(np.fromfile(tmp_path / "lab_max.raw", dtype="<u4"), want["labels_max"])
-    assert "check: gradient ok, euler ok, boundary ok" in r.stderr
+    assert "check: euler=1 (ok), mod-2 boundary: 0 odd pairs (ok)" in r.stderr
     r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--out", tmp_path / "c.json")
     assert r.returncode == 0 and (tmp_path / "c.json").stat().st_size > 0
 
