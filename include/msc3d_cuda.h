@@ -130,6 +130,20 @@ int msc3d_ctx_load_parent(msc3d_ctx* ctx, int dim, const uint32_t* host_parent, 
 int msc3d_ctx_se_arcs(msc3d_ctx* ctx);
 int msc3d_ctx_load_labels(msc3d_ctx* ctx, const uint32_t* host_label0, const uint32_t* host_label3);
 
+/* ---- audits (gradient.cpp:299-377, msc.cpp:149-167), all on the device ------------------ */
+/* validate_gradient of the context's codes: out = {matching_violations,
+ * cells_in_closed_vpath, acyclicity_checked, degenerate} (GradientReport,
+ * gradient.hpp:83-91); the acyclicity (Kahn peeling of the V-path relation) runs only
+ * when the lattice has <= max_cells_for_cycles cells, as the reference.  Offending cells
+ * (up to 4096) in array "audit_samples". */
+int msc3d_ctx_validate_gradient(msc3d_ctx* ctx, uint64_t max_cells_for_cycles, uint64_t out[4]);
+/* boundary_check of the last compute's complex ("cp_index", "arc_*"): *n_odd odd
+ * (top, low) pairs in "odd_top" / "odd_low" (u32 cp ids), ordered by top, then low. */
+int msc3d_ctx_boundary_check(msc3d_ctx* ctx, uint64_t* n_odd);
+/* The same on a complex given as host arrays (cp_index per critical point, arcs). */
+int msc3d_boundary_check_host(msc3d_ctx* ctx, uint64_t n_cp, const uint8_t* cp_index, uint64_t n_arcs,
+                              const uint32_t* src, const uint32_t* dst, const uint64_t* mult, uint64_t* n_odd);
+
 /* ---- saddle graph (saddle_graph.hpp:39-74) ------------------------------------------- */
 /* mark_reachable from the given 1-saddles (host ids, width msc3d_id_width); NULL/0 =
  * all critical 1-cells.  -> "marked" (u8, N), "one_saddles", "two_saddles". */

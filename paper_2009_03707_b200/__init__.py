@@ -97,6 +97,9 @@ def lib():
         "msc3d_ctx_compute_host_values": (i32, [vp, Dims, i32, vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_ctx_compute_codes": (i32, [vp, i32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
         "msc3d_ctx_cp_values": (i32, [vp]),
+        "msc3d_ctx_validate_gradient": (i32, [vp, u64, C.POINTER(u64)]),
+        "msc3d_ctx_boundary_check": (i32, [vp, C.POINTER(u64)]),
+        "msc3d_boundary_check_host": (i32, [vp, u64, vp, u64, vp, vp, vp, C.POINTER(u64)]),
         "msc3d_field_hash_f64": (u64, [vp, u64]),
         "msc3d_field_hash_f32": (u64, [vp, u64]),
     }
@@ -202,6 +205,34 @@ class Context:
     def ids(self, dims):
         """dtype of host cell-id arrays this context takes / returns for `dims`."""
         return np.uint64 if self.wide else id_dtype(dims)
+
+    def validate_gradient(self, max_cells_for_cycles=100000):
+        """validate_gradient (gradient.hpp:95) of the loaded codes, on the device:
+        GradientReport fields as a dict, samples = up to 32 offending cells."""
+        out = (C.c_uint64 * 4)()
+        _raise(self._L.msc3d_ctx_validate_gradient(self.h, C.c_uint64(max_cells_for_cycles), out),
+               "validate_gradient")
+        samples = np.sort(self.get("audit_samples", np.uint64))[:32]
+        return {"matching_violations": int(out[0]), "cells_in_closed_vpath": int(out[1]),
+                "acyclicity_checked": bool(out[2]), "degenerate": bool(out[3]), "samples": samples}
+
+    def boundary_check(self, cp_index=None, arc_src=None, arc_dst=None, arc_mult=None):
+        """boundary_check (msc.hpp:101) on the device: odd (top, low) cp-id pairs of the
+        last compute's complex, or of the complex given as host arrays."""
+        n = C.c_uint64()
+        if cp_index is None:
+            _raise(self._L.msc3d_ctx_boundary_check(self.h, C.byref(n)), "boundary_check")
+        else:
+            ci = np.ascontiguousarray(cp_index, dtype=np.uint8)
+            a = np.ascontiguousarray(arc_src, dtype=np.uint32)
+            b = np.ascontiguousarray(arc_dst, dtype=np.uint32)
+            c = np.ascontiguousarray(arc_mult, dtype=np.uint64)
+            p = lambda x: x.ctypes.data_as(C.c_void_p)
+            _raise(self._L.msc3d_boundary_check_host(self.h, C.c_uint64(ci.size), p(ci), C.c_uint64(a.size), p(a),
+                                                     p(b), p(c), C.byref(n)), "boundary_check")
+        if n.value == 0:
+            return np.zeros((0, 2), np.uint32)
+        return np.stack([self.get("odd_top"), self.get("odd_low")], axis=1)
 
     def cp_values(self):
         """CriticalPoint::value (msc.cpp:106) of the last compute, f64 per critical point."""

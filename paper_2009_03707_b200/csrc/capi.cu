@@ -372,6 +372,44 @@ int msc3d_sp_op(msc3d_ctx* ctx, int op, std::uint32_t xr, std::uint32_t xc, cons
     return msc3d_stage::sp_op(ctx, op, xr, xc, xp, xcol, xcnt, yr, yc, yp, ycol, ycnt);
 }
 
+int msc3d_ctx_validate_gradient(msc3d_ctx* ctx, std::uint64_t max_cells_for_cycles, std::uint64_t out[4]) {
+    if (!ctx || !out) return MSC3D_ERR_INVALID;
+    return msc3d_stage::audit_gradient(ctx, max_cells_for_cycles, out);
+}
+
+int msc3d_ctx_boundary_check(msc3d_ctx* ctx, std::uint64_t* n_odd) {
+    if (!ctx || !n_odd) return MSC3D_ERR_INVALID;
+    DevArray* idx = ctx->find("cp_index");
+    DevArray* src = ctx->find("arc_src");
+    DevArray* dst = ctx->find("arc_dst");
+    DevArray* mul = ctx->find("arc_mult");
+    if (!idx || !src || !dst || !mul) return MSC3D_ERR_STATE;
+    return msc3d_stage::boundary_check(ctx, idx->count, static_cast<const std::uint8_t*>(idx->ptr), src->count,
+                                       static_cast<const std::uint32_t*>(src->ptr),
+                                       static_cast<const std::uint32_t*>(dst->ptr),
+                                       static_cast<const std::uint64_t*>(mul->ptr), n_odd);
+}
+
+int msc3d_boundary_check_host(msc3d_ctx* ctx, std::uint64_t n_cp, const std::uint8_t* cp_index, std::uint64_t n_arcs,
+                              const std::uint32_t* src, const std::uint32_t* dst, const std::uint64_t* mult,
+                              std::uint64_t* n_odd) {
+    if (!ctx || !n_odd) return MSC3D_ERR_INVALID;
+    for (std::uint64_t i = 0; i < n_arcs; ++i)
+        if (src[i] >= n_cp || dst[i] >= n_cp) return MSC3D_ERR_INVALID;
+    auto* di = static_cast<std::uint8_t*>(ctx->ensure("bc_cp_index", std::max<std::uint64_t>(n_cp, 1), 1));
+    auto* ds = static_cast<std::uint32_t*>(ctx->ensure("bc_src", std::max<std::uint64_t>(n_arcs, 1), 4));
+    auto* dd = static_cast<std::uint32_t*>(ctx->ensure("bc_dst", std::max<std::uint64_t>(n_arcs, 1), 4));
+    auto* dm = static_cast<std::uint64_t*>(ctx->ensure("bc_mult", std::max<std::uint64_t>(n_arcs, 1), 8));
+    if (!di || !ds || !dd || !dm) return MSC3D_ERR_NOMEM;
+    if (n_cp) MSC3D_CUDA_TRY(cudaMemcpyAsync(di, cp_index, n_cp, cudaMemcpyHostToDevice, ctx->stream));
+    if (n_arcs) {
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(ds, src, n_arcs * 4, cudaMemcpyHostToDevice, ctx->stream));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(dd, dst, n_arcs * 4, cudaMemcpyHostToDevice, ctx->stream));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(dm, mult, n_arcs * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return msc3d_stage::boundary_check(ctx, n_cp, di, n_arcs, ds, dd, dm, n_odd);
+}
+
 int msc3d_ctx_minor(msc3d_ctx* ctx) {
     if (!ctx->find("marked")) return MSC3D_ERR_STATE;
     return msc3d_stage::minor(ctx);

@@ -456,51 +456,7 @@ int count_impl(const std::uint8_t* codes, const Dims& d, Pred pred, std::uint64_
     return MSC3D_OK;
 }
 
-// validate_gradient's matching audit (gradient.cpp:299-377) on the device: every
-// cell assigned; every paired cell's partner exists (inside the box), has the
-// dimension one up / one down, and is paired back with it.  bad[0] counts
-// violations.  (Cycles of V-paths are caught by the later stages' guards: the
-// forests' root finding and the saddle walks.)
-__global__ void k_validate_matching(const std::uint8_t* __restrict__ codes, Dims d, unsigned long long* bad) {
-    unsigned long long mine = 0;
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < d.n_cells;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const std::uint8_t k = codes[i];
-        if (k == kCritical) continue;
-        if (k == kUnset || k >= kCofacetBase + 6) {
-            ++mine;
-            continue;
-        }
-        const Coord c = unpack(d, i);
-        const int dir = k - (k < kCofacetBase ? kFacetBase : kCofacetBase), axis = dir >> 1, sgn = (dir & 1) ? 1 : -1;
-        const std::int64_t co[3] = {c.x, c.y, c.z}, ext[3] = {d.ex, d.ey, d.ez};
-        const std::int64_t np = co[axis] + sgn;
-        const bool to_facet = k < kCofacetBase;
-        // a facet lowers an odd coordinate, a cofacet raises an even one
-        if (np < 0 || np >= ext[axis] || ((co[axis] & 1) != (to_facet ? 1 : 0))) {
-            ++mine;
-            continue;
-        }
-        const std::uint8_t kp = codes[partner_of(d, static_cast<std::int64_t>(i), k)];
-        const std::uint8_t want = static_cast<std::uint8_t>((to_facet ? kCofacetBase : kFacetBase) + 2 * axis + (sgn > 0 ? 0 : 1));
-        if (kp != want) ++mine;
-    }
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(bad, mine);
-}
-
 }  // namespace
-
-int launch_validate_matching(const std::uint8_t* codes, const Dims& d, unsigned long long* bad, cudaStream_t s,
-                             int num_sms) {
-    if (d.n_cells == 0) return MSC3D_OK;
-    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>((d.n_cells + kThreads - 1) / kThreads,
-                                                                        static_cast<std::uint64_t>(num_sms) * 32));
-    k_validate_matching<<<grid, kThreads, 0, s>>>(codes, d, bad);
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
 
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
                           cudaStream_t s, int num_sms) {

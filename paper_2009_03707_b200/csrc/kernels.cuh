@@ -51,8 +51,6 @@ int gradient_finish(const void* values, int value_type, const Dims& d, std::uint
 int launch_critical_count(const std::uint8_t* codes, const Dims& d, std::uint64_t* d_totals,
                           cudaStream_t s, int num_sms);
 // validate_gradient's matching audit; *bad (zeroed by the caller) counts violations
-int launch_validate_matching(const std::uint8_t* codes, const Dims& d, unsigned long long* bad, cudaStream_t s,
-                             int num_sms);
 int launch_critical_compact(const std::uint8_t* codes, const Dims& d, Workspace& ws,
                             void* const outs[4], int id_width, std::uint64_t* d_totals,
                             cudaStream_t s);

@@ -300,68 +300,23 @@ CriticalCells extract_critical_cells(const GradientField& g, int) {
     return c;
 }
 
-// Host audit (gradient.cpp:299-377): matching everywhere, closed V-paths on small grids.
+// validate_gradient (gradient.cpp:299-377) on the device (audit.cu): matching over all
+// cells, Kahn peeling of the V-path relation when n <= max_cells_for_cycles.
 GradientReport validate_gradient(const GradientField& g, std::uint64_t max_cells_for_cycles) {
+    if (g.code.size() != g.dims.total_cells()) throw std::invalid_argument("gradient code array size mismatch");
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    upload_codes(dev.ctx, g);
+    std::uint64_t r[4] = {0, 0, 0, 0};
+    check(msc3d_ctx_validate_gradient(dev.ctx, max_cells_for_cycles, r), "validate_gradient");
     GradientReport rep;
-    const GridDims& d = g.dims;
-    const std::uint64_t n = d.total_cells();
-    if (g.code.size() != n) throw std::invalid_argument("gradient code array size mismatch");
-    std::uint64_t pairs = 0;
-    auto flag = [&](CellIndex c) {
-        ++rep.matching_violations;
-        if (rep.samples.size() < 32) rep.samples.push_back(c);
-    };
-    const std::int64_t ext[3] = {d.ex(), d.ey(), d.ez()};
-    for (CellIndex c = 0; c < n; ++c) {
-        const std::uint8_t k = g.code[c];
-        if (k == pair_code::kCritical) continue;
-        if (k == pair_code::kUnset || k >= pair_code::kCofacetBase + 6) {
-            flag(c);
-            continue;
-        }
-        ++pairs;
-        const bool up = k >= pair_code::kCofacetBase;
-        const int dir = k - (up ? pair_code::kCofacetBase : pair_code::kFacetBase);
-        const int axis = dir >> 1, sign = (dir & 1) ? 1 : -1;
-        const CellCoord cc = unpack_cell(d, c);
-        const std::int32_t v[3] = {cc.x, cc.y, cc.z};
-        if (((v[axis] & 1) != 0) == up || v[axis] + sign < 0 || v[axis] + sign >= ext[axis]) {
-            flag(c);
-            continue;
-        }
-        const std::uint8_t want = up ? pair_code::with_facet(axis, -sign) : pair_code::with_cofacet(axis, -sign);
-        if (g.code[g.partner(c)] != want) flag(c);
-    }
-    rep.degenerate = pairs == 0;
-    if (n <= max_cells_for_cycles) {
-        rep.acyclicity_checked = true;
-        std::vector<std::uint32_t> indeg(n, 0);
-        auto each_next = [&](CellIndex a, auto&& fn) {
-            for (CellIndex x : facets(d, g.partner(a)))
-                if (x != a && g.is_paired_with_cofacet(x)) fn(x);
-        };
-        std::uint64_t up_total = 0;
-        for (CellIndex c = 0; c < n; ++c)
-            if (g.is_paired_with_cofacet(c)) {
-                ++up_total;
-                each_next(c, [&](CellIndex x) { ++indeg[x]; });
-            }
-        std::vector<CellIndex> stack;
-        for (CellIndex c = 0; c < n; ++c)
-            if (g.is_paired_with_cofacet(c) && indeg[c] == 0) stack.push_back(c);
-        std::uint64_t peeled = 0;
-        while (!stack.empty()) {
-            const CellIndex c = stack.back();
-            stack.pop_back();
-            ++peeled;
-            each_next(c, [&](CellIndex x) {
-                if (--indeg[x] == 0) stack.push_back(x);
-            });
-        }
-        rep.cells_in_closed_vpath = up_total - peeled;
-        for (CellIndex c = 0; c < n && rep.cells_in_closed_vpath && rep.samples.size() < 32; ++c)
-            if (g.is_paired_with_cofacet(c) && indeg[c] > 0) rep.samples.push_back(c);
-    }
+    rep.matching_violations = r[0];
+    rep.cells_in_closed_vpath = r[1];
+    rep.acyclicity_checked = r[2] != 0;
+    rep.degenerate = r[3] != 0;
+    std::vector<std::uint64_t> samples = fetch<std::uint64_t>(dev.ctx, "audit_samples");
+    std::sort(samples.begin(), samples.end());
+    for (std::size_t i = 0; i < samples.size() && i < 32; ++i) rep.samples.push_back(static_cast<CellIndex>(samples[i]));
     return rep;
 }
 
@@ -643,13 +598,14 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     }
     mark("uploaded");
     double ms[5] = {0, 0, 0, 0, 0};
-    check(msc3d_ctx_compute(dev.ctx, opt.with_segmentation ? MSC3D_OPT_SEGMENTATION : 0, ms), "compute");
+    // ComputeOptions::validate: the device audit runs between the gradient and the
+    // critical stage (msc.cpp:67-70); a broken gradient -> runtime_error
+    check(msc3d_ctx_compute(dev.ctx, (opt.with_segmentation ? MSC3D_OPT_SEGMENTATION : 0) |
+                                         (opt.validate ? MSC3D_OPT_VALIDATE : 0),
+                            ms),
+          "compute");
     check(msc3d_ctx_cp_values(dev.ctx), "critical point values");
     mark("device done");
-    if (opt.validate) {
-        const GradientField g{f.dims, fetch<std::uint8_t>(dev.ctx, "codes")};
-        if (!validate_gradient(g).ok()) throw std::runtime_error("compute: gradient failed validation");
-    }
     if (opt.timings) {
         opt.timings->gradient = ms[0] / 1e3;
         opt.timings->critical = ms[1] / 1e3;
@@ -733,18 +689,28 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     return m;
 }
 
+// boundary_check (msc.cpp:149-167) on the device (audit.cu).
 BoundaryReport boundary_check(const MSComplex& m) {
-    std::vector<std::vector<std::pair<std::uint32_t, std::uint64_t>>> below(m.critical_points.size());
-    for (const Arc& a : m.arcs) below[a.dst].push_back({a.src, a.multiplicity});
-    BoundaryReport r;
-    for (const CriticalPoint& top : m.critical_points) {
-        if (top.index < 2) continue;
-        std::map<std::uint32_t, unsigned> odd;
-        for (const auto& [mid, m1] : below[top.id])
-            for (const auto& [low, m2] : below[mid]) odd[low] ^= static_cast<unsigned>(m1 & m2 & 1);
-        for (const auto& [low, o] : odd)
-            if (o) r.odd_pairs.push_back({top.id, low});
+    const std::size_t n = m.critical_points.size(), na = m.arcs.size();
+    std::vector<std::uint8_t> index(n);
+    for (std::size_t i = 0; i < n; ++i) index[i] = static_cast<std::uint8_t>(m.critical_points[i].index);
+    std::vector<std::uint32_t> src(na), dst(na);
+    std::vector<std::uint64_t> mult(na);
+    for (std::size_t i = 0; i < na; ++i) {
+        src[i] = m.arcs[i].src;
+        dst[i] = m.arcs[i].dst;
+        mult[i] = m.arcs[i].multiplicity;
     }
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    std::uint64_t n_odd = 0;
+    check(msc3d_boundary_check_host(dev.ctx, n, index.data(), na, src.data(), dst.data(), mult.data(), &n_odd),
+          "boundary_check");
+    const std::vector<std::uint32_t> top = fetch<std::uint32_t>(dev.ctx, "odd_top");
+    const std::vector<std::uint32_t> low = fetch<std::uint32_t>(dev.ctx, "odd_low");
+    BoundaryReport r;
+    r.odd_pairs.reserve(n_odd);
+    for (std::uint64_t i = 0; i < n_odd; ++i) r.odd_pairs.push_back({top[i], low[i]});
     return r;
 }
 

@@ -934,16 +934,15 @@ int compute_streamed(msc3d_ctx* ctx, const void* host_values, int value_type, in
     return rc;
 }
 
-// ComputeOptions::validate (msc.cpp:67-70): the gradient's matching audit on the
-// device; a broken gradient -> runtime_error.
+// ComputeOptions::validate (msc.cpp:67-70): validate_gradient with the reference's
+// default cycle-check bound (gradient.hpp:95-96) on the device; a broken gradient ->
+// runtime_error.
 int validate(msc3d_ctx* ctx) {
-    auto* bad = reinterpret_cast<unsigned long long*>(ctx->d_small + 21);
-    MSC3D_CUDA_TRY(cudaMemsetAsync(bad, 0, 8, ctx->stream));
-    TRY(msc3d_dev::launch_validate_matching(ctx->ptr<std::uint8_t>("codes"), ctx->dims, bad, ctx->stream,
-                                            ctx->num_sms));
-    TRY(ctx->fetch_range(21, 1));
-    ctx->scalars["validate_violations"] = static_cast<std::int64_t>(ctx->h_small[21]);
-    return ctx->h_small[21] ? MSC3D_ERR_RUNTIME : MSC3D_OK;
+    std::uint64_t r[4];
+    TRY(audit_gradient(ctx, 100000, r));
+    ctx->scalars["validate_violations"] = static_cast<std::int64_t>(r[0]);
+    ctx->scalars["validate_closed_vpath_cells"] = static_cast<std::int64_t>(r[1]);
+    return (r[0] || r[1]) ? MSC3D_ERR_RUNTIME : MSC3D_OK;
 }
 
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {

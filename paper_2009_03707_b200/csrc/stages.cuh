@@ -22,8 +22,16 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host = nullptr);
 int compute_streamed(msc3d_ctx* ctx, const void* host_values, int value_type, int options, double* stage_ms,
                      const msc3d_host_outputs* host);
-// validate_gradient's matching audit on the device (MSC3D_OPT_VALIDATE)
+// validate_gradient on the device (MSC3D_OPT_VALIDATE; audit.cu)
 int validate(msc3d_ctx* ctx);
+// out = {matching_violations, cells_in_closed_vpath, acyclicity_checked, degenerate}
+// (GradientReport, gradient.hpp:83-91) of the context's codes; offending cells in
+// array "audit_samples"
+int audit_gradient(msc3d_ctx* ctx, std::uint64_t max_cells_for_cycles, std::uint64_t out[4]);
+// boundary_check (msc.cpp:149-167) over device arrays; odd pairs -> "odd_top", "odd_low"
+int boundary_check(msc3d_ctx* ctx, std::uint64_t n_cp, const std::uint8_t* cp_index, std::uint64_t n_arcs,
+                   const std::uint32_t* src, const std::uint32_t* dst, const std::uint64_t* mult,
+                   std::uint64_t* n_odd);
 // sharded == false: sources crit1[a, a + b); true: shard a of b balanced slices
 int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host,
                        bool forests_ready, std::uint64_t a, std::uint64_t b, cudaEvent_t grad_t0,
