@@ -30,6 +30,7 @@
 // extrema.cpp:43-77) and the per-dimension critical counts.
 #include <algorithm>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -48,6 +49,17 @@ struct SlotTables {
 };
 
 __constant__ SlotTables c_slot;
+
+// Octant stars.  A lower star that is exactly one unit cube at the vertex (v, 3 edges,
+// 3 quads, 1 cube -- 93% of the vertices of a smooth field) is paired by Robins'
+// expansion according to the order of its 7 link vertices alone (distinct values;
+// ties take the general path).  g_oct[Lehmer index of that order] holds the result
+// for the canonical orientation (the cube at +x+y+z): for local cell m (bit a set =
+// the cell spans axis a; 0 = v, 7 = the cube) two bits = partner axis + 1, 0 = critical.
+// Reflections map the canonical result onto the other 7 orientations (with distinct
+// values the expansion only compares cells, so it commutes with the reflection).
+constexpr int kOctPerms = 5040;
+__device__ std::uint16_t g_oct[kOctPerms];
 
 SlotTables host_tables() {
     SlotTables s{};
@@ -77,6 +89,93 @@ SlotTables host_tables() {
         s.cofacet[t] = cof;
     }
     return s;
+}
+
+// Robins' expansion (gradient.cpp:196-264) on the canonical octant star for every
+// order of its link vertices: cells compare by their rank masks.
+std::vector<std::uint16_t> host_octant_table() {
+    std::vector<std::uint16_t> table(kOctPerms);
+    int perm[7] = {0, 1, 2, 3, 4, 5, 6};  // perm[i-1] = rank of link vertex i (local index 1..7)
+    const int fact[7] = {720, 120, 24, 6, 2, 1, 1};
+    do {
+        int idx = 0;
+        for (int i = 0; i < 7; ++i) {
+            int c = 0;
+            for (int j = i + 1; j < 7; ++j) c += perm[j] < perm[i];
+            idx += c * fact[i];
+        }
+        std::uint32_t M[8];
+        for (int m = 0; m < 8; ++m) {
+            M[m] = 1u << 7;  // v: the largest
+            for (int i = 1; i < 8; ++i)
+                if ((i & m) == i) M[m] |= 1u << perm[i - 1];
+        }
+        auto facets = [](int m) {
+            std::uint32_t f = 0;
+            for (int a = 0; a < 3; ++a)
+                if (m >> a & 1) f |= 1u << (m ^ (1 << a));
+            return f;
+        };
+        auto cofacets = [](int m) {
+            std::uint32_t f = 0;
+            for (int a = 0; a < 3; ++a)
+                if (!(m >> a & 1)) f |= 1u << (m | (1 << a));
+            return f;
+        };
+        auto argmin = [&](std::uint32_t set) {
+            int best = -1;
+            for (int m = 0; m < 8; ++m)
+                if ((set >> m & 1) && (best < 0 || M[m] < M[best])) best = m;
+            return best;
+        };
+        std::uint32_t assigned = 0, q0 = 0, q1 = 0;
+        int partner[8];
+        for (int m = 0; m < 8; ++m) partner[m] = -2;
+        auto settle = [&](int t) {
+            assigned |= 1u << t;
+            for (int c = 0; c < 8; ++c)
+                if ((cofacets(t) >> c & 1) && !(assigned >> c & 1) &&
+                    __builtin_popcount(facets(c) & ~assigned) == 1)
+                    q1 |= 1u << c;
+        };
+        const int delta = argmin(0x16u);  // edges 1, 2, 4
+        q0 = 0x16u & ~(1u << delta);
+        partner[0] = delta;
+        partner[delta] = 0;
+        settle(0);
+        settle(delta);
+        int remaining = 6;
+        while (remaining > 0) {
+            for (;;) {
+                const std::uint32_t cand = q1 & ~assigned;
+                if (!cand) break;
+                const int t = argmin(cand);
+                q1 &= ~(1u << t);
+                const std::uint32_t fr = facets(t) & ~assigned;
+                if (__builtin_popcount(fr) != 1) {
+                    q0 |= 1u << t;
+                    continue;
+                }
+                const int f = __builtin_ctz(fr);
+                partner[t] = f;
+                partner[f] = t;
+                settle(f);
+                settle(t);
+                remaining -= 2;
+            }
+            if (!remaining) break;
+            const int t = argmin(q0 & ~assigned);
+            q0 &= ~(1u << t);
+            partner[t] = -1;
+            settle(t);
+            --remaining;
+        }
+        std::uint16_t e = 0;
+        for (int m = 0; m < 8; ++m)
+            if (partner[m] >= 0) e |= static_cast<std::uint16_t>((__builtin_ctz(m ^ partner[m]) + 1) << (2 * m));
+        table[idx] = e;
+    } while (std::next_permutation(perm, perm + 7));
+    return table;
 }
 
 constexpr int TX = 32, TY = 4, TZ = 2;
@@ -141,6 +240,8 @@ template <>
 struct KeyOf<double> {
     using type = std::uint64_t;
 };
+
+constexpr std::uint32_t kX0 = kAll & ~(kXP | kXM), kY0 = kAll & ~(kYP | kYM), kZ0 = kAll & ~(kZP | kZM);
 
 // 5-bit fields indexed by slot (0..26) in three 64-bit words.
 struct Pack5 {
@@ -388,6 +489,62 @@ __device__ __forceinline__ bool star_fast(Val val, std::uint32_t S, int n,
     return true;
 }
 
+// Octant star (see g_oct): returns false (nothing written) unless S is exactly one
+// unit cube at the vertex with 7 distinct link values.  `base` points at the vertex
+// in the shared tile.
+__device__ __forceinline__ bool is_octant(std::uint32_t S) {
+    const std::uint32_t cube = S & kDim3;
+    if (__popc(cube) != 1) return false;
+    const int c = __ffs(cube) - 1;
+    const int sx = (c % 3) - 1, sy = ((c / 3) % 3) - 1, sz = c / 9 - 1;  // each +-1
+    return S == ((kX0 | (sx > 0 ? kXP : kXM)) & (kY0 | (sy > 0 ? kYP : kYM)) & (kZ0 | (sz > 0 ? kZP : kZM)));
+}
+
+template <typename T>
+__device__ __forceinline__ bool octant_fast(const T* base, std::uint32_t S, const std::uint16_t* oct_table,
+                                            StarWriter& w) {
+    // S is an octant (is_octant): its cube slot gives the orientation
+    const int c = __ffs(S & kDim3) - 1;
+    const int sx = (c % 3) - 1, sy = ((c / 3) % 3) - 1, sz = c / 9 - 1;  // each +-1
+    const int dx = sx, dy = sy * SX, dz = sz * (SX * SY);
+    T f[8];
+    f[1] = base[dx];
+    f[2] = base[dy];
+    f[3] = base[dx + dy];
+    f[4] = base[dz];
+    f[5] = base[dx + dz];
+    f[6] = base[dy + dz];
+    f[7] = base[dx + dy + dz];
+    int idx = 0;
+    bool tie = false;
+#pragma unroll
+    for (int i = 1; i <= 7; ++i) {
+        int below = 0;
+#pragma unroll
+        for (int j = i + 1; j <= 7; ++j) {
+            below += f[j] < f[i];
+            tie |= f[j] == f[i];
+        }
+        constexpr int kFact[8] = {0, 720, 120, 24, 6, 2, 1, 1};
+        idx += below * kFact[i];
+    }
+    if (tie) return false;
+    const std::uint32_t e = __ldg(&oct_table[idx]);
+    const int st[3] = {sx, 3 * sy, 9 * sz};
+#pragma unroll
+    for (int m = 1; m < 8; ++m) {
+        const int a = static_cast<int>((e >> (2 * m)) & 3u);
+        const int sm = 13 + (m & 1) * st[0] + ((m >> 1) & 1) * st[1] + ((m >> 2) & 1) * st[2];
+        if (a == 0) {
+            w.critical(sm, __popc(m));
+        } else if ((m >> (a - 1)) & 1) {  // the higher cell of the pair writes it
+            const int lo = m ^ (1 << (a - 1));
+            w.pair(13 + (lo & 1) * st[0] + ((lo >> 1) & 1) * st[1] + ((lo >> 2) & 1) * st[2], sm);
+        }
+    }
+    return true;
+}
+
 // Work lists handed from the tile kernel to the size-specialised kernels:
 // [0] stars of 9..16 cells, [1] 17..27 cells, [2] stars with tied values.
 struct StarLists {
@@ -422,7 +579,8 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ std::uint32_t s_lm[2][kListBuf];
     __shared__ std::uint32_t s_ln[2];
     __shared__ unsigned long long s_base[2];
-    __shared__ std::uint32_t s_wn[6], s_wtotal;  // phase-2 work list: buckets of star size 3..8
+    // phase-2 work list: buckets of star size 3..8, then unit-cube (octant) stars
+    __shared__ std::uint32_t s_wn[7], s_wtotal, s_woct;
     __shared__ std::uint32_t s_wS[kGroup * NT];
     __shared__ std::uint16_t s_wid[kGroup * NT];  // tile-in-group << 8 | vertex in tile
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
@@ -549,7 +707,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         };
         // ---- phase 1, own vertex of each tile: star mask; trivial stars finished here;
         //      stars of 3..8 cells binned by size; larger stars to the list kernels
-        if (tid < 6) s_wn[tid] = 0;
+        if (tid < 7) s_wn[tid] = 0;
         __syncthreads();
         int ng[kGroup];
         std::uint32_t Sg[kGroup];
@@ -582,8 +740,9 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                     s_lb[which][at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
                     s_lm[which][at] = S;
                 } else {
-                    atomicAdd(&s_wn[n - 3], 1u);
-                    ng[g] = n;
+                    const int bucket = (n == 8 && is_octant(S)) ? 6 : n - 3;
+                    atomicAdd(&s_wn[bucket], 1u);
+                    ng[g] = bucket + 3;
                     Sg[g] = S;
                 }
 #pragma unroll
@@ -593,12 +752,13 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         __syncthreads();
         if (tid == 0) {
             std::uint32_t acc = 0;
-            for (int k = 0; k < 6; ++k) {
+            for (int k = 0; k < 7; ++k) {
                 const std::uint32_t c = s_wn[k];
                 s_wn[k] = acc;
                 acc += c;
             }
             s_wtotal = acc;
+            s_woct = s_wn[6];
         }
         __syncthreads();
 #pragma unroll
@@ -609,6 +769,9 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
                 s_wid[at] = static_cast<std::uint16_t>((g << 8) | tid);
             }
         __syncthreads();
+        // the table path pays off where unit-cube stars dominate (smooth fields); on
+        // noisy tiles the generic path is as fast and the two would diverge
+        const bool use_oct = 4 * (s_wtotal - s_woct) >= 3 * s_wtotal;
         // ---- phase 2: the binned stars, one per thread, register fast path
         for (std::uint32_t k = tid; k < s_wtotal; k += NT) {
             const int g = s_wid[k] >> 8, lid = s_wid[k] & 0xff;
@@ -616,8 +779,10 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             StarWriter w;
             writer_for(g, lid, w);
             const T* base = &tiles_sm[set][g][lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + 1];
-            if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, Sw, __popc(Sw), s_fac, s_cof, &s_M[tid], NT,
-                                 w)) {
+            if (use_oct && k >= s_woct && octant_fast<T>(base, Sw, g_oct, w)) {
+                // a unit-cube star: paired from the table (false only on tied values)
+            } else if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, Sw, __popc(Sw), s_fac, s_cof,
+                                        &s_M[tid], NT, w)) {
                 const unsigned long long at = atomicAdd(&lists.count[2], 1ull);  // ties: rare
                 lists.list[2][at] = static_cast<std::uint32_t>(w.vx + d.nx * (w.vy + d.ny * w.vz));
             }
@@ -846,6 +1011,8 @@ int upload_gradient_tables(int device) {
     if (device >= 0 && device < 64 && g_tables_ready[device]) return MSC3D_OK;
     const SlotTables t = host_tables();
     MSC3D_CUDA_TRY(cudaMemcpyToSymbol(c_slot, &t, sizeof t));
+    const std::vector<std::uint16_t> oct = host_octant_table();
+    MSC3D_CUDA_TRY(cudaMemcpyToSymbol(g_oct, oct.data(), oct.size() * sizeof(std::uint16_t)));
     if (device >= 0 && device < 64) g_tables_ready[device] = true;
     return MSC3D_OK;
 }

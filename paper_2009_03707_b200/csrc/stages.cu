@@ -366,7 +366,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     const std::uint64_t nov = nj ? ctx->h_small[0] : 0;
     const std::uint64_t nskip = ctx->h_small[19];
     const std::uint64_t nq = ctx->h_small[20];
-    if (nq != nov || nq > ovq_cap) return MSC3D_ERR_RUNTIME;
+    if (nq > ovq_cap) return MSC3D_ERR_NOMEM;  // parent overflow queue capacity, not a cycle
+    if (nq != nov) return MSC3D_ERR_RUNTIME;
     ctx->scalars["junctions_contracted"] = static_cast<std::int64_t>(nskip);
     auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", std::max<std::uint64_t>(nov, 1), 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
