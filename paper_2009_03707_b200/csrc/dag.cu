@@ -52,6 +52,10 @@ constexpr std::uint32_t kSuccCrit = 1u << 12;
 constexpr std::uint32_t kFieldLow = 0x249u;  // lowest bit of each 3-bit field
 constexpr int kArenas = 64;
 constexpr std::uint64_t kBadOff = ~0ull;
+// dead-junction path bound Z (see JRec): f32 bits in a record's kind word
+constexpr float kZLimit = 18446744073709551616.0f;  // 2^64
+__device__ __forceinline__ std::uint32_t zword(float z) { return __float_as_uint(z) << 1; }
+__device__ __forceinline__ float zof(std::uint32_t kind) { return __uint_as_float(kind >> 1); }
 
 // One item per thread, blocks in id order: the resident blocks then sweep the id
 // space as a compact wavefront, so the random accesses of neighbouring items (which
@@ -551,7 +555,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                     slen[i] = m;
                     pre = true;
                 } else if (m <= 2) {
-                    rec[2 * i] = make_uint4(m, uk[0], uk[1], 0u);
+                    rec[2 * i] = make_uint4(m, uk[0], uk[1], m == 0 ? zword(1.0f) : 0u);  // dead leaf: Z = 1
                     rec[2 * i + 1] = make_uint4(uc[0], 0u, uc[1], 0u);
                     pre = true;
                 }
@@ -682,9 +686,22 @@ __global__ void k_fill_overflow(const uint4* __restrict__ ovq, std::uint64_t n, 
 // (c0 = offset of len sorted entries; offsets and capacities are multiples of 4 so
 // keys load as aligned uint4 chunks and counts as uint4 pairs).
 struct alignas(16) JRec {
-    std::uint32_t len, k0, k1, kind;
+    std::uint32_t len, k0, k1, kind;  // kind: bit 0 (0 inline, 1 pool) | zbits(Z) << 1
     std::uint64_t c0, c1;
 };
+
+// Dead-junction overflow bound (path_matrix.cpp:188-219).  The
+// reference throws overflow_error when any A* entry -- the number of paths from a
+// 1-saddle s to a junction j -- exceeds 2^64-1.  For a junction that reaches a
+// 2-saddle t that entry is at most the final count (s, t), whose overflow the merges
+// already detect; a DEAD junction (P(j) empty: it reaches no 2-saddle) is seen by no
+// final count.  Every record therefore carries Z(j) = [j dead] + sum over junction
+// children of Z(child) = the number of paths from j to dead junctions, so
+// Z(s) = sum over dead d of A*[s, d] >= max_d A*[s, d] for a source s.  Z is an f32
+// summed with round-up (an upper bound, 31 bits: positive f32 bit patterns) in the
+// record's kind word; a gather whose sum reaches 2^64 raises flags[3] ("maybe"), and
+// the host then decides exactly (stages.cu: dag_count).  Contracted pass-through
+// junctions keep the bound: a dead one's paths continue 1:1 into its dead child.
 
 struct PoolRef {
     std::uint32_t* key;
@@ -728,10 +745,12 @@ struct Inputs {
     std::uint32_t k0[4], k1[4];
     std::uint64_t c0[4], c1[4];
     std::uint64_t off[4];  // kBadOff: inline
+    float z;               // sum of the junction children's Z (dead-junction bound)
 };
 
 template <bool kL2>
-__device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ rec, Inputs& in) {
+__device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ rec, Inputs& in,
+                                       unsigned int* __restrict__ zflag) {
     const std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
     // all child records are loaded first (unconditionally: record 0 stands in for
     // terminal / absent branches), so the up to eight loads are in flight together
@@ -745,6 +764,7 @@ __device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ 
         ra[b] = ld<kL2>(p);
         rb[b] = ld<kL2>(p + 1);
     }
+    in.z = 0.0f;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
         const std::uint32_t t = dd[b];
@@ -760,7 +780,8 @@ __device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ 
         } else {
             const std::uint64_t c0 = static_cast<std::uint64_t>(rb[b].x) | (static_cast<std::uint64_t>(rb[b].y) << 32);
             in.len[b] = ra[b].x;
-            if (ra[b].w == 0) {  // kind 0: inline
+            in.z = __fadd_ru(in.z, zof(ra[b].w));
+            if ((ra[b].w & 1u) == 0) {  // kind 0: inline
                 in.k0[b] = ra[b].y;
                 in.k1[b] = ra[b].z;
                 in.c0[b] = c0;
@@ -771,6 +792,7 @@ __device__ __forceinline__ void gather(const uint4 d4, const JRec* __restrict__ 
             }
         }
     }
+    if (in.z >= kZLimit) *zflag = 1u;
 }
 
 __device__ __forceinline__ bool add_ovf(std::uint64_t a, std::uint64_t b, std::uint64_t* r) {
@@ -1142,7 +1164,7 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
         if (u < a.nj) npar = a.indeg[u];
         par0 = nr[0];
         par1 = nr[1];
-        gather<true>(d4, a.rec, in);
+        gather<true>(d4, a.rec, in, &a.flags[3]);
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
     }
@@ -1191,8 +1213,8 @@ __device__ __forceinline__ void count_iter(const CountArgs& a, WarpBuf wb, WarpQ
     };
     auto finish = [&](std::uint32_t len) {
         if (!junction) a.slen[u - a.nj] = len;
-        else if (pooled) store_rec(a.rec, u, len, 1u, 0u, 0u, off, 0ull);
-        else store_rec(a.rec, u, len, 0u, r.k0, r.k1, r.c0, r.c1);
+        else if (pooled) store_rec(a.rec, u, len, 1u | zword(in.z), 0u, 0u, off, 0ull);
+        else store_rec(a.rec, u, len, zword(len == 0 ? __fadd_ru(in.z, 1.0f) : in.z), r.k0, r.k1, r.c0, r.c1);
     };
     // inputs larger than the warp buffer: direct merge
     if (valid && S > wb.cap) {
@@ -1234,7 +1256,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
     const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
     const uint4 d4 = a.dest[u], meta = make_uint4(0u, 0u, 0u, 0u), par0 = nr[0], par1 = nr[1];
     Inputs h;
-    gather<true>(d4, a.rec, h);
+    gather<true>(d4, a.rec, h, &a.flags[3]);
     const std::uint32_t T = h.len[0] + h.len[1] + h.len[2] + h.len[3];
     const bool junction = u < a.nj;
     const std::uint64_t off = pool_alloc(a.pool, ch, lane == 0 && junction ? T : 0u, &a.flags[1]);
@@ -1267,7 +1289,7 @@ __device__ __forceinline__ void count_heavy(const CountArgs& a, WarpBuf wb, Warp
     if (__any_sync(0xffffffffu, ovf) && lane == 0) a.flags[0] = 1u;
     if (lane == 0) {
         if (!junction) a.slen[u - a.nj] = L;
-        else store_rec(a.rec, u, L, 1u, 0u, 0u, hoff, 0ull);
+        else store_rec(a.rec, u, L, 1u | zword(h.z), 0u, 0u, hoff, 0ull);
         if (junction) ++done;
     }
     __syncwarp();
@@ -1405,7 +1427,7 @@ k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __r
              i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
             if (spending[i] == kDone) continue;
             Inputs in;
-            gather<false>(sdest[i], rec, in);
+            gather<false>(sdest[i], rec, in, &flags[3]);
             const std::uint32_t T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
             if (T > kHeavy && staged_size(in) + T <= static_cast<std::uint32_t>(kWarpCap)) {
                 heavy_q[atomicAdd(heavy_n, 1ull)] = static_cast<std::uint32_t>(i);
@@ -1429,7 +1451,7 @@ k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __r
         for (int b = 0; b < 4; ++b) in.len[b] = 0;
         std::uint32_t T = 0, S = 0;
         if (valid) {
-            gather<false>(sdest[i], rec, in);
+            gather<false>(sdest[i], rec, in, &flags[3]);
             T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
             S = staged_size(in);
         }
@@ -1491,7 +1513,7 @@ k_count_write_heavy(const uint4* __restrict__ sdest, const JRec* __restrict__ re
          k += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
         const std::uint32_t i = heavy_q[k];
         Inputs h;
-        gather<false>(sdest[i], rec, h);
+        gather<false>(sdest[i], rec, h, &flags[3]);
         std::uint32_t at = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {

@@ -267,6 +267,41 @@ struct CountOut {
     std::uint64_t* paths = nullptr;
     std::uint32_t base_one = 0, base_two = 0;
 };
+// The exact A* decision behind a "maybe" of the dead-junction bound (dag.cu, JRec):
+// the minor of this BFS (saddle_graph.cpp:121-217) built on the device and
+// count_paths' own overflow rule applied to it (count_minor: forward saturating
+// totals, then the exact per-source check).  Only runs when some source's paths into
+// dead junctions may reach 2^64; it clobbers the minor/count_minor scratch arrays.
+int exact_dead_overflow(msc3d_ctx* ctx) {
+    TRY(marked_lists(ctx));
+    TRY(minor(ctx));
+    const int w = ctx->id_width();
+    static const char* kLists[4] = {"s1_to_j", "j_to_j", "j_to_s2", "s1_to_s2"};
+    std::vector<std::uint32_t> src[4], dst[4];
+    std::vector<std::uint64_t> mult[4];
+    const std::uint32_t* ps[4];
+    const std::uint32_t* pd[4];
+    const std::uint64_t* pm[4];
+    std::uint64_t cnt[4];
+    for (int k = 0; k < 4; ++k) {
+        const std::string n = kLists[k];
+        cnt[k] = ctx->count(n + ".src");
+        src[k].resize(cnt[k]);
+        dst[k].resize(cnt[k]);
+        mult[k].resize(cnt[k]);
+        if (cnt[k]) {
+            MSC3D_CUDA_TRY(cudaMemcpy(src[k].data(), ctx->ptr<void>(n + ".src"), cnt[k] * 4, cudaMemcpyDeviceToHost));
+            MSC3D_CUDA_TRY(cudaMemcpy(dst[k].data(), ctx->ptr<void>(n + ".dst"), cnt[k] * 4, cudaMemcpyDeviceToHost));
+            MSC3D_CUDA_TRY(cudaMemcpy(mult[k].data(), ctx->ptr<void>(n + ".mult"), cnt[k] * 8, cudaMemcpyDeviceToHost));
+        }
+        ps[k] = src[k].data();
+        pd[k] = dst[k].data();
+        pm[k] = mult[k].data();
+    }
+    return count_minor(ctx, nullptr, ctx->count("one_saddles"), nullptr, ctx->count("junctions"), nullptr,
+                       ctx->count("two_saddles"), ps, pd, pm, cnt, w);
+}
+
 int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::string& term_list,
               const std::function<int(std::uint64_t, CountOut*)>& place = nullptr) {
     const Dims& d = ctx->dims;
@@ -424,6 +459,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
             if (L.diag) MSC3D_CUDA_TRY(cudaMemsetAsync(L.diag, 0, 1024 * 8, s));
         }
         MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(flags + 3, 0, 4, s));  // dead-junction "maybe"
         MSC3D_CUDA_TRY(cudaMemsetAsync(ptop, 0, arenas * 8, s));
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 55, 0, 5 * 8, s));
         if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nn * 4, cudaMemcpyDeviceToDevice, s));
@@ -452,9 +488,13 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // 1-saddles: merged lengths (those the walk did not finish), offsets, sorted output
     TRY(msc3d_dev::launch_source_len(L, s, sms));
     TRY(msc3d_dev::scan_u32(slen, n1, soff, ctx->d_small, ctx->ws, s));
-    TRY(ctx->fetch_small(27));
+    TRY(ctx->fetch_small(28));
     if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
     const std::uint64_t nout = n1 ? ctx->h_small[0] : 0;
+    if (ctx->h_small[27] >> 32) {  // some source's paths into dead junctions may reach 2^64
+        ctx->scalars["dead_overflow_checks"] += 1;
+        TRY(exact_dead_overflow(ctx));
+    }
     ctx->scalars["arcs_ss"] = static_cast<std::int64_t>(nout);
     CountOut o;
     if (place) {
