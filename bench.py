@@ -174,10 +174,12 @@ def run_reference_arm(args, world, rank):
 
 
 def run_sharded(args, world, rank, local):
-    """N > 1: ONE grid across the ranks (strong scaling), paper_2009_03707_b200/multigpu.py:
-    z-slab gradient with 2-plane halos, allgather of the owned code planes (NCCL),
-    replicated critical/extrema, reachability + counting sharded by 1-saddle slices,
-    allgather-v of the 1s->2s arc blocks (NCCL).  Every rank ends with the whole complex."""
+    """N > 1: ONE grid across the ranks (strong scaling), orchestrated in C++
+    (csrc/multigpu.cu, msc3d_mg_compute) over NCCL: P2P halo exchange + z-slab gradient,
+    per-slab critical compaction (counts allgather, lists allgather-v), allgather-v of
+    the owned code planes, extrema on the replicated codes, reachability + counting from
+    each rank's 1-saddle slice, allgather-v of the arc blocks.  Every rank ends with the
+    whole complex.  Each rank's input is its own vertex planes only."""
     import torch
     import torch.distributed as dist
 
@@ -187,50 +189,48 @@ def run_sharded(args, world, rank, local):
     dims = WORKLOAD["dims"] if not args.size else (args.size,) * 3
     ncells = cells(dims)
     local = local % torch.cuda.device_count()
-    plan = mg.slab_plan(dims[2], world, rank)
+    transport = "host" if os.environ.get("MSC3D_BENCH_BACKEND", "nccl") != "nccl" else "nccl"
+    g = mg.MultiGPU(dims, rank, world, device=local, transport=transport)
     v = m.synth(WORKLOAD["kind"], dims, WORKLOAD["seed"])  # every rank builds the same field
-    sv = mg.slab_values(v, dims, plan)
+    sv = mg.slab_values(v, dims, g.plan)                    # ... and keeps its own planes
     dev_in = torch.from_numpy(sv).cuda()
-    sc = mg.ShardedCompute(m, dims, plan, local)
-    # both device contexts run on torch's current stream, which the collectives are
-    # ordered with: CUDA events on it bracket the whole step
     stream = torch.cuda.current_stream()
-    sc.set_stream(stream.cuda_stream)
+    g.set_stream(stream.cuda_stream)  # the step and the collectives on torch's stream
     for _ in range(args.warmup):
-        sc.step(dev_in, m.OPT_SEGMENTATION)
+        g.step(dev_in, m.OPT_SEGMENTATION)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
-    stage_acc = np.zeros(5)
-    l0 = sc.slab.launches() + sc.full.launches()
+    stage_acc = np.zeros(7)
+    l0 = g.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            out = sc.step(dev_in, m.OPT_SEGMENTATION)
-            stage_acc += np.array(sc.stage_ms)
+            stage_acc += np.array(g.step(dev_in, m.OPT_SEGMENTATION))
         ev1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
     ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world, f"cuda:{local}")
     value = ncells / (ms_step / 1e3) / 1e6
-    n_arcs = int(out["arc_src"].numel())
-    launches = (sc.slab.launches() + sc.full.launches() - l0) // args.steps
+    launches = (g.launches() - l0) // args.steps
+    n_arcs = int(g.full.array_info("arc_src")[1])
     if os.environ.get("MSC3D_BENCH_VERIFY") and rank == 0:
         # development check: the assembled complex equals the single-GPU compute()
+        got = g.outputs()
         want = m.compute(v, dims, with_segmentation=True)
-        for k, w in (("cp_cell", want.cp_cell), ("arc_src", want.arc_src), ("arc_dst", want.arc_dst),
-                     ("arc_mult", want.arc_mult), ("labels_min", want.labels_min), ("labels_max", want.labels_max)):
-            got = out[k].cpu().numpy()
-            if not np.array_equal(got.view(np.asarray(w).dtype) if got.dtype != np.asarray(w).dtype else got, w):
+        for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+            if not np.array_equal(got[k], np.asarray(getattr(want, k))):
                 raise AssertionError(f"sharded {k} differs from the single-GPU compute")
         print("verify ok: sharded complex == single-GPU compute", file=sys.stderr, flush=True)
 
-    # e2e: host slab in (pinned), step, rank 0 copies the assembled complex to host
+    # e2e: host own planes in (pinned), step, rank 0 copies the assembled complex to host
     e2e = None
     if not args.no_e2e:
         host_in = torch.from_numpy(sv).pin_memory()
-        hbuf = {k: torch.empty(t.numel(), dtype=t.dtype).pin_memory() for k, t in out.items()} if rank == 0 else {}
+        outs = g.device_arrays()
+        hbuf = {k: torch.empty(t.numel(), dtype=torch.uint8).pin_memory() for k, t in outs.items()
+                if t is not None} if rank == 0 else {}
         times = []
         d2h = 0
         for i in range(2 + args.steps):
@@ -238,12 +238,16 @@ def run_sharded(args, world, rank, local):
             dist.barrier()
             ta = time.perf_counter()
             dev_in.copy_(host_in, non_blocking=True)
-            o = sc.step(dev_in, m.OPT_SEGMENTATION)
+            g.step(dev_in, m.OPT_SEGMENTATION)
             if rank == 0:
                 d2h = 0
-                for k, t in o.items():
+                for k, t in g.device_arrays().items():
+                    if t is None:
+                        continue
+                    if hbuf[k].numel() < t.numel():
+                        hbuf[k] = torch.empty(t.numel(), dtype=torch.uint8).pin_memory()
                     hbuf[k][: t.numel()].copy_(t, non_blocking=True)
-                    d2h += t.numel() * t.element_size()
+                    d2h += t.numel()
             torch.cuda.synchronize()
             tb = time.perf_counter()
             if i >= 2:
@@ -251,7 +255,8 @@ def run_sharded(args, world, rank, local):
         te = max_over_ranks(sum(times) / len(times), world, f"cuda:{local}")
         e2e = {"value": ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": int(sv.nbytes), "d2h_bytes_per_step": int(d2h),
-               "path": "per rank: pinned slab -> device, sharded step (C ABI + NCCL); rank 0: complex -> pinned host"}
+               "path": "per rank: pinned own planes -> device, msc3d_mg_compute (C++ + NCCL); "
+                       "rank 0: complex -> pinned host"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mcells/s", "n_gpus": world, "steps": args.steps,
@@ -259,15 +264,17 @@ def run_sharded(args, world, rank, local):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD["name"], "dims": list(dims), "field": WORKLOAD["kind"],
                        "seed": WORKLOAD["seed"], "lattice_cells": ncells,
-                       "parallelism": f"z-slabs x{world} (gradient, 2-plane halos) + allgather codes; "
-                                      f"1-saddle shards x{world} (reachability, counting) + allgather-v arcs",
+                       "parallelism": f"z-slabs x{world} (P2P halos, gradient + critical) + allgather-v codes; "
+                                      f"1-saddle shards x{world} (reachability, counting) + allgather-v arcs; "
+                                      f"transport {transport}",
                        "l2": "inputs larger than L2"},
-            "stages_ms_rank0": dict(zip(STAGES, (stage_acc / args.steps).tolist())),
+            "stages_ms_rank0": dict(zip(("halo+gradient", "critical+gathers", "extrema", "reachability",
+                                         "counting", "arc_gather", "step"), (stage_acc / args.steps).tolist())),
             "e2e": e2e, "gpu_launches": int(launches), "counts": {"arcs": n_arcs},
             "clocks": clk.summary(), "cpu_baseline": None, "roofline": None,
         }
         print(json.dumps(line), flush=True)
-    sc.close()
+    g.close()
     dist.destroy_process_group()
     return 0
 

@@ -234,6 +234,46 @@ int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, uint32_t shard, uint32_
 uint64_t msc3d_field_hash_f64(const double* values, uint64_t n);
 uint64_t msc3d_field_hash_f32(const float* values, uint64_t n);
 
+/* ---- multi-GPU (the reference has no counterpart) ---------------------
+ * One process per GPU.  A communicator is NCCL (libnccl.so.2 loaded at run time) or a
+ * host transport: an allgather over host buffers supplied by the caller (e.g.
+ * torch.distributed/gloo when several ranks share one GPU).  msc3d_mg_compute runs one
+ * step on rank r of G (paper_2009_03707_b200/csrc/multigpu.cu): P2P halo exchange of
+ * kHalo = 2 vertex planes, z-slab gradient, per-slab critical compaction (counts
+ * allgather + lists allgather-v), allgather-v of the owned code planes, extrema on the
+ * replicated codes, reachability + counting from the rank's 1-saddle slice,
+ * allgather-v of the arc blocks.  Every rank ends with the whole complex in its
+ * full-grid context (msc3d_mg_full_ctx): "cp_cell", "cp_index", "arc_src/dst/mult",
+ * "labels_min/max". */
+typedef struct msc3d_comm msc3d_comm;
+typedef struct msc3d_mg msc3d_mg;
+typedef struct msc3d_host_transport {
+    void* user;
+    /* every rank contributes `bytes` from send; recv receives world*bytes in rank order;
+     * returns 0 on success */
+    int (*allgather)(void* user, const void* send, void* recv, uint64_t bytes);
+} msc3d_host_transport;
+
+/* Slab plan of rank `rank` of `world` over nz vertex planes: out = {z0, z1 (own vertex
+ * planes), lo, hi (slab grid incl. halo), own_c0, own_c1 (own lattice planes),
+ * local_c0 (first own lattice plane in the slab's lattice)}.  Host-only.
+ * MSC3D_ERR_INVALID if a rank would own fewer than 2 planes (the halo depth). */
+int msc3d_mg_plan(int64_t nz, int world, int rank, int64_t out[7]);
+int msc3d_nccl_unique_id(uint8_t out[128]);
+int msc3d_comm_create_nccl(msc3d_comm** out, const uint8_t id[128], int rank, int world, int device);
+int msc3d_comm_create_host(msc3d_comm** out, const msc3d_host_transport* t, int rank, int world);
+void msc3d_comm_destroy(msc3d_comm* c);
+int msc3d_mg_create(msc3d_mg** out, msc3d_comm* comm, int device);
+void msc3d_mg_destroy(msc3d_mg* g);
+msc3d_ctx* msc3d_mg_full_ctx(msc3d_mg* g);
+msc3d_ctx* msc3d_mg_slab_ctx(msc3d_mg* g);
+int msc3d_mg_set_stream(msc3d_mg* g, void* stream);
+/* own_values: device pointer to this rank's own vertex planes [z0, z1) (x-fastest).
+ * stage_ms (optional, 7 doubles): halo+slab gradient, slab critical + gathers, extrema,
+ * reachability, counting, arc gather, whole step. */
+int msc3d_mg_compute(msc3d_mg* g, msc3d_dims dims, int value_type, const void* own_values, int options,
+                     double* stage_ms);
+
 #ifdef __cplusplus
 }
 #endif

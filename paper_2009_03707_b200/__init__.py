@@ -45,6 +45,14 @@ class HostOutputs(C.Structure):
                 ("labels_max", C.c_void_p), ("n_cp", C.c_uint64), ("n_arcs", C.c_uint64)]
 
 
+# msc3d_host_transport (include/msc3d_cuda.h): allgather(user, send, recv, bytes) -> 0 ok
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", ALLGATHER_FN)]
+
+
 class IoError(RuntimeError):
     pass
 
@@ -100,6 +108,17 @@ def lib():
         "msc3d_ctx_validate_gradient": (i32, [vp, u64, C.POINTER(u64)]),
         "msc3d_ctx_boundary_check": (i32, [vp, C.POINTER(u64)]),
         "msc3d_boundary_check_host": (i32, [vp, u64, vp, u64, vp, vp, vp, C.POINTER(u64)]),
+        "msc3d_mg_plan": (i32, [i64, i32, i32, C.POINTER(i64)]),
+        "msc3d_nccl_unique_id": (i32, [C.POINTER(C.c_uint8)]),
+        "msc3d_comm_create_nccl": (i32, [C.POINTER(vp), C.POINTER(C.c_uint8), i32, i32, i32]),
+        "msc3d_comm_create_host": (i32, [C.POINTER(vp), C.POINTER(HostTransport), i32, i32]),
+        "msc3d_comm_destroy": (None, [vp]),
+        "msc3d_mg_create": (i32, [C.POINTER(vp), vp, i32]),
+        "msc3d_mg_destroy": (None, [vp]),
+        "msc3d_mg_full_ctx": (vp, [vp]),
+        "msc3d_mg_slab_ctx": (vp, [vp]),
+        "msc3d_mg_set_stream": (i32, [vp, vp]),
+        "msc3d_mg_compute": (i32, [vp, Dims, i32, vp, i32, C.POINTER(C.c_double)]),
         "msc3d_field_hash_f64": (u64, [vp, u64]),
         "msc3d_field_hash_f32": (u64, [vp, u64]),
     }
@@ -159,9 +178,21 @@ class Context:
         self.dims = None
         self.wide = False
 
+    @classmethod
+    def borrow(cls, handle, dims=None):
+        """A non-owning view of a context created elsewhere (e.g. msc3d_mg_full_ctx)."""
+        c = cls.__new__(cls)
+        c._L = lib()
+        c.h = C.c_void_p(handle)
+        c.dims = tuple(dims) if dims else None
+        c.wide = False
+        c._borrowed = True
+        return c
+
     def close(self):
         if getattr(self, "h", None):
-            self._L.msc3d_ctx_destroy(self.h)
+            if not getattr(self, "_borrowed", False):
+                self._L.msc3d_ctx_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -26,6 +26,7 @@ struct msc3d_ctx {
     msc3d_dev::Dims dims{};
     bool have_dims = false;
     bool crit_counts_valid = false;  // d_small[40..43] hold the codes' critical counts
+    bool crit_external = false;      // crit0..3 + scalars c0..c3 installed by the caller (multigpu.cu)
     int value_type = MSC3D_VALUE_F32;
     // msc3d_ctx_set_option: "wide_ids" forces 64-bit cell-id lists on any grid (the
     // path configs 4-5 take, testable on small grids); "kahn_switch_below" is the

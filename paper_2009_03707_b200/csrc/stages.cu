@@ -638,8 +638,9 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
 
     clk.mark(1, s);
 
-    // [critical]
-    TRY(critical(ctx));
+    // [critical] (multi-GPU: the per-slab lists, already gathered, multigpu.cu)
+    if (ctx->crit_external) ctx->crit_external = false;
+    else TRY(critical(ctx));
     clk.mark(2, s);
     const std::uint64_t c0 = ctx->scalars["c0"], c1 = ctx->scalars["c1"], c2 = ctx->scalars["c2"],
                         c3 = ctx->scalars["c3"];

@@ -1,36 +1,31 @@
-"""Multi-GPU MS complex: z-slab gradient with halos, replicated codes, 1-saddle-sharded
-saddle stages, allgather-v of the arcs (BASELINE.json north_star).
+"""Multi-GPU MS complex: the Python side of the C++ orchestrator (csrc/multigpu.cu).
 
-One process per GPU (torch.distributed, NCCL over NVLink; gloo on CPU for the host
-logic tests).  Per step, rank r of G:
+One process per GPU.  The step itself -- P2P halo exchange, z-slab gradient, per-slab
+critical compaction with count/list gathers, allgather-v of the owned code planes,
+extrema on the replicated codes, reachability + counting from the rank's 1-saddle
+slice, allgather-v of the arc blocks -- runs in C++ (msc3d_mg_compute) over a
+communicator:
 
-1. gradient on its z-slab of vertex planes [z0, z1) plus a 2-plane halo on each side
-   (values of planes [z0-2, z1+2) ∩ [0, nz)).  A vertex's lower star lies in its
-   3x3x3 neighbourhood (gradient.cpp:13-20), so every vertex of [z0-1, z1+1) gets its
-   exact star, hence every cell of lattice planes [2 z0 - 1, 2 z1] its exact code --
-   in particular all of the rank's own lattice planes [2 z0, 2 z1) (last rank: up to
-   ez).  Vertex ids are shifted on the slab, which the tie-break tolerates (it only
-   compares ids, and the shift preserves their order).
-2. allgather of the owned code planes (N/G bytes per rank): every rank holds the
-   whole GradientField (the north star's "replicated gradient field").
-3. critical cells and extrema on the replicated codes (cheap, replicated).
-4. reachability + path counting from a contiguous slice of the critical 1-cells
-   (crit1 is sorted by cell id, so an index slice is a z-slab of sources): the 1s->2s
-   arcs of those 1-saddles are a contiguous block of the global sorted arc list.
-5. allgather-v of the arc blocks; the complex is assembled identically on every rank.
+* NCCL (``transport="nccl"``, production: torchrun, one GPU per rank): rank 0 draws the
+  ncclUniqueId through the C ABI, torch.distributed broadcasts it, every rank builds its
+  communicator in C++ (libnccl.so.2, the library torch.distributed also loads);
+* host (``transport="host"``): the orchestrator's collectives are allgathers over host
+  buffers, implemented here with torch.distributed (gloo) -- several ranks on one GPU in
+  the tests.
 
-No step changes any result: the assembled complex equals the single-GPU compute()
-(tests/test_multigpu.py checks it on one GPU by running the shards in sequence, and the
-collectives' host logic on CPU with gloo, world_size 2).
+No step changes any result: every rank ends with the same complex as a single-GPU
+compute() (tests/test_multigpu.py).  SURVEY.md §8(e), DESIGN.md §5.
 """
 from __future__ import annotations
 
 import ctypes as C
+import sys
+import traceback
 from dataclasses import dataclass
 
 import numpy as np
 
-HALO = 2  # vertex planes of halo on each side of a slab
+HALO = 2  # vertex planes of halo on each side of a slab (multigpu.cu kHalo)
 
 
 @dataclass(frozen=True)
@@ -51,172 +46,158 @@ class SlabPlan:
         return self.hi - self.lo
 
 
-def slab_plan(nz: int, world: int, rank: int, halo: int = HALO) -> SlabPlan:
-    """Vertex planes split as evenly as possible; every rank gets >= 1 plane."""
-    if nz < 2:
-        raise ValueError("nz must be >= 2 (grid.cpp:13-16)")
-    if world > nz:
-        raise ValueError("more ranks than vertex planes")
-    z0 = nz * rank // world
-    z1 = nz * (rank + 1) // world
-    lo = max(0, z0 - halo)
-    hi = min(nz, z1 + halo)
-    ez = 2 * nz - 1
-    own_c0 = 2 * z0
-    own_c1 = ez if rank == world - 1 else 2 * z1
-    return SlabPlan(rank, world, nz, z0, z1, lo, hi, own_c0, own_c1, own_c0 - 2 * lo)
+def slab_plan(nz: int, world: int, rank: int) -> SlabPlan:
+    """msc3d_mg_plan: vertex planes split as evenly as possible (>= 2 per rank)."""
+    from . import _raise, lib
+    out = (C.c_int64 * 7)()
+    _raise(lib().msc3d_mg_plan(int(nz), int(world), int(rank), out), "msc3d_mg_plan")
+    return SlabPlan(rank, world, nz, *[int(x) for x in out])
 
 
 def source_slice(c1: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous, balanced slice [first, first + count) of the critical 1-cells."""
+    """Contiguous, balanced slice [first, first + count) of the critical 1-cells
+    (stages.cu: compute_from_codes, sharded)."""
     first = c1 * rank // world
     return first, c1 * (rank + 1) // world - first
 
 
-# ---------------------------------------------------------------------------------
-# collectives (torch.distributed; the same code runs on NCCL and on gloo)
-# ---------------------------------------------------------------------------------
-def allgather_equal(chunk, group=None):
-    """Concatenate equal-size 1-D chunks of every rank in rank order."""
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    if chunk.device.type == "cuda" and dist.get_backend(group) != "nccl":
-        # gloo (tests: several ranks sharing one GPU) gathers through host memory
-        return allgather_equal(chunk.cpu(), group).to(chunk.device)
-    out = torch.empty(world * chunk.numel(), dtype=chunk.dtype, device=chunk.device)
-    if chunk.device.type == "cuda":
-        dist.all_gather_into_tensor(out, chunk.contiguous(), group=group)
-    else:
-        dist.all_gather(list(out.chunk(world)), chunk.contiguous(), group=group)
-    return out
+def slab_values(values: np.ndarray, dims, plan: SlabPlan, own_only: bool = True) -> np.ndarray:
+    """This rank's samples out of the whole field: its own vertex planes [z0, z1)
+    (what msc3d_mg_compute takes), or the whole slab grid [lo, hi)."""
+    nx, ny, nz = dims
+    v = np.asarray(values).reshape(nz, ny, nx)
+    a, b = (plan.z0, plan.z1) if own_only else (plan.lo, plan.hi)
+    return np.ascontiguousarray(v[a:b]).reshape(-1)
 
 
-def allgather_v(t, group=None):
-    """allgather-v of a 1-D tensor (NCCL has no native allgather-v): sizes first,
-    then one equal-size allgather of the padded blocks, then the padding is dropped."""
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    sizes = allgather_equal(n, group).tolist()
-    m = max(sizes)
-    pad = torch.zeros(m, dtype=t.dtype, device=t.device)
-    pad[: t.numel()] = t
-    g = allgather_equal(pad, group).view(world, m)
-    return torch.cat([g[r, : sizes[r]] for r in range(world)]) if world > 1 else g[0, : sizes[0]]
+class HostTransport:
+    """msc3d_host_transport over torch.distributed (any backend with CPU tensors: gloo):
+    the orchestrator's only host primitive, an allgather of equal-size byte blocks."""
 
-
-def gather_codes(local_codes, plan: SlabPlan, plane_bytes: int, chunk_planes: int, group=None):
-    """Owned lattice planes of every rank -> the whole GradientField (1-D uint8).
-    local_codes: the slab grid's code array (1-D uint8 tensor)."""
-    import torch
-    own = plan.own_c1 - plan.own_c0
-    a = plan.local_c0 * plane_bytes
-    chunk = torch.zeros(chunk_planes * plane_bytes, dtype=torch.uint8, device=local_codes.device)
-    chunk[: own * plane_bytes] = local_codes[a: a + own * plane_bytes]
-    g = allgather_equal(chunk, group)
-    ez = 2 * plan.nz - 1
-    world = plan.world
-    # every rank but possibly the last owns exactly chunk_planes planes when nz is
-    # divisible by the world size: then the gathered buffer is already contiguous
-    parts = []
-    for r in range(world):
-        p = slab_plan(plan.nz, world, r)
-        n = (p.own_c1 - p.own_c0) * plane_bytes
-        parts.append(g[r * chunk_planes * plane_bytes: r * chunk_planes * plane_bytes + n])
-    codes = torch.cat(parts)
-    assert codes.numel() == ez * plane_bytes
-    return codes
-
-
-def chunk_planes_for(nz: int, world: int) -> int:
-    return max(slab_plan(nz, world, r).own_c1 - slab_plan(nz, world, r).own_c0 for r in range(world))
-
-
-# ---------------------------------------------------------------------------------
-# one sharded step on this rank
-# ---------------------------------------------------------------------------------
-class ShardedCompute:
-    """Holds the two device contexts of a rank (slab grid, whole grid) and runs one
-    multi-GPU step.  values_slab: device f32 tensor of the slab grid's vertices
-    (planes [plan.lo, plan.hi))."""
-
-    def __init__(self, m, dims, plan: SlabPlan, device: int, group=None):
-        self.m = m
-        self.dims = tuple(dims)
-        self.plan = plan
+    def __init__(self, group=None):
+        from . import ALLGATHER_FN, HostTransport as _HT
         self.group = group
-        self.slab = m.Context(device)
-        self.full = m.Context(device)
-        self.ex = 2 * dims[0] - 1
-        self.ey = 2 * dims[1] - 1
-        self.plane_bytes = self.ex * self.ey
-        self.chunk_planes = chunk_planes_for(dims[2], plan.world)
+        self.calls = 0
+        self._fn = ALLGATHER_FN(self._allgather)  # kept alive as long as the transport
+        self.struct = _HT(None, self._fn)
 
-    def set_stream(self, stream_ptr):
-        for c in (self.slab, self.full):
-            c._L.msc3d_ctx_set_stream(c.h, C.c_void_p(stream_ptr))
-
-    def _device_array(self, ctx, name, dtype):
+    def allgather_bytes(self, data: bytes) -> bytes:
         import torch
-        ptr, n, e = ctx.array_info(name)
+        import torch.distributed as dist
+        world = dist.get_world_size(self.group)
+        n = len(data)
         if n == 0:
-            return torch.empty(0, dtype=dtype, device="cuda")
-        return _wrap_device(ptr, n * e, torch.uint8).view(dtype)
+            return b""
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(out, t, group=self.group)
+        return b"".join(o.numpy().tobytes() for o in out)
 
-    def step(self, values_slab, options=1):
-        """Returns dict of device tensors of the assembled complex (identical on every rank)."""
-        import torch
-        m, plan = self.m, self.plan
-        nx, ny, nz = self.dims
-        ldims = (nx, ny, plan.local_nz)
-        m._raise(self.slab._L.msc3d_ctx_bind_values(self.slab.h, m.Dims(*ldims), m.VALUE_F32,
-                                                     C.c_void_p(values_slab.data_ptr())), "bind_values")
-        m._raise(self.slab._L.msc3d_ctx_gradient(self.slab.h), "gradient")
-        self.slab.sync()  # the contexts' stream -> torch's (collectives, copies)
-        local_codes = self._device_array(self.slab, "codes", torch.uint8)
-        codes = gather_codes(local_codes, plan, self.plane_bytes, self.chunk_planes, self.group)
-        torch.cuda.current_stream().synchronize()
-        m._raise(self.full._L.msc3d_ctx_bind_codes(self.full.h, m.Dims(*self.dims), C.c_void_p(codes.data_ptr())),
-                 "bind_codes")
-        st = (C.c_double * 5)()
-        m._raise(self.full._L.msc3d_ctx_compute_codes(self.full.h, options, plan.rank, plan.world, st),
-                 "compute_codes")
-        self.full.sync()
-        out = {k: self._device_array(self.full, k, torch.uint8) for k in ("cp_cell", "cp_index")}
-        if plan.world == 1:
-            for k, dt in (("arc_src", torch.int32), ("arc_dst", torch.int32), ("arc_mult", torch.int64)):
-                out[k] = self._device_array(self.full, k, dt)
+    def _allgather(self, user, send, recv, nbytes):
+        try:
+            self.calls += 1
+            data = C.string_at(send, nbytes) if nbytes else b""
+            got = self.allgather_bytes(data)
+            if got:
+                C.memmove(recv, got, len(got))
+            return 0
+        except Exception:  # pragma: no cover - reported to the C side as a failure
+            traceback.print_exc(file=sys.stderr)
+            return 1
+
+
+class MultiGPU:
+    """One rank of a multi-GPU compute: communicator + the orchestrator's two contexts
+    (slab grid, whole grid).  step(own) runs msc3d_mg_compute on this rank's own vertex
+    planes (a device pointer or a CUDA torch tensor)."""
+
+    def __init__(self, dims, rank: int, world: int, device: int = 0, transport: str = "nccl", group=None):
+        from . import Context, _raise, lib
+        self._L = lib()
+        self.dims = tuple(int(x) for x in dims)
+        self.rank, self.world = rank, world
+        self.plan = slab_plan(self.dims[2], world, rank)
+        self.transport = None
+        comm = C.c_void_p()
+        if transport == "nccl":
+            import torch.distributed as dist
+            uid = (C.c_uint8 * 128)()
+            if rank == 0:
+                _raise(self._L.msc3d_nccl_unique_id(uid), "ncclGetUniqueId")
+            box = [bytes(uid)]
+            if world > 1:
+                dist.broadcast_object_list(box, src=0, group=group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+            _raise(self._L.msc3d_comm_create_nccl(C.byref(comm), uid, rank, world, device), "ncclCommInitRank")
+        elif transport == "host":
+            self.transport = HostTransport(group)
+            _raise(self._L.msc3d_comm_create_host(C.byref(comm), C.byref(self.transport.struct), rank, world),
+                   "msc3d_comm_create_host")
         else:
-            for k, dt in (("src", torch.int32), ("dst", torch.int32), ("mult", torch.int64)):
-                a = self._device_array(self.full, "arcA_" + k, dt)
-                b = allgather_v(self._device_array(self.full, "arcB_" + k, dt), self.group)
-                c = self._device_array(self.full, "arcC_" + k, dt)
-                out["arc_" + k] = torch.cat([a, b, c])
-        if options & m.OPT_SEGMENTATION:
-            out["labels_min"] = self._device_array(self.full, "labels_min", torch.int32)
-            out["labels_max"] = self._device_array(self.full, "labels_max", torch.int32)
+            raise ValueError(f"unknown transport {transport!r}")
+        self.comm = comm
+        mg = C.c_void_p()
+        _raise(self._L.msc3d_mg_create(C.byref(mg), comm, int(device)), "msc3d_mg_create")
+        self.mg = mg
+        self.full = Context.borrow(self._L.msc3d_mg_full_ctx(mg), self.dims)
+        self.slab = Context.borrow(self._L.msc3d_mg_slab_ctx(mg))
+        self.stage_ms = [0.0] * 7
+
+    def set_stream(self, stream_ptr: int):
+        from . import _raise
+        _raise(self._L.msc3d_mg_set_stream(self.mg, C.c_void_p(stream_ptr)), "set_stream")
+
+    def step(self, own_values, options: int = 1, value_type: int | None = None):
+        from . import VALUE_F32, VALUE_F64, _dims, _raise
+        ptr = own_values.data_ptr() if hasattr(own_values, "data_ptr") else int(own_values)
+        if value_type is None:
+            value_type = VALUE_F64 if str(getattr(own_values, "dtype", "")).endswith("float64") else VALUE_F32
+        st = (C.c_double * 7)()
+        _raise(self._L.msc3d_mg_compute(self.mg, _dims(self.dims), int(value_type), C.c_void_p(ptr), int(options), st),
+               "msc3d_mg_compute")
         self.stage_ms = list(st)
+        return self.stage_ms
+
+    def outputs(self, names=("cp_cell", "cp_index", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max")):
+        """The assembled complex (host copies)."""
+        out = {}
+        for k in names:
+            try:
+                out[k] = self.full.get(k)
+            except Exception:
+                if k.startswith("labels"):
+                    continue
+                raise
         return out
 
+    def device_arrays(self, names=("cp_cell", "cp_index", "arc_src", "arc_dst", "arc_mult", "labels_min",
+                                   "labels_max")):
+        """Zero-copy torch views of the assembled complex on this rank's GPU."""
+        out = {}
+        for k in names:
+            ptr, n, e = self.full.array_info(k)
+            out[k] = _wrap_device(ptr, n * e) if n else None
+        return out
+
+    def launches(self) -> int:
+        return self.full.launches()
+
     def close(self):
-        self.slab.close()
-        self.full.close()
+        if getattr(self, "mg", None):
+            self.full.close()
+            self.slab.close()
+            self._L.msc3d_mg_destroy(self.mg)
+            self.mg = None
+        if getattr(self, "comm", None):
+            self._L.msc3d_comm_destroy(self.comm)
+            self.comm = None
 
 
-def _wrap_device(ptr: int, nbytes: int, dtype):
-    """A torch view of device memory owned by a context (no copy)."""
+def _wrap_device(ptr: int, nbytes: int):
+    """A torch uint8 view of device memory owned by a context (no copy)."""
     import torch
 
     class _Arr:
         __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
     return torch.as_tensor(_Arr(), device="cuda")
-
-
-def slab_values(values: np.ndarray, dims, plan: SlabPlan) -> np.ndarray:
-    """The slab grid's samples (x-fastest) out of the whole field."""
-    nx, ny, nz = dims
-    v = np.asarray(values).reshape(nz, ny, nx)
-    return np.ascontiguousarray(v[plan.lo: plan.hi]).reshape(-1)

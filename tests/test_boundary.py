@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 def test_python_mirror_binds_every_symbol():
     L = m.lib()
     for n in declared_functions():
-        assert getattr(L, n).restype is not None or n == "msc3d_ctx_destroy", n
+        assert getattr(L, n).restype is not None or n.endswith("_destroy"), n
 
 
 def test_check_dims_matches_griddims():

@@ -69,11 +69,13 @@ def test_cli_compute_matches_reference(tmp_path, ref):
 
 
 @pytest.mark.gpu
-def test_cli_large_complex_matches_device(tmp_path):
+def test_cli_large_complex_matches_reference(tmp_path, ref):
     """A complex large enough that the drop-in compute() takes its parallel host path
     (result vectors >= 64 MB: reserved, huge-page advised, pre-faulted from several
-    threads; critical point values from the device): everything equals the device
-    pipeline's own outputs, and each value is the sample at the cell's max vertex."""
+    threads; critical point values from the device): critical points (cell, index,
+    doubled coordinates, value), sorted arcs and both label volumes equal the
+    unmodified reference's compute() on the same samples (msc.cpp:57-147), and each
+    value is the sample at the cell's max vertex (grid.cpp:129-137)."""
     dims = (144, 144, 144)
     v = m.synth("gnoise", dims)
     raw = tmp_path / "v.raw"
@@ -82,9 +84,12 @@ def test_cli_large_complex_matches_device(tmp_path):
     r = run("--input", raw, "--dims", *dims, "--dtype", "f32", "--format", "csv", "--out", pre,
             "--labels", tmp_path / "lab")
     assert r.returncode == 0, r.stderr
-    want = m.compute(v, dims, with_segmentation=True)
+    r_ = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
+    want = type("W", (), {k: r_[k] for k in ("cp_cell", "cp_index", "arc_src", "arc_dst", "arc_mult",
+                                             "labels_min", "labels_max")})
     cps = np.loadtxt(f"{pre}_critical_points.csv", delimiter=",", skiprows=1, ndmin=2)
     assert len(cps) > 1_200_000  # >= 64 MB of CriticalPoint records
+    np.testing.assert_array_equal(cps[:, 9], r_["cp_value"])
     np.testing.assert_array_equal(cps[:, 0].astype(np.int64), np.arange(len(cps)))
     np.testing.assert_array_equal(cps[:, 1].astype(np.uint64), np.asarray(want.cp_cell, dtype=np.uint64))
     np.testing.assert_array_equal(cps[:, 2].astype(np.uint8), np.asarray(want.cp_index, dtype=np.uint8))
