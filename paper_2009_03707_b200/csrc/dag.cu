@@ -36,6 +36,8 @@
 // (1-saddle, 2-saddle, count) output.  Counts are exact u64 with sticky overflow.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -148,45 +150,73 @@ __device__ __forceinline__ void fill_step_tables(StepTables& t, const EGrid& g) 
 // ---------------------------------------------------------------------------------
 // successor table
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128, 16)
-k_succ_table(const std::uint8_t* __restrict__ codes, Dims d, std::uint16_t* __restrict__ succ) {
+// One block per vertex row (vy, vz): the row's edges and their cofacet quads live in 8
+// lattice rows around lattice row (2vy, 2vz); each field is one shared-memory table
+// lookup lut[edge axis][position][quad code] (12 x 256 bytes, built per block) instead
+// of decoding the pair code with branches -- the kernel was instruction-bound (142
+// instructions per edge) on the decode and 64-bit index arithmetic.
+__global__ void k_succ_lut(std::uint8_t* __restrict__ lut) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 12 * 256; i += gridDim.x * blockDim.x) {
+        const int a = i >> 10, p = (i >> 8) & 3, qc = i & 255;
+        const int b = other_axis(a, p >> 1), h = p & 1;
+        std::uint8_t f = 0;
+        if (qc == kCritical) {
+            f = 1;
+        } else if (qc >= kFacetBase && qc < kFacetBase + 6) {
+            const int dir = qc - kFacetBase, ax = dir >> 1, ps = dir & 1;
+            if (ax == b) f = ps == h ? 2 : 0;  // the other way is e itself
+            else f = ps ? 4 : 3;               // ax == a
+        }
+        lut[i] = f;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_succ_table(const std::uint8_t* __restrict__ codes, Dims d, const uint4* __restrict__ g_lut,
+             std::uint16_t* __restrict__ succ) {
+    __shared__ uint4 lut4[12 * 256 / 16];
+    for (int i = threadIdx.x; i < 12 * 256 / 16; i += blockDim.x) lut4[i] = g_lut[i];
+    __syncthreads();
+    const std::uint8_t* lut = reinterpret_cast<const std::uint8_t*>(lut4);
     const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
-    const std::int64_t step[3] = {1, d.ex, d.exy};
-    const std::int64_t nn[3] = {d.nx, d.ny, d.nz};
+    const std::int64_t ex = d.ex, exy = d.exy;
     for (std::uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const std::int64_t vz = static_cast<std::int64_t>(d.fny.div(r));
         const std::int64_t vy = static_cast<std::int64_t>(r) - vz * d.ny;
-        for (std::int64_t vx = threadIdx.x; vx < d.nx; vx += blockDim.x) {
-            const std::int64_t vc[3] = {vx, vy, vz};
-            const std::int64_t cv = 2 * vx + d.ex * (2 * vy + d.ey * 2 * vz);
-            const std::uint64_t v = static_cast<std::uint64_t>(vx) + static_cast<std::uint64_t>(d.nx) * r;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                std::uint32_t out = 0;
-                if (vc[a] < nn[a] - 1) {
-                    const std::int64_t eid = cv + step[a];
-                    if (codes[eid] == kCritical) out |= kSuccCrit;
-#pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const int b = a == 0 ? 1 + k : (a == 1 ? 2 * k : k);
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (h ? vc[b] >= nn[b] - 1 : vc[b] <= 0) continue;
-                            const std::uint8_t qc = codes[eid + (h ? step[b] : -step[b])];
-                            std::uint32_t f = 0;
-                            if (qc == kCritical) {
-                                f = 1;
-                            } else if (paired_with_facet(qc)) {
-                                const int dir = qc - kFacetBase, ax = dir >> 1, ps = dir & 1;
-                                if (ax == b) f = ps == h ? 2u : 0u;  // the other way is e itself
-                                else f = ps ? 4u : 3u;                // ax == a
-                            }
-                            out |= f << (3 * (2 * k + h));
-                        }
-                    }
-                }
-                succ[3 * v + a] = static_cast<std::uint16_t>(out);
+        const bool ym = vy > 0, yp = vy < d.ny - 1, zm = vz > 0, zp = vz < d.nz - 1;
+        const std::uint8_t* R00 = codes + (2 * vz * d.ey + 2 * vy) * ex;  // lattice row (2vy, 2vz)
+        const std::uint8_t *Rm0 = R00 - ex, *Rp0 = R00 + ex, *R0m = R00 - exy, *R0p = R00 + exy;
+        const std::uint8_t *Rpm = Rp0 - exy, *Rpp = Rp0 + exy, *Rmp = Rm0 + exy;
+        std::uint16_t* out = succ + 3 * static_cast<std::uint64_t>(d.nx) * r;
+        const int nx = static_cast<int>(d.nx);
+        for (int vx = threadIdx.x; vx < nx; vx += blockDim.x) {
+            const int x = 2 * vx;
+            const bool xm = vx > 0, xp = vx < nx - 1;
+            std::uint32_t w0 = 0, w1 = 0, w2 = 0;
+            if (xp) {  // x-edge (x+1, 2vy, 2vz): quads -y, +y, -z, +z at x+1
+                w0 = (R00[x + 1] == kCritical ? kSuccCrit : 0u);
+                if (ym) w0 |= static_cast<std::uint32_t>(lut[(0 << 8) | Rm0[x + 1]]);
+                if (yp) w0 |= static_cast<std::uint32_t>(lut[(1 << 8) | Rp0[x + 1]]) << 3;
+                if (zm) w0 |= static_cast<std::uint32_t>(lut[(2 << 8) | R0m[x + 1]]) << 6;
+                if (zp) w0 |= static_cast<std::uint32_t>(lut[(3 << 8) | R0p[x + 1]]) << 9;
             }
+            if (yp) {  // y-edge (x, 2vy+1, 2vz): quads -x, +x (same row), -z, +z
+                w1 = (Rp0[x] == kCritical ? kSuccCrit : 0u);
+                if (xm) w1 |= static_cast<std::uint32_t>(lut[(4 << 8) | Rp0[x - 1]]);
+                if (xp) w1 |= static_cast<std::uint32_t>(lut[(5 << 8) | Rp0[x + 1]]) << 3;
+                if (zm) w1 |= static_cast<std::uint32_t>(lut[(6 << 8) | Rpm[x]]) << 6;
+                if (zp) w1 |= static_cast<std::uint32_t>(lut[(7 << 8) | Rpp[x]]) << 9;
+            }
+            if (zp) {  // z-edge (x, 2vy, 2vz+1): quads -x, +x (same row), -y, +y
+                w2 = (R0p[x] == kCritical ? kSuccCrit : 0u);
+                if (xm) w2 |= static_cast<std::uint32_t>(lut[(8 << 8) | R0p[x - 1]]);
+                if (xp) w2 |= static_cast<std::uint32_t>(lut[(9 << 8) | R0p[x + 1]]) << 3;
+                if (ym) w2 |= static_cast<std::uint32_t>(lut[(10 << 8) | Rmp[x]]) << 6;
+                if (yp) w2 |= static_cast<std::uint32_t>(lut[(11 << 8) | Rpp[x]]) << 9;
+            }
+            out[3 * vx] = static_cast<std::uint16_t>(w0);
+            out[3 * vx + 1] = static_cast<std::uint16_t>(w1);
+            out[3 * vx + 2] = static_cast<std::uint16_t>(w2);
         }
     }
 }
@@ -585,6 +615,18 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
 }
 
 
+__device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::uint32_t* total) {
+    const int lane = threadIdx.x & 31;
+    std::uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    *total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
+}
+
 // Redirect every branch through fwd; contracted junctions leave the graph
 // (no branches, pending kSkip).  Each branch reference takes the next parent slot of
 // its destination (the atomic's old value): slots < kInlineParents are written
@@ -615,22 +657,40 @@ k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj
             std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
             std::uint32_t waiting = 0;  // junction children Kahn still has to finish
             bool moved = false;
+            // each dependent step for all four branches at once (pass-through bits, then
+            // forwards, then predone bits, then the slot atomics back to back): the
+            // chain of loads and returning atomics was the kernel's latency
+            bool live[4], pt[4], need[4];
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                if (dd[b] & kTerm) continue;
-                const bool pt = (ptbits[dd[b] >> 5] >> (dd[b] & 31)) & 1u;
-                const std::uint32_t t = pt ? fwd[dd[b]] : dd[b];
-                moved |= pt;
-                dd[b] = t;
-                if ((predone[t >> 5] >> (t & 31)) & 1u) continue;  // finished in the walk: not a pending child
-                ++waiting;
-                if (i >= nj) continue;  // 1-saddles wait for no release: their lengths come after the rounds
-                const std::uint32_t slot = atomicAdd(&indeg[t], 1u);
-                if (slot < static_cast<std::uint32_t>(kInlineParents)) {
-                    node[t].par[slot] = static_cast<std::uint32_t>(i);
+                live[b] = !(dd[b] & kTerm);
+                pt[b] = live[b] && ((__ldg(&ptbits[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (pt[b]) {
+                    dd[b] = __ldg(&fwd[dd[b]]);
+                    moved = true;
+                }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                // finished in the walk: not a pending child
+                need[b] = live[b] && !((__ldg(&predone[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
+                waiting += need[b] ? 1u : 0u;
+                need[b] = need[b] && i < nj;  // 1-saddles wait for no release: lengths come after the rounds
+            }
+            std::uint32_t slot[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) slot[b] = need[b] ? atomicAdd(&indeg[dd[b]], 1u) : 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                if (!need[b]) continue;
+                const std::uint32_t t = dd[b];
+                if (slot[b] < static_cast<std::uint32_t>(kInlineParents)) {
+                    node[t].par[slot[b]] = static_cast<std::uint32_t>(i);
                 } else {
                     const unsigned long long q = atomicAdd(ovq_n, 1ull);
-                    if (q < ovq_cap) ovq[q] = make_uint4(t, slot, static_cast<std::uint32_t>(i), 0u);
+                    if (q < ovq_cap) ovq[q] = make_uint4(t, slot[b], static_cast<std::uint32_t>(i), 0u);
                 }
             }
             if (pending[i] != kDone) {
@@ -1089,17 +1149,6 @@ struct CountArgs {
     unsigned long long* resume;       // [0] round [1] frontier size [2] frontier buffer (0: fa, 1: fb)
 };
 
-__device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::uint32_t* total) {
-    const int lane = threadIdx.x & 31;
-    std::uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    *total = __shfl_sync(0xffffffffu, incl, 31);
-    return incl - v;
-}
 
 // Release the parents of a finished junction (visible to the next round through
 // the grid barrier): the first kInlineParents come with the node record, the rest
@@ -1567,9 +1616,19 @@ EGrid egrid(const Dims& d) {
 int launch_succ_table(const std::uint8_t* codes, const Dims& d, std::uint16_t* succ, cudaStream_t s, int num_sms) {
     const std::uint64_t rows = static_cast<std::uint64_t>(d.ny) * d.nz;
     if (rows == 0) return MSC3D_OK;
-    // one block per row, in row order: neighbouring rows share their code lines in L2
-    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(rows, 0x7fffffffull));
-    k_succ_table<<<grid, 128, 0, s>>>(codes, d, succ);
+    // persistent blocks walking the rows in order (the resident blocks work on a
+    // compact window of rows: neighbouring rows share their code lines in L2)
+    static std::uint8_t* lut[64] = {nullptr};
+    int dev = 0;
+    MSC3D_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return MSC3D_ERR_INVALID;
+    if (!lut[dev]) {
+        MSC3D_CUDA_TRY(cudaMalloc(&lut[dev], 12 * 256));
+        k_succ_lut<<<12, 256, 0, s>>>(lut[dev]);
+        count_launch();
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(rows, static_cast<std::uint64_t>(num_sms) * 8));
+    k_succ_table<<<grid, 256, 0, s>>>(codes, d, reinterpret_cast<const uint4*>(lut[dev]), succ);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
