@@ -33,6 +33,8 @@ sys.path.insert(0, ROOT)
 METRIC = "end-to-end MS complex Mcells/s and per-stage ms vs HBM roofline, 1/2/4/8 B200"
 WORKLOAD = {"name": "config3_512cube_gnoise_f32", "dims": (512, 512, 512), "kind": "gnoise", "seed": 1}
 CPU_SAMPLE = {"dims": (128, 128, 128), "kind": "gnoise", "seed": 1}
+# like-for-like anchor: BASELINE config 2, small enough for the reference on the box's cores
+PAIR = {"name": "config2_256cube_gauss_f32", "dims": (256, 256, 256), "kind": "gauss", "seed": 1}
 STAGES = ("gradient", "critical", "extrema", "reachability", "counting")
 
 
@@ -140,10 +142,92 @@ def cpu_reference_run(sample, threads):
     if os.path.exists(REF_SO):
         r = Ref()
         out = r.compute(v, sample["dims"], threads=threads, with_segmentation=True)
-        return out["wall"] - 0.0, list(out["timings"]), "reference", threads
+        # compute()'s wall clock minus its serial field_hash (timed apart)
+        return out["wall"] - out["hash_seconds"], list(out["timings"]), "reference", threads
     o = Oracle64()
     out = o.compute(v, sample["dims"])
     return out["wall"], None, "port", 1
+
+
+def like_for_like(ctx, local, stream, reps=3):
+    """BASELINE config 2 (256^3 gauss), both sides on this box: the GPU device-resident
+    compute(), the GPU end to end through the C ABI with host buffers, the C++ drop-in
+    msc3d::compute() (with and without the serial field_hash it overlaps), and the
+    unmodified reference compute() on all host cores minus its field_hash (SURVEY.md
+    8(d)); best of `reps` each."""
+    import torch
+
+    import paper_2009_03707_b200 as m
+    from oracle.pyoracle import REF_SO, Ref
+    if not os.path.exists(REF_SO):
+        return None
+    dims = PAIR["dims"]
+    n = cells(dims)
+    v = m.synth(PAIR["kind"], dims, PAIR["seed"])
+    # GPU device-resident
+    dev = torch.from_numpy(v).to(f"cuda:{local}")
+    ctx.bind_values(dev.data_ptr(), dims, m.VALUE_F32)
+    ctx.compute(m.OPT_SEGMENTATION)
+    dev_ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.compute(m.OPT_SEGMENTATION)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dev_ms.append(e0.elapsed_time(e1))
+    # GPU end to end: pinned samples in, every output in pinned host memory
+    c = [ctx.scalar(f"c{k}") for k in range(4)]
+    na = ctx.scalar("arcs_min") + ctx.scalar("arcs_ss") + ctx.scalar("arcs_max")
+    ncp, V = sum(c), dims[0] * dims[1] * dims[2]
+    Cu = (dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1)
+    host_in = torch.from_numpy(v).pin_memory()
+    b = {k: torch.empty(x, dtype=torch.uint8).pin_memory() for k, x in
+         (("cp_cell", ncp * 4), ("cp_index", ncp), ("src", na * 4), ("dst", na * 4), ("mult", na * 8),
+          ("lmin", V * 4), ("lmax", Cu * 4))}
+    ho = m.HostOutputs(b["cp_cell"].data_ptr(), ncp * 4, b["cp_index"].data_ptr(), ncp, b["src"].data_ptr(),
+                       b["dst"].data_ptr(), b["mult"].data_ptr(), na, b["lmin"].data_ptr(), b["lmax"].data_ptr(), 0, 0)
+    e2e_s = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        rc = ctx._L.msc3d_ctx_compute_host_values(ctx.h, m.Dims(*dims), m.VALUE_F32, C.c_void_p(host_in.data_ptr()),
+                                                  m.OPT_SEGMENTATION, None, C.byref(ho))
+        e2e_s.append(time.perf_counter() - t0)
+        if rc:
+            raise RuntimeError(f"compute_host failed: {rc}")
+    # the C++ drop-in
+    L = m.lib()
+    L.msc3d_api_timed_compute.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                          C.POINTER(C.c_double)]
+    out = (C.c_double * 8)()
+    v32 = np.ascontiguousarray(v, dtype=np.float32)
+    api, api_x = [], []
+    for _ in range(reps + 1):
+        if L.msc3d_api_timed_compute(v32.ctypes.data, dims[0], dims[1], dims[2], 1, out):
+            raise RuntimeError("msc3d::compute() failed")
+        api.append(out[0])
+        api_x.append(out[6])
+    # the unmodified reference on every host core
+    threads = os.cpu_count() or 1
+    r = Ref()
+    ref_s, ref_stage = [], None
+    v64 = v.astype(np.float64)
+    for _ in range(reps):
+        o = r.compute(v64, dims, threads=threads, with_segmentation=True)
+        ref_s.append(o["wall"] - o["hash_seconds"])
+        ref_stage = list(o["timings"])
+    g_e2e, g_api, g_apix, cpu = min(e2e_s[1:]), min(api[1:]), min(api_x[1:]), min(ref_s)
+    return {
+        "workload": PAIR["name"], "dims": list(dims), "lattice_cells": n,
+        "gpu_device_ms": min(dev_ms), "gpu_e2e_ms": g_e2e * 1e3, "gpu_api_ms": g_api * 1e3,
+        "gpu_api_excl_field_hash_ms": g_apix * 1e3,
+        "cpu_reference_ms": cpu * 1e3, "cpu_reference_stage_s": ref_stage, "cpu_cores": threads,
+        "cpu_reference_field_hash_s": o["hash_seconds"],
+        "speedup_e2e": cpu / g_e2e, "speedup_api_excl_field_hash": cpu / g_apix,
+        "speedup_device": cpu / (min(dev_ms) / 1e3),
+        "note": "same field and same box; reference = unmodified compute() on all host cores, wall minus its "
+                "serial field_hash (SURVEY.md 8(d)); best of 3 each",
+    }
 
 
 def run_reference_arm(args, world, rank):
@@ -448,6 +532,7 @@ def main():
             raise RuntimeError("msc3d::compute() output sizes differ from the device-resident run")
         api = {"value": ncells / secs[-1] / 1e6, "unit": "Mcells/s", "seconds": secs[-1],
                "first_call_seconds": secs[0], "field_hash_seconds": out[3],
+               "seconds_excl_field_hash": out[6], "value_excl_field_hash": ncells / out[6] / 1e6,
                "path": "msc3d::compute(ScalarField, {with_segmentation}) -> MSComplex (C++ drop-in API): "
                        "parallel f32 conversion + pinned upload, device pipeline, pinned download, parallel "
                        "host assembly; the byte-serial field_hash (FNV-1a, msc.cpp:31-42) runs concurrently"}
@@ -461,6 +546,10 @@ def main():
                "sample": f"{d[0]}^3 {CPU_SAMPLE['kind']} f32, one full compute() with segmentation, "
                          f"threads={used}", "seconds": secs, "stage_s": tim}
 
+    pair = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.size:
+        pair = like_for_like(ctx, local, stream)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mcells/s", "n_gpus": world, "steps": args.steps,
@@ -470,7 +559,7 @@ def main():
                        "seed": WORKLOAD["seed"], "lattice_cells": ncells,
                        "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (512 MiB f32 in, 1 GiB codes)"},
             "stages_ms": dict(zip(STAGES, stage_ms)), "stages": stages, "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e, "e2e_api": api, "gpu_launches": int(launches),
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_api": api, "like_for_like": pair, "gpu_launches": int(launches),
             "counts": {"critical": c, "arcs_min": a_min, "arcs_ss": a_ss, "arcs_max": a_max},
             "clocks": clk.summary(),
         }
