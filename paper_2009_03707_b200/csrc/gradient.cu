@@ -28,7 +28,11 @@
 // Every cell is written exactly once, by the owner of its maximal vertex (plain
 // byte stores).  The same kernel emits both extremum forests (build_forest,
 // extrema.cpp:43-77) and the per-dimension critical counts.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -180,7 +184,13 @@ std::vector<std::uint16_t> host_octant_table() {
 
 constexpr int TX = 32, TY = 4, TZ = 2;
 constexpr int NT = TX * TY * TZ;
-constexpr int SX = TX + 2, SY = TY + 2, SZ = TZ + 2;
+// A tile row in shared memory starts XO = 4 columns left of the tile's first vertex
+// (the halo column is column 3) and is SX = 40 wide: the TMA box of the f32 tile loads
+// (k_gradient<float, true>) must start at a 16-byte aligned x offset and span a multiple
+// of 16 bytes.
+constexpr int XO = 4;
+constexpr int SX = TX + 2 * XO, SY = TY + 2, SZ = TZ + 2;
+constexpr unsigned kTileBytesF32 = SX * SY * SZ * 4;  // 3840 = 30 x 128 (TMA destinations stay 128-B aligned)
 constexpr std::uint32_t kCentre = 1u << 13;
 constexpr std::uint32_t kAll = (1u << 27) - 1;
 
@@ -558,18 +568,56 @@ struct StarLists {
 // every thread of the grid serialises in the L2).
 constexpr int kListBuf = 1024;
 
-template <typename T>
+// ---- TMA tile loads (sm_90+ tensor memory accelerator; Blackwell sm_100a) -------------
+// One elected thread issues the box copy global -> shared for each tile of a group;
+// completion is tracked by a transaction-count mbarrier per buffer set, which every
+// thread waits on (parity) before reading the tile.  Out-of-box coordinates (the -1
+// halo, tiles past the grid) are zero-filled by the hardware, as the cp.async path
+// does by hand.
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+        "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+template <typename T, bool kTma>
 __global__ void __launch_bounds__(NT, 5)
 k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
            std::uint32_t* __restrict__ parent0, std::uint32_t* __restrict__ parent3,
-           unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first) {
+           unsigned long long* __restrict__ crit_totals, StarLists lists, uint3 tiles, unsigned tz_first,
+           const __grid_constant__ CUtensorMap tmap) {
     // Tiles go in groups of kGroup (consecutive along x): phase 1 bins the group's
     // 3..8-cell stars by size, phase 2 runs them all -- ~2x the work per barrier, so
     // fewer idle lanes.  f32: two buffer sets, the next group streams in (cp.async)
     // while this one is processed; f64: one set (static shared memory budget).
     constexpr int kGroup = 2;
     constexpr int kSets = sizeof(T) == 4 ? 2 : 1;
-    __shared__ T tiles_sm[kSets][kGroup][SZ][SY][SX];
+    __shared__ alignas(128) T tiles_sm[kSets][kGroup][SZ][SY][SX];
+    __shared__ alignas(8) std::uint64_t s_bar[kSets];  // TMA: one transaction barrier per buffer set
     __shared__ std::uint32_t s_fac[27], s_cof[27];
     __shared__ std::int32_t s_cell[27];
     __shared__ std::uint32_t s_coff[27];
@@ -584,6 +632,9 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     __shared__ std::uint32_t s_wS[kGroup * NT];
     __shared__ std::uint16_t s_wid[kGroup * NT];  // tile-in-group << 8 | vertex in tile
     const int tid = threadIdx.x + TX * (threadIdx.y + TY * threadIdx.z);
+    // the tensor map stays in the kernel's parameter space (a copy in local memory is
+    // not a valid TMA operand): its address is taken here, outside the lambdas
+    const CUtensorMap* tmap_p = &tmap;
     if (tid < 27) {
         s_fac[tid] = c_slot.facet[tid];
         s_cof[tid] = c_slot.cofacet[tid];
@@ -610,11 +661,12 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     std::uint32_t crit[4] = {0, 0, 0, 0};
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
     const std::uint64_t ngroups = (ntiles + kGroup - 1) / kGroup;
-    // tile origin (the -1 halo corner), 32-bit: tile ids and coordinates fit
+    // tile origin (shared-memory column 0 = x - XO; the -1 halo corner in y and z),
+    // 32-bit: tile ids and coordinates fit
     auto origin = [&](std::uint64_t ti, std::int64_t& x0, std::int64_t& y0, std::int64_t& z0) {
         const std::uint32_t t32 = static_cast<std::uint32_t>(ti);
         const std::uint32_t tyz = t32 / tiles.x;
-        x0 = static_cast<std::int64_t>(static_cast<int>((t32 - tyz * tiles.x) * TX) - 1);
+        x0 = static_cast<std::int64_t>(static_cast<int>((t32 - tyz * tiles.x) * TX) - XO);
         y0 = static_cast<std::int64_t>(static_cast<int>((tyz % tiles.y) * TY) - 1);
         z0 = static_cast<std::int64_t>(static_cast<int>((tyz / tiles.y + tz_first) * TZ) - 1);
     };
@@ -625,6 +677,20 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
     // copies, the rest (and tiles past the end) 0.  Interior tiles (the common case)
     // skip the per-sample range checks.
     auto load_group = [&](std::uint64_t gi, int b) {
+        if constexpr (kTma) {
+            if (tid == 0) {
+                // the generic-proxy reads of this buffer set are done (barrier before)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&s_bar[b], kGroup * kTileBytesF32);
+                for (int g = 0; g < kGroup; ++g) {
+                    std::int64_t x0, y0, z0;
+                    origin(gi * kGroup + g, x0, y0, z0);  // past the last tile: z0 >= nz, all zero-filled
+                    tma_load_3d(&tiles_sm[b][g][0][0][0], tmap_p, static_cast<int>(x0), static_cast<int>(y0),
+                                static_cast<int>(z0), &s_bar[b]);
+                }
+            }
+            return;
+        }
         for (int g = 0; g < kGroup; ++g) {
             const std::uint64_t ti = gi * kGroup + g;
             std::int64_t x0, y0, z0;
@@ -662,10 +728,23 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    unsigned phase = 0;  // TMA: parity bit of each set's barrier (bit b)
+    if constexpr (kTma) {
+        if (tid == 0) {
+            for (int b = 0; b < kSets; ++b) mbar_init(&s_bar[b], 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the barriers, visible to the TMA unit
+        }
+        __syncthreads();
+    }
     if (blockIdx.x < ngroups) load_group(blockIdx.x, 0);
     int cur = 0;
     for (std::uint64_t gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        if constexpr (kTma) {
+            mbar_wait(&s_bar[cur], (phase >> cur) & 1u);
+            phase ^= 1u << cur;
+        } else {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
         __syncthreads();  // group gi in shared memory; the previous group's work done
         if (s_ln[0] + kGroup * NT > kListBuf || s_ln[1] + kGroup * NT > kListBuf) flush_lists();
         const std::uint64_t gn = gi + gridDim.x;
@@ -683,7 +762,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             if (ti >= ntiles) return false;
             const std::int64_t x0 = g ? ox1 : ox0, y0 = g ? oy1 : oy0, z0 = g ? oz1 : oz0;
             const int lx = lid % TX, ly = (lid / TX) % TY, lz = lid / (TX * TY);
-            w.vx = x0 + 1 + lx;
+            w.vx = x0 + XO + lx;
             w.vy = y0 + 1 + ly;
             w.vz = z0 + 1 + lz;
             if (w.vx >= d.nx || w.vy >= d.ny || w.vz >= d.nz) return false;
@@ -717,7 +796,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             Sg[g] = 0;
             StarWriter w;
             if (writer_for(g, tid, w)) {
-                const T* base = &tiles_sm[set][g][threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + 1];
+                const T* base = &tiles_sm[set][g][threadIdx.z + 1][threadIdx.y + 1][threadIdx.x + XO];
                 const T fv = base[0];
                 std::uint32_t below = kCentre;
 #pragma unroll
@@ -778,7 +857,7 @@ k_gradient(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ codes,
             const std::uint32_t Sw = s_wS[k];
             StarWriter w;
             writer_for(g, lid, w);
-            const T* base = &tiles_sm[set][g][lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + 1];
+            const T* base = &tiles_sm[set][g][lid / (TX * TY) + 1][(lid / TX) % TY + 1][lid % TX + XO];
             if (use_oct && k >= s_woct && octant_fast<T>(base, Sw, g_oct, w)) {
                 // a unit-cube star: paired from the table (false only on tied values)
             } else if (!star_fast<8, T>([&](int t) { return base[tile_off(t)]; }, Sw, __popc(Sw), s_fac, s_cof,
@@ -1005,6 +1084,35 @@ k_gradient_deferred(const T* __restrict__ f, Dims d, std::uint8_t* __restrict__ 
 
 bool g_tables_ready[64] = {false};
 
+// The samples as a 3-D tensor (x fastest) with a 36 x 6 x 4 box: one TMA copy per tile.
+// Needs 16-byte row strides (nx % 4 == 0) and an aligned base; false -> the cp.async path.
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point query,
+// so the library does not link libcuda.
+bool f32_tensor_map(const void* values, const Dims& d, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (std::getenv("MSC3D_NO_TMA")) return false;
+    if (!tried) {
+        tried = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        else
+            cudaGetLastError();
+    }
+    if (!encode || d.nx % 4 != 0 || (reinterpret_cast<std::uintptr_t>(values) & 15) != 0) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.nx), static_cast<cuuint64_t>(d.ny),
+                                static_cast<cuuint64_t>(d.nz)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d.nx) * 4, static_cast<cuuint64_t>(d.nx * d.ny) * 4};
+    const cuuint32_t box[3] = {SX, SY, SZ};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(values), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 int upload_gradient_tables(int device) {
@@ -1045,12 +1153,16 @@ int gradient_tiles(const void* values, int value_type, const Dims& d, std::uint8
     const std::uint64_t ntiles = static_cast<std::uint64_t>(tiles.x) * tiles.y * tiles.z;
     // persistent tile loop: a few blocks per SM, each walking tiles with stride grid
     const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(num_sms) * 8)));
+    CUtensorMap tmap;
     if (value_type == MSC3D_VALUE_F64)
-        k_gradient<double><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d, codes, parent0, parent3,
-                                                       crit_totals, lists, tiles, tz0);
+        k_gradient<double, false><<<grid, block, 0, stream>>>(static_cast<const double*>(values), d, codes, parent0,
+                                                              parent3, crit_totals, lists, tiles, tz0, tmap);
+    else if (f32_tensor_map(values, d, &tmap))
+        k_gradient<float, true><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes, parent0,
+                                                            parent3, crit_totals, lists, tiles, tz0, tmap);
     else
-        k_gradient<float><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes, parent0, parent3,
-                                                      crit_totals, lists, tiles, tz0);
+        k_gradient<float, false><<<grid, block, 0, stream>>>(static_cast<const float*>(values), d, codes, parent0,
+                                                             parent3, crit_totals, lists, tiles, tz0, tmap);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

@@ -8,6 +8,9 @@ counting kernel's launch configurations.
 * Config 3 (512^3 gnoise, ~40 min of reference CPU time) is compared against SHA-256
   digests of the reference's outputs, committed in tests/golden/config3_digests.json
   by tests/golden/make_config_digests.py (oracle/config_digest.cpp).
+* Config 4 (1024^3 gauss, 8.6 G lattice cells: 64-bit ids, which the reference
+  rejects, grid.cpp:17-20) is compared against digests of oracle64 (our restatement,
+  pinned against the reference below 2^32 cells; oracle/config4_digest.cpp).
 * "wide_ids" forces the 64-bit cell-id lists grids with >= 2^32 cells use (configs
   4-5; the reference rejects them, grid.cpp:17-20) on small grids, so that path is
   compared with the reference too.
@@ -27,7 +30,8 @@ from tests.fields import quantized, random_field
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-CONFIGS = {1: ("gauss", (64, 64, 64)), 2: ("gauss", (256, 256, 256)), 3: ("gnoise", (512, 512, 512))}
+CONFIGS = {1: ("gauss", (64, 64, 64)), 2: ("gauss", (256, 256, 256)), 3: ("gnoise", (512, 512, 512)),
+           4: ("gauss", (1024, 1024, 1024))}
 
 
 def _sha(a) -> str:
@@ -72,7 +76,7 @@ def test_config_live_equals_reference(ctx, ref, config):
     _assert_same(_device_outputs(ctx, v, dims), ref, v, dims)
 
 
-@pytest.mark.parametrize("config", [1, 2, 3])
+@pytest.mark.parametrize("config", [1, 2, 3, 4])
 def test_config_digests_equal_reference(ctx, config):
     path = os.path.join(GOLDEN, f"config{config}_digests.json")
     if not os.path.exists(path):
