@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -76,6 +78,15 @@ struct msc3d_ctx {
             if (cudaMalloc(&a.ptr, want) != cudaSuccess) {
                 cudaGetLastError();
                 a.ptr = nullptr;
+                if (std::getenv("MSC3D_ALLOC_TRACE")) {  // development: what holds the device memory
+                    std::size_t held = 0;
+                    for (const auto& kv : arrays) held += kv.second.cap;
+                    std::fprintf(stderr, "msc3d: cannot allocate %s (%.2f GB); the context holds %.2f GB:\n",
+                                 name.c_str(), want / 1e9, held / 1e9);
+                    for (const auto& kv : arrays)
+                        if (kv.second.cap > (std::size_t(1) << 28))
+                            std::fprintf(stderr, "  %-20s %8.2f GB\n", kv.first.c_str(), kv.second.cap / 1e9);
+                }
                 return nullptr;
             }
             a.cap = want;
