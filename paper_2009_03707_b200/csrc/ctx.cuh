@@ -112,6 +112,16 @@ struct msc3d_ctx {
         auto it = arrays.find(name);
         if (it != arrays.end()) it->second.count = 0;
     }
+    // Large grids (configs 4-5, > 2^32 cells) hand the memory of a stage's transient
+    // arrays back once the stage is done (later stages allocate into it);
+    // smaller grids keep them so that repeated computes allocate nothing.
+    bool release_transients() const { return dims.n_cells > 0xffffffffull; }
+    void release(const std::string& name) {
+        auto it = arrays.find(name);
+        if (it == arrays.end()) return;
+        if (it->second.ptr) cudaFree(it->second.ptr);  // (synchronises: large grids only)
+        arrays.erase(it);
+    }
     int id_width() const { return (!force_wide && dims.n_cells <= 0xffffffffull) ? 4 : 8; }
     // Copy the first n u64 of d_small to h_small and wait.  The copy is a tiny
     // kernel writing the mapped host mirror over the bus, not a DMA: a DMA would

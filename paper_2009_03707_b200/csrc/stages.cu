@@ -757,6 +757,11 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
                                         reinterpret_cast<unsigned long long*>(ctx->d_small + 35),
                                         ctx->h_small + 35, amin_src, amin_dst, amin_mul, s, sms));
     TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, amax_src, amax_dst, amax_mul, s, sms));
+    if (ctx->release_transients())
+        for (const char* t : {"slot_min", "per_min", "min_off", "slot_max", "cnt_max", "off_max", "sort_key",
+                              "sort_scratch", "sort_cursor", "sort_large", "rank_bits", "rank_cnt", "rank_pre",
+                              "star_list16", "star_list32", "star_list_ties", "jump_conv"})
+            ctx->release(t);
     if (host) {
         if (host->arc_cap < na) return MSC3D_ERR_INVALID;
         TRY(sink.copy(host->arc_src, amin_src, na * 4));
