@@ -308,6 +308,10 @@ struct VolumeSpec {
     bool big_endian = false;
 };
 ScalarField read_volume(const VolumeSpec& spec);
+// Extension (not in the reference API): compute(read_volume(spec), opt) with the same
+// results and errors; f32 little-endian files are read straight into pinned upload
+// memory (no vector of doubles).  The CLI's path.
+MSComplex compute_volume(const VolumeSpec& spec, const ComputeOptions& opt = {});
 
 // ---------------------------------------------------------------- serialize.hpp:21-45
 class ParseError : public std::runtime_error {

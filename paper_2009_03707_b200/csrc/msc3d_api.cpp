@@ -566,18 +566,24 @@ std::uint64_t field_hash(const ScalarField& f) { return msc3d_field_hash_f64(f.v
 // filled in parallel slices.  Results are identical to the serial assembly.
 thread_local double g_last_seconds_excl_hash = 0;  // the last compute() without field_hash
 
+namespace {
+using Clock = std::chrono::steady_clock;
+// MSC3D_API_TRACE=1: phase times of a compute() on stderr
+void trace_mark(Clock::time_point t_start, const char* what) {
+    static const bool trace = std::getenv("MSC3D_API_TRACE") != nullptr;
+    if (trace)
+        std::fprintf(stderr, "compute() %-18s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(Clock::now() - t_start).count());
+}
+MSComplex finish(Device& dev, const GridDims& dims, const ComputeOptions& opt, std::future<std::uint64_t>& hash,
+                 Clock::time_point t_start);
+}  // namespace
+
 MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     Device& dev = device();
     std::lock_guard<std::mutex> lock(dev.mu);
     const int T = host_threads(opt.threads);
-    // MSC3D_API_TRACE=1: phase times of this call on stderr
-    static const bool trace = std::getenv("MSC3D_API_TRACE") != nullptr;
-    const auto t_start = std::chrono::steady_clock::now();
-    auto mark = [&](const char* what) {
-        if (trace)
-            std::fprintf(stderr, "compute() %-18s %8.1f ms\n", what,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
-    };
+    const auto t_start = Clock::now();
     auto hash = std::async(std::launch::async, [&f] { return field_hash(f); });
     const std::size_t nv = f.values.size();
     if (nv != f.dims.vertex_count()) throw std::invalid_argument("scalar field size mismatch");
@@ -598,7 +604,51 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
         else
             check(msc3d_ctx_load_values(dev.ctx, to_c(f.dims), MSC3D_VALUE_F64, f.values.data()), "ScalarField");
     }
-    mark("uploaded");
+    trace_mark(t_start, "uploaded");
+    return finish(dev, f.dims, opt, hash, t_start);
+}
+
+// read_volume + compute for a raw volume file (the CLI's path, not in the reference API):
+// f32 little-endian samples are read straight into the pinned upload buffer -- no
+// widening to a vector of doubles, no conversion pass; field_hash runs over the widened
+// f32 samples (same bytes, msc.cpp:31-42), the device validates them (grid.cpp:86-88).
+// Other sample types take read_volume + compute.
+MSComplex compute_volume(const VolumeSpec& spec, const ComputeOptions& opt) {
+    if (spec.dtype != SampleType::f32 || spec.big_endian) return compute(read_volume(spec), opt);
+    Device& dev = device();
+    std::lock_guard<std::mutex> lock(dev.mu);
+    const auto t_start = Clock::now();
+    const std::uint64_t nv = spec.dims.vertex_count();
+    std::FILE* fp = std::fopen(spec.path.c_str(), "rb");
+    if (!fp) throw IoError("cannot read '" + spec.path + "'");
+    std::fseek(fp, 0, SEEK_END);
+    const long long size = std::ftell(fp);
+    std::fseek(fp, 0, SEEK_SET);
+    if (size < 0 || static_cast<std::uint64_t>(size) != nv * 4) {
+        std::fclose(fp);
+        throw std::invalid_argument("volume size mismatch for '" + spec.path + "': file has " +
+                                    std::to_string(size) + " bytes, need " + std::to_string(nv * 4));
+    }
+    auto* v32 = static_cast<float*>(dev.in.get(std::max<std::uint64_t>(1, nv) * 4));
+    const std::size_t got = nv ? std::fread(v32, 4, nv, fp) : 0;
+    std::fclose(fp);
+    if (got != nv) throw IoError("short read on '" + spec.path + "'");
+    trace_mark(t_start, "read (pinned)");
+    auto hash = std::async(std::launch::async, [v32, nv] { return msc3d_field_hash_f32(v32, nv); });
+    const int rc = msc3d_ctx_load_values(dev.ctx, to_c(spec.dims), MSC3D_VALUE_F32, v32);
+    if (rc != MSC3D_OK) {
+        hash.wait();
+        check(rc, "ScalarField");
+    }
+    trace_mark(t_start, "uploaded");
+    return finish(dev, spec.dims, opt, hash, t_start);
+}
+
+namespace {
+MSComplex finish(Device& dev, const GridDims& dims, const ComputeOptions& opt, std::future<std::uint64_t>& hash,
+                 Clock::time_point t_start) {
+    const int T = host_threads(opt.threads);
+    auto mark = [&](const char* what) { trace_mark(t_start, what); };
     double ms[5] = {0, 0, 0, 0, 0};
     // ComputeOptions::validate: the device audit runs between the gradient and the
     // critical stage (msc.cpp:67-70); a broken gradient -> runtime_error
@@ -626,7 +676,7 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     const std::size_t ncp = count_of("cp_cell", static_cast<int>(sizeof(CellIndex)));
     const std::size_t na = count_of("arc_src", 4);
     MSComplex m;
-    m.dims = f.dims;
+    m.dims = dims;
     m.dtype = opt.source_dtype;
     // allocation (value-initialisation + first touch) of the big vectors on their own
     // threads, overlapping the copies
@@ -666,7 +716,7 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
             cp.id = static_cast<std::uint32_t>(i);
             cp.cell = cells[i];
             cp.index = index[i];
-            cp.doubled = unpack_cell(f.dims, cells[i]);
+            cp.doubled = unpack_cell(dims, cells[i]);
             cp.midpoint = {cp.doubled.x / 2.0, cp.doubled.y / 2.0, cp.doubled.z / 2.0};
             cp.value = value[i];  // f[max_vertex_of(f, cell)], from the device
         }
@@ -687,12 +737,12 @@ MSComplex compute(const ScalarField& f, const ComputeOptions& opt) {
     }
     mark("arcs+labels filled");
     // everything but the byte-serial field_hash, which overlaps it (bench: e2e_api)
-    g_last_seconds_excl_hash =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    g_last_seconds_excl_hash = std::chrono::duration<double>(Clock::now() - t_start).count();
     m.input_hash = hash.get();
     mark("hash done");
     return m;
 }
+}  // namespace
 
 // boundary_check (msc.cpp:149-167) on the device (audit.cu).
 BoundaryReport boundary_check(const MSComplex& m) {

@@ -128,7 +128,6 @@ int cmd_compute(const Options& o) {
     spec.dims = msc3d::GridDims(o.dims[0], o.dims[1], o.dims[2]);
     spec.dtype = msc3d::parse_sample_type(o.dtype);
     spec.big_endian = o.big_endian;
-    const msc3d::ScalarField field = msc3d::read_volume(spec);
 
     msc3d::StageTimings t;
     msc3d::ComputeOptions copt;
@@ -137,7 +136,8 @@ int cmd_compute(const Options& o) {
     copt.validate = o.check;
     copt.source_dtype = msc3d::sample_type_name(spec.dtype);
     copt.timings = &t;
-    const msc3d::MSComplex cx = msc3d::compute(field, copt);
+    // read_volume + compute; f32 LE files go straight into pinned upload memory
+    const msc3d::MSComplex cx = msc3d::compute_volume(spec, copt);
 
     std::fprintf(stderr, "device stage seconds: gradient %.4f | critical %.4f | extrema %.4f | "
                          "reachability %.4f | counting %.4f\n",

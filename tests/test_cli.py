@@ -69,6 +69,29 @@ def test_cli_compute_matches_reference(tmp_path, ref):
 
 
 @pytest.mark.gpu
+def test_cli_pinned_f32_ingest_errors(tmp_path):
+    """f32 files take the pinned-ingest path (msc3d::compute_volume): a non-finite sample
+    is invalid input (exit 3, volume.cpp:89-94 / grid.cpp:86-88), as are u8 / f64 files
+    through read_volume, and a big-endian f32 file gives the same complex as the LE one."""
+    dims = (12, 10, 8)
+    v = m.synth("gnoise", dims)
+    bad = v.copy()
+    bad[17] = np.nan
+    raw = tmp_path / "nan.raw"
+    bad.astype("<f4").tofile(raw)
+    assert run("--input", raw, "--dims", *dims, "--dtype", "f32", "--out", tmp_path / "o.json").returncode == 3
+    le, be = tmp_path / "le.raw", tmp_path / "be.raw"
+    v.astype("<f4").tofile(le)
+    v.astype(">f4").tofile(be)
+    for path, extra in ((le, []), (be, ["--big-endian"])):
+        r = run("--input", path, "--dims", *dims, "--dtype", "f32", *extra, "--format", "csv",
+                "--out", tmp_path / path.stem)
+        assert r.returncode == 0, r.stderr
+    assert (tmp_path / "le_arcs.csv").read_bytes() == (tmp_path / "be_arcs.csv").read_bytes()
+    assert (tmp_path / "le_critical_points.csv").read_bytes() == (tmp_path / "be_critical_points.csv").read_bytes()
+
+
+@pytest.mark.gpu
 def test_cli_large_complex_matches_reference(tmp_path, ref):
     """A complex large enough that the drop-in compute() takes its parallel host path
     (result vectors >= 64 MB: reserved, huge-page advised, pre-faulted from several
