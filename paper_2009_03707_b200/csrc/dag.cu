@@ -721,12 +721,15 @@ k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj
     if (is_ready) ready[s_base + s_wc[w] + __popc(rb & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
 }
 
+// Overflow-list segments of the nodes with more than kInlineParents parents (~0.1%):
+// allocated by an atomic cursor (their order is irrelevant), no scan over all nodes.
 __global__ void k_parent_overflow(const std::uint32_t* __restrict__ indeg, std::uint64_t nj,
-                                  std::uint32_t* __restrict__ ovcnt) {
+                                  std::uint64_t* __restrict__ ovoff, unsigned long long* __restrict__ total) {
     for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < nj;
          j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         const std::uint32_t k = indeg[j];
-        ovcnt[j] = k > static_cast<std::uint32_t>(kInlineParents) ? k - kInlineParents : 0u;
+        if (k > static_cast<std::uint32_t>(kInlineParents))
+            ovoff[j] = atomicAdd(total, static_cast<unsigned long long>(k - kInlineParents));
     }
 }
 
@@ -1711,10 +1714,11 @@ int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nod
     return MSC3D_OK;
 }
 
-int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
-                           int num_sms) {
+int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint64_t* ovoff,
+                           unsigned long long* total, cudaStream_t s, int num_sms) {
+    MSC3D_CUDA_TRY(cudaMemsetAsync(total, 0, 8, s));
     if (nj == 0) return MSC3D_OK;
-    k_parent_overflow<<<grid_for(nj, num_sms), kThreads, 0, s>>>(indeg, nj, ovcnt);
+    k_parent_overflow<<<grid_for(nj, num_sms), kThreads, 0, s>>>(indeg, nj, ovoff, total);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

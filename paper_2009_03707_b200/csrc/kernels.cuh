@@ -214,8 +214,8 @@ int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nod
                    const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms);
-int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint32_t* ovcnt, cudaStream_t s,
-                           int num_sms);
+int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint64_t* ovoff,
+                           unsigned long long* total, cudaStream_t s, int num_sms);
 // node records' parent counts / overflow offsets, and the queued overflow parents
 int launch_fill_parents(void* node, std::uint64_t nj, const std::uint32_t* indeg, const std::uint64_t* ovoff,
                         const void* ovq, std::uint64_t n_ovq, std::uint32_t* rsrc, cudaStream_t s, int num_sms);

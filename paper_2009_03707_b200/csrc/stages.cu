@@ -339,7 +339,6 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nn, 4));
     auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
     auto* fwd = static_cast<std::uint32_t*>(ctx->ensure("jfwd", nj, 4));
-    auto* ovcnt = static_cast<std::uint32_t*>(ctx->ensure("ovcnt", nj, 4));
     auto* ovoff = static_cast<std::uint64_t*>(ctx->ensure("ovoff", nj, 8));
     void* rec = ctx->ensure("jrec", nj, msc3d_dev::count_rec_bytes());
     auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
@@ -347,7 +346,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
     auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
     auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!jlist || !node || !jdest || !pending || !pending0 || !indeg || !fwd || !ovcnt || !ovoff || !rec ||
+    if (!jlist || !node || !jdest || !pending || !pending0 || !indeg || !fwd || !ovoff || !rec ||
         !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
     void* jrank = ctx->ensure("jrank", nwords, 8);
@@ -393,8 +392,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     TRY(msc3d_dev::launch_rewrite(node, jdest, nj, nn, fwd, ptbits, predone, pending, indeg, ovq, ovq_n, ovq_cap, n_skip,
                                   ready, n_ready, s, sms));
     // parents beyond the inline ones: an overflow list
-    TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovcnt, s, sms));
-    TRY(msc3d_dev::scan_u32(ovcnt, nj, ovoff, ctx->d_small, ctx->ws, s));
+    TRY(msc3d_dev::launch_parent_overflow(indeg, nj, ovoff, reinterpret_cast<unsigned long long*>(ctx->d_small), s,
+                                          sms));
     TRY(ctx->fetch_small(28));
     if (static_cast<unsigned int>(ctx->h_small[27])) return MSC3D_ERR_RUNTIME;  // cycle in a walk
     if (nj && ctx->h_small[25] > 64) return MSC3D_ERR_RUNTIME;                  // cycle of pass-through junctions
