@@ -635,6 +635,11 @@ __device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, std::ui
 // Junctions left with no pending child are Kahn's round 0: appended to `ready` in
 // index order within a block (one reservation per block; blocks run roughly in id
 // order), so round 0 runs over a dense list instead of scanning every junction.
+// Each thread rewrites kRwPer nodes (i, i + kThreads, ...) with every dependent step
+// issued for all their branches at once (pass-through bits, then forwards, then predone
+// bits, then the slot atomics back to back): the kernel is a chain of dependent random
+// loads and returning atomics, so independent nodes per thread are what hides it.
+constexpr int kRwPer = 2;
 __global__ void __launch_bounds__(kThreads)
 k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj, std::uint64_t n_nodes,
           const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
@@ -643,82 +648,104 @@ k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj
           unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
           unsigned long long* __restrict__ n_skip, std::uint32_t* __restrict__ ready,
           unsigned long long* __restrict__ n_ready) {
-    __shared__ unsigned s_wc[kThreads / 32];
+    constexpr int NB = 4 * kRwPer;
+    __shared__ unsigned s_wc[kRwPer][kThreads / 32];
     __shared__ unsigned long long s_base;
-    const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    bool skip = false, is_ready = false;
-    if (i < n_nodes) {
-        uint4* dp = dest + i;
-        if (i < nj && ((ptbits[i >> 5] >> (i & 31)) & 1u)) {
-            pending[i] = kSkip;  // (its record is never read again)
-            skip = true;
+    std::uint64_t id[kRwPer];
+    bool act[kRwPer], skip[kRwPer], is_ready[kRwPer];
+    std::uint32_t dd[NB];
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k) {
+        id[k] = (blockIdx.x * static_cast<std::uint64_t>(kRwPer) + k) * kThreads + threadIdx.x;
+        skip[k] = id[k] < n_nodes && id[k] < nj && ((ptbits[id[k] >> 5] >> (id[k] & 31)) & 1u);
+        act[k] = id[k] < n_nodes && !skip[k];
+        is_ready[k] = false;
+        uint4 d4 = act[k] ? dest[id[k]] : make_uint4(kTerm, kTerm, kTerm, kTerm);
+        dd[4 * k] = d4.x;
+        dd[4 * k + 1] = d4.y;
+        dd[4 * k + 2] = d4.z;
+        dd[4 * k + 3] = d4.w;
+    }
+    bool live[NB], pt[NB], need[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        live[b] = !(dd[b] & kTerm);
+        pt[b] = live[b] && ((__ldg(&ptbits[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
+    }
+    bool moved[kRwPer];
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k) moved[k] = false;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+        if (pt[b]) {
+            dd[b] = __ldg(&fwd[dd[b]]);
+            moved[b / 4] = true;
+        }
+    std::uint32_t waiting[kRwPer];  // junction children Kahn still has to finish
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k) waiting[k] = 0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        // finished in the walk: not a pending child
+        need[b] = live[b] && !((__ldg(&predone[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
+        waiting[b / 4] += need[b] ? 1u : 0u;
+        need[b] = need[b] && id[b / 4] < nj;  // 1-saddles wait for no release: lengths come after the rounds
+    }
+    std::uint32_t slot[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) slot[b] = need[b] ? atomicAdd(&indeg[dd[b]], 1u) : 0u;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        if (!need[b]) continue;
+        const std::uint32_t t = dd[b];
+        const std::uint32_t parent = static_cast<std::uint32_t>(id[b / 4]);
+        if (slot[b] < static_cast<std::uint32_t>(kInlineParents)) {
+            node[t].par[slot[b]] = parent;
         } else {
-            uint4 d4 = *dp;
-            std::uint32_t dd[4] = {d4.x, d4.y, d4.z, d4.w};
-            std::uint32_t waiting = 0;  // junction children Kahn still has to finish
-            bool moved = false;
-            // each dependent step for all four branches at once (pass-through bits, then
-            // forwards, then predone bits, then the slot atomics back to back): the
-            // chain of loads and returning atomics was the kernel's latency
-            bool live[4], pt[4], need[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                live[b] = !(dd[b] & kTerm);
-                pt[b] = live[b] && ((__ldg(&ptbits[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
-            }
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (pt[b]) {
-                    dd[b] = __ldg(&fwd[dd[b]]);
-                    moved = true;
-                }
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                // finished in the walk: not a pending child
-                need[b] = live[b] && !((__ldg(&predone[dd[b] >> 5]) >> (dd[b] & 31)) & 1u);
-                waiting += need[b] ? 1u : 0u;
-                need[b] = need[b] && i < nj;  // 1-saddles wait for no release: lengths come after the rounds
-            }
-            std::uint32_t slot[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) slot[b] = need[b] ? atomicAdd(&indeg[dd[b]], 1u) : 0u;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                if (!need[b]) continue;
-                const std::uint32_t t = dd[b];
-                if (slot[b] < static_cast<std::uint32_t>(kInlineParents)) {
-                    node[t].par[slot[b]] = static_cast<std::uint32_t>(i);
-                } else {
-                    const unsigned long long q = atomicAdd(ovq_n, 1ull);
-                    if (q < ovq_cap) ovq[q] = make_uint4(t, slot[b], static_cast<std::uint32_t>(i), 0u);
-                }
-            }
-            if (pending[i] != kDone) {
-                pending[i] = waiting;
-                is_ready = i < nj && waiting == 0;
-            }
-            if (moved) *dp = make_uint4(dd[0], dd[1], dd[2], dd[3]);  // (most records are unchanged)
+            const unsigned long long q = atomicAdd(ovq_n, 1ull);
+            if (q < ovq_cap) ovq[q] = make_uint4(t, slot[b], parent, 0u);
         }
     }
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k) {
+        if (skip[k]) pending[id[k]] = kSkip;  // (its record is never read again)
+        if (!act[k]) continue;
+        if (pending[id[k]] != kDone) {
+            pending[id[k]] = waiting[k];
+            is_ready[k] = id[k] < nj && waiting[k] == 0;
+        }
+        if (moved[k])  // (most records are unchanged)
+            dest[id[k]] = make_uint4(dd[4 * k], dd[4 * k + 1], dd[4 * k + 2], dd[4 * k + 3]);
+    }
+    // Kahn's round 0 = the junctions without pending children, in index order within
+    // the block (one reservation per block)
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    const unsigned rb = __ballot_sync(0xffffffffu, is_ready);
-    const unsigned sb = __ballot_sync(0xffffffffu, skip);
-    if (lane == 0) {
-        s_wc[w] = __popc(rb);
-        if (sb) atomicAdd(n_skip, static_cast<unsigned long long>(__popc(sb)));
+    unsigned rb[kRwPer];
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k) {
+        rb[k] = __ballot_sync(0xffffffffu, is_ready[k]);
+        const unsigned sb = __ballot_sync(0xffffffffu, skip[k]);
+        if (lane == 0) {
+            s_wc[k][w] = __popc(rb[k]);
+            if (sb) atomicAdd(n_skip, static_cast<unsigned long long>(__popc(sb)));
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned tot = 0;
-        for (int k = 0; k < kThreads / 32; ++k) {
-            const unsigned c = s_wc[k];
-            s_wc[k] = tot;
-            tot += c;
-        }
+        for (int k = 0; k < kRwPer; ++k)
+            for (int q = 0; q < kThreads / 32; ++q) {
+                const unsigned c = s_wc[k][q];
+                s_wc[k][q] = tot;
+                tot += c;
+            }
         s_base = tot ? atomicAdd(n_ready, static_cast<unsigned long long>(tot)) : 0ull;
     }
     __syncthreads();
-    if (is_ready) ready[s_base + s_wc[w] + __popc(rb & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
+#pragma unroll
+    for (int k = 0; k < kRwPer; ++k)
+        if (is_ready[k])
+            ready[s_base + s_wc[k][w] + __popc(rb[k] & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(id[k]);
 }
 
 // Overflow-list segments of the nodes with more than kInlineParents parents (~0.1%):
@@ -1706,7 +1733,7 @@ int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nod
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;
-    k_rewrite<<<grid_full(n_nodes), kThreads, 0, s>>>(static_cast<NodeRec*>(node), static_cast<uint4*>(dest), nj, n_nodes, fwd, ptbits, predone,
+    k_rewrite<<<grid_full((n_nodes + kRwPer - 1) / kRwPer), kThreads, 0, s>>>(static_cast<NodeRec*>(node), static_cast<uint4*>(dest), nj, n_nodes, fwd, ptbits, predone,
                                                       pending, indeg, static_cast<uint4*>(ovq), ovq_n, ovq_cap, n_skip,
                                                       ready, n_ready);
     count_launch();
