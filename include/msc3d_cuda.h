@@ -87,6 +87,8 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
 /* Context options (not in the reference; defaults reproduce it exactly):
  *   "wide_ids" (0/1)          64-bit cell-id lists on any grid -- the layout grids with
  *                             >= 2^32 cells use (configs 4-5), testable on small grids;
+ *   "exact_batch_rows" (>=0)  1-saddles per batch of the exact A* overflow check
+ *                             (0 = as many as 2 GiB of dense rows hold);
  *   "kahn_switch_below" (>=1) frontier size at which path counting leaves its wide
  *                             launch configuration for the tail one (default 2^18).
  * Unknown names / bad values -> MSC3D_ERR_INVALID. */

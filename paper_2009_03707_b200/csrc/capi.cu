@@ -202,6 +202,9 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "kahn_switch_below") {
         if (value < 1) return MSC3D_ERR_INVALID;
         ctx->kahn_switch_below = static_cast<std::uint64_t>(value);
+    } else if (n == "exact_batch_rows") {  // rows per batch of the exact A* check (0 = by memory)
+        if (value < 0) return MSC3D_ERR_INVALID;
+        ctx->exact_batch_rows = static_cast<std::uint64_t>(value);
     } else {
         return MSC3D_ERR_INVALID;
     }

@@ -35,6 +35,7 @@ struct msc3d_ctx {
     // frontier size at which the counting kernel hands over to its tail configuration.
     bool force_wide = false;
     std::uint64_t kahn_switch_below = 1ull << 18;
+    std::uint64_t exact_batch_rows = 0;  // "exact_batch_rows": batch of the exact A* overflow check
     const void* values = nullptr;  // device pointer (owned "values" array or bound)
     std::map<std::string, DevArray> arrays;
     std::map<std::string, std::int64_t> scalars;

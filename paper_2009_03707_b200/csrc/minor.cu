@@ -282,15 +282,17 @@ __global__ void k_forward_level(const std::uint32_t* __restrict__ rows, std::uin
     }
 }
 
-// Exact A* overflow check, one thread per 1-saddle, junctions in topological order.
-__global__ void k_forward_exact(std::uint64_t n1, std::uint64_t nj, const std::uint32_t* __restrict__ topo,
+// Exact A* overflow check, one thread per 1-saddle of rows [row0, row0 + n1) (a batch:
+// A holds n1 dense rows of nj counts), junctions in topological order.
+__global__ void k_forward_exact(std::uint64_t row0, std::uint64_t n1, std::uint64_t nj, const std::uint32_t* __restrict__ topo,
                                 std::uint64_t ntopo, const std::uint64_t* __restrict__ pred_off,
                                 const std::uint32_t* __restrict__ pred_src, const std::uint64_t* __restrict__ pred_mult,
                                 const std::uint64_t* __restrict__ s_off, const std::uint32_t* __restrict__ s_dst,
                                 const std::uint64_t* __restrict__ s_mult, std::uint64_t* __restrict__ A,
                                 unsigned int* __restrict__ flags) {
-    GRID_STRIDE(i, n1) {
-        std::uint64_t* a = A + i * nj;
+    GRID_STRIDE(r, n1) {
+        const std::uint64_t i = row0 + r;
+        std::uint64_t* a = A + r * nj;
         for (std::uint64_t j = 0; j < nj; ++j) a[j] = 0;
         for (std::uint64_t k = s_off[i]; k < s_off[i + 1]; ++k) {
             const std::uint32_t t = s_dst[k];
@@ -772,17 +774,25 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
         }
         TRY(ctx->fetch_small(63));
         if (seed_sat || static_cast<unsigned int>(ctx->h_small[62])) {
-            if (n1 * nj > (1ull << 28)) return MSC3D_ERR_NOMEM;
+            // dense rows of A* for batches of 1-saddles within a 2 GiB scratch (an overflow
+            // verdict for any size, not an allocation failure; slow, but it only runs when
+            // some forward total reached 2^64)
             TRY(upload(ctx, "cm_topo", topo));
-            auto* A = static_cast<std::uint64_t*>(ctx->ensure("cm_A", n1 * nj, 8));
+            std::uint64_t batch = std::max<std::uint64_t>(1, std::min<std::uint64_t>(n1, (1ull << 28) / std::max<std::uint64_t>(nj, 1)));
+            if (ctx->exact_batch_rows) batch = std::min(batch, ctx->exact_batch_rows);
+            auto* A = static_cast<std::uint64_t*>(ctx->ensure("cm_A", batch * std::max<std::uint64_t>(nj, 1), 8));
             if (!A) return MSC3D_ERR_NOMEM;
-            msc3d_dev::k_forward_exact<<<msc3d_dev::grid_for(n1, sms), msc3d_dev::kThreads, 0, s>>>(
-                n1, nj, ctx->ptr<std::uint32_t>("cm_topo"), topo.size(), ctx->ptr<std::uint64_t>("cm_poff"),
-                ctx->ptr<std::uint32_t>("cm_psrc"), ctx->ptr<std::uint64_t>("cm_pmul"), ctx->ptr<std::uint64_t>("cm_soff"),
-                ctx->ptr<std::uint32_t>("cm_sdst"), ctx->ptr<std::uint64_t>("cm_smul"), A, flags);
-            msc3d_dev::count_launch();
-            TRY(ctx->fetch_small(27));
-            if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
+            for (std::uint64_t r0 = 0; r0 < n1; r0 += batch) {
+                const std::uint64_t nb = std::min(batch, n1 - r0);
+                msc3d_dev::k_forward_exact<<<msc3d_dev::grid_for(nb, sms), msc3d_dev::kThreads, 0, s>>>(
+                    r0, nb, nj, ctx->ptr<std::uint32_t>("cm_topo"), topo.size(), ctx->ptr<std::uint64_t>("cm_poff"),
+                    ctx->ptr<std::uint32_t>("cm_psrc"), ctx->ptr<std::uint64_t>("cm_pmul"),
+                    ctx->ptr<std::uint64_t>("cm_soff"), ctx->ptr<std::uint32_t>("cm_sdst"),
+                    ctx->ptr<std::uint64_t>("cm_smul"), A, flags);
+                msc3d_dev::count_launch();
+                TRY(ctx->fetch_small(27));
+                if (ctx->h_small[26] & 0xffffffffu) return MSC3D_ERR_OVERFLOW;
+            }
         }
     }
     MSC3D_CUDA_TRY(cudaStreamSynchronize(s));

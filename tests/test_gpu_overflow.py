@@ -71,3 +71,59 @@ def test_vpath_chain_all_sources(ref, k, end, overflows):
         c.count()
         for got, w in zip(("ss_one", "ss_two", "ss_paths"), want):
             np.testing.assert_array_equal(c.get(got), w, err_msg=got)
+
+
+def _device_count_minor(ctx, mn):
+    """msc3d_ctx_count_minor (count_paths on a host DagMinor, path_matrix.cpp:188-219)."""
+    import ctypes as C
+    names = ("s1_to_j", "j_to_j", "j_to_s2", "s1_to_s2")
+    keep = []
+
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dtype=dt)
+        keep.append(a)
+        return a.ctypes.data_as(C.c_void_p)
+
+    srcs = (C.c_void_p * 4)(*[arr(mn[k][0], np.uint32) for k in names])
+    dsts = (C.c_void_p * 4)(*[arr(mn[k][1], np.uint32) for k in names])
+    mults = (C.c_void_p * 4)(*[arr(mn[k][2], np.uint64) for k in names])
+    counts = (C.c_uint64 * 4)(*[len(mn[k][0]) for k in names])
+    ones, juncs, twos = (arr(mn[k], np.uint32) for k in ("one_saddles", "junctions", "two_saddles"))
+    return ctx._L.msc3d_ctx_count_minor(ctx.h, ones, len(mn["one_saddles"]), juncs, len(mn["junctions"]), twos,
+                                        len(mn["two_saddles"]), srcs, dsts, mults, counts, 4)
+
+
+def _minor(n1, nj, n2, edges):
+    mn = {"one_saddles": np.arange(n1) * 2 + 1, "junctions": np.arange(nj) * 2 + 3,
+          "two_saddles": np.arange(n2) * 2 + 5}
+    for k in ("s1_to_j", "j_to_j", "j_to_s2", "s1_to_s2"):
+        e = edges.get(k, [])
+        mn[k] = (np.array([x[0] for x in e], np.uint32), np.array([x[1] for x in e], np.uint32),
+                 np.array([x[2] for x in e], np.uint64))
+    return mn
+
+
+@pytest.mark.parametrize("batch", [0, 1, 2, 3])
+@pytest.mark.parametrize("overflows", [False, True])
+def test_exact_dead_junction_check_batched(ref, batch, overflows):
+    """Four 1-saddles feed a dead junction chain: their forward total saturates at 2^64,
+    so the exact per-source check runs -- in batches of `batch` sources -- and decides
+    as the reference does: no overflow while each source's A* entry fits, overflow_error
+    when one reaches 2^64 (path_matrix.cpp:188-219, test_path_matrix.cpp:342-353)."""
+    big = 1 << 62
+    e = {"s1_to_j": [(s, 0, big) for s in range(4)], "j_to_j": [(0, 1, 2 if overflows else 1)],
+         "s1_to_s2": [(s, 0, 1) for s in range(4)]}
+    if overflows:
+        e["s1_to_j"][2] = (2, 0, 1 << 63)
+    mn = _minor(4, 2, 1, e)
+    try:
+        ref.count_paths(mn)
+        want_overflow = False
+    except CheckerError as err:
+        assert err.kind == "overflow_error"
+        want_overflow = True
+    assert want_overflow == overflows
+    with m.Context(0) as c:
+        c.set_option("exact_batch_rows", batch)
+        rc = _device_count_minor(c, mn)
+    assert rc == (m.ERR_OVERFLOW if overflows else m.OK)
