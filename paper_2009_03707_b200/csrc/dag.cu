@@ -1425,6 +1425,10 @@ __global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) 
         flush_block(s_q, nxt, next_cnt);
         grid.sync();
         const unsigned long long nh = *reinterpret_cast<volatile unsigned long long*>(&a.heavy_n[r % 3]);
+        if (a.diag && grid.thread_rank() == 0 && r < kTimeline) {  // development timeline
+            a.diag[7 + 3 * r] = nh;
+            a.diag[8 + 3 * r] = gtimer();
+        }
         if (nh) {
             heavy_pass(a, wb, wq, ch, nxt, next_cnt, done, nh, &a.heavy_head[r % 3]);
             flush_block(s_q, nxt, next_cnt);
