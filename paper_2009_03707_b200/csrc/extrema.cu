@@ -81,6 +81,95 @@ __global__ void k_double(const std::uint32_t* __restrict__ in, std::uint32_t* __
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *changed = 1u;
 }
 
+// Tile-local pre-resolution of a forest whose parents are lattice neighbours (both
+// extremum forests: a vertex's parent is the other end of its paired edge, a cube's the
+// cube across its paired quad).  One block per kTRx x kTRy x kTRz box of the forest's
+// grid: the parents are read into shared memory as box-local links (root, neighbour
+// inside the box, or exit = a neighbour outside it), resolved there by pointer doubling
+// (shared-memory latency, not L2), and every item is written back pointing at its root
+// or at the first item outside the box on its path.  The global jumping that follows
+// (k_jump_all) then chases box-to-box hops: on smooth fields, where descending chains
+// run for hundreds of cells, that is a factor ~16 fewer dependent random loads.
+constexpr int kTRx = 32, kTRy = 16, kTRz = 16, kTRn = kTRx * kTRy * kTRz;
+constexpr std::uint32_t kExit = 0x80000000u;  // link flag: the chain leaves the box
+
+__global__ void __launch_bounds__(1024)
+k_tile_roots(std::uint32_t* __restrict__ p, std::uint32_t gx, std::uint32_t gy, std::uint32_t gz,
+             unsigned int* __restrict__ skip, std::uint64_t kofs, unsigned int* __restrict__ cycle) {
+    // box-local link, or kExit | s: s is the box item whose parent leaves the box (its
+    // parent in p never changes below -- it is s's own answer -- so it is re-read there)
+    __shared__ std::uint32_t lk[kTRn];
+    const std::uint32_t bx = (gx + kTRx - 1) / kTRx, by = (gy + kTRy - 1) / kTRy;
+    const std::uint32_t tb = blockIdx.x;
+    const std::uint32_t ox = (tb % bx) * kTRx, oy = ((tb / bx) % by) * kTRy, oz = (tb / (bx * by)) * kTRz;
+    const std::uint64_t sy = gx, sz = static_cast<std::uint64_t>(gx) * gy;
+    // 1. links
+    for (int t = threadIdx.x; t < kTRn; t += blockDim.x) {
+        const int lx = t % kTRx, ly = (t / kTRx) % kTRy, lz = t / (kTRx * kTRy);
+        const std::uint32_t x = ox + lx, y = oy + ly, z = oz + lz;
+        if (x >= gx || y >= gy || z >= gz) {
+            lk[t] = static_cast<std::uint32_t>(t);  // padding: a root no one points at
+            continue;
+        }
+        const std::uint64_t i = x + sy * y + sz * z;
+        const std::uint32_t j = p[i];
+        const std::int64_t dlt = static_cast<std::int64_t>(j) - static_cast<std::int64_t>(i);
+        int nx = lx, ny = ly, nz = lz;
+        if (dlt == 1) ++nx;
+        else if (dlt == -1) --nx;
+        else if (dlt == static_cast<std::int64_t>(sy)) ++ny;
+        else if (dlt == -static_cast<std::int64_t>(sy)) --ny;
+        else if (dlt == static_cast<std::int64_t>(sz)) ++nz;
+        else if (dlt == -static_cast<std::int64_t>(sz)) --nz;
+        else if (dlt != 0) nx = -1;  // not a lattice neighbour (cannot happen): leave it to the global pass
+        const bool inside = nx >= 0 && nx < kTRx && ny >= 0 && ny < kTRy && nz >= 0 && nz < kTRz &&
+                            ox + nx < gx && oy + ny < gy && oz + nz < gz;
+        lk[t] = inside ? static_cast<std::uint32_t>(nx + kTRx * (ny + kTRy * nz)) : (kExit | static_cast<std::uint32_t>(t));
+        if (!inside && skip) {  // j is an exit target: one of the items the global pass must resolve
+            const std::uint64_t k = kofs + j;
+            atomicAnd(&skip[k >> 5], ~(1u << (k & 31)));
+        }
+    }
+    __syncthreads();
+    // 2. pointer doubling inside the box (in place: any ancestor is a valid link);
+    //    until nothing changes (chains in a box are at most kTRn long)
+    constexpr int kMaxRounds = 16;  // 2^14 > kTRn: a chain inside the box is resolved by then
+    int round = 0;
+    for (; round < kMaxRounds; ++round) {
+        bool ch = false;
+        for (int t = threadIdx.x; t < kTRn; t += blockDim.x) {
+            const std::uint32_t l = lk[t];
+            if (l & kExit) continue;
+            const std::uint32_t l2 = lk[l];
+            if (l2 != l) {
+                lk[t] = l2;
+                ch = true;
+            }
+        }
+        if (!__syncthreads_or(ch)) break;  // (also the round's barrier)
+    }
+    if (round == kMaxRounds && threadIdx.x == 0) *cycle = 1u;  // a closed path in the box: invalid gradient
+    // 3. back: the root's or the exit's global index
+    for (int t = threadIdx.x; t < kTRn; t += blockDim.x) {
+        const int lx = t % kTRx, ly = (t / kTRx) % kTRy, lz = t / (kTRx * kTRy);
+        const std::uint32_t x = ox + lx, y = oy + ly, z = oz + lz;
+        if (x >= gx || y >= gy || z >= gz) continue;
+        const std::uint32_t l = lk[t];
+        std::uint32_t g;
+        if (l & kExit) {
+            const std::uint32_t e = l & ~kExit;
+            const int ex_ = static_cast<int>(e % kTRx), ey_ = static_cast<int>((e / kTRx) % kTRy),
+                      ez_ = static_cast<int>(e / (kTRx * kTRy));
+            g = p[(ox + ex_) + sy * (oy + ey_) + sz * (oz + ez_)];
+        } else {
+            const int rx = static_cast<int>(l % kTRx), ry = static_cast<int>((l / kTRx) % kTRy),
+                      rz = static_cast<int>(l / (kTRx * kTRy));
+            g = static_cast<std::uint32_t>((ox + rx) + sy * (oy + ry) + sz * (oz + rz));
+        }
+        p[x + sy * y + sz * z] = g;
+    }
+}
+
 // Both forests' roots in one cooperative launch: rounds of in-place jumping over the
 // concatenated index space of parent0 and parent3, a grid barrier per round and a
 // rotating "changed" flag -- no host round trip per round.  conv: one bit per item,
@@ -90,7 +179,7 @@ __global__ void k_double(const std::uint32_t* __restrict__ in, std::uint32_t* __
 // caller; rounds_out[0] = rounds run.
 __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std::uint32_t* __restrict__ p3,
                            std::uint64_t n3, unsigned int* __restrict__ conv, unsigned int* flags,
-                           unsigned long long* rounds_out) {
+                           unsigned long long* rounds_out, int masked) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     const std::uint64_t n = n0 + n3;
@@ -103,7 +192,7 @@ __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std
         bool any = false;
         for (std::uint64_t base = wstart; base < n; base += stride) {
             const std::uint64_t k = base + lane;
-            const unsigned word = round ? conv[base >> 5] : 0u;
+            const unsigned word = (round || masked) ? conv[base >> 5] : 0u;
             bool now = false;
             if (k < n && !((word >> lane) & 1u)) {
                 std::uint32_t* p = k < n0 ? p0 : p3;
@@ -127,7 +216,7 @@ __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std
                 }
             }
             const unsigned bits = __ballot_sync(0xffffffffu, now);
-            if (lane == 0 && (bits || !round)) conv[base >> 5] = word | bits;
+            if (lane == 0 && (bits || (!round && !masked))) conv[base >> 5] = word | bits;
         }
         if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&flags[round % 3], 1u);
         grid.sync();
@@ -294,15 +383,48 @@ int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64
     return MSC3D_OK;
 }
 
+int launch_tile_roots(std::uint32_t* p, std::uint64_t gx, std::uint64_t gy, std::uint64_t gz, unsigned int* skip,
+                      std::uint64_t kofs, unsigned int* cycle, cudaStream_t s) {
+    if (gx == 0 || gy == 0 || gz == 0) return MSC3D_OK;
+    const std::uint64_t tiles = ((gx + kTRx - 1) / kTRx) * ((gy + kTRy - 1) / kTRy) * ((gz + kTRz - 1) / kTRz);
+    if (tiles > 0x7fffffffull) return MSC3D_ERR_INVALID;
+    k_tile_roots<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(p, static_cast<std::uint32_t>(gx),
+                                                               static_cast<std::uint32_t>(gy),
+                                                               static_cast<std::uint32_t>(gz), skip, kofs, cycle);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+// After the tile pass: every item points at its root or at an exit target, and the
+// exit targets (resolved by the masked global pass) point at their roots.
+__global__ void k_resolve_exits(std::uint32_t* __restrict__ p0, std::uint64_t n0, std::uint32_t* __restrict__ p3,
+                                std::uint64_t n3) {
+    GRID_STRIDE(k, n0 + n3) {
+        std::uint32_t* p = k < n0 ? p0 : p3;
+        const std::uint64_t i = k < n0 ? k : k - n0;
+        p[i] = p[p[i]];
+    }
+}
+
+int launch_resolve_exits(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, cudaStream_t s,
+                         int num_sms) {
+    if (n0 + n3 == 0) return MSC3D_OK;
+    k_resolve_exits<<<grid_for(n0 + n3, num_sms), kThreads, 0, s>>>(p0, n0, p3, n3);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
 int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* conv,
-                    unsigned int* flags, unsigned long long* rounds, cudaStream_t s, int num_sms) {
+                    unsigned int* flags, unsigned long long* rounds, cudaStream_t s, int num_sms, int masked) {
     if (n0 + n3 == 0) return MSC3D_OK;
     int per_sm = 0;
     MSC3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jump_all, kThreads, 0));
     if (per_sm <= 0) return MSC3D_ERR_CUDA;
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
         static_cast<std::uint64_t>(per_sm) * num_sms, std::max<std::uint64_t>(1, (n0 + n3 + kThreads - 1) / kThreads)));
-    void* args[] = {&p0, &n0, &p3, &n3, &conv, &flags, &rounds};
+    void* args[] = {&p0, &n0, &p3, &n3, &conv, &flags, &rounds, &masked};
     MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_jump_all), dim3(grid), dim3(kThreads),
                                                args, 0, s));
     count_launch();

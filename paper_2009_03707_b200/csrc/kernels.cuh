@@ -89,9 +89,18 @@ int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, 
                       int num_sms);
 // roots of both extremum forests in place, all rounds in one cooperative launch;
 // conv: (n0 + n3 + 31) / 32 words of scratch
+// Tile-local root pre-resolution of a lattice-neighbour forest over a gx*gy*gz grid
+// (every parent then points at its root or out of its box); then launch_jump_all.
+// skip (optional): the jump mask over the concatenated index space (item k = kofs + j),
+// in which every exit target's bit is cleared; launch_jump_all(..., masked = 1) then
+// resolves only those, launch_resolve_exits the rest.
+int launch_tile_roots(std::uint32_t* p, std::uint64_t gx, std::uint64_t gy, std::uint64_t gz, unsigned int* skip,
+                      std::uint64_t kofs, unsigned int* cycle, cudaStream_t s);
+int launch_resolve_exits(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, cudaStream_t s,
+                         int num_sms);
 int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* conv,
                     unsigned int* flags,
-                    unsigned long long* rounds, cudaStream_t s, int num_sms);
+                    unsigned long long* rounds, cudaStream_t s, int num_sms, int masked = 0);
 int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
                          std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms);
 // rank: nwords uint2 {rank of the word's first set bit, bits} over dense(crit[k]);

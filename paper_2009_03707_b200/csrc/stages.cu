@@ -660,9 +660,22 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         auto* conv = static_cast<unsigned int*>(
             ctx->ensure("jump_conv", (ctx->count("parent0") + ctx->count("parent3")) / 32 + 1, 4));
         if (!conv) return MSC3D_ERR_NOMEM;
-        TRY(msc3d_dev::launch_jump_all(ctx->ptr<std::uint32_t>("parent0"), ctx->count("parent0"),
-                                       ctx->ptr<std::uint32_t>("parent3"), ctx->count("parent3"), conv, flags, rounds,
-                                       s, sms));
+        std::uint32_t* q0 = ctx->ptr<std::uint32_t>("parent0");
+        std::uint32_t* q3 = ctx->ptr<std::uint32_t>("parent3");
+        const std::uint64_t n0 = ctx->count("parent0"), n3 = ctx->count("parent3");
+        // Long descending / ascending chains (big basins: few extrema per item, smooth
+        // fields) are first resolved inside 32x16x16 boxes; the global jumping then only
+        // chases the boxes' exit targets and one lookup finishes every other item.  With
+        // small basins (noisy fields) the chains rarely leave a box and plain jumping is
+        // cheaper than the extra passes.
+        const bool tiled = (c0 + c3) * 64 < n0 + n3 && !std::getenv("MSC3D_NO_TILE_ROOTS");
+        if (tiled) {
+            MSC3D_CUDA_TRY(cudaMemsetAsync(conv, 0xff, ((n0 + n3) / 32 + 1) * 4, s));
+            TRY(msc3d_dev::launch_tile_roots(q0, d.nx, d.ny, d.nz, conv, 0, flags + 3, s));
+            TRY(msc3d_dev::launch_tile_roots(q3, d.nx - 1, d.ny - 1, d.nz - 1, conv, n0, flags + 3, s));
+        }
+        TRY(msc3d_dev::launch_jump_all(q0, n0, q3, n3, conv, flags, rounds, s, sms, tiled ? 1 : 0));
+        if (tiled) TRY(msc3d_dev::launch_resolve_exits(q0, n0, q3, n3, s, sms));
     }
     auto* label0 = ctx->ptr<std::uint32_t>("parent0");
     auto* label3 = ctx->ptr<std::uint32_t>("parent3");
@@ -705,7 +718,8 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     // critical points, label volumes, min->1s and 2s->max arcs; their host copies
     // overlap the saddle stages
     TRY(ctx->fetch_small(34));
-    if (ctx->h_small[25] > 64) return MSC3D_ERR_RUNTIME;  // root finding did not converge: a cycle
+    // root finding did not converge (globally, or inside a box): a cycle
+    if (ctx->h_small[25] > 64 || (ctx->h_small[24] >> 32)) return MSC3D_ERR_RUNTIME;
     ctx->scalars["jump_rounds"] = static_cast<std::int64_t>(ctx->h_small[25]);
     const std::uint64_t na = c0 ? ctx->h_small[32] : 0;  // min->1s arcs
     const std::uint64_t nc = c2 ? ctx->h_small[33] : 0;  // 2s->max arcs
