@@ -192,27 +192,44 @@ k_succ_table(const std::uint8_t* __restrict__ codes, Dims d, const uint4* __rest
         for (int vx = threadIdx.x; vx < nx; vx += blockDim.x) {
             const int x = 2 * vx;
             const bool xm = vx > 0, xp = vx < nx - 1;
+            // all thirteen code bytes first (out-of-box neighbours read a valid in-row
+            // byte and are masked below): one memory latency per vertex instead of a
+            // chain of load -> table lookup -> next load
+            const int xl = xm ? x - 1 : x, xr = xp ? x + 1 : x;
+            const std::uint8_t* Rm0_ = ym ? Rm0 : R00;
+            const std::uint8_t* Rp0_ = yp ? Rp0 : R00;
+            const std::uint8_t* R0m_ = zm ? R0m : R00;
+            const std::uint8_t* R0p_ = zp ? R0p : R00;
+            const std::uint8_t* Rpm_ = (yp && zm) ? Rpm : R00;
+            const std::uint8_t* Rpp_ = (yp && zp) ? Rpp : R00;
+            const std::uint8_t* Rmp_ = (ym && zp) ? Rmp : R00;
+            const std::uint32_t e0 = __ldg(R00 + xr), q0a = __ldg(Rm0_ + xr), q0b = __ldg(Rp0_ + xr),
+                                q0c = __ldg(R0m_ + xr), q0d = __ldg(R0p_ + xr);
+            const std::uint32_t e1 = __ldg(Rp0_ + x), q1a = __ldg(Rp0_ + xl), q1b = __ldg(Rp0_ + xr),
+                                q1c = __ldg(Rpm_ + x), q1d = __ldg(Rpp_ + x);
+            const std::uint32_t e2 = __ldg(R0p_ + x), q2a = __ldg(R0p_ + xl), q2b = __ldg(R0p_ + xr),
+                                q2c = __ldg(Rmp_ + x), q2d = __ldg(Rpp_ + x);
             std::uint32_t w0 = 0, w1 = 0, w2 = 0;
             if (xp) {  // x-edge (x+1, 2vy, 2vz): quads -y, +y, -z, +z at x+1
-                w0 = (R00[x + 1] == kCritical ? kSuccCrit : 0u);
-                if (ym) w0 |= static_cast<std::uint32_t>(lut[(0 << 8) | Rm0[x + 1]]);
-                if (yp) w0 |= static_cast<std::uint32_t>(lut[(1 << 8) | Rp0[x + 1]]) << 3;
-                if (zm) w0 |= static_cast<std::uint32_t>(lut[(2 << 8) | R0m[x + 1]]) << 6;
-                if (zp) w0 |= static_cast<std::uint32_t>(lut[(3 << 8) | R0p[x + 1]]) << 9;
+                w0 = (e0 == kCritical ? kSuccCrit : 0u);
+                if (ym) w0 |= static_cast<std::uint32_t>(lut[(0 << 8) | q0a]);
+                if (yp) w0 |= static_cast<std::uint32_t>(lut[(1 << 8) | q0b]) << 3;
+                if (zm) w0 |= static_cast<std::uint32_t>(lut[(2 << 8) | q0c]) << 6;
+                if (zp) w0 |= static_cast<std::uint32_t>(lut[(3 << 8) | q0d]) << 9;
             }
             if (yp) {  // y-edge (x, 2vy+1, 2vz): quads -x, +x (same row), -z, +z
-                w1 = (Rp0[x] == kCritical ? kSuccCrit : 0u);
-                if (xm) w1 |= static_cast<std::uint32_t>(lut[(4 << 8) | Rp0[x - 1]]);
-                if (xp) w1 |= static_cast<std::uint32_t>(lut[(5 << 8) | Rp0[x + 1]]) << 3;
-                if (zm) w1 |= static_cast<std::uint32_t>(lut[(6 << 8) | Rpm[x]]) << 6;
-                if (zp) w1 |= static_cast<std::uint32_t>(lut[(7 << 8) | Rpp[x]]) << 9;
+                w1 = (e1 == kCritical ? kSuccCrit : 0u);
+                if (xm) w1 |= static_cast<std::uint32_t>(lut[(4 << 8) | q1a]);
+                if (xp) w1 |= static_cast<std::uint32_t>(lut[(5 << 8) | q1b]) << 3;
+                if (zm) w1 |= static_cast<std::uint32_t>(lut[(6 << 8) | q1c]) << 6;
+                if (zp) w1 |= static_cast<std::uint32_t>(lut[(7 << 8) | q1d]) << 9;
             }
             if (zp) {  // z-edge (x, 2vy, 2vz+1): quads -x, +x (same row), -y, +y
-                w2 = (R0p[x] == kCritical ? kSuccCrit : 0u);
-                if (xm) w2 |= static_cast<std::uint32_t>(lut[(8 << 8) | R0p[x - 1]]);
-                if (xp) w2 |= static_cast<std::uint32_t>(lut[(9 << 8) | R0p[x + 1]]) << 3;
-                if (ym) w2 |= static_cast<std::uint32_t>(lut[(10 << 8) | Rmp[x]]) << 6;
-                if (yp) w2 |= static_cast<std::uint32_t>(lut[(11 << 8) | Rpp[x]]) << 9;
+                w2 = (e2 == kCritical ? kSuccCrit : 0u);
+                if (xm) w2 |= static_cast<std::uint32_t>(lut[(8 << 8) | q2a]);
+                if (xp) w2 |= static_cast<std::uint32_t>(lut[(9 << 8) | q2b]) << 3;
+                if (ym) w2 |= static_cast<std::uint32_t>(lut[(10 << 8) | q2c]) << 6;
+                if (yp) w2 |= static_cast<std::uint32_t>(lut[(11 << 8) | q2d]) << 9;
             }
             out[3 * vx] = static_cast<std::uint16_t>(w0);
             out[3 * vx + 1] = static_cast<std::uint16_t>(w1);
