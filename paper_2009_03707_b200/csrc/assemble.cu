@@ -114,6 +114,27 @@ __global__ void k_sort_small_buckets(const std::uint64_t* __restrict__ off, std:
             large[atomicAdd(n_large, 1ull)] = static_cast<std::uint32_t>(m);
             continue;
         }
+        if (n <= 8) {  // (most buckets) in registers: all loads first, an 8-input network
+            std::uint64_t v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = static_cast<std::uint64_t>(q) < n ? key[b + q] : ~0ull;
+            auto ce = [](std::uint64_t& x, std::uint64_t& y) {
+                const std::uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+                x = lo;
+                y = hi;
+            };
+            // Batcher odd-even merge sort, 19 comparators
+            ce(v[0], v[1]); ce(v[2], v[3]); ce(v[4], v[5]); ce(v[6], v[7]);
+            ce(v[0], v[2]); ce(v[1], v[3]); ce(v[4], v[6]); ce(v[5], v[7]);
+            ce(v[1], v[2]); ce(v[5], v[6]);
+            ce(v[0], v[4]); ce(v[1], v[5]); ce(v[2], v[6]); ce(v[3], v[7]);
+            ce(v[2], v[4]); ce(v[3], v[5]);
+            ce(v[1], v[2]); ce(v[3], v[4]); ce(v[5], v[6]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (static_cast<std::uint64_t>(q) < n) key[b + q] = v[q];
+            continue;
+        }
         for (std::uint64_t i = b + 1; i < e; ++i) {
             const std::uint64_t v = key[i];
             std::uint64_t j = i;

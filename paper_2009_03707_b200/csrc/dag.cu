@@ -432,13 +432,22 @@ __global__ void k_junction_bits(const std::uint16_t* __restrict__ succ, const un
     unsigned long long mine = 0;
     for (std::uint64_t w = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
          w += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        unsigned int bits = bitmap[w], jb = 0;
+        const unsigned int bits = bitmap[w];
+        unsigned int jb = 0;
         mine += __popc(bits);
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const std::uint32_t s = succ[32 * w + b];
-            if (!(s & kSuccCrit) && n_succ(s) > 1) jb |= 1u << b;
+        if (bits) {  // the word's 32 successor words as four 16-byte loads, all in flight together
+            const uint4* sp = reinterpret_cast<const uint4*>(succ + 32 * w);
+            const uint4 q[4] = {__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3)};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const std::uint32_t h[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const std::uint32_t s = (h[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                    if (!(s & kSuccCrit) && n_succ(s) > 1) jb |= 1u << (8 * c + e);
+                }
+            }
+            jb &= bits;
         }
         jbits[w] = jb;
         jcnt[w] = __popc(jb);

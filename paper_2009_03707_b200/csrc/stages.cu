@@ -151,7 +151,8 @@ std::vector<T> sorted_unique(const T* p, std::uint64_t n) {
 // Successor table of the current codes (dag.cu): 2 bytes per dense edge.
 int succ_table(msc3d_ctx* ctx) {
     const Dims& d = ctx->dims;
-    auto* succ = static_cast<std::uint16_t*>(ctx->ensure("succ", 3 * d.n_verts, 2));
+    // (+32: junction_bits reads whole 32-word groups)
+    auto* succ = static_cast<std::uint16_t*>(ctx->ensure("succ", 3 * d.n_verts + 32, 2));
     if (!succ) return MSC3D_ERR_NOMEM;
     return msc3d_dev::launch_succ_table(ctx->ptr<std::uint8_t>("codes"), d, succ, ctx->stream, ctx->num_sms);
 }
