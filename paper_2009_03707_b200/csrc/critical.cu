@@ -229,6 +229,26 @@ k_compact_crit(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, Id
 
 // Per-dimension masks of the critical cells among the 64 cells [first, first + 64)
 // (bit k = cell first + k): byte compares to bits, then lattice parity masks.
+// Critical-code bits of 64 consecutive cells, from four 16-byte words.
+__device__ __forceinline__ std::uint64_t crit_bits(const uint4 (&w4)[kChunks]) {
+    std::uint64_t crit = 0;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        const std::uint32_t ws[4] = {w4[q].x, w4[q].y, w4[q].z, w4[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const std::uint32_t m = __vcmpeq4(ws[e], 0x01010101u);  // kCritical bytes -> 0xff
+            const std::uint64_t b4 = ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+            crit |= b4 << (16 * q + 4 * e);
+        }
+    }
+    return crit;
+}
+
+// Per-dimension masks of the 64 cells starting at `first` from their critical bits.
+__device__ __forceinline__ void crit_dim_masks(std::uint64_t crit, const Dims& d, std::uint64_t first,
+                                               std::uint64_t M[4]);
+
 __device__ __forceinline__ void crit_chunk_masks(const std::uint8_t* __restrict__ codes, const Dims& d,
                                                  std::uint64_t first, std::uint64_t M[4]) {
     std::uint64_t crit = 0;
@@ -248,6 +268,11 @@ __device__ __forceinline__ void crit_chunk_masks(const std::uint8_t* __restrict_
         for (int k = 0; k < kPerThread; ++k)
             if (first + k < d.n_cells && codes[first + k] == kCritical) crit |= 1ull << k;
     }
+    crit_dim_masks(crit, d, first, M);
+}
+
+__device__ __forceinline__ void crit_dim_masks(std::uint64_t crit, const Dims& d, std::uint64_t first,
+                                               std::uint64_t M[4]) {
     const Coord p = unpack(d, first < d.n_cells ? first : 0);
     const std::uint64_t lenA = min(static_cast<std::uint64_t>(kPerThread), static_cast<std::uint64_t>(d.ex - p.x));
     const std::uint64_t segA = lenA >= 64 ? ~0ull : ((1ull << lenA) - 1);
@@ -318,14 +343,26 @@ k_compact_crit3(const std::uint8_t* __restrict__ codes, Dims d, TileStatus st, I
     const std::uint32_t tile = s_tile;
     std::uint64_t M[kSub][4];
     std::uint64_t packed = 0;
+    const std::uint64_t first0 = static_cast<std::uint64_t>(tile) * kSub * kTile +
+                                 static_cast<std::uint64_t>(threadIdx.x) * kSub * kPerThread;
+    if (static_cast<std::uint64_t>(tile + 1) * kSub * kTile <= d.n_cells) {
+        // a full tile: the thread's twelve 16-byte loads issued back to back, then the masks
+        uint4 w4[kSub][kChunks];
+        const uint4* src = reinterpret_cast<const uint4*>(codes + first0);
 #pragma unroll
-    for (int sb = 0; sb < kSub; ++sb) {
-        const std::uint64_t first = static_cast<std::uint64_t>(tile) * kSub * kTile +
-                                    (static_cast<std::uint64_t>(threadIdx.x) * kSub + sb) * kPerThread;
-        crit_chunk_masks(codes, d, first, M[sb]);
+        for (int sb = 0; sb < kSub; ++sb)
+#pragma unroll
+            for (int q = 0; q < kChunks; ++q) w4[sb][q] = __ldcs(src + sb * kChunks + q);
+#pragma unroll
+        for (int sb = 0; sb < kSub; ++sb) crit_dim_masks(crit_bits(w4[sb]), d, first0 + sb * kPerThread, M[sb]);
+    } else {
+#pragma unroll
+        for (int sb = 0; sb < kSub; ++sb) crit_chunk_masks(codes, d, first0 + sb * kPerThread, M[sb]);
+    }
+#pragma unroll
+    for (int sb = 0; sb < kSub; ++sb)
 #pragma unroll
         for (int dm = 0; dm < 4; ++dm) packed += static_cast<std::uint64_t>(__popcll(M[sb][dm])) << (16 * dm);
-    }
     std::uint64_t block_total;
     const std::uint64_t excl = block_excl_scan(packed, &block_total, sm);
     std::uint64_t tot[4];
