@@ -90,10 +90,17 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
  *   "exact_batch_rows" (>=0)  1-saddles per batch of the exact A* overflow check
  *                             (0 = as many as 2 GiB of dense rows hold);
  *   "kahn_switch_below" (>=1) frontier size at which path counting leaves its wide
- *                             launch configuration for the tail one (default 2^18).
+ *                             launch configuration for the tail one (default 2^18);
+ *   "frontier_cap" (>=0)      initial entries of the BFS frontier buffers (0 = 4 x the
+ *                             sources; a level that does not fit reruns the BFS with
+ *                             buffers of every dense edge);
+ *   "term_rank_words" (0/1)   the walks' 2-saddle rank lookup grids above 2^28 vertices
+ *                             use (rank words in cell order), on any grid.
  * Unknown names / bad values -> MSC3D_ERR_INVALID. */
 int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, int64_t value);
-/* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...). */
+/* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...); also
+ * "device_bytes_held" / "device_bytes_peak": device memory of the context's arrays now /
+ * at its high-water mark. */
 int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, int64_t* value);
 
 /* ---- scalar-grid load: ScalarField / read_volume (grid.hpp:117-125, volume.hpp:42) -- */

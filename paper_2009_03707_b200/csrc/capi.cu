@@ -205,6 +205,11 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "exact_batch_rows") {  // rows per batch of the exact A* check (0 = by memory)
         if (value < 0) return MSC3D_ERR_INVALID;
         ctx->exact_batch_rows = static_cast<std::uint64_t>(value);
+    } else if (n == "frontier_cap") {  // initial BFS frontier entries (0 = 4 x sources)
+        if (value < 0) return MSC3D_ERR_INVALID;
+        ctx->frontier_cap = static_cast<std::uint64_t>(value);
+    } else if (n == "term_rank_words") {  // the large-grid 2-saddle rank lookup on any grid
+        ctx->term_rank_words = value != 0;
     } else {
         return MSC3D_ERR_INVALID;
     }
@@ -212,6 +217,15 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
 }
 
 int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, std::int64_t* value) {
+    if (!ctx || !name || !value) return MSC3D_ERR_INVALID;
+    if (!std::strcmp(name, "device_bytes_held")) {
+        *value = static_cast<std::int64_t>(ctx->held_bytes());
+        return MSC3D_OK;
+    }
+    if (!std::strcmp(name, "device_bytes_peak")) {
+        *value = static_cast<std::int64_t>(ctx->peak_held);
+        return MSC3D_OK;
+    }
     auto it = ctx->scalars.find(name);
     if (it == ctx->scalars.end()) return MSC3D_ERR_STATE;
     *value = it->second;
@@ -451,8 +465,10 @@ int msc3d_ctx_compute_codes(msc3d_ctx* ctx, int options, std::uint32_t shard, st
         const int rc = msc3d_stage::validate(ctx);
         if (rc != MSC3D_OK) return rc;
     }
-    return msc3d_stage::compute_from_codes(ctx, options, stage_ms, nullptr, false, shard, n_shards, nullptr,
-                                           /*sharded=*/true);
+    const int rc = msc3d_stage::compute_from_codes(ctx, options, stage_ms, nullptr, false, shard, n_shards, nullptr,
+                                                   /*sharded=*/true);
+    if (std::getenv("MSC3D_ALLOC_TRACE")) ctx->dump_arrays("after compute_codes");
+    return rc;
 }
 
 int msc3d_ctx_compute_host_values(msc3d_ctx* ctx, msc3d_dims dims, int value_type, const void* host_values,

@@ -36,6 +36,8 @@ struct msc3d_ctx {
     bool force_wide = false;
     std::uint64_t kahn_switch_below = 1ull << 18;
     std::uint64_t exact_batch_rows = 0;  // "exact_batch_rows": batch of the exact A* overflow check
+    std::uint64_t frontier_cap = 0;      // "frontier_cap": initial BFS frontier entries (0 = 4 x sources)
+    bool term_rank_words = false;        // "term_rank_words": 2-saddle rank words on any grid
     const void* values = nullptr;  // device pointer (owned "values" array or bound)
     std::map<std::string, DevArray> arrays;
     std::map<std::string, std::int64_t> scalars;
@@ -80,21 +82,31 @@ struct msc3d_ctx {
                 cudaGetLastError();
                 a.ptr = nullptr;
                 if (std::getenv("MSC3D_ALLOC_TRACE")) {  // development: what holds the device memory
-                    std::size_t held = 0;
-                    for (const auto& kv : arrays) held += kv.second.cap;
-                    std::fprintf(stderr, "msc3d: cannot allocate %s (%.2f GB); the context holds %.2f GB:\n",
-                                 name.c_str(), want / 1e9, held / 1e9);
-                    for (const auto& kv : arrays)
-                        if (kv.second.cap > (std::size_t(1) << 28))
-                            std::fprintf(stderr, "  %-20s %8.2f GB\n", kv.first.c_str(), kv.second.cap / 1e9);
+                    std::fprintf(stderr, "msc3d: cannot allocate %s (%.2f GB)\n", name.c_str(), want / 1e9);
+                    dump_arrays("at the failure");
                 }
                 return nullptr;
             }
             a.cap = want;
+            const std::size_t held = held_bytes();
+            if (held > peak_held) peak_held = held;
         }
         a.count = count;
         a.elem = elem;
         return a.ptr;
+    }
+    std::size_t peak_held = 0;  // high-water mark of the named arrays (bytes)
+    std::size_t held_bytes() const {
+        std::size_t held = 0;
+        for (const auto& kv : arrays) held += kv.second.cap;
+        return held;
+    }
+    // development (MSC3D_ALLOC_TRACE): the arrays above 256 MB that hold device memory
+    void dump_arrays(const char* when) const {
+        std::fprintf(stderr, "msc3d: the context holds %.2f GB %s:\n", held_bytes() / 1e9, when);
+        for (const auto& kv : arrays)
+            if (kv.second.cap > (std::size_t(1) << 28))
+                std::fprintf(stderr, "  %-20s %8.2f GB\n", kv.first.c_str(), kv.second.cap / 1e9);
     }
     DevArray* find(const std::string& name) {
         auto it = arrays.find(name);

@@ -269,13 +269,17 @@ struct WarpQ {
     std::uint32_t n;
 };
 
-__device__ __forceinline__ void flush_warp(WarpQ& q, std::uint32_t* out, unsigned long long* ctr) {
+// `cap`: entries the output buffer holds; appends past it are dropped (the caller
+// sees the counter exceed cap and retries with a larger buffer).
+__device__ __forceinline__ void flush_warp(WarpQ& q, std::uint32_t* out, unsigned long long* ctr,
+                                           unsigned long long cap = ~0ull) {
     const int lane = threadIdx.x & 31;
     const std::uint32_t n = q.n;
     unsigned long long base = 0;
     if (lane == 0 && n) base = atomicAdd(ctr, static_cast<unsigned long long>(n));
     base = __shfl_sync(0xffffffffu, base, 0);
-    for (std::uint32_t k = lane; k < n; k += 32) out[base + k] = q.item[k];
+    for (std::uint32_t k = lane; k < n; k += 32)
+        if (base + k < cap) out[base + k] = q.item[k];
     __syncwarp();
     if (lane == 0) q.n = 0;
     __syncwarp();
@@ -283,7 +287,7 @@ __device__ __forceinline__ void flush_warp(WarpQ& q, std::uint32_t* out, unsigne
 
 // All lanes call; lane pushes the items[k] with bit k of `mask` set (k < 4).
 __device__ __forceinline__ void warp_push(WarpQ& q, const std::uint32_t* items, unsigned mask, std::uint32_t* out,
-                                          unsigned long long* ctr) {
+                                          unsigned long long* ctr, unsigned long long cap = ~0ull) {
     const int lane = threadIdx.x & 31;
     const unsigned mine = __popc(mask);
     unsigned incl = mine;
@@ -294,7 +298,7 @@ __device__ __forceinline__ void warp_push(WarpQ& q, const std::uint32_t* items, 
     }
     const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     if (total == 0) return;
-    if (q.n + total > kQCap) flush_warp(q, out, ctr);
+    if (q.n + total > kQCap) flush_warp(q, out, ctr, cap);
     std::uint32_t at = q.n + incl - mine;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -306,7 +310,8 @@ __device__ __forceinline__ void warp_push(WarpQ& q, const std::uint32_t* items, 
 
 // All threads of the block call (before the grid barrier): one reservation for
 // every warp queue of the block.
-__device__ __forceinline__ void flush_block(WarpQ* qs, std::uint32_t* out, unsigned long long* ctr) {
+__device__ __forceinline__ void flush_block(WarpQ* qs, std::uint32_t* out, unsigned long long* ctr,
+                                            unsigned long long cap = ~0ull) {
     __shared__ unsigned long long s_base[kThreads / 32 + 1];
     __syncthreads();
     const int nw = blockDim.x / 32;
@@ -322,7 +327,8 @@ __device__ __forceinline__ void flush_block(WarpQ* qs, std::uint32_t* out, unsig
     __syncthreads();
     WarpQ& q = qs[threadIdx.x >> 5];
     const unsigned long long base = s_base[threadIdx.x >> 5];
-    for (std::uint32_t k = threadIdx.x & 31; k < q.n; k += 32) out[base + k] = q.item[k];
+    for (std::uint32_t k = threadIdx.x & 31; k < q.n; k += 32)
+        if (base + k < cap) out[base + k] = q.item[k];
     __syncthreads();
     if ((threadIdx.x & 31) == 0) q.n = 0;
     __syncthreads();
@@ -331,10 +337,10 @@ __device__ __forceinline__ void flush_block(WarpQ* qs, std::uint32_t* out, unsig
 // cnt[0] = number of (already claimed) seeds in fa; cnt[1], cnt[2] scratch.
 // stats[0] = rounds, stats[1] = nodes claimed here.  Level-synchronous: one
 // round per BFS level, 32 nodes per warp iteration, one reservation per iteration.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 6)
 k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restrict__ bitmap,
         std::uint32_t* __restrict__ fa, std::uint32_t* __restrict__ fb, unsigned long long* __restrict__ cnt,
-        unsigned long long* __restrict__ stats) {
+        unsigned long long* __restrict__ stats, unsigned long long cap) {
     __shared__ WarpQ s_q[kThreads / 32];
     __shared__ StepTables s_tab;
     fill_step_tables(s_tab, g);
@@ -375,10 +381,11 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
                     if (!((old[p] >> (de[p] & 31)) & 1u)) won |= 1u << p;
             }
             mine += __popc(won);
-            warp_push(wq, de, won, nxt, next_cnt);
+            warp_push(wq, de, won, nxt, next_cnt, cap);
         }
-        flush_block(s_q, nxt, next_cnt);
+        flush_block(s_q, nxt, next_cnt, cap);
     };
+    bool overflow = false;  // a level larger than the frontier buffers (uniform: all read ncur)
     // Levels with big frontiers: the whole grid, a grid barrier per level.  Once the
     // frontier is small, block 0 finishes alone with block barriers (a level then costs
     // a few microseconds instead of a grid barrier's round trip); the other blocks exit
@@ -394,11 +401,15 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
         grid.sync();
         ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
         ++round;
+        if (ncur > cap) {
+            overflow = true;
+            break;
+        }
         std::uint32_t* t = cur;
         cur = nxt;
         nxt = t;
     }
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && !overflow) {
         while (ncur) {
             unsigned long long* next_cnt = &cnt[(round + 1) % 3];
             if (threadIdx.x == 0) {
@@ -410,6 +421,10 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
             ncur = *reinterpret_cast<volatile unsigned long long*>(next_cnt);
             __syncthreads();
             ++round;
+            if (ncur > cap) {
+                overflow = true;
+                break;
+            }
             std::uint32_t* t = cur;
             cur = nxt;
             nxt = t;
@@ -421,6 +436,7 @@ k_reach(const std::uint16_t* __restrict__ succ, EGrid g, unsigned int* __restric
         stats[0] = static_cast<unsigned long long>(round);
         if (round < kTimeline) stats[2 + round] = gtimer();
     }
+    if (overflow && threadIdx.x == 0) stats[0] = ~0ull;  // (block 0 decides in the solo phase)
 }
 
 // ---------------------------------------------------------------------------------
@@ -486,8 +502,27 @@ struct WalkCtx {
     const std::uint16_t* succ;
     EGrid g;
     const uint2* jrank;
-    const std::uint32_t* tmap;
+    const std::uint32_t* tmap;  // 2-saddle rank per dense quad index, or null: trank
+    const uint2* trank;         // 2-saddle rank words (term_rank)
     std::uint64_t limit;
+    FastDiv fnx, fny;
+    std::uint32_t nx, ny;
+    std::uint64_t ex, exy;
+    // Rank of the 2-saddle quad with dense index dq = 3 * (lower vertex) + normal axis
+    // in the sorted 2-saddle list: its lattice cell id, then the per-32-cells rank word
+    // (first rank of the word's 2-saddles, their bits) -- N/4 bytes instead of a u32
+    // map over all 3V quads (12 bytes per vertex: 12.9 GB at 2^30 vertices).  The
+    // map is used where it is small (one load per lookup instead of two divisions).
+    __device__ __forceinline__ std::uint32_t term_rank(std::uint32_t dq) const {
+        if (tmap) return __ldg(&tmap[dq]);
+        const std::uint32_t v = __umulhi(dq, 0xAAAAAAABu) >> 1;
+        const std::uint32_t a = dq - 3u * v;
+        const std::uint32_t t = static_cast<std::uint32_t>(fnx.div(v)), vx = v - t * nx;
+        const std::uint32_t vz = static_cast<std::uint32_t>(fny.div(t)), vy = t - vz * ny;
+        const std::uint64_t cell = (2ull * vx + (a != 0)) + ex * (2ull * vy + (a != 1)) + exy * (2ull * vz + (a != 2));
+        const uint2 r = __ldg(&trank[cell >> 5]);
+        return r.x + __popc(r.y & ((1u << (cell & 31)) - 1u));
+    }
 };
 
 // Walk from edge cur (axis a) to the branch's end.
@@ -501,13 +536,27 @@ __device__ __forceinline__ std::uint32_t walk_branch(const WalkCtx& c, const Ste
         const int p = (__ffs(present) - 1) / 3;
         const std::uint32_t f = (s >> (3 * p)) & 7u;
         const int ap = a * 4 + p;
-        if (f == 1) return kTerm | c.tmap[cur + t.tq[ap]];
+        if (f == 1) return kTerm | c.term_rank(cur + t.tq[ap]);
         cur += t.step[ap * 3 + static_cast<int>(f) - 2];
         a = f == 2 ? a : t.nax[ap];
         if (steps > c.limit) {
             *cycle = 1u;  // invalid gradient (saddle_graph.cpp:173-174)
             return kNone;
         }
+    }
+}
+
+// The 2-saddle rank words (WalkCtx::term_rank) from the sorted 2-saddle list: bit of
+// each 2-saddle's cell id; the first list entry of a word writes the word's base rank
+// (the list is sorted, so that is its own index).  Words without 2-saddles are never read.
+template <typename IdT>
+__global__ void k_term_rank(const IdT* __restrict__ list, std::uint64_t n, uint2* __restrict__ trank) {
+    for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t c = static_cast<std::uint64_t>(list[k]);
+        if (k == 0 || (static_cast<std::uint64_t>(list[k - 1]) >> 5) != (c >> 5))
+            trank[c >> 5].x = static_cast<std::uint32_t>(k);
+        atomicOr(&trank[c >> 5].y, 1u << (c & 31));
     }
 }
 
@@ -566,7 +615,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                 const std::uint32_t f = (s0 >> (3 * p)) & 7u;
                 if (f == 0) continue;
                 const int ap = a0 * 4 + p;
-                const std::uint32_t t = f == 1 ? (kTerm | c.tmap[de0 + s_tab.tq[ap]])
+                const std::uint32_t t = f == 1 ? (kTerm | c.term_rank(de0 + s_tab.tq[ap]))
                                                : walk_branch(c, s_tab, de0 + s_tab.step[ap * 3 + static_cast<int>(f) - 2],
                                                              f == 2 ? a0 : s_tab.nax[ap], &flags[2]);
                 dd[0] = nd == 0 ? t : dd[0];
@@ -1703,13 +1752,13 @@ int coop_blocks(const void* fn, int num_sms, int* grid, std::size_t smem = 0) {
 }
 
 int launch_reach(const std::uint16_t* succ, const Dims& d, unsigned int* bitmap, std::uint32_t* fa,
-                 std::uint32_t* fb, unsigned long long* cnt, unsigned long long* stats, cudaStream_t s,
-                 int num_sms) {
+                 std::uint32_t* fb, unsigned long long cap, unsigned long long* cnt, unsigned long long* stats,
+                 cudaStream_t s, int num_sms) {
     int grid = 0;
     const int rc = coop_blocks(reinterpret_cast<const void*>(k_reach), num_sms, &grid);
     if (rc != MSC3D_OK) return rc;
     EGrid g = egrid(d);
-    void* args[] = {&succ, &g, &bitmap, &fa, &fb, &cnt, &stats};
+    void* args[] = {&succ, &g, &bitmap, &fa, &fb, &cnt, &stats, &cap};
     MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_reach), dim3(grid), dim3(kThreads),
                                                args, 0, s));
     count_launch();
@@ -1736,12 +1785,14 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 }
 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
-                const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
+                const std::uint32_t* tmap, const void* trank, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
                 unsigned int* ptbits, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
-    WalkCtx c{succ, egrid(d), static_cast<const uint2*>(jrank), tmap, d.n_cells};
+    WalkCtx c{succ, egrid(d), static_cast<const uint2*>(jrank), tmap, static_cast<const uint2*>(trank), d.n_cells,
+              d.fnx, d.fny, static_cast<std::uint32_t>(d.nx), static_cast<std::uint32_t>(d.ny), static_cast<std::uint64_t>(d.ex),
+              static_cast<std::uint64_t>(d.exy)};
     auto* nr = static_cast<uint4*>(node);  // the nodes' destination records
     auto* r4 = static_cast<uint4*>(rec);
     if (id_width == 4)
@@ -1750,6 +1801,20 @@ int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
     else
         k_walk<std::uint64_t><<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(
             c, d, jlist, static_cast<const std::uint64_t*>(srcs), n, nr, pending, flags, r4, slen, predone, n_predone, fwd, ptbits);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_term_rank(const void* list, std::uint64_t n, int id_width, std::uint64_t n_cells, void* trank,
+                     cudaStream_t s, int num_sms) {
+    MSC3D_CUDA_TRY(cudaMemsetAsync(trank, 0, (n_cells / 32 + 1) * 8, s));
+    if (n == 0) return MSC3D_OK;
+    auto* tr = static_cast<uint2*>(trank);
+    if (id_width == 4)
+        k_term_rank<<<grid_for(n, num_sms), kThreads, 0, s>>>(static_cast<const std::uint32_t*>(list), n, tr);
+    else
+        k_term_rank<<<grid_for(n, num_sms), kThreads, 0, s>>>(static_cast<const std::uint64_t*>(list), n, tr);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

@@ -201,8 +201,8 @@ int count_rec_bytes();
 int count_arenas();
 int launch_succ_table(const std::uint8_t* codes, const Dims& d, std::uint16_t* succ, cudaStream_t s, int num_sms);
 int launch_reach(const std::uint16_t* succ, const Dims& d, unsigned int* bitmap, std::uint32_t* fa,
-                 std::uint32_t* fb, unsigned long long* cnt, unsigned long long* stats, cudaStream_t s,
-                 int num_sms);
+                 std::uint32_t* fb, unsigned long long cap, unsigned long long* cnt, unsigned long long* stats,
+                 cudaStream_t s, int num_sms);
 int launch_junction_bits(const std::uint16_t* succ, const unsigned int* bitmap, std::uint64_t nwords,
                          unsigned int* jbits, std::uint32_t* jcnt, unsigned long long* nodes, cudaStream_t s,
                          int num_sms);
@@ -211,8 +211,11 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
                          std::uint32_t* jlist, cudaStream_t s, int num_sms);
 // junction launch: rec / predone (bit per junction) / n_predone set, slen null;
 // 1-saddle launch: slen set (their merged length when all branches are terminal), rec/predone null
+// rank words of the sorted 2-saddle list by cell id (n_cells / 32 + 1 uint2)
+int launch_term_rank(const void* list, std::uint64_t n, int id_width, std::uint64_t n_cells, void* trank,
+                     cudaStream_t s, int num_sms);
 int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
-                const std::uint32_t* tmap, const std::uint32_t* jlist, const void* srcs, int id_width,
+                const std::uint32_t* tmap, const void* trank, const std::uint32_t* jlist, const void* srcs, int id_width,
                 std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
                 unsigned int* ptbits, cudaStream_t s,

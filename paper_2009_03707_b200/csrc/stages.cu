@@ -167,28 +167,44 @@ int bfs(msc3d_ctx* ctx, const void* d_sources, std::uint64_t n_src) {
     if (nde >= 0xffffffffull) return MSC3D_ERR_INVALID;
     TRY(succ_table(ctx));
     auto* bitmap = static_cast<unsigned int*>(ctx->ensure("visited", nwords, 4));
-    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
-    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
-    if (!bitmap || !fa || !fb) return MSC3D_ERR_NOMEM;
-    MSC3D_CUDA_TRY(cudaMemsetAsync(bitmap, 0, nwords * 4, ctx->stream));
-    auto* cnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 48);     // 3 counters
-    auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 51);
-    // [0] rounds [1] claims [2 + r] device time at the start of round r (ns)
+    if (!bitmap) return MSC3D_ERR_NOMEM;
+    // [0] rounds (~0: a level overflowed the frontier buffers) [1] claims
+    // [2 + r] device time at the start of round r (ns)
     auto* stats = static_cast<unsigned long long*>(ctx->ensure("reach_stats", 2 + 256, 8));
     if (!stats) return MSC3D_ERR_NOMEM;
-    MSC3D_CUDA_TRY(cudaMemsetAsync(stats, 0, 2 * 8, ctx->stream));
-    ctx->h_small[48] = n_src;
-    for (int k = 49; k < 54; ++k) ctx->h_small[k] = 0;
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(cnt, &ctx->h_small[48], 6 * 8, cudaMemcpyHostToDevice, ctx->stream));
-    // seeds: validated 1-saddles, their bits set (saddle_graph.cpp:29-41)
-    TRY(msc3d_dev::launch_bfs_sources(codes, d, d_sources, n_src, w, bitmap, fa, bad, ctx->stream,
-                                      ctx->num_sms));
-    if (n_src)
-        TRY(msc3d_dev::launch_reach(ctx->ptr<std::uint16_t>("succ"), d, bitmap, fa, fb, cnt, stats, ctx->stream,
-                                    ctx->num_sms));
-    MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 52, stats, 2 * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    TRY(ctx->fetch_small(54));
-    if (ctx->h_small[51] & 0xffffffffu) return MSC3D_ERR_INVALID;  // saddle_graph.cpp:29-31
+    auto* cnt = reinterpret_cast<unsigned long long*>(ctx->d_small + 48);     // 3 counters
+    auto* bad = reinterpret_cast<unsigned int*>(ctx->d_small + 51);
+    // Frontier buffers: a level has at most 4x the nodes of the one before (<= 4
+    // successors per 1-cell) and the measured levels stay near the source count, so
+    // they start at 4 x sources (not 3V entries each: 2 x 12.9 GB at 2^30 vertices);
+    // a level that does not fit is detected in the kernel and the BFS reruns with
+    // buffers of every dense edge.
+    std::uint64_t fcap = std::min<std::uint64_t>(nde, std::max<std::uint64_t>(4 * n_src, 1ull << 22));
+    if (ctx->frontier_cap) fcap = std::min<std::uint64_t>(nde, std::max<std::uint64_t>(ctx->frontier_cap, n_src));
+    for (int attempt = 0;; ++attempt) {
+        auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", fcap, 4));
+        auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", fcap, 4));
+        if (!fa || !fb) return MSC3D_ERR_NOMEM;
+        MSC3D_CUDA_TRY(cudaMemsetAsync(bitmap, 0, nwords * 4, ctx->stream));
+        MSC3D_CUDA_TRY(cudaMemsetAsync(stats, 0, 2 * 8, ctx->stream));
+        ctx->h_small[48] = n_src;
+        for (int k = 49; k < 54; ++k) ctx->h_small[k] = 0;
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(cnt, &ctx->h_small[48], 6 * 8, cudaMemcpyHostToDevice, ctx->stream));
+        // seeds: validated 1-saddles, their bits set (saddle_graph.cpp:29-41)
+        TRY(msc3d_dev::launch_bfs_sources(codes, d, d_sources, n_src, w, bitmap, fa, bad, ctx->stream,
+                                          ctx->num_sms));
+        if (n_src)
+            TRY(msc3d_dev::launch_reach(ctx->ptr<std::uint16_t>("succ"), d, bitmap, fa, fb, fcap, cnt, stats,
+                                        ctx->stream, ctx->num_sms));
+        MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 52, stats, 2 * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        TRY(ctx->fetch_small(54));
+        if (ctx->h_small[51] & 0xffffffffu) return MSC3D_ERR_INVALID;  // saddle_graph.cpp:29-31
+        if (ctx->h_small[52] != ~0ull) break;
+        if (fcap >= nde) return MSC3D_ERR_RUNTIME;  // (cannot happen: a level holds distinct edges)
+        ctx->scalars["bfs_frontier_retries"] = attempt + 1;
+        fcap = nde;
+    }
+    ctx->scalars["bfs_frontier_cap"] = static_cast<std::int64_t>(fcap);
     const std::int64_t rounds = static_cast<std::int64_t>(ctx->h_small[52]);
     ctx->h_small[49] = ctx->h_small[53];
     ctx->scalars["bfs_levels"] = rounds;  // BFS levels
@@ -317,12 +333,27 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     MSC3D_CUDA_TRY(cudaMemsetAsync(flags, 0, 16, s));
 
     // junctions: bitmap + per-word ranks + list in dense-edge order
-    auto* tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", nde, 4));
+    // 2-saddle ranks for the walks' terminal lookups: a u32 per dense quad (one load)
+    // up to 2^28 vertices (3 GB), above that rank words in cell order (N/4 bytes)
+    const bool use_tmap = d.n_verts <= (1ull << 28) && !ctx->term_rank_words;
+    std::uint32_t* tmap = nullptr;
+    void* trank = nullptr;
+    if (use_tmap) {
+        ctx->release("term_rank");
+        tmap = static_cast<std::uint32_t*>(ctx->ensure("tmap", nde, 4));
+        if (!tmap) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d, tmap, s, sms));
+    } else {
+        ctx->release("tmap");
+        trank = ctx->ensure("term_rank", d.n_cells / 32 + 1, 8);
+        if (!trank) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_term_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d.n_cells, trank, s,
+                                        sms));
+    }
     auto* jbits = static_cast<unsigned int*>(ctx->ensure("jbits", nwords, 4));
     auto* jcnt = static_cast<std::uint32_t*>(ctx->ensure("jcount", nwords, 4));
     auto* woff = static_cast<std::uint64_t*>(ctx->ensure("joff", nwords, 8));
-    if (!tmap || !jbits || !jcnt || !woff) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_scatter_quad_rank(ctx->ptr<void>(term_list), ctx->count(term_list), w, d, tmap, s, sms));
+    if (!jbits || !jcnt || !woff) return MSC3D_ERR_NOMEM;
     MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 50, 0, 8, s));
     TRY(msc3d_dev::launch_junction_bits(succ, bitmap, nwords, jbits, jcnt,
                                         reinterpret_cast<unsigned long long*>(ctx->d_small + 50), s, sms));
@@ -345,8 +376,10 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* slen = static_cast<std::uint32_t*>(ctx->ensure("slen", n1, 4));
     auto* soff = static_cast<std::uint64_t*>(ctx->ensure("soff", n1, 8));
     auto* ptop = static_cast<unsigned long long*>(ctx->ensure("pool_top", msc3d_dev::count_arenas(), 8));
-    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", nde, 4));
-    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", nde, 4));
+    // Kahn's frontiers hold junctions; the BFS buffers are reused (grown if needed)
+    const std::uint64_t fcap = std::max<std::uint64_t>(std::max<std::uint64_t>(ctx->count("frontier_a"), nn), 1024);
+    auto* fa = static_cast<std::uint32_t*>(ctx->ensure("frontier_a", fcap, 4));
+    auto* fb = static_cast<std::uint32_t*>(ctx->ensure("frontier_b", fcap, 4));
     if (!jlist || !node || !jdest || !pending || !pending0 || !indeg || !fwd || !ovoff || !rec ||
         !slen || !soff || !ptop || !fa || !fb)
         return MSC3D_ERR_NOMEM;
@@ -362,9 +395,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     // (the junction walks also flag the pass-through junctions: fwd, ptbits)
     auto* ptbits = static_cast<unsigned int*>(ctx->ensure("ptbits", (nj + 31) / 32 + 1, 4));
     if (!ptbits) return MSC3D_ERR_NOMEM;
-    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
+    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, trank, jlist, nullptr, w, nj, jdest, pending, flags, rec, nullptr,
                                predone, n_predone, fwd, ptbits, s, sms));
-    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, nullptr, src_ids, w, n1,
+    TRY(msc3d_dev::launch_walk(succ, d, jrank, tmap, trank, nullptr, src_ids, w, n1,
                                jdest + nj * 16, pending + nj, flags, nullptr, slen, nullptr, nullptr, nullptr, nullptr, s,
                                sms));
     // pass-through junctions (one live branch, to a junction: P(j) = P(child)) are
@@ -383,9 +416,9 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* ovq_n = reinterpret_cast<unsigned long long*>(ctx->d_small + 20);
     MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 19, 0, 16, s));
     // overflow queue (parents beyond the inline ones): reuse a frontier buffer
-    // (nde u32 = 3V*4 bytes, room for 3V/4 entries >> the measured ~0.1% of nodes)
+    // (>= nn u32: room for nn/4 entries >> the measured ~0.1% of nodes)
     void* ovq = fa;
-    const std::uint64_t ovq_cap = nde / 4;
+    const std::uint64_t ovq_cap = fcap / 4;
     auto* ready = static_cast<std::uint32_t*>(ctx->ensure("ready0", std::max<std::uint64_t>(nj, 1), 4));
     if (!ready) return MSC3D_ERR_NOMEM;
     auto* n_ready = reinterpret_cast<unsigned long long*>(ctx->d_small + 77);

@@ -160,6 +160,29 @@ def test_compute_synth_64(ctx, ref, kind):
         assert got.arc_src.size == 2768 and int(got.arc_mult.max()) == 4
 
 
+@pytest.mark.parametrize("kind", ["gnoise", "noise"])
+def test_bfs_frontier_overflow_retry(ref, kind):
+    """A BFS level larger than the frontier buffers is detected and the BFS reruns with
+    full-size buffers (stages.cu bfs); the complex is unchanged."""
+    dims = (40, 36, 32)
+    c = m.Context(0)
+    c.set_option("frontier_cap", 64)
+    _compute_vs_ref(c, ref, m.synth(kind, dims), dims)
+    assert c.scalar("bfs_frontier_retries") == 1
+    assert c.scalar("bfs_frontier_cap") == 3 * dims[0] * dims[1] * dims[2]
+
+
+@pytest.mark.parametrize("kind,dims", [("gnoise", (40, 36, 32)), ("noise", (33, 17, 9)), ("gauss", (48, 40, 36))])
+def test_term_rank_words(ref, kind, dims):
+    """The 2-saddle rank words in cell order (the walks' terminal lookup above 2^28
+    vertices, dag.cu WalkCtx::term_rank) give the same complex as the per-quad map."""
+    c = m.Context(0)
+    c.set_option("term_rank_words", 1)
+    _compute_vs_ref(c, ref, m.synth(kind, dims), dims)
+    c.set_option("wide_ids", 1)  # with 64-bit id lists too
+    _compute_vs_ref(c, ref, m.synth(kind, dims), dims)
+
+
 def test_compute_without_segmentation(ctx, ref):
     dims = (8, 8, 8)
     _compute_vs_ref(ctx, ref, random_field(ref, dims, 7), dims, seg=False)

@@ -15,7 +15,7 @@ codes_ptr, ncodes, _ = ctx.array_info("codes")
 codes = torch.empty(ncodes, dtype=torch.uint8, device="cuda")
 ctx.sync()
 import paper_2009_03707_b200.multigpu as mg
-src = mg._wrap_device(codes_ptr, ncodes, torch.uint8)
+src = mg._wrap_device(codes_ptr, ncodes)
 codes.copy_(src)
 torch.cuda.synchronize()
 full = m.Context(0)
