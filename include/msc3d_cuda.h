@@ -95,7 +95,9 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
  *                             sources; a level that does not fit reruns the BFS with
  *                             buffers of every dense edge);
  *   "term_rank_words" (0/1)   the walks' 2-saddle rank lookup grids above 2^28 vertices
- *                             use (rank words in cell order), on any grid.
+ *                             use (rank words in cell order), on any grid;
+ *   "release_transients" (0/1) free each stage's scratch arrays once they are dead, as
+ *                             grids above 2^32 cells do, on any grid.
  * Unknown names / bad values -> MSC3D_ERR_INVALID. */
 int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, int64_t value);
 /* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...); also

@@ -208,6 +208,8 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "frontier_cap") {  // initial BFS frontier entries (0 = 4 x sources)
         if (value < 0) return MSC3D_ERR_INVALID;
         ctx->frontier_cap = static_cast<std::uint64_t>(value);
+    } else if (n == "release_transients") {  // free stage scratch early on any grid
+        ctx->force_release = value != 0;
     } else if (n == "term_rank_words") {  // the large-grid 2-saddle rank lookup on any grid
         ctx->term_rank_words = value != 0;
     } else {

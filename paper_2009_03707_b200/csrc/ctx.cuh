@@ -128,7 +128,10 @@ struct msc3d_ctx {
     // Large grids (configs 4-5, > 2^32 cells) hand the memory of a stage's transient
     // arrays back once the stage is done (later stages allocate into it);
     // smaller grids keep them so that repeated computes allocate nothing.
-    bool release_transients() const { return dims.n_cells > 0xffffffffull; }
+    // Free stage scratch as soon as it is dead: grids above 2^32 cells (configs 4-5),
+    // or any grid with the "release_transients" option (tests)
+    bool force_release = false;
+    bool release_transients() const { return force_release || dims.n_cells > 0xffffffffull; }
     void release(const std::string& name) {
         auto it = arrays.find(name);
         if (it == arrays.end()) return;

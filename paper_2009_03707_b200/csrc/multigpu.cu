@@ -449,7 +449,15 @@ int msc3d_mg_compute(msc3d_mg* g, msc3d_dims dims, int value_type, const void* o
                                         static_cast<std::uint64_t>(world), nullptr, true));
     cudaEventRecord(ev[3], s);
 
-    // [6] the arc blocks of every rank, then min->1s ∥ blocks ∥ 2s->max
+    // [6] the arc blocks of every rank, then min->1s ∥ blocks ∥ 2s->max.  On grids
+    // above 2^32 cells the saddle stages' scratch goes first (config 5: ~25 GB of
+    // junction records, pools and frontiers make room for the gathered arcs).
+    if (world > 1 && full->release_transients())
+        for (const char* t : {"frontier_a", "frontier_b", "heavy_q", "indeg", "jbits", "jcount", "jdest", "jfwd",
+                              "jlist", "jnode", "joff", "jrank", "jrec", "ovoff", "pending", "pending0", "pool_cnt",
+                              "pool_key", "ready0", "soff", "term_rank", "tmap", "visited", "slen", "rsrc",
+                              "ready_bits", "jump_conv_pt", "predone", "ptbits", "count_stats"})
+            full->release(t);
     if (world > 1) {
         const std::uint64_t na = full->count("arcA_src"), nb = full->count("arcB_src"), nc = full->count("arcC_src");
         std::vector<std::uint64_t> allnb;
@@ -480,6 +488,12 @@ int msc3d_mg_compute(msc3d_mg* g, msc3d_dims dims, int value_type, const void* o
             MSC3D_CUDA_TRY(cudaMemcpyAsync(amul + na + tb, full->ptr<void>("arcC_mult"), nc * 8, cudaMemcpyDeviceToDevice, s));
         }
         full->scalars["arcs_total"] = static_cast<std::int64_t>(total);
+        if (full->release_transients()) {  // the blocks now live in arc_src/dst/mult
+            MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
+            for (const char* t : {"arcA_src", "arcA_dst", "arcA_mult", "arcB_src", "arcB_dst", "arcB_mult",
+                                  "arcC_src", "arcC_dst", "arcC_mult"})
+                full->release(t);
+        }
     }
     cudaEventRecord(ev[4], s);
     MSC3D_CUDA_TRY(cudaStreamSynchronize(s));

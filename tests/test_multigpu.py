@@ -152,13 +152,16 @@ def test_sharded_saddles_reassemble(kind, dims, world):
     ctx.close()
 
 
-def _mg_worker(rank, world, port, q, kind, dims):
+def _mg_worker(rank, world, port, q, kind, dims, large_grid_path=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         v = m.synth(kind, dims)
         g = mg.MultiGPU(dims, rank, world, device=0, transport="host")
+        if large_grid_path:  # what config 5 (> 2^32 cells) runs: scratch freed before the gather,
+            for opt, val in (("release_transients", 1), ("term_rank_words", 1), ("frontier_cap", 16)):
+                g.full.set_option(opt, val)  # (+ 2-saddle rank words, small frontiers: BFS rerun)
         own = torch.from_numpy(mg.slab_values(v, dims, g.plan)).cuda()
         for _ in range(2):  # a repeated step on the same contexts
             g.step(own, m.OPT_SEGMENTATION)
@@ -183,6 +186,13 @@ def _mg_worker(rank, world, port, q, kind, dims):
                                             ("gauss", (40, 36, 32), 2)])
 def test_mg_orchestrator_host_transport(kind, dims, world):
     res = _spawn(_mg_worker, world, kind, dims)
+    assert all(ok for _, ok, _ in res), res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,dims,world", [("gnoise", (24, 20, 16), 2), ("noise", (20, 18, 17), 3)])
+def test_mg_orchestrator_large_grid_path(kind, dims, world):
+    res = _spawn(_mg_worker, world, kind, dims, True)
     assert all(ok for _, ok, _ in res), res
 
 
