@@ -500,7 +500,7 @@ def main():
             t1 = time.perf_counter()
             if rc:
                 raise RuntimeError(f"compute_host failed: {rc}")
-            d2h = ho.n_cp * (idw + 1) + ho.n_arcs * 16 + (V + Cu) * 4
+            d2h = ctx.scalar("d2h_bytes")  # as counted by the delivery (multiplicities as bytes + escapes)
             if i >= 2:
                 e2e_times.append(t1 - t0)
         if ho.n_arcs != n_arcs or ho.n_cp != ncp:
@@ -509,7 +509,8 @@ def main():
         e2e = {"value": world * ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
                "path": "msc3d_ctx_compute_host_values (C ABI): pinned samples in (upload overlapped with the "
-                       "gradient), pinned host outputs (copies overlapped with the later stages)"}
+                       "gradient), pinned host outputs (copies overlapped with the later stages; multiplicities "
+                       "as one byte per arc + escapes, widened into the u64 output by host threads)"}
 
     # ---- the C++ drop-in msc3d::compute() (include/msc3d/api.hpp): host ScalarField of
     # doubles in, host MSComplex out (critical points with coordinates and values,

@@ -293,6 +293,31 @@ __global__ void k_arcs_max_emit(const std::uint32_t* __restrict__ slot, std::uin
     }
 }
 
+// Host delivery of multiplicities: one byte per arc (values <= vmax (254) as they are,
+// 255 = "see the escape list"), the rest as (index, value) pairs appended in any order
+// (warp-aggregated; ~1% of the 1s->2s arcs of a noisy field).  Appends past `cap` are
+// counted but dropped: the host then copies the u64 array instead.
+__global__ void k_pack_mult(const std::uint64_t* __restrict__ mult, std::uint64_t n, std::uint64_t vmax,
+                            std::uint8_t* __restrict__ out8, ulonglong2* __restrict__ esc, std::uint64_t cap,
+                            unsigned long long* __restrict__ n_esc) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < n;
+         base += stride) {
+        const std::uint64_t i = base + (threadIdx.x & 31);
+        const std::uint64_t m = i < n ? mult[i] : 0;
+        const bool big = i < n && m > vmax;
+        if (i < n) out8[i] = static_cast<std::uint8_t>(big ? 255u : m);
+        const unsigned ball = __ballot_sync(0xffffffffu, big);
+        if (ball) {
+            const int lane = threadIdx.x & 31, leader = __ffs(ball) - 1;
+            unsigned long long at = 0;
+            if (lane == leader) at = atomicAdd(n_esc, static_cast<unsigned long long>(__popc(ball)));
+            at = __shfl_sync(0xffffffffu, at, leader) + __popc(ball & ((1u << lane) - 1u));
+            if (big && at < cap) esc[at] = make_ulonglong2(i, m);
+        }
+    }
+}
+
 }  // namespace
 
 int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t n, int id_width,
@@ -475,6 +500,18 @@ int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint3
                          std::uint64_t* amult, cudaStream_t s, int num_sms) {
     if (n2 == 0) return MSC3D_OK;
     k_arcs_max_emit<<<grid_for(n2, num_sms), kThreads, 0, s>>>(slot, n2, base2, off, asrc, adst, amult);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+int launch_pack_mult(const std::uint64_t* mult, std::uint64_t n, std::uint64_t vmax, std::uint8_t* out8, void* esc,
+                     std::uint64_t cap, unsigned long long* n_esc, cudaStream_t s, int num_sms) {
+    if (vmax > 254) return MSC3D_ERR_INVALID;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_esc, 0, 8, s));
+    if (n == 0) return MSC3D_OK;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>((n + 255) / 256, 16ull * num_sms));
+    k_pack_mult<<<grid, 256, 0, s>>>(mult, n, vmax, out8, static_cast<ulonglong2*>(esc), cap, n_esc);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

@@ -208,6 +208,14 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "frontier_cap") {  // initial BFS frontier entries (0 = 4 x sources)
         if (value < 0) return MSC3D_ERR_INVALID;
         ctx->frontier_cap = static_cast<std::uint64_t>(value);
+    } else if (n == "d2h_narrow") {  // multiplicities cross the bus as bytes + escapes (default 1)
+        ctx->d2h_narrow = value != 0;
+    } else if (n == "d2h_escape_cap") {  // escape-list entries per arc block (0 = n / 16 + 1024)
+        if (value < 0) return MSC3D_ERR_INVALID;
+        ctx->d2h_escape_cap = static_cast<std::uint64_t>(value);
+    } else if (n == "d2h_narrow_max") {  // largest multiplicity sent as a byte (<= 254)
+        if (value < 0 || value > 254) return MSC3D_ERR_INVALID;
+        ctx->d2h_narrow_max = static_cast<std::uint64_t>(value);
     } else if (n == "release_transients") {  // free stage scratch early on any grid
         ctx->force_release = value != 0;
     } else if (n == "term_rank_words") {  // the large-grid 2-saddle rank lookup on any grid

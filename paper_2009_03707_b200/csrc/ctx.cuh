@@ -49,6 +49,29 @@ struct msc3d_ctx {
     std::uint64_t launches_at_create = 0;
     cudaStream_t copy = nullptr;  // device-to-host copies overlapping the pipeline
     cudaStream_t h2d = nullptr;   // host-to-device input chunks overlapping the gradient
+    // host deliveries (msc3d_ctx_compute_host*): multiplicities cross the bus as one
+    // byte each (+ an escape list) and are widened on host threads; "d2h_narrow" 0
+    // copies the u64 arrays instead, "d2h_escape_cap" bounds the escape list (tests)
+    bool d2h_narrow = true;
+    std::uint64_t d2h_escape_cap = 0;
+    std::uint64_t d2h_narrow_max = 254;  // largest multiplicity sent as its byte (tests: lower)
+    std::map<std::string, std::pair<void*, std::size_t>> pinned;  // pinned host staging
+
+    // Pinned host staging `name` of >= bytes (kept across calls), nullptr on failure.
+    void* host_buf(const std::string& name, std::size_t bytes) {
+        auto& b = pinned[name];
+        if (b.second < bytes || !b.first) {
+            if (b.first) cudaFreeHost(b.first);
+            b = {nullptr, 0};
+            if (cudaHostAlloc(&b.first, bytes ? bytes : 16, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                b.first = nullptr;
+                return nullptr;
+            }
+            b.second = bytes;
+        }
+        return b.first;
+    }
 
     cudaStream_t copy_stream() {
         if (!copy && cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking) != cudaSuccess) copy = nullptr;
@@ -62,6 +85,8 @@ struct msc3d_ctx {
     ~msc3d_ctx() {
         for (auto& kv : arrays)
             if (kv.second.ptr) cudaFree(kv.second.ptr);
+        for (auto& kv : pinned)
+            if (kv.second.first) cudaFreeHost(kv.second.first);
         if (d_small) cudaFree(d_small);
         if (h_small) cudaFreeHost(h_small);
         if (own_stream && stream) cudaStreamDestroy(stream);

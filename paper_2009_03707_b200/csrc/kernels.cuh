@@ -160,6 +160,9 @@ int launch_bucket_sort(const std::uint64_t* off, std::uint64_t nb, std::uint64_t
 int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dims& d,
                     const std::uint32_t* label3, RankRemap remap3, std::uint32_t* slot,
                     std::uint32_t* cnt, cudaStream_t s, int num_sms);
+// multiplicities for the host: one byte each (255 = escaped) + (index, value) escapes
+int launch_pack_mult(const std::uint64_t* mult, std::uint64_t n, std::uint64_t vmax, std::uint8_t* out8, void* esc,
+                     std::uint64_t cap, unsigned long long* n_esc, cudaStream_t s, int num_sms);
 int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint32_t base2,
                          const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,
                          std::uint64_t* amult, cudaStream_t s, int num_sms);

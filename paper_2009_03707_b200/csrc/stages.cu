@@ -1,11 +1,14 @@
 // Stage orchestration: allocation of named device arrays, launch order, and the
 // few host<->device handshakes (output sizes) each stage needs.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -591,6 +594,8 @@ struct Sink {
     const msc3d_host_outputs* out;
     cudaStream_t cs = nullptr;
     std::vector<cudaEvent_t> evs;
+    std::uint64_t bytes_moved = 0;  // D2H bytes of this delivery
+    std::chrono::steady_clock::time_point t_created = std::chrono::steady_clock::now();
     bool ok() const { return out != nullptr; }
     // development timeline (MSC3D_DIAG): [t0 on the compute stream, per copy: ready, start, end]
     bool diag = std::getenv("MSC3D_DIAG") != nullptr;
@@ -615,14 +620,114 @@ struct Sink {
             tl.push_back(a);
         }
         MSC3D_CUDA_TRY(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, cs));
+        bytes_moved += bytes;
         if (diag) {
             cudaEventRecord(b, cs);
             tl.push_back(b);
         }
         return MSC3D_OK;
     }
+    // Multiplicities (the largest output: 8 bytes per arc, almost all < 255) cross the
+    // bus as one byte per arc plus an escape list (k_pack_mult) and are widened into
+    // the caller's u64 array by host threads -- a decode job per arc block, started
+    // as soon as the block is final and joined in finish().  An escape list larger
+    // than its buffer falls back to copying the u64 array.
+    struct Job {
+        std::thread th;
+        int rc = MSC3D_OK;
+        std::uint64_t bytes = 0;  // D2H bytes the job moved itself
+    };
+    std::vector<std::unique_ptr<Job>> jobs;
+    int copy_mult(std::uint64_t* host, const std::uint64_t* dev, std::uint64_t n, const char* tag) {
+        if (!out || !host || n == 0) return MSC3D_OK;
+        if (!ctx->d2h_narrow) return copy(host, dev, n * 8);
+        const std::string t = tag;
+        const std::uint64_t cap = ctx->d2h_escape_cap ? ctx->d2h_escape_cap : n / 16 + 1024;
+        auto* d8 = static_cast<std::uint8_t*>(ctx->ensure("d2h_mult8_" + t, n, 1));
+        void* desc = ctx->ensure("d2h_esc_" + t, cap, 16);
+        auto* dcnt = static_cast<unsigned long long*>(ctx->ensure("d2h_nesc_" + t, 1, 8));
+        auto* h8 = static_cast<std::uint8_t*>(ctx->host_buf("mult8_" + t, n));
+        auto* hcnt = static_cast<unsigned long long*>(ctx->host_buf("nesc_" + t, 8));
+        auto* hesc = static_cast<ulonglong2*>(ctx->host_buf("esc_" + t, cap * 16));
+        if (!d8 || !desc || !dcnt || !h8 || !hcnt || !hesc) return MSC3D_ERR_NOMEM;
+        TRY(msc3d_dev::launch_pack_mult(dev, n, ctx->d2h_narrow_max, d8, desc, cap, dcnt, ctx->stream, ctx->num_sms));
+        TRY(copy(hcnt, dcnt, 8));
+        TRY(copy(h8, d8, n));
+        cudaEvent_t done;
+        MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        evs.push_back(done);
+        MSC3D_CUDA_TRY(cudaEventRecord(done, cs));
+        auto job = std::make_unique<Job>();
+        Job* jp = job.get();
+        const int device = ctx->device;
+        const bool dg = diag;
+        const auto t_sink = t_created;
+        jp->th = std::thread([=]() {
+            auto ms_since = [&]() {
+                return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sink).count();
+            };
+            auto fail = [&](int rc) { jp->rc = rc; };
+            if (cudaSetDevice(device) != cudaSuccess || cudaEventSynchronize(done) != cudaSuccess)
+                return fail(MSC3D_ERR_CUDA);
+            const double t_ready = ms_since();
+            const unsigned long long ne = *hcnt;
+            const bool fallback = ne > cap;  // escapes did not fit: the u64 array itself
+            cudaStream_t js = nullptr;
+            if (cudaStreamCreateWithFlags(&js, cudaStreamNonBlocking) != cudaSuccess) return fail(MSC3D_ERR_CUDA);
+            auto fetch = [&](void* h, const void* d, std::uint64_t bytes) {
+                cudaError_t e = cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, js);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(js);
+                return e == cudaSuccess;
+            };
+            if (fallback) {
+                const bool okf = fetch(host, dev, n * 8);
+                cudaStreamDestroy(js);
+                jp->bytes = n * 8;
+                return okf ? void() : fail(MSC3D_ERR_CUDA);
+            }
+            // widen the bytes into the u64 output on all host threads (overlapping the
+            // block's other copies, which occupy the copy engine), then fetch the
+            // escapes and patch them (~1% random stores, also split across threads:
+            // 3.6 M cache-missing stores cost ~18 ms on one thread at 512^3)
+            const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+            const std::uint64_t T = n < (1ull << 20) ? 1 : std::min<std::uint64_t>(hw, 32);
+            auto widen = [&](std::uint64_t a, std::uint64_t b) {
+                for (std::uint64_t i = a; i < b; ++i) host[i] = h8[i];
+            };
+            auto patch = [&](std::uint64_t a, std::uint64_t b) {
+                for (std::uint64_t k = a; k < b; ++k) host[hesc[k].x] = hesc[k].y;
+            };
+            auto team = [&](auto f, std::uint64_t m, std::uint64_t nt) {
+                std::vector<std::thread> ws;
+                for (std::uint64_t k = 1; k < nt; ++k) ws.emplace_back(f, m * k / nt, m * (k + 1) / nt);
+                f(0, m / nt);
+                for (auto& w : ws) w.join();
+            };
+            team(widen, n, T);
+            const double t_w1 = ms_since();
+            const bool oke = ne == 0 || fetch(hesc, desc, ne * 16);
+            cudaStreamDestroy(js);
+            if (!oke) return fail(MSC3D_ERR_CUDA);
+            jp->bytes = ne * 16;
+            const double t_e = ms_since();
+            team(patch, ne, ne < (1ull << 16) ? 1 : T);
+            if (dg)
+                std::fprintf(stderr, "sink widen %s: %llu arcs, bytes in at %.2f ms, widened by %.2f (%llu threads), "
+                             "%llu escapes in by %.2f, patched by %.2f ms (host clock)\n", t.c_str(),
+                             static_cast<unsigned long long>(n), t_ready, t_w1, static_cast<unsigned long long>(T), ne,
+                             t_e, ms_since());
+        });
+        jobs.push_back(std::move(job));
+        return MSC3D_OK;
+    }
     int finish() {
         int rc = MSC3D_OK;
+        for (auto& j : jobs) {
+            if (j->th.joinable()) j->th.join();
+            if (j->rc != MSC3D_OK && rc == MSC3D_OK) rc = j->rc;
+            bytes_moved += j->bytes;
+        }
+        jobs.clear();
         if (cs && cudaStreamSynchronize(cs) != cudaSuccess) rc = MSC3D_ERR_CUDA;
         if (diag && tl.size() >= 3) {
             cudaDeviceSynchronize();
@@ -641,6 +746,7 @@ struct Sink {
         }
         for (auto e : evs) cudaEventDestroy(e);
         evs.clear();
+        if (out) ctx->scalars["d2h_bytes"] = static_cast<std::int64_t>(bytes_moved);
         return rc;
     }
     ~Sink() { finish(); }
@@ -811,9 +917,10 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
             ctx->release(t);
     if (host) {
         if (host->arc_cap < na) return MSC3D_ERR_INVALID;
+        // (the multiplicity bytes first: their host widening overlaps the other copies)
+        TRY(sink.copy_mult(host->arc_mult, amin_mul, na, "A"));
         TRY(sink.copy(host->arc_src, amin_src, na * 4));
         TRY(sink.copy(host->arc_dst, amin_dst, na * 4));
-        TRY(sink.copy(host->arc_mult, amin_mul, na * 8));
     }
     clk.mark(4, s);  // (end of the untimed block: re-based below)
 
@@ -857,9 +964,9 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         if (!asrc || !adst || !amul) return MSC3D_ERR_NOMEM;
         if (host) {  // the 2s->max block's host position is known now: send it before the 1s->2s block
             if (host->arc_cap < total) return MSC3D_ERR_INVALID;
+            TRY(sink.copy_mult(host->arc_mult + na + nb, amax_mul, nc, "C"));
             TRY(sink.copy(host->arc_src + na + nb, amax_src, nc * 4));
             TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
-            TRY(sink.copy(host->arc_mult + na + nb, amax_mul, nc * 8));
         }
         o->one = asrc + na;
         o->two = adst + na;
@@ -893,9 +1000,9 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     }
     if (host) {
         if (host->arc_cap < na + nb + nc) return MSC3D_ERR_INVALID;
+        TRY(sink.copy_mult(host->arc_mult + na, amul + na, nb, "B"));
         TRY(sink.copy(host->arc_src + na, asrc + na, nb * 4));
         TRY(sink.copy(host->arc_dst + na, adst + na, nb * 4));
-        TRY(sink.copy(host->arc_mult + na, amul + na, nb * 8));
     }
     // device-side arc arrays complete: the min and max blocks around the 1s->2s block
     if (na) {

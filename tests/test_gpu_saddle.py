@@ -198,10 +198,17 @@ def test_compute_repeatable(ctx, ref):
         np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("kind", ["gnoise", "noise"])
-def test_compute_host_outputs(ctx, ref, kind):
-    """msc3d_ctx_compute_host: the overlapped host copies equal the reference."""
+@pytest.mark.parametrize("kind,narrow", [("gnoise", None), ("noise", None),
+                                         ("gnoise", {"d2h_narrow_max": 1}),  # escapes
+                                         ("noise", {"d2h_narrow_max": 0, "d2h_escape_cap": 3}),  # u64 fallback
+                                         ("gnoise", {"d2h_narrow": 0})])  # u64 copies
+def test_compute_host_outputs(ref, kind, narrow):
+    """msc3d_ctx_compute_host: the overlapped host copies (multiplicities as bytes +
+    escape list, widened on host threads) equal the reference."""
     import ctypes as C
+    ctx = m.Context(0)
+    for k, val in (narrow or {}).items():
+        ctx.set_option(k, val)
     dims = (40, 36, 32)
     v = m.synth(kind, dims)
     want = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
@@ -220,6 +227,13 @@ def test_compute_host_outputs(ctx, ref, kind):
     for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
         np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype))
     np.testing.assert_array_equal(buf["cp_index"].astype(np.int32), want["cp_index"])
+    full = ncp * 5 + na * 16 + (V + Cu) * 4
+    if narrow and narrow.get("d2h_narrow") == 0:
+        assert ctx.scalar("d2h_bytes") == full
+    elif narrow and "d2h_escape_cap" in narrow:
+        assert ctx.scalar("d2h_bytes") > full  # bytes + count, then the u64 arrays
+    elif not narrow:
+        assert ctx.scalar("d2h_bytes") < full - 6 * na
     # too small an arc buffer is rejected (invalid_argument)
     ho.arc_cap = max(0, na - 1)
     assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == m.ERR_INVALID

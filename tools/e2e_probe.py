@@ -24,9 +24,14 @@ b = {k: torch.empty(sz, dtype=torch.uint8).pin_memory() for k, sz in
      (("cc", ncp * 4), ("ci", ncp), ("as", na * 4), ("ad", na * 4), ("am", na * 8), ("lm", V * 4), ("lx", Cu * 4))}
 ho = m.HostOutputs(b["cc"].data_ptr(), ncp * 4, b["ci"].data_ptr(), ncp, b["as"].data_ptr(), b["ad"].data_ptr(),
                    b["am"].data_ptr(), na, b["lm"].data_ptr(), b["lx"].data_ptr(), 0, 0)
-rcs = []
-ms = t(lambda: rcs.append(L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho))))
-print("compute_host ms", ms, "rc", set(rcs))
+for narrow in (1, 0):
+    ctx.set_option("d2h_narrow", narrow)
+    rcs = []
+    ms = t(lambda: rcs.append(L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho))))
+    print(f"compute_host (d2h_narrow {narrow}) ms {ms:.1f} rc {set(rcs)} d2h bytes {ctx.scalar('d2h_bytes') / 1e9:.2f} GB")
+    hv = lambda: L.msc3d_ctx_compute_host_values(ctx.h, m.Dims(*dims), m.VALUE_F32, C.c_void_p(hin.data_ptr()),
+                                                 m.OPT_SEGMENTATION, None, C.byref(ho))
+    print(f"compute_host_values (d2h_narrow {narrow}) ms {t(hv):.1f}")
 dev = torch.empty(2 << 30, dtype=torch.uint8, device="cuda")
 hb = torch.empty(2 << 30, dtype=torch.uint8).pin_memory()
 ms = t(lambda: hb.copy_(dev, non_blocking=True))
