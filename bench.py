@@ -507,6 +507,7 @@ def main():
             raise RuntimeError("e2e output sizes differ from the device-resident run")
         te = max_over_ranks(sum(e2e_times) / len(e2e_times), world, f"cuda:{local}")
         e2e = {"value": world * ncells / te / 1e6, "unit": "Mcells/s", "ms_per_step": te * 1e3,
+               "step_ms": [round(x * 1e3, 1) for x in e2e_times],
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
                "path": "msc3d_ctx_compute_host_values (C ABI): pinned samples in (upload overlapped with the "
                        "gradient), pinned host outputs (copies overlapped with the later stages; multiplicities "

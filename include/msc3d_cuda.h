@@ -102,7 +102,8 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
  *                             plus an escape list, widened by host threads (default 1);
  *   "d2h_escape_cap" (>=0)    escape entries per arc block (0 = n/16 + 1024; more
  *                             escapes -> the u64 array is copied instead);
- *   "d2h_narrow_max" (0..254) largest multiplicity sent as its byte (default 254).
+ *   "d2h_narrow_max" (0..254) largest multiplicity / source step sent as its byte
+ *                             (default 254; tests lower it to exercise the escapes).
  * Unknown names / bad values -> MSC3D_ERR_INVALID. */
 int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, int64_t value);
 /* Scalar results ("rounds0", "rounds3", "euler", "bfs_levels", ...); also
@@ -210,9 +211,10 @@ int msc3d_ctx_compute(msc3d_ctx* ctx, int options, double* stage_ms);
  * bytes, arc_cap in arcs; labels_min (n_verts u32) / labels_max (n_cubes u32) only
  * with MSC3D_OPT_SEGMENTATION (NULL: not copied).  Too small a buffer ->
  * MSC3D_ERR_INVALID.  On return n_cp / n_arcs hold the sizes; the device arrays of
- * msc3d_ctx_compute stay valid as well.  Multiplicities travel as one byte per arc
- * plus an escape list and are widened into arc_mult by host threads (option
- * "d2h_narrow"); scalar "d2h_bytes" = the bytes that crossed the bus. */
+ * msc3d_ctx_compute stay valid as well.  Multiplicities travel as one byte per arc and
+ * the (sorted) sources as one-byte steps, each plus an escape list, and are decoded
+ * into arc_mult / arc_src by host threads (option "d2h_narrow"); scalar "d2h_bytes" =
+ * the bytes that crossed the bus. */
 typedef struct msc3d_host_outputs {
     void* cp_cell;
     uint64_t cp_cell_cap;

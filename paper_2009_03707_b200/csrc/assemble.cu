@@ -318,6 +318,39 @@ __global__ void k_pack_mult(const std::uint64_t* __restrict__ mult, std::uint64_
     }
 }
 
+// Host delivery of a sorted u32 array (the arc sources): one byte per entry = the
+// difference to the previous entry (<= vmax = 254), 255 = "absolute value in the escape list"
+// (also any decrease: unsorted input stays exact), and the first entry of every chunk
+// of kSrcChunk as a u32 head, so the host decodes the chunks independently.
+constexpr std::uint64_t kSrcChunk = 1ull << 16;
+__global__ void k_pack_src(const std::uint32_t* __restrict__ src, std::uint64_t n, std::uint32_t vmax,
+                           std::uint8_t* __restrict__ out8,
+                           std::uint32_t* __restrict__ heads, ulonglong2* __restrict__ esc, std::uint64_t cap,
+                           unsigned long long* __restrict__ n_esc) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t base = (blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; base < n;
+         base += stride) {
+        const std::uint64_t i = base + (threadIdx.x & 31);
+        bool big = false;
+        if (i < n) {
+            const std::uint32_t v = src[i];
+            const bool head = (i & (kSrcChunk - 1)) == 0;
+            const std::uint32_t prev = head ? v : src[i - 1];
+            big = !head && (v < prev || v - prev > vmax);
+            out8[i] = static_cast<std::uint8_t>(head ? 0u : (big ? 255u : v - prev));
+            if (head) heads[i / kSrcChunk] = v;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, big);
+        if (ball) {
+            const int lane = threadIdx.x & 31, leader = __ffs(ball) - 1;
+            unsigned long long at = 0;
+            if (lane == leader) at = atomicAdd(n_esc, static_cast<unsigned long long>(__popc(ball)));
+            at = __shfl_sync(0xffffffffu, at, leader) + __popc(ball & ((1u << lane) - 1u));
+            if (big && at < cap) esc[at] = make_ulonglong2(i, src[i]);
+        }
+    }
+}
+
 }  // namespace
 
 int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t n, int id_width,
@@ -516,5 +549,21 @@ int launch_pack_mult(const std::uint64_t* mult, std::uint64_t n, std::uint64_t v
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
+
+int launch_pack_src(const std::uint32_t* src, std::uint64_t n, std::uint64_t vmax, std::uint8_t* out8,
+                    std::uint32_t* heads, void* esc, std::uint64_t cap, unsigned long long* n_esc, cudaStream_t s,
+                    int num_sms) {
+    if (vmax > 254) return MSC3D_ERR_INVALID;
+    MSC3D_CUDA_TRY(cudaMemsetAsync(n_esc, 0, 8, s));
+    if (n == 0) return MSC3D_OK;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>((n + 255) / 256, 16ull * num_sms));
+    k_pack_src<<<grid, 256, 0, s>>>(src, n, static_cast<std::uint32_t>(vmax), out8, heads, static_cast<ulonglong2*>(esc), cap,
+                                    n_esc);
+    count_launch();
+    MSC3D_CUDA_TRY(cudaGetLastError());
+    return MSC3D_OK;
+}
+
+std::uint64_t src_chunk() { return kSrcChunk; }
 
 }  // namespace msc3d_dev

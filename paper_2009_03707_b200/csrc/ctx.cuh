@@ -56,6 +56,7 @@ struct msc3d_ctx {
     std::uint64_t d2h_escape_cap = 0;
     std::uint64_t d2h_narrow_max = 254;  // largest multiplicity sent as its byte (tests: lower)
     std::map<std::string, std::pair<void*, std::size_t>> pinned;  // pinned host staging
+    std::map<std::string, std::uint64_t> d2h_esc_memo;  // escape counts of the last delivery per block
 
     // Pinned host staging `name` of >= bytes (kept across calls), nullptr on failure.
     void* host_buf(const std::string& name, std::size_t bytes) {

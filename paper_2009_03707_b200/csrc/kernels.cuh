@@ -163,6 +163,12 @@ int launch_arcs_max(const void* crit2, std::uint64_t n2, int id_width, const Dim
 // multiplicities for the host: one byte each (255 = escaped) + (index, value) escapes
 int launch_pack_mult(const std::uint64_t* mult, std::uint64_t n, std::uint64_t vmax, std::uint8_t* out8, void* esc,
                      std::uint64_t cap, unsigned long long* n_esc, cudaStream_t s, int num_sms);
+// sorted u32 values for the host: byte deltas (255 = escaped absolute value) + a u32
+// head per src_chunk() entries
+int launch_pack_src(const std::uint32_t* src, std::uint64_t n, std::uint64_t vmax, std::uint8_t* out8,
+                    std::uint32_t* heads, void* esc, std::uint64_t cap, unsigned long long* n_esc, cudaStream_t s,
+                    int num_sms);
+std::uint64_t src_chunk();
 int launch_arcs_max_emit(const std::uint32_t* slot, std::uint64_t n2, std::uint32_t base2,
                          const std::uint64_t* off, std::uint32_t* asrc, std::uint32_t* adst,
                          std::uint64_t* amult, cudaStream_t s, int num_sms);

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "ctx.cuh"
+#include "host_decode.hpp"
 #include "kernels.cuh"
 #include "stages.cuh"
 
@@ -627,38 +628,64 @@ struct Sink {
         }
         return MSC3D_OK;
     }
-    // Multiplicities (the largest output: 8 bytes per arc, almost all < 255) cross the
-    // bus as one byte per arc plus an escape list (k_pack_mult) and are widened into
-    // the caller's u64 array by host threads -- a decode job per arc block, started
-    // as soon as the block is final and joined in finish().  An escape list larger
-    // than its buffer falls back to copying the u64 array.
+    // Narrow deliveries of the two arc arrays that compress: multiplicities (8 bytes
+    // per arc, almost all < 255) as their byte, sources (sorted) as byte deltas with a
+    // u32 head per chunk -- each with an (index, value) escape list (k_pack_mult /
+    // k_pack_src).  The bytes go first on the copy stream, the escapes right behind
+    // them (as many as the previous call of this block had, +25%, +64; the rest, if any, is
+    // fetched later), and a host job per array decodes into the caller's buffer with
+    // non-temporal stores, overlapping the block's remaining copies; finish() joins.
+    // An escape list larger than its buffer falls back to copying the full array.
     struct Job {
         std::thread th;
         int rc = MSC3D_OK;
         std::uint64_t bytes = 0;  // D2H bytes the job moved itself
+        std::string key;          // escape-count memo
+        std::uint64_t n_esc = 0;
     };
     std::vector<std::unique_ptr<Job>> jobs;
     int copy_mult(std::uint64_t* host, const std::uint64_t* dev, std::uint64_t n, const char* tag) {
         if (!out || !host || n == 0) return MSC3D_OK;
         if (!ctx->d2h_narrow) return copy(host, dev, n * 8);
-        const std::string t = tag;
+        return narrow(0, host, dev, n, std::string("mult_") + tag);
+    }
+    int copy_src(std::uint32_t* host, const std::uint32_t* dev, std::uint64_t n, const char* tag) {
+        if (!out || !host || n == 0) return MSC3D_OK;
+        if (!ctx->d2h_narrow) return copy(host, dev, n * 4);
+        return narrow(1, host, dev, n, std::string("src_") + tag);
+    }
+    // kind 0: u64 multiplicities -> widen; kind 1: sorted u32 -> prefix-decode per chunk
+    int narrow(int kind, void* host, const void* dev, std::uint64_t n, const std::string& t) {
         const std::uint64_t cap = ctx->d2h_escape_cap ? ctx->d2h_escape_cap : n / 16 + 1024;
-        auto* d8 = static_cast<std::uint8_t*>(ctx->ensure("d2h_mult8_" + t, n, 1));
-        void* desc = ctx->ensure("d2h_esc_" + t, cap, 16);
+        const std::uint64_t chunk = msc3d_dev::src_chunk();
+        const std::uint64_t nh = kind == 1 ? (n + chunk - 1) / chunk : 0;
+        auto* d8 = static_cast<std::uint8_t*>(ctx->ensure("d2h_b8_" + t, n, 1));
+        auto* desc = static_cast<ulonglong2*>(ctx->ensure("d2h_esc_" + t, cap, 16));
         auto* dcnt = static_cast<unsigned long long*>(ctx->ensure("d2h_nesc_" + t, 1, 8));
-        auto* h8 = static_cast<std::uint8_t*>(ctx->host_buf("mult8_" + t, n));
+        auto* dheads = static_cast<std::uint32_t*>(ctx->ensure("d2h_heads_" + t, nh + 1, 4));
+        auto* h8 = static_cast<std::uint8_t*>(ctx->host_buf("b8_" + t, n));
         auto* hcnt = static_cast<unsigned long long*>(ctx->host_buf("nesc_" + t, 8));
         auto* hesc = static_cast<ulonglong2*>(ctx->host_buf("esc_" + t, cap * 16));
-        if (!d8 || !desc || !dcnt || !h8 || !hcnt || !hesc) return MSC3D_ERR_NOMEM;
-        TRY(msc3d_dev::launch_pack_mult(dev, n, ctx->d2h_narrow_max, d8, desc, cap, dcnt, ctx->stream, ctx->num_sms));
+        auto* hheads = static_cast<std::uint32_t*>(ctx->host_buf("heads_" + t, (nh + 1) * 4));
+        if (!d8 || !desc || !dcnt || !dheads || !h8 || !hcnt || !hesc || !hheads) return MSC3D_ERR_NOMEM;
+        if (kind == 0)
+            TRY(msc3d_dev::launch_pack_mult(static_cast<const std::uint64_t*>(dev), n, ctx->d2h_narrow_max, d8, desc,
+                                            cap, dcnt, ctx->stream, ctx->num_sms));
+        else
+            TRY(msc3d_dev::launch_pack_src(static_cast<const std::uint32_t*>(dev), n, ctx->d2h_narrow_max, d8, dheads,
+                                           desc, cap, dcnt, ctx->stream, ctx->num_sms));
+        const std::uint64_t guess = std::min<std::uint64_t>(cap, ctx->d2h_esc_memo[t] * 5 / 4 + 64);
         TRY(copy(hcnt, dcnt, 8));
         TRY(copy(h8, d8, n));
+        if (nh) TRY(copy(hheads, dheads, nh * 4));
+        TRY(copy(hesc, desc, guess * 16));
         cudaEvent_t done;
         MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
         evs.push_back(done);
         MSC3D_CUDA_TRY(cudaEventRecord(done, cs));
         auto job = std::make_unique<Job>();
         Job* jp = job.get();
+        jp->key = t;
         const int device = ctx->device;
         const bool dg = diag;
         const auto t_sink = t_created;
@@ -671,7 +698,7 @@ struct Sink {
                 return fail(MSC3D_ERR_CUDA);
             const double t_ready = ms_since();
             const unsigned long long ne = *hcnt;
-            const bool fallback = ne > cap;  // escapes did not fit: the u64 array itself
+            jp->n_esc = ne;
             cudaStream_t js = nullptr;
             if (cudaStreamCreateWithFlags(&js, cudaStreamNonBlocking) != cudaSuccess) return fail(MSC3D_ERR_CUDA);
             auto fetch = [&](void* h, const void* d, std::uint64_t bytes) {
@@ -679,43 +706,57 @@ struct Sink {
                 if (e == cudaSuccess) e = cudaStreamSynchronize(js);
                 return e == cudaSuccess;
             };
-            if (fallback) {
-                const bool okf = fetch(host, dev, n * 8);
+            if (ne > cap) {  // escapes did not fit: the full array itself
+                const bool okf = fetch(host, dev, n * (kind == 0 ? 8 : 4));
                 cudaStreamDestroy(js);
-                jp->bytes = n * 8;
+                jp->bytes = n * (kind == 0 ? 8 : 4);
                 return okf ? void() : fail(MSC3D_ERR_CUDA);
             }
-            // widen the bytes into the u64 output on all host threads (overlapping the
-            // block's other copies, which occupy the copy engine), then fetch the
-            // escapes and patch them (~1% random stores, also split across threads:
-            // 3.6 M cache-missing stores cost ~18 ms on one thread at 512^3)
             const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
             const std::uint64_t T = n < (1ull << 20) ? 1 : std::min<std::uint64_t>(hw, 32);
-            auto widen = [&](std::uint64_t a, std::uint64_t b) {
-                for (std::uint64_t i = a; i < b; ++i) host[i] = h8[i];
-            };
-            auto patch = [&](std::uint64_t a, std::uint64_t b) {
-                for (std::uint64_t k = a; k < b; ++k) host[hesc[k].x] = hesc[k].y;
-            };
             auto team = [&](auto f, std::uint64_t m, std::uint64_t nt) {
                 std::vector<std::thread> ws;
                 for (std::uint64_t k = 1; k < nt; ++k) ws.emplace_back(f, m * k / nt, m * (k + 1) / nt);
                 f(0, m / nt);
                 for (auto& w : ws) w.join();
             };
-            team(widen, n, T);
-            const double t_w1 = ms_since();
-            const bool oke = ne == 0 || fetch(hesc, desc, ne * 16);
+            // escapes beyond the speculative prefix (a first call, or a growing count)
+            auto rest = [&]() { return ne <= guess || fetch(hesc + guess, desc + guess, (ne - guess) * 16); };
+            double t_w1 = 0, t_e = 0;
+            if (kind == 0) {
+                auto* h64 = static_cast<std::uint64_t*>(host);
+                // widen (no escape needed yet: it overlaps the block's other copies), then
+                // patch the escaped entries (~1% random stores, split across threads)
+                team([&](std::uint64_t a, std::uint64_t b) { msc3d_host::widen_u8_u64(h8, h64, a, b); }, n, T);
+                t_w1 = ms_since();
+                if (!rest()) return cudaStreamDestroy(js), fail(MSC3D_ERR_CUDA);
+                t_e = ms_since();
+                team([&](std::uint64_t a, std::uint64_t b) {
+                    for (std::uint64_t k = a; k < b; ++k) h64[hesc[k].x] = hesc[k].y;
+                }, ne, ne < (1ull << 16) ? 1 : T);
+            } else {
+                auto* h32 = static_cast<std::uint32_t*>(host);
+                if (!rest()) return cudaStreamDestroy(js), fail(MSC3D_ERR_CUDA);
+                t_e = ms_since();
+                // escaped (absolute) values first, then every chunk from its head
+                for (unsigned long long k = 0; k < ne; ++k) h32[hesc[k].x] = static_cast<std::uint32_t>(hesc[k].y);
+                const std::uint64_t nch = (n + chunk - 1) / chunk;
+                team([&](std::uint64_t c0, std::uint64_t c1) {
+                    for (std::uint64_t c = c0; c < c1; ++c) {
+                        const std::uint64_t a = c * chunk, b = std::min(n, a + chunk);
+                        msc3d_host::decode_steps(h8, hheads[c], h32, a, b);
+                    }
+                    _mm_sfence();
+                }, nch, std::min<std::uint64_t>(T, nch));
+                t_w1 = ms_since();
+            }
             cudaStreamDestroy(js);
-            if (!oke) return fail(MSC3D_ERR_CUDA);
-            jp->bytes = ne * 16;
-            const double t_e = ms_since();
-            team(patch, ne, ne < (1ull << 16) ? 1 : T);
+            jp->bytes = ne > guess ? (ne - guess) * 16 : 0;
             if (dg)
-                std::fprintf(stderr, "sink widen %s: %llu arcs, bytes in at %.2f ms, widened by %.2f (%llu threads), "
-                             "%llu escapes in by %.2f, patched by %.2f ms (host clock)\n", t.c_str(),
-                             static_cast<unsigned long long>(n), t_ready, t_w1, static_cast<unsigned long long>(T), ne,
-                             t_e, ms_since());
+                std::fprintf(stderr, "sink %s: %llu entries, bytes in at %.2f ms, escapes (%llu) by %.2f, decoded by "
+                             "%.2f, done %.2f ms (host clock, %llu threads)\n", t.c_str(),
+                             static_cast<unsigned long long>(n), t_ready, ne, t_e, t_w1, ms_since(),
+                             static_cast<unsigned long long>(T));
         });
         jobs.push_back(std::move(job));
         return MSC3D_OK;
@@ -726,6 +767,7 @@ struct Sink {
             if (j->th.joinable()) j->th.join();
             if (j->rc != MSC3D_OK && rc == MSC3D_OK) rc = j->rc;
             bytes_moved += j->bytes;
+            ctx->d2h_esc_memo[j->key] = j->n_esc;
         }
         jobs.clear();
         if (cs && cudaStreamSynchronize(cs) != cudaSuccess) rc = MSC3D_ERR_CUDA;
@@ -919,7 +961,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         if (host->arc_cap < na) return MSC3D_ERR_INVALID;
         // (the multiplicity bytes first: their host widening overlaps the other copies)
         TRY(sink.copy_mult(host->arc_mult, amin_mul, na, "A"));
-        TRY(sink.copy(host->arc_src, amin_src, na * 4));
+        TRY(sink.copy_src(host->arc_src, amin_src, na, "A"));
         TRY(sink.copy(host->arc_dst, amin_dst, na * 4));
     }
     clk.mark(4, s);  // (end of the untimed block: re-based below)
@@ -965,7 +1007,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         if (host) {  // the 2s->max block's host position is known now: send it before the 1s->2s block
             if (host->arc_cap < total) return MSC3D_ERR_INVALID;
             TRY(sink.copy_mult(host->arc_mult + na + nb, amax_mul, nc, "C"));
-            TRY(sink.copy(host->arc_src + na + nb, amax_src, nc * 4));
+            TRY(sink.copy_src(host->arc_src + na + nb, amax_src, nc, "C"));
             TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
         }
         o->one = asrc + na;
@@ -1001,7 +1043,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     if (host) {
         if (host->arc_cap < na + nb + nc) return MSC3D_ERR_INVALID;
         TRY(sink.copy_mult(host->arc_mult + na, amul + na, nb, "B"));
-        TRY(sink.copy(host->arc_src + na, asrc + na, nb * 4));
+        TRY(sink.copy_src(host->arc_src + na, asrc + na, nb, "B"));
         TRY(sink.copy(host->arc_dst + na, adst + na, nb * 4));
     }
     // device-side arc arrays complete: the min and max blocks around the 1s->2s block

@@ -199,7 +199,8 @@ def test_compute_repeatable(ctx, ref):
 
 
 @pytest.mark.parametrize("kind,narrow", [("gnoise", None), ("noise", None),
-                                         ("gnoise", {"d2h_narrow_max": 1}),  # escapes
+                                         ("gnoise", {"d2h_narrow_max": 1}),  # escapes (mult + src)
+                                         ("noise", {"d2h_narrow_max": 1, "d2h_escape_cap": 200}),
                                          ("noise", {"d2h_narrow_max": 0, "d2h_escape_cap": 3}),  # u64 fallback
                                          ("gnoise", {"d2h_narrow": 0})])  # u64 copies
 def test_compute_host_outputs(ref, kind, narrow):
@@ -227,11 +228,15 @@ def test_compute_host_outputs(ref, kind, narrow):
     for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
         np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype))
     np.testing.assert_array_equal(buf["cp_index"].astype(np.int32), want["cp_index"])
+    # a second delivery (the escape lists now ride with the bytes: sized by this one's)
+    for k in ("arc_src", "arc_mult"):
+        buf[k][:] = 0
+    assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == 0
+    for k in ("arc_src", "arc_dst", "arc_mult"):
+        np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype))
     full = ncp * 5 + na * 16 + (V + Cu) * 4
     if narrow and narrow.get("d2h_narrow") == 0:
         assert ctx.scalar("d2h_bytes") == full
-    elif narrow and "d2h_escape_cap" in narrow:
-        assert ctx.scalar("d2h_bytes") > full  # bytes + count, then the u64 arrays
     elif not narrow:
         assert ctx.scalar("d2h_bytes") < full - 6 * na
     # too small an arc buffer is rejected (invalid_argument)

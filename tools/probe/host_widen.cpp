@@ -10,6 +10,7 @@
 #include <vector>
 #include <sys/mman.h>
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 static double now() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 int main(int argc, char** argv) {
     const std::size_t n = argc > 1 ? std::atoll(argv[1]) : 285732712;
@@ -37,6 +38,38 @@ int main(int argc, char** argv) {
             });
         for (auto& th : ts) th.join();
         double t1 = now();
+        ts.clear();
+        // the same widen with non-temporal 16-byte stores (no read-for-ownership)
+        for (int t = 0; t < T; ++t)
+            ts.emplace_back([&, t] {
+                std::size_t a = n * t / T;
+                const std::size_t b = n * (t + 1) / T;
+                while (a < b && (reinterpret_cast<std::uintptr_t>(out64 + a) & 15)) { out64[a] = m8[a]; ++a; }
+                const __m128i z = _mm_setzero_si128();
+                for (; a + 16 <= b; a += 16) {
+                    const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&m8[a]));
+                    const __m128i w0 = _mm_unpacklo_epi8(v, z), w1 = _mm_unpackhi_epi8(v, z);
+                    const __m128i d0 = _mm_unpacklo_epi16(w0, z), d1 = _mm_unpackhi_epi16(w0, z);
+                    const __m128i d2 = _mm_unpacklo_epi16(w1, z), d3 = _mm_unpackhi_epi16(w1, z);
+                    __m128i* o = reinterpret_cast<__m128i*>(out64 + a);
+                    _mm_stream_si128(o + 0, _mm_unpacklo_epi32(d0, z));
+                    _mm_stream_si128(o + 1, _mm_unpackhi_epi32(d0, z));
+                    _mm_stream_si128(o + 2, _mm_unpacklo_epi32(d1, z));
+                    _mm_stream_si128(o + 3, _mm_unpackhi_epi32(d1, z));
+                    _mm_stream_si128(o + 4, _mm_unpacklo_epi32(d2, z));
+                    _mm_stream_si128(o + 5, _mm_unpackhi_epi32(d2, z));
+                    _mm_stream_si128(o + 6, _mm_unpacklo_epi32(d3, z));
+                    _mm_stream_si128(o + 7, _mm_unpackhi_epi32(d3, z));
+                }
+                for (; a < b; ++a) out64[a] = m8[a];
+                _mm_sfence();
+            });
+        for (auto& th : ts) th.join();
+        double t1b = now();
+        for (std::size_t i = 0; i < n; i += 997)
+            if (out64[i] != m8[i]) { std::printf("MISMATCH at %zu\n", i); break; }
+        std::printf("   nt-store widen %.1f ms (%.1f GB/s written)\n", (t1b - t1) * 1e3, n * 8 / (t1b - t1) / 1e9);
+        t1 = now();
         ts.clear();
         for (int t = 0; t < T; ++t)
             ts.emplace_back([&, t] {
