@@ -35,6 +35,7 @@ struct msc3d_ctx {
     // frontier size at which the counting kernel hands over to its tail configuration.
     bool force_wide = false;
     std::uint64_t kahn_switch_below = 1ull << 18;
+    bool kahn_async = true;  // "kahn_async": Kahn's tail without rounds (k_count_async); 0: rounds
     std::uint64_t exact_batch_rows = 0;  // "exact_batch_rows": batch of the exact A* overflow check
     std::uint64_t frontier_cap = 0;      // "frontier_cap": initial BFS frontier entries (0 = 4 x sources)
     bool term_rank_words = false;        // "term_rank_words": 2-saddle rank words on any grid

@@ -36,6 +36,7 @@
 // (1-saddle, 2-saddle, count) output.  Counts are exact u64 with sticky overflow.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1559,6 +1560,269 @@ __global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) 
     }
 }
 
+// ---------------------------------------------------------------------------------
+// counting, asynchronous tail: no rounds
+// ---------------------------------------------------------------------------------
+// Below the wide configuration's frontier threshold the rounds are latency-bound: each
+// costs a node's whole dependent chain (records, pool, merge, store, release) plus grid
+// barriers, ~50 us however few nodes it holds, for ~110 rounds.  The asynchronous tail
+// drops the rounds: a junction is merged as soon as its last child is, by the lane that
+// finished that child ("last child continues": the first parent it releases is its
+// next node) or, for further released parents, by whichever warp takes them from a
+// global queue.  Publication: P(u) is stored, then __threadfence(), then the parents'
+// counters are decremented; a lane that takes a node (its own release, or a queue slot)
+// fences before reading the children's records.  The queue is the frontier buffer the
+// wide configuration stopped with: slots [0, ncur) hold its frontier, later slots are
+// reserved by atomicAdd on the tail and written as node + 1 (0 = not yet written:
+// zeroed at start); an idle lane claims the next slot by atomicAdd on the head and
+// takes it once it is filled, while its warp goes on with the other lanes' work.
+// It ends when every remaining junction is done; if none is left to take while some are
+// still pending for 50 ms (a cycle: the host's count check reports it), warps give up.
+// Idle warps back off exponentially (64 ns .. 8 us) between polls of the counters.
+struct AsyncQ {
+    std::uint32_t* q;
+    unsigned long long* head;
+    unsigned long long* tail;
+    unsigned long long* done;  // junctions finished by this kernel
+    unsigned long long total;  // junctions this kernel must finish
+};
+
+__device__ __forceinline__ void async_push(const AsyncQ& Q, std::uint32_t node, bool want) {
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned long long at = 0;
+    if (lane == leader) at = atomicAdd(Q.tail, static_cast<unsigned long long>(__popc(m)));
+    at = __shfl_sync(0xffffffffu, at, leader) + __popc(m & ((1u << lane) - 1u));
+    if (want) atomicExch(&Q.q[at], node + 1u);  // (an L2 write the spinning reader sees)
+}
+
+// Release the parents of this lane's finished junction (P(u) already published):
+// the first one that becomes ready is the lane's next node (carry), the others go to
+// the queue.  All lanes call (rn = 0 for lanes without a junction).
+__device__ __forceinline__ void release_async(const CountArgs& a, const AsyncQ& Q, std::uint32_t rn, std::uint64_t ov,
+                                              const uint4 par0, const uint4 par1, std::uint32_t& carry) {
+    const std::uint32_t inl[kInlineParents] = {par0.x, par0.y, par0.z, par0.w, par1.x, par1.y, par1.z, par1.w};
+    std::uint32_t k0 = 0;
+    for (;;) {
+        std::uint32_t p[4], old[4];
+        const std::uint32_t m = rn - k0 < 4 ? rn - k0 : 4u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            p[k] = kNone;
+            if (k < static_cast<int>(m)) {
+                const std::uint32_t q = k0 + k;
+                if (q < static_cast<std::uint32_t>(kInlineParents)) {
+#pragma unroll
+                    for (int z = 0; z < kInlineParents; ++z)
+                        if (static_cast<std::uint32_t>(z) == q) p[k] = inl[z];
+                } else {
+                    p[k] = a.rsrc[ov + q - kInlineParents];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
+        k0 += m;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool ready = p[k] != kNone && old[k] == 1u;
+            const bool keep = ready && carry == kNone;
+            if (keep) carry = p[k];
+            async_push(Q, p[k], ready && !keep);
+        }
+        if (!__any_sync(0xffffffffu, k0 < rn)) break;
+    }
+}
+
+// One warp iteration of the asynchronous tail: lane `valid` holds junction u.  Light
+// nodes merge per lane from the warp's staging buffer, heavy ones (> kHeavy inputs)
+// by the whole warp right after; then the warp publishes and releases.  All lanes call.
+__device__ __forceinline__ void count_iter_async(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch, bool valid,
+                                                 std::uint32_t u, const AsyncQ& Q, std::uint32_t& carry,
+                                                 unsigned long long& done) {
+    const int lane = threadIdx.x & 31;
+    Inputs in;
+    bool ovf = false;
+    std::uint32_t T = 0, S = 0, npar = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) in.len[b] = 0;
+    uint4 par0 = make_uint4(0u, 0u, 0u, 0u), par1 = par0;
+    if (valid) {
+        const uint4* nr = reinterpret_cast<const uint4*>(a.node + u);
+        const uint4 d4 = __ldcg(&a.dest[u]);
+        npar = a.indeg[u];
+        par0 = nr[0];
+        par1 = nr[1];
+        gather<true>(d4, a.rec, in, &a.flags[3]);
+        T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
+        S = staged_size(in);
+    }
+    const bool heavy = valid && T > kHeavy && S + T <= wb.cap;
+    const bool light = valid && !heavy;
+    const bool pooled = light && T > 2;
+    const std::uint64_t off = pool_alloc(a.pool, ch, pooled ? T : 0u, &a.flags[1]);
+    std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
+    std::uint64_t* oc = a.pool.cnt + (off == kBadOff ? 0 : off);
+    JRec r;
+    r.k0 = r.k1 = 0;
+    r.c0 = r.c1 = 0;
+    auto emit = [&](std::uint32_t o, std::uint32_t k, std::uint64_t c) {
+        if (pooled) {
+            if (off != kBadOff) {
+                ok[o] = k;
+                oc[o] = c;
+            }
+        } else if (o == 0) {
+            r.k0 = k;
+            r.c0 = c;
+        } else {
+            r.k1 = k;
+            r.c1 = c;
+        }
+    };
+    auto finish = [&](std::uint32_t len) {
+        if (pooled) store_rec(a.rec, u, len, 1u | zword(in.z), 0u, 0u, off, 0ull);
+        else store_rec(a.rec, u, len, zword(len == 0 ? __fadd_ru(in.z, 1.0f) : in.z), r.k0, r.k1, r.c0, r.c1);
+    };
+    if (light && S > wb.cap) finish(merge<true>(in, a.pool, &ovf, emit));
+    __syncwarp();
+    unsigned todo = __ballot_sync(0xffffffffu, light && S <= wb.cap);
+    while (todo) {
+        const bool mine = (todo >> lane) & 1u;
+        std::uint32_t total = 0;
+        const std::uint32_t base = warp_excl_scan(mine ? S : 0u, &total);
+        const bool go = mine && base + S <= wb.cap;
+        if (go) stage<true>(in, a.pool, wb, base);
+        cp_async_wait_all();
+        __syncwarp();
+        if (go) finish(merge_staged<true>(in, wb, base, &ovf, emit));
+        __syncwarp();
+        todo &= ~__ballot_sync(0xffffffffu, go);
+    }
+    if (ovf) a.flags[0] = 1u;
+    unsigned long long dummy = 0;
+    for (unsigned hm = __ballot_sync(0xffffffffu, heavy); hm; hm &= hm - 1) {
+        const std::uint32_t uh = __shfl_sync(0xffffffffu, u, __ffs(hm) - 1);
+        count_heavy(a, wb, wq, ch, uh, nullptr, nullptr, dummy);
+    }
+    // publish every P(u) of the warp, then release the parents
+    __threadfence();
+    __syncwarp();
+    const std::uint32_t rn = valid ? npar : 0u;
+    release_async(a, Q, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, par0, par1, carry);
+    done += static_cast<unsigned long long>(__popc(__ballot_sync(0xffffffffu, valid)));  // (warp-uniform)
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsigned long long* qctl,
+                                                             const unsigned long long* n_skip,
+                                                             const unsigned long long* n_predone) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const WarpBuf wb = warp_buf(s_dyn, kWarpCap);
+    __shared__ WarpQ s_q[kThreads / 32];
+    __shared__ PoolChunk s_ch[kThreads / 32];
+    WarpQ& wq = s_q[threadIdx.x >> 5];
+    PoolChunk& ch = s_ch[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        wq.n = 0;
+        ch.base = 0;
+        ch.left = 0;
+    }
+    __syncwarp();
+    cg::grid_group grid = cg::this_grid();
+    // state left by the wide configuration
+    const unsigned long long ncur = a.resume[1];
+    std::uint32_t* q = a.resume[2] ? a.fb : a.fa;
+    const unsigned long long before = *reinterpret_cast<volatile unsigned long long*>(a.done);
+    const unsigned long long total = a.nj - *n_skip - *n_predone - before;
+    AsyncQ Q{q, qctl, qctl + 16, qctl + 32, total};  // (one 128-byte line each)
+    for (std::uint64_t i = ncur + grid.thread_rank(); i < total; i += grid.size()) q[i] = 0u;
+    for (std::uint64_t i = grid.thread_rank(); i < ncur; i += grid.size()) q[i] += 1u;  // node + 1
+    if (grid.thread_rank() == 0) {
+        qctl[0] = 0;
+        qctl[16] = ncur;
+        qctl[32] = 0;
+        qctl[40] = 0;
+        qctl[41] = gtimer();
+    }
+    grid.sync();
+    unsigned long long done = 0, flushed = 0;
+    std::uint32_t carry = kNone;
+    unsigned long long slot = ~0ull;  // this lane's claimed queue slot, not yet filled
+    bool drained = false;             // the queue's last slot is taken: carries only
+    unsigned sleep_ns = 64;  // idle back-off (thousands of idle warps must not saturate
+                             // the L2 slice that holds the queue counters)
+    unsigned long long last_seen = ~0ull, last_change = 0;
+    for (;;) {
+        bool has = carry != kNone;
+        std::uint32_t u = carry;
+        carry = kNone;
+        // lanes without work and without a claim take the next slots (atomicAdd: no
+        // compare-and-swap retries under contention; a slot beyond the tail is simply
+        // filled later -- or never, at the end)
+        const unsigned need = __ballot_sync(0xffffffffu, !has && slot == ~0ull && !drained);
+        if (need) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(Q.head, static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if ((need >> lane) & 1u) {
+                slot = base + __popc(need & ((1u << lane) - 1u));
+                if (slot >= Q.total) {  // every node passes through at most one slot
+                    slot = ~0ull;
+                    drained = true;
+                }
+            }
+        }
+        if (!has && slot != ~0ull) {  // a filled slot (checked once per iteration)
+            const std::uint32_t v = __ldcg(&Q.q[slot]);
+            if (v) {
+                u = v - 1u;
+                has = true;
+                slot = ~0ull;
+            }
+        }
+        if (!__any_sync(0xffffffffu, has)) {
+            // nothing to do: publish this warp's count, then either all is done or wait
+            if (lane == 0 && done != flushed) {
+                atomicAdd(Q.done, done - flushed);
+                flushed = done;
+            }
+            unsigned long long d = 0;
+            if (lane == 0) d = *reinterpret_cast<volatile unsigned long long*>(Q.done);
+            d = __shfl_sync(0xffffffffu, d, 0);
+            if (d >= Q.total) break;
+            const unsigned long long now = gtimer();
+            if (d != last_seen) {
+                last_seen = d;
+                last_change = now;
+            } else if (now - last_change > 50000000ull) {  // 50 ms without progress: a cycle
+                if (lane == 0) atomicAdd(qctl + 40, 1ull);  // (diagnostic: warps that gave up)
+                break;
+            }
+            __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns < 8192 ? 2 * sleep_ns : 8192;
+            continue;
+        }
+        sleep_ns = 64;
+        __threadfence();  // the children's records of the nodes just taken
+        __syncwarp();
+        count_iter_async(a, wb, wq, ch, has, u, Q, carry, done);
+        if (lane == 0 && done - flushed >= 256) {  // (the count drives termination)
+            atomicAdd(Q.done, done - flushed);
+            flushed = done;
+        }
+    }
+    if (lane == 0 && done != flushed) atomicAdd(Q.done, done - flushed);
+    grid.sync();
+    if (grid.thread_rank() == 0) {
+        atomicAdd(a.done, *reinterpret_cast<volatile unsigned long long*>(Q.done));
+        qctl[42] = gtimer();
+        qctl[43] = total;
+        qctl[44] = ncur;
+    }
+}
+
 // The sorted (1-saddle, 2-saddle, count) output.  Light 1-saddles are merged per
 // thread; heavy ones (> kHeavy input entries) are queued for k_count_write_heavy,
 // one warp per 1-saddle, like the heavy junctions of k_count.
@@ -1905,6 +2169,19 @@ int launch_count(const CountLaunch& L, cudaStream_t s, int num_sms) {
     if (rc != MSC3D_OK) return rc;
     void* args[] = {&a};
     MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(kw, dim3(grid), dim3(kThreads), args, smem_w, s));
+    if (L.async_tail) {  // the tail without rounds
+        const void* ka = reinterpret_cast<const void*>(k_count_async);
+        MSC3D_CUDA_TRY(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_d)));
+        rc = coop_blocks(ka, num_sms, &grid, smem_d);
+        if (rc != MSC3D_OK) return rc;
+        unsigned long long* qctl = L.qctl;
+        const unsigned long long* nsk = L.n_skip;
+        const unsigned long long* npd = L.n_predone;
+        void* aargs[] = {&a, &qctl, &nsk, &npd};
+        MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(ka, dim3(grid), dim3(kThreads), aargs, smem_d, s));
+        count_launch(2);
+        return MSC3D_OK;
+    }
     rc = coop_blocks(kd, num_sms, &grid, smem_d);
     if (rc != MSC3D_OK) return rc;
     MSC3D_CUDA_TRY(cudaLaunchCooperativeKernel(kd, dim3(grid), dim3(kThreads), args, smem_d, s));

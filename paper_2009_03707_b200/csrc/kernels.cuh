@@ -205,6 +205,10 @@ struct CountLaunch {
     const std::uint32_t* indeg;     // parents per junction
     const std::uint64_t* ovoff;     // overflow-list offsets
     unsigned long long switch_below;  // frontier size below which the tail configuration runs
+    bool async_tail = false;          // the tail without rounds (k_count_async)
+    const unsigned long long* n_skip = nullptr;     // contracted junctions (async tail's total)
+    const unsigned long long* n_predone = nullptr;  // junctions finished by the walks
+    unsigned long long* qctl = nullptr;  // async tail: head / tail / done, 128 bytes apart (48 words)
 };
 int count_rec_bytes();
 int count_arenas();

@@ -486,6 +486,11 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.indeg = indeg;
         L.ovoff = ovoff;
         L.switch_below = ctx->kahn_switch_below;
+        L.async_tail = ctx->kahn_async;
+        L.qctl = static_cast<unsigned long long*>(ctx->ensure("kahn_qctl", 48, 8));
+        if (!L.qctl) return MSC3D_ERR_NOMEM;
+        L.n_skip = n_skip;
+        L.n_predone = n_predone;
         L.ready = ready;
         L.n_ready = n_ready;
         if (!L.heavy_q) return MSC3D_ERR_NOMEM;

@@ -149,13 +149,17 @@ def test_wide_ids_stages_equal_reference(wide_ctx, ref, kind, dims, seed):
     np.testing.assert_array_equal(wide_ctx.get("ss_paths"), p)
 
 
+@pytest.mark.parametrize("kahn_async", [1, 0])
 @pytest.mark.parametrize("switch_below", [1, 64, 1 << 40])
 @pytest.mark.parametrize("kind,dims", [("gnoise", (48, 48, 48)), ("noise", (64, 64, 64)),
                                        ("gauss", (64, 64, 64))])
-def test_kahn_switch_threshold(ref, switch_below, kind, dims):
+def test_kahn_switch_threshold(ref, switch_below, kind, dims, kahn_async):
+    """The counting kernel's hand-off from its wide rounds to the tail -- the
+    asynchronous tail (default) or the round-based one -- at every threshold."""
     v = m.synth(kind, dims)
     with m.Context(0) as c:
         c.set_option("kahn_switch_below", switch_below)
+        c.set_option("kahn_async", kahn_async)
         got = m.compute(v, dims, with_segmentation=False, ctx=c)
     want = ref.compute(v.astype(np.float64), dims, with_segmentation=False)
     for k in ("arc_src", "arc_dst", "arc_mult"):

@@ -1,0 +1,16 @@
+"""Development: counters of the asynchronous Kahn tail ("kahn_qctl") after one compute()."""
+import sys
+import numpy as np
+sys.path.insert(0, "/root/repo")
+import paper_2009_03707_b200 as m
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+dims = (n, n, n)
+c = m.Context(0)
+c.set_option("kahn_async", 1)
+c.load_values(m.synth("gnoise", dims), dims)
+for i in range(2):
+    ms = c.compute(m.OPT_SEGMENTATION)
+    q = c.get("kahn_qctl", np.uint64)
+    print(f"run {i}: counting {ms[4]:.2f} ms; async kernel {(int(q[42]) - int(q[41])) / 1e3:.1f} us, "
+          f"total {int(q[43])} hand-off {int(q[44])} pushed {int(q[16]) - int(q[44])} head {int(q[0])} done {int(q[32])} "
+          f"gave-up warps {int(q[40])}", flush=True)
