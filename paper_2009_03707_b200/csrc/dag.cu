@@ -1745,6 +1745,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
         qctl[32] = 0;
         qctl[40] = 0;
         qctl[41] = gtimer();
+        qctl[45] = 0;
+        qctl[46] = 0;
     }
     grid.sync();
     unsigned long long done = 0, flushed = 0;
@@ -1807,6 +1809,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
         sleep_ns = 64;
         __threadfence();  // the children's records of the nodes just taken
         __syncwarp();
+        if (a.diag) {  // development: warp iterations, lanes with a node, lanes from carries
+            const unsigned hb = __ballot_sync(0xffffffffu, has);
+            if (lane == 0) {
+                atomicAdd(qctl + 45, 1ull);
+                atomicAdd(qctl + 46, static_cast<unsigned long long>(__popc(hb)));
+            }
+        }
         count_iter_async(a, wb, wq, ch, has, u, Q, carry, done);
         if (lane == 0 && done - flushed >= 256) {  // (the count drives termination)
             atomicAdd(Q.done, done - flushed);

@@ -1,6 +1,8 @@
 """Development: counters of the asynchronous Kahn tail ("kahn_qctl") after one compute()."""
+import os
 import sys
 import numpy as np
+os.environ.setdefault("MSC3D_DIAG", "1")
 sys.path.insert(0, "/root/repo")
 import paper_2009_03707_b200 as m
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
@@ -13,4 +15,5 @@ for i in range(2):
     q = c.get("kahn_qctl", np.uint64)
     print(f"run {i}: counting {ms[4]:.2f} ms; async kernel {(int(q[42]) - int(q[41])) / 1e3:.1f} us, "
           f"total {int(q[43])} hand-off {int(q[44])} pushed {int(q[16]) - int(q[44])} head {int(q[0])} done {int(q[32])} "
-          f"gave-up warps {int(q[40])}", flush=True)
+          f"gave-up warps {int(q[40])}; warp iterations {int(q[45])}, lanes busy per iteration "
+          f"{int(q[46]) / max(1, int(q[45])):.1f}", flush=True)
