@@ -29,7 +29,7 @@ for r in rows:
         a, b = int(r[ii] or 0), int(r[ti] or 0)
     except ValueError:
         continue
-    key = (fname, int(r[0]))
+    key = (r[1].strip()[:90], int(r[0]))  # (several files share line numbers: key by text too)
     inst[kern][key] += a
     thr[kern][key] += b
     src[key] = r[1].strip()[:90]
@@ -38,4 +38,4 @@ for k in seen_kernels:
     ttot = sum(thr[k].values())
     print(f"== {k}: warp inst {tot:.3e}, thread inst {ttot:.3e}, avg threads {ttot / tot:.1f}")
     for key, v in inst[k].most_common(top):
-        print(f"{v:11d} {100 * v / tot:5.1f}% {thr[k][key] / max(v, 1):5.1f}thr {key[0]}:{key[1]:<5d} {src[key]}")
+        print(f"{v:11d} {100 * v / tot:5.1f}% {thr[k][key] / max(v, 1):5.1f}thr line {key[1]:<5d} {src[key]}")
