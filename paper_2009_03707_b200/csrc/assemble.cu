@@ -171,11 +171,10 @@ __device__ void block_bitonic(std::uint64_t* s, int n_pow2) {
     }
 }
 
-__global__ void k_sort_large_buckets(const std::uint64_t* __restrict__ off, std::uint64_t nb,
-                                     std::uint64_t total, const std::uint32_t* __restrict__ large,
-                                     std::uint64_t* __restrict__ key, std::uint64_t* __restrict__ scratch) {
-    __shared__ std::uint64_t s[kChunk];
-    const std::uint32_t m = large[blockIdx.x];
+// One large bucket m, by the whole block (s: kChunk shared words).
+__device__ __forceinline__ void sort_large_one(const std::uint64_t* __restrict__ off, std::uint64_t nb,
+                                               std::uint64_t total, std::uint32_t m, std::uint64_t* __restrict__ key,
+                                               std::uint64_t* __restrict__ scratch, std::uint64_t* s) {
     const std::uint64_t b = off[m], e = m + 1 < nb ? off[m + 1] : total;
     const std::uint64_t n = e - b;
     // 1) sort chunks
@@ -227,6 +226,24 @@ __global__ void k_sort_large_buckets(const std::uint64_t* __restrict__ off, std:
     }
     if (src != key + b)
         for (std::uint64_t i = threadIdx.x; i < n; i += blockDim.x) key[b + i] = src[i];
+    __syncthreads();
+}
+
+__global__ void k_sort_large_buckets(const std::uint64_t* __restrict__ off, std::uint64_t nb,
+                                     std::uint64_t total, const std::uint32_t* __restrict__ large,
+                                     std::uint64_t* __restrict__ key, std::uint64_t* __restrict__ scratch) {
+    __shared__ std::uint64_t s[kChunk];
+    sort_large_one(off, nb, total, large[blockIdx.x], key, scratch, s);
+}
+
+// The same with the number of large buckets read on the device (no host round trip):
+// blocks take buckets large[blockIdx.x + k * gridDim.x].
+__global__ void k_sort_large_loop(const std::uint64_t* __restrict__ off, std::uint64_t nb, std::uint64_t total,
+                                  const std::uint32_t* __restrict__ large, const unsigned long long* __restrict__ n_large,
+                                  std::uint64_t* __restrict__ key, std::uint64_t* __restrict__ scratch) {
+    __shared__ std::uint64_t s[kChunk];
+    const unsigned long long nl = *n_large;
+    for (unsigned long long k = blockIdx.x; k < nl; k += gridDim.x) sort_large_one(off, nb, total, large[k], key, scratch, s);
 }
 
 // Block A arcs out of the sorted buckets, one arc per thread: dst = saddle id, mult.
@@ -470,18 +487,11 @@ int launch_arcs_min_sort(const std::uint32_t* slot_min, std::uint64_t n1, std::u
     k_sort_small_buckets<<<grid_for(n0, num_sms), kThreads, 0, s>>>(off, n0, total, key, large, n_large);
     count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
-    {  // kernel copy into the mapped host mirror (a DMA would queue behind bulk copies)
-        std::uint64_t* hd = nullptr;
-        MSC3D_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd), h_small, 0));
-        const int rc = launch_small_copy(reinterpret_cast<const std::uint64_t*>(n_large), hd, 1, s);
-        if (rc != MSC3D_OK) return rc;
-    }
-    MSC3D_CUDA_TRY(cudaStreamSynchronize(s));
-    const std::uint64_t nl = h_small[0];
-    if (nl) {
-        k_sort_large_buckets<<<static_cast<unsigned>(nl), 512, 0, s>>>(off, n0, total, large, key, scratch);
-        count_launch();
-    }
+    // large buckets: their count stays on the device (no host round trip: this chain runs
+    // on a side stream beside the saddle stages)
+    (void)h_small;
+    k_sort_large_loop<<<static_cast<unsigned>(2 * num_sms), 512, 0, s>>>(off, n0, total, large, n_large, key, scratch);
+    count_launch();
     k_arcs_min_emit<<<grid_for(total, num_sms), kThreads, 0, s>>>(total, key, adst, amult);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());

@@ -238,6 +238,14 @@ int msc3d_ctx_scalar(msc3d_ctx* ctx, const char* name, std::int64_t* value) {
         *value = static_cast<std::int64_t>(ctx->peak_held);
         return MSC3D_OK;
     }
+    if (!std::strcmp(name, "host_syncs")) {  // host round trips since the context was created
+        *value = static_cast<std::int64_t>(ctx->n_fetch);
+        return MSC3D_OK;
+    }
+    if (!std::strcmp(name, "host_sync_us")) {  // host time spent waiting in them
+        *value = static_cast<std::int64_t>(ctx->fetch_us);
+        return MSC3D_OK;
+    }
     auto it = ctx->scalars.find(name);
     if (it == ctx->scalars.end()) return MSC3D_ERR_STATE;
     *value = it->second;

@@ -3,6 +3,7 @@
 // the same grid allocates nothing.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -79,6 +80,11 @@ struct msc3d_ctx {
         if (!copy && cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking) != cudaSuccess) copy = nullptr;
         return copy;
     }
+    cudaStream_t side = nullptr;  // assembly kernels beside the saddle stages
+    cudaStream_t side_stream() {
+        if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) side = nullptr;
+        return side;
+    }
     cudaStream_t h2d_stream() {
         if (!h2d && cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess) h2d = nullptr;
         return h2d;
@@ -94,6 +100,7 @@ struct msc3d_ctx {
         if (own_stream && stream) cudaStreamDestroy(stream);
         if (copy) cudaStreamDestroy(copy);
         if (h2d) cudaStreamDestroy(h2d);
+        if (side) cudaStreamDestroy(side);
     }
 
     // Ensure array `name` holds `count` elements of `elem` bytes; contents undefined.
@@ -170,10 +177,15 @@ struct msc3d_ctx {
     // kernel writing the mapped host mirror over the bus, not a DMA: a DMA would
     // queue behind bulk device-to-host output copies on the copy engine.
     int fetch_small(int n) { return fetch_range(0, n); }
+    std::uint64_t n_fetch = 0;  // host round trips (development counters: scalars "host_syncs", "host_sync_us")
+    double fetch_us = 0;
     int fetch_range(int first, int n) {
         if (msc3d_dev::launch_small_copy(d_small + first, h_small_dev + first, n, stream) != MSC3D_OK)
             return MSC3D_ERR_CUDA;
+        const auto t0 = std::chrono::steady_clock::now();
         if (cudaStreamSynchronize(stream) != cudaSuccess) return MSC3D_ERR_CUDA;
+        ++n_fetch;
+        fetch_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
         return MSC3D_OK;
     }
 };

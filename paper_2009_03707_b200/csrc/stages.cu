@@ -601,6 +601,8 @@ struct Sink {
     cudaStream_t cs = nullptr;
     std::vector<cudaEvent_t> evs;
     std::uint64_t bytes_moved = 0;  // D2H bytes of this delivery
+    cudaStream_t producer = nullptr;  // stream that produced the arrays being copied (null: ctx->stream)
+    cudaStream_t prod() const { return producer ? producer : ctx->stream; }
     std::chrono::steady_clock::time_point t_created = std::chrono::steady_clock::now();
     bool ok() const { return out != nullptr; }
     // development timeline (MSC3D_DIAG): [t0 on the compute stream, per copy: ready, start, end]
@@ -615,7 +617,7 @@ struct Sink {
         cudaEvent_t ev;
         MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&ev, diag ? cudaEventDefault : cudaEventDisableTiming));
         evs.push_back(ev);
-        MSC3D_CUDA_TRY(cudaEventRecord(ev, ctx->stream));
+        MSC3D_CUDA_TRY(cudaEventRecord(ev, prod()));
         MSC3D_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
         cudaEvent_t a = nullptr, b = nullptr;
         if (diag) {
@@ -675,10 +677,10 @@ struct Sink {
         if (!d8 || !desc || !dcnt || !dheads || !h8 || !hcnt || !hesc || !hheads) return MSC3D_ERR_NOMEM;
         if (kind == 0)
             TRY(msc3d_dev::launch_pack_mult(static_cast<const std::uint64_t*>(dev), n, ctx->d2h_narrow_max, d8, desc,
-                                            cap, dcnt, ctx->stream, ctx->num_sms));
+                                            cap, dcnt, prod(), ctx->num_sms));
         else
             TRY(msc3d_dev::launch_pack_src(static_cast<const std::uint32_t*>(dev), n, ctx->d2h_narrow_max, d8, dheads,
-                                           desc, cap, dcnt, ctx->stream, ctx->num_sms));
+                                           desc, cap, dcnt, prod(), ctx->num_sms));
         const std::uint64_t guess = std::min<std::uint64_t>(cap, ctx->d2h_esc_memo[t] * 5 / 4 + 64);
         TRY(copy(hcnt, dcnt, 8));
         TRY(copy(h8, d8, n));
@@ -927,11 +929,38 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     if (!cp_cell || !cp_index || !amin_src || !amin_dst || !amin_mul || !amax_src || !amax_dst || !amax_mul || !key ||
         !scratch || !cursor || !large)
         return MSC3D_ERR_NOMEM;
+    // The assembly of the extremum-side outputs (critical point list, label volumes,
+    // sorted min->1s and 2s->max arcs: ~3 ms of small bandwidth-bound kernels, no host
+    // round trips) runs on a side stream, beside the latency-bound saddle stages; the
+    // main stream waits for it before it touches those arrays (Join, at every exit).
+    // (Grids above 2^32 cells free scratch mid-way: they keep one stream.)
+    static const bool no_side = std::getenv("MSC3D_NO_SIDE_STREAM") != nullptr;  // (A/B)
+    const cudaStream_t sa = ctx->release_transients() || no_side ? s : ctx->side_stream();
+    if (!sa) return MSC3D_ERR_CUDA;
+    struct Join {
+        cudaStream_t main, side;
+        cudaEvent_t ev = nullptr;
+        ~Join() {
+            if (!ev) return;
+            cudaEventRecord(ev, side);
+            cudaStreamWaitEvent(main, ev, 0);
+            cudaEventDestroy(ev);
+        }
+    } join{s, sa};
+    if (sa != s) {
+        cudaEvent_t fork;
+        MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        MSC3D_CUDA_TRY(cudaEventRecord(fork, s));
+        MSC3D_CUDA_TRY(cudaStreamWaitEvent(sa, fork, 0));
+        cudaEventDestroy(fork);
+        MSC3D_CUDA_TRY(cudaEventCreateWithFlags(&join.ev, cudaEventDisableTiming));
+    }
+    sink.producer = sa;
     std::uint64_t at = 0;
     for (int k = 0; k < 4; ++k) {
         const std::string nm = "crit" + std::to_string(k);
         const std::uint64_t n = ctx->count(nm);
-        TRY(msc3d_dev::launch_cp_concat(ctx->ptr<void>(nm), n, at, k, w, cp_cell, cp_index, s, sms));
+        TRY(msc3d_dev::launch_cp_concat(ctx->ptr<void>(nm), n, at, k, w, cp_cell, cp_index, sa, sms));
         at += n;
     }
     if (host) {
@@ -943,8 +972,8 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         auto* lmin = static_cast<std::uint32_t*>(ctx->ensure("labels_min", d.n_verts, 4));
         auto* lmax = static_cast<std::uint32_t*>(ctx->ensure("labels_max", d.n_cubes, 4));
         if (!lmin || (!lmax && d.n_cubes)) return MSC3D_ERR_NOMEM;
-        TRY(msc3d_dev::launch_gather(label0, remap0, d.n_verts, lmin, s, sms));
-        TRY(msc3d_dev::launch_gather(label3, remap3, d.n_cubes, lmax, s, sms));
+        TRY(msc3d_dev::launch_gather(label0, remap0, d.n_verts, lmin, sa, sms));
+        TRY(msc3d_dev::launch_gather(label3, remap3, d.n_cubes, lmax, sa, sms));
         if (host) {
             TRY(sink.copy(host->labels_min, lmin, d.n_verts * 4));
             TRY(sink.copy(host->labels_max, lmax, d.n_cubes * 4));
@@ -955,8 +984,8 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     }
     TRY(msc3d_dev::launch_arcs_min_sort(slot_min, c1, base1, min_off, c0, na, cursor, key, scratch, large,
                                         reinterpret_cast<unsigned long long*>(ctx->d_small + 35),
-                                        ctx->h_small + 35, amin_src, amin_dst, amin_mul, s, sms));
-    TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, amax_src, amax_dst, amax_mul, s, sms));
+                                        ctx->h_small + 35, amin_src, amin_dst, amin_mul, sa, sms));
+    TRY(msc3d_dev::launch_arcs_max_emit(slot_max, c2, base2, off_max, amax_src, amax_dst, amax_mul, sa, sms));
     if (ctx->release_transients())
         for (const char* t : {"slot_min", "per_min", "min_off", "slot_max", "cnt_max", "off_max", "sort_key",
                               "sort_scratch", "sort_cursor", "sort_large", "rank_bits", "rank_cnt", "rank_pre",
@@ -969,6 +998,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         TRY(sink.copy_src(host->arc_src, amin_src, na, "A"));
         TRY(sink.copy(host->arc_dst, amin_dst, na * 4));
     }
+    sink.producer = nullptr;
     clk.mark(4, s);  // (end of the untimed block: re-based below)
 
     // [reachability]
@@ -1011,9 +1041,11 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         if (!asrc || !adst || !amul) return MSC3D_ERR_NOMEM;
         if (host) {  // the 2s->max block's host position is known now: send it before the 1s->2s block
             if (host->arc_cap < total) return MSC3D_ERR_INVALID;
+            sink.producer = sa;  // (produced on the side stream)
             TRY(sink.copy_mult(host->arc_mult + na + nb, amax_mul, nc, "C"));
             TRY(sink.copy_src(host->arc_src + na + nb, amax_src, nc, "C"));
             TRY(sink.copy(host->arc_dst + na + nb, amax_dst, nc * 4));
+            sink.producer = nullptr;
         }
         o->one = asrc + na;
         o->two = adst + na;
@@ -1052,6 +1084,10 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         TRY(sink.copy(host->arc_dst + na, adst + na, nb * 4));
     }
     // device-side arc arrays complete: the min and max blocks around the 1s->2s block
+    if (join.ev) {  // (the side stream's arrays: wait for them here already)
+        MSC3D_CUDA_TRY(cudaEventRecord(join.ev, sa));
+        MSC3D_CUDA_TRY(cudaStreamWaitEvent(s, join.ev, 0));
+    }
     if (na) {
         MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc, amin_src, na * 4, cudaMemcpyDeviceToDevice, s));
         MSC3D_CUDA_TRY(cudaMemcpyAsync(adst, amin_dst, na * 4, cudaMemcpyDeviceToDevice, s));
