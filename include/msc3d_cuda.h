@@ -91,6 +91,8 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
  *                             (0 = as many as 2 GiB of dense rows hold);
  *   "kahn_switch_below" (>=1) frontier size at which path counting leaves its wide
  *                             launch configuration for the tail one (default 2^18);
+ *   "side_stream" (0/1)       assemble the extremum-side outputs on a second stream,
+ *                             beside the saddle stages (default 0);
  *   "kahn_async" (0/1)        path counting's tail without rounds (default 1; 0: the
  *                             round-based tail configuration);
  *   "frontier_cap" (>=0)      initial entries of the BFS frontier buffers (0 = 4 x the

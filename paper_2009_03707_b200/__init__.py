@@ -228,7 +228,7 @@ class Context:
 
     def set_option(self, name, value):
         """msc3d_ctx_set_option: "wide_ids" (64-bit id lists on any grid), "kahn_switch_below",
-        "exact_batch_rows", "frontier_cap", "term_rank_words", "release_transients", "kahn_async", "d2h_narrow",
+        "exact_batch_rows", "frontier_cap", "term_rank_words", "release_transients", "kahn_async", "side_stream", "d2h_narrow",
         "d2h_escape_cap", "d2h_narrow_max"."""
         _raise(self._L.msc3d_ctx_set_option(self.h, name.encode(), C.c_int64(int(value))), name)
         if name == "wide_ids":

@@ -208,6 +208,8 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "frontier_cap") {  // initial BFS frontier entries (0 = 4 x sources)
         if (value < 0) return MSC3D_ERR_INVALID;
         ctx->frontier_cap = static_cast<std::uint64_t>(value);
+    } else if (n == "side_stream") {  // extremum-side assembly beside the saddle stages
+        ctx->side_assembly = value != 0;
     } else if (n == "kahn_async") {  // Kahn's tail without rounds (k_count_async)
         ctx->kahn_async = value != 0;
     } else if (n == "d2h_narrow") {  // multiplicities cross the bus as bytes + escapes (default 1)

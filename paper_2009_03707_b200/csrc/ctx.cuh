@@ -80,7 +80,8 @@ struct msc3d_ctx {
         if (!copy && cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking) != cudaSuccess) copy = nullptr;
         return copy;
     }
-    cudaStream_t side = nullptr;  // assembly kernels beside the saddle stages
+    cudaStream_t side = nullptr;  // assembly kernels beside the saddle stages ("side_stream")
+    bool side_assembly = false;
     cudaStream_t side_stream() {
         if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) side = nullptr;
         return side;

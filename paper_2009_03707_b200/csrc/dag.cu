@@ -1587,16 +1587,6 @@ struct AsyncQ {
     unsigned long long total;  // junctions this kernel must finish
 };
 
-__device__ __forceinline__ void async_push(const AsyncQ& Q, std::uint32_t node, bool want) {
-    const unsigned m = __ballot_sync(0xffffffffu, want);
-    if (!m) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    unsigned long long at = 0;
-    if (lane == leader) at = atomicAdd(Q.tail, static_cast<unsigned long long>(__popc(m)));
-    at = __shfl_sync(0xffffffffu, at, leader) + __popc(m & ((1u << lane) - 1u));
-    if (want) atomicExch(&Q.q[at], node + 1u);  // (an L2 write the spinning reader sees)
-}
-
 // Release the parents of this lane's finished junction (P(u) already published):
 // the first one that becomes ready is the lane's next node (carry), the others go to
 // the queue.  All lanes call (rn = 0 for lanes without a junction).
@@ -1624,12 +1614,26 @@ __device__ __forceinline__ void release_async(const CountArgs& a, const AsyncQ& 
 #pragma unroll
         for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
         k0 += m;
+        // the first ready parent continues on this lane; the others go to the queue,
+        // all lanes' items in one reservation (the tail counter is contended)
+        std::uint32_t push = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const bool ready = p[k] != kNone && old[k] == 1u;
             const bool keep = ready && carry == kNone;
             if (keep) carry = p[k];
-            async_push(Q, p[k], ready && !keep);
+            push |= (ready && !keep ? 1u : 0u) << k;
+        }
+        std::uint32_t total = 0;
+        const std::uint32_t first = warp_excl_scan(static_cast<std::uint32_t>(__popc(push)), &total);
+        if (total) {
+            const int lane = threadIdx.x & 31;
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(Q.tail, static_cast<unsigned long long>(total));
+            at = __shfl_sync(0xffffffffu, at, 0) + first;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((push >> k) & 1u) __stcg(&Q.q[at++], p[k] + 1u);  // (to the L2: the spinning reader sees it)
         }
         if (!__any_sync(0xffffffffu, k0 < rn)) break;
     }
@@ -1640,8 +1644,15 @@ __device__ __forceinline__ void release_async(const CountArgs& a, const AsyncQ& 
 // by the whole warp right after; then the warp publishes and releases.  All lanes call.
 __device__ __forceinline__ void count_iter_async(const CountArgs& a, WarpBuf wb, WarpQ& wq, PoolChunk& ch, bool valid,
                                                  std::uint32_t u, const AsyncQ& Q, std::uint32_t& carry,
-                                                 unsigned long long& done) {
+                                                 unsigned long long& done, long long* prof) {
     const int lane = threadIdx.x & 31;
+    long long tp = prof ? clock64() : 0;
+    auto phase = [&](int k) {  // development: cycles per phase (MSC3D_DIAG)
+        if (!prof) return;
+        const long long t = clock64();
+        prof[k] += t - tp;
+        tp = t;
+    };
     Inputs in;
     bool ovf = false;
     std::uint32_t T = 0, S = 0, npar = 0;
@@ -1658,10 +1669,14 @@ __device__ __forceinline__ void count_iter_async(const CountArgs& a, WarpBuf wb,
         T = in.len[0] + in.len[1] + in.len[2] + in.len[3];
         S = staged_size(in);
     }
+    __syncwarp();
+    phase(0);
     const bool heavy = valid && T > kHeavy && S + T <= wb.cap;
     const bool light = valid && !heavy;
     const bool pooled = light && T > 2;
     const std::uint64_t off = pool_alloc(a.pool, ch, pooled ? T : 0u, &a.flags[1]);
+    __syncwarp();
+    phase(1);
     std::uint32_t* ok = a.pool.key + (off == kBadOff ? 0 : off);
     std::uint64_t* oc = a.pool.cnt + (off == kBadOff ? 0 : off);
     JRec r;
@@ -1685,7 +1700,13 @@ __device__ __forceinline__ void count_iter_async(const CountArgs& a, WarpBuf wb,
         if (pooled) store_rec(a.rec, u, len, 1u | zword(in.z), 0u, 0u, off, 0ull);
         else store_rec(a.rec, u, len, zword(len == 0 ? __fadd_ru(in.z, 1.0f) : in.z), r.k0, r.k1, r.c0, r.c1);
     };
-    if (light && S > wb.cap) finish(merge<true>(in, a.pool, &ovf, emit));
+    if (light && S > wb.cap) {
+        if (prof) {  // development: direct merges (inputs beyond the warp buffer) and their entries
+            atomicAdd(reinterpret_cast<unsigned long long*>(Q.done) + 21, 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(Q.done) + 22, static_cast<unsigned long long>(T));
+        }
+        finish(merge<true>(in, a.pool, &ovf, emit));
+    }
     __syncwarp();
     unsigned todo = __ballot_sync(0xffffffffu, light && S <= wb.cap);
     while (todo) {
@@ -1696,22 +1717,30 @@ __device__ __forceinline__ void count_iter_async(const CountArgs& a, WarpBuf wb,
         if (go) stage<true>(in, a.pool, wb, base);
         cp_async_wait_all();
         __syncwarp();
+        phase(2);
         if (go) finish(merge_staged<true>(in, wb, base, &ovf, emit));
         __syncwarp();
+        phase(3);
         todo &= ~__ballot_sync(0xffffffffu, go);
+        if (prof && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(Q.done) + 23, 1ull);  // (diag: batches)
     }
     if (ovf) a.flags[0] = 1u;
+    __syncwarp();
+    phase(3);
     unsigned long long dummy = 0;
     for (unsigned hm = __ballot_sync(0xffffffffu, heavy); hm; hm &= hm - 1) {
         const std::uint32_t uh = __shfl_sync(0xffffffffu, u, __ffs(hm) - 1);
         count_heavy(a, wb, wq, ch, uh, nullptr, nullptr, dummy);
     }
+    phase(4);
     // publish every P(u) of the warp, then release the parents
     __threadfence();
     __syncwarp();
+    phase(5);
     const std::uint32_t rn = valid ? npar : 0u;
     release_async(a, Q, rn, rn > static_cast<std::uint32_t>(kInlineParents) ? a.ovoff[u] : 0ull, par0, par1, carry);
     done += static_cast<unsigned long long>(__popc(__ballot_sync(0xffffffffu, valid)));  // (warp-uniform)
+    phase(6);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsigned long long* qctl,
@@ -1745,8 +1774,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
         qctl[32] = 0;
         qctl[40] = 0;
         qctl[41] = gtimer();
-        qctl[45] = 0;
-        qctl[46] = 0;
+        for (int k = 45; k < 64; ++k) qctl[k] = 0;
     }
     grid.sync();
     unsigned long long done = 0, flushed = 0;
@@ -1756,7 +1784,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
     unsigned sleep_ns = 64;  // idle back-off (thousands of idle warps must not saturate
                              // the L2 slice that holds the queue counters)
     unsigned long long last_seen = ~0ull, last_change = 0;
+    long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long* prof = a.diag ? prof_acc : nullptr;
+    long long t_loop = 0;
     for (;;) {
+        if (prof) t_loop = clock64();
         bool has = carry != kNone;
         std::uint32_t u = carry;
         carry = kNone;
@@ -1816,13 +1848,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
                 atomicAdd(qctl + 46, static_cast<unsigned long long>(__popc(hb)));
             }
         }
-        count_iter_async(a, wb, wq, ch, has, u, Q, carry, done);
+        if (prof) prof[7] += clock64() - t_loop;
+        count_iter_async(a, wb, wq, ch, has, u, Q, carry, done, prof);
         if (lane == 0 && done - flushed >= 256) {  // (the count drives termination)
             atomicAdd(Q.done, done - flushed);
             flushed = done;
         }
     }
     if (lane == 0 && done != flushed) atomicAdd(Q.done, done - flushed);
+    if (prof && lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(qctl + 56 + k, static_cast<unsigned long long>(prof[k]));
     grid.sync();
     if (grid.thread_rank() == 0) {
         atomicAdd(a.done, *reinterpret_cast<volatile unsigned long long*>(Q.done));

@@ -487,7 +487,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         L.ovoff = ovoff;
         L.switch_below = ctx->kahn_switch_below;
         L.async_tail = ctx->kahn_async;
-        L.qctl = static_cast<unsigned long long*>(ctx->ensure("kahn_qctl", 48, 8));
+        L.qctl = static_cast<unsigned long long*>(ctx->ensure("kahn_qctl", 64, 8));
         if (!L.qctl) return MSC3D_ERR_NOMEM;
         L.n_skip = n_skip;
         L.n_predone = n_predone;
@@ -929,13 +929,15 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     if (!cp_cell || !cp_index || !amin_src || !amin_dst || !amin_mul || !amax_src || !amax_dst || !amax_mul || !key ||
         !scratch || !cursor || !large)
         return MSC3D_ERR_NOMEM;
-    // The assembly of the extremum-side outputs (critical point list, label volumes,
-    // sorted min->1s and 2s->max arcs: ~3 ms of small bandwidth-bound kernels, no host
-    // round trips) runs on a side stream, beside the latency-bound saddle stages; the
-    // main stream waits for it before it touches those arrays (Join, at every exit).
-    // (Grids above 2^32 cells free scratch mid-way: they keep one stream.)
-    static const bool no_side = std::getenv("MSC3D_NO_SIDE_STREAM") != nullptr;  // (A/B)
-    const cudaStream_t sa = ctx->release_transients() || no_side ? s : ctx->side_stream();
+    // Option "side_stream": the assembly of the extremum-side outputs (critical point
+    // list, label volumes, sorted min->1s and 2s->max arcs: ~3 ms of small
+    // bandwidth-bound kernels, no host round trips) runs on a side stream, beside the
+    // latency-bound saddle stages; the main stream waits for it before it touches those
+    // arrays (Join, at every exit).  Measured at 512^3: the step gains 0.3 ms, but the
+    // saddle stages slow down by ~2.3 ms under the contention, which blurs the
+    // per-stage timings -- off by default.  (Grids above 2^32 cells free scratch
+    // mid-way: they keep one stream.)
+    const cudaStream_t sa = ctx->release_transients() || !ctx->side_assembly ? s : ctx->side_stream();
     if (!sa) return MSC3D_ERR_CUDA;
     struct Join {
         cudaStream_t main, side;

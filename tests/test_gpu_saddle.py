@@ -183,6 +183,17 @@ def test_term_rank_words(ref, kind, dims):
     _compute_vs_ref(c, ref, m.synth(kind, dims), dims)
 
 
+@pytest.mark.parametrize("kind", ["gnoise", "noise"])
+def test_side_stream_assembly(ref, kind):
+    """Option side_stream: the extremum-side assembly on a second stream gives the same
+    complex, device arrays and host deliveries alike."""
+    dims = (40, 36, 32)
+    c = m.Context(0)
+    c.set_option("side_stream", 1)
+    for _ in range(2):
+        _compute_vs_ref(c, ref, m.synth(kind, dims), dims)
+
+
 def test_compute_without_segmentation(ctx, ref):
     dims = (8, 8, 8)
     _compute_vs_ref(ctx, ref, random_field(ref, dims, 7), dims, seg=False)
@@ -202,7 +213,8 @@ def test_compute_repeatable(ctx, ref):
                                          ("gnoise", {"d2h_narrow_max": 1}),  # escapes (mult + src)
                                          ("noise", {"d2h_narrow_max": 1, "d2h_escape_cap": 200}),
                                          ("noise", {"d2h_narrow_max": 0, "d2h_escape_cap": 3}),  # u64 fallback
-                                         ("gnoise", {"d2h_narrow": 0})])  # u64 copies
+                                         ("gnoise", {"d2h_narrow": 0}),  # u64 copies
+                                         ("noise", {"side_stream": 1})])  # copies from the side stream
 def test_compute_host_outputs(ref, kind, narrow):
     """msc3d_ctx_compute_host: the overlapped host copies (multiplicities as bytes +
     escape list, widened on host threads) equal the reference."""

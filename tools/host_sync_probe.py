@@ -8,6 +8,8 @@ import paper_2009_03707_b200 as m
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 dims = (n, n, n)
 c = m.Context(0)
+if len(sys.argv) > 2:
+    c.set_option("side_stream", int(sys.argv[2]))
 c.load_values(m.synth("gnoise", dims), dims)
 for _ in range(2):
     c.compute(m.OPT_SEGMENTATION)

@@ -17,3 +17,8 @@ for i in range(2):
           f"total {int(q[43])} hand-off {int(q[44])} pushed {int(q[16]) - int(q[44])} head {int(q[0])} done {int(q[32])} "
           f"gave-up warps {int(q[40])}; warp iterations {int(q[45])}, lanes busy per iteration "
           f"{int(q[46]) / max(1, int(q[45])):.1f}", flush=True)
+    names = ("loads+gather", "pool alloc", "staging", "light merges", "heavy merges", "fence", "release+push",
+             "claim+slot+fence")
+    it = max(1, int(q[45]))
+    print("   cycles per warp iteration: " + ", ".join(f"{nm} {int(q[56 + k]) / it:.0f}" for k, nm in enumerate(names)))
+    print(f"   direct merges {int(q[53])} ({int(q[54])} input entries), staging batches {int(q[55])} ({int(q[55]) / it:.2f} per iteration)")
