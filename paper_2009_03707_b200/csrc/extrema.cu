@@ -398,20 +398,27 @@ int launch_tile_roots(std::uint32_t* p, std::uint64_t gx, std::uint64_t gy, std:
 
 // After the tile pass: every item points at its root or at an exit target, and the
 // exit targets (resolved by the masked global pass) point at their roots.
-__global__ void k_resolve_exits(std::uint32_t* __restrict__ p0, std::uint64_t n0, std::uint32_t* __restrict__ p3,
-                                std::uint64_t n3) {
-    GRID_STRIDE(k, n0 + n3) {
-        std::uint32_t* p = k < n0 ? p0 : p3;
-        const std::uint64_t i = k < n0 ? k : k - n0;
-        p[i] = p[p[i]];
+// Four items per thread: one 16-byte load of their pointers, the four gathers in flight
+// together, a 16-byte store only when something changed (items whose box root is a
+// real root are final already).  Arrays are 16-byte aligned; the < 4 tail items of
+// each array go one by one.
+__global__ void k_resolve_exits(std::uint32_t* __restrict__ p, std::uint64_t n) {
+    const std::uint64_t n4 = n / 4;
+    uint4* p4 = reinterpret_cast<uint4*>(p);
+    GRID_STRIDE(k, n4) {
+        const uint4 v = p4[k];
+        const uint4 r = make_uint4(p[v.x], p[v.y], p[v.z], p[v.w]);
+        if (r.x != v.x || r.y != v.y || r.z != v.z || r.w != v.w) p4[k] = r;
     }
+    const std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    if (t < n - 4 * n4) p[4 * n4 + t] = p[p[4 * n4 + t]];
 }
 
 int launch_resolve_exits(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, cudaStream_t s,
                          int num_sms) {
-    if (n0 + n3 == 0) return MSC3D_OK;
-    k_resolve_exits<<<grid_for(n0 + n3, num_sms), kThreads, 0, s>>>(p0, n0, p3, n3);
-    count_launch();
+    if (n0) k_resolve_exits<<<grid_for((n0 + 3) / 4, num_sms), kThreads, 0, s>>>(p0, n0);
+    if (n3) k_resolve_exits<<<grid_for((n3 + 3) / 4, num_sms), kThreads, 0, s>>>(p3, n3);
+    count_launch(2);
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;
 }
