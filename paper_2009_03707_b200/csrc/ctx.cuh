@@ -143,6 +143,38 @@ struct msc3d_ctx {
             if (kv.second.cap > (std::size_t(1) << 28))
                 std::fprintf(stderr, "  %-20s %8.2f GB\n", kv.first.c_str(), kv.second.cap / 1e9);
     }
+    // ensure() that keeps the first `keep` bytes when it has to grow (a new buffer, the
+    // bytes copied on `s`, the old one freed after the device is idle -- rare: capacities
+    // persist across calls).
+    void* ensure_keep(const std::string& name, std::uint64_t count, int elem, std::size_t keep, cudaStream_t s) {
+        DevArray& a = arrays[name];
+        const std::size_t bytes = static_cast<std::size_t>(count) * elem;
+        if (a.ptr && a.cap >= bytes) {
+            a.count = count;
+            a.elem = elem;
+            return a.ptr;
+        }
+        void* fresh = nullptr;
+        if (cudaMalloc(&fresh, bytes ? bytes : 16) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        if (a.ptr && keep) {
+            if (cudaMemcpyAsync(fresh, a.ptr, std::min(keep, a.cap), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+                cudaDeviceSynchronize() != cudaSuccess)
+                return nullptr;
+        } else if (a.ptr) {
+            cudaDeviceSynchronize();
+        }
+        if (a.ptr) cudaFree(a.ptr);
+        a.ptr = fresh;
+        a.cap = bytes ? bytes : 16;
+        a.count = count;
+        a.elem = elem;
+        const std::size_t held = held_bytes();
+        if (held > peak_held) peak_held = held;
+        return a.ptr;
+    }
     DevArray* find(const std::string& name) {
         auto it = arrays.find(name);
         return it == arrays.end() ? nullptr : &it->second;

@@ -916,9 +916,23 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
     ctx->scalars["arcs_max"] = static_cast<std::int64_t>(nc);
     void* cp_cell = ctx->ensure("cp_cell", ncp, w);
     auto* cp_index = static_cast<std::uint8_t*>(ctx->ensure("cp_index", ncp, 1));
-    auto* amin_src = static_cast<std::uint32_t*>(ctx->ensure("arcA_src", na, 4));
-    auto* amin_dst = static_cast<std::uint32_t*>(ctx->ensure("arcA_dst", na, 4));
-    auto* amin_mul = static_cast<std::uint64_t*>(ctx->ensure("arcA_mult", na, 8));
+    // A whole compute() writes the min->1s block straight into the final arc arrays (it
+    // leads them), sized by the previous call's 1s->2s count (or 4 per 1-saddle) and
+    // grown keeping it if the count turns out larger; a 1-saddle slice keeps it apart.
+    const bool a_in_place = !(sharded ? src_count > 1
+                                      : (src_first != 0 || src_first > c1 ||
+                                         std::min<std::uint64_t>(src_count, c1 - src_first) != c1));
+    std::uint64_t nb_guess = 4 * c1;
+    if (auto it = ctx->scalars.find("arcs_ss"); it != ctx->scalars.end()) nb_guess = static_cast<std::uint64_t>(it->second);
+    const std::uint64_t a_cap = na + nb_guess + nc;
+    auto* amin_src = static_cast<std::uint32_t*>(a_in_place ? ctx->ensure("arc_src", a_cap, 4) : ctx->ensure("arcA_src", na, 4));
+    auto* amin_dst = static_cast<std::uint32_t*>(a_in_place ? ctx->ensure("arc_dst", a_cap, 4) : ctx->ensure("arcA_dst", na, 4));
+    auto* amin_mul = static_cast<std::uint64_t*>(a_in_place ? ctx->ensure("arc_mult", a_cap, 8) : ctx->ensure("arcA_mult", na, 8));
+    if (a_in_place) {
+        ctx->drop("arcA_src");
+        ctx->drop("arcA_dst");
+        ctx->drop("arcA_mult");
+    }
     auto* amax_src = static_cast<std::uint32_t*>(ctx->ensure("arcC_src", nc, 4));
     auto* amax_dst = static_cast<std::uint32_t*>(ctx->ensure("arcC_dst", nc, 4));
     auto* amax_mul = static_cast<std::uint64_t*>(ctx->ensure("arcC_mult", nc, 8));
@@ -1037,9 +1051,10 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
             return MSC3D_OK;
         }
         const std::uint64_t total = na + nb + nc;
-        asrc = static_cast<std::uint32_t*>(ctx->ensure("arc_src", total, 4));
-        adst = static_cast<std::uint32_t*>(ctx->ensure("arc_dst", total, 4));
-        amul = static_cast<std::uint64_t*>(ctx->ensure("arc_mult", total, 8));
+        const std::uint64_t keep = a_in_place ? na : 0;  // (the min->1s block already in place)
+        asrc = static_cast<std::uint32_t*>(ctx->ensure_keep("arc_src", total, 4, keep * 4, s));
+        adst = static_cast<std::uint32_t*>(ctx->ensure_keep("arc_dst", total, 4, keep * 4, s));
+        amul = static_cast<std::uint64_t*>(ctx->ensure_keep("arc_mult", total, 8, keep * 8, s));
         if (!asrc || !adst || !amul) return MSC3D_ERR_NOMEM;
         if (host) {  // the 2s->max block's host position is known now: send it before the 1s->2s block
             if (host->arc_cap < total) return MSC3D_ERR_INVALID;
@@ -1090,7 +1105,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
         MSC3D_CUDA_TRY(cudaEventRecord(join.ev, sa));
         MSC3D_CUDA_TRY(cudaStreamWaitEvent(s, join.ev, 0));
     }
-    if (na) {
+    if (na && !a_in_place) {
         MSC3D_CUDA_TRY(cudaMemcpyAsync(asrc, amin_src, na * 4, cudaMemcpyDeviceToDevice, s));
         MSC3D_CUDA_TRY(cudaMemcpyAsync(adst, amin_dst, na * 4, cudaMemcpyDeviceToDevice, s));
         MSC3D_CUDA_TRY(cudaMemcpyAsync(amul, amin_mul, na * 8, cudaMemcpyDeviceToDevice, s));
