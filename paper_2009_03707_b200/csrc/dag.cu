@@ -566,14 +566,25 @@ __global__ void k_term_rank(const IdT* __restrict__ list, std::uint64_t n, uint2
 // rare) go to an overflow list.  (The branch destinations live in their own dense
 // array, the parent count in the counters.)
 constexpr int kInlineParents = 8;
-constexpr std::uint32_t kSkip = 0xffffffffu;  // pending0 of a contracted pass-through junction
+// Pending-children counters are one byte per node (a node has <= 4 junction children):
+// 4x less memory for the release atomics to hit (they decrement a byte inside its
+// 32-bit word: the counter is >= 1 when a child releases it, so no borrow crosses into
+// the neighbouring bytes).
+constexpr std::uint8_t kSkip = 0xffu;  // pending0 of a contracted pass-through junction
 
 struct alignas(16) NodeRec {
     std::uint32_t par[kInlineParents];
 };
 static_assert(sizeof(NodeRec) == 32, "NodeRec is one 32-byte sector");
 
-constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by the walk itself
+constexpr std::uint8_t kDone = 0xfeu;  // pending0 of a node finished by the walk itself
+
+// Decrement node q's pending byte; returns the byte's value before.
+__device__ __forceinline__ std::uint32_t pending_release(std::uint8_t* pending, std::uint32_t q) {
+    const std::uint32_t sh = 8u * (q & 3u);
+    const std::uint32_t old = atomicSub(reinterpret_cast<unsigned int*>(pending) + (q >> 2), 1u << sh);
+    return (old >> sh) & 0xffu;
+}
 
 // Leaves finished during the walk: a node whose branches all end at 2-saddles (or
 // dead ends) has P = its sorted terminal keys with multiplicities.  A junction leaf
@@ -585,7 +596,7 @@ constexpr std::uint32_t kDone = 0xfffffffeu;  // pending0 of a node finished by 
 template <typename IdT>
 __global__ void __launch_bounds__(128)
 k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __restrict__ srcs, std::uint64_t n,
-       uint4* __restrict__ dest, std::uint32_t* __restrict__ pending, unsigned int* __restrict__ flags,
+       uint4* __restrict__ dest, std::uint8_t* __restrict__ pending, unsigned int* __restrict__ flags,
        uint4* __restrict__ rec, std::uint32_t* __restrict__ slen, unsigned int* __restrict__ predone,
        unsigned long long* __restrict__ n_predone,
        std::uint32_t* __restrict__ fwd, unsigned int* __restrict__ ptbits) {
@@ -666,7 +677,7 @@ k_walk(WalkCtx c, Dims d, const std::uint32_t* __restrict__ jlist, const IdT* __
                     pre = true;
                 }
             }
-            pending[i] = pre ? kDone : pend;
+            pending[i] = pre ? kDone : static_cast<std::uint8_t>(pend);
             if (fwd) {  // pass-through: one live branch, ending at a junction (P(j) = P(child))
                 int live = 0;
                 std::uint32_t child = kNone;
@@ -719,7 +730,7 @@ constexpr int kRwPer = 2;
 __global__ void __launch_bounds__(kThreads)
 k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj, std::uint64_t n_nodes,
           const std::uint32_t* __restrict__ fwd, const unsigned int* __restrict__ ptbits,
-          const unsigned int* __restrict__ predone, std::uint32_t* __restrict__ pending,
+          const unsigned int* __restrict__ predone, std::uint8_t* __restrict__ pending,
           std::uint32_t* __restrict__ indeg, uint4* __restrict__ ovq,
           unsigned long long* __restrict__ ovq_n, std::uint64_t ovq_cap,
           unsigned long long* __restrict__ n_skip, std::uint32_t* __restrict__ ready,
@@ -787,7 +798,7 @@ k_rewrite(NodeRec* __restrict__ node, uint4* __restrict__ dest, std::uint64_t nj
         if (skip[k]) pending[id[k]] = kSkip;  // (its record is never read again)
         if (!act[k]) continue;
         if (pending[id[k]] != kDone) {
-            pending[id[k]] = waiting[k];
+            pending[id[k]] = static_cast<std::uint8_t>(waiting[k]);
             is_ready[k] = id[k] < nj && waiting[k] == 0;
         }
         if (moved[k])  // (most records are unchanged)
@@ -1232,8 +1243,8 @@ struct CountArgs {
     const std::uint32_t* ready;  // Kahn's round 0 (from the rewrite)
     const unsigned long long* n_ready;
     const NodeRec* node;         // nj junctions, then n1 sources
-    std::uint32_t* pending;      // live counters (nj + n1)
-    const std::uint32_t* pending0;
+    std::uint8_t* pending;       // live counters (nj + n1), one byte each
+    const std::uint8_t* pending0;
     const std::uint32_t* rsrc;   // parents beyond the inline ones
     JRec* rec;
     PoolRef pool;
@@ -1284,7 +1295,7 @@ __device__ __forceinline__ void release_parents(const CountArgs& a, WarpQ& wq, s
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
+        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? pending_release(a.pending, p[k]) : 0u;
         k0 += m;
         unsigned rel = 0;
 #pragma unroll
@@ -1612,7 +1623,7 @@ __device__ __forceinline__ void release_async(const CountArgs& a, const AsyncQ& 
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? atomicSub(&a.pending[p[k]], 1u) : 0u;
+        for (int k = 0; k < 4; ++k) old[k] = p[k] != kNone ? pending_release(a.pending, p[k]) : 0u;
         k0 += m;
         // the first ready parent continues on this lane; the others go to the queue,
         // all lanes' items in one reservation (the tail counter is contended)
@@ -1882,7 +1893,7 @@ k_count_write(const uint4* __restrict__ sdest, std::uint64_t n1, const JRec* __r
               std::uint32_t* __restrict__ o_two, std::uint64_t* __restrict__ o_cnt,
               std::uint32_t base_one, std::uint32_t base_two, unsigned int* __restrict__ flags,
               std::uint32_t* __restrict__ heavy_q, unsigned long long* __restrict__ heavy_n,
-              const std::uint32_t* __restrict__ spending, std::uint32_t* __restrict__ slen) {
+              const std::uint8_t* __restrict__ spending, std::uint32_t* __restrict__ slen) {
     // Light sources (<= kHeavy input entries): the warp stages its lanes' inputs in
     // shared memory (asynchronous 16-byte copies, all in flight at once) and each lane
     // merges its own from there -- instead of a chain of dependent global loads.
@@ -2094,7 +2105,7 @@ int launch_junction_list(const unsigned int* jbits, std::uint64_t nwords, const 
 
 int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
                 const std::uint32_t* tmap, const void* trank, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
+                std::uint64_t n, void* node, std::uint8_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
                 unsigned int* ptbits, cudaStream_t s, int num_sms) {
     if (n == 0) return MSC3D_OK;
@@ -2132,7 +2143,7 @@ int node_rec_bytes() { return static_cast<int>(sizeof(NodeRec)); }
 
 
 int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, const unsigned int* predone, std::uint8_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms) {
     if (n_nodes == 0) return MSC3D_OK;

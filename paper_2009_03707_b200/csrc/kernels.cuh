@@ -178,8 +178,8 @@ namespace msc3d_dev {
 // dag.cu -- successor table, reachability, junction ranks, branch walks, counting
 struct CountLaunch {
     const void* node;               // node_rec_bytes() per node: nj junctions, then n1 1-saddles
-    std::uint32_t* pending;
-    const std::uint32_t* pending0;
+    std::uint8_t* pending;          // one byte per node
+    const std::uint8_t* pending0;
     const std::uint32_t* rsrc;      // parents beyond the inline ones
     void* rec;                      // count_rec_bytes() per junction
     std::uint32_t* pool_key;
@@ -229,14 +229,14 @@ int launch_term_rank(const void* list, std::uint64_t n, int id_width, std::uint6
                      cudaStream_t s, int num_sms);
 int launch_walk(const std::uint16_t* succ, const Dims& d, const void* jrank,
                 const std::uint32_t* tmap, const void* trank, const std::uint32_t* jlist, const void* srcs, int id_width,
-                std::uint64_t n, void* node, std::uint32_t* pending, unsigned int* flags, void* rec,
+                std::uint64_t n, void* node, std::uint8_t* pending, unsigned int* flags, void* rec,
                 std::uint32_t* slen, unsigned int* predone, unsigned long long* n_predone, std::uint32_t* fwd,
                 unsigned int* ptbits, cudaStream_t s,
                 int num_sms);
 int node_rec_bytes();
 
 int launch_rewrite(void* node, void* dest, std::uint64_t nj, std::uint64_t n_nodes, const std::uint32_t* fwd,
-                   const unsigned int* ptbits, const unsigned int* predone, std::uint32_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
+                   const unsigned int* ptbits, const unsigned int* predone, std::uint8_t* pending, std::uint32_t* indeg, void* ovq, unsigned long long* ovq_n,
                    std::uint64_t ovq_cap, unsigned long long* n_skip, std::uint32_t* ready,
                    unsigned long long* n_ready, cudaStream_t s, int num_sms);
 int launch_parent_overflow(const std::uint32_t* indeg, std::uint64_t nj, std::uint64_t* ovoff,

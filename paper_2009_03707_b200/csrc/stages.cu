@@ -371,8 +371,8 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* jlist = static_cast<std::uint32_t*>(ctx->ensure("jlist", nj, 4));
     void* node = ctx->ensure("jnode", nn, msc3d_dev::node_rec_bytes());
     auto* jdest = static_cast<char*>(ctx->ensure("jdest", std::max<std::uint64_t>(nn, 1), 16));  // branch destinations
-    auto* pending = static_cast<std::uint32_t*>(ctx->ensure("pending", nn, 4));
-    auto* pending0 = static_cast<std::uint32_t*>(ctx->ensure("pending0", nn, 4));
+    auto* pending = static_cast<std::uint8_t*>(ctx->ensure("pending", nn + 4, 1));  // (+4: word-wide atomics)
+    auto* pending0 = static_cast<std::uint8_t*>(ctx->ensure("pending0", nn + 4, 1));
     auto* indeg = static_cast<std::uint32_t*>(ctx->ensure("indeg", nj, 4));
     auto* fwd = static_cast<std::uint32_t*>(ctx->ensure("jfwd", nj, 4));
     auto* ovoff = static_cast<std::uint64_t*>(ctx->ensure("ovoff", nj, 8));
@@ -444,7 +444,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
     auto* rsrc = static_cast<std::uint32_t*>(ctx->ensure("rsrc", std::max<std::uint64_t>(nov, 1), 4));
     if (!rsrc) return MSC3D_ERR_NOMEM;
     TRY(msc3d_dev::launch_fill_parents(node, nj, indeg, ovoff, ovq, nq, rsrc, s, sms));
-    if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nn * 4, cudaMemcpyDeviceToDevice, s));
+    if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending0, pending, nn, cudaMemcpyDeviceToDevice, s));
 
     // count vectors, "last child continues"; grow the pool and rerun if it ran out
     const std::uint64_t m = static_cast<std::uint64_t>(ctx->scalars["dag_nodes"]);
@@ -504,7 +504,7 @@ int dag_count(msc3d_ctx* ctx, const void* src_ids, std::uint64_t n1, const std::
         MSC3D_CUDA_TRY(cudaMemsetAsync(flags + 3, 0, 4, s));  // dead-junction "maybe"
         MSC3D_CUDA_TRY(cudaMemsetAsync(ptop, 0, arenas * 8, s));
         MSC3D_CUDA_TRY(cudaMemsetAsync(ctx->d_small + 55, 0, 5 * 8, s));
-        if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nn * 4, cudaMemcpyDeviceToDevice, s));
+        if (nn) MSC3D_CUDA_TRY(cudaMemcpyAsync(pending, pending0, nn, cudaMemcpyDeviceToDevice, s));
         TRY(msc3d_dev::launch_count(L, s, sms));
         MSC3D_CUDA_TRY(cudaMemcpyAsync(ctx->d_small + 58, kstats, 8, cudaMemcpyDeviceToDevice, s));
         TRY(ctx->fetch_small(60));
