@@ -1819,8 +1819,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
                 }
             }
         }
-        if (!has && slot != ~0ull) {  // a filled slot (checked once per iteration)
-            const std::uint32_t v = __ldcg(&Q.q[slot]);
+        if (!has && slot != ~0ull) {  // a filled slot (checked once per iteration; a volatile load:
+                                      // another SM writes it meanwhile, the compiler must not keep it)
+            const std::uint32_t v = *reinterpret_cast<volatile const std::uint32_t*>(&Q.q[slot]);
             if (v) {
                 u = v - 1u;
                 has = true;
