@@ -1588,7 +1588,8 @@ __global__ void __launch_bounds__(kThreads, kWide ? 3 : 2) k_count(CountArgs a) 
 // zeroed at start); an idle lane claims the next slot by atomicAdd on the head and
 // takes it once it is filled, while its warp goes on with the other lanes' work.
 // It ends when every remaining junction is done; if none is left to take while some are
-// still pending for 50 ms (a cycle: the host's count check reports it), warps give up.
+// still pending for 250 ms (a cycle: the host's count check reports it), warps give up
+// (generous: a warp merging one huge vector must not look like a stall).
 // Idle warps back off exponentially (64 ns .. 8 us) between polls of the counters.
 struct AsyncQ {
     std::uint32_t* q;
@@ -1842,7 +1843,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_count_async(CountArgs a, unsign
             if (d != last_seen) {
                 last_seen = d;
                 last_change = now;
-            } else if (now - last_change > 50000000ull) {  // 50 ms without progress: a cycle
+            } else if (now - last_change > 250000000ull) {  // 250 ms without progress: a cycle
                 if (lane == 0) atomicAdd(qctl + 40, 1ull);  // (diagnostic: warps that gave up)
                 break;
             }
