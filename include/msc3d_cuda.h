@@ -234,6 +234,10 @@ typedef struct msc3d_host_outputs {
     uint64_t n_arcs; /* out */
 } msc3d_host_outputs;
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out);
+/* The device outputs of the last computation (msc3d_ctx_compute, or the full context of a
+ * multi-GPU step) delivered to host buffers the way msc3d_ctx_compute_host delivers them
+ * (narrow multiplicities / sources decoded on host threads).  Not in the reference. */
+int msc3d_ctx_deliver_host(msc3d_ctx* ctx, msc3d_host_outputs* out);
 /* Host samples in, host results out: msc3d_ctx_load_values + msc3d_ctx_compute_host in
  * one call, with the upload overlapped too -- the samples go up in z-chunks and the
  * gradient's tile layers start as soon as the planes they read have arrived.  Same

@@ -101,6 +101,7 @@ def lib():
         "msc3d_ctx_count_minor": (i32, [vp, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp, i32]),
         "msc3d_ctx_compute": (i32, [vp, i32, C.POINTER(C.c_double)]),
         "msc3d_ctx_compute_host": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
+        "msc3d_ctx_deliver_host": (i32, [vp, C.POINTER(HostOutputs)]),
         "msc3d_ctx_bind_codes": (i32, [vp, Dims, vp]),
         "msc3d_ctx_compute_host_values": (i32, [vp, Dims, i32, vp, i32, C.POINTER(C.c_double), C.POINTER(HostOutputs)]),
         "msc3d_ctx_compute_codes": (i32, [vp, i32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),

@@ -502,6 +502,11 @@ int msc3d_ctx_compute_host_values(msc3d_ctx* ctx, msc3d_dims dims, int value_typ
     return msc3d_stage::compute_streamed(ctx, host_values, value_type, options, stage_ms, out);
 }
 
+int msc3d_ctx_deliver_host(msc3d_ctx* ctx, msc3d_host_outputs* out) {
+    if (!ctx || !out) return MSC3D_ERR_INVALID;
+    return msc3d_stage::deliver_host(ctx, out);
+}
+
 int msc3d_ctx_compute_host(msc3d_ctx* ctx, int options, double* stage_ms, msc3d_host_outputs* out) {
     if (!ctx || !out) return MSC3D_ERR_INVALID;
     if (!ctx->values) return MSC3D_ERR_STATE;

@@ -1246,6 +1246,32 @@ int validate(msc3d_ctx* ctx) {
     return (r[0] || r[1]) ? MSC3D_ERR_RUNTIME : MSC3D_OK;
 }
 
+// The outputs of the last computation (device arrays of the context) delivered to host
+// buffers the way compute_host does: multiplicities and sorted sources narrow, decoded
+// by host threads, the rest copied.  For results computed device-resident (e.g. by the
+// multi-GPU step) that are wanted on the host afterwards.
+int deliver_host(msc3d_ctx* ctx, const msc3d_host_outputs* host) {
+    for (const char* nm : {"cp_cell", "cp_index", "arc_src", "arc_dst", "arc_mult"})
+        if (!ctx->find(nm)) return MSC3D_ERR_STATE;
+    const std::uint64_t ncp = ctx->count("cp_index"), na = ctx->count("arc_src");
+    const int w = ctx->id_width();
+    if (host->cp_cell_cap < ncp * w || host->cp_index_cap < ncp || host->arc_cap < na) return MSC3D_ERR_INVALID;
+    Sink sink{ctx, host};
+    TRY(sink.copy(host->cp_cell, ctx->ptr<void>("cp_cell"), ncp * w));
+    TRY(sink.copy(host->cp_index, ctx->ptr<void>("cp_index"), ncp));
+    if (host->labels_min && ctx->find("labels_min") && ctx->count("labels_min"))
+        TRY(sink.copy(host->labels_min, ctx->ptr<void>("labels_min"), ctx->count("labels_min") * 4));
+    if (host->labels_max && ctx->find("labels_max") && ctx->count("labels_max"))
+        TRY(sink.copy(host->labels_max, ctx->ptr<void>("labels_max"), ctx->count("labels_max") * 4));
+    TRY(sink.copy_mult(host->arc_mult, ctx->ptr<std::uint64_t>("arc_mult"), na, "X"));
+    TRY(sink.copy_src(host->arc_src, ctx->ptr<std::uint32_t>("arc_src"), na, "X"));
+    TRY(sink.copy(host->arc_dst, ctx->ptr<void>("arc_dst"), na * 4));
+    auto* h = const_cast<msc3d_host_outputs*>(host);
+    h->n_cp = ncp;
+    h->n_arcs = na;
+    return sink.finish();
+}
+
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host) {
     // [gradient] codes + both extremum forests in one kernel
     cudaEvent_t t0 = nullptr;

@@ -20,6 +20,7 @@ int count_minor(msc3d_ctx* ctx, const void* ones, std::uint64_t n1, const void* 
                 const std::uint32_t* const* src, const std::uint32_t* const* dst,
                 const std::uint64_t* const* mult, const std::uint64_t* count, int id_width);
 int compute(msc3d_ctx* ctx, int options, double* stage_ms, const msc3d_host_outputs* host = nullptr);
+int deliver_host(msc3d_ctx* ctx, const msc3d_host_outputs* host);
 int compute_streamed(msc3d_ctx* ctx, const void* host_values, int value_type, int options, double* stage_ms,
                      const msc3d_host_outputs* host);
 // validate_gradient on the device (MSC3D_OPT_VALIDATE; audit.cu)

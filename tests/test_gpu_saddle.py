@@ -256,6 +256,32 @@ def test_compute_host_outputs(ref, kind, narrow):
     assert ctx._L.msc3d_ctx_compute_host(ctx.h, m.OPT_SEGMENTATION, None, C.byref(ho)) == m.ERR_INVALID
 
 
+def test_deliver_host(ref):
+    """msc3d_ctx_deliver_host: a device-resident compute's outputs delivered to host
+    buffers afterwards (the narrow path) equal the reference."""
+    import ctypes as C
+    ctx = m.Context(0)
+    dims = (36, 34, 30)
+    v = m.synth("gnoise", dims)
+    want = ref.compute(v.astype(np.float64), dims, with_segmentation=True)
+    ncp, na = len(want["cp_cell"]), len(want["arc_src"])
+    V, Cu = dims[0] * dims[1] * dims[2], (dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1)
+    buf = {"cp_cell": np.zeros(ncp, np.uint32), "cp_index": np.zeros(ncp, np.uint8),
+           "arc_src": np.zeros(na, np.uint32), "arc_dst": np.zeros(na, np.uint32),
+           "arc_mult": np.zeros(na, np.uint64), "labels_min": np.zeros(V, np.uint32),
+           "labels_max": np.zeros(Cu, np.uint32)}
+    ptr = {k: a.ctypes.data for k, a in buf.items()}
+    ho = m.HostOutputs(ptr["cp_cell"], ncp * 4, ptr["cp_index"], ncp, ptr["arc_src"], ptr["arc_dst"],
+                       ptr["arc_mult"], na, ptr["labels_min"], ptr["labels_max"], 0, 0)
+    assert ctx._L.msc3d_ctx_deliver_host(ctx.h, C.byref(ho)) == m.ERR_STATE  # nothing computed yet
+    ctx.load_values(v, dims)
+    ctx.compute(m.OPT_SEGMENTATION)
+    assert ctx._L.msc3d_ctx_deliver_host(ctx.h, C.byref(ho)) == 0
+    assert ho.n_cp == ncp and ho.n_arcs == na
+    for k in ("cp_cell", "arc_src", "arc_dst", "arc_mult", "labels_min", "labels_max"):
+        np.testing.assert_array_equal(buf[k], np.asarray(want[k]).astype(buf[k].dtype), err_msg=k)
+
+
 @pytest.mark.parametrize("chunk_kb", ["8", "16", "100000"])
 def test_compute_host_values_streamed(ctx, ref, monkeypatch, chunk_kb):
     """msc3d_ctx_compute_host_values: chunked upload overlapped with the gradient, host
