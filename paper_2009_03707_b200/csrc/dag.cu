@@ -27,10 +27,11 @@
 // Counting (path_matrix.cpp:188-219).  Every junction / 1-saddle branch is walked
 // to its end (k_walk).  Each junction j then needs P(j), the sorted sparse vector
 // of path counts to 2-saddles, P(j) = sum over branches of P(dest): Kahn's
-// algorithm over the junction graph in one cooperative kernel -- round 0 scans
-// every node without pending children in index order (coalesced, no frontier),
-// later rounds take the frontier of nodes whose last child finished in the
-// previous round.  P(j) with <= 2 entries is stored inline in a 32-byte record,
+// algorithm over the junction graph -- a cooperative kernel runs round 0 over the
+// nodes without pending children (in index order, from the rewrite) and the big early
+// rounds over the frontier of nodes whose last child finished in the previous round;
+// an asynchronous kernel finishes the rest without rounds (k_count_async: a node is
+// merged as soon as its last child is).  P(j) with <= 2 entries is stored inline in a 32-byte record,
 // longer ones in a pool (64 arenas, one reservation per warp).  1-saddles are the
 // roots: they only record their merged length; a final pass writes the sorted
 // (1-saddle, 2-saddle, count) output.  Counts are exact u64 with sticky overflow.
