@@ -23,3 +23,13 @@ nd = dst - src
 print("dst - src: |.|<2^15", np.count_nonzero(np.abs(nd) < 2**15), "|.|<2^23", np.count_nonzero(np.abs(nd) < 2**23))
 lm = r.labels_min.astype(np.int64)
 print("labels_min delta==0 along x", np.count_nonzero(np.diff(lm) == 0) / len(lm))
+# signed deltas to the previous entry, whole arrays (candidate i8 / i16 + escapes encodings)
+def dstat(name, x):
+    d = np.diff(x.astype(np.int64))
+    n = max(len(d), 1)
+    print(f"{name}: n {len(x)}  |d|<128 {np.count_nonzero(np.abs(d) < 128) / n:.4f}  "
+          f"|d|<32768 {np.count_nonzero(np.abs(d) < 32768) / n:.4f}  d==0 {np.count_nonzero(d == 0) / n:.4f}")
+dstat("dst (all arcs)", dst)
+ncs = [int(np.count_nonzero(src == src))]
+dstat("labels_min", lm)
+dstat("labels_max", r.labels_max.astype(np.int64))
