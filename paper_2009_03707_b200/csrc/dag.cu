@@ -1211,7 +1211,9 @@ __device__ __forceinline__ std::uint64_t pool_alloc(const PoolRef& pool, PoolChu
     const std::uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
     if (total == 0) return kBadOff;
     __syncwarp();
-    if (total > ch.left) {  // warp-uniform
+    const std::uint32_t left = ch.left;
+    __syncwarp();  // (every lane has read it before lane 0 refills the chunk)
+    if (total > left) {  // warp-uniform
         if (lane == 0) {
             const std::uint32_t take = total > kPoolChunk ? total : kPoolChunk;
             const int arena = static_cast<int>(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % kArenas);

@@ -131,21 +131,33 @@ k_tile_roots(std::uint32_t* __restrict__ p, std::uint32_t gx, std::uint32_t gy, 
         }
     }
     __syncthreads();
-    // 2. pointer doubling inside the box (in place: any ancestor is a valid link);
-    //    until nothing changes (chains in a box are at most kTRn long)
+    // 2. pointer doubling inside the box until nothing changes (chains in a box are at
+    //    most kTRn long): each round reads every link's link, then (after a barrier)
+    //    writes them -- no thread reads a word another one is writing.  (1024 threads:
+    //    kTRn / 1024 items each, kept in registers between the two halves.)
     constexpr int kMaxRounds = 16;  // 2^14 > kTRn: a chain inside the box is resolved by then
+    constexpr int kPer = kTRn / 1024;
     int round = 0;
     for (; round < kMaxRounds; ++round) {
         bool ch = false;
-        for (int t = threadIdx.x; t < kTRn; t += blockDim.x) {
-            const std::uint32_t l = lk[t];
+        std::uint32_t nv[kPer];
+        unsigned upd = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const std::uint32_t l = lk[threadIdx.x + 1024 * k];
+            nv[k] = l;
             if (l & kExit) continue;
             const std::uint32_t l2 = lk[l];
             if (l2 != l) {
-                lk[t] = l2;
-                ch = true;
+                nv[k] = l2;
+                upd |= 1u << k;
             }
         }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if ((upd >> k) & 1u) lk[threadIdx.x + 1024 * k] = nv[k];
+        ch = upd != 0;
         if (!__syncthreads_or(ch)) break;  // (also the round's barrier)
     }
     if (round == kMaxRounds && threadIdx.x == 0) *cycle = 1u;  // a closed path in the box: invalid gradient
@@ -388,7 +400,7 @@ int launch_tile_roots(std::uint32_t* p, std::uint64_t gx, std::uint64_t gy, std:
     if (gx == 0 || gy == 0 || gz == 0) return MSC3D_OK;
     const std::uint64_t tiles = ((gx + kTRx - 1) / kTRx) * ((gy + kTRy - 1) / kTRy) * ((gz + kTRz - 1) / kTRz);
     if (tiles > 0x7fffffffull) return MSC3D_ERR_INVALID;
-    k_tile_roots<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(p, static_cast<std::uint32_t>(gx),
+    k_tile_roots<<<static_cast<unsigned>(tiles), 1024 /* kPer */, 0, s>>>(p, static_cast<std::uint32_t>(gx),
                                                                static_cast<std::uint32_t>(gy),
                                                                static_cast<std::uint32_t>(gz), skip, kofs, cycle);
     count_launch();
