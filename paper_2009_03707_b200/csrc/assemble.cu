@@ -32,10 +32,6 @@ __global__ void k_gather_ids(const IdT* __restrict__ list, const std::uint32_t* 
     GRID_STRIDE(i, n) out[i] = list[idx[i]];
 }
 
-__global__ void k_add_base(std::uint32_t* __restrict__ v, std::uint64_t n, std::uint32_t base) {
-    GRID_STRIDE(i, n) v[i] += base;
-}
-
 template <typename IdT>
 __global__ void k_cp_concat(const IdT* __restrict__ src, std::uint64_t n, std::uint64_t at,
                             std::uint8_t index, IdT* __restrict__ cp_cell,
@@ -379,15 +375,6 @@ int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t 
     else
         k_gather_ids<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
             static_cast<const std::uint64_t*>(list), idx, n, static_cast<std::uint64_t*>(out));
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
-
-int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaStream_t s,
-                    int num_sms) {
-    if (n == 0 || base == 0) return MSC3D_OK;
-    k_add_base<<<grid_for(n, num_sms), kThreads, 0, s>>>(v, n, base);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

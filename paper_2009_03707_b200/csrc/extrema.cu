@@ -6,8 +6,10 @@
 //    gets the same parents for free from the gradient kernel).
 //  * k_double: one synchronous pointer-doubling round next[i] = label[label[i]]
 //    (extrema.cpp:79-101) -- bit-exact labels AND round count for find_roots.
-//  * k_jump: asynchronous in-place pointer jumping (same fixpoint, fewer passes)
-//    for the compute() pipeline where the round count is not observable.
+//  * k_tile_roots + k_jump_all + k_resolve_exits: in-place pointer jumping (same
+//    fixpoint, fewer passes) for the compute() pipeline, where the round count is
+//    not observable: box-local doubling on smooth fields, then both forests' global
+//    jumping in one cooperative launch.
 //  * se kernels: per saddle, the roots of its two descending (1-saddle) or
 //    ascending (2-saddle) walks, merged into multiplicity-2 arcs when equal.
 #include <cooperative_groups.h>
@@ -238,38 +240,6 @@ __global__ void k_jump_all(std::uint32_t* __restrict__ p0, std::uint64_t n0, std
     if (grid.thread_rank() == 0) *rounds_out = static_cast<unsigned long long>(round + 1);
 }
 
-__global__ void k_jump(std::uint32_t* __restrict__ p, std::uint64_t n, unsigned int* changed) {
-    bool any = false;
-    GRID_STRIDE(i, n) {
-        std::uint32_t l = p[i];
-        std::uint32_t nl = p[l];
-        if (nl != l) {
-            // Chase a few steps at once: every intermediate is an ancestor, so
-            // writing any of them keeps the forest valid.
-#pragma unroll
-            for (int s = 0; s < 3; ++s) {
-                const std::uint32_t nn = p[nl];
-                if (nn == nl) break;
-                nl = nn;
-            }
-            p[i] = nl;
-            any = true;
-        }
-    }
-    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *changed = 1u;
-}
-
-// remap[dense(crit[k])] = base + k
-template <typename IdT>
-__global__ void k_scatter_remap(const IdT* __restrict__ crit, std::uint64_t n, Dims d, int dim,
-                                std::uint32_t base, std::uint32_t* __restrict__ remap) {
-    GRID_STRIDE(k, n) {
-        const Coord c = unpack(d, crit[k]);
-        const std::uint32_t di = dim == 0 ? vertex_dense(d, c) : cube_dense(d, c);
-        remap[di] = base + static_cast<std::uint32_t>(k);
-    }
-}
-
 // four labels per thread with 16-byte loads and stores (label arrays are 16-byte aligned)
 __global__ void k_gather(const std::uint32_t* __restrict__ label, RankRemap remap, std::uint64_t n,
                          std::uint32_t* __restrict__ out) {
@@ -450,18 +420,6 @@ int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std:
     return MSC3D_OK;
 }
 
-int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, cudaStream_t s,
-                      int num_sms) {
-    // capped grid: every block reports "changed" once, and in-place jumping gains
-    // from later items seeing earlier updates within a pass
-    const unsigned g = static_cast<unsigned>(std::max<std::uint64_t>(
-        1, std::min<std::uint64_t>((n + kThreads - 1) / kThreads, static_cast<std::uint64_t>(num_sms) * 16)));
-    k_jump<<<g, kThreads, 0, s>>>(p, n, changed);
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
-
 int launch_rank_map(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
                     unsigned int* bits, std::uint32_t* cnt, std::uint64_t* pre, void* rank, std::uint64_t nwords,
                     Workspace& ws, std::uint64_t* d_total, cudaStream_t s, int num_sms) {
@@ -481,20 +439,6 @@ int launch_rank_map(const void* crit, std::uint64_t n, int id_width, const Dims&
     int rc = scan_u32(cnt, nwords, pre, d_total, ws, s);
     if (rc != MSC3D_OK) return rc;
     k_pack_rank<<<grid_for(nwords, num_sms), kThreads, 0, s>>>(bits, pre, nwords, static_cast<uint2*>(rank));
-    count_launch();
-    MSC3D_CUDA_TRY(cudaGetLastError());
-    return MSC3D_OK;
-}
-
-int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
-                         std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms) {
-    if (n == 0) return MSC3D_OK;
-    if (id_width == 4)
-        k_scatter_remap<std::uint32_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
-            static_cast<const std::uint32_t*>(crit), n, d, dim, base, remap);
-    else
-        k_scatter_remap<std::uint64_t><<<grid_for(n, num_sms), kThreads, 0, s>>>(
-            static_cast<const std::uint64_t*>(crit), n, d, dim, base, remap);
     count_launch();
     MSC3D_CUDA_TRY(cudaGetLastError());
     return MSC3D_OK;

@@ -85,8 +85,6 @@ int launch_forest(const std::uint8_t* codes, const Dims& d, int dim, std::uint32
                   cudaStream_t s, int num_sms);
 int launch_double_round(const std::uint32_t* in, std::uint32_t* out, std::uint64_t n,
                         unsigned int* changed, cudaStream_t s, int num_sms);
-int launch_jump_round(std::uint32_t* p, std::uint64_t n, unsigned int* changed, cudaStream_t s,
-                      int num_sms);
 // roots of both extremum forests in place, all rounds in one cooperative launch;
 // conv: (n0 + n3 + 31) / 32 words of scratch
 // Tile-local root pre-resolution of a lattice-neighbour forest over a gx*gy*gz grid
@@ -101,8 +99,6 @@ int launch_resolve_exits(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3,
 int launch_jump_all(std::uint32_t* p0, std::uint64_t n0, std::uint32_t* p3, std::uint64_t n3, unsigned int* conv,
                     unsigned int* flags,
                     unsigned long long* rounds, cudaStream_t s, int num_sms, int masked = 0);
-int launch_scatter_remap(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
-                         std::uint32_t base, std::uint32_t* remap, cudaStream_t s, int num_sms);
 // rank: nwords uint2 {rank of the word's first set bit, bits} over dense(crit[k]);
 // bits / cnt / pre: nwords scratch (u32, u32, u64)
 int launch_rank_map(const void* crit, std::uint64_t n, int id_width, const Dims& d, int dim,
@@ -138,8 +134,6 @@ namespace msc3d_dev {
 // assemble.cu
 int launch_gather_ids(const void* list, const std::uint32_t* idx, std::uint64_t n, int id_width,
                       void* out, cudaStream_t s, int num_sms);
-int launch_add_base(std::uint32_t* v, std::uint64_t n, std::uint32_t base, cudaStream_t s,
-                    int num_sms);
 // CriticalPoint::value of every critical cell (max vertex by value, then id), as f64
 int launch_cp_values(const void* cells, int id_width, std::uint64_t n, const Dims& d, const void* values,
                      int value_type, double* out, cudaStream_t s, int num_sms);

@@ -37,27 +37,6 @@ inline unsigned grid_for(std::uint64_t n, int num_sms, int per_sm = 16) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; \
          i < (n); i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
 
-// Visited-edge bitmap of a marked subgraph (bit de <=> marked edge).
-__global__ void k_marked_to_bitmap(const std::uint8_t* __restrict__ marked, Dims d,
-                                   unsigned int* __restrict__ bitmap, std::uint64_t nwords) {
-    GRID_STRIDE(w, nwords) {
-        unsigned int bits = 0;
-        for (int b = 0; b < 32; ++b) {
-            const std::uint64_t de = w * 32 + b;
-            if (de >= 3 * d.n_verts) break;
-            const std::uint64_t v = de / 3;
-            const int a = static_cast<int>(de - 3 * v);
-            const std::uint64_t r = d.fnx.div(v), vx = v - r * d.nx, vz = d.fny.div(r), vy = r - vz * d.ny;
-            if (a == 0 && static_cast<std::int64_t>(vx) == d.nx - 1) continue;
-            if (a == 1 && static_cast<std::int64_t>(vy) == d.ny - 1) continue;
-            if (a == 2 && static_cast<std::int64_t>(vz) == d.nz - 1) continue;
-            const std::uint64_t cell = pack(d, 2 * vx + (a == 0), 2 * vy + (a == 1), 2 * vz + (a == 2));
-            if (marked[cell]) bits |= 1u << b;
-        }
-        bitmap[w] = bits;
-    }
-}
-
 // jlist_de[k] = dense edge of junction cell k; jidx[dense edge] = k
 template <typename IdT>
 __global__ void k_junction_dense(const IdT* __restrict__ cells, std::uint64_t n, Dims d,
