@@ -100,8 +100,10 @@ int msc3d_ctx_download(msc3d_ctx* ctx, const char* name, void* host, uint64_t ca
  *                             buffers of every dense edge);
  *   "term_rank_words" (0/1)   the walks' 2-saddle rank lookup grids above 2^28 vertices
  *                             use (rank words in cell order), on any grid;
- *   "release_transients" (0/1) free each stage's scratch arrays once they are dead, as
- *                             grids above 2^32 cells do, on any grid;
+ *   "release_transients" (-1/0/1) free each stage's scratch arrays once they are dead:
+ *                             1 on any grid, 0 never, -1 (default) above 2^32 cells when
+ *                             the saddle stages may not fit beside them (1 KB per saddle
+ *                             against the free device memory);
  *   "d2h_narrow" (0/1)        host deliveries send multiplicities as one byte per arc
  *                             plus an escape list, widened by host threads (default 1);
  *   "d2h_escape_cap" (>=0)    escape entries per arc block (0 = n/16 + 1024; more

@@ -220,8 +220,9 @@ int msc3d_ctx_set_option(msc3d_ctx* ctx, const char* name, std::int64_t value) {
     } else if (n == "d2h_narrow_max") {  // largest multiplicity sent as a byte (<= 254)
         if (value < 0 || value > 254) return MSC3D_ERR_INVALID;
         ctx->d2h_narrow_max = static_cast<std::uint64_t>(value);
-    } else if (n == "release_transients") {  // free stage scratch early on any grid
-        ctx->force_release = value != 0;
+    } else if (n == "release_transients") {  // 1: free stage scratch early on any grid; 0: never; -1: auto
+        ctx->force_release = value > 0;
+        ctx->never_release = value == 0;
     } else if (n == "term_rank_words") {  // the large-grid 2-saddle rank lookup on any grid
         ctx->term_rank_words = value != 0;
     } else {

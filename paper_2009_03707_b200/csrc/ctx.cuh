@@ -198,7 +198,24 @@ struct msc3d_ctx {
     // Free stage scratch as soon as it is dead: grids above 2^32 cells (configs 4-5),
     // or any grid with the "release_transients" option (tests)
     bool force_release = false;
-    bool release_transients() const { return force_release || dims.n_cells > 0xffffffffull; }
+    bool never_release = false;
+    bool release_auto = false;  // decided per compute() once the saddle counts are known
+    bool release_transients() const { return force_release || (!never_release && release_auto); }
+    // Above 2^32 cells the stage scratch is freed early when the saddle stages may not
+    // fit beside it: their arrays grow with the saddle count (< 1 KB per saddle at every
+    // measured size).  Smooth large grids (config 4: a few thousand saddles) keep
+    // everything -- freeing and re-allocating costs ~19 ms per call there and does not
+    // lower the peak.
+    void decide_release(std::uint64_t saddles) {
+        release_auto = false;
+        if (dims.n_cells <= 0xffffffffull) return;
+        std::size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            release_auto = true;
+            return;
+        }
+        release_auto = saddles * 1024ull > fr;
+    }
     void release(const std::string& name) {
         auto it = arrays.find(name);
         if (it == arrays.end()) return;

@@ -834,6 +834,7 @@ int compute_from_codes(msc3d_ctx* ctx, int options, double* stage_ms, const msc3
                         c3 = ctx->scalars["c3"];
     const std::uint64_t ncp = c0 + c1 + c2 + c3;
     if (ncp >= 0xffffffffull) return MSC3D_ERR_INVALID;  // cp ids are u32 (msc.hpp:25)
+    ctx->decide_release(c1 + c2);
     const std::uint32_t base1 = static_cast<std::uint32_t>(c0), base2 = static_cast<std::uint32_t>(c0 + c1),
                         base3 = static_cast<std::uint32_t>(c0 + c1 + c2);
 
